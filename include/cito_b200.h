@@ -1,0 +1,175 @@
+/*
+ * cito_b200.h — C ABI of the B200-native discretize+linearize path.
+ *
+ * Drop-in boundary for the reference's Python class
+ *   cito.augmentation.Discretizer   (/root/reference/pkg/src/cito/augmentation.py:172-255)
+ * and the value scatter of the multiple-shooting rows of
+ *   cito.scp.build_subproblem      (/root/reference/pkg/src/cito/scp.py:226-236)
+ *   cito.conic.canonicalize        (/root/reference/pkg/src/cito/conic.py:209-269).
+ * The reference has no FFI of its own (pure Python + JAX); these entry points
+ * are what a ctypes binding of that class binds (INTEGRATION.md shows it).
+ *
+ * Conventions: plain pointers + sizes, row-major float64 arrays, int32 CSC
+ * indices, no torch types.  `*_host` entry points take HOST buffers and do
+ * the host<->device copies inside the call; `*_dev` entry points take DEVICE
+ * buffers and a cudaStream_t passed as void*.  Every call returns a
+ * cito_status; cito_last_error() gives a message for the calling thread.
+ * All entry points are reentrant (per-handle mutex around the staging
+ * buffers), so the reference's ThreadPoolExecutor fan-out
+ * (/root/reference/pkg/src/cito/scp.py:101-112) can call them concurrently.
+ */
+#ifndef CITO_B200_H
+#define CITO_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CITO_MAX_LINKS 16
+#define CITO_MAX_JOINTS 16
+#define CITO_MAX_CONTACTS 8
+#define CITO_MAX_PATH 48 /* n_g = n_c + 2*joint_limits + 2*height_bounds */
+#define CITO_MAX_GOUT 48 /* rows of the mixing matrix */
+#define CITO_MAX_EXPR 256
+
+/* surface kinds (cito/multibody.py:107-172) */
+#define CITO_SURFACE_FLAT 0
+#define CITO_SURFACE_IMPLICIT 1
+
+/* postfix byte-code of an implicit surface h(px, pz) (cito/multibody.py:144-172);
+ * the grammar of the reference: constants, +, *, ** (constant exponent), sin, cos */
+#define CITO_OP_CONST 0 /* push arg */
+#define CITO_OP_PX 1
+#define CITO_OP_PZ 2
+#define CITO_OP_ADD 3
+#define CITO_OP_MUL 4
+#define CITO_OP_POW 5 /* a**arg (constant exponent) */
+#define CITO_OP_SIN 6
+#define CITO_OP_COS 7
+#define CITO_OP_NEG 8
+
+typedef enum {
+  CITO_OK = 0,
+  CITO_ERR_ARG = 1,         /* bad argument / unsupported model (ValueError) */
+  CITO_ERR_NONFINITE = 2,   /* non-finite end state (FloatingPointError)       */
+  CITO_ERR_CUDA = 3,        /* CUDA runtime failure                            */
+  CITO_ERR_UNSUPPORTED = 4  /* model topology outside the compiled set         */
+} cito_status;
+
+/*
+ * Packed RobotModel + path-constraint spec + mixing matrix.
+ *   links     cito/multibody.py:53-66     (mass, inertia, com_offset)
+ *   joints    cito/multibody.py:68-89     (parent -1 = world)
+ *   contacts  cito/multibody.py:92-104
+ *   path g    cito/augmentation.py:100-131 (rows: -sd per contact, then
+ *             (rel-hi, lo-rel) per joint limit, then (lo-pz, pz-hi) per height bound)
+ *   mixing    n_g_out x n_g, row-major in mixing[] (cito/ocp.py:121-126); n_g_out = 0
+ *             means the Discretizer was built with mixing=None (no path channels).
+ */
+typedef struct cito_model_desc {
+  int32_t n_links, n_joints, n_contacts, surface_kind;
+  double gravity;
+  double surface_height;
+  double link_mass[CITO_MAX_LINKS];
+  double link_inertia[CITO_MAX_LINKS];
+  double link_com[CITO_MAX_LINKS][2];
+  int32_t joint_parent[CITO_MAX_JOINTS];
+  int32_t joint_child[CITO_MAX_JOINTS];
+  int32_t joint_actuated[CITO_MAX_JOINTS];
+  int32_t joint_spring[CITO_MAX_JOINTS]; /* stiffness != 0 or damping != 0 */
+  double joint_parent_anchor[CITO_MAX_JOINTS][2];
+  double joint_child_anchor[CITO_MAX_JOINTS][2];
+  double joint_stiffness[CITO_MAX_JOINTS];
+  double joint_damping[CITO_MAX_JOINTS];
+  double joint_rest[CITO_MAX_JOINTS];
+  int32_t contact_link[CITO_MAX_CONTACTS];
+  double contact_offset[CITO_MAX_CONTACTS][2];
+  double contact_mu[CITO_MAX_CONTACTS];
+  double contact_restitution[CITO_MAX_CONTACTS];
+  int32_t n_joint_limits;
+  int32_t jl_joint[CITO_MAX_PATH];
+  double jl_lo[CITO_MAX_PATH], jl_hi[CITO_MAX_PATH];
+  int32_t n_height_bounds;
+  int32_t hb_link[CITO_MAX_PATH];
+  double hb_lo[CITO_MAX_PATH], hb_hi[CITO_MAX_PATH];
+  int32_t n_g_out;
+  int32_t expr_len;
+  double mixing[CITO_MAX_GOUT * CITO_MAX_PATH];
+  int32_t expr_op[CITO_MAX_EXPR];
+  double expr_arg[CITO_MAX_EXPR];
+} cito_model_desc;
+
+typedef struct cito_handle cito_handle;
+
+/* sizes derived exactly as cito/augmentation.py:267-269, cito/contact_dynamics.py:35-37 */
+typedef struct cito_dims {
+  int32_t n_q, n_x, n_u, n_y, n_xt, n_j, n_a, n_g, D;
+} cito_dims;
+
+const char* cito_last_error(void);
+const char* cito_version(void);
+
+/* Discretizer.__init__ (cito/augmentation.py:180-216). substeps < 1 -> CITO_ERR_ARG. */
+cito_status cito_create(const cito_model_desc* desc, int32_t substeps, cito_handle** out);
+cito_status cito_destroy(cito_handle* h);
+cito_status cito_get_dims(const cito_handle* h, cito_dims* out);
+
+/* Discretizer.propagate_batch (cito/augmentation.py:226-234):
+ *   xt0s (B, n_xt), Us (B, 2*n_u) = [U-, U+], Ss (B) -> ends (B, n_xt).
+ * bad (B, optional) receives 1 for intervals whose end state is non-finite;
+ * the call then returns CITO_ERR_NONFINITE (the Python layer raises
+ * FloatingPointError listing them). */
+cito_status cito_propagate_host(cito_handle* h, int64_t B, const double* xt0s, const double* Us,
+                                const double* Ss, double* ends, int32_t* bad);
+cito_status cito_propagate_dev(cito_handle* h, int64_t B, const double* xt0s, const double* Us,
+                               const double* Ss, double* ends, int32_t* bad, void* stream);
+
+/* Discretizer.linearize_batch (cito/augmentation.py:236-242):
+ *   -> ends (B, n_xt), jx (B, n_xt, n_xt), ju (B, n_xt, 2*n_u), js (B, n_xt).
+ * Exact forward-mode derivatives of the discrete RKF recursion. */
+cito_status cito_linearize_host(cito_handle* h, int64_t B, const double* xt0s, const double* Us,
+                                const double* Ss, double* ends, double* jx, double* ju, double* js,
+                                int32_t* bad);
+cito_status cito_linearize_dev(cito_handle* h, int64_t B, const double* xt0s, const double* Us,
+                               const double* Ss, double* ends, double* jx, double* ju, double* js,
+                               int32_t* bad, void* stream);
+
+/* Node relations of cito.ocp.Transcription (cito/ocp.py:277-303, 336-365):
+ *   psi  (Np, n_psi) and psi_jac (Np, n_psi, 2 n_y) from y_pairs (Np, 2 n_y)
+ *   theta (Nn, 6 n_c) and theta_jac (Nn, 6 n_c, 3 n_q + 3 n_c) from theta_vecs
+ *   imp  (Nn, n_q)  and imp_jac (Nn, n_q, 3 n_q + 2 n_c) from the first
+ *        3 n_q + 2 n_c entries of theta_vecs.  Device buffers. */
+cito_status cito_node_linearize_dev(cito_handle* h, int64_t Np, int64_t Nn, const double* y_pairs,
+                                    const double* theta_vecs, double delta, double epsilon,
+                                    double* psi, double* psi_jac, double* theta, double* theta_jac,
+                                    double* imp, double* imp_jac, void* stream);
+
+/* Multiple-shooting rows of the SCP subproblem, written straight into CSC value
+ * slots (cito/scp.py:226-236 + cito/conic.py:209-269).  The slot map is built
+ * once per sparsity pattern by the host (paper_2604_09993_b200/scatter.py):
+ *   slot_x (n_int, n_xt, n_xt), slot_u (n_int, n_xt, 2 n_u), slot_s (n_int, n_xt)
+ *   give the position in A_data of -jx[k,r,j]*sigma etc., or -1 where the
+ *   reference pattern has no entry (the value must then be exactly zero).
+ * b_rows (n_int*n_xt) receives b = ends - (jx.z_xp + ju.z_u + js.z_s).
+ * mismatch (device int32, 1 element) counts entries whose value is nonzero
+ * but has no slot (or zero with a slot) -> caller must rebuild the pattern. */
+cito_status cito_scatter_dynamics_dev(cito_handle* h, int64_t n_int, const double* ends,
+                                      const double* jx, const double* ju, const double* js,
+                                      const double* z_ref, const int64_t* xp_off,
+                                      const int64_t* u_off, const int64_t* s_off,
+                                      const double* sig_x, const double* sig_u, double sig_s,
+                                      const int32_t* slot_x, const int32_t* slot_u,
+                                      const int32_t* slot_s, double* A_data, double* b_rows,
+                                      int32_t* mismatch, void* stream);
+
+/* Number of kernel launches issued by this handle since creation (evidence
+ * for bench.py's gpu_launches). */
+int64_t cito_launch_count(const cito_handle* h);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CITO_B200_H */

@@ -1,0 +1,119 @@
+"""ctypes binding of libcito_b200.so (the C ABI of include/cito_b200.h).
+
+There is no CPU fallback: if the library is missing this module raises at
+import, and every compute entry point requires a CUDA device.
+"""
+
+import ctypes
+import os
+import threading
+
+from .model import Dims, ModelDesc
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+SO_PATH = os.path.join(_HERE, "_lib", "libcito_b200.so")
+
+CITO_OK, CITO_ERR_ARG, CITO_ERR_NONFINITE, CITO_ERR_CUDA, CITO_ERR_UNSUPPORTED = range(5)
+
+_dp = ctypes.c_void_p  # device or host double* (raw address)
+_lock = threading.Lock()
+_lib = None
+
+
+class CitoError(RuntimeError):
+    pass
+
+
+class UnsupportedModelError(CitoError, NotImplementedError):
+    pass
+
+
+def _load():
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(SO_PATH):
+            raise ImportError(
+                f"{SO_PATH} not built; run `python -m paper_2604_09993_b200.build` "
+                "(there is no CPU fallback for the discretize/linearize path)")
+        L = ctypes.CDLL(SO_PATH)
+        L.cito_last_error.restype = ctypes.c_char_p
+        L.cito_version.restype = ctypes.c_char_p
+        L.cito_create.restype = ctypes.c_int
+        L.cito_create.argtypes = [ctypes.POINTER(ModelDesc), ctypes.c_int32, ctypes.POINTER(ctypes.c_void_p)]
+        L.cito_destroy.restype = ctypes.c_int
+        L.cito_destroy.argtypes = [ctypes.c_void_p]
+        L.cito_get_dims.restype = ctypes.c_int
+        L.cito_get_dims.argtypes = [ctypes.c_void_p, ctypes.POINTER(Dims)]
+        L.cito_launch_count.restype = ctypes.c_int64
+        L.cito_launch_count.argtypes = [ctypes.c_void_p]
+        L.cito_linearize_host.restype = ctypes.c_int
+        L.cito_linearize_host.argtypes = [ctypes.c_void_p, ctypes.c_int64] + [_dp] * 8
+        L.cito_linearize_dev.restype = ctypes.c_int
+        L.cito_linearize_dev.argtypes = [ctypes.c_void_p, ctypes.c_int64] + [_dp] * 9
+        L.cito_propagate_host.restype = ctypes.c_int
+        L.cito_propagate_host.argtypes = [ctypes.c_void_p, ctypes.c_int64] + [_dp] * 5
+        L.cito_propagate_dev.restype = ctypes.c_int
+        L.cito_propagate_dev.argtypes = [ctypes.c_void_p, ctypes.c_int64] + [_dp] * 6
+        L.cito_node_linearize_dev.restype = ctypes.c_int
+        L.cito_node_linearize_dev.argtypes = ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, _dp, _dp,
+                                               ctypes.c_double, ctypes.c_double] + [_dp] * 7)
+        L.cito_scatter_dynamics_dev.restype = ctypes.c_int
+        L.cito_scatter_dynamics_dev.argtypes = ([ctypes.c_void_p, ctypes.c_int64] + [_dp] * 11 +
+                                                [ctypes.c_double] + [_dp] * 7)
+        _lib = L
+        return L
+
+
+def lib():
+    return _load()
+
+
+def check(status, what=""):
+    if status == CITO_OK:
+        return
+    msg = lib().cito_last_error().decode(errors="replace")
+    if status == CITO_ERR_NONFINITE:
+        raise FloatingPointError(msg)
+    if status == CITO_ERR_ARG:
+        raise ValueError(msg)
+    if status == CITO_ERR_UNSUPPORTED:
+        raise UnsupportedModelError(msg)
+    raise CitoError(f"{what}: {msg}")
+
+
+class Handle:
+    """Owns one cito_handle (per model/mixing/path spec/substeps)."""
+
+    def __init__(self, desc, substeps):
+        self._ptr = ctypes.c_void_p()
+        self.desc = desc
+        check(lib().cito_create(ctypes.byref(desc), int(substeps), ctypes.byref(self._ptr)), "cito_create")
+        d = Dims()
+        check(lib().cito_get_dims(self._ptr, ctypes.byref(d)), "cito_get_dims")
+        self.dims = d
+
+    @property
+    def ptr(self):
+        return self._ptr
+
+    def launch_count(self):
+        return int(lib().cito_launch_count(self._ptr))
+
+    def __del__(self):
+        try:
+            if self._ptr:
+                lib().cito_destroy(self._ptr)
+                self._ptr = ctypes.c_void_p()
+        except Exception:
+            pass
+
+
+def addr(a):
+    """Raw address of a numpy array or torch tensor (None -> NULL)."""
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):
+        return a.data_ptr()
+    return a.ctypes.data

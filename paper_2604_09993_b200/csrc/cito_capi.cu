@@ -1,0 +1,404 @@
+// cito_capi.cu — C ABI (include/cito_b200.h) over the sm_100a kernels.
+//
+// Replaces the jit/vmap plumbing of cito.augmentation.Discretizer
+// (/root/reference/pkg/src/cito/augmentation.py:180-242): a handle caches the
+// per-(model, mixing, path spec, substeps) kernel selection and parameters the
+// way the reference caches its jitted closures.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/cito_b200.h"
+#include "cito_kernels.cuh"
+#include "cito_node.cuh"
+#include "cito_scatter.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+cito_status fail(cito_status st, const std::string& msg) {
+  g_err = msg;
+  return st;
+}
+
+#define CUDA_TRY(expr)                                                                  \
+  do {                                                                                  \
+    cudaError_t e_ = (expr);                                                            \
+    if (e_ != cudaSuccess) return fail(CITO_ERR_CUDA, std::string(#expr ": ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+// RKF tableau (cito/augmentation.py:46-56)
+const double RKF_C[6] = {0.0, 1.0 / 4, 3.0 / 8, 12.0 / 13, 1.0, 1.0 / 2};
+const double RKF_A[6][5] = {{0},
+                            {1.0 / 4},
+                            {3.0 / 32, 9.0 / 32},
+                            {1932.0 / 2197, -7200.0 / 2197, 7296.0 / 2197},
+                            {439.0 / 216, -8.0, 3680.0 / 513, -845.0 / 4104},
+                            {-8.0 / 27, 2.0, -3544.0 / 2565, 1859.0 / 4104, -11.0 / 40}};
+const double RKF_B[6] = {16.0 / 135, 0.0, 6656.0 / 12825, 28561.0 / 56430, -9.0 / 50, 2.0 / 55};
+
+struct TopoOps {
+  const char* key;
+  cito_status (*linearize)(const KParams&, int64_t, const double*, const double*, const double*, double*, double*,
+                           double*, double*, int32_t*, cudaStream_t);
+  cito_status (*propagate)(const KParams&, int64_t, const double*, const double*, const double*, double*, int32_t*,
+                           cudaStream_t);
+  cito_status (*node)(const KParams&, int64_t, int64_t, const double*, const double*, double, double, double*,
+                      double*, double*, double*, double*, double*, cudaStream_t);
+};
+
+template <class M>
+cito_status launch_linearize(const KParams& P, int64_t B, const double* xt0s, const double* Us, const double* Ss,
+                             double* ends, double* jx, double* ju, double* js, int32_t* bad, cudaStream_t st) {
+  if (B <= 0) return CITO_OK;
+  const size_t smem = sizeof(LinShared<M>);
+  static bool attr_done = false;
+  if (!attr_done) {
+    CUDA_TRY(cudaFuncSetAttribute(k_linearize<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_done = true;
+  }
+  k_linearize<M><<<(unsigned)B, Dims<M>::NT, smem, st>>>(P, B, xt0s, Us, Ss, ends, jx, ju, js, bad);
+  CUDA_TRY(cudaGetLastError());
+  return CITO_OK;
+}
+
+template <class M>
+cito_status launch_propagate(const KParams& P, int64_t B, const double* xt0s, const double* Us, const double* Ss,
+                             double* ends, int32_t* bad, cudaStream_t st) {
+  if (B <= 0) return CITO_OK;
+  const int nt = 128;
+  k_propagate<M><<<(unsigned)((B + nt - 1) / nt), nt, 0, st>>>(P, B, xt0s, Us, Ss, ends, bad);
+  CUDA_TRY(cudaGetLastError());
+  return CITO_OK;
+}
+
+template <class M>
+cito_status launch_node(const KParams& P, int64_t Np, int64_t Nn, const double* y_pairs, const double* theta_vecs,
+                        double delta, double eps, double* psi, double* psi_jac, double* th, double* th_jac,
+                        double* imp, double* imp_jac, cudaStream_t st) {
+  constexpr int NQ = 3 * M::NL, NC = M::NC, NY = 5 * NC + M::NGO;
+  const int64_t total = Np * (2 * NY) + Nn * (3 * NQ + 3 * NC) + Nn * (3 * NQ + 2 * NC);
+  if (total <= 0) return CITO_OK;
+  const int nt = 64;
+  k_node<M><<<(unsigned)((total + nt - 1) / nt), nt, 0, st>>>(P, Np, Nn, y_pairs, theta_vecs, delta, eps, psi,
+                                                               psi_jac, th, th_jac, imp, imp_jac);
+  CUDA_TRY(cudaGetLastError());
+  return CITO_OK;
+}
+
+#define CITO_TOPO_ENTRY(T, K) {K, launch_linearize<T>, launch_propagate<T>, launch_node<T>},
+const TopoOps kTopos[] = {CITO_FOR_EACH_TOPOLOGY(CITO_TOPO_ENTRY)};
+#undef CITO_TOPO_ENTRY
+
+std::string topo_key(const cito_model_desc& d) {
+  std::string k = "L" + std::to_string(d.n_links) + "|J";
+  for (int j = 0; j < d.n_joints; ++j) {
+    if (j) k += ",";
+    k += std::to_string(d.joint_parent[j]) + ">" + std::to_string(d.joint_child[j]) +
+         (d.joint_actuated[j] ? "a" : "p");
+  }
+  k += "|C";
+  for (int i = 0; i < d.n_contacts; ++i) {
+    if (i) k += ",";
+    k += std::to_string(d.contact_link[i]);
+  }
+  k += std::string("|S") + (d.surface_kind == CITO_SURFACE_IMPLICIT ? "i" : "f");
+  k += "|G" + std::to_string(d.n_g_out) + "|JL";
+  for (int i = 0; i < d.n_joint_limits; ++i) {
+    if (i) k += ",";
+    k += std::to_string(d.jl_joint[i]);
+  }
+  k += "|HB";
+  for (int i = 0; i < d.n_height_bounds; ++i) {
+    if (i) k += ",";
+    k += std::to_string(d.hb_link[i]);
+  }
+  return k;
+}
+
+}  // namespace
+
+struct cito_handle {
+  cito_model_desc desc;
+  KParams P;
+  cito_dims dims;
+  const TopoOps* ops = nullptr;
+  std::mutex mu;
+  // device staging for the *_host entry points
+  void* dbuf = nullptr;
+  size_t dcap = 0;
+  cudaStream_t stream = nullptr;
+  int64_t launches = 0;
+};
+
+extern "C" {
+
+const char* cito_last_error(void) { return g_err.c_str(); }
+const char* cito_version(void) { return "paper_2604_09993_b200 0.1 (sm_100a fp64)"; }
+
+cito_status cito_create(const cito_model_desc* desc, int32_t substeps, cito_handle** out) {
+  if (!desc || !out) return fail(CITO_ERR_ARG, "null argument");
+  if (substeps < 1) return fail(CITO_ERR_ARG, "substeps must be >= 1");
+  const cito_model_desc& d = *desc;
+  if (d.n_links < 1 || d.n_links > KMAX_L || d.n_joints > KMAX_J || d.n_contacts > KMAX_C)
+    return fail(CITO_ERR_ARG, "model size outside kernel limits");
+  const int n_g = d.n_contacts + 2 * d.n_joint_limits + 2 * d.n_height_bounds;
+  if (d.n_g_out > KMAX_GO || (d.n_g_out > 0 && n_g > KMAX_G))
+    return fail(CITO_ERR_ARG, "too many path-constraint rows for the kernel parameter block");
+  if (d.surface_kind == CITO_SURFACE_IMPLICIT && (d.expr_len < 1 || d.expr_len > KMAX_E))
+    return fail(CITO_ERR_ARG, "implicit surface byte-code missing or too long");
+  const std::string key = topo_key(d);
+  const TopoOps* ops = nullptr;
+  for (const auto& t : kTopos)
+    if (key == t.key) ops = &t;
+  if (!ops) return fail(CITO_ERR_UNSUPPORTED, "model topology not compiled into this library: " + key);
+
+  cito_handle* h = new cito_handle();
+  h->desc = d;
+  h->ops = ops;
+  KParams& P = h->P;
+  memset(&P, 0, sizeof(P));
+  for (int l = 0; l < d.n_links; ++l) {
+    P.minv_m[l] = 1.0 / d.link_mass[l];
+    P.minv_I[l] = 1.0 / d.link_inertia[l];
+    P.neg_mg[l] = -d.link_mass[l] * d.gravity;  // multibody.py:300
+  }
+  for (int j = 0; j < d.n_joints; ++j) {
+    const int p = d.joint_parent[j], c = d.joint_child[j];
+    for (int a = 0; a < 2; ++a) {
+      P.jrp[j][a] = p >= 0 ? d.joint_parent_anchor[j][a] - d.link_com[p][a] : d.joint_parent_anchor[j][a];
+      P.jrc[j][a] = d.joint_child_anchor[j][a] - d.link_com[c][a];
+    }
+    P.jk[j] = d.joint_stiffness[j];
+    P.jd[j] = d.joint_damping[j];
+    P.jrest[j] = d.joint_rest[j];
+    P.jspring[j] = d.joint_spring[j];
+  }
+  for (int i = 0; i < d.n_contacts; ++i) {
+    const int l = d.contact_link[i];
+    for (int a = 0; a < 2; ++a) P.cr[i][a] = d.contact_offset[i][a] - d.link_com[l][a];
+    P.mu[i] = d.contact_mu[i];
+    P.crest[i] = d.contact_restitution[i];
+  }
+  P.height = d.surface_height;
+  for (int k = 0; k < d.n_joint_limits; ++k) {
+    P.jl_lo[k] = d.jl_lo[k];
+    P.jl_hi[k] = d.jl_hi[k];
+  }
+  for (int k = 0; k < d.n_height_bounds; ++k) {
+    P.hb_lo[k] = d.hb_lo[k];
+    P.hb_hi[k] = d.hb_hi[k];
+  }
+  for (int o = 0; o < d.n_g_out; ++o)
+    for (int g = 0; g < n_g; ++g) P.mix[o][g] = d.mixing[o * CITO_MAX_PATH + g];
+  P.expr_len = d.expr_len;
+  for (int k = 0; k < d.expr_len; ++k) {
+    P.expr_op[k] = d.expr_op[k];
+    P.expr_arg[k] = d.expr_arg[k];
+  }
+  // tableau products for h = 1/substeps
+  const double hh = 1.0 / substeps;
+  P.substeps = substeps;
+  P.h = hh;
+  for (int i = 0; i < 6; ++i) {
+    P.ch[i] = RKF_C[i] * hh;
+    P.b[i] = RKF_B[i];
+    double c1 = 0.0;
+    for (int j = 0; j < i; ++j) {
+      P.ha[i][j] = hh * RKF_A[i][j];
+      c1 += RKF_A[i][j];
+    }
+    P.hc1[i] = hh * c1;
+    for (int l = 0; l < i; ++l) {
+      double s = 0.0;
+      for (int j = l + 1; j < i; ++j) s += RKF_A[i][j] * RKF_A[j][l];
+      P.cq[i][l] = hh * hh * s;
+    }
+  }
+  double e1 = 0.0;
+  for (int i = 0; i < 6; ++i) e1 += RKF_B[i];
+  P.he1 = hh * e1;
+  for (int l = 0; l < 6; ++l) {
+    double s = 0.0;
+    for (int i = l + 1; i < 6; ++i) s += RKF_B[i] * RKF_A[i][l];
+    P.e2[l] = hh * hh * s;
+  }
+  // dims (cito/augmentation.py:267-269, cito/contact_dynamics.py:35-37)
+  int na = 0;
+  for (int j = 0; j < d.n_joints; ++j) na += d.joint_actuated[j] ? 1 : 0;
+  cito_dims& D = h->dims;
+  D.n_q = 3 * d.n_links;
+  D.n_x = 2 * D.n_q;
+  D.n_a = na;
+  D.n_u = na + 3 * d.n_contacts;
+  D.n_y = 5 * d.n_contacts + d.n_g_out;
+  D.n_xt = D.n_x + D.n_y;
+  D.n_j = 2 * d.n_joints;
+  D.n_g = n_g;
+  D.D = D.n_xt + 2 * D.n_u + 1;
+  // the private stream of the *_host entry points is created on first use, so a
+  // handle (topology lookup, dims) can be created on a machine without a GPU
+  *out = h;
+  return CITO_OK;
+}
+
+cito_status cito_destroy(cito_handle* h) {
+  if (!h) return CITO_OK;
+  if (h->dbuf) cudaFree(h->dbuf);
+  if (h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+  return CITO_OK;
+}
+
+cito_status cito_get_dims(const cito_handle* h, cito_dims* out) {
+  if (!h || !out) return fail(CITO_ERR_ARG, "null argument");
+  *out = h->dims;
+  return CITO_OK;
+}
+
+int64_t cito_launch_count(const cito_handle* h) { return h ? h->launches : 0; }
+
+cito_status cito_linearize_dev(cito_handle* h, int64_t B, const double* xt0s, const double* Us, const double* Ss,
+                               double* ends, double* jx, double* ju, double* js, int32_t* bad, void* stream) {
+  if (!h) return fail(CITO_ERR_ARG, "null handle");
+  cito_status st = h->ops->linearize(h->P, B, xt0s, Us, Ss, ends, jx, ju, js, bad, (cudaStream_t)stream);
+  if (st == CITO_OK && B > 0) __atomic_add_fetch(&h->launches, 1, __ATOMIC_RELAXED);
+  return st;
+}
+
+cito_status cito_propagate_dev(cito_handle* h, int64_t B, const double* xt0s, const double* Us, const double* Ss,
+                               double* ends, int32_t* bad, void* stream) {
+  if (!h) return fail(CITO_ERR_ARG, "null handle");
+  cito_status st = h->ops->propagate(h->P, B, xt0s, Us, Ss, ends, bad, (cudaStream_t)stream);
+  if (st == CITO_OK && B > 0) __atomic_add_fetch(&h->launches, 1, __ATOMIC_RELAXED);
+  return st;
+}
+
+cito_status cito_node_linearize_dev(cito_handle* h, int64_t Np, int64_t Nn, const double* y_pairs,
+                                    const double* theta_vecs, double delta, double epsilon, double* psi,
+                                    double* psi_jac, double* theta, double* theta_jac, double* imp, double* imp_jac,
+                                    void* stream) {
+  if (!h) return fail(CITO_ERR_ARG, "null handle");
+  cito_status st = h->ops->node(h->P, Np, Nn, y_pairs, theta_vecs, delta, epsilon, psi, psi_jac, theta, theta_jac,
+                                imp, imp_jac, (cudaStream_t)stream);
+  if (st == CITO_OK && Np + Nn > 0) __atomic_add_fetch(&h->launches, 1, __ATOMIC_RELAXED);
+  return st;
+}
+
+static cito_status ensure_dbuf(cito_handle* h, size_t bytes) {
+  if (!h->stream) CUDA_TRY(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  if (bytes <= h->dcap) return CITO_OK;
+  if (h->dbuf) cudaFree(h->dbuf);
+  h->dbuf = nullptr;
+  h->dcap = 0;
+  CUDA_TRY(cudaMalloc(&h->dbuf, bytes));
+  h->dcap = bytes;
+  return CITO_OK;
+}
+
+static size_t al256(size_t n) { return (n + 255) & ~size_t(255); }
+
+static cito_status count_bad(const int32_t* bad, int64_t B) {
+  if (!bad) return CITO_OK;
+  for (int64_t b = 0; b < B; ++b)
+    if (bad[b]) return fail(CITO_ERR_NONFINITE, "non-finite state during interval integration");
+  return CITO_OK;
+}
+
+cito_status cito_linearize_host(cito_handle* h, int64_t B, const double* xt0s, const double* Us, const double* Ss,
+                                double* ends, double* jx, double* ju, double* js, int32_t* bad) {
+  if (!h) return fail(CITO_ERR_ARG, "null handle");
+  if (B <= 0) return CITO_OK;
+  std::lock_guard<std::mutex> lk(h->mu);
+  const cito_dims& D = h->dims;
+  const size_t nin = al256(B * D.n_xt * 8) + al256(B * 2 * D.n_u * 8) + al256(B * 8);
+  const size_t nout = al256(B * D.n_xt * 8) + al256(B * D.n_xt * D.n_xt * 8) +
+                      al256(B * D.n_xt * 2 * D.n_u * 8) + al256(B * D.n_xt * 8) + al256(B * 4);
+  cito_status st = ensure_dbuf(h, nin + nout);
+  if (st != CITO_OK) return st;
+  char* p = (char*)h->dbuf;
+  double* d_x = (double*)p;
+  p += al256(B * D.n_xt * 8);
+  double* d_U = (double*)p;
+  p += al256(B * 2 * D.n_u * 8);
+  double* d_S = (double*)p;
+  p += al256(B * 8);
+  double* d_e = (double*)p;
+  p += al256(B * D.n_xt * 8);
+  double* d_jx = (double*)p;
+  p += al256(B * D.n_xt * D.n_xt * 8);
+  double* d_ju = (double*)p;
+  p += al256(B * D.n_xt * 2 * D.n_u * 8);
+  double* d_js = (double*)p;
+  p += al256(B * D.n_xt * 8);
+  int32_t* d_bad = (int32_t*)p;
+  cudaStream_t s = h->stream;
+  CUDA_TRY(cudaMemcpyAsync(d_x, xt0s, B * D.n_xt * 8, cudaMemcpyHostToDevice, s));
+  if (D.n_u) CUDA_TRY(cudaMemcpyAsync(d_U, Us, B * 2 * D.n_u * 8, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemcpyAsync(d_S, Ss, B * 8, cudaMemcpyHostToDevice, s));
+  st = h->ops->linearize(h->P, B, d_x, d_U, d_S, d_e, d_jx, d_ju, d_js, d_bad, s);
+  if (st != CITO_OK) return st;
+  h->launches++;
+  CUDA_TRY(cudaMemcpyAsync(ends, d_e, B * D.n_xt * 8, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaMemcpyAsync(jx, d_jx, B * D.n_xt * D.n_xt * 8, cudaMemcpyDeviceToHost, s));
+  if (D.n_u) CUDA_TRY(cudaMemcpyAsync(ju, d_ju, B * D.n_xt * 2 * D.n_u * 8, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaMemcpyAsync(js, d_js, B * D.n_xt * 8, cudaMemcpyDeviceToHost, s));
+  int32_t* hb = bad;
+  if (hb) CUDA_TRY(cudaMemcpyAsync(hb, d_bad, B * 4, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return count_bad(hb, B);
+}
+
+cito_status cito_propagate_host(cito_handle* h, int64_t B, const double* xt0s, const double* Us, const double* Ss,
+                                double* ends, int32_t* bad) {
+  if (!h) return fail(CITO_ERR_ARG, "null handle");
+  if (B <= 0) return CITO_OK;
+  std::lock_guard<std::mutex> lk(h->mu);
+  const cito_dims& D = h->dims;
+  const size_t n1 = al256(B * D.n_xt * 8), n2 = al256(B * 2 * D.n_u * 8 + 8), n3 = al256(B * 8);
+  cito_status st = ensure_dbuf(h, 2 * n1 + n2 + n3 + al256(B * 4));
+  if (st != CITO_OK) return st;
+  char* p = (char*)h->dbuf;
+  double* d_x = (double*)p;
+  double* d_U = (double*)(p + n1);
+  double* d_S = (double*)(p + n1 + n2);
+  double* d_e = (double*)(p + n1 + n2 + n3);
+  int32_t* d_bad = (int32_t*)(p + 2 * n1 + n2 + n3);
+  cudaStream_t s = h->stream;
+  CUDA_TRY(cudaMemcpyAsync(d_x, xt0s, B * D.n_xt * 8, cudaMemcpyHostToDevice, s));
+  if (D.n_u) CUDA_TRY(cudaMemcpyAsync(d_U, Us, B * 2 * D.n_u * 8, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemcpyAsync(d_S, Ss, B * 8, cudaMemcpyHostToDevice, s));
+  st = h->ops->propagate(h->P, B, d_x, d_U, d_S, d_e, d_bad, s);
+  if (st != CITO_OK) return st;
+  h->launches++;
+  CUDA_TRY(cudaMemcpyAsync(ends, d_e, B * D.n_xt * 8, cudaMemcpyDeviceToHost, s));
+  if (bad) CUDA_TRY(cudaMemcpyAsync(bad, d_bad, B * 4, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return count_bad(bad, B);
+}
+
+cito_status cito_scatter_dynamics_dev(cito_handle* h, int64_t n_int, const double* ends, const double* jx,
+                                      const double* ju, const double* js, const double* z_ref, const int64_t* xp_off,
+                                      const int64_t* u_off, const int64_t* s_off, const double* sig_x,
+                                      const double* sig_u, double sig_s, const int32_t* slot_x,
+                                      const int32_t* slot_u, const int32_t* slot_s, double* A_data, double* b_rows,
+                                      int32_t* mismatch, void* stream) {
+  if (!h) return fail(CITO_ERR_ARG, "null handle");
+  if (n_int <= 0) return CITO_OK;
+  const cito_dims& D = h->dims;
+  const int nt = 128;
+  const int64_t rows = n_int * D.n_xt;
+  k_scatter_dynamics<<<(unsigned)((rows + nt / 32 - 1) / (nt / 32)), nt, 0, (cudaStream_t)stream>>>(
+      n_int, D.n_xt, D.n_u, ends, jx, ju, js, z_ref, xp_off, u_off, s_off, sig_x, sig_u, sig_s, slot_x, slot_u,
+      slot_s, A_data, b_rows, mismatch);
+  CUDA_TRY(cudaGetLastError());
+  __atomic_add_fetch(&h->launches, 1, __ATOMIC_RELAXED);
+  return CITO_OK;
+}
+
+}  // extern "C"

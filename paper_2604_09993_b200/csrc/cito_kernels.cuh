@@ -1,0 +1,883 @@
+// cito_kernels.cuh — fp64 discretize+linearize kernels for sm_100a.
+//
+// Replaces cito.augmentation.Discretizer.{propagate_batch, linearize_batch}
+// (/root/reference/pkg/src/cito/augmentation.py:180-242): a fixed-step
+// Runge-Kutta-Fehlberg flow (5th-order weights, :46-56, :195-211) of the
+// dilated augmented dynamics S*(f(x,u), Omega(x,u)) (:134-163) and the exact
+// forward-mode derivatives of that discrete recursion w.r.t. (x~+, U, S).
+//
+// Formulation (differs from the reference's dense jacfwd on purpose):
+//  * per RK stage the rate function is evaluated ONCE (primal, incl. the
+//    Cholesky factor of the joint Gram matrix), then its Jacobian is formed
+//    column by column (one thread per structurally relevant input direction)
+//    with hand-derived forward-mode tangents that reuse the primal factor:
+//       dlam = -G^{-1}(dJ vdot + J M^{-1}(dW + dJ^T lam) + dcurv)
+//    (derivative of cito/contact_dynamics.py:86-95);
+//  * the tangent columns of the interval map (one thread per column) are
+//    advanced through the stage recursion with that Jacobian; only the
+//    velocity-row stage increments are stored (q-row stage inputs follow
+//    from q' = S v through precomputed tableau products).
+// The topology (links/joints/contacts/path rows) is a compile-time template
+// parameter (models_gen.cuh); numeric parameters are kernel arguments.
+#pragma once
+
+#include <cstdint>
+
+#include "models_gen.cuh"
+
+#define KMAX_L 16
+#define KMAX_J 16
+#define KMAX_C 8
+#define KMAX_G 16
+#define KMAX_GO 16
+#define KMAX_E 96
+
+// Numeric model parameters + tableau products, passed by value (constant bank).
+struct KParams {
+  double minv_m[KMAX_L], minv_I[KMAX_L], neg_mg[KMAX_L];
+  double jrp[KMAX_J][2], jrc[KMAX_J][2];  // anchor - com (world parent: anchor itself)
+  double jk[KMAX_J], jd[KMAX_J], jrest[KMAX_J];
+  int32_t jspring[KMAX_J];
+  double cr[KMAX_C][2], mu[KMAX_C], crest[KMAX_C];
+  double height;
+  double jl_lo[KMAX_G], jl_hi[KMAX_G], hb_lo[KMAX_G], hb_hi[KMAX_G];
+  double mix[KMAX_GO][KMAX_G];
+  // tableau (h = 1/substeps)
+  int32_t substeps;
+  double h;
+  double ha[6][6];  // h * a_ij (the reference's `h * a` factor)
+  double ch[6];     // c_i * h
+  double b[6];      // b_i
+  double hc1[6];    // h * sum_j a_ij
+  double cq[6][6];  // h^2 * sum_j a_ij a_jl
+  double e2[6];     // h^2 * sum_{i>l} b_i a_il
+  double he1;       // h * sum_i b_i
+  int32_t expr_len;
+  int32_t expr_op[KMAX_E];
+  double expr_arg[KMAX_E];
+};
+
+template <int N>
+struct Pos {
+  static constexpr int v = N > 0 ? N : 1;
+};
+
+// ---------------------------------------------------------------------------
+// implicit surface h(px, pz): value, gradient, Hessian (cito/multibody.py:144-172)
+struct T2 {
+  double v, gx, gz, hxx, hxz, hzz;
+};
+
+__device__ inline T2 surface_t2(const KParams& P, double px, double pz) {
+  T2 st[16];
+  int sp = 0;
+  for (int k = 0; k < P.expr_len; ++k) {
+    const int op = P.expr_op[k];
+    const double arg = P.expr_arg[k];
+    T2 r = {0, 0, 0, 0, 0, 0};
+    if (op == 0) {
+      r.v = arg;
+    } else if (op == 1) {
+      r.v = px;
+      r.gx = 1.0;
+    } else if (op == 2) {
+      r.v = pz;
+      r.gz = 1.0;
+    } else if (op == 3 || op == 4) {
+      T2 bb = st[--sp], a = st[--sp];
+      if (op == 3) {
+        r.v = a.v + bb.v;
+        r.gx = a.gx + bb.gx;
+        r.gz = a.gz + bb.gz;
+        r.hxx = a.hxx + bb.hxx;
+        r.hxz = a.hxz + bb.hxz;
+        r.hzz = a.hzz + bb.hzz;
+      } else {
+        r.v = a.v * bb.v;
+        r.gx = a.gx * bb.v + a.v * bb.gx;
+        r.gz = a.gz * bb.v + a.v * bb.gz;
+        r.hxx = a.hxx * bb.v + 2.0 * a.gx * bb.gx + a.v * bb.hxx;
+        r.hxz = a.hxz * bb.v + a.gx * bb.gz + a.gz * bb.gx + a.v * bb.hxz;
+        r.hzz = a.hzz * bb.v + 2.0 * a.gz * bb.gz + a.v * bb.hzz;
+      }
+    } else {
+      T2 a = st[--sp];
+      double f0, f1, f2;
+      if (op == 5) {
+        f0 = pow(a.v, arg);
+        f1 = arg * pow(a.v, arg - 1.0);
+        f2 = arg * (arg - 1.0) * pow(a.v, arg - 2.0);
+      } else if (op == 6) {
+        sincos(a.v, &f0, &f1);
+        f2 = -f0;
+      } else if (op == 7) {
+        double s;
+        sincos(a.v, &s, &f0);
+        f1 = -s;
+        f2 = -f0;
+      } else {
+        f0 = -a.v;
+        f1 = -1.0;
+        f2 = 0.0;
+      }
+      r.v = f0;
+      r.gx = f1 * a.gx;
+      r.gz = f1 * a.gz;
+      r.hxx = f1 * a.hxx + f2 * a.gx * a.gx;
+      r.hxz = f1 * a.hxz + f2 * a.gx * a.gz;
+      r.hzz = f1 * a.hzz + f2 * a.gz * a.gz;
+    }
+    st[sp++] = r;
+  }
+  return st[0];
+}
+
+__device__ __forceinline__ double sabs(double x) { return sqrt(x * x + 1.0) - 1.0; }        // smoothmath.py:43-45
+__device__ __forceinline__ double sabs_d(double x) { return x / sqrt(x * x + 1.0); }
+__device__ __forceinline__ double srelu(double x) { return 0.5 * (x + sqrt(x * x + 1.0) - 1.0); }  // :60-63
+__device__ __forceinline__ double srelu_d(double x) { return 0.5 * (1.0 + x / sqrt(x * x + 1.0)); }
+
+// ---------------------------------------------------------------------------
+// primal intermediates of one rate evaluation, consumed by the tangent threads
+template <class M>
+struct Prim {
+  static constexpr int NL = M::NL, NJ2 = Pos<2 * M::NJ>::v, NC = Pos<M::NC>::v;
+  static constexpr int NG = M::NC + 2 * M::NJL + 2 * M::NHB;
+  double c[NL], s[NL];
+  double rp[Pos<M::NJ>::v][2], rc[Pos<M::NJ>::v][2];  // R(theta) * (anchor - com)
+  double L[NJ2][NJ2];                                 // Cholesky factor of the Gram matrix
+  double lam[NJ2];                                    // joint reactions (phi_j)
+  double vdot[3 * M::NL];
+  double rr[NC][2], n[NC][2], t[NC][2], F[NC][2], Jv[NC][2];
+  double hv[NC], g[NC][2], H[NC][3], gn[NC];  // implicit surface data
+  double sd[NC], lamc[NC], sg[NC];
+  double gp[Pos<NG>::v];
+  double u[Pos<M::NA + 3 * M::NC>::v];
+};
+
+// rate function WITHOUT the dilation factor: out = [v; vdot; Omega] (n_xt)
+//   forward_dynamics  cito/contact_dynamics.py:98-108 (+ :40-47, :76-95)
+//   generalized_forces cito/multibody.py:285-321, kinematics :259-392
+//   aux_rate           cito/augmentation.py:134-153, path g :112-129
+template <class M>
+__device__ void prim_rate(const KParams& P, const double* xs, const double* u, Prim<M>& pr, double* out) {
+  constexpr int NL = M::NL, NJ = M::NJ, NC = M::NC, NA = M::NA, NQ = 3 * NL;
+  constexpr int NU = NA + 3 * NC;
+  const double* q = xs;
+  const double* v = xs + NQ;
+#pragma unroll
+  for (int m = 0; m < NU; ++m) pr.u[m] = u[m];
+#pragma unroll
+  for (int l = 0; l < NL; ++l) sincos(q[3 * l + 2], &pr.s[l], &pr.c[l]);
+  double W[NQ];
+#pragma unroll
+  for (int k = 0; k < NQ; ++k) W[k] = 0.0;
+#pragma unroll
+  for (int l = 0; l < NL; ++l) W[3 * l + 1] += P.neg_mg[l];
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {
+    const int p = M::jparent(j), c = M::jchild(j), a = M::jact(j);
+    double mo = 0.0;
+    if (a >= 0) mo = mo + u[a];
+    if (P.jspring[j]) {
+      const double th_p = p >= 0 ? q[3 * p + 2] : 0.0;
+      const double om_p = p >= 0 ? v[3 * p + 2] : 0.0;
+      const double rel = q[3 * c + 2] - th_p - P.jrest[j];
+      mo = mo - P.jk[j] * rel - P.jd[j] * (v[3 * c + 2] - om_p);
+    }
+    W[3 * c + 2] += mo;
+    if (p >= 0) W[3 * p + 2] += -mo;
+  }
+  // contacts: frame, world force, wrench, Omega ingredients
+#pragma unroll
+  for (int i = 0; i < NC; ++i) {
+    const int l = M::clink(i);
+    const double rx = pr.c[l] * P.cr[i][0] - pr.s[l] * P.cr[i][1];
+    const double rz = pr.s[l] * P.cr[i][0] + pr.c[l] * P.cr[i][1];
+    pr.rr[i][0] = rx;
+    pr.rr[i][1] = rz;
+    const double Px = q[3 * l] + rx, Pz = q[3 * l + 1] + rz;
+    double n0, n1;
+    if constexpr (M::IMPLICIT) {
+      T2 t2 = surface_t2(P, Px, Pz);
+      pr.hv[i] = t2.v;
+      pr.g[i][0] = t2.gx;
+      pr.g[i][1] = t2.gz;
+      pr.H[i][0] = t2.hxx;
+      pr.H[i][1] = t2.hxz;
+      pr.H[i][2] = t2.hzz;
+      const double gn = sqrt(t2.gx * t2.gx + t2.gz * t2.gz);
+      pr.gn[i] = gn;
+      n0 = t2.gx / gn;
+      n1 = t2.gz / gn;
+      pr.sd[i] = t2.v / gn;
+    } else {
+      n0 = 0.0;
+      n1 = 1.0;
+      pr.sd[i] = Pz - P.height;
+    }
+    const double t0 = n1, t1 = -n0;
+    pr.n[i][0] = n0;
+    pr.n[i][1] = n1;
+    pr.t[i][0] = t0;
+    pr.t[i][1] = t1;
+    const double ft = u[NA + 2 * i], fn = u[NA + 2 * i + 1];
+    const double F0 = t0 * ft + n0 * fn, F1 = t1 * ft + n1 * fn;
+    pr.F[i][0] = F0;
+    pr.F[i][1] = F1;
+    W[3 * l] += F0;
+    W[3 * l + 1] += F1;
+    W[3 * l + 2] += (-rz) * F0 + rx * F1;
+    const double w = v[3 * l + 2];
+    pr.Jv[i][0] = v[3 * l] + (-rz) * w;
+    pr.Jv[i][1] = v[3 * l + 1] + rx * w;
+  }
+  double* vdot = out + NQ;
+  if constexpr (NJ == 0) {
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+      vdot[3 * l] = P.minv_m[l] * W[3 * l];
+      vdot[3 * l + 1] = P.minv_m[l] * W[3 * l + 1];
+      vdot[3 * l + 2] = P.minv_I[l] * W[3 * l + 2];
+    }
+  } else {
+    constexpr int NJ2 = 2 * NJ;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      const int p = M::jparent(j), c = M::jchild(j);
+      if (p >= 0) {
+        pr.rp[j][0] = pr.c[p] * P.jrp[j][0] - pr.s[p] * P.jrp[j][1];
+        pr.rp[j][1] = pr.s[p] * P.jrp[j][0] + pr.c[p] * P.jrp[j][1];
+      }
+      pr.rc[j][0] = pr.c[c] * P.jrc[j][0] - pr.s[c] * P.jrc[j][1];
+      pr.rc[j][1] = pr.s[c] * P.jrc[j][0] + pr.c[c] * P.jrc[j][1];
+    }
+    // Gram matrix G = J M^-1 J^T, only link-sharing joint pairs (compile-time)
+    double G[NJ2][NJ2];
+#pragma unroll
+    for (int a = 0; a < NJ2; ++a)
+#pragma unroll
+      for (int bb = 0; bb < NJ2; ++bb) G[a][bb] = 0.0;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j)
+#pragma unroll
+      for (int k = 0; k <= j; ++k)
+#pragma unroll
+        for (int sa = 0; sa < 2; ++sa)
+#pragma unroll
+          for (int sb = 0; sb < 2; ++sb) {
+            const int la = sa == 0 ? M::jparent(j) : M::jchild(j);
+            const int lb = sb == 0 ? M::jparent(k) : M::jchild(k);
+            if (la < 0 || la != lb) continue;
+            const double sg = (sa == sb) ? 1.0 : -1.0;
+            const double* Ra = sa == 0 ? pr.rp[j] : pr.rc[j];
+            const double* Rb = sb == 0 ? pr.rp[k] : pr.rc[k];
+            const double dA[2] = {-Ra[1], Ra[0]}, dB[2] = {-Rb[1], Rb[0]};
+#pragma unroll
+            for (int al = 0; al < 2; ++al)
+#pragma unroll
+              for (int be = 0; be < 2; ++be) {
+                double val = dA[al] * dB[be] * P.minv_I[la];
+                if (al == be) val += P.minv_m[la];
+                G[2 * j + al][2 * k + be] += sg * val;
+              }
+          }
+    // rhs = J (M^-1 W) + curv
+    double rhs[NJ2];
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+#pragma unroll
+      for (int al = 0; al < 2; ++al) {
+        double acc = 0.0;
+#pragma unroll
+        for (int sa = 0; sa < 2; ++sa) {
+          const int l = sa == 0 ? M::jparent(j) : M::jchild(j);
+          if (l < 0) continue;
+          const double sgn = sa == 0 ? 1.0 : -1.0;
+          const double* R = sa == 0 ? pr.rp[j] : pr.rc[j];
+          const double dP = al == 0 ? -R[1] : R[0];
+          const double w = v[3 * l + 2];
+          acc += sgn * (P.minv_m[l] * W[3 * l + al] + dP * P.minv_I[l] * W[3 * l + 2] - R[al] * w * w);
+        }
+        rhs[2 * j + al] = acc;
+      }
+    }
+    // Cholesky G = L L^T (lower) and solve
+#pragma unroll
+    for (int cc = 0; cc < NJ2; ++cc) {
+      double d = G[cc][cc];
+#pragma unroll
+      for (int k = 0; k < cc; ++k) d -= pr.L[cc][k] * pr.L[cc][k];
+      const double lcc = sqrt(d);
+      pr.L[cc][cc] = lcc;
+      const double il = 1.0 / lcc;
+#pragma unroll
+      for (int r = cc + 1; r < NJ2; ++r) {
+        double x = G[r][cc];
+#pragma unroll
+        for (int k = 0; k < cc; ++k) x -= pr.L[r][k] * pr.L[cc][k];
+        pr.L[r][cc] = x * il;
+      }
+    }
+    double y[NJ2];
+#pragma unroll
+    for (int r = 0; r < NJ2; ++r) {
+      double x = rhs[r];
+#pragma unroll
+      for (int k = 0; k < r; ++k) x -= pr.L[r][k] * y[k];
+      y[r] = x / pr.L[r][r];
+    }
+#pragma unroll
+    for (int r = NJ2 - 1; r >= 0; --r) {
+      double x = y[r];
+#pragma unroll
+      for (int k = r + 1; k < NJ2; ++k) x -= pr.L[k][r] * y[k];
+      y[r] = x / pr.L[r][r];
+    }
+#pragma unroll
+    for (int r = 0; r < NJ2; ++r) pr.lam[r] = -y[r];
+    // vdot = M^-1 (W + J^T lam)
+#pragma unroll
+    for (int j = 0; j < NJ; ++j)
+#pragma unroll
+      for (int sa = 0; sa < 2; ++sa) {
+        const int l = sa == 0 ? M::jparent(j) : M::jchild(j);
+        if (l < 0) continue;
+        const double sgn = sa == 0 ? 1.0 : -1.0;
+        const double* R = sa == 0 ? pr.rp[j] : pr.rc[j];
+        const double l0 = pr.lam[2 * j], l1 = pr.lam[2 * j + 1];
+        W[3 * l] += sgn * l0;
+        W[3 * l + 1] += sgn * l1;
+        W[3 * l + 2] += sgn * ((-R[1]) * l0 + R[0] * l1);
+      }
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+      vdot[3 * l] = P.minv_m[l] * W[3 * l];
+      vdot[3 * l + 1] = P.minv_m[l] * W[3 * l + 1];
+      vdot[3 * l + 2] = P.minv_I[l] * W[3 * l + 2];
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NQ; ++k) {
+    out[k] = v[k];
+    pr.vdot[k] = vdot[k];
+  }
+  // Omega (aux_rate)
+  double* y = out + 2 * NQ;
+#pragma unroll
+  for (int i = 0; i < NC; ++i) {
+    const double ft = u[NA + 2 * i], fn = u[NA + 2 * i + 1], gam = u[NA + 2 * NC + i];
+    const double vt = pr.t[i][0] * pr.Jv[i][0] + pr.t[i][1] * pr.Jv[i][1];
+    const double sgt = ft / sqrt(ft * ft + 1.0);
+    pr.sg[i] = sgt;
+    const double lamc = vt + gam * sgt;
+    pr.lamc[i] = lamc;
+    y[5 * i + 0] = fn;
+    y[5 * i + 1] = sabs(lamc);
+    y[5 * i + 2] = gam;
+    y[5 * i + 3] = sabs(P.mu[i] * fn) - sabs(ft);
+    y[5 * i + 4] = srelu(pr.sd[i]);
+  }
+  if constexpr (M::NGO > 0) {
+    constexpr int NG = Prim<M>::NG;
+    double sgv[Pos<NG>::v];
+    int r = 0;
+#pragma unroll
+    for (int i = 0; i < NC; ++i) pr.gp[r++] = -pr.sd[i];
+#pragma unroll
+    for (int k = 0; k < M::NJL; ++k) {
+      const int jj = M::jl_joint(k);
+      const int p = M::jparent(jj), c = M::jchild(jj);
+      const double rel = q[3 * c + 2] - (p >= 0 ? q[3 * p + 2] : 0.0);
+      pr.gp[r++] = rel - P.jl_hi[k];
+      pr.gp[r++] = P.jl_lo[k] - rel;
+    }
+#pragma unroll
+    for (int k = 0; k < M::NHB; ++k) {
+      const double pz = q[3 * M::hb_link(k) + 1];
+      pr.gp[r++] = P.hb_lo[k] - pz;
+      pr.gp[r++] = pz - P.hb_hi[k];
+    }
+#pragma unroll
+    for (int jg = 0; jg < NG; ++jg) sgv[jg] = srelu(pr.gp[jg]);
+#pragma unroll
+    for (int o = 0; o < M::NGO; ++o) {
+      double acc = 0.0;
+#pragma unroll
+      for (int jg = 0; jg < NG; ++jg) acc += P.mix[o][jg] * sgv[jg];
+      y[5 * NC + o] = acc;
+    }
+  }
+}
+
+// Tangent of the unscaled rate along one input direction `dir` of (q, v, u):
+//   dir in [0, NQ) -> q_dir, [NQ, 2NQ) -> v, [2NQ, 2NQ+NU) -> u.
+// Writes out[0:NQ] = d vdot, out[NQ:NQ+NY] = d Omega.
+template <class M>
+__device__ void tan_rate(const KParams& P, const Prim<M>& pr, const double* xs, int dir, double* out,
+                         int ostride) {
+  constexpr int NL = M::NL, NJ = M::NJ, NC = M::NC, NA = M::NA, NQ = 3 * NL, NX = 2 * NQ;
+  const double* q = xs;
+  const double* v = xs + NQ;
+  (void)q;
+#define SQ(k) ((dir) == (k) ? 1.0 : 0.0)
+#define SV(k) ((dir) == NQ + (k) ? 1.0 : 0.0)
+#define SU(m) ((dir) == NX + (m) ? 1.0 : 0.0)
+  double dW[NQ];
+#pragma unroll
+  for (int k = 0; k < NQ; ++k) dW[k] = 0.0;
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {
+    const int p = M::jparent(j), c = M::jchild(j), a = M::jact(j);
+    double dm = a >= 0 ? SU(a) : 0.0;
+    if (P.jspring[j]) {
+      const double dth_p = p >= 0 ? SQ(3 * p + 2) : 0.0;
+      const double dom_p = p >= 0 ? SV(3 * p + 2) : 0.0;
+      dm = dm - P.jk[j] * (SQ(3 * c + 2) - dth_p) - P.jd[j] * (SV(3 * c + 2) - dom_p);
+    }
+    dW[3 * c + 2] += dm;
+    if (p >= 0) dW[3 * p + 2] -= dm;
+  }
+  double dP[Pos<NC>::v][2], dn[Pos<NC>::v][2], dsd[Pos<NC>::v];
+#pragma unroll
+  for (int i = 0; i < NC; ++i) {
+    const int l = M::clink(i);
+    const double rx = pr.rr[i][0], rz = pr.rr[i][1];
+    const double dth = SQ(3 * l + 2);
+    dP[i][0] = SQ(3 * l) + dth * (-rz);
+    dP[i][1] = SQ(3 * l + 1) + dth * rx;
+    double dt0 = 0.0, dt1 = 0.0, dn0 = 0.0, dn1 = 0.0;
+    if constexpr (M::IMPLICIT) {
+      const double Hd0 = pr.H[i][0] * dP[i][0] + pr.H[i][1] * dP[i][1];
+      const double Hd1 = pr.H[i][1] * dP[i][0] + pr.H[i][2] * dP[i][1];
+      const double gn = pr.gn[i], g0 = pr.g[i][0], g1 = pr.g[i][1];
+      const double gHd = g0 * Hd0 + g1 * Hd1;
+      const double ign3 = 1.0 / (gn * gn * gn);
+      dn0 = Hd0 / gn - g0 * gHd * ign3;
+      dn1 = Hd1 / gn - g1 * gHd * ign3;
+      dt0 = dn1;
+      dt1 = -dn0;
+      dsd[i] = (g0 * dP[i][0] + g1 * dP[i][1]) / gn - pr.hv[i] * gHd * ign3;
+    } else {
+      dsd[i] = dP[i][1];
+    }
+    dn[i][0] = dn0;
+    dn[i][1] = dn1;
+    const double ft = pr.u[NA + 2 * i], fn = pr.u[NA + 2 * i + 1];
+    const double dft = SU(NA + 2 * i), dfn = SU(NA + 2 * i + 1);
+    const double dF0 = dt0 * ft + pr.t[i][0] * dft + dn0 * fn + pr.n[i][0] * dfn;
+    const double dF1 = dt1 * ft + pr.t[i][1] * dft + dn1 * fn + pr.n[i][1] * dfn;
+    dW[3 * l] += dF0;
+    dW[3 * l + 1] += dF1;
+    dW[3 * l + 2] += -dth * (rx * pr.F[i][0] + rz * pr.F[i][1]) + (-rz) * dF0 + rx * dF1;
+  }
+  if constexpr (NJ == 0) {
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+      out[(3 * l) * ostride] = P.minv_m[l] * dW[3 * l];
+      out[(3 * l + 1) * ostride] = P.minv_m[l] * dW[3 * l + 1];
+      out[(3 * l + 2) * ostride] = P.minv_I[l] * dW[3 * l + 2];
+    }
+  } else {
+    constexpr int NJ2 = 2 * NJ;
+    // g = dW + dJ^T lam (theta coordinates only)
+#pragma unroll
+    for (int j = 0; j < NJ; ++j)
+#pragma unroll
+      for (int sa = 0; sa < 2; ++sa) {
+        const int l = sa == 0 ? M::jparent(j) : M::jchild(j);
+        if (l < 0) continue;
+        const double sgn = sa == 0 ? 1.0 : -1.0;
+        const double* R = sa == 0 ? pr.rp[j] : pr.rc[j];
+        dW[3 * l + 2] += sgn * (-SQ(3 * l + 2)) * (R[0] * pr.lam[2 * j] + R[1] * pr.lam[2 * j + 1]);
+      }
+    // rhs' = dJ vdot + J M^-1 g + dcurv
+    double z[NJ2];
+#pragma unroll
+    for (int j = 0; j < NJ; ++j)
+#pragma unroll
+      for (int al = 0; al < 2; ++al) {
+        double acc = 0.0;
+#pragma unroll
+        for (int sa = 0; sa < 2; ++sa) {
+          const int l = sa == 0 ? M::jparent(j) : M::jchild(j);
+          if (l < 0) continue;
+          const double sgn = sa == 0 ? 1.0 : -1.0;
+          const double* R = sa == 0 ? pr.rp[j] : pr.rc[j];
+          const double dPa = al == 0 ? -R[1] : R[0];
+          const double dth = SQ(3 * l + 2), w = v[3 * l + 2], dw = SV(3 * l + 2);
+          const double term = -dth * R[al] * pr.vdot[3 * l + 2] + P.minv_m[l] * dW[3 * l + al] +
+                              dPa * P.minv_I[l] * dW[3 * l + 2] - dth * dPa * w * w - 2.0 * R[al] * w * dw;
+          acc += sgn * term;
+        }
+        z[2 * j + al] = acc;
+      }
+    // z <- G^{-1} z with the primal Cholesky factor; dlam = -z
+#pragma unroll
+    for (int r = 0; r < NJ2; ++r) {
+      double x = z[r];
+#pragma unroll
+      for (int k = 0; k < r; ++k) x -= pr.L[r][k] * z[k];
+      z[r] = x / pr.L[r][r];
+    }
+#pragma unroll
+    for (int r = NJ2 - 1; r >= 0; --r) {
+      double x = z[r];
+#pragma unroll
+      for (int k = r + 1; k < NJ2; ++k) x -= pr.L[k][r] * z[k];
+      z[r] = x / pr.L[r][r];
+    }
+    // dvdot = M^-1 (g + J^T dlam)
+#pragma unroll
+    for (int j = 0; j < NJ; ++j)
+#pragma unroll
+      for (int sa = 0; sa < 2; ++sa) {
+        const int l = sa == 0 ? M::jparent(j) : M::jchild(j);
+        if (l < 0) continue;
+        const double sgn = sa == 0 ? 1.0 : -1.0;
+        const double* R = sa == 0 ? pr.rp[j] : pr.rc[j];
+        const double l0 = -z[2 * j], l1 = -z[2 * j + 1];
+        dW[3 * l] += sgn * l0;
+        dW[3 * l + 1] += sgn * l1;
+        dW[3 * l + 2] += sgn * ((-R[1]) * l0 + R[0] * l1);
+      }
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+      out[(3 * l) * ostride] = P.minv_m[l] * dW[3 * l];
+      out[(3 * l + 1) * ostride] = P.minv_m[l] * dW[3 * l + 1];
+      out[(3 * l + 2) * ostride] = P.minv_I[l] * dW[3 * l + 2];
+    }
+  }
+  // d Omega
+  double* dy = out + NQ * ostride;
+#pragma unroll
+  for (int i = 0; i < NC; ++i) {
+    const int l = M::clink(i);
+    const double ft = pr.u[NA + 2 * i], fn = pr.u[NA + 2 * i + 1], gam = pr.u[NA + 2 * NC + i];
+    const double dft = SU(NA + 2 * i), dfn = SU(NA + 2 * i + 1), dgam = SU(NA + 2 * NC + i);
+    const double rx = pr.rr[i][0], rz = pr.rr[i][1];
+    const double dth = SQ(3 * l + 2), w = v[3 * l + 2], dw = SV(3 * l + 2);
+    // d(J_i v) = dv_lin + d(dP/dth) w + dP/dth dw, d(dP/dth) = -dth * rr
+    const double dJv0 = SV(3 * l) - dth * rx * w + (-rz) * dw;
+    const double dJv1 = SV(3 * l + 1) - dth * rz * w + rx * dw;
+    const double dvt = (dn[i][1]) * pr.Jv[i][0] + (-dn[i][0]) * pr.Jv[i][1] + pr.t[i][0] * dJv0 +
+                       pr.t[i][1] * dJv1;
+    const double q1 = ft * ft + 1.0;
+    const double dsg = dft / (q1 * sqrt(q1));
+    const double dlamc = dvt + dgam * pr.sg[i] + gam * dsg;
+    dy[(5 * i + 0) * ostride] = dfn;
+    dy[(5 * i + 1) * ostride] = sabs_d(pr.lamc[i]) * dlamc;
+    dy[(5 * i + 2) * ostride] = dgam;
+    dy[(5 * i + 3) * ostride] = sabs_d(P.mu[i] * fn) * P.mu[i] * dfn - pr.sg[i] * dft;
+    dy[(5 * i + 4) * ostride] = srelu_d(pr.sd[i]) * dsd[i];
+  }
+  if constexpr (M::NGO > 0) {
+    constexpr int NG = Prim<M>::NG;
+    double dg[Pos<NG>::v];
+    int r = 0;
+#pragma unroll
+    for (int i = 0; i < NC; ++i) dg[r++] = -dsd[i];
+#pragma unroll
+    for (int k = 0; k < M::NJL; ++k) {
+      const int jj = M::jl_joint(k);
+      const int p = M::jparent(jj), c = M::jchild(jj);
+      const double drel = SQ(3 * c + 2) - (p >= 0 ? SQ(3 * p + 2) : 0.0);
+      dg[r++] = drel;
+      dg[r++] = -drel;
+    }
+#pragma unroll
+    for (int k = 0; k < M::NHB; ++k) {
+      const double dpz = SQ(3 * M::hb_link(k) + 1);
+      dg[r++] = -dpz;
+      dg[r++] = dpz;
+    }
+#pragma unroll
+    for (int jg = 0; jg < NG; ++jg) dg[jg] *= srelu_d(pr.gp[jg]);
+#pragma unroll
+    for (int o = 0; o < M::NGO; ++o) {
+      double acc = 0.0;
+#pragma unroll
+      for (int jg = 0; jg < NG; ++jg) acc += P.mix[o][jg] * dg[jg];
+      dy[(5 * NC + o) * ostride] = acc;
+    }
+  }
+#undef SQ
+#undef SV
+#undef SU
+}
+
+template <class M>
+struct Dims {
+  static constexpr int NL = M::NL, NQ = 3 * NL, NX = 2 * NQ, NC = M::NC, NA = M::NA;
+  static constexpr int NU = NA + 3 * NC, NY = 5 * NC + M::NGO, NXT = NX + NY;
+  static constexpr int NCOL = NX + 2 * NU + 1;       // non-y tangent columns
+  static constexpr int NDIR = M::NDIRX + NU;         // rate-Jacobian input directions
+  static constexpr int NR = NQ + NY;                 // rate rows with a non-trivial Jacobian
+  static constexpr int NCOLP = NCOL | 1;             // odd stride (bank spread)
+  static constexpr int NT = ((NCOL > NDIR ? NCOL : NDIR) + 31) / 32 * 32;
+};
+
+// Shared state of one interval in the linearize kernel
+template <class M>
+struct LinShared {
+  using D = Dims<M>;
+  Prim<M> pr;
+  double x[D::NXT];
+  double xs[D::NX];
+  double r[D::NXT];
+  double K[6][D::NX];
+  double VS[6][D::NQ];
+  double kyacc[Pos<D::NY>::v];
+  double wq[D::NQ];
+  double vb[D::NQ];
+  double U[2 * D::NU + 1];
+  double A[D::NR][D::NDIR];
+  double KV[5][D::NQ][D::NCOLP];
+  double S;
+  int bad;
+};
+
+// ---------------------------------------------------------------------------
+// K1: one CTA per interval.  Thread 0 runs the primal stage chain; threads
+// < NDIR form the rate Jacobian; threads < NCOL advance tangent columns.
+template <class M>
+__global__ void __launch_bounds__(Dims<M>::NT) k_linearize(const KParams P, int64_t B, const double* __restrict__ xt0s,
+                                                          const double* __restrict__ Us, const double* __restrict__ Ss,
+                                                          double* __restrict__ ends, double* __restrict__ jx,
+                                                          double* __restrict__ ju, double* __restrict__ js,
+                                                          int32_t* __restrict__ bad) {
+  using D = Dims<M>;
+  constexpr int NQ = D::NQ, NX = D::NX, NU = D::NU, NY = D::NY, NXT = D::NXT, NCOL = D::NCOL, NR = D::NR;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  LinShared<M>& sh = *reinterpret_cast<LinShared<M>*>(smem_raw);
+  const int64_t b = blockIdx.x;
+  if (b >= B) return;
+  const int tid = threadIdx.x;
+  for (int k = tid; k < NXT; k += blockDim.x) sh.x[k] = xt0s[b * NXT + k];
+  for (int k = tid; k < 2 * NU; k += blockDim.x) sh.U[k] = Us[b * 2 * NU + k];
+  if (tid == 0) {
+    sh.S = Ss[b];
+#pragma unroll
+    for (int k = 0; k < (NY > 0 ? NY : 1); ++k) sh.kyacc[k] = 0.0;
+  }
+  __syncthreads();
+  const double S = sh.S;
+
+  // column state (registers): seed = unit column of [x~+ | U | S]
+  const bool colthr = tid < NCOL;
+  const int col = tid;
+  const double dS = (col == NCOL - 1) ? 1.0 : 0.0;
+  const int uj = col - NX;  // U column index if 0 <= uj < 2NU
+  const bool isU = (uj >= 0) && (uj < 2 * NU);
+  const int um = isU ? (uj % Pos<NU>::v) : 0;
+  const bool uplus = isU && (uj >= NU);
+  double dq[NQ], dv[NQ], dy[Pos<NY>::v];
+#pragma unroll
+  for (int k = 0; k < NQ; ++k) {
+    dq[k] = (col == k) ? 1.0 : 0.0;
+    dv[k] = (col == NQ + k) ? 1.0 : 0.0;
+  }
+#pragma unroll
+  for (int k = 0; k < NY; ++k) dy[k] = 0.0;
+
+  const double h = P.h;
+  for (int s = 0; s < P.substeps; ++s) {
+    const double tau0 = h * (double)s;
+    for (int i = 0; i < 6; ++i) {
+      const double tau = tau0 + P.ch[i];
+      // ---- primal stage (cito/augmentation.py:200-208)
+      if (tid == 0) {
+#pragma unroll
+        for (int k = 0; k < NX; ++k) {
+          double a = sh.x[k];
+          for (int j = 0; j < i; ++j) a = a + P.ha[i][j] * sh.K[j][k];
+          sh.xs[k] = a;
+        }
+#pragma unroll
+        for (int k = 0; k < NQ; ++k) {
+          sh.VS[i][k] = sh.xs[NQ + k];
+          double w = 0.0;
+          for (int j = 0; j < i; ++j) w += P.ha[i][j] * sh.VS[j][k];
+          sh.wq[k] = w;
+        }
+        double u[NU > 0 ? NU : 1];
+#pragma unroll
+        for (int m = 0; m < NU; ++m) u[m] = (1.0 - tau) * sh.U[m] + tau * sh.U[NU + m];  // foh_eval :166-169
+        prim_rate<M>(P, sh.xs, u, sh.pr, sh.r);
+#pragma unroll
+        for (int k = 0; k < NX; ++k) sh.K[i][k] = S * sh.r[k];
+#pragma unroll
+        for (int k = 0; k < NY; ++k) sh.kyacc[k] += P.b[i] * (S * sh.r[NX + k]);
+        if (i == 5) {
+#pragma unroll
+          for (int k = 0; k < NQ; ++k) {
+            double w = 0.0;
+            for (int j = 0; j < 6; ++j) w += P.b[j] * sh.VS[j][k];
+            sh.vb[k] = h * w;
+          }
+#pragma unroll
+          for (int k = 0; k < NX; ++k) {
+            double inc = 0.0;
+            for (int j = 0; j < 6; ++j) inc += P.b[j] * sh.K[j][k];
+            sh.x[k] = sh.x[k] + h * inc;
+          }
+#pragma unroll
+          for (int k = 0; k < NY; ++k) {
+            sh.x[NX + k] = sh.x[NX + k] + h * sh.kyacc[k];
+            sh.kyacc[k] = 0.0;
+          }
+        }
+      }
+      __syncthreads();
+      // ---- rate Jacobian, one input direction per thread
+      if (tid < D::NDIR) {
+        const int dir = tid < M::NDIRX ? M::dir(tid) : NX + (tid - M::NDIRX);
+        tan_rate<M>(P, sh.pr, sh.xs, dir, &sh.A[0][tid], D::NDIR);
+      }
+      __syncthreads();
+      // ---- tangent columns through stage i
+      if (colthr) {
+        double acc[NR];
+#pragma unroll
+        for (int rr = 0; rr < NR; ++rr) acc[rr] = 0.0;
+        const double Shc1 = S * P.hc1[i];
+#pragma unroll
+        for (int kd = 0; kd < M::NDIRX; ++kd) {
+          const int d = M::dir(kd);
+          double val;
+          if (d < NQ) {
+            val = dq[d] + Shc1 * dv[d] + dS * sh.wq[d];
+            for (int l = 0; l < i; ++l) val += S * P.cq[i][l] * sh.KV[l][d][col];
+          } else {
+            const int rv = d - NQ;
+            val = dv[rv];
+            for (int l = 0; l < i; ++l) val += P.ha[i][l] * sh.KV[l][rv][col];
+          }
+#pragma unroll
+          for (int rr = 0; rr < NR; ++rr) acc[rr] += sh.A[rr][kd] * val;
+        }
+        if (isU) {
+          const double coef = uplus ? tau : (1.0 - tau);
+#pragma unroll
+          for (int rr = 0; rr < NR; ++rr) acc[rr] += sh.A[rr][M::NDIRX + um] * coef;
+        }
+        // dk = S * J * d(stage input) + dS * rate
+        double dk[NR];
+#pragma unroll
+        for (int rr = 0; rr < NR; ++rr) dk[rr] = S * acc[rr] + dS * sh.r[NQ + rr];
+#pragma unroll
+        for (int m = 0; m < NY; ++m) dy[m] += (h * P.b[i]) * dk[NQ + m];
+        if (i < 5) {
+#pragma unroll
+          for (int rv = 0; rv < NQ; ++rv) sh.KV[i][rv][col] = dk[rv];
+        } else {
+#pragma unroll
+          for (int rv = 0; rv < NQ; ++rv) {
+            double incv = P.b[5] * dk[rv];
+            double incq = 0.0;
+#pragma unroll
+            for (int l = 0; l < 5; ++l) {
+              const double kv = sh.KV[l][rv][col];
+              incv += P.b[l] * kv;
+              incq += P.e2[l] * kv;
+            }
+            dq[rv] = dq[rv] + P.he1 * S * dv[rv] + S * incq + dS * sh.vb[rv];
+            dv[rv] = dv[rv] + h * incv;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // ---- outputs
+  double* jxb = jx + b * NXT * NXT;
+  double* jub = ju + b * NXT * 2 * NU;
+  double* jsb = js + b * NXT;
+  if (colthr) {
+    double* dst;
+    int stride;
+    if (col < NX) {
+      dst = jxb + col;
+      stride = NXT;
+    } else if (isU) {
+      dst = jub + uj;
+      stride = 2 * NU;
+    } else {
+      dst = jsb;
+      stride = 1;
+    }
+#pragma unroll
+    for (int k = 0; k < NQ; ++k) {
+      dst[k * stride] = dq[k];
+      dst[(NQ + k) * stride] = dv[k];
+    }
+#pragma unroll
+    for (int k = 0; k < NY; ++k) dst[(NX + k) * stride] = dy[k];
+  }
+  // y0 columns of jx are the identity (rates ignore y)
+  for (int e = tid; e < NXT * NY; e += blockDim.x) {
+    const int r = e / Pos<NY>::v, c = NX + e % Pos<NY>::v;
+    jxb[r * NXT + c] = (r == c) ? 1.0 : 0.0;
+  }
+  if (tid == 0) sh.bad = 0;
+  __syncthreads();
+  for (int k = tid; k < NXT; k += blockDim.x) {
+    const double e = sh.x[k];
+    ends[b * NXT + k] = e;
+    if (!isfinite(e)) sh.bad = 1;
+  }
+  __syncthreads();
+  if (tid == 0 && bad) bad[b] = sh.bad;
+}
+
+// ---------------------------------------------------------------------------
+// K2: primal-only flow, one thread per interval (propagate / propagate_batch).
+template <class M>
+__global__ void __launch_bounds__(128) k_propagate(const KParams P, int64_t B, const double* __restrict__ xt0s,
+                                                   const double* __restrict__ Us, const double* __restrict__ Ss,
+                                                   double* __restrict__ ends, int32_t* __restrict__ bad) {
+  using D = Dims<M>;
+  constexpr int NQ = D::NQ, NX = D::NX, NU = D::NU, NY = D::NY, NXT = D::NXT;
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  double x[NXT], xs[NX], r[NXT], K[6][NX], ky[Pos<NY>::v], U[2 * NU + 1];
+  Prim<M> pr;
+  for (int k = 0; k < NXT; ++k) x[k] = xt0s[b * NXT + k];
+  for (int k = 0; k < 2 * NU; ++k) U[k] = Us[b * 2 * NU + k];
+  const double S = Ss[b];
+  const double h = P.h;
+  for (int s = 0; s < P.substeps; ++s) {
+    const double tau0 = h * (double)s;
+#pragma unroll
+    for (int k = 0; k < NY; ++k) ky[k] = 0.0;
+    for (int i = 0; i < 6; ++i) {
+      const double tau = tau0 + P.ch[i];
+      for (int k = 0; k < NX; ++k) {
+        double a = x[k];
+        for (int j = 0; j < i; ++j) a = a + P.ha[i][j] * K[j][k];
+        xs[k] = a;
+      }
+      double u[NU > 0 ? NU : 1];
+#pragma unroll
+      for (int m = 0; m < NU; ++m) u[m] = (1.0 - tau) * U[m] + tau * U[NU + m];
+      prim_rate<M>(P, xs, u, pr, r);
+      for (int k = 0; k < NX; ++k) K[i][k] = S * r[k];
+#pragma unroll
+      for (int k = 0; k < NY; ++k) ky[k] += P.b[i] * (S * r[NX + k]);
+    }
+    for (int k = 0; k < NX; ++k) {
+      double inc = 0.0;
+      for (int j = 0; j < 6; ++j) inc += P.b[j] * K[j][k];
+      x[k] = x[k] + h * inc;
+    }
+#pragma unroll
+    for (int k = 0; k < NY; ++k) x[NX + k] = x[NX + k] + h * ky[k];
+  }
+  int nb = 0;
+  for (int k = 0; k < NXT; ++k) {
+    ends[b * NXT + k] = x[k];
+    nb |= !isfinite(x[k]);
+  }
+  if (bad) bad[b] = nb;
+  (void)NQ;
+}

@@ -1,0 +1,326 @@
+// cito_node.cuh — node relations of the transcription and their Jacobians (K3).
+//
+// Replaces cito.ocp.Transcription.node_constraints / node_jacobians
+// (/root/reference/pkg/src/cito/ocp.py:272-365):
+//   psi_fn     ocp.py:277-287   (integral cross-complementarity, FB on y increments)
+//   theta_fn   ocp.py:289-296 -> impact_residuals cito/contact_dynamics.py:134-172
+//   impulse_fn ocp.py:298-303 -> impact_map       cito/contact_dynamics.py:111-124
+// One thread per (node item, input direction): the function is evaluated in
+// forward-mode dual arithmetic seeded on that direction, giving one Jacobian
+// column; direction 0 also writes the values.
+#pragma once
+
+#include "cito_kernels.cuh"
+
+struct Dn {
+  double v, d;
+};
+__device__ __forceinline__ Dn dn(double v) { return {v, 0.0}; }
+__device__ __forceinline__ Dn operator+(Dn a, Dn b) { return {a.v + b.v, a.d + b.d}; }
+__device__ __forceinline__ Dn operator-(Dn a, Dn b) { return {a.v - b.v, a.d - b.d}; }
+__device__ __forceinline__ Dn operator-(Dn a) { return {-a.v, -a.d}; }
+__device__ __forceinline__ Dn operator*(Dn a, Dn b) { return {a.v * b.v, a.d * b.v + a.v * b.d}; }
+__device__ __forceinline__ Dn operator*(double c, Dn a) { return {c * a.v, c * a.d}; }
+__device__ __forceinline__ Dn operator/(Dn a, Dn b) {
+  const double r = a.v / b.v;
+  return {r, (a.d - r * b.d) / b.v};
+}
+__device__ __forceinline__ Dn dsqrt(Dn a) {
+  const double r = sqrt(a.v);
+  return {r, a.d * 0.5 / r};
+}
+__device__ __forceinline__ Dn dsabs(Dn x) { return dsqrt(x * x + dn(1.0)) - dn(1.0); }
+__device__ __forceinline__ Dn dfb(Dn a, Dn b, double delta) {  // smoothmath.py:90-92
+  return a + b - dsqrt(a * a + b * b + dn(delta));
+}
+__device__ __forceinline__ Dn dsng(Dn x) { return x / dsqrt(x * x + dn(1.0)); }  // contact_dynamics.py:50-52
+
+// contact point, frame and signed distance in dual arithmetic (multibody.py:264-269, 384-411)
+template <class M>
+__device__ void contact_geom(const KParams& P, const Dn* q, int i, Dn* dPdth, Dn* n, Dn* t, Dn& sd) {
+  const int l = M::clink(i);
+  double sv, cv;
+  sincos(q[3 * l + 2].v, &sv, &cv);
+  const Dn c = {cv, -sv * q[3 * l + 2].d}, s = {sv, cv * q[3 * l + 2].d};
+  const Dn rx = P.cr[i][0] * c - P.cr[i][1] * s;
+  const Dn rz = P.cr[i][0] * s + P.cr[i][1] * c;
+  const Dn Px = q[3 * l] + rx, Pz = q[3 * l + 1] + rz;
+  dPdth[0] = -rz;
+  dPdth[1] = rx;
+  if constexpr (M::IMPLICIT) {
+    T2 t2 = surface_t2(P, Px.v, Pz.v);
+    const Dn h = {t2.v, t2.gx * Px.d + t2.gz * Pz.d};
+    const Dn gx = {t2.gx, t2.hxx * Px.d + t2.hxz * Pz.d};
+    const Dn gz = {t2.gz, t2.hxz * Px.d + t2.hzz * Pz.d};
+    const Dn gn = dsqrt(gx * gx + gz * gz);
+    n[0] = gx / gn;
+    n[1] = gz / gn;
+    sd = h / gn;
+  } else {
+    n[0] = dn(0.0);
+    n[1] = dn(1.0);
+    sd = Pz - dn(P.height);
+  }
+  t[0] = n[1];
+  t[1] = -n[0];
+}
+
+template <class M>
+__device__ void node_psi(const KParams& P, const double* yp, int dir, double delta, double eps, double* val,
+                         double* jcol, int jstride) {
+  constexpr int NC = M::NC, NY = 5 * NC + M::NGO;
+  auto Y = [&](int k) -> Dn { return {yp[k], dir == k ? 1.0 : 0.0}; };
+  int r = 0;
+#pragma unroll
+  for (int i = 0; i < NC; ++i) {
+    Dn d[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) d[k] = Y(NY + 5 * i + k) - Y(5 * i + k);
+    const Dn rows[3] = {dfb(d[0], d[4], delta), dfb(d[0], d[1], delta), dfb(d[2], d[3], delta)};
+#pragma unroll
+    for (int k = 0; k < 3; ++k, ++r) {
+      if (val) val[r] = rows[k].v;
+      jcol[r * jstride] = rows[k].d;
+    }
+  }
+#pragma unroll
+  for (int o = 0; o < M::NGO; ++o, ++r) {
+    const Dn v = Y(NY + 5 * NC + o) - Y(5 * NC + o) - dn(eps);
+    if (val) val[r] = v.v;
+    jcol[r * jstride] = v.d;
+  }
+}
+
+template <class M>
+__device__ void node_theta(const KParams& P, const double* vec, int dir, double delta, double* val, double* jcol,
+                           int jstride) {
+  constexpr int NL = M::NL, NC = M::NC, NQ = 3 * NL, NV = 3 * NQ + 3 * NC;
+  Dn x[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) x[k] = {vec[k], dir == k ? 1.0 : 0.0};
+  const Dn* q = x;
+  const Dn* vm = x + NQ;
+  const Dn* vp = x + 2 * NQ;
+  const Dn* Phi = x + 3 * NQ;
+  const Dn* Gam = x + 3 * NQ + 2 * NC;
+#pragma unroll
+  for (int i = 0; i < NC; ++i) {
+    const int l = M::clink(i);
+    Dn dP[2], n[2], t[2], sd;
+    contact_geom<M>(P, q, i, dP, n, t, sd);
+    Dn va[3], vb[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      va[k] = vp[3 * l + k] + P.crest[i] * vm[3 * l + k];
+      vb[k] = vp[3 * l + k];
+    }
+    const Dn Ja0 = va[0] + dP[0] * va[2], Ja1 = va[1] + dP[1] * va[2];
+    const Dn Jb0 = vb[0] + dP[0] * vb[2], Jb1 = vb[1] + dP[1] * vb[2];
+    const Dn vn_rest = n[0] * Ja0 + n[1] * Ja1;
+    const Dn vt_plus = t[0] * Jb0 + t[1] * Jb1;
+    const Dn Pt = Phi[2 * i], Pn = Phi[2 * i + 1];
+    const Dn cone = dsabs(P.mu[i] * Pn) - dsabs(Pt);
+    const Dn rows[6] = {Pn * vn_rest, Pn * (vt_plus + Gam[i] * dsng(Pt)), dfb(Pn, sd, delta),
+                        dfb(Gam[i], cone, delta), -sd, -vn_rest};
+    const int ro[6] = {2 * i, 2 * i + 1, 2 * NC + 4 * i, 2 * NC + 4 * i + 1, 2 * NC + 4 * i + 2,
+                       2 * NC + 4 * i + 3};
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      if (val) val[ro[k]] = rows[k].v;
+      jcol[ro[k] * jstride] = rows[k].d;
+    }
+  }
+}
+
+template <class M>
+__device__ void node_impulse(const KParams& P, const double* vec, int dir, double* val, double* jcol, int jstride) {
+  constexpr int NL = M::NL, NJ = M::NJ, NC = M::NC, NQ = 3 * NL, NI = 3 * NQ + 2 * NC;
+  Dn x[NI];
+#pragma unroll
+  for (int k = 0; k < NI; ++k) x[k] = {vec[k], dir == k ? 1.0 : 0.0};
+  const Dn* q = x;
+  const Dn* vm = x + NQ;
+  const Dn* vp = x + 2 * NQ;
+  const Dn* Phi = x + 3 * NQ;
+  Dn w[NQ];
+#pragma unroll
+  for (int k = 0; k < NQ; ++k) w[k] = dn(0.0);
+#pragma unroll
+  for (int i = 0; i < NC; ++i) {  // _contact_wrench with impulses
+    const int l = M::clink(i);
+    Dn dP[2], n[2], t[2], sd;
+    contact_geom<M>(P, q, i, dP, n, t, sd);
+    const Dn F0 = t[0] * Phi[2 * i] + n[0] * Phi[2 * i + 1];
+    const Dn F1 = t[1] * Phi[2 * i] + n[1] * Phi[2 * i + 1];
+    w[3 * l] = w[3 * l] + F0;
+    w[3 * l + 1] = w[3 * l + 1] + F1;
+    w[3 * l + 2] = w[3 * l + 2] + (dP[0] * F0 + dP[1] * F1);
+  }
+  Dn out[NQ];
+  if constexpr (NJ == 0) {
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+      out[3 * l] = vm[3 * l] + P.minv_m[l] * w[3 * l];
+      out[3 * l + 1] = vm[3 * l + 1] + P.minv_m[l] * w[3 * l + 1];
+      out[3 * l + 2] = vm[3 * l + 2] + P.minv_I[l] * w[3 * l + 2];
+    }
+  } else {
+    constexpr int NJ2 = 2 * NJ;
+    Dn cth[NL], sth[NL];
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+      double sv, cv;
+      sincos(q[3 * l + 2].v, &sv, &cv);
+      cth[l] = {cv, -sv * q[3 * l + 2].d};
+      sth[l] = {sv, cv * q[3 * l + 2].d};
+    }
+    Dn R[Pos<NJ>::v][2][2];  // [joint][side][xz]
+#pragma unroll
+    for (int j = 0; j < NJ; ++j)
+#pragma unroll
+      for (int sa = 0; sa < 2; ++sa) {
+        const int l = sa == 0 ? M::jparent(j) : M::jchild(j);
+        if (l < 0) continue;
+        const double ax = sa == 0 ? P.jrp[j][0] : P.jrc[j][0], az = sa == 0 ? P.jrp[j][1] : P.jrc[j][1];
+        R[j][sa][0] = ax * cth[l] - az * sth[l];
+        R[j][sa][1] = ax * sth[l] + az * cth[l];
+      }
+    Dn G[NJ2][NJ2];
+#pragma unroll
+    for (int a = 0; a < NJ2; ++a)
+#pragma unroll
+      for (int bb = 0; bb < NJ2; ++bb) G[a][bb] = dn(0.0);
+#pragma unroll
+    for (int j = 0; j < NJ; ++j)
+#pragma unroll
+      for (int k = 0; k <= j; ++k)
+#pragma unroll
+        for (int sa = 0; sa < 2; ++sa)
+#pragma unroll
+          for (int sb = 0; sb < 2; ++sb) {
+            const int la = sa == 0 ? M::jparent(j) : M::jchild(j);
+            const int lb = sb == 0 ? M::jparent(k) : M::jchild(k);
+            if (la < 0 || la != lb) continue;
+            const double sg = (sa == sb) ? 1.0 : -1.0;
+            const Dn dA[2] = {-R[j][sa][1], R[j][sa][0]}, dB[2] = {-R[k][sb][1], R[k][sb][0]};
+#pragma unroll
+            for (int al = 0; al < 2; ++al)
+#pragma unroll
+              for (int be = 0; be < 2; ++be) {
+                Dn v = P.minv_I[la] * (dA[al] * dB[be]);
+                if (al == be) v = v + dn(P.minv_m[la]);
+                G[2 * j + al][2 * k + be] = G[2 * j + al][2 * k + be] + sg * v;
+              }
+          }
+    // rhs = J (v- + M^-1 w)
+    Dn a[NQ];
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+      a[3 * l] = vm[3 * l] + P.minv_m[l] * w[3 * l];
+      a[3 * l + 1] = vm[3 * l + 1] + P.minv_m[l] * w[3 * l + 1];
+      a[3 * l + 2] = vm[3 * l + 2] + P.minv_I[l] * w[3 * l + 2];
+    }
+    Dn z[NJ2];
+#pragma unroll
+    for (int j = 0; j < NJ; ++j)
+#pragma unroll
+      for (int al = 0; al < 2; ++al) {
+        Dn acc = dn(0.0);
+#pragma unroll
+        for (int sa = 0; sa < 2; ++sa) {
+          const int l = sa == 0 ? M::jparent(j) : M::jchild(j);
+          if (l < 0) continue;
+          const double sgn = sa == 0 ? 1.0 : -1.0;
+          const Dn dPa = al == 0 ? -R[j][sa][1] : R[j][sa][0];
+          acc = acc + sgn * (a[3 * l + al] + dPa * a[3 * l + 2]);
+        }
+        z[2 * j + al] = acc;
+      }
+    // Cholesky in dual arithmetic, solve, Phi_j = -x
+    Dn L[NJ2][NJ2];
+#pragma unroll
+    for (int cc = 0; cc < NJ2; ++cc) {
+      Dn d = G[cc][cc];
+#pragma unroll
+      for (int k = 0; k < cc; ++k) d = d - L[cc][k] * L[cc][k];
+      L[cc][cc] = dsqrt(d);
+#pragma unroll
+      for (int r = cc + 1; r < NJ2; ++r) {
+        Dn x2 = G[r][cc];
+#pragma unroll
+        for (int k = 0; k < cc; ++k) x2 = x2 - L[r][k] * L[cc][k];
+        L[r][cc] = x2 / L[cc][cc];
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < NJ2; ++r) {
+      Dn x2 = z[r];
+#pragma unroll
+      for (int k = 0; k < r; ++k) x2 = x2 - L[r][k] * z[k];
+      z[r] = x2 / L[r][r];
+    }
+#pragma unroll
+    for (int r = NJ2 - 1; r >= 0; --r) {
+      Dn x2 = z[r];
+#pragma unroll
+      for (int k = r + 1; k < NJ2; ++k) x2 = x2 - L[k][r] * z[k];
+      z[r] = x2 / L[r][r];
+    }
+    // v+ = v- + M^-1 (w + J^T Phi_j)
+#pragma unroll
+    for (int j = 0; j < NJ; ++j)
+#pragma unroll
+      for (int sa = 0; sa < 2; ++sa) {
+        const int l = sa == 0 ? M::jparent(j) : M::jchild(j);
+        if (l < 0) continue;
+        const double sgn = sa == 0 ? 1.0 : -1.0;
+        const Dn l0 = -z[2 * j], l1 = -z[2 * j + 1];
+        w[3 * l] = w[3 * l] + sgn * l0;
+        w[3 * l + 1] = w[3 * l + 1] + sgn * l1;
+        w[3 * l + 2] = w[3 * l + 2] + sgn * ((-R[j][sa][1]) * l0 + R[j][sa][0] * l1);
+      }
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+      out[3 * l] = vm[3 * l] + P.minv_m[l] * w[3 * l];
+      out[3 * l + 1] = vm[3 * l + 1] + P.minv_m[l] * w[3 * l + 1];
+      out[3 * l + 2] = vm[3 * l + 2] + P.minv_I[l] * w[3 * l + 2];
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NQ; ++k) {
+    const Dn r = vp[k] - out[k];
+    if (val) val[k] = r.v;
+    jcol[k * jstride] = r.d;
+  }
+}
+
+template <class M>
+__global__ void __launch_bounds__(64) k_node(const KParams P, int64_t Np, int64_t Nn, const double* __restrict__ y_pairs,
+                                             const double* __restrict__ theta_vecs, double delta, double eps,
+                                             double* __restrict__ psi, double* __restrict__ psi_jac,
+                                             double* __restrict__ th, double* __restrict__ th_jac,
+                                             double* __restrict__ imp, double* __restrict__ imp_jac) {
+  constexpr int NL = M::NL, NC = M::NC, NQ = 3 * NL, NY = 5 * NC + M::NGO;
+  constexpr int NPSI = 3 * NC + M::NGO, NV = 3 * NQ + 3 * NC, NI = 3 * NQ + 2 * NC;
+  // item space: [Np * 2NY psi columns][Nn * NV theta columns][Nn * NI impulse columns]
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n_psi = Np * (2 * NY), n_th = Nn * NV, n_imp = Nn * NI;
+  if (t < n_psi) {
+    constexpr int NY2 = Pos<2 * NY>::v;
+    const int64_t k = t / NY2;
+    const int d = (int)(t % NY2);
+    node_psi<M>(P, y_pairs + k * 2 * NY, d, delta, eps, d == 0 ? psi + k * NPSI : nullptr,
+                psi_jac + k * NPSI * 2 * NY + d, 2 * NY);
+  } else if (t < n_psi + n_th) {
+    const int64_t e = t - n_psi;
+    const int64_t k = e / NV;
+    const int d = (int)(e % NV);
+    node_theta<M>(P, theta_vecs + k * NV, d, delta, d == 0 ? th + k * 6 * NC : nullptr,
+                  th_jac + k * 6 * NC * NV + d, NV);
+  } else if (t < n_psi + n_th + n_imp) {
+    const int64_t e = t - n_psi - n_th;
+    const int64_t k = e / NI;
+    const int d = (int)(e % NI);
+    node_impulse<M>(P, theta_vecs + k * NV, d, d == 0 ? imp + k * NQ : nullptr, imp_jac + k * NQ * NI + d, NI);
+  }
+}

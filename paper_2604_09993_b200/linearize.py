@@ -1,0 +1,177 @@
+"""GPU-resident ``linearize_all`` (cito/scp.py:87-135) and node relations.
+
+``GpuTranscription`` owns, for one scenario, the interval discretizer (K1/K2),
+the node-relation kernel (K3) and the device-side index maps of the decision
+vector layout (cito/ocp.py:131-203).  ``linearize_all`` gathers the interval
+starts/controls/dilations and the node input vectors from z on the device,
+runs K1 and K3, forms the multiple-shooting defects, and returns a
+``LinearizedProblem`` with the reference's field names and shapes (numpy,
+physical units) -- or keeps everything on the device (``to_host=False``) for
+the CSC scatter (scatter.py).
+"""
+
+import sys
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .discretizer import Discretizer
+
+__all__ = ["node_inputs", "LinearizedProblem", "GpuTranscription", "linearize_all", "NodeLinearizer"]
+
+
+def node_inputs(lay, z):
+    """y pairs and packed node vectors exactly as Transcription._node_inputs (ocp.py:312-334)."""
+    n_q = lay.n_q
+    N = lay.N
+    y_pairs = np.stack([np.concatenate([z[lay.y_of_xp(k)], z[lay.y_of_xm(k + 1)]]) for k in range(N - 1)])
+    theta_vecs = np.stack([
+        np.concatenate([z[lay.xm(k)][:n_q], z[lay.xm(k)][n_q: 2 * n_q], z[lay.xp(k)][n_q: 2 * n_q],
+                        z[lay.phi(k)], z[lay.gam(k)]]) for k in range(N)])
+    return y_pairs, theta_vecs
+
+
+@dataclass
+class LinearizedProblem:
+    """Same fields as cito.scp.LinearizedProblem (scp.py:69-84)."""
+
+    z_ref: np.ndarray
+    ends: np.ndarray
+    jx: np.ndarray
+    ju: np.ndarray
+    js: np.ndarray
+    defects: np.ndarray
+    psi: np.ndarray
+    psi_jac: np.ndarray
+    theta: np.ndarray
+    theta_jac: np.ndarray
+    imp_v: np.ndarray
+    imp_jac: np.ndarray
+
+
+def _lp_type():
+    mod = sys.modules.get("cito.scp")
+    if mod is not None and hasattr(mod, "LinearizedProblem"):
+        return mod.LinearizedProblem
+    return LinearizedProblem
+
+
+class NodeLinearizer:
+    """Transcription.node_constraints + node_jacobians (ocp.py:336-365) via K3."""
+
+    def __init__(self, disc):
+        self.disc = disc
+
+    def device(self, y_pairs, theta_vecs, delta, epsilon, out=None, stream=None):
+        import torch
+
+        h = self.disc._h
+        d = h.dims
+        n_c = len(self.disc.model.contacts)
+        n_q, n_y = d.n_q, d.n_y
+        n_psi = 3 * n_c + (n_y - 5 * n_c)
+        Np, Nn = y_pairs.shape[0], theta_vecs.shape[0]
+        dev = theta_vecs.device
+        f64 = dict(dtype=torch.float64, device=dev)
+        if out is None:
+            out = (torch.empty((Np, n_psi), **f64), torch.empty((Np, n_psi, 2 * n_y), **f64),
+                   torch.empty((Nn, 6 * n_c), **f64), torch.empty((Nn, 6 * n_c, 3 * n_q + 3 * n_c), **f64),
+                   torch.empty((Nn, n_q), **f64), torch.empty((Nn, n_q, 3 * n_q + 2 * n_c), **f64))
+        s = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
+        yp = y_pairs if Np else theta_vecs
+        _lib.check(_lib.lib().cito_node_linearize_dev(h.ptr, Np, Nn, yp.data_ptr(), theta_vecs.data_ptr(),
+                                                      float(delta), float(epsilon),
+                                                      *[o.data_ptr() for o in out], s), "node_linearize")
+        return out
+
+    def host(self, y_pairs, theta_vecs, delta, epsilon):
+        import torch
+
+        dev = torch.device("cuda", torch.cuda.current_device())
+        yp = torch.as_tensor(np.ascontiguousarray(y_pairs, dtype=np.float64), device=dev)
+        tv = torch.as_tensor(np.ascontiguousarray(theta_vecs, dtype=np.float64), device=dev)
+        out = self.device(yp, tv, delta, epsilon)
+        torch.cuda.current_stream(dev).synchronize()
+        return tuple(o.cpu().numpy() for o in out)
+
+
+class GpuTranscription:
+    """Device-side workspace of one scenario (reference Transcription or our ScenarioSpec)."""
+
+    def __init__(self, tr_or_scenario, device=None):
+        import torch
+
+        if hasattr(tr_or_scenario, "layout") and hasattr(tr_or_scenario, "discretizer"):
+            tr = tr_or_scenario
+            self.scenario = tr.scenario
+            self.lay = tr.layout
+            self.disc = Discretizer(tr.model, mixing=tr.mixing, path_fn=tr.path_fn, substeps=tr.scenario.substeps)
+        else:
+            from .scenario import Layout
+
+            sc = tr_or_scenario
+            self.scenario = sc
+            self.lay = Layout(sc)
+            g, n_g = sc.path_constraints()
+            self.disc = Discretizer(sc.model, mixing=sc.mixing_matrix(n_g), path_fn=g, substeps=sc.substeps)
+        self.nodes = NodeLinearizer(self.disc)
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        lay = self.lay
+        N, n_q = lay.N, lay.n_q
+        idx_start = np.stack([lay.xp(k) for k in range(N - 1)])
+        idx_end = np.stack([lay.xm(k + 1) for k in range(N - 1)])
+        idx_u = np.stack([lay.u(k) for k in range(N - 1)])
+        idx_s = np.array([lay.s(k)[0] for k in range(N - 1)])
+        idx_yp = np.stack([np.concatenate([lay.y_of_xp(k), lay.y_of_xm(k + 1)]) for k in range(N - 1)])
+        idx_th = np.stack([np.concatenate([lay.xm(k)[:n_q], lay.xm(k)[n_q: 2 * n_q], lay.xp(k)[n_q: 2 * n_q],
+                                           lay.phi(k), lay.gam(k)]) for k in range(N)])
+        t = lambda a: torch.as_tensor(np.ascontiguousarray(a, dtype=np.int64), device=self.device)
+        self._i_start, self._i_end, self._i_u, self._i_s = t(idx_start), t(idx_end), t(idx_u), t(idx_s)
+        self._i_yp, self._i_th = t(idx_yp), t(idx_th)
+        self.n_imp = 3 * n_q + 2 * lay.n_c
+
+    def linearize_device(self, z_dev, delta, epsilon=None):
+        """Everything on the device; returns a dict of torch tensors."""
+        if epsilon is None:
+            epsilon = self.scenario.ctcs_epsilon
+        starts = z_dev[self._i_start]
+        Us = z_dev[self._i_u]
+        Ss = z_dev[self._i_s]
+        ends, jx, ju, js, bad = self.disc.linearize_batch_device(starts, Us, Ss)
+        defects = z_dev[self._i_end] - ends
+        y_pairs = z_dev[self._i_yp]
+        theta_vecs = z_dev[self._i_th]
+        psi, psi_j, th, th_j, imp, imp_j = self.nodes.device(y_pairs, theta_vecs, delta, epsilon)
+        return dict(starts=starts, Us=Us, Ss=Ss, ends=ends, jx=jx, ju=ju, js=js, bad=bad, defects=defects,
+                    psi=psi, psi_jac=psi_j, theta=th, theta_jac=th_j, imp_v=imp, imp_jac=imp_j)
+
+    def linearize_all(self, z, delta, epsilon=None, jobs=1):
+        """Drop-in for cito.scp.linearize_all(tr, z, delta, epsilon, jobs) (scp.py:87-135)."""
+        import torch
+
+        z = np.asarray(z, dtype=float)
+        if not np.all(np.isfinite(z)):
+            raise FloatingPointError("non-finite reference point")
+        z_dev = torch.as_tensor(np.ascontiguousarray(z), device=self.device)
+        r = self.linearize_device(z_dev, delta, epsilon)
+        host = {k: v.cpu().numpy() for k, v in r.items()}
+        if host["bad"].any():
+            raise FloatingPointError(f"non-finite state in intervals {np.where(host['bad'] != 0)[0].tolist()}")
+        LP = _lp_type()
+        return LP(z_ref=z.copy(), ends=host["ends"], jx=host["jx"], ju=host["ju"], js=host["js"],
+                  defects=host["defects"], psi=host["psi"], psi_jac=host["psi_jac"], theta=host["theta"],
+                  theta_jac=host["theta_jac"], imp_v=host["imp_v"], imp_jac=host["imp_jac"])
+
+
+_cache = {}
+
+
+def linearize_all(tr, z, delta, epsilon=None, jobs=1):
+    """Module-level drop-in for cito.scp.linearize_all: caches one GpuTranscription per tr."""
+    key = id(tr)
+    g = _cache.get(key)
+    if g is None or g[0] is not tr:
+        g = (tr, GpuTranscription(tr))
+        _cache[key] = g
+    return g[1].linearize_all(z, delta, epsilon, jobs)
