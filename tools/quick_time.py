@@ -1,0 +1,27 @@
+"""Quick device-resident timing of K1/K2 on synthetic HalfCheetah intervals."""
+import sys, time
+import numpy as np
+import torch
+sys.path.insert(0, ".")
+from paper_2604_09993_b200 import scenario as S, synth, Discretizer
+
+sc = S.bundled("halfcheetah_bound", N=30)
+g, n_g = sc.path_constraints()
+disc = Discretizer(sc.model, sc.mixing_matrix(n_g), g, substeps=sc.substeps)
+for B in [int(a) for a in (sys.argv[1:] or ["29", "4096"])]:
+    x, U, Sv = synth.random_intervals(sc, B, seed=0)
+    dev = torch.device("cuda")
+    xd, Ud, Sd = (torch.as_tensor(a, device=dev) for a in (x, U, Sv))
+    out = disc.linearize_batch_device(xd, Ud, Sd)
+    torch.cuda.synchronize()
+    for name, fn in (("linearize", lambda: disc.linearize_batch_device(xd, Ud, Sd, out=out)),
+                     ("propagate", lambda: disc.propagate_batch_device(xd, Ud, Sd))):
+        for _ in range(3): fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n = 10
+        e0.record()
+        for _ in range(n): fn()
+        e1.record(); torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / n
+        print(f"B={B} {name}: {ms:.3f} ms  -> {B/ms*1e3:.3e} intervals/s", flush=True)
