@@ -1,0 +1,446 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 discretize+linearize hot path (one JSON line on rank 0).
+
+Metric (BASELINE.json): interval linearizations/sec (fp64), HalfCheetah N=30;
+SCP-iteration linearize ms (= ms_per_step).
+
+Workload ``scp`` (default, configs[1]): one SCP iteration's linearization of
+HalfCheetah (halfcheetah_bound.json, N=30, 5 substeps -> 29 intervals) at an
+SCP-realistic point (the scenario's initial guess; rank r uses seed r):
+gather from z -> K1 interval linearize (ends, Phi, B-, B+, dS) -> defects ->
+K3 node relations + Jacobians -> K4 scatter of the dynamics rows into CSC
+values + b.  ``batch``: configs[2], 4096 independent synthetic intervals per
+GPU (one K1 launch per step).
+
+  value  device-resident throughput (inputs already in HBM), CUDA events per
+         step on the launching stream, L2 flushed (256 MiB write) between steps,
+         max over ranks.
+  e2e    same step through the public API with host buffers: H2D of z (pinned)
+         + device work + D2H of every output (LinearizedProblem arrays, CSC
+         values, b) inside the timed region.
+  --impl reference   the reference algorithm on the host cores: the C oracle
+         port (oracle/cito_oracle.c; JAX, the reference's runtime, is not
+         installable here), all threads, same workload/metric.
+
+Multi-GPU: one process per GPU (torchrun); each rank linearizes its own
+independent problem(s) (weak scaling), no data-path collective.
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "interval linearizations/sec (fp64) HalfCheetah N=30; SCP-iteration linearize ms"
+UNIT = "intervals/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=50)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--workload", choices=["scp", "batch"], default="scp")
+    p.add_argument("--batch", type=int, default=4096)
+    p.add_argument("--cpu-seconds", type=float, default=10.0)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-batch-extra", action="store_true")
+    return p.parse_args()
+
+
+def env_rank():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+# --------------------------------------------------------------------------- shared problem setup
+def scp_problem(seed):
+    from paper_2604_09993_b200 import scenario as S
+
+    sc = S.bundled("halfcheetah_bound", N=30)
+    sc.seed = seed
+    return sc
+
+
+def cpu_step_fn(sc, seed):
+    """One reference-algorithm SCP linearization on the host (oracle port)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle
+
+    from paper_2604_09993_b200.linearize import node_inputs
+    from paper_2604_09993_b200.model import pack_model
+    from paper_2604_09993_b200.scenario import Layout
+
+    lay = Layout(sc)
+    g, n_g = sc.path_constraints()
+    desc = pack_model(sc.model, sc.mixing_matrix(n_g), g)
+    z = np.load(os.path.join(ROOT, "tests", "golden", "halfcheetah_n30.npz"))["ig_z"]
+    starts = np.stack([z[lay.xp(k)] for k in range(lay.N - 1)])
+    Us = np.stack([z[lay.u(k)] for k in range(lay.N - 1)])
+    Ss = np.array([z[lay.s(k)][0] for k in range(lay.N - 1)])
+    yp, tv = node_inputs(lay, z)
+
+    def step():
+        pyoracle.linearize(desc, sc.substeps, starts, Us, Ss)
+        pyoracle.node_linearize(desc, yp, tv, 1.0, sc.ctcs_epsilon)
+        return lay.N - 1
+
+    return step, pyoracle
+
+
+def cpu_batch_fn(sc, B):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle
+
+    from paper_2604_09993_b200 import synth
+    from paper_2604_09993_b200.model import pack_model
+
+    g, n_g = sc.path_constraints()
+    desc = pack_model(sc.model, sc.mixing_matrix(n_g), g)
+    x, U, S = synth.random_intervals(sc, B, seed=0)
+
+    def step():
+        pyoracle.linearize(desc, sc.substeps, x, U, S)
+        return B
+
+    return step, pyoracle
+
+
+def time_cpu(step, seconds, min_steps=1):
+    n, t0 = 0, time.perf_counter()
+    units = 0
+    while n < min_steps or time.perf_counter() - t0 < seconds:
+        units += step()
+        n += 1
+    dt = time.perf_counter() - t0
+    return units / dt, n, dt
+
+
+# --------------------------------------------------------------------------- GPU helpers
+class Clocks:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = [l.split(",") for l in open(self.f.name).read().strip().splitlines() if l.count(",") >= 8]
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm = [float(r[1]) for r in rows]
+        mx = float(rows[0][2])
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if "Active" in v and "Not" not in v})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": reasons, "samples": len(rows),
+                "power_w_max": max(float(r[3]) for r in rows if r[3].strip() not in ("", "[N/A]"))}
+
+
+def fp64_peak_tflops(torch, dev):
+    from paper_2604_09993_b200 import _lib
+
+    out = torch.zeros(1, dtype=torch.float64, device=dev)
+    s = torch.cuda.current_stream(dev)
+    best = 0.0
+    for iters in (64, 2048, 2048, 2048, 2048):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        fl = _lib.lib().cito_dfma_peak(iters, out.data_ptr(), s.cuda_stream)
+        e1.record(s)
+        s.synchronize()
+        best = max(best, fl / (e0.elapsed_time(e1) * 1e-3) / 1e12)
+    return best
+
+
+def flops_per_interval(key):
+    path = os.path.join(ROOT, "profiles", "flops_per_interval.json")
+    if not os.path.exists(path):
+        return None, None
+    d = json.load(open(path))
+    e = d.get(key)
+    return (e["flops"], d.get("definition")) if e else (None, None)
+
+
+def ncu_traffic(key):
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(path):
+        return None
+    return json.load(open(path)).get(key, {}).get("dram_bytes_per_launch")
+
+
+def run_ours(args):
+    import torch
+
+    rank, world, local = env_rank()
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    dev = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(dev)
+    from paper_2604_09993_b200 import synth
+    from paper_2604_09993_b200.linearize import GpuTranscription, initial_guess
+    from paper_2604_09993_b200.scatter import DynamicsScatter, n_cols
+    from paper_2604_09993_b200.scenario import build_scaling
+
+    sc = scp_problem(seed=rank)
+    gt = GpuTranscription(sc, device=dev.index)
+    lay = gt.lay
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
+
+    # --- SCP-iteration workload state
+    z = initial_guess(sc, gt.disc, lay)
+    z_dev = torch.as_tensor(z, device=dev)
+    delta = 1.0
+    scale_v, state_scale, u_scale = build_scaling(sc, lay)
+    scat = DynamicsScatter(gt.disc, lay, state_scale, u_scale, sc.s_nominal, dev)
+    r0 = gt.linearize_device(z_dev, delta)
+    pat = scat.build_pattern(r0["jx"].cpu().numpy(), r0["ju"].cpu().numpy(), r0["js"].cpu().numpy(),
+                             n_cols(lay, 3 * lay.n_c + lay.n_g_out), state_scale)
+    A_data = torch.as_tensor(pat.template_data(), device=dev)
+    b_dyn = torch.empty(pat.n_rows, dtype=torch.float64, device=dev)
+    n_int = lay.N - 1
+
+    k1_ev = []
+
+    def scp_step(zd, record=False):
+        if record:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            r = gt.linearize_device(zd, delta, k1_events=(e0, e1))
+            k1_ev.append((e0, e1))
+        else:
+            r = gt.linearize_device(zd, delta)
+        scat.scatter(r["ends"], r["jx"], r["ju"], r["js"], zd, A_data, b_dyn)
+        return r
+
+    # --- batch workload state
+    if args.workload == "batch" or not args.no_batch_extra:
+        B = args.batch
+        ok = lambda x, u, s: synth.well_posed(gt.disc.propagate_batch_device(
+            *(torch.as_tensor(a, device=dev) for a in (x, u, s)))[0].cpu().numpy())
+        xb, Ub, Sb, redrawn = synth.random_intervals(sc, B, seed=100 + rank, finite_fn=ok)
+        xb_d, Ub_d, Sb_d = (torch.as_tensor(a, device=dev) for a in (xb, Ub, Sb))
+        bout = gt.disc.linearize_batch_device(xb_d, Ub_d, Sb_d)
+
+    def batch_step(record=False):
+        if record:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+        gt.disc.linearize_batch_device(xb_d, Ub_d, Sb_d, out=bout)
+        if record:
+            e1.record(stream)
+            k1_ev.append((e0, e1))
+
+    def timed(step_fn, K, W):
+        for _ in range(W):
+            step_fn(False)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        k1_ev.clear()
+        evs = []
+        launches0 = gt.disc.launch_count()
+        for _ in range(K):
+            flush.zero_()  # L2 flush outside the timed events
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step_fn(True)
+            e1.record(stream)
+            evs.append((e0, e1))
+        torch.cuda.synchronize()
+        launches = gt.disc.launch_count() - launches0
+        ms = float(np.sum([a.elapsed_time(b) for a, b in evs]))
+        k1_ms = float(np.mean([a.elapsed_time(b) for a, b in k1_ev]))
+        if dist:
+            t = torch.tensor([ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+            dist.barrier()
+        return ms, k1_ms, launches
+
+    K, W = args.steps, max(3, args.warmup)
+    clocks = Clocks(dev.index if world == 1 else local)
+    if args.workload == "scp":
+        ms_tot, k1_ms, launches = timed(lambda rec: scp_step(z_dev, rec), K, W)
+        units_per_step, B_k1 = n_int, n_int
+    else:
+        ms_tot, k1_ms, launches = timed(batch_step, K, W)
+        units_per_step, B_k1 = args.batch, args.batch
+    clk = clocks.stop()
+    ms_per_step = ms_tot / K
+    value = world * units_per_step * K / (ms_tot * 1e-3)
+
+    extra = {}
+    if args.workload == "scp" and not args.no_batch_extra:
+        bms, bk1, _ = timed(batch_step, max(5, K // 5), 3)
+        nb = max(5, K // 5)
+        extra["batch_extra"] = {"workload": f"HalfCheetah synthetic batch of {args.batch} intervals (configs[2])",
+                                "value": args.batch * nb / (bms * 1e-3), "unit": UNIT, "ms_per_step": bms / nb,
+                                "k1_ms": bk1}
+
+    # --- e2e through the public API with host (pinned) buffers
+    if args.workload == "scp":
+        z_pin = torch.as_tensor(z).pin_memory()
+        outs = None
+
+        def e2e_step():
+            nonlocal outs
+            zd = z_pin.to(dev, non_blocking=True)
+            r = gt.linearize_device(zd, delta)
+            scat.scatter(r["ends"], r["jx"], r["ju"], r["js"], zd, A_data, b_dyn)
+            res = dict(r)
+            res["A_data"] = A_data
+            res["b"] = b_dyn
+            keys = ["ends", "jx", "ju", "js", "defects", "psi", "psi_jac", "theta", "theta_jac", "imp_v", "imp_jac",
+                    "A_data", "b", "bad"]
+            if outs is None:
+                outs = {k: torch.empty(res[k].shape, dtype=res[k].dtype, pin_memory=True) for k in keys}
+            for k in keys:
+                outs[k].copy_(res[k], non_blocking=True)
+            torch.cuda.current_stream(dev).synchronize()
+            return outs
+
+        e2e_step()
+        h2d = z.nbytes
+        d2h = int(sum(v.numel() * v.element_size() for v in outs.values()))
+    else:
+        xb_p, Ub_p, Sb_p = (torch.as_tensor(a).pin_memory() for a in (xb, Ub, Sb))
+        bouts = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in bout]
+
+        def e2e_step():
+            ins = [a.to(dev, non_blocking=True) for a in (xb_p, Ub_p, Sb_p)]
+            o = gt.disc.linearize_batch_device(*ins, out=bout)
+            for hb, db in zip(bouts, o):
+                hb.copy_(db, non_blocking=True)
+            torch.cuda.current_stream(dev).synchronize()
+
+        e2e_step()
+        h2d = xb.nbytes + Ub.nbytes + Sb.nbytes
+        d2h = int(sum(t.numel() * t.element_size() for t in bout))
+    for _ in range(W):
+        e2e_step()
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(K):
+        e2e_step()
+    e2e_s = time.perf_counter() - t0
+    if dist:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = world * units_per_step * K / e2e_s
+
+    peak = fp64_peak_tflops(torch, dev)
+    key = "halfcheetah_s5"
+    F, fdef = flops_per_interval(key)
+    achieved = F * B_k1 / (k1_ms * 1e-3) / 1e12 if F else None
+    roofline = {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": (achieved / peak) if achieved else None, "traffic": ncu_traffic(f"k_linearize_{args.workload}"),
+                "kernel": "k_linearize<Topo_halfcheetah_g2>", "kernel_ms": k1_ms, "intervals_per_launch": B_k1,
+                "flops_per_interval": F, "flops_definition": fdef,
+                "peak_source": "measured in this run: FP64 DFMA probe kernel (cito_dfma_peak); MEASURED_PEAKS.json "
+                               "has no fp64 entry"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        if args.workload == "scp":
+            step, po = cpu_step_fn(sc, 0)
+            sample = "HalfCheetah N=30 initial-guess SCP linearization (29 intervals + node relations), repeated"
+        else:
+            step, po = cpu_batch_fn(sc, 64)
+            sample = "64 synthetic HalfCheetah intervals per call, repeated"
+        v, n, dt = time_cpu(step, args.cpu_seconds)
+        cpu = {"value": v, "unit": UNIT, "cores": po.get_threads(), "kind": "port",
+               "sample": f"{sample}: {n} calls in {dt:.1f} s on {os.cpu_count()} host cores (oracle/cito_oracle.c, "
+                         "dense forward-mode dual numbers like the reference's jax.jacfwd)"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic" if args.workload == "batch" else "synthetic (scenario initial guess, seed=rank)",
+        "config": {"workload": ("scp: one SCP-iteration linearize of HalfCheetah N=30 (halfcheetah_bound.json, "
+                                "5 RKF substeps, 29 intervals; K1+K3+K4)") if args.workload == "scp" else
+                   f"batch: {args.batch} independent synthetic HalfCheetah intervals per GPU (configs[2])",
+                   "intervals_per_step_per_gpu": units_per_step, "l2": "flushed (256 MiB write) between timed steps",
+                   "parallelism": f"replicas x{world} (independent problems per rank, no collective)"},
+        "roofline": roofline, "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "ms_per_step": e2e_s / K * 1e3},
+        "gpu_launches": int(launches), "clocks": clk,
+    }
+    line.update(extra)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def run_reference(args):
+    rank, world, local = env_rank()
+    if rank != 0:
+        return
+    sc = scp_problem(seed=0)
+    if args.workload == "scp":
+        step, po = cpu_step_fn(sc, 0)
+        sample = "HalfCheetah N=30 initial-guess SCP linearization (29 intervals + node relations) per step"
+    else:
+        B = max(8, min(args.batch, 256))
+        step, po = cpu_batch_fn(sc, B)
+        sample = f"{B} synthetic HalfCheetah intervals per step (bounded sample of the {args.batch}-interval batch)"
+    for _ in range(max(1, args.warmup)):
+        step()
+    t0 = time.perf_counter()
+    units = 0
+    for _ in range(args.steps):
+        units += step()
+    dt = time.perf_counter() - t0
+    v = units / dt
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": args.workload, "note": "reference algorithm on host cores via the C oracle port; "
+                       "the reference's JAX runtime is not installable (no jax wheel, no network)"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": po.get_threads(), "kind": "port", "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -164,6 +164,11 @@ cito_status cito_scatter_dynamics_dev(cito_handle* h, int64_t n_int, const doubl
                                       const int32_t* slot_s, double* A_data, double* b_rows,
                                       int32_t* mismatch, void* stream);
 
+/* FP64 DFMA throughput probe (roofline denominator; not part of the reference
+ * interface).  Launches one kernel on `stream`; returns the flops it issues
+ * (time it with events on the same stream), or -1 on launch failure. */
+double cito_dfma_peak(int32_t iters, double* out_dev, void* stream);
+
 /* Number of kernel launches issued by this handle since creation (evidence
  * for bench.py's gpu_launches). */
 int64_t cito_launch_count(const cito_handle* h);

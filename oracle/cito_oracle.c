@@ -100,6 +100,14 @@ typedef struct {
 
 static __thread int ND; /* active directions */
 
+/* Algorithmic-flop counter: when enabled, every
+ * dual op counts the flops a structurally sparse forward mode executes -- the
+ * value flop(s) plus work only on tangent entries that are nonzero.  Counting
+ * convention: + - * / sqrt sin cos = 1, FMA = 2. */
+static __thread int COUNT;
+static __thread double FLOPS;
+static inline int nzd(const double* d, int i) { return d[i] != 0.0; }
+
 static inline dual dc(double c) {
   dual r;
   r.v = c;
@@ -107,28 +115,54 @@ static inline dual dc(double c) {
   return r;
 }
 static inline dual dadd(dual a, dual b) {
+  if (COUNT) {
+    FLOPS += 1;
+    for (int i = 0; i < ND; ++i) FLOPS += (nzd(a.d, i) && nzd(b.d, i));
+  }
   for (int i = 0; i < ND; ++i) a.d[i] += b.d[i];
   a.v += b.v;
   return a;
 }
 static inline dual dsub(dual a, dual b) {
+  if (COUNT) {
+    FLOPS += 1;
+    for (int i = 0; i < ND; ++i) FLOPS += (nzd(a.d, i) || nzd(b.d, i)) && nzd(b.d, i);
+  }
   for (int i = 0; i < ND; ++i) a.d[i] -= b.d[i];
   a.v -= b.v;
   return a;
 }
 static inline dual dmul(dual a, dual b) {
   dual r;
+  if (COUNT) {
+    FLOPS += 1;
+    for (int i = 0; i < ND; ++i) {
+      const int na = nzd(a.d, i), nb = nzd(b.d, i);
+      FLOPS += (na && nb) ? 3 : (na || nb);
+    }
+  }
   r.v = a.v * b.v;
   for (int i = 0; i < ND; ++i) r.d[i] = a.d[i] * b.v + a.v * b.d[i];
   return r;
 }
 static inline dual dscale(dual a, double c) {
+  if (COUNT) {
+    FLOPS += 1;
+    for (int i = 0; i < ND; ++i) FLOPS += nzd(a.d, i);
+  }
   a.v *= c;
   for (int i = 0; i < ND; ++i) a.d[i] *= c;
   return a;
 }
 static inline dual ddiv(dual a, dual b) {
   dual r;
+  if (COUNT) {
+    FLOPS += 2;
+    for (int i = 0; i < ND; ++i) {
+      const int na = nzd(a.d, i), nb = nzd(b.d, i);
+      FLOPS += nb ? 3 : na;
+    }
+  }
   r.v = a.v / b.v;
   double ib = 1.0 / b.v;
   for (int i = 0; i < ND; ++i) r.d[i] = (a.d[i] - r.v * b.d[i]) * ib;
@@ -136,6 +170,10 @@ static inline dual ddiv(dual a, dual b) {
 }
 static inline dual dsqrt(dual a) {
   dual r;
+  if (COUNT) {
+    FLOPS += 2;
+    for (int i = 0; i < ND; ++i) FLOPS += nzd(a.d, i);
+  }
   r.v = sqrt(a.v);
   double f = 0.5 / r.v;
   for (int i = 0; i < ND; ++i) r.d[i] = a.d[i] * f;
@@ -143,6 +181,10 @@ static inline dual dsqrt(dual a) {
 }
 static inline dual dsin(dual a) {
   dual r;
+  if (COUNT) {
+    FLOPS += 2;
+    for (int i = 0; i < ND; ++i) FLOPS += nzd(a.d, i);
+  }
   r.v = sin(a.v);
   double c = cos(a.v);
   for (int i = 0; i < ND; ++i) r.d[i] = a.d[i] * c;
@@ -150,6 +192,10 @@ static inline dual dsin(dual a) {
 }
 static inline dual dcos(dual a) {
   dual r;
+  if (COUNT) {
+    FLOPS += 2;
+    for (int i = 0; i < ND; ++i) FLOPS += nzd(a.d, i);
+  }
   r.v = cos(a.v);
   double s = -sin(a.v);
   for (int i = 0; i < ND; ++i) r.d[i] = a.d[i] * s;
@@ -811,3 +857,44 @@ void oracle_node_linearize(const cito_model_desc* m, int64_t Np, int64_t Nn, con
 }
 
 int oracle_max_directions(void) { return MAXD; }
+
+typedef struct {
+  const cito_model_desc* m;
+  int substeps;
+  const double *xt0, *U;
+  double S, flops;
+} count_ctx;
+
+static double count_flops_impl(const cito_model_desc* m, int substeps, const double* xt0, const double* U,
+                               double S);
+static void count_body(void* v, int64_t i) {
+  (void)i;
+  count_ctx* c = (count_ctx*)v;
+  c->flops = count_flops_impl(c->m, c->substeps, c->xt0, c->U, c->S);
+}
+
+/* structurally-sparse forward-mode flops of ONE interval linearization */
+double oracle_count_flops(const cito_model_desc* m, int substeps, const double* xt0, const double* U, double S) {
+  count_ctx c = {m, substeps, xt0, U, S, 0.0};
+  parallel_for(1, count_body, &c); /* worker thread: large stack */
+  return c.flops;
+}
+
+static double count_flops_impl(const cito_model_desc* m, int substeps, const double* xt0, const double* U,
+                               double S) {
+  int nq, nu, ny, nxt;
+  dims(m, &nq, &nu, &ny, &nxt);
+  double* end = (double*)malloc(sizeof(double) * nxt);
+  double* jx = (double*)malloc(sizeof(double) * nxt * nxt);
+  double* ju = (double*)malloc(sizeof(double) * nxt * 2 * nu + 8);
+  double* js = (double*)malloc(sizeof(double) * nxt);
+  COUNT = 1;
+  FLOPS = 0.0;
+  flow_interval(m, substeps, xt0, U, S, 1, end, jx, ju, js);
+  COUNT = 0;
+  free(end);
+  free(jx);
+  free(ju);
+  free(js);
+  return FLOPS;
+}

@@ -40,6 +40,11 @@ def lib():
         L.oracle_node_linearize.restype = None
         L.oracle_node_linearize.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, _dp, _dp,
                                             ctypes.c_double, ctypes.c_double, _dp, _dp, _dp, _dp, _dp, _dp]
+        L.oracle_count_flops.restype = ctypes.c_double
+        L.oracle_count_flops.argtypes = [ctypes.c_void_p, ctypes.c_int, _dp, _dp, ctypes.c_double]
+        L.oracle_set_threads.restype = ctypes.c_int
+        L.oracle_set_threads.argtypes = [ctypes.c_int]
+        L.oracle_get_threads.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -102,3 +107,20 @@ def node_linearize(desc, y_pairs, theta_vecs, delta, epsilon):
                                 float(epsilon), _p(psi), _p(psi_jac), _p(th), _p(th_jac), _p(imp),
                                 _p(imp_jac))
     return psi, psi_jac, th, th_jac, imp, imp_jac
+
+
+def count_flops(desc, substeps, xt0, U, S):
+    """Structurally-sparse forward-mode flops of one interval linearization."""
+    xt0 = np.ascontiguousarray(xt0, dtype=np.float64)
+    U = np.ascontiguousarray(U, dtype=np.float64).reshape(-1)
+    if U.size == 0:
+        U = np.zeros(1)
+    return float(lib().oracle_count_flops(ctypes.byref(desc), int(substeps), _p(xt0), _p(U), float(S)))
+
+
+def set_threads(n):
+    return lib().oracle_set_threads(int(n))
+
+
+def get_threads():
+    return lib().oracle_get_threads()

@@ -16,6 +16,7 @@
 #include "cito_kernels.cuh"
 #include "cito_node.cuh"
 #include "cito_scatter.cuh"
+#include "cito_bench.cuh"
 
 namespace {
 
@@ -399,6 +400,16 @@ cito_status cito_scatter_dynamics_dev(cito_handle* h, int64_t n_int, const doubl
   CUDA_TRY(cudaGetLastError());
   __atomic_add_fetch(&h->launches, 1, __ATOMIC_RELAXED);
   return CITO_OK;
+}
+
+double cito_dfma_peak(int32_t iters, double* out_dev, void* stream) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int blocks = sms * 8, threads = 256;
+  k_dfma_peak<<<blocks, threads, 0, (cudaStream_t)stream>>>(iters, 1.0, out_dev);
+  if (cudaGetLastError() != cudaSuccess) return -1.0;
+  return 2.0 * 64.0 * (double)iters * blocks * threads;  // flops issued
 }
 
 }  // extern "C"

@@ -18,7 +18,8 @@ import numpy as np
 from . import _lib
 from .discretizer import Discretizer
 
-__all__ = ["node_inputs", "LinearizedProblem", "GpuTranscription", "linearize_all", "NodeLinearizer"]
+__all__ = ["node_inputs", "LinearizedProblem", "GpuTranscription", "linearize_all", "NodeLinearizer",
+           "initial_guess"]
 
 
 def node_inputs(lay, z):
@@ -131,14 +132,21 @@ class GpuTranscription:
         self._i_yp, self._i_th = t(idx_yp), t(idx_th)
         self.n_imp = 3 * n_q + 2 * lay.n_c
 
-    def linearize_device(self, z_dev, delta, epsilon=None):
-        """Everything on the device; returns a dict of torch tensors."""
+    def linearize_device(self, z_dev, delta, epsilon=None, k1_events=None):
+        """Everything on the device; returns a dict of torch tensors.  ``k1_events``
+        = (start, end) CUDA events recorded around the interval kernel (K1)."""
+        import torch
+
         if epsilon is None:
             epsilon = self.scenario.ctcs_epsilon
         starts = z_dev[self._i_start]
         Us = z_dev[self._i_u]
         Ss = z_dev[self._i_s]
+        if k1_events is not None:
+            k1_events[0].record(torch.cuda.current_stream(self.device))
         ends, jx, ju, js, bad = self.disc.linearize_batch_device(starts, Us, Ss)
+        if k1_events is not None:
+            k1_events[1].record(torch.cuda.current_stream(self.device))
         defects = z_dev[self._i_end] - ends
         y_pairs = z_dev[self._i_yp]
         theta_vecs = z_dev[self._i_th]
@@ -162,6 +170,57 @@ class GpuTranscription:
         return LP(z_ref=z.copy(), ends=host["ends"], jx=host["jx"], ju=host["ju"], js=host["js"],
                   defects=host["defects"], psi=host["psi"], psi_jac=host["psi_jac"], theta=host["theta"],
                   theta_jac=host["theta_jac"], imp_v=host["imp_v"], imp_jac=host["imp_jac"])
+
+
+def initial_guess(scenario, disc, lay=None, seed=None):
+    """Transcription.initial_guess (cito/ocp.py:461-505) with the y forward pass on the GPU.
+
+    Same RNG draw order as the reference, so U/S/impulses are bit-identical; the
+    auxiliary channels come from the N-1 sequential K2 propagations."""
+    from .scenario import Layout
+
+    sc = scenario
+    lay = lay or Layout(sc)
+    model = sc.model
+    rng = np.random.default_rng(sc.seed if seed is None else seed)
+    n_q = lay.n_q
+    z = np.zeros(lay.dim)
+    q_i, q_f = sc.x_init[:n_q], sc.x_final[:n_q]
+    for k in range(lay.N):
+        frac = k / (lay.N - 1)
+        pose = (1.0 - frac) * q_i + frac * q_f
+        z[lay.xm(k)[:n_q]] = pose
+        z[lay.xp(k)[:n_q]] = pose
+    for k in range(lay.N - 1):
+        u = np.zeros(2 * lay.n_u)
+        for side in range(2):
+            base = side * lay.n_u + lay.n_a
+            for i in range(lay.n_c):
+                mu = model.contacts[i].friction_mu
+                fn = rng.uniform(0.0, sc.guess_force_scale)
+                ft = rng.uniform(-mu * fn, mu * fn) if fn > 0 else 0.0
+                u[base + 2 * i] = ft
+                u[base + 2 * i + 1] = fn
+        z[lay.u(k)] = u
+        z[lay.s(k)] = sc.s_nominal
+    for k in range(lay.N):
+        blk = np.zeros(2 * lay.n_c)
+        for i in range(lay.n_c):
+            mu = model.contacts[i].friction_mu
+            pn = rng.uniform(0.0, sc.guess_impulse_scale) if sc.guess_impulse_scale else 0.0
+            pt = rng.uniform(-mu * pn, mu * pn) if pn > 0 else 0.0
+            blk[2 * i] = pt
+            blk[2 * i + 1] = pn
+        z[lay.phi(k)] = blk
+    z[lay.y_of_xm(0)] = np.zeros(lay.n_y)
+    for k in range(lay.N):
+        z[lay.y_of_xp(k)] = z[lay.y_of_xm(k)]
+        if k == lay.N - 1:
+            break
+        start = np.concatenate([z[lay.xp(k)][: 2 * n_q], z[lay.y_of_xp(k)]])
+        end = disc.propagate(start, z[lay.u(k)].reshape(2, -1), float(z[lay.s(k)][0]))
+        z[lay.y_of_xm(k + 1)] = end[2 * n_q:]
+    return z
 
 
 _cache = {}

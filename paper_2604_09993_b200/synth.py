@@ -11,6 +11,18 @@ Dilation S = s_nom * U(0.5, 2), inside the default bounds [0.2, 5] s_nom (ocp.py
 import numpy as np
 
 
+DIVERGED = 1e6  # |end state| above this = the fixed-step integration blew up
+
+
+def well_posed(ends):
+    """Accept mask for random draws: finite and not diverged.  Random states of the
+    joint-constrained models at large dilation can make the explicit RK flow blow
+    up to |x| ~ 1e20..1e300 while staying finite; such intervals are chaotic
+    (rounding is amplified by ||Phi|| ~ 1e30+) and carry no parity information."""
+    ends = np.asarray(ends)
+    return np.all(np.isfinite(ends), axis=1) & (np.max(np.abs(np.nan_to_num(ends, nan=np.inf)), axis=1) < DIVERGED)
+
+
 def random_intervals(scenario, B, seed=0, finite_fn=None, max_rounds=50):
     """Seeded synthetic batch.  ``finite_fn(xt0, U, S) -> bool mask`` (e.g. a GPU
     propagate) triggers re-drawing of intervals whose end state is non-finite

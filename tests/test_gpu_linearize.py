@@ -56,8 +56,8 @@ def test_linearize_vs_oracle_batch(name, B):
 
     sc = golden_scenario(name)
     desc = scenario_desc(sc)
-    xt0, U, S, _ = synth.random_intervals(
-        sc, B, seed=11, finite_fn=lambda x, u, s: pyoracle.propagate(desc, sc.substeps, x, u, s)[1] == 0)
+    xt0, U, S, _ = synth.random_intervals(sc, B, seed=11, finite_fn=lambda x, u, s: synth.well_posed(
+        pyoracle.propagate(desc, sc.substeps, x, u, s)[0]))
     e0, jx0, ju0, js0, bad = pyoracle.linearize(desc, sc.substeps, xt0, U, S)
     e, jx, ju, js = _disc(sc).linearize_batch(xt0, U, S)
     worst = 0.0

@@ -1,0 +1,123 @@
+"""CSC scatter of the multiple-shooting rows (K4) vs the reference's own
+build_subproblem -> canonicalize output (golden, tests/golden/make_golden.py).
+Pattern/indices must be bit-exact; values rel <= 1e-9."""
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from conftest import golden_scenario, load_golden, rel_err
+
+CASES = ["pointmass_rest", "monoped_n20", "halfcheetah_n30"]
+
+
+def _ref_dyn(g, lay):
+    A = sp.csc_matrix((g["csc_A_data"], g["csc_A_indices"], g["csc_A_indptr"]), shape=tuple(g["csc_A_shape"]))
+    n_dyn = int(g["csc_n_dyn_rows"])
+    Ad = A[:n_dyn, :].tocsc()
+    Ad.sort_indices()
+    return A, Ad, n_dyn
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_pattern_matches_reference_csc(name):
+    from paper_2604_09993_b200.scatter import DynamicsCSC, n_cols
+    from paper_2604_09993_b200.scenario import Layout, build_scaling
+
+    g = load_golden(name)
+    sc = golden_scenario(name)
+    lay = Layout(sc)
+    A, Ad, n_dyn = _ref_dyn(g, lay)
+    n_psi = 3 * lay.n_c + lay.n_g_out
+    assert n_cols(lay, n_psi) == A.shape[1]
+    _, state_scale, _ = build_scaling(sc, lay)
+    pat = DynamicsCSC(lay, A.shape[1], state_scale, g["ig_jx"] != 0, g["ig_ju"] != 0, g["ig_js"] != 0)
+    assert np.array_equal(pat.indptr, Ad.indptr.astype(np.int32))
+    assert np.array_equal(pat.indices, Ad.indices.astype(np.int32))
+    # constant entries carry exactly the reference values
+    data = pat.template_data()
+    assert np.array_equal(data[pat.const_pos], Ad.data[pat.const_pos])
+    # slots into the full reference A agree with the pattern's own ordering
+    sx, su, ss = DynamicsCSC.slots_into(A.indptr, A.indices, lay)
+    assert ((sx >= 0) == pat.slot_x.__ge__(0)).all() and ((su >= 0) == (pat.slot_u >= 0)).all()
+    # host restatement of the values, exactly as scp.py:186-201 computes them
+    _, sx_, su_ = build_scaling(sc, lay)
+    vx = -g["ig_jx"] * state_scale[None, None, :]
+    assert np.array_equal(A.data[sx[sx >= 0]], vx[sx >= 0])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", CASES)
+def test_gpu_scatter_values_match_reference(name):
+    import torch
+
+    from paper_2604_09993_b200.linearize import GpuTranscription
+    from paper_2604_09993_b200.scatter import DynamicsCSC, DynamicsScatter
+    from paper_2604_09993_b200.scenario import Layout, build_scaling
+
+    g = load_golden(name)
+    sc = golden_scenario(name)
+    gt = GpuTranscription(sc)
+    lay = gt.lay
+    A, Ad, n_dyn = _ref_dyn(g, lay)
+    scale_v, state_scale, u_scale = build_scaling(sc, lay)
+    dev = gt.device
+    z = torch.as_tensor(g["ig_z"], device=dev)
+    r = gt.linearize_device(z, float(g["ig_delta"]))
+    scat = DynamicsScatter(gt.disc, lay, state_scale, u_scale, sc.s_nominal, dev)
+    pat = scat.build_pattern(r["jx"].cpu().numpy(), r["ju"].cpu().numpy(), r["js"].cpu().numpy(), A.shape[1],
+                             state_scale)
+    assert np.array_equal(pat.indices, Ad.indices) and np.array_equal(pat.indptr, Ad.indptr)
+    data = torch.as_tensor(pat.template_data(), device=dev)
+    b = torch.empty(n_dyn, dtype=torch.float64, device=dev)
+    mm = scat.scatter(r["ends"], r["jx"], r["ju"], r["js"], z, data, b)
+    torch.cuda.synchronize()
+    assert int(mm.item()) == 0
+    assert rel_err(data.cpu().numpy(), Ad.data) <= 1e-9
+    assert rel_err(b.cpu().numpy(), g["csc_b"][:n_dyn]) <= 1e-9
+    # and straight into the reference's full A.data (other rows untouched)
+    sx, su, ss = DynamicsCSC.slots_into(A.indptr, A.indices, lay)
+    scat.set_slots(sx, su, ss)
+    full = torch.as_tensor(A.data.copy(), device=dev)
+    keep = full.clone()
+    mm = scat.scatter(r["ends"], r["jx"], r["ju"], r["js"], z, full, b)
+    torch.cuda.synchronize()
+    assert int(mm.item()) == 0
+    assert rel_err(full.cpu().numpy(), A.data) <= 1e-9
+    touched = np.zeros(A.data.size, bool)
+    for s_ in (sx, su, ss):
+        touched[s_[s_ >= 0]] = True
+    assert np.array_equal(full.cpu().numpy()[~touched], keep.cpu().numpy()[~touched])
+
+
+@pytest.mark.gpu
+def test_linearize_all_matches_reference_golden():
+    """GpuTranscription.linearize_all == cito.scp.linearize_all at the initial guess."""
+    from paper_2604_09993_b200.linearize import GpuTranscription
+
+    for name in ["pointmass_rest", "monoped_n20", "halfcheetah_n30", "biped_walk"]:
+        g = load_golden(name)
+        gt = GpuTranscription(golden_scenario(name))
+        lin = gt.linearize_all(g["ig_z"], float(g["ig_delta"]))
+        for f, k in (("ends", "ig_ends"), ("jx", "ig_jx"), ("ju", "ig_ju"), ("js", "ig_js"),
+                     ("defects", "ig_defects"), ("psi", "ig_psi"), ("psi_jac", "ig_psi_jac"),
+                     ("theta", "ig_theta"), ("theta_jac", "ig_theta_jac"), ("imp_v", "ig_imp"),
+                     ("imp_jac", "ig_imp_jac")):
+            assert rel_err(getattr(lin, f), g[k]) <= 1e-9, (name, f)
+        with pytest.raises(FloatingPointError):
+            gt.linearize_all(np.full_like(g["ig_z"], np.nan), 1.0)
+
+
+@pytest.mark.gpu
+def test_node_relations_random_z_vs_reference():
+    import torch
+
+    from paper_2604_09993_b200.linearize import GpuTranscription, node_inputs
+
+    for name in ["pointmass_rest", "monoped_n20", "halfcheetah_n30", "biped_walk"]:
+        g = load_golden(name)
+        gt = GpuTranscription(golden_scenario(name))
+        yp, tv = node_inputs(gt.lay, g["nd_z"])
+        out = gt.nodes.host(yp, tv, float(g["nd_delta"]), gt.scenario.ctcs_epsilon)
+        for a, k in zip(out, ("psi", "psi_jac", "theta", "theta_jac", "imp", "imp_jac")):
+            assert rel_err(a, g["nd_" + k]) <= 1e-9, (name, k)
