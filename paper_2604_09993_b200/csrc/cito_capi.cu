@@ -53,18 +53,50 @@ struct TopoOps {
                       double*, double*, double*, double*, double*, cudaStream_t);
 };
 
+// Stream-ordered workspace (records of the primal trajectory): allocated from
+// the device's default memory pool with a high release threshold, so repeated
+// calls reuse the same memory and concurrent calls on different streams never
+// share a buffer.
+cito_status ensure_pool() {
+  static std::once_flag once;
+  static cudaError_t err = cudaSuccess;
+  std::call_once(once, [] {
+    int dev = 0;
+    cudaMemPool_t pool;
+    err = cudaGetDevice(&dev);
+    if (err == cudaSuccess) err = cudaDeviceGetDefaultMemPool(&pool, dev);
+    uint64_t thr = ~0ull;
+    if (err == cudaSuccess) err = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  });
+  if (err != cudaSuccess) return fail(CITO_ERR_CUDA, std::string("mempool: ") + cudaGetErrorString(err));
+  return CITO_OK;
+}
+
 template <class M>
 cito_status launch_linearize(const KParams& P, int64_t B, const double* xt0s, const double* Us, const double* Ss,
                              double* ends, double* jx, double* ju, double* js, int32_t* bad, cudaStream_t st) {
   if (B <= 0) return CITO_OK;
-  const size_t smem = sizeof(LinShared<M>);
+  cito_status cs = ensure_pool();
+  if (cs != CITO_OK) return cs;
+  const size_t smem = sizeof(TanShared<M>);
   static bool attr_done = false;
   if (!attr_done) {
-    CUDA_TRY(cudaFuncSetAttribute(k_linearize<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CUDA_TRY(cudaFuncSetAttribute(k_tangent<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr_done = true;
   }
-  k_linearize<M><<<(unsigned)B, Dims<M>::NT, smem, st>>>(P, B, xt0s, Us, Ss, ends, jx, ju, js, bad);
+  const size_t nrec = (size_t)B * 6 * P.substeps;
+  const size_t bytes_rec = nrec * sizeof(Rec<M>);
+  const size_t bytes_vb = (size_t)B * P.substeps * Dims<M>::NQ * sizeof(double);
+  void* ws = nullptr;
+  CUDA_TRY(cudaMallocAsync(&ws, bytes_rec + bytes_vb, st));
+  Rec<M>* rec = (Rec<M>*)ws;
+  double* vb = (double*)((char*)ws + bytes_rec);
+  const int nt = 64;
+  k_primal<M, true><<<(unsigned)((B + nt - 1) / nt), nt, 0, st>>>(P, B, xt0s, Us, Ss, ends, bad, rec, vb);
   CUDA_TRY(cudaGetLastError());
+  k_tangent<M><<<(unsigned)B, Dims<M>::NT, smem, st>>>(P, B, Us, Ss, rec, vb, jx, ju, js);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaFreeAsync(ws, st));
   return CITO_OK;
 }
 
@@ -72,8 +104,8 @@ template <class M>
 cito_status launch_propagate(const KParams& P, int64_t B, const double* xt0s, const double* Us, const double* Ss,
                              double* ends, int32_t* bad, cudaStream_t st) {
   if (B <= 0) return CITO_OK;
-  const int nt = 128;
-  k_propagate<M><<<(unsigned)((B + nt - 1) / nt), nt, 0, st>>>(P, B, xt0s, Us, Ss, ends, bad);
+  const int nt = 64;
+  k_primal<M, false><<<(unsigned)((B + nt - 1) / nt), nt, 0, st>>>(P, B, xt0s, Us, Ss, ends, bad, nullptr, nullptr);
   CUDA_TRY(cudaGetLastError());
   return CITO_OK;
 }

@@ -57,6 +57,8 @@ struct KParams {
   double expr_arg[KMAX_E];
 };
 
+#define LI(r, c) ((r) * ((r) + 1) / 2 + (c))
+
 template <int N>
 struct Pos {
   static constexpr int v = N > 0 ? N : 1;
@@ -145,7 +147,7 @@ struct Prim {
   static constexpr int NG = M::NC + 2 * M::NJL + 2 * M::NHB;
   double c[NL], s[NL];
   double rp[Pos<M::NJ>::v][2], rc[Pos<M::NJ>::v][2];  // R(theta) * (anchor - com)
-  double L[NJ2][NJ2];                                 // Cholesky factor of the Gram matrix
+  double L[NJ2 * (NJ2 + 1) / 2];                      // packed lower Cholesky factor of the Gram matrix
   double lam[NJ2];                                    // joint reactions (phi_j)
   double vdot[3 * M::NL];
   double rr[NC][2], n[NC][2], t[NC][2], F[NC][2], Jv[NC][2];
@@ -307,16 +309,16 @@ __device__ void prim_rate(const KParams& P, const double* xs, const double* u, P
     for (int cc = 0; cc < NJ2; ++cc) {
       double d = G[cc][cc];
 #pragma unroll
-      for (int k = 0; k < cc; ++k) d -= pr.L[cc][k] * pr.L[cc][k];
+      for (int k = 0; k < cc; ++k) d -= pr.L[LI(cc, k)] * pr.L[LI(cc, k)];
       const double lcc = sqrt(d);
-      pr.L[cc][cc] = lcc;
+      pr.L[LI(cc, cc)] = lcc;
       const double il = 1.0 / lcc;
 #pragma unroll
       for (int r = cc + 1; r < NJ2; ++r) {
         double x = G[r][cc];
 #pragma unroll
-        for (int k = 0; k < cc; ++k) x -= pr.L[r][k] * pr.L[cc][k];
-        pr.L[r][cc] = x * il;
+        for (int k = 0; k < cc; ++k) x -= pr.L[LI(r, k)] * pr.L[LI(cc, k)];
+        pr.L[LI(r, cc)] = x * il;
       }
     }
     double y[NJ2];
@@ -324,15 +326,15 @@ __device__ void prim_rate(const KParams& P, const double* xs, const double* u, P
     for (int r = 0; r < NJ2; ++r) {
       double x = rhs[r];
 #pragma unroll
-      for (int k = 0; k < r; ++k) x -= pr.L[r][k] * y[k];
-      y[r] = x / pr.L[r][r];
+      for (int k = 0; k < r; ++k) x -= pr.L[LI(r, k)] * y[k];
+      y[r] = x / pr.L[LI(r, r)];
     }
 #pragma unroll
     for (int r = NJ2 - 1; r >= 0; --r) {
       double x = y[r];
 #pragma unroll
-      for (int k = r + 1; k < NJ2; ++k) x -= pr.L[k][r] * y[k];
-      y[r] = x / pr.L[r][r];
+      for (int k = r + 1; k < NJ2; ++k) x -= pr.L[LI(k, r)] * y[k];
+      y[r] = x / pr.L[LI(r, r)];
     }
 #pragma unroll
     for (int r = 0; r < NJ2; ++r) pr.lam[r] = -y[r];
@@ -414,12 +416,9 @@ __device__ void prim_rate(const KParams& P, const double* xs, const double* u, P
 //   dir in [0, NQ) -> q_dir, [NQ, 2NQ) -> v, [2NQ, 2NQ+NU) -> u.
 // Writes out[0:NQ] = d vdot, out[NQ:NQ+NY] = d Omega.
 template <class M>
-__device__ void tan_rate(const KParams& P, const Prim<M>& pr, const double* xs, int dir, double* out,
+__device__ void tan_rate(const KParams& P, const Prim<M>& pr, const double* v, int dir, double* out,
                          int ostride) {
   constexpr int NL = M::NL, NJ = M::NJ, NC = M::NC, NA = M::NA, NQ = 3 * NL, NX = 2 * NQ;
-  const double* q = xs;
-  const double* v = xs + NQ;
-  (void)q;
 #define SQ(k) ((dir) == (k) ? 1.0 : 0.0)
 #define SV(k) ((dir) == NQ + (k) ? 1.0 : 0.0)
 #define SU(m) ((dir) == NX + (m) ? 1.0 : 0.0)
@@ -517,15 +516,15 @@ __device__ void tan_rate(const KParams& P, const Prim<M>& pr, const double* xs, 
     for (int r = 0; r < NJ2; ++r) {
       double x = z[r];
 #pragma unroll
-      for (int k = 0; k < r; ++k) x -= pr.L[r][k] * z[k];
-      z[r] = x / pr.L[r][r];
+      for (int k = 0; k < r; ++k) x -= pr.L[LI(r, k)] * z[k];
+      z[r] = x / pr.L[LI(r, r)];
     }
 #pragma unroll
     for (int r = NJ2 - 1; r >= 0; --r) {
       double x = z[r];
 #pragma unroll
-      for (int k = r + 1; k < NJ2; ++k) x -= pr.L[k][r] * z[k];
-      z[r] = x / pr.L[r][r];
+      for (int k = r + 1; k < NJ2; ++k) x -= pr.L[LI(k, r)] * z[k];
+      z[r] = x / pr.L[LI(r, r)];
     }
     // dvdot = M^-1 (g + J^T dlam)
 #pragma unroll
@@ -606,68 +605,144 @@ __device__ void tan_rate(const KParams& P, const Prim<M>& pr, const double* xs, 
 #undef SU
 }
 
+
 template <class M>
 struct Dims {
   static constexpr int NL = M::NL, NQ = 3 * NL, NX = 2 * NQ, NC = M::NC, NA = M::NA;
   static constexpr int NU = NA + 3 * NC, NY = 5 * NC + M::NGO, NXT = NX + NY;
-  static constexpr int NCOL = NX + 2 * NU + 1;       // non-y tangent columns
-  static constexpr int NDIR = M::NDIRX + NU;         // rate-Jacobian input directions
-  static constexpr int NR = NQ + NY;                 // rate rows with a non-trivial Jacobian
-  static constexpr int NCOLP = NCOL | 1;             // odd stride (bank spread)
+  static constexpr int NCOL = NX + 2 * NU + 1;  // non-y tangent columns: x~+ (q,v), U-, U+, S
+  static constexpr int NDIR = M::NDIRX + NU;    // rate-Jacobian input directions
+  static constexpr int NR = NQ + NY;            // rate rows with a non-trivial Jacobian (vdot, Omega)
+  static constexpr int NCOLP = NCOL | 1;        // odd column stride (bank spread)
+  static constexpr int NH = Pos<M::NHIST>::v;
   static constexpr int NT = ((NCOL > NDIR ? NCOL : NDIR) + 31) / 32 * 32;
 };
 
-// Shared state of one interval in the linearize kernel
+// Per-stage record of the primal trajectory: everything the tangent kernel needs
+// to form the rate Jacobian of that stage and the dS terms, so K1b never
+// recomputes (or waits on) the primal chain.
 template <class M>
-struct LinShared {
-  using D = Dims<M>;
+struct Rec {
   Prim<M> pr;
-  double x[D::NXT];
-  double xs[D::NX];
-  double r[D::NXT];
-  double K[6][D::NX];
-  double VS[6][D::NQ];
-  double kyacc[Pos<D::NY>::v];
-  double wq[D::NQ];
-  double vb[D::NQ];
-  double U[2 * D::NU + 1];
-  double A[D::NR][D::NDIR];
-  double KV[5][D::NQ][D::NCOLP];
-  double S;
-  int bad;
+  double vs[3 * M::NL];       // stage-input velocities
+  double r[Dims<M>::NR];      // unscaled rate rows: vdot (NQ), Omega (NY)
+  double wq[3 * M::NL];       // sum_j h a_ij v_{s,j}: dS term of the q-row stage inputs
 };
 
 // ---------------------------------------------------------------------------
-// K1: one CTA per interval.  Thread 0 runs the primal stage chain; threads
-// < NDIR form the rate Jacobian; threads < NCOL advance tangent columns.
+// K1a / K2: primal RKF flow, one thread per interval (cito/augmentation.py:195-211).
+// REC=true also writes the per-stage records (rec) and the per-substep
+// h*sum_i b_i v_{s,i} (vb) consumed by K1b.
+template <class M, bool REC>
+__global__ void __launch_bounds__(64) k_primal(const KParams P, int64_t B, const double* __restrict__ xt0s,
+                                               const double* __restrict__ Us, const double* __restrict__ Ss,
+                                               double* __restrict__ ends, int32_t* __restrict__ bad,
+                                               Rec<M>* __restrict__ rec, double* __restrict__ vb) {
+  using D = Dims<M>;
+  constexpr int NQ = D::NQ, NX = D::NX, NU = D::NU, NY = D::NY, NXT = D::NXT, NR = D::NR;
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  double x[NXT], xs[NX], r[NXT], K[6][NX], ky[Pos<NY>::v], U[2 * NU + 1], VS[6][NQ];
+  Prim<M> pr;
+  for (int k = 0; k < NXT; ++k) x[k] = xt0s[b * NXT + k];
+  for (int k = 0; k < 2 * NU; ++k) U[k] = Us[b * 2 * NU + k];
+  const double S = Ss[b];
+  const double h = P.h;
+  const int nst = 6 * P.substeps;
+  for (int s = 0; s < P.substeps; ++s) {
+    const double tau0 = h * (double)s;
+#pragma unroll
+    for (int k = 0; k < NY; ++k) ky[k] = 0.0;
+    for (int i = 0; i < 6; ++i) {
+      const double tau = tau0 + P.ch[i];
+      for (int k = 0; k < NX; ++k) {
+        double a = x[k];
+        for (int j = 0; j < i; ++j) a = a + P.ha[i][j] * K[j][k];
+        xs[k] = a;
+      }
+      double u[NU > 0 ? NU : 1];
+#pragma unroll
+      for (int m = 0; m < NU; ++m) u[m] = (1.0 - tau) * U[m] + tau * U[NU + m];  // foh_eval :166-169
+      prim_rate<M>(P, xs, u, pr, r);
+      for (int k = 0; k < NX; ++k) K[i][k] = S * r[k];
+#pragma unroll
+      for (int k = 0; k < NY; ++k) ky[k] += P.b[i] * (S * r[NX + k]);
+      if (REC) {
+        Rec<M>& R = rec[b * nst + s * 6 + i];
+        R.pr = pr;
+        for (int k = 0; k < NQ; ++k) {
+          VS[i][k] = xs[NQ + k];
+          R.vs[k] = xs[NQ + k];
+          double w = 0.0;
+          for (int j = 0; j < i; ++j) w += P.ha[i][j] * VS[j][k];
+          R.wq[k] = w;
+        }
+        for (int k = 0; k < NR; ++k) R.r[k] = r[NQ + k];
+      }
+    }
+    for (int k = 0; k < NX; ++k) {
+      double inc = 0.0;
+      for (int j = 0; j < 6; ++j) inc += P.b[j] * K[j][k];
+      x[k] = x[k] + h * inc;
+    }
+#pragma unroll
+    for (int k = 0; k < NY; ++k) x[NX + k] = x[NX + k] + h * ky[k];
+    if (REC) {
+      for (int k = 0; k < NQ; ++k) {
+        double w = 0.0;
+        for (int j = 0; j < 6; ++j) w += P.b[j] * VS[j][k];
+        vb[(b * P.substeps + s) * NQ + k] = h * w;
+      }
+    }
+  }
+  int nb = 0;
+  for (int k = 0; k < NXT; ++k) {
+    ends[b * NXT + k] = x[k];
+    nb |= !isfinite(x[k]);
+  }
+  if (bad) bad[b] = nb;
+}
+
 template <class M>
-__global__ void __launch_bounds__(Dims<M>::NT) k_linearize(const KParams P, int64_t B, const double* __restrict__ xt0s,
-                                                          const double* __restrict__ Us, const double* __restrict__ Ss,
-                                                          double* __restrict__ ends, double* __restrict__ jx,
-                                                          double* __restrict__ ju, double* __restrict__ js,
-                                                          int32_t* __restrict__ bad) {
+struct TanShared {
+  using D = Dims<M>;
+  Rec<M> rec;
+  double A[D::NR][D::NDIR];
+  double KV[5][D::NH][D::NCOLP];
+  double vbs[D::NQ];
+  double U[2 * D::NU + 1];
+  double S;
+};
+
+// ---------------------------------------------------------------------------
+// K1b: tangent columns of the interval map, one CTA per interval.  Per stage:
+// threads < NDIR form one column each of the rate Jacobian (tan_rate), then
+// threads < NCOL advance one tangent column each through the stage recursion.
+// Only coordinates the rate Jacobian reads keep velocity-row stage history
+// (M::hslot); all other rows are accumulated in push form.
+template <class M>
+__global__ void __launch_bounds__(Dims<M>::NT) k_tangent(const KParams P, int64_t B, const double* __restrict__ Us,
+                                                        const double* __restrict__ Ss,
+                                                        const Rec<M>* __restrict__ rec,
+                                                        const double* __restrict__ vb, double* __restrict__ jx,
+                                                        double* __restrict__ ju, double* __restrict__ js) {
   using D = Dims<M>;
   constexpr int NQ = D::NQ, NX = D::NX, NU = D::NU, NY = D::NY, NXT = D::NXT, NCOL = D::NCOL, NR = D::NR;
+  constexpr int NDIRX = M::NDIRX, NDIR = D::NDIR;
+  constexpr int RECD = sizeof(Rec<M>) / sizeof(double);
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  LinShared<M>& sh = *reinterpret_cast<LinShared<M>*>(smem_raw);
+  TanShared<M>& sh = *reinterpret_cast<TanShared<M>*>(smem_raw);
   const int64_t b = blockIdx.x;
   if (b >= B) return;
   const int tid = threadIdx.x;
-  for (int k = tid; k < NXT; k += blockDim.x) sh.x[k] = xt0s[b * NXT + k];
   for (int k = tid; k < 2 * NU; k += blockDim.x) sh.U[k] = Us[b * 2 * NU + k];
-  if (tid == 0) {
-    sh.S = Ss[b];
-#pragma unroll
-    for (int k = 0; k < (NY > 0 ? NY : 1); ++k) sh.kyacc[k] = 0.0;
-  }
+  if (tid == 0) sh.S = Ss[b];
   __syncthreads();
   const double S = sh.S;
-
-  // column state (registers): seed = unit column of [x~+ | U | S]
   const bool colthr = tid < NCOL;
   const int col = tid;
   const double dS = (col == NCOL - 1) ? 1.0 : 0.0;
-  const int uj = col - NX;  // U column index if 0 <= uj < 2NU
+  const int uj = col - NX;
   const bool isU = (uj >= 0) && (uj < 2 * NU);
   const int um = isU ? (uj % Pos<NU>::v) : 0;
   const bool uplus = isU && (uj >= NU);
@@ -679,117 +754,84 @@ __global__ void __launch_bounds__(Dims<M>::NT) k_linearize(const KParams P, int6
   }
 #pragma unroll
   for (int k = 0; k < NY; ++k) dy[k] = 0.0;
-
   const double h = P.h;
+  const int nst = 6 * P.substeps;
   for (int s = 0; s < P.substeps; ++s) {
     const double tau0 = h * (double)s;
     for (int i = 0; i < 6; ++i) {
       const double tau = tau0 + P.ch[i];
-      // ---- primal stage (cito/augmentation.py:200-208)
-      if (tid == 0) {
-#pragma unroll
-        for (int k = 0; k < NX; ++k) {
-          double a = sh.x[k];
-          for (int j = 0; j < i; ++j) a = a + P.ha[i][j] * sh.K[j][k];
-          sh.xs[k] = a;
-        }
-#pragma unroll
-        for (int k = 0; k < NQ; ++k) {
-          sh.VS[i][k] = sh.xs[NQ + k];
-          double w = 0.0;
-          for (int j = 0; j < i; ++j) w += P.ha[i][j] * sh.VS[j][k];
-          sh.wq[k] = w;
-        }
-        double u[NU > 0 ? NU : 1];
-#pragma unroll
-        for (int m = 0; m < NU; ++m) u[m] = (1.0 - tau) * sh.U[m] + tau * sh.U[NU + m];  // foh_eval :166-169
-        prim_rate<M>(P, sh.xs, u, sh.pr, sh.r);
-#pragma unroll
-        for (int k = 0; k < NX; ++k) sh.K[i][k] = S * sh.r[k];
-#pragma unroll
-        for (int k = 0; k < NY; ++k) sh.kyacc[k] += P.b[i] * (S * sh.r[NX + k]);
-        if (i == 5) {
-#pragma unroll
-          for (int k = 0; k < NQ; ++k) {
-            double w = 0.0;
-            for (int j = 0; j < 6; ++j) w += P.b[j] * sh.VS[j][k];
-            sh.vb[k] = h * w;
-          }
-#pragma unroll
-          for (int k = 0; k < NX; ++k) {
-            double inc = 0.0;
-            for (int j = 0; j < 6; ++j) inc += P.b[j] * sh.K[j][k];
-            sh.x[k] = sh.x[k] + h * inc;
-          }
-#pragma unroll
-          for (int k = 0; k < NY; ++k) {
-            sh.x[NX + k] = sh.x[NX + k] + h * sh.kyacc[k];
-            sh.kyacc[k] = 0.0;
-          }
-        }
+      {  // stage record -> smem (coalesced)
+        const double* src = reinterpret_cast<const double*>(rec + (b * nst + s * 6 + i));
+        double* dst = reinterpret_cast<double*>(&sh.rec);
+        for (int k = tid; k < RECD; k += blockDim.x) dst[k] = src[k];
+        if (i == 0)
+          for (int k = tid; k < NQ; k += blockDim.x) sh.vbs[k] = vb[(b * P.substeps + s) * NQ + k];
       }
       __syncthreads();
-      // ---- rate Jacobian, one input direction per thread
-      if (tid < D::NDIR) {
-        const int dir = tid < M::NDIRX ? M::dir(tid) : NX + (tid - M::NDIRX);
-        tan_rate<M>(P, sh.pr, sh.xs, dir, &sh.A[0][tid], D::NDIR);
+      if (tid < NDIR) {
+        const int dir = tid < NDIRX ? M::dir(tid) : NX + (tid - NDIRX);
+        tan_rate<M>(P, sh.rec.pr, sh.rec.vs, dir, &sh.A[0][tid], NDIR);
       }
       __syncthreads();
-      // ---- tangent columns through stage i
       if (colthr) {
-        double acc[NR];
+        if (i == 0) {  // push rows: substep-start terms of the q-row update
 #pragma unroll
-        for (int rr = 0; rr < NR; ++rr) acc[rr] = 0.0;
-        const double Shc1 = S * P.hc1[i];
+          for (int c = 0; c < NQ; ++c)
+            if (M::hslot(c) < 0) dq[c] += P.he1 * S * dv[c] + dS * sh.vbs[c];
+        }
+        double vals[Pos<NDIRX>::v];
 #pragma unroll
-        for (int kd = 0; kd < M::NDIRX; ++kd) {
+        for (int kd = 0; kd < NDIRX; ++kd) {
           const int d = M::dir(kd);
           double val;
           if (d < NQ) {
-            val = dq[d] + Shc1 * dv[d] + dS * sh.wq[d];
-            for (int l = 0; l < i; ++l) val += S * P.cq[i][l] * sh.KV[l][d][col];
+            const int hs = M::hslot(d);
+            val = dq[d] + S * P.hc1[i] * dv[d] + dS * sh.rec.wq[d];
+            for (int l = 0; l < i; ++l) val += S * P.cq[i][l] * sh.KV[l][hs][col];
           } else {
-            const int rv = d - NQ;
+            const int rv = d - NQ, hs = M::hslot(d - NQ);
             val = dv[rv];
-            for (int l = 0; l < i; ++l) val += P.ha[i][l] * sh.KV[l][rv][col];
+            for (int l = 0; l < i; ++l) val += P.ha[i][l] * sh.KV[l][hs][col];
           }
-#pragma unroll
-          for (int rr = 0; rr < NR; ++rr) acc[rr] += sh.A[rr][kd] * val;
+          vals[kd] = val;
         }
-        if (isU) {
-          const double coef = uplus ? tau : (1.0 - tau);
+        const double coef = uplus ? tau : (1.0 - tau);
+        const double hb = h * P.b[i];
 #pragma unroll
-          for (int rr = 0; rr < NR; ++rr) acc[rr] += sh.A[rr][M::NDIRX + um] * coef;
-        }
-        // dk = S * J * d(stage input) + dS * rate
-        double dk[NR];
+        for (int rr = 0; rr < NR; ++rr) {
+          double acc = 0.0;
 #pragma unroll
-        for (int rr = 0; rr < NR; ++rr) dk[rr] = S * acc[rr] + dS * sh.r[NQ + rr];
+          for (int kd = 0; kd < NDIRX; ++kd) acc += sh.A[rr][kd] * vals[kd];
+          if (isU) acc += sh.A[rr][NDIRX + um] * coef;
+          const double dk = S * acc + dS * sh.rec.r[rr];
+          if (rr < NQ) {
+            const int hs = M::hslot(rr);
+            if (hs >= 0) {
+              if (i < 5) {
+                sh.KV[i][hs][col] = dk;
+              } else {
+                double incv = P.b[5] * dk, incq = 0.0;
 #pragma unroll
-        for (int m = 0; m < NY; ++m) dy[m] += (h * P.b[i]) * dk[NQ + m];
-        if (i < 5) {
-#pragma unroll
-          for (int rv = 0; rv < NQ; ++rv) sh.KV[i][rv][col] = dk[rv];
-        } else {
-#pragma unroll
-          for (int rv = 0; rv < NQ; ++rv) {
-            double incv = P.b[5] * dk[rv];
-            double incq = 0.0;
-#pragma unroll
-            for (int l = 0; l < 5; ++l) {
-              const double kv = sh.KV[l][rv][col];
-              incv += P.b[l] * kv;
-              incq += P.e2[l] * kv;
+                for (int l = 0; l < 5; ++l) {
+                  const double kv = sh.KV[l][hs][col];
+                  incv += P.b[l] * kv;
+                  incq += P.e2[l] * kv;
+                }
+                dq[rr] = dq[rr] + P.he1 * S * dv[rr] + S * incq + dS * sh.vbs[rr];
+                dv[rr] = dv[rr] + h * incv;
+              }
+            } else {
+              dv[rr] += hb * dk;
+              dq[rr] += S * P.e2[i] * dk;
             }
-            dq[rv] = dq[rv] + P.he1 * S * dv[rv] + S * incq + dS * sh.vb[rv];
-            dv[rv] = dv[rv] + h * incv;
+          } else {
+            dy[rr - NQ] += hb * dk;
           }
         }
       }
       __syncthreads();
     }
   }
-  // ---- outputs
   double* jxb = jx + b * NXT * NXT;
   double* jub = ju + b * NXT * 2 * NU;
   double* jsb = js + b * NXT;
@@ -814,70 +856,8 @@ __global__ void __launch_bounds__(Dims<M>::NT) k_linearize(const KParams P, int6
 #pragma unroll
     for (int k = 0; k < NY; ++k) dst[(NX + k) * stride] = dy[k];
   }
-  // y0 columns of jx are the identity (rates ignore y)
-  for (int e = tid; e < NXT * NY; e += blockDim.x) {
+  for (int e = tid; e < NXT * NY; e += blockDim.x) {  // y0 columns of jx: identity (rates ignore y)
     const int r = e / Pos<NY>::v, c = NX + e % Pos<NY>::v;
     jxb[r * NXT + c] = (r == c) ? 1.0 : 0.0;
   }
-  if (tid == 0) sh.bad = 0;
-  __syncthreads();
-  for (int k = tid; k < NXT; k += blockDim.x) {
-    const double e = sh.x[k];
-    ends[b * NXT + k] = e;
-    if (!isfinite(e)) sh.bad = 1;
-  }
-  __syncthreads();
-  if (tid == 0 && bad) bad[b] = sh.bad;
-}
-
-// ---------------------------------------------------------------------------
-// K2: primal-only flow, one thread per interval (propagate / propagate_batch).
-template <class M>
-__global__ void __launch_bounds__(128) k_propagate(const KParams P, int64_t B, const double* __restrict__ xt0s,
-                                                   const double* __restrict__ Us, const double* __restrict__ Ss,
-                                                   double* __restrict__ ends, int32_t* __restrict__ bad) {
-  using D = Dims<M>;
-  constexpr int NQ = D::NQ, NX = D::NX, NU = D::NU, NY = D::NY, NXT = D::NXT;
-  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= B) return;
-  double x[NXT], xs[NX], r[NXT], K[6][NX], ky[Pos<NY>::v], U[2 * NU + 1];
-  Prim<M> pr;
-  for (int k = 0; k < NXT; ++k) x[k] = xt0s[b * NXT + k];
-  for (int k = 0; k < 2 * NU; ++k) U[k] = Us[b * 2 * NU + k];
-  const double S = Ss[b];
-  const double h = P.h;
-  for (int s = 0; s < P.substeps; ++s) {
-    const double tau0 = h * (double)s;
-#pragma unroll
-    for (int k = 0; k < NY; ++k) ky[k] = 0.0;
-    for (int i = 0; i < 6; ++i) {
-      const double tau = tau0 + P.ch[i];
-      for (int k = 0; k < NX; ++k) {
-        double a = x[k];
-        for (int j = 0; j < i; ++j) a = a + P.ha[i][j] * K[j][k];
-        xs[k] = a;
-      }
-      double u[NU > 0 ? NU : 1];
-#pragma unroll
-      for (int m = 0; m < NU; ++m) u[m] = (1.0 - tau) * U[m] + tau * U[NU + m];
-      prim_rate<M>(P, xs, u, pr, r);
-      for (int k = 0; k < NX; ++k) K[i][k] = S * r[k];
-#pragma unroll
-      for (int k = 0; k < NY; ++k) ky[k] += P.b[i] * (S * r[NX + k]);
-    }
-    for (int k = 0; k < NX; ++k) {
-      double inc = 0.0;
-      for (int j = 0; j < 6; ++j) inc += P.b[j] * K[j][k];
-      x[k] = x[k] + h * inc;
-    }
-#pragma unroll
-    for (int k = 0; k < NY; ++k) x[NX + k] = x[NX + k] + h * ky[k];
-  }
-  int nb = 0;
-  for (int k = 0; k < NXT; ++k) {
-    ends[b * NXT + k] = x[k];
-    nb |= !isfinite(x[k]);
-  }
-  if (bad) bad[b] = nb;
-  (void)NQ;
 }
