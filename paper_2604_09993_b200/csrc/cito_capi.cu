@@ -76,27 +76,14 @@ template <class M>
 cito_status launch_linearize(const KParams& P, int64_t B, const double* xt0s, const double* Us, const double* Ss,
                              double* ends, double* jx, double* ju, double* js, int32_t* bad, cudaStream_t st) {
   if (B <= 0) return CITO_OK;
-  cito_status cs = ensure_pool();
-  if (cs != CITO_OK) return cs;
-  const size_t smem = sizeof(TanShared<M>);
+  const size_t smem = sizeof(FusedShared<M>);
   static bool attr_done = false;
   if (!attr_done) {
-    CUDA_TRY(cudaFuncSetAttribute(k_tangent<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CUDA_TRY(cudaFuncSetAttribute(k_linearize<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr_done = true;
   }
-  const size_t nrec = (size_t)B * 6 * P.substeps;
-  const size_t bytes_rec = nrec * sizeof(Rec<M>);
-  const size_t bytes_vb = (size_t)B * P.substeps * Dims<M>::NQ * sizeof(double);
-  void* ws = nullptr;
-  CUDA_TRY(cudaMallocAsync(&ws, bytes_rec + bytes_vb, st));
-  Rec<M>* rec = (Rec<M>*)ws;
-  double* vb = (double*)((char*)ws + bytes_rec);
-  const int nt = 64;
-  k_primal<M, true><<<(unsigned)((B + nt - 1) / nt), nt, 0, st>>>(P, B, xt0s, Us, Ss, ends, bad, rec, vb);
+  k_linearize<M><<<(unsigned)B, FusedDims<M>::NT, smem, st>>>(P, B, xt0s, Us, Ss, ends, jx, ju, js, bad);
   CUDA_TRY(cudaGetLastError());
-  k_tangent<M><<<(unsigned)B, Dims<M>::NT, smem, st>>>(P, B, Us, Ss, rec, vb, jx, ju, js);
-  CUDA_TRY(cudaGetLastError());
-  CUDA_TRY(cudaFreeAsync(ws, st));
   return CITO_OK;
 }
 

@@ -148,6 +148,7 @@ struct Prim {
   double c[NL], s[NL];
   double rp[Pos<M::NJ>::v][2], rc[Pos<M::NJ>::v][2];  // R(theta) * (anchor - com)
   double L[NJ2 * (NJ2 + 1) / 2];                      // packed lower Cholesky factor of the Gram matrix
+  double Li[NJ2];                                     // reciprocal pivots
   double lam[NJ2];                                    // joint reactions (phi_j)
   double vdot[3 * M::NL];
   double rr[NC][2], n[NC][2], t[NC][2], F[NC][2], Jv[NC][2];
@@ -254,12 +255,10 @@ __device__ void prim_rate(const KParams& P, const double* xs, const double* u, P
       pr.rc[j][0] = pr.c[c] * P.jrc[j][0] - pr.s[c] * P.jrc[j][1];
       pr.rc[j][1] = pr.s[c] * P.jrc[j][0] + pr.c[c] * P.jrc[j][1];
     }
-    // Gram matrix G = J M^-1 J^T, only link-sharing joint pairs (compile-time)
-    double G[NJ2][NJ2];
+    // Gram matrix G = J M^-1 J^T built in place in the packed lower factor,
+    // only link-sharing joint pairs (compile-time)
 #pragma unroll
-    for (int a = 0; a < NJ2; ++a)
-#pragma unroll
-      for (int bb = 0; bb < NJ2; ++bb) G[a][bb] = 0.0;
+    for (int a = 0; a < NJ2 * (NJ2 + 1) / 2; ++a) pr.L[a] = 0.0;
 #pragma unroll
     for (int j = 0; j < NJ; ++j)
 #pragma unroll
@@ -279,9 +278,10 @@ __device__ void prim_rate(const KParams& P, const double* xs, const double* u, P
             for (int al = 0; al < 2; ++al)
 #pragma unroll
               for (int be = 0; be < 2; ++be) {
+                if (k == j && be > al) continue;
                 double val = dA[al] * dB[be] * P.minv_I[la];
                 if (al == be) val += P.minv_m[la];
-                G[2 * j + al][2 * k + be] += sg * val;
+                pr.L[LI(2 * j + al, 2 * k + be)] += sg * val;
               }
           }
     // rhs = J (M^-1 W) + curv
@@ -304,18 +304,19 @@ __device__ void prim_rate(const KParams& P, const double* xs, const double* u, P
         rhs[2 * j + al] = acc;
       }
     }
-    // Cholesky G = L L^T (lower) and solve
+    // in-place Cholesky G = L L^T (lower), reciprocal pivots kept for the solves
 #pragma unroll
     for (int cc = 0; cc < NJ2; ++cc) {
-      double d = G[cc][cc];
+      double d = pr.L[LI(cc, cc)];
 #pragma unroll
       for (int k = 0; k < cc; ++k) d -= pr.L[LI(cc, k)] * pr.L[LI(cc, k)];
       const double lcc = sqrt(d);
       pr.L[LI(cc, cc)] = lcc;
       const double il = 1.0 / lcc;
+      pr.Li[cc] = il;
 #pragma unroll
       for (int r = cc + 1; r < NJ2; ++r) {
-        double x = G[r][cc];
+        double x = pr.L[LI(r, cc)];
 #pragma unroll
         for (int k = 0; k < cc; ++k) x -= pr.L[LI(r, k)] * pr.L[LI(cc, k)];
         pr.L[LI(r, cc)] = x * il;
@@ -327,14 +328,14 @@ __device__ void prim_rate(const KParams& P, const double* xs, const double* u, P
       double x = rhs[r];
 #pragma unroll
       for (int k = 0; k < r; ++k) x -= pr.L[LI(r, k)] * y[k];
-      y[r] = x / pr.L[LI(r, r)];
+      y[r] = x * pr.Li[r];
     }
 #pragma unroll
     for (int r = NJ2 - 1; r >= 0; --r) {
       double x = y[r];
 #pragma unroll
       for (int k = r + 1; k < NJ2; ++k) x -= pr.L[LI(k, r)] * y[k];
-      y[r] = x / pr.L[LI(r, r)];
+      y[r] = x * pr.Li[r];
     }
 #pragma unroll
     for (int r = 0; r < NJ2; ++r) pr.lam[r] = -y[r];
@@ -517,14 +518,14 @@ __device__ void tan_rate(const KParams& P, const Prim<M>& pr, const double* v, i
       double x = z[r];
 #pragma unroll
       for (int k = 0; k < r; ++k) x -= pr.L[LI(r, k)] * z[k];
-      z[r] = x / pr.L[LI(r, r)];
+      z[r] = x * pr.Li[r];
     }
 #pragma unroll
     for (int r = NJ2 - 1; r >= 0; --r) {
       double x = z[r];
 #pragma unroll
       for (int k = r + 1; k < NJ2; ++k) x -= pr.L[LI(k, r)] * z[k];
-      z[r] = x / pr.L[LI(r, r)];
+      z[r] = x * pr.Li[r];
     }
     // dvdot = M^-1 (g + J^T dlam)
 #pragma unroll
@@ -860,4 +861,254 @@ __global__ void __launch_bounds__(Dims<M>::NT) k_tangent(const KParams P, int64_
     const int r = e / Pos<NY>::v, c = NX + e % Pos<NY>::v;
     jxb[r * NXT + c] = (r == c) ? 1.0 : 0.0;
   }
+}
+
+// ===========================================================================
+// K1 (fused, warp-specialized, software-pipelined) -- one CTA per interval.
+//   warp 0      : primal producer.  Tick t computes RK stage t of the primal
+//                 chain (lane 0 runs the rate function; the warp does the
+//                 elementwise stage algebra) and publishes its record in
+//                 ring[t % 3].
+//   warp 1      : rate Jacobian of stage t-1 (one input direction per lane,
+//                 tan_rate reusing the record's Cholesky factor) -> A[(t-1) % 2].
+//   warps 2..   : one tangent column per thread, stage t-2.
+// One __syncthreads per tick; the primal chain and the tangent work overlap,
+// so a linearization takes ~max(primal, tangent) instead of their sum.
+template <class M>
+struct FusedDims {
+  using D = Dims<M>;
+  static constexpr int NCW = (D::NCOL + 31) / 32;
+  static constexpr int NT = 64 + 32 * NCW;
+};
+
+template <class M>
+struct FusedShared {
+  using D = Dims<M>;
+  Rec<M> ring[3];
+  double A[2][D::NR][D::NDIR];
+  double KV[5][D::NH][D::NCOLP];
+  double PQ[Pos<M::NPUSH>::v][D::NCOLP];
+  double PV[Pos<M::NPUSH>::v][D::NCOLP];
+  double DY[Pos<D::NY>::v][D::NCOLP];
+  double x[D::NXT];
+  double xs[D::NX];
+  double rf[D::NXT];
+  double K[6][D::NX];
+  double VS[6][D::NQ];
+  double ky[Pos<D::NY>::v];
+  double vbs[2][D::NQ];
+  double U[2 * D::NU + 1];
+  double S;
+  int bad;
+};
+
+template <class M>
+__device__ __forceinline__ void fused_primal(const KParams& P, FusedShared<M>& sh, int t, int lane) {
+  using D = Dims<M>;
+  constexpr int NQ = D::NQ, NX = D::NX, NU = D::NU, NY = D::NY, NR = D::NR;
+  const int s = t / 6, i = t % 6;
+  const double h = P.h, S = sh.S;
+  const double tau = h * (double)s + P.ch[i];
+  Rec<M>& R = sh.ring[t % 3];
+  for (int k = lane; k < NX; k += 32) {  // stage input (cito/augmentation.py:200-205)
+    double a = sh.x[k];
+    for (int j = 0; j < i; ++j) a = a + P.ha[i][j] * sh.K[j][k];
+    sh.xs[k] = a;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    double u[Pos<NU>::v];
+#pragma unroll
+    for (int m = 0; m < NU; ++m) u[m] = (1.0 - tau) * sh.U[m] + tau * sh.U[NU + m];  // foh_eval :166-169
+    prim_rate<M>(P, sh.xs, u, R.pr, sh.rf);
+  }
+  __syncwarp();
+  for (int k = lane; k < NX; k += 32) sh.K[i][k] = S * sh.rf[k];
+  for (int k = lane; k < NY; k += 32) sh.ky[k] = (i == 0 ? 0.0 : sh.ky[k]) + P.b[i] * (S * sh.rf[NX + k]);
+  for (int k = lane; k < NQ; k += 32) {
+    const double vsk = sh.xs[NQ + k];
+    sh.VS[i][k] = vsk;
+    R.vs[k] = vsk;
+    double w = 0.0;
+    for (int j = 0; j < i; ++j) w += P.ha[i][j] * sh.VS[j][k];
+    R.wq[k] = w;
+  }
+  for (int k = lane; k < NR; k += 32) R.r[k] = sh.rf[NQ + k];
+  __syncwarp();
+  if (i == 5) {  // end of substep: x <- x + h sum_i b_i k_i (:209)
+    for (int k = lane; k < NQ; k += 32) {
+      double w = 0.0;
+      for (int j = 0; j < 6; ++j) w += P.b[j] * sh.VS[j][k];
+      sh.vbs[s & 1][k] = h * w;
+    }
+    for (int k = lane; k < NX; k += 32) {
+      double inc = 0.0;
+      for (int j = 0; j < 6; ++j) inc += P.b[j] * sh.K[j][k];
+      sh.x[k] = sh.x[k] + h * inc;
+    }
+    for (int k = lane; k < NY; k += 32) sh.x[NX + k] = sh.x[NX + k] + h * sh.ky[k];
+  }
+}
+
+template <class M>
+__global__ void __launch_bounds__(FusedDims<M>::NT) k_linearize(const KParams P, int64_t B,
+                                                               const double* __restrict__ xt0s,
+                                                               const double* __restrict__ Us,
+                                                               const double* __restrict__ Ss,
+                                                               double* __restrict__ ends, double* __restrict__ jx,
+                                                               double* __restrict__ ju, double* __restrict__ js,
+                                                               int32_t* __restrict__ bad) {
+  using D = Dims<M>;
+  constexpr int NQ = D::NQ, NX = D::NX, NU = D::NU, NY = D::NY, NXT = D::NXT, NCOL = D::NCOL, NR = D::NR;
+  constexpr int NDIRX = M::NDIRX, NDIR = D::NDIR, NHIST = M::NHIST;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  FusedShared<M>& sh = *reinterpret_cast<FusedShared<M>*>(smem_raw);
+  const int64_t b = blockIdx.x;
+  if (b >= B) return;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int k = tid; k < NXT; k += blockDim.x) sh.x[k] = xt0s[b * NXT + k];
+  for (int k = tid; k < 2 * NU; k += blockDim.x) sh.U[k] = Us[b * 2 * NU + k];
+  if (tid == 0) {
+    sh.S = Ss[b];
+    sh.bad = 0;
+  }
+  // column state: seed = unit column of [x~+ | U- | U+ | S]
+  const int col = tid - 64;
+  const bool colthr = warp >= 2 && col < NCOL;
+  const double dS = (col == NCOL - 1) ? 1.0 : 0.0;
+  const int uj = col - NX;
+  const bool isU = (uj >= 0) && (uj < 2 * NU);
+  const int um = isU ? (uj % Pos<NU>::v) : 0;
+  const bool uplus = isU && (uj >= NU);
+  double hq[Pos<NHIST>::v], hv[Pos<NHIST>::v];  // history coordinates: substep-start values
+  if (colthr) {
+#pragma unroll
+    for (int c = 0; c < NQ; ++c) {
+      const double e_q = (col == c) ? 1.0 : 0.0, e_v = (col == NQ + c) ? 1.0 : 0.0;
+      if (M::hslot(c) >= 0) {
+        hq[M::hslot(c)] = e_q;
+        hv[M::hslot(c)] = e_v;
+      } else {
+        sh.PQ[M::pslot(c)][col] = e_q;
+        sh.PV[M::pslot(c)][col] = e_v;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < NY; ++k) sh.DY[k][col] = 0.0;
+  }
+  __syncthreads();
+  const double S = sh.S, h = P.h;
+  const int NST = 6 * P.substeps;
+  for (int t = 0; t < NST + 2; ++t) {
+    if (warp == 0) {
+      if (t < NST) fused_primal<M>(P, sh, t, lane);
+    } else if (warp == 1) {
+      if (t >= 1 && t <= NST) {
+        const int st = t - 1;
+        const Rec<M>& R = sh.ring[st % 3];
+        for (int kd = lane; kd < NDIR; kd += 32) {
+          const int dir = kd < NDIRX ? M::dir(kd) : NX + (kd - NDIRX);
+          tan_rate<M>(P, R.pr, R.vs, dir, &sh.A[st & 1][0][kd], NDIR);
+        }
+      }
+    } else if (colthr && t >= 2) {
+      const int st = t - 2, s = st / 6, i = st % 6;
+      const Rec<M>& R = sh.ring[st % 3];
+      const double(*Ab)[NDIR] = sh.A[st & 1];
+      const double tau = h * (double)s + P.ch[i];
+      const double hb = h * P.b[i];
+      if (i == 0) {  // push q rows: S h sum(b) * (substep-start dv)
+#pragma unroll
+        for (int p = 0; p < M::NPUSH; ++p) sh.PQ[p][col] += P.he1 * S * sh.PV[p][col];
+      }
+      double vals[Pos<NDIRX>::v];
+#pragma unroll
+      for (int kd = 0; kd < NDIRX; ++kd) {
+        const int d = M::dir(kd);
+        double val;
+        if (d < NQ) {
+          const int hs = M::hslot(d);
+          val = hq[hs] + S * P.hc1[i] * hv[hs] + dS * R.wq[d];
+          for (int l = 0; l < i; ++l) val += S * P.cq[i][l] * sh.KV[l][hs][col];
+        } else {
+          const int hs = M::hslot(d - NQ);
+          val = hv[hs];
+          for (int l = 0; l < i; ++l) val += P.ha[i][l] * sh.KV[l][hs][col];
+        }
+        vals[kd] = val;
+      }
+      const double coef = uplus ? tau : (1.0 - tau);
+#pragma unroll
+      for (int rr = 0; rr < NR; ++rr) {
+        double acc = 0.0;
+#pragma unroll
+        for (int kd = 0; kd < NDIRX; ++kd)
+          if (M::adep(rr, kd)) acc += Ab[rr][kd] * vals[kd];
+        if (isU) acc += Ab[rr][NDIRX + um] * coef;
+        const double dk = S * acc + dS * R.r[rr];
+        if (rr < NQ) {
+          const int hs = M::hslot(rr);
+          if (hs >= 0) {
+            if (i < 5) {
+              sh.KV[i][hs][col] = dk;
+            } else {
+              double incv = P.b[5] * dk, incq = 0.0;
+#pragma unroll
+              for (int l = 0; l < 5; ++l) {
+                const double kv = sh.KV[l][hs][col];
+                incv += P.b[l] * kv;
+                incq += P.e2[l] * kv;
+              }
+              hq[hs] = hq[hs] + P.he1 * S * hv[hs] + S * incq + dS * sh.vbs[s & 1][rr];
+              hv[hs] = hv[hs] + h * incv;
+            }
+          } else {
+            const int p = M::pslot(rr);
+            sh.PV[p][col] += hb * dk;
+            sh.PQ[p][col] += S * P.e2[i] * dk + dS * hb * R.vs[rr];
+          }
+        } else {
+          sh.DY[rr - NQ][col] += hb * dk;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // ---- outputs
+  double* jxb = jx + b * NXT * NXT;
+  double* jub = ju + b * NXT * 2 * NU;
+  double* jsb = js + b * NXT;
+  if (colthr) {
+    double* dst;
+    int stride;
+    if (col < NX) {
+      dst = jxb + col;
+      stride = NXT;
+    } else if (isU) {
+      dst = jub + uj;
+      stride = 2 * NU;
+    } else {
+      dst = jsb;
+      stride = 1;
+    }
+#pragma unroll
+    for (int c = 0; c < NQ; ++c) {
+      const int hs = M::hslot(c);
+      dst[c * stride] = hs >= 0 ? hq[hs] : sh.PQ[M::pslot(c)][col];
+      dst[(NQ + c) * stride] = hs >= 0 ? hv[hs] : sh.PV[M::pslot(c)][col];
+    }
+#pragma unroll
+    for (int k = 0; k < NY; ++k) dst[(NX + k) * stride] = sh.DY[k][col];
+  }
+  for (int e = tid; e < NXT * NY; e += blockDim.x) {  // y0 columns of jx: identity (rates ignore y)
+    const int r = e / Pos<NY>::v, c = NX + e % Pos<NY>::v;
+    jxb[r * NXT + c] = (r == c) ? 1.0 : 0.0;
+  }
+  for (int k = tid; k < NXT; k += blockDim.x) {
+    const double e = sh.x[k];
+    ends[b * NXT + k] = e;
+    if (!isfinite(e)) sh.bad = 1;
+  }
+  __syncthreads();
+  if (tid == 0 && bad) bad[b] = sh.bad;
 }
