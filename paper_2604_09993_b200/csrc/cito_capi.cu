@@ -79,10 +79,19 @@ cito_status launch_linearize(const KParams& P, int64_t B, const double* xt0s, co
   const size_t smem = sizeof(FusedShared<M>);
   static bool attr_done = false;
   if (!attr_done) {
-    CUDA_TRY(cudaFuncSetAttribute(k_linearize<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CUDA_TRY(cudaFuncSetAttribute(k_linearize<M, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CUDA_TRY(cudaFuncSetAttribute(k_linearize<M, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr_done = true;
   }
-  k_linearize<M><<<(unsigned)B, FusedDims<M>::NT, smem, st>>>(P, B, xt0s, Us, Ss, ends, jx, ju, js, bad);
+  // latency variant (full register budget) while the grid fits the SMs once,
+  // occupancy variant (<= 3 CTAs/SM register budget) for large batches
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (B <= sms)
+    k_linearize<M, 1><<<(unsigned)B, FusedDims<M>::NT, smem, st>>>(P, B, xt0s, Us, Ss, ends, jx, ju, js, bad);
+  else
+    k_linearize<M, 3><<<(unsigned)B, FusedDims<M>::NT, smem, st>>>(P, B, xt0s, Us, Ss, ends, jx, ju, js, bad);
   CUDA_TRY(cudaGetLastError());
   return CITO_OK;
 }

@@ -164,14 +164,25 @@ struct Prim {
 //   aux_rate           cito/augmentation.py:134-153, path g :112-129
 template <class M>
 __device__ void prim_rate(const KParams& P, const double* xs, const double* u, Prim<M>& pr, double* out) {
+  // Every intermediate lives in registers; `pr` (shared memory) is only written,
+  // so the dependent chain never waits on a shared-memory round trip.
   constexpr int NL = M::NL, NJ = M::NJ, NC = M::NC, NA = M::NA, NQ = 3 * NL;
   constexpr int NU = NA + 3 * NC;
-  const double* q = xs;
-  const double* v = xs + NQ;
+  double q[NQ], v[NQ];
+#pragma unroll
+  for (int k = 0; k < NQ; ++k) {
+    q[k] = xs[k];
+    v[k] = xs[NQ + k];
+  }
 #pragma unroll
   for (int m = 0; m < NU; ++m) pr.u[m] = u[m];
+  double cl[NL], sl[NL];
 #pragma unroll
-  for (int l = 0; l < NL; ++l) sincos(q[3 * l + 2], &pr.s[l], &pr.c[l]);
+  for (int l = 0; l < NL; ++l) {
+    sincos(q[3 * l + 2], &sl[l], &cl[l]);
+    pr.c[l] = cl[l];
+    pr.s[l] = sl[l];
+  }
   double W[NQ];
 #pragma unroll
   for (int k = 0; k < NQ; ++k) W[k] = 0.0;
@@ -192,11 +203,12 @@ __device__ void prim_rate(const KParams& P, const double* xs, const double* u, P
     if (p >= 0) W[3 * p + 2] += -mo;
   }
   // contacts: frame, world force, wrench, Omega ingredients
+  double sdl[Pos<NC>::v], Jvl[Pos<NC>::v][2], tl[Pos<NC>::v][2];
 #pragma unroll
   for (int i = 0; i < NC; ++i) {
     const int l = M::clink(i);
-    const double rx = pr.c[l] * P.cr[i][0] - pr.s[l] * P.cr[i][1];
-    const double rz = pr.s[l] * P.cr[i][0] + pr.c[l] * P.cr[i][1];
+    const double rx = cl[l] * P.cr[i][0] - sl[l] * P.cr[i][1];
+    const double rz = sl[l] * P.cr[i][0] + cl[l] * P.cr[i][1];
     pr.rr[i][0] = rx;
     pr.rr[i][1] = rz;
     const double Px = q[3 * l] + rx, Pz = q[3 * l + 1] + rz;
@@ -213,13 +225,16 @@ __device__ void prim_rate(const KParams& P, const double* xs, const double* u, P
       pr.gn[i] = gn;
       n0 = t2.gx / gn;
       n1 = t2.gz / gn;
-      pr.sd[i] = t2.v / gn;
+      sdl[i] = t2.v / gn;
     } else {
       n0 = 0.0;
       n1 = 1.0;
-      pr.sd[i] = Pz - P.height;
+      sdl[i] = Pz - P.height;
     }
+    pr.sd[i] = sdl[i];
     const double t0 = n1, t1 = -n0;
+    tl[i][0] = t0;
+    tl[i][1] = t1;
     pr.n[i][0] = n0;
     pr.n[i][1] = n1;
     pr.t[i][0] = t0;
@@ -232,8 +247,10 @@ __device__ void prim_rate(const KParams& P, const double* xs, const double* u, P
     W[3 * l + 1] += F1;
     W[3 * l + 2] += (-rz) * F0 + rx * F1;
     const double w = v[3 * l + 2];
-    pr.Jv[i][0] = v[3 * l] + (-rz) * w;
-    pr.Jv[i][1] = v[3 * l + 1] + rx * w;
+    Jvl[i][0] = v[3 * l] + (-rz) * w;
+    Jvl[i][1] = v[3 * l + 1] + rx * w;
+    pr.Jv[i][0] = Jvl[i][0];
+    pr.Jv[i][1] = Jvl[i][1];
   }
   double* vdot = out + NQ;
   if constexpr (NJ == 0) {
@@ -242,27 +259,41 @@ __device__ void prim_rate(const KParams& P, const double* xs, const double* u, P
       vdot[3 * l] = P.minv_m[l] * W[3 * l];
       vdot[3 * l + 1] = P.minv_m[l] * W[3 * l + 1];
       vdot[3 * l + 2] = P.minv_I[l] * W[3 * l + 2];
+      pr.vdot[3 * l + 2] = vdot[3 * l + 2];
     }
   } else {
     constexpr int NJ2 = 2 * NJ;
+    double R[NJ][2][2];  // [joint][side parent/child][x,z] = R(theta) (anchor - com)
 #pragma unroll
     for (int j = 0; j < NJ; ++j) {
       const int p = M::jparent(j), c = M::jchild(j);
       if (p >= 0) {
-        pr.rp[j][0] = pr.c[p] * P.jrp[j][0] - pr.s[p] * P.jrp[j][1];
-        pr.rp[j][1] = pr.s[p] * P.jrp[j][0] + pr.c[p] * P.jrp[j][1];
+        R[j][0][0] = cl[p] * P.jrp[j][0] - sl[p] * P.jrp[j][1];
+        R[j][0][1] = sl[p] * P.jrp[j][0] + cl[p] * P.jrp[j][1];
+        pr.rp[j][0] = R[j][0][0];
+        pr.rp[j][1] = R[j][0][1];
+      } else {
+        R[j][0][0] = R[j][0][1] = 0.0;
       }
-      pr.rc[j][0] = pr.c[c] * P.jrc[j][0] - pr.s[c] * P.jrc[j][1];
-      pr.rc[j][1] = pr.s[c] * P.jrc[j][0] + pr.c[c] * P.jrc[j][1];
+      R[j][1][0] = cl[c] * P.jrc[j][0] - sl[c] * P.jrc[j][1];
+      R[j][1][1] = sl[c] * P.jrc[j][0] + cl[c] * P.jrc[j][1];
+      pr.rc[j][0] = R[j][1][0];
+      pr.rc[j][1] = R[j][1][1];
     }
-    // Gram matrix G = J M^-1 J^T built in place in the packed lower factor,
-    // only link-sharing joint pairs (compile-time)
+    // Gram matrix G = J M^-1 J^T in the no-fill elimination order M::jperm
+    // (gen_models.py), packed lower, only the structurally nonzero blocks
+    double Lr[NJ2 * (NJ2 + 1) / 2];
 #pragma unroll
-    for (int a = 0; a < NJ2 * (NJ2 + 1) / 2; ++a) pr.L[a] = 0.0;
+    for (int a = 0; a < NJ; ++a)
 #pragma unroll
-    for (int j = 0; j < NJ; ++j)
+      for (int bp = 0; bp <= a; ++bp) {
+        if (!M::lnzb(a, bp)) continue;
+        const int j = M::jperm(a), k = M::jperm(bp);
 #pragma unroll
-      for (int k = 0; k <= j; ++k)
+        for (int al = 0; al < 2; ++al)
+#pragma unroll
+          for (int be = 0; be < 2; ++be)
+            if (!(a == bp && be > al)) Lr[LI(2 * a + al, 2 * bp + be)] = 0.0;
 #pragma unroll
         for (int sa = 0; sa < 2; ++sa)
 #pragma unroll
@@ -271,23 +302,23 @@ __device__ void prim_rate(const KParams& P, const double* xs, const double* u, P
             const int lb = sb == 0 ? M::jparent(k) : M::jchild(k);
             if (la < 0 || la != lb) continue;
             const double sg = (sa == sb) ? 1.0 : -1.0;
-            const double* Ra = sa == 0 ? pr.rp[j] : pr.rc[j];
-            const double* Rb = sb == 0 ? pr.rp[k] : pr.rc[k];
-            const double dA[2] = {-Ra[1], Ra[0]}, dB[2] = {-Rb[1], Rb[0]};
+            const double dA[2] = {-R[j][sa][1], R[j][sa][0]}, dB[2] = {-R[k][sb][1], R[k][sb][0]};
 #pragma unroll
             for (int al = 0; al < 2; ++al)
 #pragma unroll
               for (int be = 0; be < 2; ++be) {
-                if (k == j && be > al) continue;
+                if (a == bp && be > al) continue;
                 double val = dA[al] * dB[be] * P.minv_I[la];
                 if (al == be) val += P.minv_m[la];
-                pr.L[LI(2 * j + al, 2 * k + be)] += sg * val;
+                Lr[LI(2 * a + al, 2 * bp + be)] += sg * val;
               }
           }
-    // rhs = J (M^-1 W) + curv
-    double rhs[NJ2];
+      }
+    // rhs = J (M^-1 W) + curv, in elimination order
+    double y[NJ2];
 #pragma unroll
-    for (int j = 0; j < NJ; ++j) {
+    for (int a = 0; a < NJ; ++a) {
+      const int j = M::jperm(a);
 #pragma unroll
       for (int al = 0; al < 2; ++al) {
         double acc = 0.0;
@@ -296,119 +327,134 @@ __device__ void prim_rate(const KParams& P, const double* xs, const double* u, P
           const int l = sa == 0 ? M::jparent(j) : M::jchild(j);
           if (l < 0) continue;
           const double sgn = sa == 0 ? 1.0 : -1.0;
-          const double* R = sa == 0 ? pr.rp[j] : pr.rc[j];
-          const double dP = al == 0 ? -R[1] : R[0];
+          const double dP = al == 0 ? -R[j][sa][1] : R[j][sa][0];
           const double w = v[3 * l + 2];
-          acc += sgn * (P.minv_m[l] * W[3 * l + al] + dP * P.minv_I[l] * W[3 * l + 2] - R[al] * w * w);
+          acc += sgn * (P.minv_m[l] * W[3 * l + al] + dP * P.minv_I[l] * W[3 * l + 2] - R[j][sa][al] * w * w);
         }
-        rhs[2 * j + al] = acc;
+        y[2 * a + al] = acc;
       }
     }
-    // in-place Cholesky G = L L^T (lower), reciprocal pivots kept for the solves
+    // sparse Cholesky G = L L^T (no fill outside M::lnzb), reciprocal pivots
+    double Lir[NJ2];
 #pragma unroll
     for (int cc = 0; cc < NJ2; ++cc) {
-      double d = pr.L[LI(cc, cc)];
+      double d = Lr[LI(cc, cc)];
 #pragma unroll
-      for (int k = 0; k < cc; ++k) d -= pr.L[LI(cc, k)] * pr.L[LI(cc, k)];
+      for (int k = 0; k < cc; ++k)
+        if (M::lnzb(cc / 2, k / 2)) d -= Lr[LI(cc, k)] * Lr[LI(cc, k)];
       const double lcc = sqrt(d);
-      pr.L[LI(cc, cc)] = lcc;
+      Lr[LI(cc, cc)] = lcc;
       const double il = 1.0 / lcc;
-      pr.Li[cc] = il;
+      Lir[cc] = il;
 #pragma unroll
       for (int r = cc + 1; r < NJ2; ++r) {
-        double x = pr.L[LI(r, cc)];
+        if (!M::lnzb(r / 2, cc / 2)) continue;
+        double x = Lr[LI(r, cc)];
 #pragma unroll
-        for (int k = 0; k < cc; ++k) x -= pr.L[LI(r, k)] * pr.L[LI(cc, k)];
-        pr.L[LI(r, cc)] = x * il;
+        for (int k = 0; k < cc; ++k)
+          if (M::lnzb(r / 2, k / 2) && M::lnzb(cc / 2, k / 2)) x -= Lr[LI(r, k)] * Lr[LI(cc, k)];
+        Lr[LI(r, cc)] = x * il;
       }
     }
-    double y[NJ2];
 #pragma unroll
     for (int r = 0; r < NJ2; ++r) {
-      double x = rhs[r];
+      double x = y[r];
 #pragma unroll
-      for (int k = 0; k < r; ++k) x -= pr.L[LI(r, k)] * y[k];
-      y[r] = x * pr.Li[r];
+      for (int k = 0; k < r; ++k)
+        if (M::lnzb(r / 2, k / 2)) x -= Lr[LI(r, k)] * y[k];
+      y[r] = x * Lir[r];
     }
 #pragma unroll
     for (int r = NJ2 - 1; r >= 0; --r) {
       double x = y[r];
 #pragma unroll
-      for (int k = r + 1; k < NJ2; ++k) x -= pr.L[LI(k, r)] * y[k];
-      y[r] = x * pr.Li[r];
+      for (int k = r + 1; k < NJ2; ++k)
+        if (M::lnzb(k / 2, r / 2)) x -= Lr[LI(k, r)] * y[k];
+      y[r] = x * Lir[r];
     }
+    // publish the factor (elimination order) for the tangent threads
 #pragma unroll
-    for (int r = 0; r < NJ2; ++r) pr.lam[r] = -y[r];
-    // vdot = M^-1 (W + J^T lam)
+    for (int r = 0; r < NJ2; ++r) {
+      pr.Li[r] = Lir[r];
 #pragma unroll
-    for (int j = 0; j < NJ; ++j)
+      for (int c = 0; c <= r; ++c)
+        if (M::lnzb(r / 2, c / 2)) pr.L[LI(r, c)] = Lr[LI(r, c)];
+    }
+    // lam (joint order) = -G^{-1} rhs ; vdot = M^-1 (W + J^T lam)
+#pragma unroll
+    for (int a = 0; a < NJ; ++a) {
+      const int j = M::jperm(a);
+      const double l0 = -y[2 * a], l1 = -y[2 * a + 1];
+      pr.lam[2 * j] = l0;
+      pr.lam[2 * j + 1] = l1;
 #pragma unroll
       for (int sa = 0; sa < 2; ++sa) {
         const int l = sa == 0 ? M::jparent(j) : M::jchild(j);
         if (l < 0) continue;
         const double sgn = sa == 0 ? 1.0 : -1.0;
-        const double* R = sa == 0 ? pr.rp[j] : pr.rc[j];
-        const double l0 = pr.lam[2 * j], l1 = pr.lam[2 * j + 1];
         W[3 * l] += sgn * l0;
         W[3 * l + 1] += sgn * l1;
-        W[3 * l + 2] += sgn * ((-R[1]) * l0 + R[0] * l1);
+        W[3 * l + 2] += sgn * ((-R[j][sa][1]) * l0 + R[j][sa][0] * l1);
       }
+    }
 #pragma unroll
     for (int l = 0; l < NL; ++l) {
       vdot[3 * l] = P.minv_m[l] * W[3 * l];
       vdot[3 * l + 1] = P.minv_m[l] * W[3 * l + 1];
       vdot[3 * l + 2] = P.minv_I[l] * W[3 * l + 2];
+      pr.vdot[3 * l + 2] = vdot[3 * l + 2];
     }
   }
 #pragma unroll
-  for (int k = 0; k < NQ; ++k) {
-    out[k] = v[k];
-    pr.vdot[k] = vdot[k];
-  }
+  for (int k = 0; k < NQ; ++k) out[k] = v[k];
   // Omega (aux_rate)
-  double* y = out + 2 * NQ;
+  double* yo = out + 2 * NQ;
 #pragma unroll
   for (int i = 0; i < NC; ++i) {
     const double ft = u[NA + 2 * i], fn = u[NA + 2 * i + 1], gam = u[NA + 2 * NC + i];
-    const double vt = pr.t[i][0] * pr.Jv[i][0] + pr.t[i][1] * pr.Jv[i][1];
+    const double vt = tl[i][0] * Jvl[i][0] + tl[i][1] * Jvl[i][1];
     const double sgt = ft / sqrt(ft * ft + 1.0);
     pr.sg[i] = sgt;
     const double lamc = vt + gam * sgt;
     pr.lamc[i] = lamc;
-    y[5 * i + 0] = fn;
-    y[5 * i + 1] = sabs(lamc);
-    y[5 * i + 2] = gam;
-    y[5 * i + 3] = sabs(P.mu[i] * fn) - sabs(ft);
-    y[5 * i + 4] = srelu(pr.sd[i]);
+    yo[5 * i + 0] = fn;
+    yo[5 * i + 1] = sabs(lamc);
+    yo[5 * i + 2] = gam;
+    yo[5 * i + 3] = sabs(P.mu[i] * fn) - sabs(ft);
+    yo[5 * i + 4] = srelu(sdl[i]);
   }
   if constexpr (M::NGO > 0) {
     constexpr int NG = Prim<M>::NG;
-    double sgv[Pos<NG>::v];
+    double gpl[Pos<NG>::v];
     int r = 0;
 #pragma unroll
-    for (int i = 0; i < NC; ++i) pr.gp[r++] = -pr.sd[i];
+    for (int i = 0; i < NC; ++i) gpl[r++] = -sdl[i];
 #pragma unroll
     for (int k = 0; k < M::NJL; ++k) {
       const int jj = M::jl_joint(k);
       const int p = M::jparent(jj), c = M::jchild(jj);
       const double rel = q[3 * c + 2] - (p >= 0 ? q[3 * p + 2] : 0.0);
-      pr.gp[r++] = rel - P.jl_hi[k];
-      pr.gp[r++] = P.jl_lo[k] - rel;
+      gpl[r++] = rel - P.jl_hi[k];
+      gpl[r++] = P.jl_lo[k] - rel;
     }
 #pragma unroll
     for (int k = 0; k < M::NHB; ++k) {
       const double pz = q[3 * M::hb_link(k) + 1];
-      pr.gp[r++] = P.hb_lo[k] - pz;
-      pr.gp[r++] = pz - P.hb_hi[k];
+      gpl[r++] = P.hb_lo[k] - pz;
+      gpl[r++] = pz - P.hb_hi[k];
     }
+    double sgv[Pos<NG>::v];
 #pragma unroll
-    for (int jg = 0; jg < NG; ++jg) sgv[jg] = srelu(pr.gp[jg]);
+    for (int jg = 0; jg < NG; ++jg) {
+      pr.gp[jg] = gpl[jg];
+      sgv[jg] = srelu(gpl[jg]);
+    }
 #pragma unroll
     for (int o = 0; o < M::NGO; ++o) {
       double acc = 0.0;
 #pragma unroll
       for (int jg = 0; jg < NG; ++jg) acc += P.mix[o][jg] * sgv[jg];
-      y[5 * NC + o] = acc;
+      yo[5 * NC + o] = acc;
     }
   }
 }
@@ -512,20 +558,33 @@ __device__ void tan_rate(const KParams& P, const Prim<M>& pr, const double* v, i
         }
         z[2 * j + al] = acc;
       }
-    // z <- G^{-1} z with the primal Cholesky factor; dlam = -z
+    // z <- G^{-1} z with the primal factor (elimination order M::jperm); dlam = -z
+    double zp[NJ2];
+#pragma unroll
+    for (int a = 0; a < NJ; ++a) {
+      zp[2 * a] = z[2 * M::jperm(a)];
+      zp[2 * a + 1] = z[2 * M::jperm(a) + 1];
+    }
 #pragma unroll
     for (int r = 0; r < NJ2; ++r) {
-      double x = z[r];
+      double x = zp[r];
 #pragma unroll
-      for (int k = 0; k < r; ++k) x -= pr.L[LI(r, k)] * z[k];
-      z[r] = x * pr.Li[r];
+      for (int k = 0; k < r; ++k)
+        if (M::lnzb(r / 2, k / 2)) x -= pr.L[LI(r, k)] * zp[k];
+      zp[r] = x * pr.Li[r];
     }
 #pragma unroll
     for (int r = NJ2 - 1; r >= 0; --r) {
-      double x = z[r];
+      double x = zp[r];
 #pragma unroll
-      for (int k = r + 1; k < NJ2; ++k) x -= pr.L[LI(k, r)] * z[k];
-      z[r] = x * pr.Li[r];
+      for (int k = r + 1; k < NJ2; ++k)
+        if (M::lnzb(k / 2, r / 2)) x -= pr.L[LI(k, r)] * zp[k];
+      zp[r] = x * pr.Li[r];
+    }
+#pragma unroll
+    for (int a = 0; a < NJ; ++a) {
+      z[2 * M::jperm(a)] = zp[2 * a];
+      z[2 * M::jperm(a) + 1] = zp[2 * a + 1];
     }
     // dvdot = M^-1 (g + J^T dlam)
 #pragma unroll
@@ -704,165 +763,6 @@ __global__ void __launch_bounds__(64) k_primal(const KParams P, int64_t B, const
   if (bad) bad[b] = nb;
 }
 
-template <class M>
-struct TanShared {
-  using D = Dims<M>;
-  Rec<M> rec;
-  double A[D::NR][D::NDIR];
-  double KV[5][D::NH][D::NCOLP];
-  double vbs[D::NQ];
-  double U[2 * D::NU + 1];
-  double S;
-};
-
-// ---------------------------------------------------------------------------
-// K1b: tangent columns of the interval map, one CTA per interval.  Per stage:
-// threads < NDIR form one column each of the rate Jacobian (tan_rate), then
-// threads < NCOL advance one tangent column each through the stage recursion.
-// Only coordinates the rate Jacobian reads keep velocity-row stage history
-// (M::hslot); all other rows are accumulated in push form.
-template <class M>
-__global__ void __launch_bounds__(Dims<M>::NT) k_tangent(const KParams P, int64_t B, const double* __restrict__ Us,
-                                                        const double* __restrict__ Ss,
-                                                        const Rec<M>* __restrict__ rec,
-                                                        const double* __restrict__ vb, double* __restrict__ jx,
-                                                        double* __restrict__ ju, double* __restrict__ js) {
-  using D = Dims<M>;
-  constexpr int NQ = D::NQ, NX = D::NX, NU = D::NU, NY = D::NY, NXT = D::NXT, NCOL = D::NCOL, NR = D::NR;
-  constexpr int NDIRX = M::NDIRX, NDIR = D::NDIR;
-  constexpr int RECD = sizeof(Rec<M>) / sizeof(double);
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  TanShared<M>& sh = *reinterpret_cast<TanShared<M>*>(smem_raw);
-  const int64_t b = blockIdx.x;
-  if (b >= B) return;
-  const int tid = threadIdx.x;
-  for (int k = tid; k < 2 * NU; k += blockDim.x) sh.U[k] = Us[b * 2 * NU + k];
-  if (tid == 0) sh.S = Ss[b];
-  __syncthreads();
-  const double S = sh.S;
-  const bool colthr = tid < NCOL;
-  const int col = tid;
-  const double dS = (col == NCOL - 1) ? 1.0 : 0.0;
-  const int uj = col - NX;
-  const bool isU = (uj >= 0) && (uj < 2 * NU);
-  const int um = isU ? (uj % Pos<NU>::v) : 0;
-  const bool uplus = isU && (uj >= NU);
-  double dq[NQ], dv[NQ], dy[Pos<NY>::v];
-#pragma unroll
-  for (int k = 0; k < NQ; ++k) {
-    dq[k] = (col == k) ? 1.0 : 0.0;
-    dv[k] = (col == NQ + k) ? 1.0 : 0.0;
-  }
-#pragma unroll
-  for (int k = 0; k < NY; ++k) dy[k] = 0.0;
-  const double h = P.h;
-  const int nst = 6 * P.substeps;
-  for (int s = 0; s < P.substeps; ++s) {
-    const double tau0 = h * (double)s;
-    for (int i = 0; i < 6; ++i) {
-      const double tau = tau0 + P.ch[i];
-      {  // stage record -> smem (coalesced)
-        const double* src = reinterpret_cast<const double*>(rec + (b * nst + s * 6 + i));
-        double* dst = reinterpret_cast<double*>(&sh.rec);
-        for (int k = tid; k < RECD; k += blockDim.x) dst[k] = src[k];
-        if (i == 0)
-          for (int k = tid; k < NQ; k += blockDim.x) sh.vbs[k] = vb[(b * P.substeps + s) * NQ + k];
-      }
-      __syncthreads();
-      if (tid < NDIR) {
-        const int dir = tid < NDIRX ? M::dir(tid) : NX + (tid - NDIRX);
-        tan_rate<M>(P, sh.rec.pr, sh.rec.vs, dir, &sh.A[0][tid], NDIR);
-      }
-      __syncthreads();
-      if (colthr) {
-        if (i == 0) {  // push rows: substep-start terms of the q-row update
-#pragma unroll
-          for (int c = 0; c < NQ; ++c)
-            if (M::hslot(c) < 0) dq[c] += P.he1 * S * dv[c] + dS * sh.vbs[c];
-        }
-        double vals[Pos<NDIRX>::v];
-#pragma unroll
-        for (int kd = 0; kd < NDIRX; ++kd) {
-          const int d = M::dir(kd);
-          double val;
-          if (d < NQ) {
-            const int hs = M::hslot(d);
-            val = dq[d] + S * P.hc1[i] * dv[d] + dS * sh.rec.wq[d];
-            for (int l = 0; l < i; ++l) val += S * P.cq[i][l] * sh.KV[l][hs][col];
-          } else {
-            const int rv = d - NQ, hs = M::hslot(d - NQ);
-            val = dv[rv];
-            for (int l = 0; l < i; ++l) val += P.ha[i][l] * sh.KV[l][hs][col];
-          }
-          vals[kd] = val;
-        }
-        const double coef = uplus ? tau : (1.0 - tau);
-        const double hb = h * P.b[i];
-#pragma unroll
-        for (int rr = 0; rr < NR; ++rr) {
-          double acc = 0.0;
-#pragma unroll
-          for (int kd = 0; kd < NDIRX; ++kd) acc += sh.A[rr][kd] * vals[kd];
-          if (isU) acc += sh.A[rr][NDIRX + um] * coef;
-          const double dk = S * acc + dS * sh.rec.r[rr];
-          if (rr < NQ) {
-            const int hs = M::hslot(rr);
-            if (hs >= 0) {
-              if (i < 5) {
-                sh.KV[i][hs][col] = dk;
-              } else {
-                double incv = P.b[5] * dk, incq = 0.0;
-#pragma unroll
-                for (int l = 0; l < 5; ++l) {
-                  const double kv = sh.KV[l][hs][col];
-                  incv += P.b[l] * kv;
-                  incq += P.e2[l] * kv;
-                }
-                dq[rr] = dq[rr] + P.he1 * S * dv[rr] + S * incq + dS * sh.vbs[rr];
-                dv[rr] = dv[rr] + h * incv;
-              }
-            } else {
-              dv[rr] += hb * dk;
-              dq[rr] += S * P.e2[i] * dk;
-            }
-          } else {
-            dy[rr - NQ] += hb * dk;
-          }
-        }
-      }
-      __syncthreads();
-    }
-  }
-  double* jxb = jx + b * NXT * NXT;
-  double* jub = ju + b * NXT * 2 * NU;
-  double* jsb = js + b * NXT;
-  if (colthr) {
-    double* dst;
-    int stride;
-    if (col < NX) {
-      dst = jxb + col;
-      stride = NXT;
-    } else if (isU) {
-      dst = jub + uj;
-      stride = 2 * NU;
-    } else {
-      dst = jsb;
-      stride = 1;
-    }
-#pragma unroll
-    for (int k = 0; k < NQ; ++k) {
-      dst[k * stride] = dq[k];
-      dst[(NQ + k) * stride] = dv[k];
-    }
-#pragma unroll
-    for (int k = 0; k < NY; ++k) dst[(NX + k) * stride] = dy[k];
-  }
-  for (int e = tid; e < NXT * NY; e += blockDim.x) {  // y0 columns of jx: identity (rates ignore y)
-    const int r = e / Pos<NY>::v, c = NX + e % Pos<NY>::v;
-    jxb[r * NXT + c] = (r == c) ? 1.0 : 0.0;
-  }
-}
-
 // ===========================================================================
 // K1 (fused, warp-specialized, software-pipelined) -- one CTA per interval.
 //   warp 0      : primal producer.  Tick t computes RK stage t of the primal
@@ -950,8 +850,8 @@ __device__ __forceinline__ void fused_primal(const KParams& P, FusedShared<M>& s
   }
 }
 
-template <class M>
-__global__ void __launch_bounds__(FusedDims<M>::NT) k_linearize(const KParams P, int64_t B,
+template <class M, int MINB>
+__global__ void __launch_bounds__(FusedDims<M>::NT, MINB) k_linearize(const KParams P, int64_t B,
                                                                const double* __restrict__ xt0s,
                                                                const double* __restrict__ Us,
                                                                const double* __restrict__ Ss,
