@@ -782,9 +782,19 @@ struct FusedDims {
 };
 
 template <class M>
+struct PrimScratch {
+  static constexpr int NJ2 = Pos<2 * M::NJ>::v;
+  double W[3 * M::NL];
+  double Lw[NJ2 * (NJ2 + 1) / 2];
+  double y[NJ2];
+  double mo[Pos<M::NJ>::v];
+};
+
+template <class M>
 struct FusedShared {
   using D = Dims<M>;
   Rec<M> ring[3];
+  PrimScratch<M> ps;
   double A[2][D::NR][D::NDIR];
   double KV[5][D::NH][D::NCOLP];
   double PQ[Pos<M::NPUSH>::v][D::NCOLP];
@@ -802,44 +812,331 @@ struct FusedShared {
   int bad;
 };
 
+// Warp-cooperative primal stage (the same arithmetic as prim_rate, spread over
+// the 32 lanes of warp 0: links, joint sides, contacts, Gram blocks in
+// parallel; only the sparse Cholesky + solves run on one lane).
 template <class M>
 __device__ __forceinline__ void fused_primal(const KParams& P, FusedShared<M>& sh, int t, int lane) {
   using D = Dims<M>;
-  constexpr int NQ = D::NQ, NX = D::NX, NU = D::NU, NY = D::NY, NR = D::NR;
+  constexpr int NL = M::NL, NJ = M::NJ, NC = M::NC, NA = M::NA, NQ = D::NQ, NX = D::NX, NU = D::NU, NY = D::NY;
+  constexpr int NR = D::NR, NJ2 = 2 * NJ;
   const int s = t / 6, i = t % 6;
   const double h = P.h, S = sh.S;
   const double tau = h * (double)s + P.ch[i];
   Rec<M>& R = sh.ring[t % 3];
-  for (int k = lane; k < NX; k += 32) {  // stage input (cito/augmentation.py:200-205)
+  Prim<M>& pr = R.pr;
+  PrimScratch<M>& w = sh.ps;
+  const double* q = sh.xs;
+  const double* v = sh.xs + NQ;
+  // 0: stage input (cito/augmentation.py:200-205)
+  for (int k = lane; k < NX; k += 32) {
     double a = sh.x[k];
     for (int j = 0; j < i; ++j) a = a + P.ha[i][j] * sh.K[j][k];
     sh.xs[k] = a;
   }
   __syncwarp();
-  if (lane == 0) {
-    double u[Pos<NU>::v];
-#pragma unroll
-    for (int m = 0; m < NU; ++m) u[m] = (1.0 - tau) * sh.U[m] + tau * sh.U[NU + m];  // foh_eval :166-169
-    prim_rate<M>(P, sh.xs, u, R.pr, sh.rf);
+  // 1: cos/sin per link, FOH control (foh_eval :166-169)
+  for (int e = lane; e < NL + NU; e += 32) {
+    if (e < NL) {
+      double sv, cv;
+      sincos(q[3 * e + 2], &sv, &cv);
+      pr.s[e] = sv;
+      pr.c[e] = cv;
+    } else {
+      const int m = e - NL;
+      pr.u[m] = (1.0 - tau) * sh.U[m] + tau * sh.U[NU + m];
+    }
   }
   __syncwarp();
-  for (int k = lane; k < NX; k += 32) sh.K[i][k] = S * sh.rf[k];
-  for (int k = lane; k < NY; k += 32) sh.ky[k] = (i == 0 ? 0.0 : sh.ky[k]) + P.b[i] * (S * sh.rf[NX + k]);
+  // 2: rotated joint anchors, contacts (frame, force, Omega ingredients), joint moments
+  for (int e = lane; e < 2 * NJ + NC + NJ; e += 32) {
+    if (e < 2 * NJ) {
+      const int j = e >> 1, side = e & 1;
+      const int l = side ? M::jchild(j) : M::jparent(j);
+      if (l >= 0) {
+        const double ax = side ? P.jrc[j][0] : P.jrp[j][0], az = side ? P.jrc[j][1] : P.jrp[j][1];
+        const double c = pr.c[l], sn = pr.s[l];
+        double* Rj = side ? pr.rc[j] : pr.rp[j];
+        Rj[0] = c * ax - sn * az;
+        Rj[1] = sn * ax + c * az;
+      }
+    } else if (e < 2 * NJ + NC) {
+      const int ci = e - 2 * NJ, l = M::clink(ci);
+      const double c = pr.c[l], sn = pr.s[l];
+      const double rx = c * P.cr[ci][0] - sn * P.cr[ci][1];
+      const double rz = sn * P.cr[ci][0] + c * P.cr[ci][1];
+      pr.rr[ci][0] = rx;
+      pr.rr[ci][1] = rz;
+      const double Px = q[3 * l] + rx, Pz = q[3 * l + 1] + rz;
+      double n0, n1, sd;
+      if constexpr (M::IMPLICIT) {
+        T2 t2 = surface_t2(P, Px, Pz);
+        pr.hv[ci] = t2.v;
+        pr.g[ci][0] = t2.gx;
+        pr.g[ci][1] = t2.gz;
+        pr.H[ci][0] = t2.hxx;
+        pr.H[ci][1] = t2.hxz;
+        pr.H[ci][2] = t2.hzz;
+        const double gn = sqrt(t2.gx * t2.gx + t2.gz * t2.gz);
+        pr.gn[ci] = gn;
+        n0 = t2.gx / gn;
+        n1 = t2.gz / gn;
+        sd = t2.v / gn;
+      } else {
+        n0 = 0.0;
+        n1 = 1.0;
+        sd = Pz - P.height;
+      }
+      pr.sd[ci] = sd;
+      const double t0 = n1, t1 = -n0;
+      pr.n[ci][0] = n0;
+      pr.n[ci][1] = n1;
+      pr.t[ci][0] = t0;
+      pr.t[ci][1] = t1;
+      const double ft = pr.u[NA + 2 * ci], fn = pr.u[NA + 2 * ci + 1], gam = pr.u[NA + 2 * NC + ci];
+      pr.F[ci][0] = t0 * ft + n0 * fn;
+      pr.F[ci][1] = t1 * ft + n1 * fn;
+      const double om = v[3 * l + 2];
+      const double Jv0 = v[3 * l] + (-rz) * om, Jv1 = v[3 * l + 1] + rx * om;
+      pr.Jv[ci][0] = Jv0;
+      pr.Jv[ci][1] = Jv1;
+      const double sgt = ft / sqrt(ft * ft + 1.0);  // friction_stationarity (contact_dynamics.py:55-66)
+      pr.sg[ci] = sgt;
+      pr.lamc[ci] = t0 * Jv0 + t1 * Jv1 + gam * sgt;
+    } else {
+      const int j = e - 2 * NJ - NC;  // joint moment (multibody.py:303-320)
+      const int p = M::jparent(j), c = M::jchild(j), a = M::jact(j);
+      double mo = 0.0;
+      if (a >= 0) mo = mo + pr.u[a];
+      if (P.jspring[j]) {
+        const double th_p = p >= 0 ? q[3 * p + 2] : 0.0;
+        const double om_p = p >= 0 ? v[3 * p + 2] : 0.0;
+        const double rel = q[3 * c + 2] - th_p - P.jrest[j];
+        mo = mo - P.jk[j] * rel - P.jd[j] * (v[3 * c + 2] - om_p);
+      }
+      w.mo[j] = mo;
+    }
+  }
+  __syncwarp();
+  // 3: generalized forces per link; Gram blocks (elimination order, nonzero blocks only)
+  for (int e = lane; e < NL + M::NBLK; e += 32) {
+    if (e < NL) {
+      const int l = e;
+      double W0 = 0.0, W1 = P.neg_mg[l], W2 = 0.0;
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        if (M::jchild(j) == l) W2 += w.mo[j];
+        if (M::jparent(j) == l) W2 += -w.mo[j];
+      }
+#pragma unroll
+      for (int ci = 0; ci < NC; ++ci)
+        if (M::clink(ci) == l) {
+          const double F0 = pr.F[ci][0], F1 = pr.F[ci][1];
+          W0 += F0;
+          W1 += F1;
+          W2 += (-pr.rr[ci][1]) * F0 + pr.rr[ci][0] * F1;
+        }
+      w.W[3 * l] = W0;
+      w.W[3 * l + 1] = W1;
+      w.W[3 * l + 2] = W2;
+    } else if constexpr (NJ > 0) {
+      const int kb = e - NL, a = M::blk_a(kb), bp = M::blk_b(kb);
+      const int j = M::jperm(a), k = M::jperm(bp);
+      double g00 = 0.0, g01 = 0.0, g10 = 0.0, g11 = 0.0;
+#pragma unroll
+      for (int sa = 0; sa < 2; ++sa)
+#pragma unroll
+        for (int sb = 0; sb < 2; ++sb) {
+          const int la = sa == 0 ? M::jparent(j) : M::jchild(j);
+          const int lb = sb == 0 ? M::jparent(k) : M::jchild(k);
+          if (la < 0 || la != lb) continue;
+          const double sg = (sa == sb) ? 1.0 : -1.0;
+          const double* Ra = sa == 0 ? pr.rp[j] : pr.rc[j];
+          const double* Rb = sb == 0 ? pr.rp[k] : pr.rc[k];
+          const double dA0 = -Ra[1], dA1 = Ra[0], dB0 = -Rb[1], dB1 = Rb[0];
+          const double mI = P.minv_I[la], mm = P.minv_m[la];
+          g00 += sg * (dA0 * dB0 * mI + mm);
+          g01 += sg * (dA0 * dB1 * mI);
+          g10 += sg * (dA1 * dB0 * mI);
+          g11 += sg * (dA1 * dB1 * mI + mm);
+        }
+      w.Lw[LI(2 * a, 2 * bp)] = g00;
+      w.Lw[LI(2 * a + 1, 2 * bp)] = g10;
+      w.Lw[LI(2 * a + 1, 2 * bp + 1)] = g11;
+      if (a != bp) w.Lw[LI(2 * a, 2 * bp + 1)] = g01;
+    }
+  }
+  __syncwarp();
+  if constexpr (NJ > 0) {
+    // 4: rhs = J (M^-1 W) + curv, per joint (elimination order)
+    for (int a = lane; a < NJ; a += 32) {
+      const int j = M::jperm(a);
+#pragma unroll
+      for (int al = 0; al < 2; ++al) {
+        double acc = 0.0;
+#pragma unroll
+        for (int sa = 0; sa < 2; ++sa) {
+          const int l = sa == 0 ? M::jparent(j) : M::jchild(j);
+          if (l < 0) continue;
+          const double sgn = sa == 0 ? 1.0 : -1.0;
+          const double* Rj = sa == 0 ? pr.rp[j] : pr.rc[j];
+          const double dP = al == 0 ? -Rj[1] : Rj[0];
+          const double om = v[3 * l + 2];
+          acc += sgn * (P.minv_m[l] * w.W[3 * l + al] + dP * P.minv_I[l] * w.W[3 * l + 2] - Rj[al] * om * om);
+        }
+        w.y[2 * a + al] = acc;
+      }
+    }
+    __syncwarp();
+    // 5: sparse Cholesky + both triangular solves on one lane, in registers
+    if (lane == 0) {
+      double Lr[NJ2 * (NJ2 + 1) / 2], y[NJ2], Lir[NJ2];
+#pragma unroll
+      for (int r = 0; r < NJ2; ++r) {
+        y[r] = w.y[r];
+#pragma unroll
+        for (int c = 0; c <= r; ++c) Lr[LI(r, c)] = M::lnzb(r / 2, c / 2) ? w.Lw[LI(r, c)] : 0.0;
+      }
+      // fill-in positions (none for trees) start from zero
+#pragma unroll
+      for (int cc = 0; cc < NJ2; ++cc) {
+        double d = Lr[LI(cc, cc)];
+#pragma unroll
+        for (int k = 0; k < cc; ++k)
+          if (M::lnzb(cc / 2, k / 2)) d -= Lr[LI(cc, k)] * Lr[LI(cc, k)];
+        const double lcc = sqrt(d);
+        Lr[LI(cc, cc)] = lcc;
+        const double il = 1.0 / lcc;
+        Lir[cc] = il;
+#pragma unroll
+        for (int r = cc + 1; r < NJ2; ++r) {
+          if (!M::lnzb(r / 2, cc / 2)) continue;
+          double x = Lr[LI(r, cc)];
+#pragma unroll
+          for (int k = 0; k < cc; ++k)
+            if (M::lnzb(r / 2, k / 2) && M::lnzb(cc / 2, k / 2)) x -= Lr[LI(r, k)] * Lr[LI(cc, k)];
+          Lr[LI(r, cc)] = x * il;
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < NJ2; ++r) {
+        double x = y[r];
+#pragma unroll
+        for (int k = 0; k < r; ++k)
+          if (M::lnzb(r / 2, k / 2)) x -= Lr[LI(r, k)] * y[k];
+        y[r] = x * Lir[r];
+      }
+#pragma unroll
+      for (int r = NJ2 - 1; r >= 0; --r) {
+        double x = y[r];
+#pragma unroll
+        for (int k = r + 1; k < NJ2; ++k)
+          if (M::lnzb(k / 2, r / 2)) x -= Lr[LI(k, r)] * y[k];
+        y[r] = x * Lir[r];
+      }
+#pragma unroll
+      for (int r = 0; r < NJ2; ++r) {
+        pr.Li[r] = Lir[r];
+#pragma unroll
+        for (int c = 0; c <= r; ++c)
+          if (M::lnzb(r / 2, c / 2)) pr.L[LI(r, c)] = Lr[LI(r, c)];
+      }
+#pragma unroll
+      for (int a = 0; a < NJ; ++a) {
+        pr.lam[2 * M::jperm(a)] = -y[2 * a];
+        pr.lam[2 * M::jperm(a) + 1] = -y[2 * a + 1];
+      }
+    }
+    __syncwarp();
+  }
+  // 6: vdot per link (M^-1 (W + J^T lam)), Omega per contact, mixed path rows
+  double* rf = sh.rf;
+  for (int e = lane; e < NL + NC + (M::NGO > 0 ? 1 : 0); e += 32) {
+    if (e < NL) {
+      const int l = e;
+      double W0 = w.W[3 * l], W1 = w.W[3 * l + 1], W2 = w.W[3 * l + 2];
+#pragma unroll
+      for (int j = 0; j < NJ; ++j)
+#pragma unroll
+        for (int sa = 0; sa < 2; ++sa) {
+          const int lj = sa == 0 ? M::jparent(j) : M::jchild(j);
+          if (lj != l) continue;
+          const double sgn = sa == 0 ? 1.0 : -1.0;
+          const double* Rj = sa == 0 ? pr.rp[j] : pr.rc[j];
+          const double l0 = pr.lam[2 * j], l1 = pr.lam[2 * j + 1];
+          W0 += sgn * l0;
+          W1 += sgn * l1;
+          W2 += sgn * ((-Rj[1]) * l0 + Rj[0] * l1);
+        }
+      rf[NQ + 3 * l] = P.minv_m[l] * W0;
+      rf[NQ + 3 * l + 1] = P.minv_m[l] * W1;
+      const double vd2 = P.minv_I[l] * W2;
+      rf[NQ + 3 * l + 2] = vd2;
+      pr.vdot[3 * l + 2] = vd2;
+    } else if (e < NL + NC) {
+      const int ci = e - NL;
+      const double ft = pr.u[NA + 2 * ci], fn = pr.u[NA + 2 * ci + 1], gam = pr.u[NA + 2 * NC + ci];
+      double* yo = rf + 2 * NQ + 5 * ci;
+      yo[0] = fn;
+      yo[1] = sabs(pr.lamc[ci]);
+      yo[2] = gam;
+      yo[3] = sabs(P.mu[ci] * fn) - sabs(ft);
+      yo[4] = srelu(pr.sd[ci]);
+    } else if constexpr (M::NGO > 0) {
+      constexpr int NG = Prim<M>::NG;
+      double gpl[Pos<NG>::v];
+      int r = 0;
+#pragma unroll
+      for (int ci = 0; ci < NC; ++ci) gpl[r++] = -pr.sd[ci];
+#pragma unroll
+      for (int k = 0; k < M::NJL; ++k) {
+        const int jj = M::jl_joint(k);
+        const int p = M::jparent(jj), c = M::jchild(jj);
+        const double rel = q[3 * c + 2] - (p >= 0 ? q[3 * p + 2] : 0.0);
+        gpl[r++] = rel - P.jl_hi[k];
+        gpl[r++] = P.jl_lo[k] - rel;
+      }
+#pragma unroll
+      for (int k = 0; k < M::NHB; ++k) {
+        const double pz = q[3 * M::hb_link(k) + 1];
+        gpl[r++] = P.hb_lo[k] - pz;
+        gpl[r++] = pz - P.hb_hi[k];
+      }
+      double sgv[Pos<NG>::v];
+#pragma unroll
+      for (int jg = 0; jg < NG; ++jg) {
+        pr.gp[jg] = gpl[jg];
+        sgv[jg] = srelu(gpl[jg]);
+      }
+#pragma unroll
+      for (int o = 0; o < M::NGO; ++o) {
+        double acc = 0.0;
+#pragma unroll
+        for (int jg = 0; jg < NG; ++jg) acc += P.mix[o][jg] * sgv[jg];
+        rf[2 * NQ + 5 * NC + o] = acc;
+      }
+    }
+  }
+  for (int k = lane; k < NQ; k += 32) rf[k] = v[k];
+  __syncwarp();
+  // 7: stage bookkeeping
+  for (int k = lane; k < NX; k += 32) sh.K[i][k] = S * rf[k];
+  for (int k = lane; k < NY; k += 32) sh.ky[k] = (i == 0 ? 0.0 : sh.ky[k]) + P.b[i] * (S * rf[NX + k]);
   for (int k = lane; k < NQ; k += 32) {
-    const double vsk = sh.xs[NQ + k];
+    const double vsk = v[k];
     sh.VS[i][k] = vsk;
     R.vs[k] = vsk;
-    double w = 0.0;
-    for (int j = 0; j < i; ++j) w += P.ha[i][j] * sh.VS[j][k];
-    R.wq[k] = w;
+    double ws = 0.0;
+    for (int j = 0; j < i; ++j) ws += P.ha[i][j] * sh.VS[j][k];
+    R.wq[k] = ws;
   }
-  for (int k = lane; k < NR; k += 32) R.r[k] = sh.rf[NQ + k];
+  for (int k = lane; k < NR; k += 32) R.r[k] = rf[NQ + k];
   __syncwarp();
   if (i == 5) {  // end of substep: x <- x + h sum_i b_i k_i (:209)
     for (int k = lane; k < NQ; k += 32) {
-      double w = 0.0;
-      for (int j = 0; j < 6; ++j) w += P.b[j] * sh.VS[j][k];
-      sh.vbs[s & 1][k] = h * w;
+      double ws = 0.0;
+      for (int j = 0; j < 6; ++j) ws += P.b[j] * sh.VS[j][k];
+      sh.vbs[s & 1][k] = h * ws;
     }
     for (int k = lane; k < NX; k += 32) {
       double inc = 0.0;
