@@ -440,4 +440,10 @@ double cito_dfma_peak(int32_t iters, double* out_dev, void* stream) {
   return 2.0 * 64.0 * (double)iters * blocks * threads;  // flops issued
 }
 
+#ifdef CITO_PROF
+int cito_prof_set(long long* dev_buf) {
+  return (int)cudaMemcpyToSymbol(g_cito_prof, &dev_buf, sizeof(dev_buf));
+}
+#endif
+
 }  // extern "C"

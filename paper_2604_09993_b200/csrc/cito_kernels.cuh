@@ -59,6 +59,20 @@ struct KParams {
 
 #define LI(r, c) ((r) * ((r) + 1) / 2 + (c))
 
+// Optional per-role cycle instrumentation (tools/role_timing.py builds a separate
+// library with -DCITO_PROF; the product build has none of it).
+#ifdef CITO_PROF
+__device__ long long* g_cito_prof = nullptr;
+#define CITO_MARK(slot)                                                        \
+  do {                                                                         \
+    if (g_cito_prof && blockIdx.x == 0 && (threadIdx.x & 31) == 0) g_cito_prof[(slot)] = clock64(); \
+  } while (0)
+#else
+#define CITO_MARK(slot) \
+  do {                  \
+  } while (0)
+#endif
+
 template <int N>
 struct Pos {
   static constexpr int v = N > 0 ? N : 1;
@@ -1197,6 +1211,7 @@ __global__ void __launch_bounds__(FusedDims<M>::NT, MINB) k_linearize(const KPar
   const double S = sh.S, h = P.h;
   const int NST = 6 * P.substeps;
   for (int t = 0; t < NST + 2; ++t) {
+    CITO_MARK((t * 8 + warp) * 2);
     if (warp == 0) {
       if (t < NST) fused_primal<M>(P, sh, t, lane);
     } else if (warp == 1) {
@@ -1269,6 +1284,7 @@ __global__ void __launch_bounds__(FusedDims<M>::NT, MINB) k_linearize(const KPar
         }
       }
     }
+    CITO_MARK((t * 8 + warp) * 2 + 1);
     __syncthreads();
   }
   // ---- outputs

@@ -1,0 +1,71 @@
+"""Per-role cycle timing of the fused linearize kernel (CTA 0), via a -DCITO_PROF build.
+
+  python tools/role_timing.py build          # (CPU) build paper_2604_09993_b200/_lib/libcito_b200_prof.so
+  python tools/role_timing.py run [B]        # (GPU) print per-tick cycles of each warp role
+"""
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+PROF_SO = os.path.join(ROOT, "paper_2604_09993_b200", "_lib", "libcito_b200_prof.so")
+
+
+def build():
+    from paper_2604_09993_b200 import build as b
+
+    b.build()  # regenerates models_gen.cuh
+    cmd = [b.NVCC, "-std=c++17", "-O3", "-lineinfo", "-gencode", "arch=compute_100a,code=sm_100a", "-DCITO_PROF",
+           "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"),
+           "-o", PROF_SO, os.path.join(b.CSRC, "cito_capi.cu"), "-lcudart"]
+    subprocess.check_call(cmd)
+
+
+def run(B):
+    import ctypes
+
+    import numpy as np
+    import torch
+
+    from paper_2604_09993_b200 import _lib
+
+    _lib.SO_PATH = PROF_SO
+    from paper_2604_09993_b200 import scenario as S, synth, Discretizer
+
+    L = _lib.lib()
+    L.cito_prof_set.argtypes = [ctypes.c_void_p]
+    sc = S.bundled("halfcheetah_bound", N=30)
+    g, n_g = sc.path_constraints()
+    disc = Discretizer(sc.model, sc.mixing_matrix(n_g), g, substeps=sc.substeps)
+    x, U, Sv = synth.random_intervals(sc, B, seed=0)
+    dev = torch.device("cuda")
+    xd, Ud, Sd = (torch.as_tensor(a, device=dev) for a in (x, U, Sv))
+    buf = torch.zeros(40 * 8 * 2, dtype=torch.int64, device=dev)
+    for _ in range(3):
+        disc.linearize_batch_device(xd, Ud, Sd)
+    torch.cuda.synchronize()
+    assert L.cito_prof_set(buf.data_ptr()) == 0
+    disc.linearize_batch_device(xd, Ud, Sd)
+    torch.cuda.synchronize()
+    L.cito_prof_set(None)
+    a = buf.cpu().numpy().reshape(40, 8, 2).astype(np.int64)
+    nt = 32
+    t0 = a[0, :, 0][a[0, :, 0] > 0].min()
+    print("tick  " + "  ".join(f"w{w}:work" for w in range(5)) + "   tick_total")
+    tot = []
+    for t in range(nt):
+        st, en = a[t, :5, 0], a[t, :5, 1]
+        if not (st > 0).all():
+            continue
+        nxt = a[t + 1, :5, 0].min() if t + 1 < nt and (a[t + 1, :5, 0] > 0).all() else en.max()
+        tot.append(nxt - st.min())
+        print(f"{t:4d}  " + "  ".join(f"{int(e - s):8d}" for s, e in zip(st, en)) + f"   {int(nxt - st.min()):8d}")
+    print("total cycles", int(a[nt - 1, :5, 1].max() - t0), "mean tick", float(np.mean(tot)))
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "build":
+        build()
+    else:
+        run(int(sys.argv[2]) if len(sys.argv) > 2 else 29)
