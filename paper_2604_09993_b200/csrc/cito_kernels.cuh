@@ -67,7 +67,14 @@ __device__ long long* g_cito_prof = nullptr;
   do {                                                                         \
     if (g_cito_prof && blockIdx.x == 0 && (threadIdx.x & 31) == 0) g_cito_prof[(slot)] = clock64(); \
   } while (0)
+#define CITO_MARK_P(t, k)                                                                  \
+  do {                                                                                     \
+    if (g_cito_prof && blockIdx.x == 0 && threadIdx.x == 0) g_cito_prof[1024 + (t) * 16 + (k)] = clock64(); \
+  } while (0)
 #else
+#define CITO_MARK_P(t, k) \
+  do {                    \
+  } while (0)
 #define CITO_MARK(slot) \
   do {                  \
   } while (0)
@@ -842,6 +849,7 @@ __device__ __forceinline__ void fused_primal(const KParams& P, FusedShared<M>& s
   PrimScratch<M>& w = sh.ps;
   const double* q = sh.xs;
   const double* v = sh.xs + NQ;
+  CITO_MARK_P(t, 0);
   // 0: stage input (cito/augmentation.py:200-205)
   for (int k = lane; k < NX; k += 32) {
     double a = sh.x[k];
@@ -849,6 +857,7 @@ __device__ __forceinline__ void fused_primal(const KParams& P, FusedShared<M>& s
     sh.xs[k] = a;
   }
   __syncwarp();
+  CITO_MARK_P(t, 1);
   // 1: cos/sin per link, FOH control (foh_eval :166-169)
   for (int e = lane; e < NL + NU; e += 32) {
     if (e < NL) {
@@ -862,6 +871,7 @@ __device__ __forceinline__ void fused_primal(const KParams& P, FusedShared<M>& s
     }
   }
   __syncwarp();
+  CITO_MARK_P(t, 2);
   // 2: rotated joint anchors, contacts (frame, force, Omega ingredients), joint moments
   for (int e = lane; e < 2 * NJ + NC + NJ; e += 32) {
     if (e < 2 * NJ) {
@@ -932,6 +942,7 @@ __device__ __forceinline__ void fused_primal(const KParams& P, FusedShared<M>& s
     }
   }
   __syncwarp();
+  CITO_MARK_P(t, 3);
   // 3: generalized forces per link; Gram blocks (elimination order, nonzero blocks only)
   for (int e = lane; e < NL + M::NBLK; e += 32) {
     if (e < NL) {
@@ -981,6 +992,7 @@ __device__ __forceinline__ void fused_primal(const KParams& P, FusedShared<M>& s
     }
   }
   __syncwarp();
+  CITO_MARK_P(t, 4);
   if constexpr (NJ > 0) {
     // 4: rhs = J (M^-1 W) + curv, per joint (elimination order)
     for (int a = lane; a < NJ; a += 32) {
@@ -1002,6 +1014,7 @@ __device__ __forceinline__ void fused_primal(const KParams& P, FusedShared<M>& s
       }
     }
     __syncwarp();
+  CITO_MARK_P(t, 5);
     // 5: sparse Cholesky + both triangular solves on one lane, in registers
     if (lane == 0) {
       double Lr[NJ2 * (NJ2 + 1) / 2], y[NJ2], Lir[NJ2];
@@ -1062,6 +1075,7 @@ __device__ __forceinline__ void fused_primal(const KParams& P, FusedShared<M>& s
       }
     }
     __syncwarp();
+  CITO_MARK_P(t, 6);
   }
   // 6: vdot per link (M^-1 (W + J^T lam)), Omega per contact, mixed path rows
   double* rf = sh.rf;
@@ -1133,6 +1147,7 @@ __device__ __forceinline__ void fused_primal(const KParams& P, FusedShared<M>& s
   }
   for (int k = lane; k < NQ; k += 32) rf[k] = v[k];
   __syncwarp();
+  CITO_MARK_P(t, 7);
   // 7: stage bookkeeping
   for (int k = lane; k < NX; k += 32) sh.K[i][k] = S * rf[k];
   for (int k = lane; k < NY; k += 32) sh.ky[k] = (i == 0 ? 0.0 : sh.ky[k]) + P.b[i] * (S * rf[NX + k]);
@@ -1146,6 +1161,7 @@ __device__ __forceinline__ void fused_primal(const KParams& P, FusedShared<M>& s
   }
   for (int k = lane; k < NR; k += 32) R.r[k] = rf[NQ + k];
   __syncwarp();
+  CITO_MARK_P(t, 8);
   if (i == 5) {  // end of substep: x <- x + h sum_i b_i k_i (:209)
     for (int k = lane; k < NQ; k += 32) {
       double ws = 0.0;
