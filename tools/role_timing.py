@@ -41,7 +41,7 @@ def run(B):
     x, U, Sv = synth.random_intervals(sc, B, seed=0)
     dev = torch.device("cuda")
     xd, Ud, Sd = (torch.as_tensor(a, device=dev) for a in (x, U, Sv))
-    buf = torch.zeros(40 * 8 * 2, dtype=torch.int64, device=dev)
+    buf = torch.zeros(1024 + 40 * 16, dtype=torch.int64, device=dev)
     for _ in range(3):
         disc.linearize_batch_device(xd, Ud, Sd)
     torch.cuda.synchronize()
@@ -49,7 +49,12 @@ def run(B):
     disc.linearize_batch_device(xd, Ud, Sd)
     torch.cuda.synchronize()
     L.cito_prof_set(None)
-    a = buf.cpu().numpy().reshape(40, 8, 2).astype(np.int64)
+    full = buf.cpu().numpy().astype(np.int64)
+    a = full[:640].reshape(40, 8, 2)
+    pp = full[1024:].reshape(40, 16)
+    for t in (3, 10, 17):
+        row = pp[t][pp[t] > 0]
+        print("primal tick", t, "sub-step cycles", np.diff(row).tolist())
     nt = 32
     t0 = a[0, :, 0][a[0, :, 0] > 0].min()
     print("tick  " + "  ".join(f"w{w}:work" for w in range(5)) + "   tick_total")
