@@ -803,6 +803,15 @@ struct FusedDims {
 };
 
 template <class M>
+struct SParams {
+  static constexpr int NL = M::NL, NJ = Pos<M::NJ>::v, NC = Pos<M::NC>::v;
+  double minv_m[NL], minv_I[NL], neg_mg[NL];
+  double jrp[NJ][2], jrc[NJ][2], jk[NJ], jd[NJ], jrest[NJ];
+  int jspring[NJ];
+  double cr[NC][2], mu[NC];
+};
+
+template <class M>
 struct PrimScratch {
   static constexpr int NJ2 = Pos<2 * M::NJ>::v;
   double W[3 * M::NL];
@@ -816,6 +825,7 @@ struct FusedShared {
   using D = Dims<M>;
   Rec<M> ring[3];
   PrimScratch<M> ps;
+  SParams<M> sp;
   double A[2][D::NR][D::NDIR];
   double KV[5][D::NH][D::NCOLP];
   double PQ[Pos<M::NPUSH>::v][D::NCOLP];
@@ -847,6 +857,7 @@ __device__ __forceinline__ void fused_primal(const KParams& P, FusedShared<M>& s
   Rec<M>& R = sh.ring[t % 3];
   Prim<M>& pr = R.pr;
   PrimScratch<M>& w = sh.ps;
+  const SParams<M>& Q = sh.sp;  // runtime-indexed parameters live in smem (divergent lanes)
   const double* q = sh.xs;
   const double* v = sh.xs + NQ;
   CITO_MARK_P(t, 0);
@@ -878,7 +889,7 @@ __device__ __forceinline__ void fused_primal(const KParams& P, FusedShared<M>& s
       const int j = e >> 1, side = e & 1;
       const int l = side ? M::jchild(j) : M::jparent(j);
       if (l >= 0) {
-        const double ax = side ? P.jrc[j][0] : P.jrp[j][0], az = side ? P.jrc[j][1] : P.jrp[j][1];
+        const double ax = side ? Q.jrc[j][0] : Q.jrp[j][0], az = side ? Q.jrc[j][1] : Q.jrp[j][1];
         const double c = pr.c[l], sn = pr.s[l];
         double* Rj = side ? pr.rc[j] : pr.rp[j];
         Rj[0] = c * ax - sn * az;
@@ -887,8 +898,8 @@ __device__ __forceinline__ void fused_primal(const KParams& P, FusedShared<M>& s
     } else if (e < 2 * NJ + NC) {
       const int ci = e - 2 * NJ, l = M::clink(ci);
       const double c = pr.c[l], sn = pr.s[l];
-      const double rx = c * P.cr[ci][0] - sn * P.cr[ci][1];
-      const double rz = sn * P.cr[ci][0] + c * P.cr[ci][1];
+      const double rx = c * Q.cr[ci][0] - sn * Q.cr[ci][1];
+      const double rz = sn * Q.cr[ci][0] + c * Q.cr[ci][1];
       pr.rr[ci][0] = rx;
       pr.rr[ci][1] = rz;
       const double Px = q[3 * l] + rx, Pz = q[3 * l + 1] + rz;
@@ -932,11 +943,11 @@ __device__ __forceinline__ void fused_primal(const KParams& P, FusedShared<M>& s
       const int p = M::jparent(j), c = M::jchild(j), a = M::jact(j);
       double mo = 0.0;
       if (a >= 0) mo = mo + pr.u[a];
-      if (P.jspring[j]) {
+      if (Q.jspring[j]) {
         const double th_p = p >= 0 ? q[3 * p + 2] : 0.0;
         const double om_p = p >= 0 ? v[3 * p + 2] : 0.0;
-        const double rel = q[3 * c + 2] - th_p - P.jrest[j];
-        mo = mo - P.jk[j] * rel - P.jd[j] * (v[3 * c + 2] - om_p);
+        const double rel = q[3 * c + 2] - th_p - Q.jrest[j];
+        mo = mo - Q.jk[j] * rel - Q.jd[j] * (v[3 * c + 2] - om_p);
       }
       w.mo[j] = mo;
     }
@@ -947,7 +958,7 @@ __device__ __forceinline__ void fused_primal(const KParams& P, FusedShared<M>& s
   for (int e = lane; e < NL + M::NBLK; e += 32) {
     if (e < NL) {
       const int l = e;
-      double W0 = 0.0, W1 = P.neg_mg[l], W2 = 0.0;
+      double W0 = 0.0, W1 = Q.neg_mg[l], W2 = 0.0;
 #pragma unroll
       for (int j = 0; j < NJ; ++j) {
         if (M::jchild(j) == l) W2 += w.mo[j];
@@ -979,7 +990,7 @@ __device__ __forceinline__ void fused_primal(const KParams& P, FusedShared<M>& s
           const double* Ra = sa == 0 ? pr.rp[j] : pr.rc[j];
           const double* Rb = sb == 0 ? pr.rp[k] : pr.rc[k];
           const double dA0 = -Ra[1], dA1 = Ra[0], dB0 = -Rb[1], dB1 = Rb[0];
-          const double mI = P.minv_I[la], mm = P.minv_m[la];
+          const double mI = Q.minv_I[la], mm = Q.minv_m[la];
           g00 += sg * (dA0 * dB0 * mI + mm);
           g01 += sg * (dA0 * dB1 * mI);
           g10 += sg * (dA1 * dB0 * mI);
@@ -1008,7 +1019,7 @@ __device__ __forceinline__ void fused_primal(const KParams& P, FusedShared<M>& s
           const double* Rj = sa == 0 ? pr.rp[j] : pr.rc[j];
           const double dP = al == 0 ? -Rj[1] : Rj[0];
           const double om = v[3 * l + 2];
-          acc += sgn * (P.minv_m[l] * w.W[3 * l + al] + dP * P.minv_I[l] * w.W[3 * l + 2] - Rj[al] * om * om);
+          acc += sgn * (Q.minv_m[l] * w.W[3 * l + al] + dP * Q.minv_I[l] * w.W[3 * l + 2] - Rj[al] * om * om);
         }
         w.y[2 * a + al] = acc;
       }
@@ -1031,9 +1042,9 @@ __device__ __forceinline__ void fused_primal(const KParams& P, FusedShared<M>& s
 #pragma unroll
         for (int k = 0; k < cc; ++k)
           if (M::lnzb(cc / 2, k / 2)) d -= Lr[LI(cc, k)] * Lr[LI(cc, k)];
-        const double lcc = sqrt(d);
+        const double il = rsqrt(d);
+        const double lcc = d * il;
         Lr[LI(cc, cc)] = lcc;
-        const double il = 1.0 / lcc;
         Lir[cc] = il;
 #pragma unroll
         for (int r = cc + 1; r < NJ2; ++r) {
@@ -1096,9 +1107,9 @@ __device__ __forceinline__ void fused_primal(const KParams& P, FusedShared<M>& s
           W1 += sgn * l1;
           W2 += sgn * ((-Rj[1]) * l0 + Rj[0] * l1);
         }
-      rf[NQ + 3 * l] = P.minv_m[l] * W0;
-      rf[NQ + 3 * l + 1] = P.minv_m[l] * W1;
-      const double vd2 = P.minv_I[l] * W2;
+      rf[NQ + 3 * l] = Q.minv_m[l] * W0;
+      rf[NQ + 3 * l + 1] = Q.minv_m[l] * W1;
+      const double vd2 = Q.minv_I[l] * W2;
       rf[NQ + 3 * l + 2] = vd2;
       pr.vdot[3 * l + 2] = vd2;
     } else if (e < NL + NC) {
@@ -1108,7 +1119,7 @@ __device__ __forceinline__ void fused_primal(const KParams& P, FusedShared<M>& s
       yo[0] = fn;
       yo[1] = sabs(pr.lamc[ci]);
       yo[2] = gam;
-      yo[3] = sabs(P.mu[ci] * fn) - sabs(ft);
+      yo[3] = sabs(Q.mu[ci] * fn) - sabs(ft);
       yo[4] = srelu(pr.sd[ci]);
     } else if constexpr (M::NGO > 0) {
       constexpr int NG = Prim<M>::NG;
@@ -1199,6 +1210,26 @@ __global__ void __launch_bounds__(FusedDims<M>::NT, MINB) k_linearize(const KPar
     sh.S = Ss[b];
     sh.bad = 0;
   }
+  for (int l = tid; l < M::NL; l += blockDim.x) {
+    sh.sp.minv_m[l] = P.minv_m[l];
+    sh.sp.minv_I[l] = P.minv_I[l];
+    sh.sp.neg_mg[l] = P.neg_mg[l];
+  }
+  for (int j = tid; j < M::NJ; j += blockDim.x) {
+    sh.sp.jrp[j][0] = P.jrp[j][0];
+    sh.sp.jrp[j][1] = P.jrp[j][1];
+    sh.sp.jrc[j][0] = P.jrc[j][0];
+    sh.sp.jrc[j][1] = P.jrc[j][1];
+    sh.sp.jk[j] = P.jk[j];
+    sh.sp.jd[j] = P.jd[j];
+    sh.sp.jrest[j] = P.jrest[j];
+    sh.sp.jspring[j] = P.jspring[j];
+  }
+  for (int c = tid; c < M::NC; c += blockDim.x) {
+    sh.sp.cr[c][0] = P.cr[c][0];
+    sh.sp.cr[c][1] = P.cr[c][1];
+    sh.sp.mu[c] = P.mu[c];
+  }
   // column state: seed = unit column of [x~+ | U- | U+ | S]
   const int col = tid - 64;
   const bool colthr = warp >= 2 && col < NCOL;
@@ -1266,13 +1297,19 @@ __global__ void __launch_bounds__(FusedDims<M>::NT, MINB) k_linearize(const KPar
         vals[kd] = val;
       }
       const double coef = uplus ? tau : (1.0 - tau);
+      double accs[NR];
+#pragma unroll
+      for (int rr = 0; rr < NR; ++rr) accs[rr] = isU ? Ab[rr][NDIRX + um] * coef : 0.0;
+#pragma unroll
+      for (int kd = 0; kd < NDIRX; ++kd) {
+        const double vk = vals[kd];
+#pragma unroll
+        for (int rr = 0; rr < NR; ++rr)
+          if (M::adep(rr, kd)) accs[rr] += Ab[rr][kd] * vk;
+      }
 #pragma unroll
       for (int rr = 0; rr < NR; ++rr) {
-        double acc = 0.0;
-#pragma unroll
-        for (int kd = 0; kd < NDIRX; ++kd)
-          if (M::adep(rr, kd)) acc += Ab[rr][kd] * vals[kd];
-        if (isU) acc += Ab[rr][NDIRX + um] * coef;
+        const double acc = accs[rr];
         const double dk = S * acc + dS * R.r[rr];
         if (rr < NQ) {
           const int hs = M::hslot(rr);
