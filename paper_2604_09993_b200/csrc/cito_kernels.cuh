@@ -809,6 +809,10 @@ struct SParams {
   double jrp[NJ][2], jrc[NJ][2], jk[NJ], jd[NJ], jrest[NJ];
   int jspring[NJ];
   double cr[NC][2], mu[NC];
+  // topology tables for lane-indexed lookups (constexpr selects with a runtime
+  // index compile to divergent jump tables)
+  int jp[NJ], jc[NJ], ja[NJ], jperm[NJ], cl[NC];
+  int ba[Pos<M::NBLK>::v], bb[Pos<M::NBLK>::v];
 };
 
 template <class M>
@@ -887,7 +891,7 @@ __device__ __forceinline__ void fused_primal(const KParams& P, FusedShared<M>& s
   for (int e = lane; e < 2 * NJ + NC + NJ; e += 32) {
     if (e < 2 * NJ) {
       const int j = e >> 1, side = e & 1;
-      const int l = side ? M::jchild(j) : M::jparent(j);
+      const int l = side ? Q.jc[j] : Q.jp[j];
       if (l >= 0) {
         const double ax = side ? Q.jrc[j][0] : Q.jrp[j][0], az = side ? Q.jrc[j][1] : Q.jrp[j][1];
         const double c = pr.c[l], sn = pr.s[l];
@@ -896,7 +900,7 @@ __device__ __forceinline__ void fused_primal(const KParams& P, FusedShared<M>& s
         Rj[1] = sn * ax + c * az;
       }
     } else if (e < 2 * NJ + NC) {
-      const int ci = e - 2 * NJ, l = M::clink(ci);
+      const int ci = e - 2 * NJ, l = Q.cl[ci];
       const double c = pr.c[l], sn = pr.s[l];
       const double rx = c * Q.cr[ci][0] - sn * Q.cr[ci][1];
       const double rz = sn * Q.cr[ci][0] + c * Q.cr[ci][1];
@@ -940,7 +944,7 @@ __device__ __forceinline__ void fused_primal(const KParams& P, FusedShared<M>& s
       pr.lamc[ci] = t0 * Jv0 + t1 * Jv1 + gam * sgt;
     } else {
       const int j = e - 2 * NJ - NC;  // joint moment (multibody.py:303-320)
-      const int p = M::jparent(j), c = M::jchild(j), a = M::jact(j);
+      const int p = Q.jp[j], c = Q.jc[j], a = Q.ja[j];
       double mo = 0.0;
       if (a >= 0) mo = mo + pr.u[a];
       if (Q.jspring[j]) {
@@ -976,15 +980,15 @@ __device__ __forceinline__ void fused_primal(const KParams& P, FusedShared<M>& s
       w.W[3 * l + 1] = W1;
       w.W[3 * l + 2] = W2;
     } else if constexpr (NJ > 0) {
-      const int kb = e - NL, a = M::blk_a(kb), bp = M::blk_b(kb);
-      const int j = M::jperm(a), k = M::jperm(bp);
+      const int kb = e - NL, a = Q.ba[kb], bp = Q.bb[kb];
+      const int j = Q.jperm[a], k = Q.jperm[bp];
       double g00 = 0.0, g01 = 0.0, g10 = 0.0, g11 = 0.0;
 #pragma unroll
       for (int sa = 0; sa < 2; ++sa)
 #pragma unroll
         for (int sb = 0; sb < 2; ++sb) {
-          const int la = sa == 0 ? M::jparent(j) : M::jchild(j);
-          const int lb = sb == 0 ? M::jparent(k) : M::jchild(k);
+          const int la = sa == 0 ? Q.jp[j] : Q.jc[j];
+          const int lb = sb == 0 ? Q.jp[k] : Q.jc[k];
           if (la < 0 || la != lb) continue;
           const double sg = (sa == sb) ? 1.0 : -1.0;
           const double* Ra = sa == 0 ? pr.rp[j] : pr.rc[j];
@@ -1007,13 +1011,13 @@ __device__ __forceinline__ void fused_primal(const KParams& P, FusedShared<M>& s
   if constexpr (NJ > 0) {
     // 4: rhs = J (M^-1 W) + curv, per joint (elimination order)
     for (int a = lane; a < NJ; a += 32) {
-      const int j = M::jperm(a);
+      const int j = Q.jperm[a];
 #pragma unroll
       for (int al = 0; al < 2; ++al) {
         double acc = 0.0;
 #pragma unroll
         for (int sa = 0; sa < 2; ++sa) {
-          const int l = sa == 0 ? M::jparent(j) : M::jchild(j);
+          const int l = sa == 0 ? Q.jp[j] : Q.jc[j];
           if (l < 0) continue;
           const double sgn = sa == 0 ? 1.0 : -1.0;
           const double* Rj = sa == 0 ? pr.rp[j] : pr.rc[j];
@@ -1224,6 +1228,22 @@ __global__ void __launch_bounds__(FusedDims<M>::NT, MINB) k_linearize(const KPar
     sh.sp.jd[j] = P.jd[j];
     sh.sp.jrest[j] = P.jrest[j];
     sh.sp.jspring[j] = P.jspring[j];
+  }
+  if (tid == 0) {
+#pragma unroll
+    for (int j = 0; j < M::NJ; ++j) {
+      sh.sp.jp[j] = M::jparent(j);
+      sh.sp.jc[j] = M::jchild(j);
+      sh.sp.ja[j] = M::jact(j);
+      sh.sp.jperm[j] = M::jperm(j);
+    }
+#pragma unroll
+    for (int c = 0; c < M::NC; ++c) sh.sp.cl[c] = M::clink(c);
+#pragma unroll
+    for (int k = 0; k < M::NBLK; ++k) {
+      sh.sp.ba[k] = M::blk_a(k);
+      sh.sp.bb[k] = M::blk_b(k);
+    }
   }
   for (int c = tid; c < M::NC; c += blockDim.x) {
     sh.sp.cr[c][0] = P.cr[c][0];
