@@ -694,6 +694,7 @@ struct Dims {
   static constexpr int NCOL = NX + 2 * NU + 1;  // non-y tangent columns: x~+ (q,v), U-, U+, S
   static constexpr int NDIR = M::NDIRX + NU;    // rate-Jacobian input directions
   static constexpr int NR = NQ + NY;            // rate rows with a non-trivial Jacobian (vdot, Omega)
+  static constexpr int NRP = (NR + 1) & ~1;     // padded to 16 B rows
   static constexpr int NCOLP = NCOL | 1;        // odd column stride (bank spread)
   static constexpr int NH = Pos<M::NHIST>::v;
   static constexpr int NT = ((NCOL > NDIR ? NCOL : NDIR) + 31) / 32 * 32;
@@ -830,7 +831,7 @@ struct FusedShared {
   Rec<M> ring[3];
   PrimScratch<M> ps;
   SParams<M> sp;
-  double A[2][D::NR][D::NDIR];
+  double At[2][D::NDIR][D::NRP];  // rate Jacobian, direction-major (row pairs load as LDS.128)
   double KV[5][D::NH][D::NCOLP];
   double PQ[Pos<M::NPUSH>::v][D::NCOLP];
   double PV[Pos<M::NPUSH>::v][D::NCOLP];
@@ -1192,6 +1193,88 @@ __device__ __forceinline__ void fused_primal(const KParams& P, FusedShared<M>& s
   }
 }
 
+// One tangent column through RK stage I (column warps of k_linearize).
+template <class M, int I>
+__device__ __forceinline__ void col_stage(const KParams& P, FusedShared<M>& sh, int st, int col, double S, double dS,
+                                          bool isU, int um, bool uplus, double (&hq)[Pos<M::NHIST>::v],
+                                          double (&hv)[Pos<M::NHIST>::v]) {
+  using D = Dims<M>;
+  constexpr int NQ = D::NQ, NR = D::NR, NDIRX = M::NDIRX;
+  const int s = st / 6;
+  const Rec<M>& R = sh.ring[st % 3];
+  const double(*At)[D::NRP] = sh.At[st & 1];
+  const double h = P.h;
+  const double tau = h * (double)s + P.ch[I];
+  const double hb = h * P.b[I];
+  if (I == 0) {  // push q rows: S h sum(b) * (substep-start dv)
+#pragma unroll
+    for (int p = 0; p < M::NPUSH; ++p) sh.PQ[p][col] += P.he1 * S * sh.PV[p][col];
+  }
+  double vals[Pos<NDIRX>::v];
+#pragma unroll
+  for (int kd = 0; kd < NDIRX; ++kd) {
+    const int d = M::dir(kd);
+    double val;
+    if (d < NQ) {
+      const int hs = M::hslot(d);
+      val = hq[hs] + S * P.hc1[I] * hv[hs] + dS * R.wq[d];
+#pragma unroll
+      for (int l = 0; l < I; ++l) val += S * P.cq[I][l] * sh.KV[l][hs][col];
+    } else {
+      const int hs = M::hslot(d - NQ);
+      val = hv[hs];
+#pragma unroll
+      for (int l = 0; l < I; ++l) val += P.ha[I][l] * sh.KV[l][hs][col];
+    }
+    vals[kd] = val;
+  }
+  const double coef = uplus ? tau : (1.0 - tau);
+  double accs[NR];
+  if (isU) {
+    const double* Au = At[NDIRX + um];
+#pragma unroll
+    for (int rr = 0; rr < NR; ++rr) accs[rr] = Au[rr] * coef;
+  } else {
+#pragma unroll
+    for (int rr = 0; rr < NR; ++rr) accs[rr] = 0.0;
+  }
+#pragma unroll
+  for (int kd = 0; kd < NDIRX; ++kd) {
+    const double vk = vals[kd];
+#pragma unroll
+    for (int rr = 0; rr < NR; ++rr)
+      if (M::adep(rr, kd)) accs[rr] += At[kd][rr] * vk;
+  }
+#pragma unroll
+  for (int rr = 0; rr < NR; ++rr) {
+    const double dk = S * accs[rr] + dS * R.r[rr];
+    if (rr < NQ) {
+      const int hs = M::hslot(rr);
+      if (hs >= 0) {
+        if (I < 5) {
+          sh.KV[I][hs][col] = dk;
+        } else {
+          double incv = P.b[5] * dk, incq = 0.0;
+#pragma unroll
+          for (int l = 0; l < 5; ++l) {
+            const double kv = sh.KV[l][hs][col];
+            incv += P.b[l] * kv;
+            incq += P.e2[l] * kv;
+          }
+          hq[hs] = hq[hs] + P.he1 * S * hv[hs] + S * incq + dS * sh.vbs[s & 1][rr];
+          hv[hs] = hv[hs] + h * incv;
+        }
+      } else {
+        const int p = M::pslot(rr);
+        sh.PV[p][col] += hb * dk;
+        sh.PQ[p][col] += S * P.e2[I] * dk + dS * hb * R.vs[rr];
+      }
+    } else {
+      sh.DY[rr - NQ][col] += hb * dk;
+    }
+  }
+}
+
 template <class M, int MINB>
 __global__ void __launch_bounds__(FusedDims<M>::NT, MINB) k_linearize(const KParams P, int64_t B,
                                                                const double* __restrict__ xt0s,
@@ -1287,74 +1370,18 @@ __global__ void __launch_bounds__(FusedDims<M>::NT, MINB) k_linearize(const KPar
         const Rec<M>& R = sh.ring[st % 3];
         for (int kd = lane; kd < NDIR; kd += 32) {
           const int dir = kd < NDIRX ? M::dir(kd) : NX + (kd - NDIRX);
-          tan_rate<M>(P, R.pr, R.vs, dir, &sh.A[st & 1][0][kd], NDIR);
+          tan_rate<M>(P, R.pr, R.vs, dir, &sh.At[st & 1][kd][0], 1);
         }
       }
     } else if (colthr && t >= 2) {
-      const int st = t - 2, s = st / 6, i = st % 6;
-      const Rec<M>& R = sh.ring[st % 3];
-      const double(*Ab)[NDIR] = sh.A[st & 1];
-      const double tau = h * (double)s + P.ch[i];
-      const double hb = h * P.b[i];
-      if (i == 0) {  // push q rows: S h sum(b) * (substep-start dv)
-#pragma unroll
-        for (int p = 0; p < M::NPUSH; ++p) sh.PQ[p][col] += P.he1 * S * sh.PV[p][col];
-      }
-      double vals[Pos<NDIRX>::v];
-#pragma unroll
-      for (int kd = 0; kd < NDIRX; ++kd) {
-        const int d = M::dir(kd);
-        double val;
-        if (d < NQ) {
-          const int hs = M::hslot(d);
-          val = hq[hs] + S * P.hc1[i] * hv[hs] + dS * R.wq[d];
-          for (int l = 0; l < i; ++l) val += S * P.cq[i][l] * sh.KV[l][hs][col];
-        } else {
-          const int hs = M::hslot(d - NQ);
-          val = hv[hs];
-          for (int l = 0; l < i; ++l) val += P.ha[i][l] * sh.KV[l][hs][col];
-        }
-        vals[kd] = val;
-      }
-      const double coef = uplus ? tau : (1.0 - tau);
-      double accs[NR];
-#pragma unroll
-      for (int rr = 0; rr < NR; ++rr) accs[rr] = isU ? Ab[rr][NDIRX + um] * coef : 0.0;
-#pragma unroll
-      for (int kd = 0; kd < NDIRX; ++kd) {
-        const double vk = vals[kd];
-#pragma unroll
-        for (int rr = 0; rr < NR; ++rr)
-          if (M::adep(rr, kd)) accs[rr] += Ab[rr][kd] * vk;
-      }
-#pragma unroll
-      for (int rr = 0; rr < NR; ++rr) {
-        const double acc = accs[rr];
-        const double dk = S * acc + dS * R.r[rr];
-        if (rr < NQ) {
-          const int hs = M::hslot(rr);
-          if (hs >= 0) {
-            if (i < 5) {
-              sh.KV[i][hs][col] = dk;
-            } else {
-              double incv = P.b[5] * dk, incq = 0.0;
-#pragma unroll
-              for (int l = 0; l < 5; ++l) {
-                const double kv = sh.KV[l][hs][col];
-                incv += P.b[l] * kv;
-                incq += P.e2[l] * kv;
-              }
-              hq[hs] = hq[hs] + P.he1 * S * hv[hs] + S * incq + dS * sh.vbs[s & 1][rr];
-              hv[hs] = hv[hs] + h * incv;
-            }
-          } else {
-            const int p = M::pslot(rr);
-            sh.PV[p][col] += hb * dk;
-            sh.PQ[p][col] += S * P.e2[i] * dk + dS * hb * R.vs[rr];
-          }
-        } else {
-          sh.DY[rr - NQ][col] += hb * dk;
-        }
+      const int st = t - 2;
+      switch (st % 6) {  // warp-uniform: the stage index becomes a compile-time constant
+        case 0: col_stage<M, 0>(P, sh, st, col, S, dS, isU, um, uplus, hq, hv); break;
+        case 1: col_stage<M, 1>(P, sh, st, col, S, dS, isU, um, uplus, hq, hv); break;
+        case 2: col_stage<M, 2>(P, sh, st, col, S, dS, isU, um, uplus, hq, hv); break;
+        case 3: col_stage<M, 3>(P, sh, st, col, S, dS, isU, um, uplus, hq, hv); break;
+        case 4: col_stage<M, 4>(P, sh, st, col, S, dS, isU, um, uplus, hq, hv); break;
+        default: col_stage<M, 5>(P, sh, st, col, S, dS, isU, um, uplus, hq, hv); break;
       }
     }
     CITO_MARK((t * 8 + warp) * 2 + 1);
