@@ -146,6 +146,19 @@ cito_status cito_node_linearize_dev(cito_handle* h, int64_t Np, int64_t Nn, cons
                                     double* psi, double* psi_jac, double* theta, double* theta_jac,
                                     double* imp, double* imp_jac, void* stream);
 
+/* linearize_all (cito/scp.py:87-135) on a device-resident decision vector z
+ * (layout cito/ocp.py:154-174: node states [xm_k, xp_k] at 2k n_xt / (2k+1) n_xt,
+ * interval blocks [U_k, S_k] at base_u + k (2 n_u + 1), node impulses
+ * [Phi_k, Gamma_k] at base_p + 3 n_c k; base_u = 2 N n_xt,
+ * base_p = base_u + (N-1)(2 n_u + 1)).  Interval kernel and node-relation
+ * kernel read z directly (no host/device gathers), run concurrently (the node
+ * kernel on an internal stream joined back into `stream`), and the defects
+ * z[xm(k+1)] - ends[k] are written by the interval kernel. */
+cito_status cito_linearize_all_dev(cito_handle* h, int32_t N, int64_t base_u, int64_t base_p, const double* z,
+                                   double delta, double epsilon, double* ends, double* jx, double* ju, double* js,
+                                   double* defects, int32_t* bad, double* psi, double* psi_jac, double* theta,
+                                   double* theta_jac, double* imp, double* imp_jac, void* stream);
+
 /* Multiple-shooting rows of the SCP subproblem, written straight into CSC value
  * slots (cito/scp.py:226-236 + cito/conic.py:209-269).  The slot map is built
  * once per sparsity pattern by the host (paper_2604_09993_b200/scatter.py):

@@ -46,11 +46,11 @@ const double RKF_B[6] = {16.0 / 135, 0.0, 6656.0 / 12825, 28561.0 / 56430, -9.0 
 struct TopoOps {
   const char* key;
   cito_status (*linearize)(const KParams&, int64_t, const double*, const double*, const double*, double*, double*,
-                           double*, double*, int32_t*, cudaStream_t);
+                           double*, double*, int32_t*, cudaStream_t, ZSrc);
   cito_status (*propagate)(const KParams&, int64_t, const double*, const double*, const double*, double*, int32_t*,
                            cudaStream_t);
   cito_status (*node)(const KParams&, int64_t, int64_t, const double*, const double*, double, double, double*,
-                      double*, double*, double*, double*, double*, cudaStream_t);
+                      double*, double*, double*, double*, double*, cudaStream_t, ZSrc);
 };
 
 // Stream-ordered workspace (records of the primal trajectory): allocated from
@@ -74,7 +74,8 @@ cito_status ensure_pool() {
 
 template <class M>
 cito_status launch_linearize(const KParams& P, int64_t B, const double* xt0s, const double* Us, const double* Ss,
-                             double* ends, double* jx, double* ju, double* js, int32_t* bad, cudaStream_t st) {
+                             double* ends, double* jx, double* ju, double* js, int32_t* bad, cudaStream_t st,
+                             ZSrc zs) {
   if (B <= 0) return CITO_OK;
   const size_t smem = sizeof(FusedShared<M>);
   static bool attr_done = false;
@@ -89,9 +90,9 @@ cito_status launch_linearize(const KParams& P, int64_t B, const double* xt0s, co
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (B <= sms)
-    k_linearize<M, 1><<<(unsigned)B, FusedDims<M>::NT, smem, st>>>(P, B, xt0s, Us, Ss, ends, jx, ju, js, bad);
+    k_linearize<M, 1><<<(unsigned)B, FusedDims<M>::NT, smem, st>>>(P, B, xt0s, Us, Ss, ends, jx, ju, js, bad, zs);
   else
-    k_linearize<M, 3><<<(unsigned)B, FusedDims<M>::NT, smem, st>>>(P, B, xt0s, Us, Ss, ends, jx, ju, js, bad);
+    k_linearize<M, 3><<<(unsigned)B, FusedDims<M>::NT, smem, st>>>(P, B, xt0s, Us, Ss, ends, jx, ju, js, bad, zs);
   CUDA_TRY(cudaGetLastError());
   return CITO_OK;
 }
@@ -109,13 +110,13 @@ cito_status launch_propagate(const KParams& P, int64_t B, const double* xt0s, co
 template <class M>
 cito_status launch_node(const KParams& P, int64_t Np, int64_t Nn, const double* y_pairs, const double* theta_vecs,
                         double delta, double eps, double* psi, double* psi_jac, double* th, double* th_jac,
-                        double* imp, double* imp_jac, cudaStream_t st) {
+                        double* imp, double* imp_jac, cudaStream_t st, ZSrc zs) {
   constexpr int NQ = 3 * M::NL, NC = M::NC, NY = 5 * NC + M::NGO;
   const int64_t total = Np * (2 * NY) + Nn * (3 * NQ + 3 * NC) + Nn * (3 * NQ + 2 * NC);
   if (total <= 0) return CITO_OK;
   const int nt = 64;
   k_node<M><<<(unsigned)((total + nt - 1) / nt), nt, 0, st>>>(P, Np, Nn, y_pairs, theta_vecs, delta, eps, psi,
-                                                               psi_jac, th, th_jac, imp, imp_jac);
+                                                               psi_jac, th, th_jac, imp, imp_jac, zs);
   CUDA_TRY(cudaGetLastError());
   return CITO_OK;
 }
@@ -162,6 +163,8 @@ struct cito_handle {
   void* dbuf = nullptr;
   size_t dcap = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t aux = nullptr;  // concurrent node-relation kernel of linearize_all
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   int64_t launches = 0;
 };
 
@@ -280,6 +283,9 @@ cito_status cito_destroy(cito_handle* h) {
   if (!h) return CITO_OK;
   if (h->dbuf) cudaFree(h->dbuf);
   if (h->stream) cudaStreamDestroy(h->stream);
+  if (h->aux) cudaStreamDestroy(h->aux);
+  if (h->ev_in) cudaEventDestroy(h->ev_in);
+  if (h->ev_out) cudaEventDestroy(h->ev_out);
   delete h;
   return CITO_OK;
 }
@@ -295,7 +301,7 @@ int64_t cito_launch_count(const cito_handle* h) { return h ? h->launches : 0; }
 cito_status cito_linearize_dev(cito_handle* h, int64_t B, const double* xt0s, const double* Us, const double* Ss,
                                double* ends, double* jx, double* ju, double* js, int32_t* bad, void* stream) {
   if (!h) return fail(CITO_ERR_ARG, "null handle");
-  cito_status st = h->ops->linearize(h->P, B, xt0s, Us, Ss, ends, jx, ju, js, bad, (cudaStream_t)stream);
+  cito_status st = h->ops->linearize(h->P, B, xt0s, Us, Ss, ends, jx, ju, js, bad, (cudaStream_t)stream, ZSrc{});
   if (st == CITO_OK && B > 0) __atomic_add_fetch(&h->launches, 1, __ATOMIC_RELAXED);
   return st;
 }
@@ -314,7 +320,7 @@ cito_status cito_node_linearize_dev(cito_handle* h, int64_t Np, int64_t Nn, cons
                                     void* stream) {
   if (!h) return fail(CITO_ERR_ARG, "null handle");
   cito_status st = h->ops->node(h->P, Np, Nn, y_pairs, theta_vecs, delta, epsilon, psi, psi_jac, theta, theta_jac,
-                                imp, imp_jac, (cudaStream_t)stream);
+                                imp, imp_jac, (cudaStream_t)stream, ZSrc{});
   if (st == CITO_OK && Np + Nn > 0) __atomic_add_fetch(&h->launches, 1, __ATOMIC_RELAXED);
   return st;
 }
@@ -370,7 +376,7 @@ cito_status cito_linearize_host(cito_handle* h, int64_t B, const double* xt0s, c
   CUDA_TRY(cudaMemcpyAsync(d_x, xt0s, B * D.n_xt * 8, cudaMemcpyHostToDevice, s));
   if (D.n_u) CUDA_TRY(cudaMemcpyAsync(d_U, Us, B * 2 * D.n_u * 8, cudaMemcpyHostToDevice, s));
   CUDA_TRY(cudaMemcpyAsync(d_S, Ss, B * 8, cudaMemcpyHostToDevice, s));
-  st = h->ops->linearize(h->P, B, d_x, d_U, d_S, d_e, d_jx, d_ju, d_js, d_bad, s);
+  st = h->ops->linearize(h->P, B, d_x, d_U, d_S, d_e, d_jx, d_ju, d_js, d_bad, s, ZSrc{});
   if (st != CITO_OK) return st;
   h->launches++;
   CUDA_TRY(cudaMemcpyAsync(ends, d_e, B * D.n_xt * 8, cudaMemcpyDeviceToHost, s));
@@ -409,6 +415,34 @@ cito_status cito_propagate_host(cito_handle* h, int64_t B, const double* xt0s, c
   if (bad) CUDA_TRY(cudaMemcpyAsync(bad, d_bad, B * 4, cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
   return count_bad(bad, B);
+}
+
+cito_status cito_linearize_all_dev(cito_handle* h, int32_t N, int64_t base_u, int64_t base_p, const double* z,
+                                   double delta, double epsilon, double* ends, double* jx, double* ju, double* js,
+                                   double* defects, int32_t* bad, double* psi, double* psi_jac, double* theta,
+                                   double* theta_jac, double* imp, double* imp_jac, void* stream) {
+  if (!h) return fail(CITO_ERR_ARG, "null handle");
+  if (N < 2) return fail(CITO_ERR_ARG, "need at least two grid nodes");
+  cudaStream_t s = (cudaStream_t)stream;
+  std::lock_guard<std::mutex> lk(h->mu);
+  if (!h->aux) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&h->aux, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&h->ev_in, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&h->ev_out, cudaEventDisableTiming));
+  }
+  const ZSrc zs{z, base_u, base_p, defects};
+  // node relations (K3) on the auxiliary stream, concurrently with the interval kernel (K1)
+  CUDA_TRY(cudaEventRecord(h->ev_in, s));
+  CUDA_TRY(cudaStreamWaitEvent(h->aux, h->ev_in, 0));
+  cito_status st = h->ops->node(h->P, N - 1, N, nullptr, nullptr, delta, epsilon, psi, psi_jac, theta, theta_jac, imp,
+                                imp_jac, h->aux, zs);
+  if (st != CITO_OK) return st;
+  CUDA_TRY(cudaEventRecord(h->ev_out, h->aux));
+  st = h->ops->linearize(h->P, N - 1, nullptr, nullptr, nullptr, ends, jx, ju, js, bad, s, zs);
+  if (st != CITO_OK) return st;
+  CUDA_TRY(cudaStreamWaitEvent(s, h->ev_out, 0));
+  __atomic_add_fetch(&h->launches, 2, __ATOMIC_RELAXED);
+  return CITO_OK;
 }
 
 cito_status cito_scatter_dynamics_dev(cito_handle* h, int64_t n_int, const double* ends, const double* jx,

@@ -80,6 +80,16 @@ __device__ long long* g_cito_prof = nullptr;
   } while (0)
 #endif
 
+// Decision-vector source of a linearize_all call: interval k reads x~+_k at
+// z[(2k+1) n_xt], [U_k, S_k] at z[base_u + k (2 n_u + 1)] and writes the
+// defect z[xm(k+1)] - end_k (cito/ocp.py:154-174, cito/scp.py:98-115).
+struct ZSrc {
+  const double* z;
+  int64_t base_u;
+  int64_t base_p;
+  double* defects;
+};
+
 template <int N>
 struct Pos {
   static constexpr int v = N > 0 ? N : 1;
@@ -1282,7 +1292,7 @@ __global__ void __launch_bounds__(FusedDims<M>::NT, MINB) k_linearize(const KPar
                                                                const double* __restrict__ Ss,
                                                                double* __restrict__ ends, double* __restrict__ jx,
                                                                double* __restrict__ ju, double* __restrict__ js,
-                                                               int32_t* __restrict__ bad) {
+                                                               int32_t* __restrict__ bad, const ZSrc zs) {
   using D = Dims<M>;
   constexpr int NQ = D::NQ, NX = D::NX, NU = D::NU, NY = D::NY, NXT = D::NXT, NCOL = D::NCOL, NR = D::NR;
   constexpr int NDIRX = M::NDIRX, NDIR = D::NDIR, NHIST = M::NHIST;
@@ -1291,10 +1301,14 @@ __global__ void __launch_bounds__(FusedDims<M>::NT, MINB) k_linearize(const KPar
   const int64_t b = blockIdx.x;
   if (b >= B) return;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int k = tid; k < NXT; k += blockDim.x) sh.x[k] = xt0s[b * NXT + k];
-  for (int k = tid; k < 2 * NU; k += blockDim.x) sh.U[k] = Us[b * 2 * NU + k];
+  // inputs: either packed batches or gathered straight from the decision vector
+  // z (cito/scp.py:98-100, layout cito/ocp.py:154-174)
+  const double* src_x = zs.z ? zs.z + (2 * b + 1) * NXT : xt0s + b * NXT;
+  const double* src_U = zs.z ? zs.z + zs.base_u + b * (2 * NU + 1) : Us + b * 2 * NU;
+  for (int k = tid; k < NXT; k += blockDim.x) sh.x[k] = src_x[k];
+  for (int k = tid; k < 2 * NU; k += blockDim.x) sh.U[k] = src_U[k];
   if (tid == 0) {
-    sh.S = Ss[b];
+    sh.S = zs.z ? src_U[2 * NU] : Ss[b];
     sh.bad = 0;
   }
   for (int l = tid; l < M::NL; l += blockDim.x) {
@@ -1420,6 +1434,7 @@ __global__ void __launch_bounds__(FusedDims<M>::NT, MINB) k_linearize(const KPar
   for (int k = tid; k < NXT; k += blockDim.x) {
     const double e = sh.x[k];
     ends[b * NXT + k] = e;
+    if (zs.defects) zs.defects[b * NXT + k] = zs.z[(2 * b + 2) * NXT + k] - e;  // scp.py:115
     if (!isfinite(e)) sh.bad = 1;
   }
   __syncthreads();

@@ -299,9 +299,10 @@ __global__ void __launch_bounds__(64) k_node(const KParams P, int64_t Np, int64_
                                              const double* __restrict__ theta_vecs, double delta, double eps,
                                              double* __restrict__ psi, double* __restrict__ psi_jac,
                                              double* __restrict__ th, double* __restrict__ th_jac,
-                                             double* __restrict__ imp, double* __restrict__ imp_jac) {
+                                             double* __restrict__ imp, double* __restrict__ imp_jac, const ZSrc zs) {
   constexpr int NL = M::NL, NC = M::NC, NQ = 3 * NL, NY = 5 * NC + M::NGO;
   constexpr int NPSI = 3 * NC + M::NGO, NV = 3 * NQ + 3 * NC, NI = 3 * NQ + 2 * NC;
+  constexpr int NXT = 2 * NQ + NY;
   // item space: [Np * 2NY psi columns][Nn * NV theta columns][Nn * NI impulse columns]
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n_psi = Np * (2 * NY), n_th = Nn * NV, n_imp = Nn * NI;
@@ -309,18 +310,38 @@ __global__ void __launch_bounds__(64) k_node(const KParams P, int64_t Np, int64_
     constexpr int NY2 = Pos<2 * NY>::v;
     const int64_t k = t / NY2;
     const int d = (int)(t % NY2);
-    node_psi<M>(P, y_pairs + k * 2 * NY, d, delta, eps, d == 0 ? psi + k * NPSI : nullptr,
-                psi_jac + k * NPSI * 2 * NY + d, 2 * NY);
-  } else if (t < n_psi + n_th) {
-    const int64_t e = t - n_psi;
-    const int64_t k = e / NV;
-    const int d = (int)(e % NV);
-    node_theta<M>(P, theta_vecs + k * NV, d, delta, d == 0 ? th + k * 6 * NC : nullptr,
-                  th_jac + k * 6 * NC * NV + d, NV);
+    double buf[NY2];
+    const double* yp = y_pairs + k * 2 * NY;
+    if (zs.z) {  // [y+_k, y-_{k+1}] straight from z (Transcription._node_inputs, ocp.py:316-318)
+#pragma unroll
+      for (int i = 0; i < NY; ++i) {
+        buf[i] = zs.z[(2 * k + 1) * NXT + 2 * NQ + i];
+        buf[NY + i] = zs.z[(2 * k + 2) * NXT + 2 * NQ + i];
+      }
+      yp = buf;
+    }
+    node_psi<M>(P, yp, d, delta, eps, d == 0 ? psi + k * NPSI : nullptr, psi_jac + k * NPSI * 2 * NY + d, 2 * NY);
   } else if (t < n_psi + n_th + n_imp) {
-    const int64_t e = t - n_psi - n_th;
-    const int64_t k = e / NI;
-    const int d = (int)(e % NI);
-    node_impulse<M>(P, theta_vecs + k * NV, d, d == 0 ? imp + k * NQ : nullptr, imp_jac + k * NQ * NI + d, NI);
+    const bool is_th = t < n_psi + n_th;
+    const int64_t e = is_th ? t - n_psi : t - n_psi - n_th;
+    const int64_t k = is_th ? e / NV : e / NI;
+    const int d = is_th ? (int)(e % NV) : (int)(e % NI);
+    double buf[NV];
+    const double* vec = theta_vecs + k * NV;
+    if (zs.z) {  // [q-, v-, v+, Phi, Gamma] of node k straight from z (ocp.py:319-333)
+#pragma unroll
+      for (int i = 0; i < 2 * NQ; ++i) buf[i] = zs.z[2 * k * NXT + i];
+#pragma unroll
+      for (int i = 0; i < NQ; ++i) buf[2 * NQ + i] = zs.z[(2 * k + 1) * NXT + NQ + i];
+#pragma unroll
+      for (int i = 0; i < 3 * NC; ++i) buf[3 * NQ + i] = zs.z[zs.base_p + 3 * NC * k + i];
+      vec = buf;
+    }
+    if (is_th) {
+      if (NC > 0)
+        node_theta<M>(P, vec, d, delta, d == 0 ? th + k * 6 * NC : nullptr, th_jac + k * 6 * NC * NV + d, NV);
+    } else {
+      node_impulse<M>(P, vec, d, d == 0 ? imp + k * NQ : nullptr, imp_jac + k * NQ * NI + d, NI);
+    }
   }
 }

@@ -127,32 +127,50 @@ class GpuTranscription:
         idx_yp = np.stack([np.concatenate([lay.y_of_xp(k), lay.y_of_xm(k + 1)]) for k in range(N - 1)])
         idx_th = np.stack([np.concatenate([lay.xm(k)[:n_q], lay.xm(k)[n_q: 2 * n_q], lay.xp(k)[n_q: 2 * n_q],
                                            lay.phi(k), lay.gam(k)]) for k in range(N)])
+        # layout bases as used by the fused kernels (identical to ocp.Layout's formulas, ocp.py:154-174)
+        self.base_u = 2 * N * lay.n_xt
+        self.base_p = self.base_u + (N - 1) * (2 * lay.n_u + 1)
+        assert int(lay.u(0)[0]) == self.base_u and int(lay.phi(0)[0]) == self.base_p
+        assert int(lay.xp(N - 1)[0]) == (2 * (N - 1) + 1) * lay.n_xt
         t = lambda a: torch.as_tensor(np.ascontiguousarray(a, dtype=np.int64), device=self.device)
         self._i_start, self._i_end, self._i_u, self._i_s = t(idx_start), t(idx_end), t(idx_u), t(idx_s)
         self._i_yp, self._i_th = t(idx_yp), t(idx_th)
         self.n_imp = 3 * n_q + 2 * lay.n_c
 
-    def linearize_device(self, z_dev, delta, epsilon=None, k1_events=None):
-        """Everything on the device; returns a dict of torch tensors.  ``k1_events``
-        = (start, end) CUDA events recorded around the interval kernel (K1)."""
+    def linearize_device(self, z_dev, delta, epsilon=None, k1_events=None, out=None):
+        """Everything on the device in one C-ABI call (cito_linearize_all_dev): the
+        interval kernel and the node-relation kernel read z directly and run
+        concurrently.  Returns a dict of torch tensors.  ``k1_events`` = (start,
+        end) CUDA events recorded around the call on the current stream."""
         import torch
 
         if epsilon is None:
             epsilon = self.scenario.ctcs_epsilon
-        starts = z_dev[self._i_start]
-        Us = z_dev[self._i_u]
-        Ss = z_dev[self._i_s]
+        lay = self.lay
+        N, nxt, nu, nq, nc = lay.N, lay.n_xt, lay.n_u, lay.n_q, lay.n_c
+        n_psi = 3 * nc + lay.n_g_out
+        if out is None:
+            f64 = dict(dtype=torch.float64, device=self.device)
+            out = dict(ends=torch.empty((N - 1, nxt), **f64), jx=torch.empty((N - 1, nxt, nxt), **f64),
+                       ju=torch.empty((N - 1, nxt, 2 * nu), **f64), js=torch.empty((N - 1, nxt), **f64),
+                       defects=torch.empty((N - 1, nxt), **f64),
+                       bad=torch.empty((N - 1,), dtype=torch.int32, device=self.device),
+                       psi=torch.empty((N - 1, n_psi), **f64), psi_jac=torch.empty((N - 1, n_psi, 2 * lay.n_y), **f64),
+                       theta=torch.empty((N, 6 * nc), **f64), theta_jac=torch.empty((N, 6 * nc, 3 * nq + 3 * nc), **f64),
+                       imp_v=torch.empty((N, nq), **f64), imp_jac=torch.empty((N, nq, 3 * nq + 2 * nc), **f64))
+        stream = torch.cuda.current_stream(self.device)
         if k1_events is not None:
-            k1_events[0].record(torch.cuda.current_stream(self.device))
-        ends, jx, ju, js, bad = self.disc.linearize_batch_device(starts, Us, Ss)
+            k1_events[0].record(stream)
+        o = out
+        _lib.check(_lib.lib().cito_linearize_all_dev(
+            self.disc._h.ptr, N, int(self.base_u), int(self.base_p), z_dev.data_ptr(), float(delta), float(epsilon),
+            o["ends"].data_ptr(), o["jx"].data_ptr(), o["ju"].data_ptr(), o["js"].data_ptr(), o["defects"].data_ptr(),
+            o["bad"].data_ptr(), o["psi"].data_ptr(), o["psi_jac"].data_ptr(), o["theta"].data_ptr(),
+            o["theta_jac"].data_ptr(), o["imp_v"].data_ptr(), o["imp_jac"].data_ptr(), stream.cuda_stream),
+            "linearize_all")
         if k1_events is not None:
-            k1_events[1].record(torch.cuda.current_stream(self.device))
-        defects = z_dev[self._i_end] - ends
-        y_pairs = z_dev[self._i_yp]
-        theta_vecs = z_dev[self._i_th]
-        psi, psi_j, th, th_j, imp, imp_j = self.nodes.device(y_pairs, theta_vecs, delta, epsilon)
-        return dict(starts=starts, Us=Us, Ss=Ss, ends=ends, jx=jx, ju=ju, js=js, bad=bad, defects=defects,
-                    psi=psi, psi_jac=psi_j, theta=th, theta_jac=th_j, imp_v=imp, imp_jac=imp_j)
+            k1_events[1].record(stream)
+        return out
 
     def linearize_all(self, z, delta, epsilon=None, jobs=1):
         """Drop-in for cito.scp.linearize_all(tr, z, delta, epsilon, jobs) (scp.py:87-135)."""
