@@ -49,7 +49,8 @@ def parse():
     p.add_argument("--steps", type=int, default=50)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--workload", choices=["scp", "batch"], default="scp")
+    p.add_argument("--workload", choices=["scp", "batch", "multistart"], default="scp")
+    p.add_argument("--problems", type=int, default=128, help="multistart: problems per GPU (configs[3]: 1024 / 8)")
     p.add_argument("--batch", type=int, default=4096)
     p.add_argument("--cpu-seconds", type=float, default=10.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -241,7 +242,7 @@ def run_ours(args):
         return r
 
     # --- batch workload state
-    if args.workload == "batch" or not args.no_batch_extra:
+    if args.workload == "batch" or (args.workload == "scp" and not args.no_batch_extra):
         B = args.batch
         ok = lambda x, u, s: synth.well_posed(gt.disc.propagate_batch_device(
             *(torch.as_tensor(a, device=dev) for a in (x, u, s)))[0].cpu().numpy())
@@ -257,6 +258,30 @@ def run_ours(args):
         if record:
             e1.record(stream)
             k1_ev.append((e0, e1))
+
+    if args.workload == "multistart":
+        # configs[3] analogue: HalfCheetah N=50 multi-start initial guesses (no quadruped
+        # exists in the reference); each rank owns `problems` starts
+        from paper_2604_09993_b200 import scenario as S2
+        from paper_2604_09993_b200.parallel import gather_rows
+
+        sc50 = S2.bundled("halfcheetah_bound", N=50)
+        gt50 = GpuTranscription(sc50, device=dev.index)
+        seeds = [rank * args.problems + i for i in range(args.problems)]
+        Z = np.stack([initial_guess(sc50, gt50.disc, gt50.lay, seed=sd) for sd in seeds])
+        Z_dev = torch.as_tensor(Z, device=dev)
+        ms_out = gt50.linearize_device(Z_dev, 1.0)
+
+        def ms_step(record=False):
+            if record:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                gt50.linearize_device(Z_dev, 1.0, k1_events=(e0, e1), out=ms_out)
+                k1_ev.append((e0, e1))
+            else:
+                gt50.linearize_device(Z_dev, 1.0, out=ms_out)
+            # result collection: per-problem max |defect| to every rank (NCCL all_gather at N > 1)
+            metric = ms_out["defects"].view(args.problems, -1).abs().amax(dim=1)
+            return gather_rows(metric) if dist else metric
 
     def timed(step_fn, K, W):
         for _ in range(W):
@@ -291,6 +316,10 @@ def run_ours(args):
     if args.workload == "scp":
         ms_tot, k1_ms, launches = timed(lambda rec: scp_step(z_dev, rec), K, W)
         units_per_step, B_k1 = n_int, n_int
+    elif args.workload == "multistart":
+        gt.disc = gt50.disc  # launch counter of the handle actually used
+        ms_tot, k1_ms, launches = timed(ms_step, K, W)
+        units_per_step = B_k1 = args.problems * (sc50.N - 1)
     else:
         ms_tot, k1_ms, launches = timed(batch_step, K, W)
         units_per_step, B_k1 = args.batch, args.batch
@@ -331,6 +360,20 @@ def run_ours(args):
         e2e_step()
         h2d = z.nbytes
         d2h = int(sum(v.numel() * v.element_size() for v in outs.values()))
+    elif args.workload == "multistart":
+        Z_pin = torch.as_tensor(Z).pin_memory()
+        ms_host = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in ms_out.items()}
+
+        def e2e_step():
+            zd = Z_pin.to(dev, non_blocking=True)
+            o = gt50.linearize_device(zd, 1.0, out=ms_out)
+            for k, v in o.items():
+                ms_host[k].copy_(v, non_blocking=True)
+            torch.cuda.current_stream(dev).synchronize()
+
+        e2e_step()
+        h2d = Z.nbytes
+        d2h = int(sum(v.numel() * v.element_size() for v in ms_out.values()))
     else:
         xb_p, Ub_p, Sb_p = (torch.as_tensor(a).pin_memory() for a in (xb, Ub, Sb))
         bouts = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in bout]
@@ -387,9 +430,13 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic" if args.workload == "batch" else "synthetic (scenario initial guess, seed=rank)",
-        "config": {"workload": ("scp: one SCP-iteration linearize of HalfCheetah N=30 (halfcheetah_bound.json, "
-                                "5 RKF substeps, 29 intervals; K1+K3+K4)") if args.workload == "scp" else
-                   f"batch: {args.batch} independent synthetic HalfCheetah intervals per GPU (configs[2])",
+        "config": {"workload": {"scp": "scp: one SCP-iteration linearize of HalfCheetah N=30 (halfcheetah_bound.json, "
+                                       "5 RKF substeps, 29 intervals; K1+K3+K4)",
+                                "batch": f"batch: {args.batch} independent synthetic HalfCheetah intervals per GPU "
+                                         "(configs[2])",
+                                "multistart": f"multistart: {args.problems} HalfCheetah N=50 initial guesses per GPU "
+                                              "(configs[3] analogue), linearize_all (K1+K3) + NCCL all_gather of "
+                                              "per-problem defect norms"}[args.workload],
                    "intervals_per_step_per_gpu": units_per_step, "l2": "flushed (256 MiB write) between timed steps",
                    "parallelism": f"replicas x{world} (independent problems per rank, no collective)"},
         "roofline": roofline, "cpu_baseline": cpu,

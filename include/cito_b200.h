@@ -153,9 +153,11 @@ cito_status cito_node_linearize_dev(cito_handle* h, int64_t Np, int64_t Nn, cons
  * base_p = base_u + (N-1)(2 n_u + 1)).  Interval kernel and node-relation
  * kernel read z directly (no host/device gathers), run concurrently (the node
  * kernel on an internal stream joined back into `stream`), and the defects
- * z[xm(k+1)] - ends[k] are written by the interval kernel. */
-cito_status cito_linearize_all_dev(cito_handle* h, int32_t N, int64_t base_u, int64_t base_p, const double* z,
-                                   double delta, double epsilon, double* ends, double* jx, double* ju, double* js,
+ * z[xm(k+1)] - ends[k] are written by the interval kernel.  n_problems > 1
+ * linearizes a multi-start batch of independent decision vectors stored
+ * zstride doubles apart in one launch (outputs stacked problem-major). */
+cito_status cito_linearize_all_dev(cito_handle* h, int32_t N, int32_t n_problems, int64_t zstride, int64_t base_u,
+                                   int64_t base_p, const double* z, double delta, double epsilon, double* ends, double* jx, double* ju, double* js,
                                    double* defects, int32_t* bad, double* psi, double* psi_jac, double* theta,
                                    double* theta_jac, double* imp, double* imp_jac, void* stream);
 

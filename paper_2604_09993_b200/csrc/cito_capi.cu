@@ -417,12 +417,14 @@ cito_status cito_propagate_host(cito_handle* h, int64_t B, const double* xt0s, c
   return count_bad(bad, B);
 }
 
-cito_status cito_linearize_all_dev(cito_handle* h, int32_t N, int64_t base_u, int64_t base_p, const double* z,
-                                   double delta, double epsilon, double* ends, double* jx, double* ju, double* js,
+cito_status cito_linearize_all_dev(cito_handle* h, int32_t N, int32_t n_problems, int64_t zstride, int64_t base_u,
+                                   int64_t base_p, const double* z, double delta, double epsilon, double* ends, double* jx, double* ju, double* js,
                                    double* defects, int32_t* bad, double* psi, double* psi_jac, double* theta,
                                    double* theta_jac, double* imp, double* imp_jac, void* stream) {
   if (!h) return fail(CITO_ERR_ARG, "null handle");
   if (N < 2) return fail(CITO_ERR_ARG, "need at least two grid nodes");
+  if (n_problems < 1) return fail(CITO_ERR_ARG, "n_problems must be >= 1");
+  const int64_t P = n_problems;
   cudaStream_t s = (cudaStream_t)stream;
   std::lock_guard<std::mutex> lk(h->mu);
   if (!h->aux) {
@@ -430,15 +432,15 @@ cito_status cito_linearize_all_dev(cito_handle* h, int32_t N, int64_t base_u, in
     CUDA_TRY(cudaEventCreateWithFlags(&h->ev_in, cudaEventDisableTiming));
     CUDA_TRY(cudaEventCreateWithFlags(&h->ev_out, cudaEventDisableTiming));
   }
-  const ZSrc zs{z, base_u, base_p, defects};
+  const ZSrc zs{z, base_u, base_p, defects, zstride, N - 1, N};
   // node relations (K3) on the auxiliary stream, concurrently with the interval kernel (K1)
   CUDA_TRY(cudaEventRecord(h->ev_in, s));
   CUDA_TRY(cudaStreamWaitEvent(h->aux, h->ev_in, 0));
-  cito_status st = h->ops->node(h->P, N - 1, N, nullptr, nullptr, delta, epsilon, psi, psi_jac, theta, theta_jac, imp,
-                                imp_jac, h->aux, zs);
+  cito_status st = h->ops->node(h->P, P * (N - 1), P * N, nullptr, nullptr, delta, epsilon, psi, psi_jac, theta,
+                                theta_jac, imp, imp_jac, h->aux, zs);
   if (st != CITO_OK) return st;
   CUDA_TRY(cudaEventRecord(h->ev_out, h->aux));
-  st = h->ops->linearize(h->P, N - 1, nullptr, nullptr, nullptr, ends, jx, ju, js, bad, s, zs);
+  st = h->ops->linearize(h->P, P * (N - 1), nullptr, nullptr, nullptr, ends, jx, ju, js, bad, s, zs);
   if (st != CITO_OK) return st;
   CUDA_TRY(cudaStreamWaitEvent(s, h->ev_out, 0));
   __atomic_add_fetch(&h->launches, 2, __ATOMIC_RELAXED);

@@ -88,6 +88,9 @@ struct ZSrc {
   int64_t base_u;
   int64_t base_p;
   double* defects;
+  int64_t zstride;  // distance between the decision vectors of consecutive problems (multi-start batches)
+  int32_t n_int;    // intervals per problem (N - 1)
+  int32_t n_node;   // nodes per problem (N)
 };
 
 template <int N>
@@ -1303,8 +1306,10 @@ __global__ void __launch_bounds__(FusedDims<M>::NT, MINB) k_linearize(const KPar
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   // inputs: either packed batches or gathered straight from the decision vector
   // z (cito/scp.py:98-100, layout cito/ocp.py:154-174)
-  const double* src_x = zs.z ? zs.z + (2 * b + 1) * NXT : xt0s + b * NXT;
-  const double* src_U = zs.z ? zs.z + zs.base_u + b * (2 * NU + 1) : Us + b * 2 * NU;
+  const int64_t zp = zs.z ? b / zs.n_int : 0, zk = zs.z ? b % zs.n_int : 0;  // problem, interval
+  const double* zb = zs.z ? zs.z + zp * zs.zstride : nullptr;
+  const double* src_x = zs.z ? zb + (2 * zk + 1) * NXT : xt0s + b * NXT;
+  const double* src_U = zs.z ? zb + zs.base_u + zk * (2 * NU + 1) : Us + b * 2 * NU;
   for (int k = tid; k < NXT; k += blockDim.x) sh.x[k] = src_x[k];
   for (int k = tid; k < 2 * NU; k += blockDim.x) sh.U[k] = src_U[k];
   if (tid == 0) {
@@ -1434,7 +1439,7 @@ __global__ void __launch_bounds__(FusedDims<M>::NT, MINB) k_linearize(const KPar
   for (int k = tid; k < NXT; k += blockDim.x) {
     const double e = sh.x[k];
     ends[b * NXT + k] = e;
-    if (zs.defects) zs.defects[b * NXT + k] = zs.z[(2 * b + 2) * NXT + k] - e;  // scp.py:115
+    if (zs.defects) zs.defects[b * NXT + k] = zb[(2 * zk + 2) * NXT + k] - e;  // scp.py:115
     if (!isfinite(e)) sh.bad = 1;
   }
   __syncthreads();

@@ -313,10 +313,12 @@ __global__ void __launch_bounds__(64) k_node(const KParams P, int64_t Np, int64_
     double buf[NY2];
     const double* yp = y_pairs + k * 2 * NY;
     if (zs.z) {  // [y+_k, y-_{k+1}] straight from z (Transcription._node_inputs, ocp.py:316-318)
+      const double* zb = zs.z + (k / zs.n_int) * zs.zstride;
+      const int64_t kk = k % zs.n_int;
 #pragma unroll
       for (int i = 0; i < NY; ++i) {
-        buf[i] = zs.z[(2 * k + 1) * NXT + 2 * NQ + i];
-        buf[NY + i] = zs.z[(2 * k + 2) * NXT + 2 * NQ + i];
+        buf[i] = zb[(2 * kk + 1) * NXT + 2 * NQ + i];
+        buf[NY + i] = zb[(2 * kk + 2) * NXT + 2 * NQ + i];
       }
       yp = buf;
     }
@@ -329,12 +331,14 @@ __global__ void __launch_bounds__(64) k_node(const KParams P, int64_t Np, int64_
     double buf[NV];
     const double* vec = theta_vecs + k * NV;
     if (zs.z) {  // [q-, v-, v+, Phi, Gamma] of node k straight from z (ocp.py:319-333)
+      const double* zb = zs.z + (k / zs.n_node) * zs.zstride;
+      const int64_t kk = k % zs.n_node;
 #pragma unroll
-      for (int i = 0; i < 2 * NQ; ++i) buf[i] = zs.z[2 * k * NXT + i];
+      for (int i = 0; i < 2 * NQ; ++i) buf[i] = zb[2 * kk * NXT + i];
 #pragma unroll
-      for (int i = 0; i < NQ; ++i) buf[2 * NQ + i] = zs.z[(2 * k + 1) * NXT + NQ + i];
+      for (int i = 0; i < NQ; ++i) buf[2 * NQ + i] = zb[(2 * kk + 1) * NXT + NQ + i];
 #pragma unroll
-      for (int i = 0; i < 3 * NC; ++i) buf[3 * NQ + i] = zs.z[zs.base_p + 3 * NC * k + i];
+      for (int i = 0; i < 3 * NC; ++i) buf[3 * NQ + i] = zb[zs.base_p + 3 * NC * kk + i];
       vec = buf;
     }
     if (is_th) {

@@ -140,34 +140,40 @@ class GpuTranscription:
     def linearize_device(self, z_dev, delta, epsilon=None, k1_events=None, out=None):
         """Everything on the device in one C-ABI call (cito_linearize_all_dev): the
         interval kernel and the node-relation kernel read z directly and run
-        concurrently.  Returns a dict of torch tensors.  ``k1_events`` = (start,
-        end) CUDA events recorded around the call on the current stream."""
+        concurrently.  ``z_dev`` is (dim,) or a multi-start batch (P, dim); outputs
+        are stacked problem-major ((P*(N-1), ...) / (P*N, ...)).  Returns a dict of
+        torch tensors.  ``k1_events`` = (start, end) CUDA events recorded around
+        the call on the current stream."""
         import torch
 
         if epsilon is None:
             epsilon = self.scenario.ctcs_epsilon
         lay = self.lay
+        P = 1 if z_dev.dim() == 1 else z_dev.shape[0]
+        if z_dev.shape[-1] != lay.dim or not z_dev.is_contiguous():
+            raise ValueError(f"z must be contiguous with last dimension {lay.dim}")
         N, nxt, nu, nq, nc = lay.N, lay.n_xt, lay.n_u, lay.n_q, lay.n_c
+        NI, NN = P * (N - 1), P * N
         n_psi = 3 * nc + lay.n_g_out
         if out is None:
             f64 = dict(dtype=torch.float64, device=self.device)
-            out = dict(ends=torch.empty((N - 1, nxt), **f64), jx=torch.empty((N - 1, nxt, nxt), **f64),
-                       ju=torch.empty((N - 1, nxt, 2 * nu), **f64), js=torch.empty((N - 1, nxt), **f64),
-                       defects=torch.empty((N - 1, nxt), **f64),
-                       bad=torch.empty((N - 1,), dtype=torch.int32, device=self.device),
-                       psi=torch.empty((N - 1, n_psi), **f64), psi_jac=torch.empty((N - 1, n_psi, 2 * lay.n_y), **f64),
-                       theta=torch.empty((N, 6 * nc), **f64), theta_jac=torch.empty((N, 6 * nc, 3 * nq + 3 * nc), **f64),
-                       imp_v=torch.empty((N, nq), **f64), imp_jac=torch.empty((N, nq, 3 * nq + 2 * nc), **f64))
+            out = dict(ends=torch.empty((NI, nxt), **f64), jx=torch.empty((NI, nxt, nxt), **f64),
+                       ju=torch.empty((NI, nxt, 2 * nu), **f64), js=torch.empty((NI, nxt), **f64),
+                       defects=torch.empty((NI, nxt), **f64),
+                       bad=torch.empty((NI,), dtype=torch.int32, device=self.device),
+                       psi=torch.empty((NI, n_psi), **f64), psi_jac=torch.empty((NI, n_psi, 2 * lay.n_y), **f64),
+                       theta=torch.empty((NN, 6 * nc), **f64), theta_jac=torch.empty((NN, 6 * nc, 3 * nq + 3 * nc), **f64),
+                       imp_v=torch.empty((NN, nq), **f64), imp_jac=torch.empty((NN, nq, 3 * nq + 2 * nc), **f64))
         stream = torch.cuda.current_stream(self.device)
         if k1_events is not None:
             k1_events[0].record(stream)
         o = out
         _lib.check(_lib.lib().cito_linearize_all_dev(
-            self.disc._h.ptr, N, int(self.base_u), int(self.base_p), z_dev.data_ptr(), float(delta), float(epsilon),
-            o["ends"].data_ptr(), o["jx"].data_ptr(), o["ju"].data_ptr(), o["js"].data_ptr(), o["defects"].data_ptr(),
-            o["bad"].data_ptr(), o["psi"].data_ptr(), o["psi_jac"].data_ptr(), o["theta"].data_ptr(),
-            o["theta_jac"].data_ptr(), o["imp_v"].data_ptr(), o["imp_jac"].data_ptr(), stream.cuda_stream),
-            "linearize_all")
+            self.disc._h.ptr, N, P, int(lay.dim), int(self.base_u), int(self.base_p), z_dev.data_ptr(), float(delta),
+            float(epsilon), o["ends"].data_ptr(), o["jx"].data_ptr(), o["ju"].data_ptr(), o["js"].data_ptr(),
+            o["defects"].data_ptr(), o["bad"].data_ptr(), o["psi"].data_ptr(), o["psi_jac"].data_ptr(),
+            o["theta"].data_ptr(), o["theta_jac"].data_ptr(), o["imp_v"].data_ptr(), o["imp_jac"].data_ptr(),
+            stream.cuda_stream), "linearize_all")
         if k1_events is not None:
             k1_events[1].record(stream)
         return out

@@ -121,3 +121,25 @@ def test_node_relations_random_z_vs_reference():
         out = gt.nodes.host(yp, tv, float(g["nd_delta"]), gt.scenario.ctcs_epsilon)
         for a, k in zip(out, ("psi", "psi_jac", "theta", "theta_jac", "imp", "imp_jac")):
             assert rel_err(a, g["nd_" + k]) <= 1e-9, (name, k)
+
+
+@pytest.mark.gpu
+def test_multistart_batch_equals_single_problems():
+    """n_problems > 1 in cito_linearize_all_dev == one call per problem (configs[3] path)."""
+    import torch
+
+    from paper_2604_09993_b200.linearize import GpuTranscription, initial_guess
+
+    sc = golden_scenario("halfcheetah_n30")
+    gt = GpuTranscription(sc)
+    Z = np.stack([initial_guess(sc, gt.disc, gt.lay, seed=s) for s in range(3)])
+    Z[1] += 0.01 * np.random.default_rng(0).normal(size=Z.shape[1])
+    zd = torch.as_tensor(Z, device=gt.device)
+    allp = gt.linearize_device(zd, 0.5)
+    n_int, n_node = gt.lay.N - 1, gt.lay.N
+    for p in range(3):
+        one = gt.linearize_device(zd[p].contiguous(), 0.5)
+        for k, v in one.items():
+            rows = n_node if k in ("theta", "theta_jac", "imp_v", "imp_jac") else n_int
+            got = allp[k][p * rows:(p + 1) * rows]
+            assert rel_err(got.cpu().numpy(), v.cpu().numpy()) <= 1e-12, k
