@@ -704,7 +704,8 @@ template <class M>
 struct Dims {
   static constexpr int NL = M::NL, NQ = 3 * NL, NX = 2 * NQ, NC = M::NC, NA = M::NA;
   static constexpr int NU = NA + 3 * NC, NY = 5 * NC + M::NGO, NXT = NX + NY;
-  static constexpr int NCOL = NX + 2 * NU + 1;  // non-y tangent columns: x~+ (q,v), U-, U+, S
+  static constexpr int NCOL = M::NHCOL + 2 * NU + 1;  // advanced tangent columns: heavy x~+ columns, U-, U+, S
+  static constexpr int NCOLX = NX + 2 * NU + 1;         // all non-y columns (incl. closed-form ones)
   static constexpr int NDIR = M::NDIRX + NU;    // rate-Jacobian input directions
   static constexpr int NR = NQ + NY;            // rate rows with a non-trivial Jacobian (vdot, Omega)
   static constexpr int NRP = (NR + 1) & ~1;     // padded to 16 B rows
@@ -827,6 +828,7 @@ struct SParams {
   // index compile to divergent jump tables)
   int jp[NJ], jc[NJ], ja[NJ], jperm[NJ], cl[NC];
   int ba[Pos<M::NBLK>::v], bb[Pos<M::NBLK>::v];
+  int lc[Pos<M::NLCOL>::v];
 };
 
 template <class M>
@@ -1346,6 +1348,8 @@ __global__ void __launch_bounds__(FusedDims<M>::NT, MINB) k_linearize(const KPar
       sh.sp.ba[k] = M::blk_a(k);
       sh.sp.bb[k] = M::blk_b(k);
     }
+#pragma unroll
+    for (int k = 0; k < M::NLCOL; ++k) sh.sp.lc[k] = M::lcol(k);
   }
   for (int c = tid; c < M::NC; c += blockDim.x) {
     sh.sp.cr[c][0] = P.cr[c][0];
@@ -1356,7 +1360,10 @@ __global__ void __launch_bounds__(FusedDims<M>::NT, MINB) k_linearize(const KPar
   const int col = tid - 64;
   const bool colthr = warp >= 2 && col < NCOL;
   const double dS = (col == NCOL - 1) ? 1.0 : 0.0;
-  const int uj = col - NX;
+  // state column seeded by this thread (heavy columns only; the closed-form ones
+  // are written at the end)
+  const int sc = (col >= 0 && col < M::NHCOL) ? M::hcol(col) : -1;
+  const int uj = col - M::NHCOL;
   const bool isU = (uj >= 0) && (uj < 2 * NU);
   const int um = isU ? (uj % Pos<NU>::v) : 0;
   const bool uplus = isU && (uj >= NU);
@@ -1364,7 +1371,7 @@ __global__ void __launch_bounds__(FusedDims<M>::NT, MINB) k_linearize(const KPar
   if (colthr) {
 #pragma unroll
     for (int c = 0; c < NQ; ++c) {
-      const double e_q = (col == c) ? 1.0 : 0.0, e_v = (col == NQ + c) ? 1.0 : 0.0;
+      const double e_q = (sc == c) ? 1.0 : 0.0, e_v = (sc == NQ + c) ? 1.0 : 0.0;
       if (M::hslot(c) >= 0) {
         hq[M::hslot(c)] = e_q;
         hv[M::hslot(c)] = e_v;
@@ -1413,8 +1420,8 @@ __global__ void __launch_bounds__(FusedDims<M>::NT, MINB) k_linearize(const KPar
   if (colthr) {
     double* dst;
     int stride;
-    if (col < NX) {
-      dst = jxb + col;
+    if (sc >= 0) {
+      dst = jxb + sc;
       stride = NXT;
     } else if (isU) {
       dst = jub + uj;
@@ -1431,6 +1438,22 @@ __global__ void __launch_bounds__(FusedDims<M>::NT, MINB) k_linearize(const KPar
     }
 #pragma unroll
     for (int k = 0; k < NY; ++k) dst[(NX + k) * stride] = sh.DY[k][col];
+  }
+  if constexpr (M::NLCOL > 0) {  // closed-form columns (state directions no rate reads)
+    double dqc = 0.0;  // q-row of a v-column: per substep h * (sum_i b_i S), as the RK recursion computes it
+    for (int ss = 0; ss < P.substeps; ++ss) {
+      double inc = 0.0;
+#pragma unroll
+      for (int ii = 0; ii < 6; ++ii) inc += P.b[ii] * S;
+      dqc = dqc + h * inc;
+    }
+    for (int e = tid; e < M::NLCOL * NXT; e += blockDim.x) {
+      const int lc = e / NXT, r = e % NXT;
+      const int c = sh.sp.lc[lc];
+      double val = (r == c) ? 1.0 : 0.0;
+      if (c >= NQ && r == c - NQ) val = dqc;
+      jxb[r * NXT + c] = val;
+    }
   }
   for (int e = tid; e < NXT * NY; e += blockDim.x) {  // y0 columns of jx: identity (rates ignore y)
     const int r = e / Pos<NY>::v, c = NX + e % Pos<NY>::v;
