@@ -57,16 +57,17 @@ def run(B):
         print("primal tick", t, "sub-step cycles", np.diff(row).tolist())
     nt = 32
     t0 = a[0, :, 0][a[0, :, 0] > 0].min()
-    print("tick  " + "  ".join(f"w{w}:work" for w in range(5)) + "   tick_total")
+    nw = int(sum(1 for w in range(8) if a[2, w, 0] > 0))
+    print("tick  " + "  ".join(f"w{w}:work" for w in range(nw)) + "   tick_total")
     tot = []
     for t in range(nt):
-        st, en = a[t, :5, 0], a[t, :5, 1]
+        st, en = a[t, :nw, 0], a[t, :nw, 1]
         if not (st > 0).all():
             continue
-        nxt = a[t + 1, :5, 0].min() if t + 1 < nt and (a[t + 1, :5, 0] > 0).all() else en.max()
+        nxt = a[t + 1, :nw, 0].min() if t + 1 < nt and (a[t + 1, :nw, 0] > 0).all() else en.max()
         tot.append(nxt - st.min())
         print(f"{t:4d}  " + "  ".join(f"{int(e - s):8d}" for s, e in zip(st, en)) + f"   {int(nxt - st.min()):8d}")
-    print("total cycles", int(a[nt - 1, :5, 1].max() - t0), "mean tick", float(np.mean(tot)))
+    print("total cycles", int(a[nt - 1, :nw, 1].max() - t0), "mean tick", float(np.mean(tot)))
 
 
 if __name__ == "__main__":
