@@ -496,16 +496,13 @@ __device__ void prim_rate(const KParams& P, const double* xs, const double* u, P
 // Tangent of the unscaled rate along one input direction `dir` of (q, v, u):
 //   dir in [0, NQ) -> q_dir, [NQ, 2NQ) -> v, [2NQ, 2NQ+NU) -> u.
 // Writes out[0:NQ] = d vdot, out[NQ:NQ+NY] = d Omega.
-// KIND: 0 = any direction, 1 = state directions only (control seeds are
-// compile-time zero), 2 = control directions only (state seeds are zero), so
-// each specialized warp compiles without the dead seed terms.
-template <class M, int KIND = 0>
+template <class M>
 __device__ void tan_rate(const KParams& P, const Prim<M>& pr, const double* v, int dir, double* out,
                          int ostride) {
   constexpr int NL = M::NL, NJ = M::NJ, NC = M::NC, NA = M::NA, NQ = 3 * NL, NX = 2 * NQ;
-#define SQ(k) ((KIND != 2 && (dir) == (k)) ? 1.0 : 0.0)
-#define SV(k) ((KIND != 2 && (dir) == NQ + (k)) ? 1.0 : 0.0)
-#define SU(m) ((KIND != 1 && (dir) == NX + (m)) ? 1.0 : 0.0)
+#define SQ(k) ((dir) == (k) ? 1.0 : 0.0)
+#define SV(k) ((dir) == NQ + (k) ? 1.0 : 0.0)
+#define SU(m) ((dir) == NX + (m) ? 1.0 : 0.0)
   double dW[NQ];
 #pragma unroll
   for (int k = 0; k < NQ; ++k) dW[k] = 0.0;
@@ -817,7 +814,7 @@ template <class M>
 struct FusedDims {
   using D = Dims<M>;
   static constexpr int NCW = (D::NCOL + 31) / 32;
-  static constexpr int NT = 96 + 32 * NCW;  // primal warp, 2 Jacobian warps, column warps
+  static constexpr int NT = 64 + 32 * NCW;
 };
 
 template <class M>
@@ -1360,8 +1357,8 @@ __global__ void __launch_bounds__(FusedDims<M>::NT, MINB) k_linearize(const KPar
     sh.sp.mu[c] = P.mu[c];
   }
   // column state: seed = unit column of [x~+ | U- | U+ | S]
-  const int col = tid - 96;
-  const bool colthr = warp >= 3 && col < NCOL;
+  const int col = tid - 64;
+  const bool colthr = warp >= 2 && col < NCOL;
   const double dS = (col == NCOL - 1) ? 1.0 : 0.0;
   // state column seeded by this thread (heavy columns only; the closed-form ones
   // are written at the end)
@@ -1393,17 +1390,14 @@ __global__ void __launch_bounds__(FusedDims<M>::NT, MINB) k_linearize(const KPar
     CITO_MARK((t * 8 + warp) * 2);
     if (warp == 0) {
       if (t < NST) fused_primal<M>(P, sh, t, lane);
-    } else if (warp == 1) {  // rate Jacobian, state directions
+    } else if (warp == 1) {
       if (t >= 1 && t <= NST) {
         const int st = t - 1;
         const Rec<M>& R = sh.ring[st % 3];
-        for (int kd = lane; kd < NDIRX; kd += 32) tan_rate<M, 1>(P, R.pr, R.vs, M::dir(kd), &sh.At[st & 1][kd][0], 1);
-      }
-    } else if (warp == 2) {  // rate Jacobian, control directions
-      if (t >= 1 && t <= NST) {
-        const int st = t - 1;
-        const Rec<M>& R = sh.ring[st % 3];
-        for (int m = lane; m < NU; m += 32) tan_rate<M, 2>(P, R.pr, R.vs, NX + m, &sh.At[st & 1][NDIRX + m][0], 1);
+        for (int kd = lane; kd < NDIR; kd += 32) {
+          const int dir = kd < NDIRX ? M::dir(kd) : NX + (kd - NDIRX);
+          tan_rate<M>(P, R.pr, R.vs, dir, &sh.At[st & 1][kd][0], 1);
+        }
       }
     } else if (colthr && t >= 2) {
       const int st = t - 2;
