@@ -179,6 +179,25 @@ cito_status cito_scatter_dynamics_dev(cito_handle* h, int64_t n_int, const doubl
                                       const int32_t* slot_s, double* A_data, double* b_rows,
                                       int32_t* mismatch, void* stream);
 
+/* Whole-subproblem CSC assembly (cito/scp.py:160-351 +
+ * cito/conic.py:99-125, 209-269).  A superset CSC (sp_ptr[ncols+1], sp_row)
+ * carries one value recipe per entry: sp_src < 0 -> constant sp_val, else
+ * (sp_val * lin[sp_src][sp_idx]) * sigma[col].  Exact zeros are dropped and the
+ * rest compacted: out_ptr[ncols+1] (int32), out_rows/out_vals[<= superset nnz].
+ * lin: HOST array of 10 device pointers {jx, ju, js, imp_jac, theta_jac,
+ * psi_jac, ends, imp_v, theta, psi}; counts: device workspace [ncols]. */
+cito_status cito_csc_assemble_dev(int32_t ncols, const int64_t* sp_ptr, const int32_t* sp_row, const int8_t* sp_src,
+                                  const int64_t* sp_idx, const double* sp_val, const double* sigma,
+                                  const double* const* lin, int32_t* counts, int32_t* out_ptr, int32_t* out_rows,
+                                  double* out_vals, void* stream);
+
+/* b / h of the linearized rows: out[rows[i]] = form ? J.z[cols] - v : v - J.z[cols]
+ * with J split in up to 3 segments (seg_src < 0 = unused), v = lin[vsrc[i]][voff[i]]. */
+cito_status cito_rhs_dev(int64_t nrows, const int32_t* rows, const int8_t* form, const int8_t* vsrc,
+                         const int64_t* voff, const int8_t* seg_src, const int64_t* seg_off, const int32_t* seg_len,
+                         const int64_t* seg_cb, const int64_t* cols, const double* z, const double* const* lin,
+                         double* out, void* stream);
+
 /* FP64 DFMA throughput probe (roofline denominator; not part of the reference
  * interface).  Launches one kernel on `stream`; returns the flops it issues
  * (time it with events on the same stream), or -1 on launch failure. */

@@ -66,6 +66,10 @@ def _load():
         L.cito_linearize_all_dev.argtypes = ([ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64,
                                               ctypes.c_int64, ctypes.c_int64, _dp, ctypes.c_double, ctypes.c_double]
                                              + [_dp] * 13)
+        L.cito_csc_assemble_dev.restype = ctypes.c_int
+        L.cito_csc_assemble_dev.argtypes = [ctypes.c_int32] + [_dp] * 12
+        L.cito_rhs_dev.restype = ctypes.c_int
+        L.cito_rhs_dev.argtypes = [ctypes.c_int64] + [_dp] * 13
         L.cito_dfma_peak.restype = ctypes.c_double
         L.cito_dfma_peak.argtypes = [ctypes.c_int32, _dp, _dp]
         _lib = L

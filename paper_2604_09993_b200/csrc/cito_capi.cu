@@ -17,6 +17,7 @@
 #include "cito_node.cuh"
 #include "cito_scatter.cuh"
 #include "cito_bench.cuh"
+#include "cito_subproblem.cuh"
 
 namespace {
 
@@ -463,6 +464,40 @@ cito_status cito_scatter_dynamics_dev(cito_handle* h, int64_t n_int, const doubl
       slot_s, A_data, b_rows, mismatch);
   CUDA_TRY(cudaGetLastError());
   __atomic_add_fetch(&h->launches, 1, __ATOMIC_RELAXED);
+  return CITO_OK;
+}
+
+cito_status cito_csc_assemble_dev(int32_t ncols, const int64_t* sp_ptr, const int32_t* sp_row, const int8_t* sp_src,
+                                  const int64_t* sp_idx, const double* sp_val, const double* sigma,
+                                  const double* const* lin, int32_t* counts, int32_t* out_ptr, int32_t* out_rows,
+                                  double* out_vals, void* stream) {
+  if (ncols <= 0) return CITO_OK;
+  LinTable L;
+  for (int k = 0; k < 10; ++k) L.p[k] = lin ? lin[k] : nullptr;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int wpb = 8;
+  const unsigned grid = (unsigned)((ncols + wpb - 1) / wpb);
+  k_csc_count<<<grid, 32 * wpb, 0, s>>>(ncols, sp_ptr, sp_src, sp_idx, sp_val, sigma, L, counts);
+  CUDA_TRY(cudaGetLastError());
+  k_scan<<<1, 1024, 0, s>>>(ncols, counts, out_ptr);
+  CUDA_TRY(cudaGetLastError());
+  k_csc_write<<<grid, 32 * wpb, 0, s>>>(ncols, sp_ptr, sp_row, sp_src, sp_idx, sp_val, sigma, L, out_ptr, out_rows,
+                                       out_vals);
+  CUDA_TRY(cudaGetLastError());
+  return CITO_OK;
+}
+
+cito_status cito_rhs_dev(int64_t nrows, const int32_t* rows, const int8_t* form, const int8_t* vsrc,
+                         const int64_t* voff, const int8_t* seg_src, const int64_t* seg_off, const int32_t* seg_len,
+                         const int64_t* seg_cb, const int64_t* cols, const double* z, const double* const* lin,
+                         double* out, void* stream) {
+  if (nrows <= 0) return CITO_OK;
+  LinTable L;
+  for (int k = 0; k < 10; ++k) L.p[k] = lin ? lin[k] : nullptr;
+  const int wpb = 8;
+  k_rhs<<<(unsigned)((nrows + wpb - 1) / wpb), 32 * wpb, 0, (cudaStream_t)stream>>>(
+      nrows, rows, form, vsrc, voff, seg_src, seg_off, seg_len, seg_cb, cols, z, L, out);
+  CUDA_TRY(cudaGetLastError());
   return CITO_OK;
 }
 

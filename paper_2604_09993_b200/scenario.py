@@ -120,17 +120,22 @@ def scenario_from_dict(data, base_dir="."):  # ocp.py:578-624
 
 
 def load_scenario(path, **overrides):
+    """Load a scenario file; overrides follow the reference's recipe
+    ``dataclasses.replace(sc, N=N, s_bounds=None)``: derived
+    fields already filled by __post_init__ (force_max, impulse_max,
+    guess_force_scale) keep the values of the file's own N."""
+    from dataclasses import replace
+
     with open(path) as f:
         data = json.load(f)
+    sc = scenario_from_dict(data, base_dir=os.path.dirname(os.path.abspath(path)))
     if "N" in overrides:
-        data["N"] = overrides.pop("N")
-        data.get("horizon", {}).pop("s_min", None)
-        data.get("horizon", {}).pop("s_max", None)
+        sc = replace(sc, N=int(overrides.pop("N")), s_bounds=None)
     if "substeps" in overrides:
-        data["substeps"] = overrides.pop("substeps")
+        sc = replace(sc, substeps=int(overrides.pop("substeps")))
     if overrides:
         raise TypeError(f"unknown overrides {sorted(overrides)}")
-    return scenario_from_dict(data, base_dir=os.path.dirname(os.path.abspath(path)))
+    return sc
 
 
 class Layout:

@@ -1,0 +1,460 @@
+"""GPU assembly of the whole SCP convex subproblem.
+
+Replaces `cito.scp.build_subproblem` + `cito.conic.canonicalize`
+(/root/reference/pkg/src/cito/scp.py:160-351, conic.py:99-125, 209-269) for the
+iteration loop: every row of A (equalities) and G (orthant rows, then SOC
+blocks) is laid out once per (scenario, SCP config) as a *superset* CSC pattern
+whose entries carry a value recipe -- a constant (computed on the host exactly
+as the reference computes it) or `(sign * LIN[src][idx]) * sigma[col]` for the
+linearized rows (dynamics, impulse map, impact complementarity Theta, integral
+complementarity Psi).  Per iteration the device evaluates the recipes, drops
+exact zeros (the reference's `keep = vals != 0` and `eliminate_zeros`) and
+compacts to the final CSC (sorted rows, int32 indices), and forms b/h of the
+linearized rows; c depends on z_j only.  The pattern therefore moves with the
+data exactly as the reference's does (node rows change with Phi, §0.5).
+
+Row order (scp.py:226-337): A = [dynamics (k, r)], per node k [impulse (n_q),
+copy (n_q + n_y), Theta-eq (2 n_c)], [x_init (2 n_q), y_init (n_y), masked
+x_final, fixed time]; G = per node k [Theta-ineq (4 n_c), impulse boxes (3 per
+contact)], per interval [Psi (n_psi), accumulator increments (5 n_c)], control
+boxes per (k, side), dilation boxes, slack nonnegativity, then SOC blocks in
+add_soc order (node impulse cones inside the node loop, control cones).
+"""
+
+import sys
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+
+__all__ = ["SubproblemPattern", "SubproblemAssembler", "LIN_SOURCES"]
+
+# value sources (device pointer table order)
+LIN_SOURCES = ["jx", "ju", "js", "imp_jac", "theta_jac", "psi_jac", "ends", "imp_v", "theta", "psi"]
+SRC = {k: i for i, k in enumerate(LIN_SOURCES)}
+
+
+class _Rows:
+    """Append-only COO with recipes: const entries (src = -1, val = value) or
+    linearized entries (src >= 0, idx = flat index, val = sign)."""
+
+    def __init__(self):
+        self.row, self.col, self.src, self.idx, self.val = [], [], [], [], []
+        self.rhs = []  # constant rhs per row (np.nan where the device computes it)
+        self.n = 0
+
+    def add(self, cols, src, idx, val, rhs):
+        cols = np.asarray(cols, dtype=np.int64)
+        m = cols.size
+        self.row.append(np.full(m, self.n, dtype=np.int64))
+        self.col.append(cols)
+        self.src.append(np.broadcast_to(np.asarray(src, dtype=np.int8), (m,)).copy())
+        self.idx.append(np.broadcast_to(np.asarray(idx, dtype=np.int64), (m,)).copy())
+        self.val.append(np.broadcast_to(np.asarray(val, dtype=np.float64), (m,)).copy())
+        self.rhs.append(rhs)
+        self.n += 1
+        return self.n - 1
+
+    def arrays(self):
+        cat = lambda L, dt: np.concatenate(L).astype(dt) if L else np.zeros(0, dt)
+        return (cat(self.row, np.int64), cat(self.col, np.int64), cat(self.src, np.int8), cat(self.idx, np.int64),
+                cat(self.val, np.float64), np.asarray(self.rhs, dtype=np.float64))
+
+
+class SubproblemPattern:
+    """Superset CSC + recipes of A and G, constant rhs, P, cones (host, once)."""
+
+    def __init__(self, scenario, lay, scale_v, w_prox=2000.0, w_ep=50000.0):
+        sc = scenario
+        model = sc.model
+        self.lay = lay
+        N, n_q, n_c, n_y, n_xt, n_u, n_a = lay.N, lay.n_q, lay.n_c, lay.n_y, lay.n_xt, lay.n_u, lay.n_a
+        self.n_psi = n_psi = 3 * n_c + lay.n_g_out
+        sigma = np.asarray(scale_v, dtype=float)
+        self.sigma = sigma
+        self.n_eq_slack = n_eq = (N - 1) * n_xt + N * (n_q + 2 * n_c)
+        self.n_in_slack = n_in = (N - 1) * n_psi + N * 4 * n_c
+        dim = lay.dim
+        self.n = n = dim + 2 * n_eq + n_in
+        sp0, sm0, t0 = dim, dim + n_eq, dim + 2 * n_eq
+        self.z_idx = np.arange(0, dim)
+        self.sp_idx = np.arange(sp0, sp0 + n_eq)
+        self.sm_idx = np.arange(sm0, sm0 + n_eq)
+        self.t_idx = np.arange(t0, t0 + n_in)
+        A, G, S = _Rows(), _Rows(), _Rows()
+        lin_rows_A, lin_rows_G = [], []  # (row, form, segments[(src, off, len, cols)], vsrc, voff)
+        state = lambda idx: idx  # noqa: E731
+        nu2 = 2 * n_u
+        eq_s = 0
+        in_s = 0
+        # -- multiple-shooting defects (scp.py:226-236)
+        for k in range(N - 1):
+            xp_k, xm_n, u_k, s_k = lay.xp(k), lay.xm(k + 1), lay.u(k), lay.s(k)
+            for r in range(n_xt):
+                cols = np.concatenate([[xm_n[r]], xp_k, u_k, s_k, [sp0 + eq_s, sm0 + eq_s]])
+                src = np.concatenate([[-1], np.full(n_xt, SRC["jx"]), np.full(nu2, SRC["ju"]), [SRC["js"]], [-1, -1]])
+                idx = np.concatenate([[0], (k * n_xt + r) * n_xt + np.arange(n_xt),
+                                      (k * n_xt + r) * nu2 + np.arange(nu2), [k * n_xt + r], [0, 0]])
+                val = np.concatenate([[1.0 * sigma[xm_n[r]]], -np.ones(n_xt + nu2 + 1), [-1.0, 1.0]])
+                row = A.add(cols, src, idx, val, np.nan)
+                lin_rows_A.append((row, 0, [(SRC["jx"], (k * n_xt + r) * n_xt, n_xt, xp_k),
+                                            (SRC["ju"], (k * n_xt + r) * nu2, nu2, u_k),
+                                            (SRC["js"], k * n_xt + r, 1, s_k)], SRC["ends"], k * n_xt + r))
+                eq_s += 1
+        # -- node relations (scp.py:239-282)
+        _, imp_hi = _impulse_bounds(sc, lay)
+        n_vec = 3 * n_q + 3 * n_c
+        n_imp = 3 * n_q + 2 * n_c
+        for k in range(N):
+            xm_k, xp_k, phi_k, gam_k = lay.xm(k), lay.xp(k), lay.phi(k), lay.gam(k)
+            vec_cols = np.concatenate([xm_k[:n_q], xm_k[n_q: 2 * n_q], xp_k[n_q: 2 * n_q], phi_k, gam_k])
+            imp_cols = vec_cols[:n_imp]
+            for r in range(n_q):  # impulse-map velocity rows
+                cols = np.concatenate([imp_cols, [sp0 + eq_s, sm0 + eq_s]])
+                src = np.concatenate([np.full(n_imp, SRC["imp_jac"]), [-1, -1]])
+                idx = np.concatenate([(k * n_q + r) * n_imp + np.arange(n_imp), [0, 0]])
+                val = np.concatenate([np.ones(n_imp), [-1.0, 1.0]])
+                row = A.add(cols, src, idx, val, np.nan)
+                lin_rows_A.append((row, 1, [(SRC["imp_jac"], (k * n_q + r) * n_imp, n_imp, imp_cols)],
+                                   SRC["imp_v"], k * n_q + r))
+                eq_s += 1
+            for r in list(range(n_q)) + list(range(2 * n_q, n_xt)):  # copy rows
+                cols = np.array([xp_k[r], xm_k[r]])
+                vals = np.array([1.0, -1.0]) * sigma[cols]
+                A.add(cols, -1, 0, vals, 0.0)
+            for r in range(2 * n_c):  # Theta equality rows
+                cols = np.concatenate([vec_cols, [sp0 + eq_s, sm0 + eq_s]])
+                src = np.concatenate([np.full(n_vec, SRC["theta_jac"]), [-1, -1]])
+                idx = np.concatenate([(k * 6 * n_c + r) * n_vec + np.arange(n_vec), [0, 0]])
+                val = np.concatenate([np.ones(n_vec), [-1.0, 1.0]])
+                row = A.add(cols, src, idx, val, np.nan)
+                lin_rows_A.append((row, 1, [(SRC["theta_jac"], (k * 6 * n_c + r) * n_vec, n_vec, vec_cols)],
+                                   SRC["theta"], k * 6 * n_c + r))
+                eq_s += 1
+            for r in range(2 * n_c, 6 * n_c):  # Theta inequality rows
+                cols = np.concatenate([vec_cols, [t0 + in_s]])
+                src = np.concatenate([np.full(n_vec, SRC["theta_jac"]), [-1]])
+                idx = np.concatenate([(k * 6 * n_c + r) * n_vec + np.arange(n_vec), [0]])
+                val = np.concatenate([np.ones(n_vec), [-1.0]])
+                row = G.add(cols, src, idx, val, np.nan)
+                lin_rows_G.append((row, 1, [(SRC["theta_jac"], (k * 6 * n_c + r) * n_vec, n_vec, vec_cols)],
+                                   SRC["theta"], k * 6 * n_c + r))
+                in_s += 1
+            for i in range(n_c):  # impulse boxes
+                G.add([phi_k[2 * i + 1]], -1, 0, [1.0 * sigma[phi_k[2 * i + 1]]], float(imp_hi[2 * i + 1]))
+                G.add([gam_k[i]], -1, 0, [1.0 * sigma[gam_k[i]]], float(imp_hi[2 * n_c + i]))
+                G.add([gam_k[i]], -1, 0, [-1.0 * sigma[gam_k[i]]], 0.0)
+            for i in range(n_c):  # impulse friction cones (SOC)
+                mu = model.contacts[i].friction_mu
+                self._soc(S, ((phi_k[2 * i + 1], -mu), (phi_k[2 * i], -1.0)), sigma)
+        # -- integral complementarity rows (scp.py:285-301)
+        for k in range(N - 1):
+            pair_cols = np.concatenate([lay.y_of_xp(k), lay.y_of_xm(k + 1)])
+            for r in range(n_psi):
+                cols = np.concatenate([pair_cols, [t0 + in_s]])
+                src = np.concatenate([np.full(2 * n_y, SRC["psi_jac"]), [-1]])
+                idx = np.concatenate([(k * n_psi + r) * 2 * n_y + np.arange(2 * n_y), [0]])
+                val = np.concatenate([np.ones(2 * n_y), [-1.0]])
+                row = G.add(cols, src, idx, val, np.nan)
+                lin_rows_G.append((row, 1, [(SRC["psi_jac"], (k * n_psi + r) * 2 * n_y, 2 * n_y, pair_cols)],
+                                   SRC["psi"], k * n_psi + r))
+                in_s += 1
+            for i in range(5 * n_c):
+                margin = 2.0 * sc.ctcs_epsilon if i % 5 == 4 else 0.0
+                cols = np.array([pair_cols[n_y + i], pair_cols[i]])
+                G.add(cols, -1, 0, np.array([-1.0, 1.0]) * sigma[cols], margin)
+        # -- control boxes, cones, dilation boxes (scp.py:304-324)
+        lo_u, hi_u = _control_bounds(sc, lay)
+        for k in range(N - 1):
+            u_k, s_k = lay.u(k), lay.s(k)
+            for side in range(2):
+                base = side * n_u
+                for i in range(n_a):
+                    c = u_k[base + i]
+                    G.add([c], -1, 0, [1.0 * sigma[c]], float(hi_u[i]))
+                    G.add([c], -1, 0, [-1.0 * sigma[c]], float(-lo_u[i]))
+                for i in range(n_c):
+                    c = u_k[base + n_a + 2 * i + 1]
+                    G.add([c], -1, 0, [1.0 * sigma[c]], float(hi_u[n_a + 2 * i + 1]))
+                    gi = n_a + 2 * n_c + i
+                    c = u_k[base + gi]
+                    G.add([c], -1, 0, [1.0 * sigma[c]], float(hi_u[gi]))
+                    G.add([c], -1, 0, [-1.0 * sigma[c]], 0.0)
+                for i in range(n_c):
+                    mu = model.contacts[i].friction_mu
+                    fn = u_k[base + n_a + 2 * i + 1]
+                    ft = u_k[base + n_a + 2 * i]
+                    self._soc(S, ((fn, -mu), (ft, -1.0)), sigma)
+            G.add(s_k, -1, 0, [1.0 * sigma[s_k[0]]], float(sc.s_bounds[1]))
+            G.add(s_k, -1, 0, [-1.0 * sigma[s_k[0]]], float(-sc.s_bounds[0]))
+        # -- boundary conditions (scp.py:327-337)
+        x_dim = 2 * n_q
+        for r in range(x_dim):
+            c = lay.xm(0)[r]
+            A.add([c], -1, 0, [1.0 * sigma[c]], float(sc.x_init[r]))
+        for r in range(n_y):
+            c = lay.y_of_xm(0)[r]
+            A.add([c], -1, 0, [1.0 * sigma[c]], 0.0)
+        for r in range(x_dim):
+            if sc.mask_final[r]:
+                c = lay.xp(N - 1)[r]
+                A.add([c], -1, 0, [1.0 * sigma[c]], float(sc.x_final[r]))
+        if sc.fixed_time:
+            cols = np.concatenate([lay.s(k) for k in range(N - 1)])
+            A.add(cols, -1, 0, np.ones(N - 1) * sigma[cols], float(sc.t_f))
+        # -- slack nonnegativity (scp.py:345-348)
+        for idx_set in (self.sp_idx, self.sm_idx, self.t_idx):
+            for i in idx_set:
+                G.add([i], -1, 0, [-1.0], 0.0)
+        assert eq_s == n_eq and in_s == n_in
+        self.n_orthant = G.n
+        # SOC rows follow the orthant rows (conic.py:250-258)
+        g_rows = G.arrays()
+        s_rows = S.arrays()
+        s_rows = (s_rows[0] + G.n,) + s_rows[1:]
+        G_all = tuple(np.concatenate([a, b]) for a, b in zip(g_rows, s_rows))
+        self.soc_dims = tuple([2] * (S.n // 2))
+        self.A = self._csc(A.arrays(), A.n, n)
+        self.G = self._csc(G_all, G.n + S.n, n)
+        self.lin_rows_A = lin_rows_A
+        self.lin_rows_G = lin_rows_G
+        # objective (scp.py:340-348 + conic.py:214-232): P diagonal, c
+        P_cost, c_cost = _cost_quadratic(sc, lay)
+        pdiag = np.zeros(n)
+        v1 = P_cost * sigma[:dim] ** 2
+        pdiag[:dim] = np.where(v1 != 0.0, v1, 0.0)
+        pdiag[:dim] = pdiag[:dim] + 2.0 * w_prox
+        self.P_diag = pdiag
+        self.c_fixed = np.zeros(n)
+        lin0 = sigma[:dim] * (P_cost * 0.0 + c_cost)
+        self.c_fixed[:dim] = np.where(lin0 != 0.0, lin0, 0.0)
+        for idx_set in (self.sp_idx, self.sm_idx, self.t_idx):
+            self.c_fixed[idx_set] += w_ep
+        self.w_prox = w_prox
+
+    def sigma_full(self):
+        """Per-column scale of the whole variable vector (slacks are unscaled)."""
+        return np.concatenate([self.sigma, np.ones(self.n - self.lay.dim)])
+
+    def objective_c(self, z_j):
+        """c of the subproblem at iterate z_j (scp.py:341-346, conic.py:227-229)."""
+        dim = self.lay.dim
+        c = self.c_fixed.copy()
+        add = -2.0 * self.w_prox * ((np.asarray(z_j, dtype=float) - 0.0) / self.sigma[:dim])
+        c[:dim] = c[:dim] + add
+        return c
+
+    @staticmethod
+    def _soc(S, entries, sigma):
+        for (c, v) in entries:  # soc_entry: vals * sigma[cols], offset 0 (scp.py:218-221)
+            S.add([c], -1, 0, [np.float64(v) * sigma[c]], 0.0)
+
+    def _csc(self, arrs, nrows, ncols):
+        row, col, src, idx, val, rhs = arrs
+        order = np.lexsort((row, col))
+        key = col[order] * (nrows + 1) + row[order]
+        assert np.all(np.diff(key) > 0), "duplicate (row, col) in the superset"
+        counts = np.bincount(col, minlength=ncols)
+        return dict(indptr=np.concatenate([[0], np.cumsum(counts)]).astype(np.int64), row=row[order].astype(np.int32),
+                    col=col[order], src=src[order], idx=idx[order], val=val[order], rhs=rhs, nrows=nrows)
+
+
+def _impulse_bounds(sc, lay):  # ocp.py:443-457
+    n_c = lay.n_c
+    lo = np.empty(3 * n_c)
+    hi = np.empty(3 * n_c)
+    for i in range(n_c):
+        mu = sc.model.contacts[i].friction_mu
+        lo[2 * i] = -mu * sc.impulse_max
+        hi[2 * i] = mu * sc.impulse_max
+        lo[2 * i + 1] = 0.0
+        hi[2 * i + 1] = sc.impulse_max
+    lo[2 * n_c:] = 0.0
+    hi[2 * n_c:] = sc.gamma_max
+    return lo, hi
+
+
+def _control_bounds(sc, lay):  # ocp.py:419-441
+    model = sc.model
+    lo = np.empty(lay.n_u)
+    hi = np.empty(lay.n_u)
+    for a, j in enumerate(model.actuated_joints):
+        lo[a] = model.joints[j].torque_min
+        hi[a] = model.joints[j].torque_max
+    for i in range(lay.n_c):
+        mu = model.contacts[i].friction_mu
+        lo[lay.n_a + 2 * i] = -mu * sc.force_max
+        hi[lay.n_a + 2 * i] = mu * sc.force_max
+        lo[lay.n_a + 2 * i + 1] = 0.0
+        hi[lay.n_a + 2 * i + 1] = sc.force_max
+    lo[lay.n_a + 2 * lay.n_c:] = 0.0
+    hi[lay.n_a + 2 * lay.n_c:] = sc.gamma_max
+    return lo, hi
+
+
+def _cost_quadratic(sc, lay):  # ocp.py:380-390
+    P = np.zeros(lay.dim)
+    c = np.zeros(lay.dim)
+    for k in range(lay.N - 1):
+        tq = np.concatenate([lay.u(k)[: lay.n_a], lay.u(k)[lay.n_u: lay.n_u + lay.n_a]])
+        P[tq] += sc.torque_weight
+        if sc.s_reg:
+            P[lay.s(k)] += sc.s_reg
+            c[lay.s(k)] += -sc.s_reg * sc.s_nominal
+    return P, c
+
+
+@dataclass
+class _Meta:
+    """Same interface as cito.scp._SubproblemMeta (scp.py:138-157)."""
+
+    z_idx: np.ndarray
+    sp_idx: np.ndarray
+    sm_idx: np.ndarray
+    t_idx: np.ndarray
+
+    def step_scaled(self, sol, z_j_scaled):
+        return sol.x[self.z_idx] - z_j_scaled
+
+    def j_px(self, sol, z_j_scaled):
+        d = self.step_scaled(sol, z_j_scaled)
+        return float(d @ d)
+
+    def j_ep(self, sol):
+        return float(np.sum(sol.x[self.sp_idx]) + np.sum(sol.x[self.sm_idx]) + np.sum(sol.x[self.t_idx]))
+
+
+def _conic_types():
+    mod = sys.modules.get("cito.conic")
+    if mod is not None and hasattr(mod, "ConicProgram"):
+        return mod.ConicProgram, mod.ConeSpec
+    from dataclasses import make_dataclass
+
+    ConeSpec = make_dataclass("ConeSpec", [("nonneg", int, 0), ("soc", tuple, ())], frozen=True)
+    ConicProgram = make_dataclass("ConicProgram", ["P", "c", "A", "b", "G", "h", "cones"])
+    return ConicProgram, ConeSpec
+
+
+class SubproblemAssembler:
+    """Device-side assembly of the whole subproblem from a device linearization."""
+
+    def __init__(self, pattern, device):
+        import torch
+
+        self.pat = pattern
+        self.device = device
+        t = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a, dtype=dt), device=device)  # noqa: E731
+        self.sigma_dev = t(pattern.sigma_full(), np.float64)
+        self._mats = {}
+        for M, rows in (("A", pattern.lin_rows_A), ("G", pattern.lin_rows_G)):
+            csc = getattr(pattern, M)
+            d = dict(sp_ptr=t(csc["indptr"], np.int64), row=t(csc["row"], np.int32), src=t(csc["src"], np.int8),
+                     idx=t(csc["idx"], np.int64), val=t(csc["val"], np.float64), nrows=csc["nrows"],
+                     nsup=int(csc["row"].size), rhs_const=t(np.nan_to_num(csc["rhs"]), np.float64))
+            d["counts"] = torch.empty(pattern.n, dtype=torch.int32, device=device)
+            # rhs descriptors of the linearized rows
+            nr = len(rows)
+            r_row = np.array([r[0] for r in rows], dtype=np.int32)
+            r_form = np.array([r[1] for r in rows], dtype=np.int8)
+            r_vsrc = np.array([r[3] for r in rows], dtype=np.int8)
+            r_voff = np.array([r[4] for r in rows], dtype=np.int64)
+            seg_src = np.full((nr, 3), -1, dtype=np.int8)
+            seg_off = np.zeros((nr, 3), dtype=np.int64)
+            seg_len = np.zeros((nr, 3), dtype=np.int32)
+            seg_cb = np.zeros((nr, 3), dtype=np.int64)
+            cols, cache = [], {}
+            total = 0
+            for i, (_, _, segs, _, _) in enumerate(rows):
+                for j, (s, off, ln, cz) in enumerate(segs):
+                    key = (int(cz[0]), int(len(cz)))
+                    if key not in cache:
+                        cache[key] = total
+                        cols.append(np.asarray(cz, dtype=np.int64))
+                        total += len(cz)
+                    seg_src[i, j], seg_off[i, j], seg_len[i, j], seg_cb[i, j] = s, off, ln, cache[key]
+            d.update(nlin=nr, r_row=t(r_row, np.int32), r_form=t(r_form, np.int8), r_vsrc=t(r_vsrc, np.int8),
+                     r_voff=t(r_voff, np.int64), seg_src=t(seg_src, np.int8), seg_off=t(seg_off, np.int64),
+                     seg_len=t(seg_len, np.int32), seg_cb=t(seg_cb, np.int64),
+                     cols=t(np.concatenate(cols) if cols else np.zeros(1), np.int64))
+            self._mats[M] = d
+
+    def assemble_device(self, lin, z_ref_dev, stream=None):
+        """lin: dict of device tensors with the LIN_SOURCES fields.  Returns device
+        tensors {A_indptr, A_indices, A_data, b, G_indptr, G_indices, G_data, h}
+        (data/indices sized to the superset; valid prefix = indptr[-1])."""
+        import torch
+
+        s = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
+        ptrs = (ctypes_ptr_array([lin[k].data_ptr() for k in LIN_SOURCES]))
+        out = {}
+        for M, d in self._mats.items():
+            indptr = torch.empty(self.pat.n + 1, dtype=torch.int32, device=self.device)
+            rows = torch.empty(max(1, d["nsup"]), dtype=torch.int32, device=self.device)
+            vals = torch.empty(max(1, d["nsup"]), dtype=torch.float64, device=self.device)
+            _lib.check(_lib.lib().cito_csc_assemble_dev(
+                self.pat.n, d["sp_ptr"].data_ptr(), d["row"].data_ptr(), d["src"].data_ptr(), d["idx"].data_ptr(),
+                d["val"].data_ptr(), self.sigma_dev.data_ptr(), ptrs, d["counts"].data_ptr(), indptr.data_ptr(),
+                rows.data_ptr(), vals.data_ptr(), s), "csc_assemble")
+            rhs = d["rhs_const"].clone()
+            _lib.check(_lib.lib().cito_rhs_dev(
+                d["nlin"], d["r_row"].data_ptr(), d["r_form"].data_ptr(), d["r_vsrc"].data_ptr(),
+                d["r_voff"].data_ptr(), d["seg_src"].data_ptr(), d["seg_off"].data_ptr(), d["seg_len"].data_ptr(),
+                d["seg_cb"].data_ptr(), d["cols"].data_ptr(), z_ref_dev.data_ptr(), ptrs, rhs.data_ptr(), s), "rhs")
+            out[f"{M}_indptr"], out[f"{M}_indices"], out[f"{M}_data"] = indptr, rows, vals
+            out["b" if M == "A" else "h"] = rhs
+        return out
+
+    def to_program(self, dev_out, z_j):
+        """Host ConicProgram (scipy CSC, the reference's types when loaded) + meta."""
+        import scipy.sparse as sp
+
+        ConicProgram, ConeSpec = _conic_types()
+        pat = self.pat
+        mats = {}
+        for M in ("A", "G"):
+            indptr = dev_out[f"{M}_indptr"].cpu().numpy()
+            nnz = int(indptr[-1])
+            mats[M] = sp.csc_matrix((dev_out[f"{M}_data"][:nnz].cpu().numpy(), dev_out[f"{M}_indices"][:nnz].cpu().numpy(),
+                                     indptr), shape=(self._mats[M]["nrows"], pat.n))
+        dim = pat.lay.dim
+        P = sp.csc_matrix((pat.P_diag[:dim], np.arange(dim, dtype=np.int32),
+                           np.concatenate([np.arange(dim + 1), np.full(pat.n - dim, dim)]).astype(np.int32)),
+                          shape=(pat.n, pat.n))
+        prog = ConicProgram(P=P, c=pat.objective_c(z_j), A=mats["A"], b=dev_out["b"].cpu().numpy(), G=mats["G"],
+                            h=dev_out["h"].cpu().numpy(), cones=ConeSpec(nonneg=pat.n_orthant, soc=pat.soc_dims))
+        meta = _Meta(pat.z_idx, pat.sp_idx, pat.sm_idx, pat.t_idx)
+        return prog, meta
+
+
+def ctypes_ptr_array(ptrs):
+    import ctypes
+
+    arr = (ctypes.c_void_p * len(ptrs))(*ptrs)
+    return ctypes.cast(arr, ctypes.c_void_p)
+
+
+_assemblers = {}
+
+
+def build_subproblem(tr, lin, z_j, delta, config):
+    """Drop-in for cito.scp.build_subproblem (scp.py:160-351): values assembled on
+    the GPU from a host LinearizedProblem; returns (ConicProgram, meta)."""
+    import torch
+
+    from .scenario import build_scaling
+
+    key = (id(tr), float(config.w_prox), float(config.w_ep))
+    asm = _assemblers.get(key)
+    if asm is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+        scale_v = tr.scaling.scale if hasattr(tr, "scaling") else build_scaling(tr.scenario, tr.layout)[0]
+        pat = SubproblemPattern(tr.scenario, tr.layout, scale_v, config.w_prox, config.w_ep)
+        asm = SubproblemAssembler(pat, dev)
+        _assemblers[key] = asm
+    dev = asm.device
+    lin_dev = {k: torch.as_tensor(np.ascontiguousarray(getattr(lin, k), dtype=np.float64), device=dev)
+               for k in LIN_SOURCES}
+    z_ref = torch.as_tensor(np.ascontiguousarray(lin.z_ref, dtype=np.float64), device=dev)
+    out = asm.assemble_device(lin_dev, z_ref)
+    return asm.to_program(out, z_j)
