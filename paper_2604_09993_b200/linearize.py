@@ -191,9 +191,13 @@ class GpuTranscription:
         if host["bad"].any():
             raise FloatingPointError(f"non-finite state in intervals {np.where(host['bad'] != 0)[0].tolist()}")
         LP = _lp_type()
-        return LP(z_ref=z.copy(), ends=host["ends"], jx=host["jx"], ju=host["ju"], js=host["js"],
-                  defects=host["defects"], psi=host["psi"], psi_jac=host["psi_jac"], theta=host["theta"],
-                  theta_jac=host["theta_jac"], imp_v=host["imp_v"], imp_jac=host["imp_jac"])
+        lin = LP(z_ref=z.copy(), ends=host["ends"], jx=host["jx"], ju=host["ju"], js=host["js"],
+                 defects=host["defects"], psi=host["psi"], psi_jac=host["psi_jac"], theta=host["theta"],
+                 theta_jac=host["theta_jac"], imp_v=host["imp_v"], imp_jac=host["imp_jac"])
+        # keep the device copy so build_subproblem (subproblem.py) can assemble from it
+        # without another host->device round trip
+        self.last = (lin, r, z_dev)
+        return lin
 
 
 def initial_guess(scenario, disc, lay=None, seed=None):
@@ -250,11 +254,16 @@ def initial_guess(scenario, disc, lay=None, seed=None):
 _cache = {}
 
 
-def linearize_all(tr, z, delta, epsilon=None, jobs=1):
-    """Module-level drop-in for cito.scp.linearize_all: caches one GpuTranscription per tr."""
+def transcription_for(tr):
+    """The cached GpuTranscription of a reference Transcription (one per tr)."""
     key = id(tr)
     g = _cache.get(key)
     if g is None or g[0] is not tr:
         g = (tr, GpuTranscription(tr))
         _cache[key] = g
-    return g[1].linearize_all(z, delta, epsilon, jobs)
+    return g[1]
+
+
+def linearize_all(tr, z, delta, epsilon=None, jobs=1):
+    """Module-level drop-in for cito.scp.linearize_all: caches one GpuTranscription per tr."""
+    return transcription_for(tr).linearize_all(z, delta, epsilon, jobs)

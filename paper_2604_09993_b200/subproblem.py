@@ -453,8 +453,15 @@ def build_subproblem(tr, lin, z_j, delta, config):
         asm = SubproblemAssembler(pat, dev)
         _assemblers[key] = asm
     dev = asm.device
-    lin_dev = {k: torch.as_tensor(np.ascontiguousarray(getattr(lin, k), dtype=np.float64), device=dev)
-               for k in LIN_SOURCES}
-    z_ref = torch.as_tensor(np.ascontiguousarray(lin.z_ref, dtype=np.float64), device=dev)
+    from .linearize import _cache
+
+    cached = _cache.get(id(tr))
+    last = getattr(cached[1], "last", None) if cached and cached[0] is tr else None
+    if last is not None and last[0] is lin:  # produced by our linearize_all: already on the device
+        lin_dev, z_ref = last[1], last[2]
+    else:
+        lin_dev = {k: torch.as_tensor(np.ascontiguousarray(getattr(lin, k), dtype=np.float64), device=dev)
+                   for k in LIN_SOURCES}
+        z_ref = torch.as_tensor(np.ascontiguousarray(lin.z_ref, dtype=np.float64), device=dev)
     out = asm.assemble_device(lin_dev, z_ref)
     return asm.to_program(out, z_j)

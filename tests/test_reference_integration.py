@@ -37,6 +37,7 @@ cito = ref_runner.import_cito()
 from dataclasses import replace
 from cito import ocp, scp
 import paper_2604_09993_b200.linearize as G
+import paper_2604_09993_b200.subproblem as SPB
 from paper_2604_09993_b200 import install
 
 name, iters, compare = sys.argv[1], int(sys.argv[2]), sys.argv[3] == "1"
@@ -51,12 +52,13 @@ if compare:
 ocp._transcriptions.clear()
 tr = ocp.get_transcription(sc)
 install(tr)                       # tr.discretizer -> GPU (initial_guess uses it)
-orig = scp.linearize_all
-scp.linearize_all = G.linearize_all   # GPU linearize_all (intervals + node relations)
+orig = scp.linearize_all, scp.build_subproblem
+scp.linearize_all = G.linearize_all         # GPU linearize_all (intervals + node relations)
+scp.build_subproblem = SPB.build_subproblem  # GPU subproblem assembly (CSC values, b, h)
 try:
     z, hist, st = scp.solve(sc, cfg)
 finally:
-    scp.linearize_all = orig
+    scp.linearize_all, scp.build_subproblem = orig
 out["gpu"] = [h.z.tolist() for h in hist]
 out["gpu_delta"] = [h.delta for h in hist]
 out["status"] = st
