@@ -53,6 +53,7 @@ def parse():
     p.add_argument("--problems", type=int, default=128, help="multistart: problems per GPU (configs[3]: 1024 / 8)")
     p.add_argument("--batch", type=int, default=4096)
     p.add_argument("--cpu-seconds", type=float, default=10.0)
+    p.add_argument("--sample-seconds", type=float, default=None, help="reference arm: time-bounded sample")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-batch-extra", action="store_true")
     return p.parse_args()
@@ -71,8 +72,29 @@ def scp_problem(seed):
     return sc
 
 
+def _reference_scp():
+    """The reference's own Python (cito.scp/ocp/conic, installed in baseline/_ref) via the
+    jax shim, for the host-side subproblem assembly; None when not installed."""
+    src = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(src, "cito")):
+        return None
+    os.environ["CITO_REF_SRC"] = src
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    try:
+        import ref_runner
+
+        ref_runner.import_cito()
+        from cito import ocp, scp
+
+        return ocp, scp
+    except Exception:
+        return None
+
+
 def cpu_step_fn(sc, seed):
-    """One reference-algorithm SCP linearization on the host (oracle port)."""
+    """One SCP iteration's pre-IPM work on the host: the reference's linearization
+    algorithm via the oracle port (intervals + node relations) and, when the
+    reference is installed, its own build_subproblem + canonicalize."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle
 
@@ -88,13 +110,31 @@ def cpu_step_fn(sc, seed):
     Us = np.stack([z[lay.u(k)] for k in range(lay.N - 1)])
     Ss = np.array([z[lay.s(k)][0] for k in range(lay.N - 1)])
     yp, tv = node_inputs(lay, z)
+    ref = _reference_scp()
+    tr = None
+    if ref is not None:
+        from dataclasses import replace
+
+        ocp, scp = ref
+        rsc = ocp.load_scenario(os.path.join(ROOT, "tests", "golden", "assets", "halfcheetah_bound.json"))
+        tr = ocp.Transcription(replace(rsc, N=sc.N, s_bounds=None))
+    step_fn.with_assembly = tr is not None
 
     def step():
-        pyoracle.linearize(desc, sc.substeps, starts, Us, Ss)
-        pyoracle.node_linearize(desc, yp, tv, 1.0, sc.ctcs_epsilon)
+        e, jx, ju, js, _ = pyoracle.linearize(desc, sc.substeps, starts, Us, Ss)
+        psi, pj, th, tj, imp, ij = pyoracle.node_linearize(desc, yp, tv, 1.0, sc.ctcs_epsilon)
+        if tr is not None:
+            defects = np.stack([z[lay.xm(k + 1)] for k in range(lay.N - 1)]) - e
+            lin = scp.LinearizedProblem(z_ref=z, ends=e, jx=jx, ju=ju, js=js, defects=defects, psi=psi, psi_jac=pj,
+                                        theta=th, theta_jac=tj, imp_v=imp, imp_jac=ij)
+            scp.build_subproblem(tr, lin, z, 1.0, scp.SCPConfig())
         return lay.N - 1
 
     return step, pyoracle
+
+
+def step_fn():
+    pass
 
 
 def cpu_batch_fn(sc, B):
@@ -207,8 +247,8 @@ def run_ours(args):
     torch.cuda.set_device(dev)
     from paper_2604_09993_b200 import synth
     from paper_2604_09993_b200.linearize import GpuTranscription, initial_guess
-    from paper_2604_09993_b200.scatter import DynamicsScatter, n_cols
     from paper_2604_09993_b200.scenario import build_scaling
+    from paper_2604_09993_b200.subproblem import SubproblemAssembler, SubproblemPattern, build_subproblem
 
     sc = scp_problem(seed=rank)
     gt = GpuTranscription(sc, device=dev.index)
@@ -221,12 +261,7 @@ def run_ours(args):
     z_dev = torch.as_tensor(z, device=dev)
     delta = 1.0
     scale_v, state_scale, u_scale = build_scaling(sc, lay)
-    scat = DynamicsScatter(gt.disc, lay, state_scale, u_scale, sc.s_nominal, dev)
-    r0 = gt.linearize_device(z_dev, delta)
-    pat = scat.build_pattern(r0["jx"].cpu().numpy(), r0["ju"].cpu().numpy(), r0["js"].cpu().numpy(),
-                             n_cols(lay, 3 * lay.n_c + lay.n_g_out), state_scale)
-    A_data = torch.as_tensor(pat.template_data(), device=dev)
-    b_dyn = torch.empty(pat.n_rows, dtype=torch.float64, device=dev)
+    asm = SubproblemAssembler(SubproblemPattern(sc, lay, scale_v), dev)
     n_int = lay.N - 1
 
     k1_ev = []
@@ -238,7 +273,7 @@ def run_ours(args):
             k1_ev.append((e0, e1))
         else:
             r = gt.linearize_device(zd, delta)
-        scat.scatter(r["ends"], r["jx"], r["ju"], r["js"], zd, A_data, b_dyn)
+        asm.assemble_device(r, zd)  # whole subproblem: CSC of A, G (+ zero compaction), b, h
         return r
 
     # --- batch workload state
@@ -337,29 +372,29 @@ def run_ours(args):
 
     # --- e2e through the public API with host (pinned) buffers
     if args.workload == "scp":
-        z_pin = torch.as_tensor(z).pin_memory()
-        outs = None
+        # the two reference-facing calls cito.scp.solve makes per iteration (scp.py:412-413),
+        # host numpy in / host scipy out: linearize_all (LinearizedProblem) + build_subproblem
+        from types import SimpleNamespace
+
+        cfg = SimpleNamespace(w_prox=2000.0, w_ep=50000.0)
+        e2e_bytes = {}
+        trs = _TrShim(gt)
 
         def e2e_step():
-            nonlocal outs
-            zd = z_pin.to(dev, non_blocking=True)
-            r = gt.linearize_device(zd, delta)
-            scat.scatter(r["ends"], r["jx"], r["ju"], r["js"], zd, A_data, b_dyn)
-            res = dict(r)
-            res["A_data"] = A_data
-            res["b"] = b_dyn
-            keys = ["ends", "jx", "ju", "js", "defects", "psi", "psi_jac", "theta", "theta_jac", "imp_v", "imp_jac",
-                    "A_data", "b", "bad"]
-            if outs is None:
-                outs = {k: torch.empty(res[k].shape, dtype=res[k].dtype, pin_memory=True) for k in keys}
-            for k in keys:
-                outs[k].copy_(res[k], non_blocking=True)
-            torch.cuda.current_stream(dev).synchronize()
-            return outs
+            lin = gt.linearize_all(z, delta)
+            prog, meta = build_subproblem(trs, lin, z, delta, cfg)
+            if not e2e_bytes:
+                e2e_bytes["d2h"] = int(sum(getattr(lin, f).nbytes for f in ("ends", "jx", "ju", "js", "defects", "psi",
+                                                                              "psi_jac", "theta", "theta_jac", "imp_v",
+                                                                              "imp_jac"))
+                                       + prog.A.data.nbytes + prog.A.indices.nbytes + prog.A.indptr.nbytes
+                                       + prog.G.data.nbytes + prog.G.indices.nbytes + prog.G.indptr.nbytes
+                                       + prog.b.nbytes + prog.h.nbytes)
+            return prog
 
         e2e_step()
         h2d = z.nbytes
-        d2h = int(sum(v.numel() * v.element_size() for v in outs.values()))
+        d2h = e2e_bytes["d2h"]
     elif args.workload == "multistart":
         Z_pin = torch.as_tensor(Z).pin_memory()
         ms_host = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in ms_out.items()}
@@ -415,16 +450,13 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        if args.workload == "scp":
-            step, po = cpu_step_fn(sc, 0)
-            sample = "HalfCheetah N=30 initial-guess SCP linearization (29 intervals + node relations), repeated"
-        else:
-            step, po = cpu_batch_fn(sc, 64)
-            sample = "64 synthetic HalfCheetah intervals per call, repeated"
-        v, n, dt = time_cpu(step, args.cpu_seconds)
-        cpu = {"value": v, "unit": UNIT, "cores": po.get_threads(), "kind": "port",
-               "sample": f"{sample}: {n} calls in {dt:.1f} s on {os.cpu_count()} host cores (oracle/cito_oracle.c, "
-                         "dense forward-mode dual numbers like the reference's jax.jacfwd)"}
+        # the reference arm itself, in a subprocess (isolates the jax shim), time-bounded sample
+        p = subprocess.run([sys.executable, os.path.abspath(__file__), "--impl", "reference", "--workload", args.workload,
+                            "--sample-seconds", str(args.cpu_seconds), "--warmup", "1", "--problems",
+                            str(args.problems), "--batch", str(args.batch)], capture_output=True, text=True,
+                           cwd=ROOT, env={k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE")})
+        lines = [l for l in p.stdout.splitlines() if l.startswith("{")]
+        cpu = json.loads(lines[-1])["cpu_baseline"] if lines else {"error": p.stderr[-400:]}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
@@ -456,9 +488,11 @@ def run_reference(args):
     if rank != 0:
         return
     sc = scp_problem(seed=0)
-    if args.workload == "scp":
+    if args.workload in ("scp", "multistart"):
         step, po = cpu_step_fn(sc, 0)
-        sample = "HalfCheetah N=30 initial-guess SCP linearization (29 intervals + node relations) per step"
+        sample = ("HalfCheetah N=30 initial-guess SCP iteration per step: oracle-port linearization (29 intervals "
+                  "+ node relations)" + (" + the reference's own build_subproblem/canonicalize (baseline/_ref)"
+                                         if step_fn.with_assembly else " (reference not installed: no assembly)"))
     else:
         B = max(8, min(args.batch, 256))
         step, po = cpu_batch_fn(sc, B)
@@ -466,13 +500,15 @@ def run_reference(args):
     for _ in range(max(1, args.warmup)):
         step()
     t0 = time.perf_counter()
-    units = 0
-    for _ in range(args.steps):
+    units, n = 0, 0
+    while (n < args.steps) if args.sample_seconds is None else (n < 1 or time.perf_counter() - t0 < args.sample_seconds):
         units += step()
+        n += 1
     dt = time.perf_counter() - t0
     v = units / dt
-    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+    sample += f"; {n} steps in {dt:.1f} s on {os.cpu_count()} host cores"
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": n, "warmup": args.warmup,
+            "ms_per_step": dt / n * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic", "impl": "reference",
             "config": {"workload": args.workload, "note": "reference algorithm on host cores via the C oracle port; "
                        "the reference's JAX runtime is not installable (no jax wheel, no network)"},
@@ -491,3 +527,15 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+class _TrShim:
+    """Minimal Transcription-like view of a GpuTranscription for build_subproblem."""
+
+    def __init__(self, gt):
+        from paper_2604_09993_b200.linearize import _cache
+        from paper_2604_09993_b200.scenario import build_scaling
+
+        self.scenario, self.layout = gt.scenario, gt.lay
+        self.scaling = type("S", (), {"scale": build_scaling(gt.scenario, gt.lay)[0]})()
+        _cache[id(self)] = (self, gt)
