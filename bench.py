@@ -517,6 +517,18 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+class _TrShim:
+    """Minimal Transcription-like view of a GpuTranscription for build_subproblem."""
+
+    def __init__(self, gt):
+        from paper_2604_09993_b200.linearize import _cache
+        from paper_2604_09993_b200.scenario import build_scaling
+
+        self.scenario, self.layout = gt.scenario, gt.lay
+        self.scaling = type("S", (), {"scale": build_scaling(gt.scenario, gt.lay)[0]})()
+        _cache[id(self)] = (self, gt)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -528,14 +540,3 @@ def main():
 if __name__ == "__main__":
     main()
 
-
-class _TrShim:
-    """Minimal Transcription-like view of a GpuTranscription for build_subproblem."""
-
-    def __init__(self, gt):
-        from paper_2604_09993_b200.linearize import _cache
-        from paper_2604_09993_b200.scenario import build_scaling
-
-        self.scenario, self.layout = gt.scenario, gt.lay
-        self.scaling = type("S", (), {"scale": build_scaling(gt.scenario, gt.lay)[0]})()
-        _cache[id(self)] = (self, gt)
