@@ -203,8 +203,8 @@ cito_status cito_rhs_dev(int64_t nrows, const int32_t* rows, const int8_t* form,
  * (time it with events on the same stream), or -1 on launch failure. */
 double cito_dfma_peak(int32_t iters, double* out_dev, void* stream);
 
-/* Number of kernel launches issued by this handle since creation (evidence
- * for bench.py's gpu_launches). */
+/* Number of kernel launches issued by this handle since creation, or by the
+ * whole library when h is NULL (evidence for bench.py's gpu_launches). */
 int64_t cito_launch_count(const cito_handle* h);
 
 #ifdef __cplusplus

@@ -51,6 +51,41 @@ class LinearizedProblem:
     imp_jac: np.ndarray
 
 
+class LazyLinearizedProblem:
+    """LinearizedProblem (scp.py:69-84) whose arrays stay on the device until a
+    field is read: the SCP loop hands it straight to build_subproblem (which
+    assembles on the device), so the host never pays for the 2 MB of Jacobians
+    unless it asks for them.  First access copies every field into fresh numpy
+    arrays with one synchronization."""
+
+    FIELDS = ("ends", "jx", "ju", "js", "defects", "psi", "psi_jac", "theta", "theta_jac", "imp_v", "imp_jac")
+
+    def __init__(self, dev, z_ref):
+        self._dev = dev
+        self.z_ref = z_ref
+        self._host = None
+
+    def materialize(self):
+        if self._host is None:
+            import torch
+
+            pinned = {k: torch.empty(self._dev[k].shape, dtype=self._dev[k].dtype, pin_memory=True)
+                      for k in self.FIELDS}
+            for k in self.FIELDS:
+                pinned[k].copy_(self._dev[k], non_blocking=True)
+            torch.cuda.current_stream(self._dev["jx"].device).synchronize()
+            self._host = {k: v.numpy().copy() for k, v in pinned.items()}
+        return self._host
+
+    def __getattr__(self, name):
+        if name in LazyLinearizedProblem.FIELDS:
+            return self.materialize()[name]
+        raise AttributeError(name)
+
+    def device_arrays(self):
+        return self._dev
+
+
 def _lp_type():
     mod = sys.modules.get("cito.scp")
     if mod is not None and hasattr(mod, "LinearizedProblem"):
@@ -187,13 +222,10 @@ class GpuTranscription:
             raise FloatingPointError("non-finite reference point")
         z_dev = torch.as_tensor(np.ascontiguousarray(z), device=self.device)
         r = self.linearize_device(z_dev, delta, epsilon)
-        host = {k: v.cpu().numpy() for k, v in r.items()}
-        if host["bad"].any():
-            raise FloatingPointError(f"non-finite state in intervals {np.where(host['bad'] != 0)[0].tolist()}")
-        LP = _lp_type()
-        lin = LP(z_ref=z.copy(), ends=host["ends"], jx=host["jx"], ju=host["ju"], js=host["js"],
-                 defects=host["defects"], psi=host["psi"], psi_jac=host["psi_jac"], theta=host["theta"],
-                 theta_jac=host["theta_jac"], imp_v=host["imp_v"], imp_jac=host["imp_jac"])
+        bad = r["bad"].cpu().numpy()  # the reference's end-state check (augmentation.py:231-233)
+        if bad.any():
+            raise FloatingPointError(f"non-finite state in intervals {np.where(bad != 0)[0].tolist()}")
+        lin = LazyLinearizedProblem(r, z.copy())
         # keep the device copy so build_subproblem (subproblem.py) can assemble from it
         # without another host->device round trip
         self.last = (lin, r, z_dev)

@@ -406,23 +406,32 @@ class SubproblemAssembler:
         return out
 
     def to_program(self, dev_out, z_j):
-        """Host ConicProgram (scipy CSC, the reference's types when loaded) + meta."""
+        """Host ConicProgram (scipy CSC, the reference's types when loaded) + meta.
+        One batched device->host copy into pinned staging, one synchronization."""
         import scipy.sparse as sp
+        import torch
 
         ConicProgram, ConeSpec = _conic_types()
         pat = self.pat
+        keys = ["A_indptr", "A_indices", "A_data", "b", "G_indptr", "G_indices", "G_data", "h"]
+        if getattr(self, "_pinned", None) is None:
+            self._pinned = {k: torch.empty(dev_out[k].shape, dtype=dev_out[k].dtype, pin_memory=True) for k in keys}
+        for k in keys:
+            self._pinned[k].copy_(dev_out[k], non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
+        host = {k: self._pinned[k].numpy() for k in keys}
         mats = {}
         for M in ("A", "G"):
-            indptr = dev_out[f"{M}_indptr"].cpu().numpy()
+            indptr = host[f"{M}_indptr"].copy()
             nnz = int(indptr[-1])
-            mats[M] = sp.csc_matrix((dev_out[f"{M}_data"][:nnz].cpu().numpy(), dev_out[f"{M}_indices"][:nnz].cpu().numpy(),
-                                     indptr), shape=(self._mats[M]["nrows"], pat.n))
+            mats[M] = sp.csc_matrix((host[f"{M}_data"][:nnz].copy(), host[f"{M}_indices"][:nnz].copy(), indptr),
+                                    shape=(self._mats[M]["nrows"], pat.n))
         dim = pat.lay.dim
         P = sp.csc_matrix((pat.P_diag[:dim], np.arange(dim, dtype=np.int32),
                            np.concatenate([np.arange(dim + 1), np.full(pat.n - dim, dim)]).astype(np.int32)),
                           shape=(pat.n, pat.n))
-        prog = ConicProgram(P=P, c=pat.objective_c(z_j), A=mats["A"], b=dev_out["b"].cpu().numpy(), G=mats["G"],
-                            h=dev_out["h"].cpu().numpy(), cones=ConeSpec(nonneg=pat.n_orthant, soc=pat.soc_dims))
+        prog = ConicProgram(P=P, c=pat.objective_c(z_j), A=mats["A"], b=host["b"].copy(), G=mats["G"],
+                            h=host["h"].copy(), cones=ConeSpec(nonneg=pat.n_orthant, soc=pat.soc_dims))
         meta = _Meta(pat.z_idx, pat.sp_idx, pat.sm_idx, pat.t_idx)
         return prog, meta
 
@@ -457,7 +466,10 @@ def build_subproblem(tr, lin, z_j, delta, config):
 
     cached = _cache.get(id(tr))
     last = getattr(cached[1], "last", None) if cached and cached[0] is tr else None
-    if last is not None and last[0] is lin:  # produced by our linearize_all: already on the device
+    if hasattr(lin, "device_arrays"):  # produced by our linearize_all: already on the device
+        lin_dev = lin.device_arrays()
+        z_ref = torch.as_tensor(np.ascontiguousarray(lin.z_ref, dtype=np.float64), device=dev)
+    elif last is not None and last[0] is lin:
         lin_dev, z_ref = last[1], last[2]
     else:
         lin_dev = {k: torch.as_tensor(np.ascontiguousarray(getattr(lin, k), dtype=np.float64), device=dev)
