@@ -325,14 +325,33 @@ class _Meta:
         return float(np.sum(sol.x[self.sp_idx]) + np.sum(sol.x[self.sm_idx]) + np.sum(sol.x[self.t_idx]))
 
 
+@dataclass(frozen=True)
+class ConeSpec:
+    """Same fields as cito.conic.ConeSpec (conic.py:37-51)."""
+
+    nonneg: int = 0
+    soc: tuple = ()
+
+
+@dataclass
+class ConicProgram:
+    """Same fields as cito.conic.ConicProgram (conic.py:54-84)."""
+
+    P: object
+    c: np.ndarray
+    A: object
+    b: np.ndarray
+    G: object
+    h: np.ndarray
+    cones: ConeSpec
+
+
 def _conic_types():
+    """The reference's own program types when cito.conic is loaded (so its IPM and
+    validate() accept the result), else the local mirrors."""
     mod = sys.modules.get("cito.conic")
     if mod is not None and hasattr(mod, "ConicProgram"):
         return mod.ConicProgram, mod.ConeSpec
-    from dataclasses import make_dataclass
-
-    ConeSpec = make_dataclass("ConeSpec", [("nonneg", int, 0), ("soc", tuple, ())], frozen=True)
-    ConicProgram = make_dataclass("ConicProgram", ["P", "c", "A", "b", "G", "h", "cones"])
     return ConicProgram, ConeSpec
 
 
