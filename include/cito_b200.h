@@ -191,6 +191,15 @@ cito_status cito_csc_assemble_dev(int32_t ncols, const int64_t* sp_ptr, const in
                                   const double* const* lin, int32_t* counts, int32_t* out_ptr, int32_t* out_rows,
                                   double* out_vals, void* stream);
 
+/* Same as cito_csc_assemble_dev for nmat (1 or 2, e.g. A and G) matrices with
+ * the same column count in one set of launches; every pointer argument except
+ * sigma and lin is a HOST array of nmat device pointers. */
+cito_status cito_csc_assemble2_dev(int32_t nmat, int32_t ncols, const int64_t* const* sp_ptr,
+                                   const int32_t* const* sp_row, const int8_t* const* sp_src,
+                                   const int64_t* const* sp_idx, const double* const* sp_val, const double* sigma,
+                                   const double* const* lin, int32_t* const* counts, int32_t* const* out_ptr,
+                                   int32_t* const* out_rows, double* const* out_vals, void* stream);
+
 /* b / h of the linearized rows: out[rows[i]] = form ? J.z[cols] - v : v - J.z[cols]
  * with J split in up to 3 segments (seg_src < 0 = unused), v = lin[vsrc[i]][voff[i]]. */
 cito_status cito_rhs_dev(int64_t nrows, const int32_t* rows, const int8_t* form, const int8_t* vsrc,

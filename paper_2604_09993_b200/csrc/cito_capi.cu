@@ -473,25 +473,49 @@ cito_status cito_scatter_dynamics_dev(cito_handle* h, int64_t n_int, const doubl
   return CITO_OK;
 }
 
-cito_status cito_csc_assemble_dev(int32_t ncols, const int64_t* sp_ptr, const int32_t* sp_row, const int8_t* sp_src,
-                                  const int64_t* sp_idx, const double* sp_val, const double* sigma,
-                                  const double* const* lin, int32_t* counts, int32_t* out_ptr, int32_t* out_rows,
-                                  double* out_vals, void* stream) {
-  if (ncols <= 0) return CITO_OK;
+cito_status cito_csc_assemble2_dev(int32_t nmat, int32_t ncols, const int64_t* const* sp_ptr,
+                                   const int32_t* const* sp_row, const int8_t* const* sp_src,
+                                   const int64_t* const* sp_idx, const double* const* sp_val, const double* sigma,
+                                   const double* const* lin, int32_t* const* counts, int32_t* const* out_ptr,
+                                   int32_t* const* out_rows, double* const* out_vals, void* stream) {
+  if (ncols <= 0 || nmat < 1 || nmat > 2) return nmat == 0 ? CITO_OK : fail(CITO_ERR_ARG, "nmat must be 1 or 2");
   LinTable L;
   for (int k = 0; k < 10; ++k) L.p[k] = lin ? lin[k] : nullptr;
   cudaStream_t s = (cudaStream_t)stream;
   const int wpb = 8;
-  const unsigned grid = (unsigned)((ncols + wpb - 1) / wpb);
+  const unsigned gx = (unsigned)((ncols + wpb - 1) / wpb);
+  CscArgs ca;
+  ScanArgs sa;
+  for (int m = 0; m < nmat; ++m) {
+    ca.sp_ptr[m] = sp_ptr[m];
+    ca.row[m] = sp_row[m];
+    ca.src[m] = sp_src[m];
+    ca.idx[m] = sp_idx[m];
+    ca.val[m] = sp_val[m];
+    ca.counts[m] = counts[m];
+    ca.out_ptr[m] = out_ptr[m];
+    ca.out_rows[m] = out_rows[m];
+    ca.out_vals[m] = out_vals[m];
+    sa.n[m] = ncols;
+    sa.counts[m] = counts[m];
+    sa.out_ptr[m] = out_ptr[m];
+  }
   count_launch(3);
-  k_csc_count<<<grid, 32 * wpb, 0, s>>>(ncols, sp_ptr, sp_src, sp_idx, sp_val, sigma, L, counts);
+  k_csc_count<<<dim3(gx, nmat), 32 * wpb, 0, s>>>(ncols, ca, sigma, L);
   CUDA_TRY(cudaGetLastError());
-  k_scan<<<1, 1024, 0, s>>>(ncols, counts, out_ptr);
+  k_scan<<<nmat, 1024, 0, s>>>(sa);
   CUDA_TRY(cudaGetLastError());
-  k_csc_write<<<grid, 32 * wpb, 0, s>>>(ncols, sp_ptr, sp_row, sp_src, sp_idx, sp_val, sigma, L, out_ptr, out_rows,
-                                       out_vals);
+  k_csc_write<<<dim3(gx, nmat), 32 * wpb, 0, s>>>(ncols, ca, sigma, L);
   CUDA_TRY(cudaGetLastError());
   return CITO_OK;
+}
+
+cito_status cito_csc_assemble_dev(int32_t ncols, const int64_t* sp_ptr, const int32_t* sp_row, const int8_t* sp_src,
+                                  const int64_t* sp_idx, const double* sp_val, const double* sigma,
+                                  const double* const* lin, int32_t* counts, int32_t* out_ptr, int32_t* out_rows,
+                                  double* out_vals, void* stream) {
+  return cito_csc_assemble2_dev(1, ncols, &sp_ptr, &sp_row, &sp_src, &sp_idx, &sp_val, sigma, lin, &counts, &out_ptr,
+                                &out_rows, &out_vals, stream);
 }
 
 cito_status cito_rhs_dev(int64_t nrows, const int32_t* rows, const int8_t* form, const int8_t* vsrc,

@@ -26,70 +26,103 @@ __device__ __forceinline__ double sp_value(int64_t e, double sig, const int8_t* 
   return s < 0 ? val[e] : (val[e] * L.p[s][idx[e]]) * sig;
 }
 
-__global__ void __launch_bounds__(256) k_csc_count(int32_t ncols, const int64_t* __restrict__ sp_ptr,
-                                                   const int8_t* __restrict__ src, const int64_t* __restrict__ idx,
-                                                   const double* __restrict__ val, const double* __restrict__ sigma,
-                                                   const LinTable L, int32_t* __restrict__ counts) {
+// up to two matrices (A, G) per launch: blockIdx.y selects the matrix
+struct CscArgs {
+  const int64_t* sp_ptr[2];
+  const int32_t* row[2];
+  const int8_t* src[2];
+  const int64_t* idx[2];
+  const double* val[2];
+  int32_t* counts[2];
+  int32_t* out_ptr[2];
+  int32_t* out_rows[2];
+  double* out_vals[2];
+};
+
+__global__ void __launch_bounds__(256) k_csc_count(int32_t ncols, const CscArgs a, const double* __restrict__ sigma,
+                                                   const LinTable L) {
+  const int m = blockIdx.y;
   const int lane = threadIdx.x & 31;
   const int64_t c = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (c >= ncols) return;
+  const int64_t* __restrict__ sp_ptr = a.sp_ptr[m];
   const double sig = sigma[c];
   int n = 0;
-  for (int64_t e = sp_ptr[c] + lane; e < sp_ptr[c + 1]; e += 32) n += sp_value(e, sig, src, idx, val, L) != 0.0;
+  for (int64_t e = sp_ptr[c] + lane; e < sp_ptr[c + 1]; e += 32)
+    n += sp_value(e, sig, a.src[m], a.idx[m], a.val[m], L) != 0.0;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
-  if (lane == 0) counts[c] = n;
+  if (lane == 0) a.counts[m][c] = n;
 }
 
-__global__ void __launch_bounds__(1024) k_scan(int32_t n, const int32_t* __restrict__ counts,
-                                               int32_t* __restrict__ out_ptr) {
-  __shared__ int32_t part[1024];
-  __shared__ int32_t carry;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  for (int32_t base = 0; base < n; base += 1024) {
-    const int32_t i = base + threadIdx.x;
-    int32_t v = i < n ? counts[i] : 0;
-    part[threadIdx.x] = v;
-    __syncthreads();
-    for (int off = 1; off < 1024; off <<= 1) {  // Hillis-Steele inclusive scan
-      const int32_t t = threadIdx.x >= off ? part[threadIdx.x - off] : 0;
-      __syncthreads();
-      part[threadIdx.x] += t;
-      __syncthreads();
-    }
-    if (i < n) out_ptr[i] = carry + part[threadIdx.x] - v;
-    __syncthreads();
-    if (threadIdx.x == 1023) carry += part[1023];
-    __syncthreads();
+// Exclusive scan of the per-column counts -> indptr (int32), one CTA per matrix
+// (blockIdx.x selects the matrix).  Each thread scans a contiguous run in
+// registers, warps combine with shuffles, one pass over the data.
+struct ScanArgs {
+  int32_t n[2];
+  const int32_t* counts[2];
+  int32_t* out_ptr[2];
+};
+
+__global__ void __launch_bounds__(1024) k_scan(const ScanArgs a) {
+  const int m = blockIdx.x;
+  const int32_t n = a.n[m];
+  const int32_t* __restrict__ counts = a.counts[m];
+  int32_t* __restrict__ out_ptr = a.out_ptr[m];
+  __shared__ int32_t warp_tot[32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int32_t per = (n + 1023) / 1024;
+  const int32_t lo = min(n, tid * per), hi = min(n, lo + per);
+  int32_t local = 0;
+  for (int32_t i = lo; i < hi; ++i) local += counts[i];
+  int32_t incl = local;  // inclusive warp scan of the per-thread totals
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
   }
-  if (threadIdx.x == 0) out_ptr[n] = carry;
+  if (lane == 31) warp_tot[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    int32_t w = warp_tot[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t t = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += t;
+    }
+    warp_tot[lane] = w;  // inclusive over warps
+  }
+  __syncthreads();
+  int32_t run = (wid > 0 ? warp_tot[wid - 1] : 0) + incl - local;  // exclusive prefix of this thread's run
+  for (int32_t i = lo; i < hi; ++i) {
+    out_ptr[i] = run;
+    run += counts[i];
+  }
+  if (tid == 1023) out_ptr[n] = warp_tot[31];
 }
 
-__global__ void __launch_bounds__(256) k_csc_write(int32_t ncols, const int64_t* __restrict__ sp_ptr,
-                                                   const int32_t* __restrict__ row, const int8_t* __restrict__ src,
-                                                   const int64_t* __restrict__ idx, const double* __restrict__ val,
-                                                   const double* __restrict__ sigma, const LinTable L,
-                                                   const int32_t* __restrict__ out_ptr, int32_t* __restrict__ out_rows,
-                                                   double* __restrict__ out_vals) {
+__global__ void __launch_bounds__(256) k_csc_write(int32_t ncols, const CscArgs a, const double* __restrict__ sigma,
+                                                   const LinTable L) {
+  const int m = blockIdx.y;
   const int lane = threadIdx.x & 31;
   const int64_t c = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (c >= ncols) return;
+  const int64_t* __restrict__ sp_ptr = a.sp_ptr[m];
   const double sig = sigma[c];
-  int32_t base = out_ptr[c];
+  int32_t base = a.out_ptr[m][c];
   const unsigned lt = (1u << lane) - 1u;
   for (int64_t e0 = sp_ptr[c]; e0 < sp_ptr[c + 1]; e0 += 32) {
     const int64_t e = e0 + lane;
     const bool in = e < sp_ptr[c + 1];
-    const double v = in ? sp_value(e, sig, src, idx, val, L) : 0.0;
+    const double v = in ? sp_value(e, sig, a.src[m], a.idx[m], a.val[m], L) : 0.0;
     const bool nz = in && v != 0.0;
-    const unsigned m = __ballot_sync(0xffffffffu, nz);
+    const unsigned msk = __ballot_sync(0xffffffffu, nz);
     if (nz) {
-      const int32_t pos = base + __popc(m & lt);
-      out_rows[pos] = row[e];
-      out_vals[pos] = v;
+      const int32_t pos = base + __popc(msk & lt);
+      a.out_rows[m][pos] = a.row[m][e];
+      a.out_vals[m][pos] = v;
     }
-    base += __popc(m);
+    base += __popc(msk);
   }
 }
 

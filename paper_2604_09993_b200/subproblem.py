@@ -398,30 +398,53 @@ class SubproblemAssembler:
                      cols=t(np.concatenate(cols) if cols else np.zeros(1), np.int64))
             self._mats[M] = d
 
+    def _prepare_batched(self):
+        """Concatenate the rhs descriptors of A and G (one launch) and allocate
+        the per-iteration outputs once."""
+        import torch
+
+        dA, dG = self._mats["A"], self._mats["G"]
+        nA = dA["nrows"]
+        cat = lambda k: torch.cat([dA[k], dG[k]])  # noqa: E731
+        self._rhs = dict(rows=torch.cat([dA["r_row"], dG["r_row"] + nA]), form=cat("r_form"), vsrc=cat("r_vsrc"),
+                         voff=cat("r_voff"), seg_src=cat("seg_src"), seg_off=cat("seg_off"), seg_len=cat("seg_len"),
+                         seg_cb=torch.cat([dA["seg_cb"], dG["seg_cb"] + dA["cols"].numel()]),
+                         cols=torch.cat([dA["cols"], dG["cols"]]), const=torch.cat([dA["rhs_const"], dG["rhs_const"]]),
+                         n=dA["nlin"] + dG["nlin"], nA=nA)
+
     def assemble_device(self, lin, z_ref_dev, stream=None):
         """lin: dict of device tensors with the LIN_SOURCES fields.  Returns device
         tensors {A_indptr, A_indices, A_data, b, G_indptr, G_indices, G_data, h}
-        (data/indices sized to the superset; valid prefix = indptr[-1])."""
+        (data/indices sized to the superset; valid prefix = indptr[-1]).
+        Four kernel launches: count (A and G), scan, write, rhs."""
         import torch
 
+        if getattr(self, "_rhs", None) is None:
+            self._prepare_batched()
         s = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
-        ptrs = (ctypes_ptr_array([lin[k].data_ptr() for k in LIN_SOURCES]))
+        ptrs = ctypes_ptr_array([lin[k].data_ptr() for k in LIN_SOURCES])
         out = {}
-        for M, d in self._mats.items():
+        mats = [self._mats["A"], self._mats["G"]]
+        outs = []
+        for M, d in zip(("A", "G"), mats):
             indptr = torch.empty(self.pat.n + 1, dtype=torch.int32, device=self.device)
             rows = torch.empty(max(1, d["nsup"]), dtype=torch.int32, device=self.device)
             vals = torch.empty(max(1, d["nsup"]), dtype=torch.float64, device=self.device)
-            _lib.check(_lib.lib().cito_csc_assemble_dev(
-                self.pat.n, d["sp_ptr"].data_ptr(), d["row"].data_ptr(), d["src"].data_ptr(), d["idx"].data_ptr(),
-                d["val"].data_ptr(), self.sigma_dev.data_ptr(), ptrs, d["counts"].data_ptr(), indptr.data_ptr(),
-                rows.data_ptr(), vals.data_ptr(), s), "csc_assemble")
-            rhs = d["rhs_const"].clone()
-            _lib.check(_lib.lib().cito_rhs_dev(
-                d["nlin"], d["r_row"].data_ptr(), d["r_form"].data_ptr(), d["r_vsrc"].data_ptr(),
-                d["r_voff"].data_ptr(), d["seg_src"].data_ptr(), d["seg_off"].data_ptr(), d["seg_len"].data_ptr(),
-                d["seg_cb"].data_ptr(), d["cols"].data_ptr(), z_ref_dev.data_ptr(), ptrs, rhs.data_ptr(), s), "rhs")
             out[f"{M}_indptr"], out[f"{M}_indices"], out[f"{M}_data"] = indptr, rows, vals
-            out["b" if M == "A" else "h"] = rhs
+            outs.append((indptr, rows, vals))
+        arr = lambda xs: ctypes_ptr_array([x.data_ptr() for x in xs])  # noqa: E731
+        _lib.check(_lib.lib().cito_csc_assemble2_dev(
+            2, self.pat.n, arr([d["sp_ptr"] for d in mats]), arr([d["row"] for d in mats]),
+            arr([d["src"] for d in mats]), arr([d["idx"] for d in mats]), arr([d["val"] for d in mats]),
+            self.sigma_dev.data_ptr(), ptrs, arr([d["counts"] for d in mats]), arr([o[0] for o in outs]),
+            arr([o[1] for o in outs]), arr([o[2] for o in outs]), s), "csc_assemble")
+        r = self._rhs
+        rhs = r["const"].clone()
+        _lib.check(_lib.lib().cito_rhs_dev(
+            r["n"], r["rows"].data_ptr(), r["form"].data_ptr(), r["vsrc"].data_ptr(), r["voff"].data_ptr(),
+            r["seg_src"].data_ptr(), r["seg_off"].data_ptr(), r["seg_len"].data_ptr(), r["seg_cb"].data_ptr(),
+            r["cols"].data_ptr(), z_ref_dev.data_ptr(), ptrs, rhs.data_ptr(), s), "rhs")
+        out["b"], out["h"] = rhs[: r["nA"]], rhs[r["nA"]:]
         return out
 
     def to_program(self, dev_out, z_j):
