@@ -1209,8 +1209,12 @@ __device__ __forceinline__ void fused_primal(const KParams& P, FusedShared<M>& s
 }
 
 // One tangent column through RK stage I (column warps of k_linearize).
-template <class M, int I>
-__device__ __forceinline__ void col_stage(const KParams& P, FusedShared<M>& sh, int st, int col, double S, double dS,
+// (one code copy for all six RK stages: the stage index I is runtime and the
+// history loops are unrolled to 5 with predication -- keeps the kernel's code
+// footprint inside the instruction caches)
+template <class M>
+__device__ __forceinline__ void col_stage(const KParams& P, FusedShared<M>& sh, int st, const int I, int col, double S,
+                                          double dS,
                                           bool isU, int um, bool uplus, double (&hq)[Pos<M::NHIST>::v],
                                           double (&hv)[Pos<M::NHIST>::v]) {
   using D = Dims<M>;
@@ -1221,7 +1225,7 @@ __device__ __forceinline__ void col_stage(const KParams& P, FusedShared<M>& sh, 
   const double h = P.h;
   const double tau = h * (double)s + P.ch[I];
   const double hb = h * P.b[I];
-  if (I == 0) {  // push q rows: S h sum(b) * (substep-start dv)
+  if (I == 0) {  // push q rows: S h sum(b) * (substep-start dv)  (warp-uniform branch)
 #pragma unroll
     for (int p = 0; p < M::NPUSH; ++p) sh.PQ[p][col] += P.he1 * S * sh.PV[p][col];
   }
@@ -1234,12 +1238,14 @@ __device__ __forceinline__ void col_stage(const KParams& P, FusedShared<M>& sh, 
       const int hs = M::hslot(d);
       val = hq[hs] + S * P.hc1[I] * hv[hs] + dS * R.wq[d];
 #pragma unroll
-      for (int l = 0; l < I; ++l) val += S * P.cq[I][l] * sh.KV[l][hs][col];
+      for (int l = 0; l < 5; ++l)
+        if (l < I) val += S * P.cq[I][l] * sh.KV[l][hs][col];
     } else {
       const int hs = M::hslot(d - NQ);
       val = hv[hs];
 #pragma unroll
-      for (int l = 0; l < I; ++l) val += P.ha[I][l] * sh.KV[l][hs][col];
+      for (int l = 0; l < 5; ++l)
+        if (l < I) val += P.ha[I][l] * sh.KV[l][hs][col];
     }
     vals[kd] = val;
   }
@@ -1401,14 +1407,7 @@ __global__ void __launch_bounds__(FusedDims<M>::NT, MINB) k_linearize(const KPar
       }
     } else if (colthr && t >= 2) {
       const int st = t - 2;
-      switch (st % 6) {  // warp-uniform: the stage index becomes a compile-time constant
-        case 0: col_stage<M, 0>(P, sh, st, col, S, dS, isU, um, uplus, hq, hv); break;
-        case 1: col_stage<M, 1>(P, sh, st, col, S, dS, isU, um, uplus, hq, hv); break;
-        case 2: col_stage<M, 2>(P, sh, st, col, S, dS, isU, um, uplus, hq, hv); break;
-        case 3: col_stage<M, 3>(P, sh, st, col, S, dS, isU, um, uplus, hq, hv); break;
-        case 4: col_stage<M, 4>(P, sh, st, col, S, dS, isU, um, uplus, hq, hv); break;
-        default: col_stage<M, 5>(P, sh, st, col, S, dS, isU, um, uplus, hq, hv); break;
-      }
+      col_stage<M>(P, sh, st, st % 6, col, S, dS, isU, um, uplus, hq, hv);
     }
     CITO_MARK((t * 8 + warp) * 2 + 1);
     __syncthreads();
