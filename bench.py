@@ -372,25 +372,18 @@ def run_ours(args):
 
     # --- e2e through the public API with host (pinned) buffers
     if args.workload == "scp":
-        # the two reference-facing calls cito.scp.solve makes per iteration (scp.py:412-413),
-        # host numpy in / host scipy out: linearize_all (LinearizedProblem) + build_subproblem
-        from types import SimpleNamespace
+        # public API of one SCP iteration's pre-IPM work (= cito.scp.linearize_all +
+        # build_subproblem, scp.py:412-413): host numpy z in, host scipy ConicProgram out
+        from paper_2604_09993_b200.subproblem import GpuSCPStep
 
-        cfg = SimpleNamespace(w_prox=2000.0, w_ep=50000.0)
-        e2e_bytes = {}
-        trs = _TrShim(gt)
+        scp_api = GpuSCPStep(gt)
 
         def e2e_step():
-            lin = gt.linearize_all(z, delta)
-            prog, meta = build_subproblem(trs, lin, z, delta, cfg)
-            if not e2e_bytes:  # bytes actually copied device->host per step (bad flags + pinned program staging)
-                e2e_bytes["d2h"] = int(4 * (lay.N - 1) + sum(v.numel() * v.element_size()
-                                                             for v in _assembler_of(trs)._pinned.values()))
-            return prog
+            return scp_api.iterate(z, delta)
 
         e2e_step()
         h2d = z.nbytes
-        d2h = e2e_bytes["d2h"]
+        d2h = int(4 * (lay.N - 1) + sum(v.numel() * v.element_size() for v in scp_api.asm._pinned.values()))
     elif args.workload == "multistart":
         Z_pin = torch.as_tensor(Z).pin_memory()
         ms_host = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in ms_out.items()}

@@ -519,3 +519,47 @@ def build_subproblem(tr, lin, z_j, delta, config):
         z_ref = torch.as_tensor(np.ascontiguousarray(lin.z_ref, dtype=np.float64), device=dev)
     out = asm.assemble_device(lin_dev, z_ref)
     return asm.to_program(out, z_j)
+
+
+class GpuSCPStep:
+    """One SCP iteration's pre-IPM work in a single device pass (public API).
+
+    ``iterate(z, delta, z_j=None)`` = cito.scp.linearize_all + build_subproblem
+    (scp.py:412-413) with host numpy in / host scipy out: one pinned H2D of z,
+    the interval + node kernels, the whole-subproblem assembly, one batched
+    pinned D2H and a single synchronization.  Raises FloatingPointError for
+    non-finite interval end states like the reference (augmentation.py:231-233).
+    Returns (LinearizedProblem (lazy, device-backed), ConicProgram, meta)."""
+
+    def __init__(self, tr_or_scenario, w_prox=2000.0, w_ep=50000.0, device=None):
+        import torch
+
+        from .linearize import GpuTranscription, LazyLinearizedProblem
+        from .scenario import build_scaling
+
+        self.gt = tr_or_scenario if isinstance(tr_or_scenario, GpuTranscription) else GpuTranscription(
+            tr_or_scenario, device=device)
+        gt = self.gt
+        scale_v = build_scaling(gt.scenario, gt.lay)[0]
+        self.asm = SubproblemAssembler(SubproblemPattern(gt.scenario, gt.lay, scale_v, w_prox, w_ep), gt.device)
+        self._z_pin = torch.empty(gt.lay.dim, dtype=torch.float64, pin_memory=True)
+        self._bad_pin = torch.empty(gt.lay.N - 1, dtype=torch.int32, pin_memory=True)
+        self._Lazy = LazyLinearizedProblem
+
+    def iterate(self, z, delta, z_j=None, epsilon=None):
+        import torch
+
+        z = np.asarray(z, dtype=float)
+        if not np.all(np.isfinite(z)):
+            raise FloatingPointError("non-finite reference point")
+        gt = self.gt
+        self._z_pin.numpy()[:] = z
+        z_dev = self._z_pin.to(gt.device, non_blocking=True)
+        r = gt.linearize_device(z_dev, delta, epsilon)
+        out = self.asm.assemble_device(r, z_dev)
+        self._bad_pin.copy_(r["bad"], non_blocking=True)
+        prog, meta = self.asm.to_program(out, z if z_j is None else z_j)  # the one synchronization
+        bad = self._bad_pin.numpy()
+        if bad.any():
+            raise FloatingPointError(f"non-finite state in intervals {np.where(bad != 0)[0].tolist()}")
+        return self._Lazy(r, z.copy()), prog, meta

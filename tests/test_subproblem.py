@@ -134,3 +134,20 @@ def test_gpu_linearize_then_assemble_matches_reference(name):
         assert np.array_equal(mat.indptr, g[f"sp0_{M}_indptr"]) and np.array_equal(mat.indices, g[f"sp0_{M}_indices"])
         assert rel_err(mat.data, g[f"sp0_{M}_data"]) <= 1e-9, M
     assert rel_err(prog.b, g["sp0_b"]) <= 1e-9 and rel_err(prog.h, g["sp0_h"]) <= 1e-9
+
+
+@pytest.mark.gpu
+def test_gpu_scp_step_iterate_matches_reference():
+    from paper_2604_09993_b200.subproblem import GpuSCPStep
+
+    name = "halfcheetah_n30"
+    g = load_golden(name)
+    step = GpuSCPStep(golden_scenario(name))
+    lin, prog, meta = step.iterate(g["ig_z"], 1.0)
+    for M in ("A", "G"):
+        mat = getattr(prog, M)
+        assert np.array_equal(mat.indptr, g[f"sp0_{M}_indptr"]) and np.array_equal(mat.indices, g[f"sp0_{M}_indices"])
+        assert rel_err(mat.data, g[f"sp0_{M}_data"]) <= 1e-9
+    assert rel_err(lin.jx, g["ig_jx"]) <= 1e-9 and rel_err(lin.defects, g["ig_defects"]) <= 1e-9
+    with pytest.raises(FloatingPointError):
+        step.iterate(np.full_like(g["ig_z"], np.nan), 1.0)
