@@ -8,7 +8,6 @@
 
 #include <cmath>
 #include <cstdio>
-#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -85,7 +84,6 @@ cito_status launch_linearize(const KParams& P, int64_t B, const double* xt0s, co
   static bool attr_done = false;
   if (!attr_done) {
     CUDA_TRY(cudaFuncSetAttribute(k_linearize<M, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    CUDA_TRY(cudaFuncSetAttribute(k_linearize<M, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CUDA_TRY(cudaFuncSetAttribute(k_linearize<M, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr_done = true;
   }
@@ -97,10 +95,8 @@ cito_status launch_linearize(const KParams& P, int64_t B, const double* xt0s, co
   count_launch();
   if (B <= sms)
     k_linearize<M, 1><<<(unsigned)B, FusedDims<M>::NT, smem, st>>>(P, B, xt0s, Us, Ss, ends, jx, ju, js, bad, zs);
-  else if (getenv("CITO_MINB3"))
-    k_linearize<M, 3><<<(unsigned)B, FusedDims<M>::NT, smem, st>>>(P, B, xt0s, Us, Ss, ends, jx, ju, js, bad, zs);
   else
-    k_linearize<M, 2><<<(unsigned)B, FusedDims<M>::NT, smem, st>>>(P, B, xt0s, Us, Ss, ends, jx, ju, js, bad, zs);
+    k_linearize<M, 3><<<(unsigned)B, FusedDims<M>::NT, smem, st>>>(P, B, xt0s, Us, Ss, ends, jx, ju, js, bad, zs);
   CUDA_TRY(cudaGetLastError());
   return CITO_OK;
 }
