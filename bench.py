@@ -302,8 +302,10 @@ def run_ours(args):
 
         sc50 = S2.bundled("halfcheetah_bound", N=50)
         gt50 = GpuTranscription(sc50, device=dev.index)
+        from paper_2604_09993_b200.linearize import initial_guess_batch
+
         seeds = [rank * args.problems + i for i in range(args.problems)]
-        Z = np.stack([initial_guess(sc50, gt50.disc, gt50.lay, seed=sd) for sd in seeds])
+        Z = initial_guess_batch(sc50, gt50.disc, seeds, gt50.lay)  # batched multi-start generation (§8(f) 4)
         Z_dev = torch.as_tensor(Z, device=dev)
         ms_out = gt50.linearize_device(Z_dev, 1.0)
 

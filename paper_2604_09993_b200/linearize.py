@@ -19,7 +19,7 @@ from . import _lib
 from .discretizer import Discretizer
 
 __all__ = ["node_inputs", "LinearizedProblem", "GpuTranscription", "linearize_all", "NodeLinearizer",
-           "initial_guess"]
+           "initial_guess", "initial_guess_batch"]
 
 
 def node_inputs(lay, z):
@@ -280,6 +280,62 @@ def initial_guess(scenario, disc, lay=None, seed=None):
         start = np.concatenate([z[lay.xp(k)][: 2 * n_q], z[lay.y_of_xp(k)]])
         end = disc.propagate(start, z[lay.u(k)].reshape(2, -1), float(z[lay.s(k)][0]))
         z[lay.y_of_xm(k + 1)] = end[2 * n_q:]
+    return z
+
+
+def initial_guess_batch(scenario, disc, seeds, lay=None):
+    """Multi-start initial guesses (cito/ocp.py:461-505 for each seed), with the y
+    forward pass batched across problems: N-1 propagate launches (one per
+    interval index, all problems at once) instead of P*(N-1).  Row p equals
+    initial_guess(scenario, disc, lay, seed=seeds[p])."""
+    from .scenario import Layout
+
+    lay = lay or Layout(scenario)
+    n_q, N = lay.n_q, lay.N
+    Z = np.stack([_initial_guess_no_y(scenario, lay, s) for s in seeds])
+    for k in range(N):
+        Z[:, lay.y_of_xp(k)] = Z[:, lay.y_of_xm(k)]
+        if k == N - 1:
+            break
+        starts = np.concatenate([Z[:, lay.xp(k)[: 2 * n_q]], Z[:, lay.y_of_xp(k)]], axis=1)
+        ends = disc.propagate_batch(starts, Z[:, lay.u(k)], Z[:, lay.s(k)[0]])
+        Z[:, lay.y_of_xm(k + 1)] = ends[:, 2 * n_q:]
+    return Z
+
+
+def _initial_guess_no_y(sc, lay, seed):
+    """Everything of initial_guess except the y forward pass (same RNG draw order)."""
+    model = sc.model
+    rng = np.random.default_rng(sc.seed if seed is None else seed)
+    n_q = lay.n_q
+    z = np.zeros(lay.dim)
+    q_i, q_f = sc.x_init[:n_q], sc.x_final[:n_q]
+    for k in range(lay.N):
+        frac = k / (lay.N - 1)
+        pose = (1.0 - frac) * q_i + frac * q_f
+        z[lay.xm(k)[:n_q]] = pose
+        z[lay.xp(k)[:n_q]] = pose
+    for k in range(lay.N - 1):
+        u = np.zeros(2 * lay.n_u)
+        for side in range(2):
+            base = side * lay.n_u + lay.n_a
+            for i in range(lay.n_c):
+                mu = model.contacts[i].friction_mu
+                fn = rng.uniform(0.0, sc.guess_force_scale)
+                ft = rng.uniform(-mu * fn, mu * fn) if fn > 0 else 0.0
+                u[base + 2 * i] = ft
+                u[base + 2 * i + 1] = fn
+        z[lay.u(k)] = u
+        z[lay.s(k)] = sc.s_nominal
+    for k in range(lay.N):
+        blk = np.zeros(2 * lay.n_c)
+        for i in range(lay.n_c):
+            mu = model.contacts[i].friction_mu
+            pn = rng.uniform(0.0, sc.guess_impulse_scale) if sc.guess_impulse_scale else 0.0
+            pt = rng.uniform(-mu * pn, mu * pn) if pn > 0 else 0.0
+            blk[2 * i] = pt
+            blk[2 * i + 1] = pn
+        z[lay.phi(k)] = blk
     return z
 
 

@@ -143,3 +143,20 @@ def test_multistart_batch_equals_single_problems():
             rows = n_node if k in ("theta", "theta_jac", "imp_v", "imp_jac") else n_int
             got = allp[k][p * rows:(p + 1) * rows]
             assert rel_err(got.cpu().numpy(), v.cpu().numpy()) <= 1e-12, k
+
+
+@pytest.mark.gpu
+def test_initial_guess_matches_reference_and_batch():
+    """GPU initial guess == the reference's initial_guess (golden ig_z); the
+    multi-start batched version == one call per seed."""
+    from paper_2604_09993_b200.linearize import GpuTranscription, initial_guess, initial_guess_batch
+
+    for name in ["pointmass_rest", "monoped_n20", "halfcheetah_n30"]:
+        g = load_golden(name)
+        sc = golden_scenario(name)
+        gt = GpuTranscription(sc)
+        z = initial_guess(sc, gt.disc, gt.lay)
+        assert rel_err(z, g["ig_z"]) <= 1e-9, name
+        Z = initial_guess_batch(sc, gt.disc, [sc.seed, 3, 11], gt.lay)
+        assert np.array_equal(Z[0], z)
+        assert np.array_equal(Z[2], initial_guess(sc, gt.disc, gt.lay, seed=11))
