@@ -193,12 +193,15 @@ cito_status cito_csc_assemble_dev(int32_t ncols, const int64_t* sp_ptr, const in
 
 /* Same as cito_csc_assemble_dev for nmat (1 or 2, e.g. A and G) matrices with
  * the same column count in one set of launches; every pointer argument except
- * sigma and lin is a HOST array of nmat device pointers. */
+ * sigma and lin is a HOST array of nmat device pointers.  rowmax (optional,
+ * NULL = off): per matrix a ZEROED device uint64[nrows] that receives the row
+ * inf-norms (bit patterns of max |value|) for cito_precondition_dev. */
 cito_status cito_csc_assemble2_dev(int32_t nmat, int32_t ncols, const int64_t* const* sp_ptr,
                                    const int32_t* const* sp_row, const int8_t* const* sp_src,
                                    const int64_t* const* sp_idx, const double* const* sp_val, const double* sigma,
                                    const double* const* lin, int32_t* const* counts, int32_t* const* out_ptr,
-                                   int32_t* const* out_rows, double* const* out_vals, void* stream);
+                                   int32_t* const* out_rows, double* const* out_vals,
+                                   unsigned long long* const* rowmax, void* stream);
 
 /* b / h of the linearized rows: out[rows[i]] = form ? J.z[cols] - v : v - J.z[cols]
  * with J split in up to 3 segments (seg_src < 0 = unused), v = lin[vsrc[i]][voff[i]]. */
@@ -206,6 +209,25 @@ cito_status cito_rhs_dev(int64_t nrows, const int32_t* rows, const int8_t* form,
                          const int64_t* voff, const int8_t* seg_src, const int64_t* seg_off, const int32_t* seg_len,
                          const int64_t* seg_cb, const int64_t* cols, const double* z, const double* const* lin,
                          double* out, void* stream);
+
+/* cito.conic.precondition (cito/conic.py:290-338) of a device-resident program
+ * (CSC A: nA rows, G: nG rows, int32 indptr/indices, ncols columns), in place:
+ *   row_scale_A[i] = 1 / inf-norm of row i (1 for an all-zero row);
+ *   row_scale_G    = the same for the n_nonneg orthant rows; each SOC block
+ *                    k (rows soc_start[k] .. + soc_dim[k], device int32 arrays)
+ *                    shares 1 / max over its rows (1 if that max is 0);
+ *   A.data, b, G.data, h multiplied by their row's scale (values bit-identical
+ *   to scipy's Da @ A).
+ * rowmax_A/G: device uint64 workspaces [nA]/[nG]; rowmax_ready != 0 means they
+ * already hold the norms (fused into cito_csc_assemble2_dev), else this call
+ * computes them.  max_nnz: upper bound of the stored entries of A and G.
+ * The cost scaling (c / omega, P / omega) is a host-side scalar (Python layer). */
+cito_status cito_precondition_dev(int32_t ncols, const int32_t* A_ptr, const int32_t* A_rows, double* A_data,
+                                  int32_t nA, double* b, const int32_t* G_ptr, const int32_t* G_rows, double* G_data,
+                                  int32_t nG, double* h, int32_t n_nonneg, int32_t n_soc, const int32_t* soc_start,
+                                  const int32_t* soc_dim, unsigned long long* rowmax_A, unsigned long long* rowmax_G,
+                                  int32_t rowmax_ready, int32_t max_nnz, double* row_scale_A, double* row_scale_G,
+                                  void* stream);
 
 /* FP64 DFMA throughput probe (roofline denominator; not part of the reference
  * interface).  Launches one kernel on `stream`; returns the flops it issues

@@ -477,7 +477,8 @@ cito_status cito_csc_assemble2_dev(int32_t nmat, int32_t ncols, const int64_t* c
                                    const int32_t* const* sp_row, const int8_t* const* sp_src,
                                    const int64_t* const* sp_idx, const double* const* sp_val, const double* sigma,
                                    const double* const* lin, int32_t* const* counts, int32_t* const* out_ptr,
-                                   int32_t* const* out_rows, double* const* out_vals, void* stream) {
+                                   int32_t* const* out_rows, double* const* out_vals,
+                                   unsigned long long* const* rowmax, void* stream) {
   if (ncols <= 0 || nmat < 1 || nmat > 2) return nmat == 0 ? CITO_OK : fail(CITO_ERR_ARG, "nmat must be 1 or 2");
   LinTable L;
   for (int k = 0; k < 10; ++k) L.p[k] = lin ? lin[k] : nullptr;
@@ -496,6 +497,7 @@ cito_status cito_csc_assemble2_dev(int32_t nmat, int32_t ncols, const int64_t* c
     ca.out_ptr[m] = out_ptr[m];
     ca.out_rows[m] = out_rows[m];
     ca.out_vals[m] = out_vals[m];
+    ca.rowmax[m] = rowmax ? rowmax[m] : nullptr;
     sa.n[m] = ncols;
     sa.counts[m] = counts[m];
     sa.out_ptr[m] = out_ptr[m];
@@ -515,7 +517,7 @@ cito_status cito_csc_assemble_dev(int32_t ncols, const int64_t* sp_ptr, const in
                                   const double* const* lin, int32_t* counts, int32_t* out_ptr, int32_t* out_rows,
                                   double* out_vals, void* stream) {
   return cito_csc_assemble2_dev(1, ncols, &sp_ptr, &sp_row, &sp_src, &sp_idx, &sp_val, sigma, lin, &counts, &out_ptr,
-                                &out_rows, &out_vals, stream);
+                                &out_rows, &out_vals, nullptr, stream);
 }
 
 cito_status cito_rhs_dev(int64_t nrows, const int32_t* rows, const int8_t* form, const int8_t* vsrc,
@@ -530,6 +532,60 @@ cito_status cito_rhs_dev(int64_t nrows, const int32_t* rows, const int8_t* form,
   k_rhs<<<(unsigned)((nrows + wpb - 1) / wpb), 32 * wpb, 0, (cudaStream_t)stream>>>(
       nrows, rows, form, vsrc, voff, seg_src, seg_off, seg_len, seg_cb, cols, z, L, out);
   CUDA_TRY(cudaGetLastError());
+  return CITO_OK;
+}
+
+cito_status cito_precondition_dev(int32_t ncols, const int32_t* A_ptr, const int32_t* A_rows, double* A_data,
+                                  int32_t nA, double* b, const int32_t* G_ptr, const int32_t* G_rows, double* G_data,
+                                  int32_t nG, double* h, int32_t n_nonneg, int32_t n_soc, const int32_t* soc_start,
+                                  const int32_t* soc_dim, unsigned long long* rowmax_A, unsigned long long* rowmax_G,
+                                  int32_t rowmax_ready, int32_t max_nnz, double* row_scale_A, double* row_scale_G,
+                                  void* stream) {
+  if (ncols < 0 || nA < 0 || nG < 0 || n_nonneg < 0 || n_nonneg > nG || n_soc < 0 || max_nnz < 0)
+    return fail(CITO_ERR_ARG, "precondition: bad sizes");
+  cudaStream_t s = (cudaStream_t)stream;
+  PcArgs a;
+  a.ptr[0] = A_ptr;
+  a.ptr[1] = G_ptr;
+  a.rows[0] = A_rows;
+  a.rows[1] = G_rows;
+  a.data[0] = A_data;
+  a.data[1] = G_data;
+  a.rhs[0] = b;
+  a.rhs[1] = h;
+  a.nrows[0] = nA;
+  a.nrows[1] = nG;
+  a.rowmax[0] = rowmax_A;
+  a.rowmax[1] = rowmax_G;
+  a.scale[0] = row_scale_A;
+  a.scale[1] = row_scale_G;
+  if (!rowmax_ready) {
+    if (nA) CUDA_TRY(cudaMemsetAsync(rowmax_A, 0, sizeof(unsigned long long) * (size_t)nA, s));
+    if (nG) CUDA_TRY(cudaMemsetAsync(rowmax_G, 0, sizeof(unsigned long long) * (size_t)nG, s));
+    if (ncols > 0) {
+      const int wpb = 8;
+      count_launch();
+      k_row_absmax<<<dim3((unsigned)((ncols + wpb - 1) / wpb), 2), 32 * wpb, 0, s>>>(ncols, a);
+      CUDA_TRY(cudaGetLastError());
+    }
+  }
+  const int64_t nsc = (int64_t)nA + n_nonneg + n_soc;
+  if (nsc > 0) {
+    count_launch();
+    k_row_scale<<<(unsigned)((nsc + 255) / 256), 256, 0, s>>>(a, n_nonneg, n_soc, soc_start, soc_dim);
+    CUDA_TRY(cudaGetLastError());
+  }
+  const int64_t work = (int64_t)max_nnz + (nA > nG ? nA : nG);
+  if (ncols > 0 && work > 0) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t want = (work + 255) / 256;
+    const unsigned gx = (unsigned)(want < 4 * sms ? want : 4 * sms);
+    count_launch();
+    k_row_apply<<<dim3(gx, 2), 256, 0, s>>>(ncols, a);
+    CUDA_TRY(cudaGetLastError());
+  }
   return CITO_OK;
 }
 

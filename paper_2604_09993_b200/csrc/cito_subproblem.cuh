@@ -37,6 +37,7 @@ struct CscArgs {
   int32_t* out_ptr[2];
   int32_t* out_rows[2];
   double* out_vals[2];
+  unsigned long long* rowmax[2];  // optional (nullptr): row inf-norms for the preconditioner, as |v| bits
 };
 
 __global__ void __launch_bounds__(256) k_csc_count(int32_t ncols, const CscArgs a, const double* __restrict__ sigma,
@@ -119,8 +120,11 @@ __global__ void __launch_bounds__(256) k_csc_write(int32_t ncols, const CscArgs 
     const unsigned msk = __ballot_sync(0xffffffffu, nz);
     if (nz) {
       const int32_t pos = base + __popc(msk & lt);
-      a.out_rows[m][pos] = a.row[m][e];
+      const int32_t r = a.row[m][e];
+      a.out_rows[m][pos] = r;
       a.out_vals[m][pos] = v;
+      // fused row inf-norm (cito/conic.py:281-287): non-negative doubles order like their bits
+      if (a.rowmax[m]) atomicMax(&a.rowmax[m][r], (unsigned long long)__double_as_longlong(fabs(v)));
     }
     base += __popc(msk);
   }
@@ -151,5 +155,80 @@ __global__ void __launch_bounds__(256) k_rhs(int64_t nrows, const int32_t* __res
   if (lane == 0) {
     const double v = L.p[vsrc[i]][voff[i]];
     out[rows[i]] = form[i] == 0 ? v - dot : dot - v;  // dynamics: ends - J.ref ; others: J.ref - value
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Preconditioning of the assembled program on the device:
+// cito.conic.precondition (/root/reference/pkg/src/cito/conic.py:290-338).
+//   row inf-norms  (conic.py:281-287)  fused into k_csc_write, or k_row_absmax
+//                                      for a program that was uploaded as is
+//   row scales     (conic.py:294-309)  A and the orthant rows of G: 1/norm (1 for
+//                                      an all-zero row); each SOC block of G
+//                                      shares 1/max over its rows (1 if the max is 0)
+//   scaling        (conic.py:321-331)  data[e] *= scale[row[e]], b *= sA, h *= sG
+//                                      (Da @ A is one product per entry in scipy too,
+//                                      so the scaled values are bit-identical)
+struct PcArgs {
+  const int32_t* ptr[2];
+  const int32_t* rows[2];
+  double* data[2];
+  double* rhs[2];
+  int32_t nrows[2];
+  unsigned long long* rowmax[2];
+  double* scale[2];
+};
+
+__global__ void __launch_bounds__(256) k_row_absmax(int32_t ncols, const PcArgs a) {
+  const int m = blockIdx.y;
+  const int lane = threadIdx.x & 31;
+  const int64_t c = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (c >= ncols) return;
+  for (int32_t e = a.ptr[m][c] + lane; e < a.ptr[m][c + 1]; e += 32) {
+    const double v = a.data[m][e];
+    if (v != 0.0) atomicMax(&a.rowmax[m][a.rows[m][e]], (unsigned long long)__double_as_longlong(fabs(v)));
+  }
+}
+
+// one thread per A row, per orthant row of G, and per SOC block of G
+__global__ void __launch_bounds__(256) k_row_scale(const PcArgs a, int32_t n_nonneg, int32_t n_soc,
+                                                   const int32_t* __restrict__ soc_start,
+                                                   const int32_t* __restrict__ soc_dim) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nA = a.nrows[0];
+  if (i < nA) {
+    const double r = __longlong_as_double((long long)a.rowmax[0][i]);
+    a.scale[0][i] = 1.0 / (r == 0.0 ? 1.0 : r);  // ra[ra == 0] = 1; da = 1 / ra
+    return;
+  }
+  const int64_t j = i - nA;
+  if (j < n_nonneg) {
+    const double r = __longlong_as_double((long long)a.rowmax[1][j]);
+    a.scale[1][j] = r != 0.0 ? 1.0 / r : 1.0;
+    return;
+  }
+  const int64_t k = j - n_nonneg;
+  if (k < n_soc) {
+    const int32_t s0 = soc_start[k], d = soc_dim[k];
+    double mx = 0.0;
+    for (int32_t r = 0; r < d; ++r) mx = fmax(mx, __longlong_as_double((long long)a.rowmax[1][s0 + r]));
+    const double sc = mx > 0.0 ? 1.0 / mx : 1.0;
+    for (int32_t r = 0; r < d; ++r) a.scale[1][s0 + r] = sc;
+  }
+}
+
+// grid-stride over the stored entries (valid prefix = ptr[ncols]) and the rhs rows
+__global__ void __launch_bounds__(256) k_row_apply(int32_t ncols, const PcArgs a) {
+  const int m = blockIdx.y;
+  const int32_t nnz = a.ptr[m][ncols];
+  const int64_t total = (int64_t)nnz + a.nrows[m];
+  const double* __restrict__ sc = a.scale[m];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < nnz) {
+      a.data[m][i] = sc[a.rows[m][i]] * a.data[m][i];
+    } else {
+      const int64_t r = i - nnz;
+      a.rhs[m][r] = sc[r] * a.rhs[m][r];
+    }
   }
 }

@@ -28,7 +28,7 @@ import numpy as np
 
 from . import _lib
 
-__all__ = ["SubproblemPattern", "SubproblemAssembler", "LIN_SOURCES"]
+__all__ = ["SubproblemPattern", "SubproblemAssembler", "LIN_SOURCES", "build_subproblem", "precondition", "GpuSCPStep"]
 
 # value sources (device pointer table order)
 LIN_SOURCES = ["jx", "ju", "js", "imp_jac", "theta_jac", "psi_jac", "ends", "imp_v", "theta", "psi"]
@@ -325,6 +325,114 @@ class _Meta:
         return float(np.sum(sol.x[self.sp_idx]) + np.sum(sol.x[self.sm_idx]) + np.sum(sol.x[self.t_idx]))
 
 
+@dataclass
+class Preconditioner:
+    """Same fields as cito.conic.Preconditioner (conic.py:270-277)."""
+
+    row_scale_A: np.ndarray
+    row_scale_G: np.ndarray
+    var_scale: np.ndarray
+    cost_scale: float = 1.0
+
+
+def _preconditioner_type():
+    mod = sys.modules.get("cito.conic")
+    return getattr(mod, "Preconditioner", Preconditioner) if mod is not None else Preconditioner
+
+
+def soc_tables(n_nonneg, soc_dims, device):
+    """Device int32 (start row, dim) of every SOC block of G (G rows: orthant, then SOC blocks)."""
+    import torch
+
+    dims = np.asarray(soc_dims, dtype=np.int32).reshape(-1)
+    start = (n_nonneg + np.concatenate([[0], np.cumsum(dims)[:-1]])).astype(np.int32) if dims.size else dims
+    t = lambda a: torch.as_tensor(np.ascontiguousarray(a if a.size else np.zeros(1, np.int32)), device=device)  # noqa
+    return t(start), t(dims)
+
+
+def precondition_device(ncols, out, nA, nG, n_nonneg, n_soc, soc_start, soc_dim, rowmax, max_nnz, stream):
+    """Row scaling of a device program in place (cito_precondition_dev); returns
+    the device row scales (A, G).  rowmax = (A, G) zeroed int64 workspaces that
+    already hold the fused norms, or None (computed here)."""
+    import torch
+
+    dev = out["A_data"].device
+    ready = rowmax is not None
+    if not ready:
+        rm = torch.empty(max(1, nA + nG), dtype=torch.int64, device=dev)
+        rowmax = (rm[:nA], rm[nA:])
+    sA = torch.empty(max(1, nA), dtype=torch.float64, device=dev)
+    sG = torch.empty(max(1, nG), dtype=torch.float64, device=dev)
+    _lib.check(_lib.lib().cito_precondition_dev(
+        int(ncols), out["A_indptr"].data_ptr(), out["A_indices"].data_ptr(), out["A_data"].data_ptr(), int(nA),
+        out["b"].data_ptr(), out["G_indptr"].data_ptr(), out["G_indices"].data_ptr(), out["G_data"].data_ptr(),
+        int(nG), out["h"].data_ptr(), int(n_nonneg), int(n_soc), soc_start.data_ptr(), soc_dim.data_ptr(),
+        rowmax[0].data_ptr(), rowmax[1].data_ptr(), int(ready), int(max_nnz), sA.data_ptr(), sG.data_ptr(), stream),
+        "precondition")
+    return sA[:nA], sG[:nG]
+
+
+def precondition(prog):
+    """Drop-in for cito.conic.precondition (conic.py:290-338), computed on the GPU.
+
+    A program produced by this package's build_subproblem is scaled where it
+    already lives (device copy of the last assembly); any other program is
+    uploaded, scaled by the same kernels and copied back.  Returns
+    (scaled ConicProgram, Preconditioner) with the reference's types when
+    cito.conic is loaded; A/G values and row scales are bit-identical to the
+    reference's, b/h scale the GPU's own b/h by the same factors."""
+    import scipy.sparse as sp
+    import torch
+
+    ConicProgram, ConeSpec = _conic_types()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    cones = prog.cones
+    n = int(prog.A.shape[1])
+    nA, nG = int(prog.A.shape[0]), int(prog.G.shape[0])
+    own = None
+    for asm in _assemblers.values():
+        last = getattr(asm, "last", None)
+        if last is not None and last[0] is prog:
+            own = last[1]
+            break
+    if own is not None:  # device copy of exactly these values (to_program copied it out unchanged)
+        out = {k: own[k].clone() for k in ("A_indptr", "A_indices", "A_data", "b", "G_indptr", "G_indices", "G_data",
+                                           "h")}
+    else:
+        def up(M):
+            M = sp.csc_matrix(M)
+            M.sort_indices()
+            return (torch.as_tensor(M.indptr.astype(np.int32), device=dev),
+                    torch.as_tensor(M.indices.astype(np.int32) if M.nnz else np.zeros(1, np.int32), device=dev),
+                    torch.as_tensor(M.data.astype(np.float64) if M.nnz else np.zeros(1), device=dev))
+
+        out = {}
+        for M, mat in (("A", prog.A), ("G", prog.G)):
+            out[f"{M}_indptr"], out[f"{M}_indices"], out[f"{M}_data"] = up(mat)
+        out["b"] = torch.as_tensor(np.ascontiguousarray(prog.b, dtype=np.float64).reshape(-1), device=dev)
+        out["h"] = torch.as_tensor(np.ascontiguousarray(prog.h, dtype=np.float64).reshape(-1), device=dev)
+    start, dim = soc_tables(int(cones.nonneg), tuple(cones.soc), dev)
+    max_nnz = max(int(prog.A.nnz), int(prog.G.nnz))
+    sA, sG = precondition_device(n, out, nA, nG, int(cones.nonneg), len(cones.soc), start, dim, None, max_nnz, stream)
+    host = {k: v.cpu().numpy() for k, v in out.items()}
+    mats = {}
+    for M, mat in (("A", prog.A), ("G", prog.G)):
+        indptr = host[f"{M}_indptr"]
+        nnz = int(indptr[-1])
+        mats[M] = sp.csc_matrix((host[f"{M}_data"][:nnz], host[f"{M}_indices"][:nnz], indptr), shape=mat.shape)
+    omega = max(1.0, float(np.max(np.abs(prog.c))) if prog.c.size else 0.0)
+    if prog.P.nnz:
+        omega = max(omega, float(np.max(np.abs(prog.P.data))))
+    P = sp.csc_matrix(prog.P / omega)
+    P.sort_indices()
+    scaled = ConicProgram(P=P, c=prog.c / omega, A=mats["A"], b=host["b"][:nA].copy(), G=mats["G"],
+                          h=host["h"][:nG].copy(), cones=cones)
+    prec = _preconditioner_type()(row_scale_A=sA.cpu().numpy().copy(), row_scale_G=sG.cpu().numpy().copy(),
+                                  var_scale=np.ones(n), cost_scale=omega)
+    return scaled, prec
+
+
 @dataclass(frozen=True)
 class ConeSpec:
     """Same fields as cito.conic.ConeSpec (conic.py:37-51)."""
@@ -412,11 +520,15 @@ class SubproblemAssembler:
                          cols=torch.cat([dA["cols"], dG["cols"]]), const=torch.cat([dA["rhs_const"], dG["rhs_const"]]),
                          n=dA["nlin"] + dG["nlin"], nA=nA)
 
-    def assemble_device(self, lin, z_ref_dev, stream=None):
+    def assemble_device(self, lin, z_ref_dev, stream=None, precondition=False):
         """lin: dict of device tensors with the LIN_SOURCES fields.  Returns device
         tensors {A_indptr, A_indices, A_data, b, G_indptr, G_indices, G_data, h}
         (data/indices sized to the superset; valid prefix = indptr[-1]).
-        Four kernel launches: count (A and G), scan, write, rhs."""
+        Four kernel launches: count (A and G), scan, write, rhs.  With
+        ``precondition`` the program is returned already row-scaled as
+        cito.conic.precondition does (conic.py:290-338): the row inf-norms are
+        fused into the CSC write and two more launches form and apply the row
+        scales (+ ``row_scale_A`` / ``row_scale_G`` in the result)."""
         import torch
 
         if getattr(self, "_rhs", None) is None:
@@ -433,11 +545,17 @@ class SubproblemAssembler:
             out[f"{M}_indptr"], out[f"{M}_indices"], out[f"{M}_data"] = indptr, rows, vals
             outs.append((indptr, rows, vals))
         arr = lambda xs: ctypes_ptr_array([x.data_ptr() for x in xs])  # noqa: E731
+        rowmax = None
+        if precondition:
+            nA, nG = mats[0]["nrows"], mats[1]["nrows"]
+            rm = torch.zeros(max(1, nA + nG), dtype=torch.int64, device=self.device)
+            rowmax = (rm[:nA], rm[nA:])
         _lib.check(_lib.lib().cito_csc_assemble2_dev(
             2, self.pat.n, arr([d["sp_ptr"] for d in mats]), arr([d["row"] for d in mats]),
             arr([d["src"] for d in mats]), arr([d["idx"] for d in mats]), arr([d["val"] for d in mats]),
             self.sigma_dev.data_ptr(), ptrs, arr([d["counts"] for d in mats]), arr([o[0] for o in outs]),
-            arr([o[1] for o in outs]), arr([o[2] for o in outs]), s), "csc_assemble")
+            arr([o[1] for o in outs]), arr([o[2] for o in outs]), arr(rowmax) if rowmax else None, s),
+            "csc_assemble")
         r = self._rhs
         rhs = r["const"].clone()
         _lib.check(_lib.lib().cito_rhs_dev(
@@ -445,20 +563,40 @@ class SubproblemAssembler:
             r["seg_src"].data_ptr(), r["seg_off"].data_ptr(), r["seg_len"].data_ptr(), r["seg_cb"].data_ptr(),
             r["cols"].data_ptr(), z_ref_dev.data_ptr(), ptrs, rhs.data_ptr(), s), "rhs")
         out["b"], out["h"] = rhs[: r["nA"]], rhs[r["nA"]:]
+        if precondition:
+            self._precondition(out, rowmax, s)
         return out
+
+    def _soc_tables(self):
+        if getattr(self, "_soc_dev", None) is None:
+            self._soc_dev = soc_tables(self.pat.n_orthant, self.pat.soc_dims, self.device)
+        return self._soc_dev
+
+    def _precondition(self, out, rowmax, stream):
+        start, dim = self._soc_tables()
+        out["row_scale_A"], out["row_scale_G"] = precondition_device(
+            self.pat.n, out, self._mats["A"]["nrows"], self._mats["G"]["nrows"], self.pat.n_orthant,
+            len(self.pat.soc_dims), start, dim, rowmax, max(self._mats["A"]["nsup"], self._mats["G"]["nsup"]),
+            stream)
 
     def to_program(self, dev_out, z_j):
         """Host ConicProgram (scipy CSC, the reference's types when loaded) + meta.
-        One batched device->host copy into pinned staging, one synchronization."""
+        One batched device->host copy into pinned staging, one synchronization.
+        For a preconditioned ``dev_out`` returns (scaled program, Preconditioner, meta)."""
         import scipy.sparse as sp
         import torch
 
         ConicProgram, ConeSpec = _conic_types()
         pat = self.pat
         keys = ["A_indptr", "A_indices", "A_data", "b", "G_indptr", "G_indices", "G_data", "h"]
+        scaled = "row_scale_A" in dev_out
+        if scaled:
+            keys = keys + ["row_scale_A", "row_scale_G"]
         if getattr(self, "_pinned", None) is None:
-            self._pinned = {k: torch.empty(dev_out[k].shape, dtype=dev_out[k].dtype, pin_memory=True) for k in keys}
+            self._pinned = {}
         for k in keys:
+            if k not in self._pinned:
+                self._pinned[k] = torch.empty(dev_out[k].shape, dtype=dev_out[k].dtype, pin_memory=True)
             self._pinned[k].copy_(dev_out[k], non_blocking=True)
         torch.cuda.current_stream(self.device).synchronize()
         host = {k: self._pinned[k].numpy() for k in keys}
@@ -469,12 +607,26 @@ class SubproblemAssembler:
             mats[M] = sp.csc_matrix((host[f"{M}_data"][:nnz].copy(), host[f"{M}_indices"][:nnz].copy(), indptr),
                                     shape=(self._mats[M]["nrows"], pat.n))
         dim = pat.lay.dim
-        P = sp.csc_matrix((pat.P_diag[:dim], np.arange(dim, dtype=np.int32),
+        P_data = pat.P_diag[:dim]
+        c = pat.objective_c(z_j)
+        omega = 1.0
+        if scaled:  # cost normalization (conic.py:311-316): host scalars
+            omega = max(1.0, float(np.max(np.abs(c))) if c.size else 0.0)
+            if P_data.size:
+                omega = max(omega, float(np.max(np.abs(P_data))))
+            P_data, c = P_data * (1.0 / omega), c / omega  # scipy's P / omega is P * (1 / omega)
+        P = sp.csc_matrix((P_data, np.arange(dim, dtype=np.int32),
                            np.concatenate([np.arange(dim + 1), np.full(pat.n - dim, dim)]).astype(np.int32)),
                           shape=(pat.n, pat.n))
-        prog = ConicProgram(P=P, c=pat.objective_c(z_j), A=mats["A"], b=host["b"].copy(), G=mats["G"],
+        prog = ConicProgram(P=P, c=c, A=mats["A"], b=host["b"].copy(), G=mats["G"],
                             h=host["h"].copy(), cones=ConeSpec(nonneg=pat.n_orthant, soc=pat.soc_dims))
         meta = _Meta(pat.z_idx, pat.sp_idx, pat.sm_idx, pat.t_idx)
+        if scaled:
+            prec = _preconditioner_type()(row_scale_A=host["row_scale_A"].copy(),
+                                          row_scale_G=host["row_scale_G"].copy(), var_scale=np.ones(pat.n),
+                                          cost_scale=omega)
+            return prog, prec, meta
+        self.last = (prog, dev_out)  # the precondition drop-in reuses the device copy
         return prog, meta
 
 
@@ -546,7 +698,10 @@ class GpuSCPStep:
         self._bad_pin = torch.empty(gt.lay.N - 1, dtype=torch.int32, pin_memory=True)
         self._Lazy = LazyLinearizedProblem
 
-    def iterate(self, z, delta, z_j=None, epsilon=None):
+    def iterate(self, z, delta, z_j=None, epsilon=None, precondition=False):
+        """Returns (lin, prog, meta); with ``precondition`` the program comes back
+        row-scaled on the device (= cito.conic.precondition, scp.py:414) and the
+        result is (lin, scaled_prog, Preconditioner, meta)."""
         import torch
 
         z = np.asarray(z, dtype=float)
@@ -556,10 +711,10 @@ class GpuSCPStep:
         self._z_pin.numpy()[:] = z
         z_dev = self._z_pin.to(gt.device, non_blocking=True)
         r = gt.linearize_device(z_dev, delta, epsilon)
-        out = self.asm.assemble_device(r, z_dev)
+        out = self.asm.assemble_device(r, z_dev, precondition=precondition)
         self._bad_pin.copy_(r["bad"], non_blocking=True)
-        prog, meta = self.asm.to_program(out, z if z_j is None else z_j)  # the one synchronization
+        res = self.asm.to_program(out, z if z_j is None else z_j)  # the one synchronization
         bad = self._bad_pin.numpy()
         if bad.any():
             raise FloatingPointError(f"non-finite state in intervals {np.where(bad != 0)[0].tolist()}")
-        return self._Lazy(r, z.copy()), prog, meta
+        return (self._Lazy(r, z.copy()),) + tuple(res)

@@ -2,8 +2,9 @@
 
 The unmodified reference package (installed copy in baseline/_ref, or
 /root/reference in the build container) runs through the jax shim
-(oracle/jaxshim, test infrastructure); its `cito.scp.linearize_all` and the
-transcription's discretizer are replaced by the GPU implementations and
+(oracle/jaxshim, test infrastructure); its `cito.scp.linearize_all`,
+`build_subproblem`, `precondition` and the transcription's discretizer are
+replaced by the GPU implementations and
 `cito.scp.solve` runs a few SCP iterations (host IPM + homotopy unchanged).
 The iterates must match the reference's own path.  Runs in a subprocess so
 the shim's global torch settings cannot leak into other tests.
@@ -52,13 +53,14 @@ if compare:
 ocp._transcriptions.clear()
 tr = ocp.get_transcription(sc)
 install(tr)                       # tr.discretizer -> GPU (initial_guess uses it)
-orig = scp.linearize_all, scp.build_subproblem
+orig = scp.linearize_all, scp.build_subproblem, scp.precondition
 scp.linearize_all = G.linearize_all         # GPU linearize_all (intervals + node relations)
 scp.build_subproblem = SPB.build_subproblem  # GPU subproblem assembly (CSC values, b, h)
+scp.precondition = SPB.precondition          # GPU row scaling of the assembled program
 try:
     z, hist, st = scp.solve(sc, cfg)
 finally:
-    scp.linearize_all, scp.build_subproblem = orig
+    scp.linearize_all, scp.build_subproblem, scp.precondition = orig
 out["gpu"] = [h.z.tolist() for h in hist]
 out["gpu_delta"] = [h.delta for h in hist]
 out["status"] = st
