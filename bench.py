@@ -49,7 +49,8 @@ def parse():
     p.add_argument("--steps", type=int, default=50)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--workload", choices=["scp", "batch", "multistart"], default="scp")
+    p.add_argument("--workload", choices=["scp", "fine", "batch", "multistart"], default="scp")
+    p.add_argument("--no-fine-extra", action="store_true")
     p.add_argument("--problems", type=int, default=128, help="multistart: problems per GPU (configs[3]: 1024 / 8)")
     p.add_argument("--batch", type=int, default=4096)
     p.add_argument("--cpu-seconds", type=float, default=10.0)
@@ -64,12 +65,34 @@ def env_rank():
 
 
 # --------------------------------------------------------------------------- shared problem setup
-def scp_problem(seed):
+FINE = dict(N=200, substeps=8)  # configs[4]: HalfCheetah fine grid (the reference has no RK4: its RKF at 8 substeps)
+
+
+def scp_problem(seed, fine=False):
     from paper_2604_09993_b200 import scenario as S
 
-    sc = S.bundled("halfcheetah_bound", N=30)
+    sc = S.bundled("halfcheetah_bound", **(FINE if fine else dict(N=30)))
     sc.seed = seed
     return sc
+
+
+class _OracleDisc:
+    """propagate() through the CPU oracle: builds the reference-arm input (the
+    scenario's initial guess) without touching the GPU path."""
+
+    def __init__(self, sc):
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import pyoracle
+
+        from paper_2604_09993_b200.model import pack_model
+
+        g, n_g = sc.path_constraints()
+        self.po, self.desc, self.substeps = pyoracle, pack_model(sc.model, sc.mixing_matrix(n_g), g), sc.substeps
+
+    def propagate(self, xt0, U, S):
+        e = self.po.propagate(self.desc, self.substeps, np.asarray(xt0)[None], np.asarray(U).reshape(1, -1),
+                              np.array([float(S)]))[0]
+        return e[0]
 
 
 def _reference_scp():
@@ -105,7 +128,9 @@ def cpu_step_fn(sc, seed):
     lay = Layout(sc)
     g, n_g = sc.path_constraints()
     desc = pack_model(sc.model, sc.mixing_matrix(n_g), g)
-    z = np.load(os.path.join(ROOT, "tests", "golden", "halfcheetah_n30.npz"))["ig_z"]
+    from paper_2604_09993_b200.linearize import initial_guess
+
+    z = initial_guess(sc, _OracleDisc(sc), lay)
     starts = np.stack([z[lay.xp(k)] for k in range(lay.N - 1)])
     Us = np.stack([z[lay.u(k)] for k in range(lay.N - 1)])
     Ss = np.array([z[lay.s(k)][0] for k in range(lay.N - 1)])
@@ -117,7 +142,7 @@ def cpu_step_fn(sc, seed):
 
         ocp, scp = ref
         rsc = ocp.load_scenario(os.path.join(ROOT, "tests", "golden", "assets", "halfcheetah_bound.json"))
-        tr = ocp.Transcription(replace(rsc, N=sc.N, s_bounds=None))
+        tr = ocp.Transcription(replace(rsc, N=sc.N, s_bounds=None, substeps=sc.substeps))
     step_fn.with_assembly = tr is not None
 
     def step():
@@ -250,7 +275,8 @@ def run_ours(args):
     from paper_2604_09993_b200.scenario import build_scaling
     from paper_2604_09993_b200.subproblem import SubproblemAssembler, SubproblemPattern, build_subproblem
 
-    sc = scp_problem(seed=rank)
+    fine = args.workload == "fine"
+    sc = scp_problem(seed=rank, fine=fine)
     gt = GpuTranscription(sc, device=dev.index)
     lay = gt.lay
     stream = torch.cuda.current_stream(dev)
@@ -350,7 +376,7 @@ def run_ours(args):
 
     K, W = args.steps, max(3, args.warmup)
     clocks = Clocks(dev.index if world == 1 else local)
-    if args.workload == "scp":
+    if args.workload in ("scp", "fine"):
         ms_tot, k1_ms, launches = timed(lambda rec: scp_step(z_dev, rec), K, W)
         units_per_step, B_k1 = n_int, n_int
     elif args.workload == "multistart":
@@ -372,8 +398,31 @@ def run_ours(args):
                                 "value": args.batch * nb / (bms * 1e-3), "unit": UNIT, "ms_per_step": bms / nb,
                                 "k1_ms": bk1}
 
+    if args.workload == "scp" and not args.no_fine_extra:
+        # configs[4]: HalfCheetah N=200, 8 substeps, one SCP iteration (K1 + K3 + assembly)
+        scf = scp_problem(seed=rank, fine=True)
+        gtf = GpuTranscription(scf, device=dev.index)
+        zf = torch.as_tensor(initial_guess(scf, gtf.disc, gtf.lay), device=dev)
+        asmf = SubproblemAssembler(SubproblemPattern(scf, gtf.lay, build_scaling(scf, gtf.lay)[0]), dev)
+
+        def fine_step(record=False):
+            if record:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                r = gtf.linearize_device(zf, delta, k1_events=(e0, e1))
+                k1_ev.append((e0, e1))
+            else:
+                r = gtf.linearize_device(zf, delta)
+            asmf.assemble_device(r, zf)
+
+        nf = max(5, K // 5)
+        fms, fk1, _ = timed(fine_step, nf, 3)
+        extra["fine_extra"] = {"workload": "HalfCheetah N=200, 8 RKF substeps, one SCP iteration (configs[4]; "
+                                           "the reference has no RK4)",
+                               "value": (scf.N - 1) * nf / (fms * 1e-3), "unit": UNIT, "ms_per_step": fms / nf,
+                               "k1_ms": fk1}
+
     # --- e2e through the public API with host (pinned) buffers
-    if args.workload == "scp":
+    if args.workload in ("scp", "fine"):
         # public API of one SCP iteration's pre-IPM work (= cito.scp.linearize_all +
         # build_subproblem, scp.py:412-413): host numpy z in, host scipy ConicProgram out
         from paper_2604_09993_b200.subproblem import GpuSCPStep
@@ -429,11 +478,12 @@ def run_ours(args):
     e2e_value = world * units_per_step * K / e2e_s
 
     peak = fp64_peak_tflops(torch, dev)
-    key = "halfcheetah_s5"
+    key = "halfcheetah_s8" if fine else "halfcheetah_s5"
     F, fdef = flops_per_interval(key)
     achieved = F * B_k1 / (k1_ms * 1e-3) / 1e12 if F else None
     roofline = {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": (achieved / peak) if achieved else None, "traffic": ncu_traffic(f"k_linearize_{args.workload}"),
+                "frac": (achieved / peak) if achieved else None,
+                "traffic": ncu_traffic(f"k_linearize_{'scp' if fine else args.workload}"),
                 "kernel": "k_linearize<Topo_halfcheetah_g2>", "kernel_ms": k1_ms, "intervals_per_launch": B_k1,
                 "flops_per_interval": F, "flops_definition": fdef,
                 "peak_source": "measured in this run: FP64 DFMA probe kernel (cito_dfma_peak); MEASURED_PEAKS.json "
@@ -454,7 +504,9 @@ def run_ours(args):
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic" if args.workload == "batch" else "synthetic (scenario initial guess, seed=rank)",
         "config": {"workload": {"scp": "scp: one SCP-iteration linearize of HalfCheetah N=30 (halfcheetah_bound.json, "
-                                       "5 RKF substeps, 29 intervals; K1+K3+K4)",
+                                       "5 RKF substeps, 29 intervals; K1+K3 + whole-subproblem assembly)",
+                                "fine": "fine: one SCP-iteration linearize of HalfCheetah N=200, 8 RKF substeps "
+                                        "(configs[4]; 199 intervals; K1+K3 + whole-subproblem assembly)",
                                 "batch": f"batch: {args.batch} independent synthetic HalfCheetah intervals per GPU "
                                          "(configs[2])",
                                 "multistart": f"multistart: {args.problems} HalfCheetah N=50 initial guesses per GPU "
@@ -478,11 +530,11 @@ def run_reference(args):
     rank, world, local = env_rank()
     if rank != 0:
         return
-    sc = scp_problem(seed=0)
-    if args.workload in ("scp", "multistart"):
+    sc = scp_problem(seed=0, fine=args.workload == "fine")
+    if args.workload in ("scp", "fine", "multistart"):
         step, po = cpu_step_fn(sc, 0)
-        sample = ("HalfCheetah N=30 initial-guess SCP iteration per step: oracle-port linearization (29 intervals "
-                  "+ node relations)" + (" + the reference's own build_subproblem/canonicalize (baseline/_ref)"
+        sample = (f"HalfCheetah N={sc.N} ({sc.substeps} substeps) initial-guess SCP iteration per step: oracle-port "
+                  f"linearization ({sc.N - 1} intervals + node relations)" + (" + the reference's own build_subproblem/canonicalize (baseline/_ref)"
                                          if step_fn.with_assembly else " (reference not installed: no assembly)"))
     else:
         B = max(8, min(args.batch, 256))

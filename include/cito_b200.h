@@ -146,6 +146,16 @@ cito_status cito_node_linearize_dev(cito_handle* h, int64_t Np, int64_t Nn, cons
                                     double* psi, double* psi_jac, double* theta, double* theta_jac,
                                     double* imp, double* imp_jac, void* stream);
 
+/* Pointwise audit of sampled states for verifier.replay_check
+ * (cito/verifier.py:257-272, 314-318): for each of B samples, x = the first n_x
+ * entries of row b of xs (row stride xstride >= n_x), u = us (B, n_u):
+ *   sds   (B, n_c)        contact signed distances (multibody.py:384-392)
+ *   cj    (B, 2 n_joints) joint anchor residuals   (multibody.py:324-336)
+ *   omega (B, n_y)        auxiliary rates Omega(x, u) (augmentation.py:134-153).
+ * Device buffers. */
+cito_status cito_audit_dev(cito_handle* h, int64_t B, const double* xs, int64_t xstride, const double* us,
+                           double* sds, double* cj, double* omega, void* stream);
+
 /* linearize_all (cito/scp.py:87-135) on a device-resident decision vector z
  * (layout cito/ocp.py:154-174: node states [xm_k, xp_k] at 2k n_xt / (2k+1) n_xt,
  * interval blocks [U_k, S_k] at base_u + k (2 n_u + 1), node impulses

@@ -66,6 +66,8 @@ def _load():
         L.cito_linearize_all_dev.argtypes = ([ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64,
                                               ctypes.c_int64, ctypes.c_int64, _dp, ctypes.c_double, ctypes.c_double]
                                              + [_dp] * 13)
+        L.cito_audit_dev.restype = ctypes.c_int
+        L.cito_audit_dev.argtypes = [ctypes.c_void_p, ctypes.c_int64, _dp, ctypes.c_int64] + [_dp] * 5
         L.cito_csc_assemble_dev.restype = ctypes.c_int
         L.cito_csc_assemble_dev.argtypes = [ctypes.c_int32] + [_dp] * 12
         L.cito_csc_assemble2_dev.restype = ctypes.c_int

@@ -18,7 +18,7 @@ SO = os.path.join(OUT_DIR, "libcito_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 SOURCES = ["cito_capi.cu"]
-DEPS = ["cito_capi.cu", "cito_kernels.cuh", "cito_node.cuh", "cito_scatter.cuh", "cito_bench.cuh", "cito_subproblem.cuh", "gen_models.py"]
+DEPS = ["cito_capi.cu", "cito_kernels.cuh", "cito_k1v2.cuh", "cito_node.cuh", "cito_scatter.cuh", "cito_bench.cuh", "cito_subproblem.cuh", "gen_models.py"]
 
 
 def _stale():

@@ -8,12 +8,14 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
 
 #include "../../include/cito_b200.h"
 #include "cito_kernels.cuh"
+#include "cito_k1v2.cuh"
 #include "cito_node.cuh"
 #include "cito_scatter.cuh"
 #include "cito_bench.cuh"
@@ -54,6 +56,8 @@ struct TopoOps {
                            cudaStream_t);
   cito_status (*node)(const KParams&, int64_t, int64_t, const double*, const double*, double, double, double*,
                       double*, double*, double*, double*, double*, cudaStream_t, ZSrc);
+  cito_status (*audit)(const KParams&, int64_t, const double*, int64_t, const double*, double*, double*, double*,
+                       cudaStream_t);
 };
 
 // Stream-ordered workspace (records of the primal trajectory): allocated from
@@ -75,28 +79,46 @@ cito_status ensure_pool() {
   return CITO_OK;
 }
 
+// Kernel generation of K1: 1 = k_linearize (cito_kernels.cuh, default),
+// 2 = k_linearize2 (short-primal-chain variant, cito_k1v2.cuh; CITO_K1=2).
+static int k1_version() {
+  static int v = [] {
+    const char* e = getenv("CITO_K1");
+    return (e && e[0] == '2') ? 2 : 1;
+  }();
+  return v;
+}
+
 template <class M>
 cito_status launch_linearize(const KParams& P, int64_t B, const double* xt0s, const double* Us, const double* Ss,
                              double* ends, double* jx, double* ju, double* js, int32_t* bad, cudaStream_t st,
                              ZSrc zs) {
   if (B <= 0) return CITO_OK;
-  const size_t smem = sizeof(FusedShared<M>);
   static bool attr_done = false;
+  const size_t smem1 = sizeof(FusedShared<M>), smem2 = sizeof(Fused2Shared<M>);
   if (!attr_done) {
-    CUDA_TRY(cudaFuncSetAttribute(k_linearize<M, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    CUDA_TRY(cudaFuncSetAttribute(k_linearize<M, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CUDA_TRY(cudaFuncSetAttribute(k_linearize<M, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1));
+    CUDA_TRY(cudaFuncSetAttribute(k_linearize<M, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1));
+    CUDA_TRY(cudaFuncSetAttribute(k_linearize2<M, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+    CUDA_TRY(cudaFuncSetAttribute(k_linearize2<M, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
     attr_done = true;
   }
   // latency variant (full register budget) while the grid fits the SMs once,
-  // occupancy variant (<= 3 CTAs/SM register budget) for large batches
+  // occupancy variant for large batches
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   count_launch();
-  if (B <= sms)
-    k_linearize<M, 1><<<(unsigned)B, FusedDims<M>::NT, smem, st>>>(P, B, xt0s, Us, Ss, ends, jx, ju, js, bad, zs);
-  else
-    k_linearize<M, 3><<<(unsigned)B, FusedDims<M>::NT, smem, st>>>(P, B, xt0s, Us, Ss, ends, jx, ju, js, bad, zs);
+  if (k1_version() == 2) {
+    if (B <= sms)
+      k_linearize2<M, 1><<<(unsigned)B, K2Dims<M>::NT, smem2, st>>>(P, B, xt0s, Us, Ss, ends, jx, ju, js, bad, zs);
+    else
+      k_linearize2<M, 2><<<(unsigned)B, K2Dims<M>::NT, smem2, st>>>(P, B, xt0s, Us, Ss, ends, jx, ju, js, bad, zs);
+  } else if (B <= sms) {
+    k_linearize<M, 1><<<(unsigned)B, FusedDims<M>::NT, smem1, st>>>(P, B, xt0s, Us, Ss, ends, jx, ju, js, bad, zs);
+  } else {
+    k_linearize<M, 3><<<(unsigned)B, FusedDims<M>::NT, smem1, st>>>(P, B, xt0s, Us, Ss, ends, jx, ju, js, bad, zs);
+  }
   CUDA_TRY(cudaGetLastError());
   return CITO_OK;
 }
@@ -127,7 +149,18 @@ cito_status launch_node(const KParams& P, int64_t Np, int64_t Nn, const double* 
   return CITO_OK;
 }
 
-#define CITO_TOPO_ENTRY(T, K) {K, launch_linearize<T>, launch_propagate<T>, launch_node<T>},
+template <class M>
+cito_status launch_audit(const KParams& P, int64_t B, const double* xs, int64_t xstride, const double* us,
+                         double* sds, double* cj, double* omega, cudaStream_t st) {
+  if (B <= 0) return CITO_OK;
+  const int nt = 64;
+  count_launch();
+  k_audit<M><<<(unsigned)((B + nt - 1) / nt), nt, 0, st>>>(P, B, xs, xstride, us, sds, cj, omega);
+  CUDA_TRY(cudaGetLastError());
+  return CITO_OK;
+}
+
+#define CITO_TOPO_ENTRY(T, K) {K, launch_linearize<T>, launch_propagate<T>, launch_node<T>, launch_audit<T>},
 const TopoOps kTopos[] = {CITO_FOR_EACH_TOPOLOGY(CITO_TOPO_ENTRY)};
 #undef CITO_TOPO_ENTRY
 
@@ -328,6 +361,15 @@ cito_status cito_node_linearize_dev(cito_handle* h, int64_t Np, int64_t Nn, cons
   cito_status st = h->ops->node(h->P, Np, Nn, y_pairs, theta_vecs, delta, epsilon, psi, psi_jac, theta, theta_jac,
                                 imp, imp_jac, (cudaStream_t)stream, ZSrc{});
   if (st == CITO_OK && Np + Nn > 0) __atomic_add_fetch(&h->launches, 1, __ATOMIC_RELAXED);
+  return st;
+}
+
+cito_status cito_audit_dev(cito_handle* h, int64_t B, const double* xs, int64_t xstride, const double* us,
+                           double* sds, double* cj, double* omega, void* stream) {
+  if (!h) return fail(CITO_ERR_ARG, "null handle");
+  if (B < 0 || xstride < h->dims.n_x) return fail(CITO_ERR_ARG, "audit: bad batch/stride");
+  cito_status st = h->ops->audit(h->P, B, xs, xstride, us, sds, cj, omega, (cudaStream_t)stream);
+  if (st == CITO_OK && B > 0) __atomic_add_fetch(&h->launches, 1, __ATOMIC_RELAXED);
   return st;
 }
 

@@ -1,0 +1,928 @@
+// cito_k1v2.cuh — K1 v2: the fused interval linearization with a short primal
+// critical chain (one CTA per interval, fp64, sm_100a).
+//
+// Same mathematics as k_linearize (cito_kernels.cuh; reference
+// cito.augmentation.Discretizer.linearize_batch, augmentation.py:180-242), but
+// the per-stage work is split so that only the dependent chain of the RK stage
+// recursion sits on the critical path:
+//
+//   warp 0        stage t   critical chain only: stage input (lanes own state
+//                           coordinates, stage slopes in registers), sin/cos and
+//                           FOH control (lane per link / control), then ONE lane
+//                           runs kinematics -> forces -> Gram -> straight-line
+//                           sparse Cholesky (generated per topology) -> joint
+//                           reactions -> vdot, all in registers.
+//   warp 1        stage t-1 everything off the chain: contact frames, signed
+//                           distances, Omega and path rows, the y accumulators,
+//                           the dS terms of the q-row stage inputs.
+//   warps 2,3,4   stage t-2 rate Jacobian, one warp per direction kind (q, v, u),
+//                           forward-mode tangents specialised per kind so the
+//                           structurally zero seed terms are never evaluated.
+//   warps 5..     stage t-3 tangent columns (one thread per column).
+//
+// A 4-slot ring of per-stage records in shared memory carries the stage from
+// role to role; one __syncthreads per tick.
+#pragma once
+
+#include "cito_kernels.cuh"
+
+// ---------------------------------------------------------------------------
+// Rate-Jacobian column of one input direction, specialised on the direction
+// kind (1: q, 2: v, 3: u): the derivative of prim_rate restricted to the seed
+// terms that kind can make nonzero (cito/contact_dynamics.py:86-108,
+// multibody.py:285-392, augmentation.py:100-153).  Same arithmetic as tan_rate
+// for the surviving terms.
+template <class M, int KIND>
+__device__ __forceinline__ void tan_rate_k(const KParams& P, const Prim<M>& pr, const double* v, int dir, double* out) {
+  constexpr int NL = M::NL, NJ = M::NJ, NC = M::NC, NA = M::NA, NQ = 3 * NL, NX = 2 * NQ;
+  constexpr bool HQ = KIND == 1, HV = KIND == 2, HU = KIND == 3;
+  (void)NL;
+#define SQ(k) ((dir) == (k) ? 1.0 : 0.0)
+#define SV(k) ((dir) == NQ + (k) ? 1.0 : 0.0)
+#define SU(m) ((dir) == NX + (m) ? 1.0 : 0.0)
+  double dW[NQ];
+#pragma unroll
+  for (int k = 0; k < NQ; ++k) dW[k] = 0.0;
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {
+    const int p = M::jparent(j), c = M::jchild(j), a = M::jact(j);
+    double dm = 0.0;
+    bool any = false;
+    if constexpr (HU) {
+      if (a >= 0) {
+        dm = SU(a);
+        any = true;
+      }
+    }
+    if constexpr (HQ) {
+      if (P.jspring[j]) {
+        const double dth_p = p >= 0 ? SQ(3 * p + 2) : 0.0;
+        dm = dm - P.jk[j] * (SQ(3 * c + 2) - dth_p);
+        any = true;
+      }
+    }
+    if constexpr (HV) {
+      if (P.jspring[j]) {
+        const double dom_p = p >= 0 ? SV(3 * p + 2) : 0.0;
+        dm = dm - P.jd[j] * (SV(3 * c + 2) - dom_p);
+        any = true;
+      }
+    }
+    if (any) {
+      dW[3 * c + 2] += dm;
+      if (p >= 0) dW[3 * p + 2] -= dm;
+    }
+  }
+  double dP[Pos<NC>::v][2], dn[Pos<NC>::v][2], dsd[Pos<NC>::v];
+#pragma unroll
+  for (int i = 0; i < NC; ++i) {
+    const int l = M::clink(i);
+    const double rx = pr.rr[i][0], rz = pr.rr[i][1];
+    dP[i][0] = dP[i][1] = dn[i][0] = dn[i][1] = dsd[i] = 0.0;
+    if constexpr (HQ) {
+      const double dth = SQ(3 * l + 2);
+      dP[i][0] = SQ(3 * l) + dth * (-rz);
+      dP[i][1] = SQ(3 * l + 1) + dth * rx;
+      if constexpr (M::IMPLICIT) {
+        const double Hd0 = pr.H[i][0] * dP[i][0] + pr.H[i][1] * dP[i][1];
+        const double Hd1 = pr.H[i][1] * dP[i][0] + pr.H[i][2] * dP[i][1];
+        const double gn = pr.gn[i], g0 = pr.g[i][0], g1 = pr.g[i][1];
+        const double gHd = g0 * Hd0 + g1 * Hd1;
+        const double ign3 = 1.0 / (gn * gn * gn);
+        dn[i][0] = Hd0 / gn - g0 * gHd * ign3;
+        dn[i][1] = Hd1 / gn - g1 * gHd * ign3;
+        dsd[i] = (g0 * dP[i][0] + g1 * dP[i][1]) / gn - pr.hv[i] * gHd * ign3;
+      } else {
+        dsd[i] = dP[i][1];
+      }
+      const double ft = pr.u[NA + 2 * i], fn = pr.u[NA + 2 * i + 1];
+      double dF0 = 0.0, dF1 = 0.0;
+      if constexpr (M::IMPLICIT) {
+        const double dt0 = dn[i][1], dt1 = -dn[i][0];
+        dF0 = dt0 * ft + dn[i][0] * fn;
+        dF1 = dt1 * ft + dn[i][1] * fn;
+        dW[3 * l] += dF0;
+        dW[3 * l + 1] += dF1;
+      }
+      dW[3 * l + 2] += -dth * (rx * pr.F[i][0] + rz * pr.F[i][1]) + (-rz) * dF0 + rx * dF1;
+    }
+    if constexpr (HU) {
+      const double dft = SU(NA + 2 * i), dfn = SU(NA + 2 * i + 1);
+      const double dF0 = pr.t[i][0] * dft + pr.n[i][0] * dfn;
+      const double dF1 = pr.t[i][1] * dft + pr.n[i][1] * dfn;
+      dW[3 * l] += dF0;
+      dW[3 * l + 1] += dF1;
+      dW[3 * l + 2] += (-rz) * dF0 + rx * dF1;
+    }
+  }
+  if constexpr (NJ == 0) {
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+      out[3 * l] = P.minv_m[l] * dW[3 * l];
+      out[3 * l + 1] = P.minv_m[l] * dW[3 * l + 1];
+      out[3 * l + 2] = P.minv_I[l] * dW[3 * l + 2];
+    }
+  } else {
+    constexpr int NJ2 = 2 * NJ;
+    if constexpr (HQ) {  // g = dW + dJ^T lam (theta coordinates only)
+#pragma unroll
+      for (int j = 0; j < NJ; ++j)
+#pragma unroll
+        for (int sa = 0; sa < 2; ++sa) {
+          const int l = sa == 0 ? M::jparent(j) : M::jchild(j);
+          if (l < 0) continue;
+          const double sgn = sa == 0 ? 1.0 : -1.0;
+          const double* R = sa == 0 ? pr.rp[j] : pr.rc[j];
+          dW[3 * l + 2] += sgn * (-SQ(3 * l + 2)) * (R[0] * pr.lam[2 * j] + R[1] * pr.lam[2 * j + 1]);
+        }
+    }
+    // rhs' = dJ vdot + J M^-1 g + dcurv, directly in elimination order
+    double zp[NJ2];
+#pragma unroll
+    for (int a = 0; a < NJ; ++a) {
+      const int j = M::jperm(a);
+#pragma unroll
+      for (int al = 0; al < 2; ++al) {
+        double acc = 0.0;
+#pragma unroll
+        for (int sa = 0; sa < 2; ++sa) {
+          const int l = sa == 0 ? M::jparent(j) : M::jchild(j);
+          if (l < 0) continue;
+          const double sgn = sa == 0 ? 1.0 : -1.0;
+          const double* R = sa == 0 ? pr.rp[j] : pr.rc[j];
+          const double dPa = al == 0 ? -R[1] : R[0];
+          const double w = v[3 * l + 2];
+          double term = P.minv_m[l] * dW[3 * l + al] + dPa * P.minv_I[l] * dW[3 * l + 2];
+          if constexpr (HQ) {
+            const double dth = SQ(3 * l + 2);
+            term = -dth * R[al] * pr.vdot[3 * l + 2] + term - dth * dPa * w * w;
+          }
+          if constexpr (HV) term = term - 2.0 * R[al] * w * SV(3 * l + 2);
+          acc += sgn * term;
+        }
+        zp[2 * a + al] = acc;
+      }
+    }
+    M::tri_solve(pr.L, pr.Li, zp);  // generated straight-line sparse solves (gen_models.py)
+    // dvdot = M^-1 (g + J^T dlam), dlam = -z (joint order)
+#pragma unroll
+    for (int a = 0; a < NJ; ++a) {
+      const int j = M::jperm(a);
+#pragma unroll
+      for (int sa = 0; sa < 2; ++sa) {
+        const int l = sa == 0 ? M::jparent(j) : M::jchild(j);
+        if (l < 0) continue;
+        const double sgn = sa == 0 ? 1.0 : -1.0;
+        const double* R = sa == 0 ? pr.rp[j] : pr.rc[j];
+        const double l0 = -zp[2 * a], l1 = -zp[2 * a + 1];
+        dW[3 * l] += sgn * l0;
+        dW[3 * l + 1] += sgn * l1;
+        dW[3 * l + 2] += sgn * ((-R[1]) * l0 + R[0] * l1);
+      }
+    }
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+      out[3 * l] = P.minv_m[l] * dW[3 * l];
+      out[3 * l + 1] = P.minv_m[l] * dW[3 * l + 1];
+      out[3 * l + 2] = P.minv_I[l] * dW[3 * l + 2];
+    }
+  }
+  // d Omega (aux_rate, augmentation.py:134-153)
+  double* dy = out + NQ;
+#pragma unroll
+  for (int i = 0; i < NC; ++i) {
+    const int l = M::clink(i);
+    const double ft = pr.u[NA + 2 * i], fn = pr.u[NA + 2 * i + 1], gam = pr.u[NA + 2 * NC + i];
+    const double rx = pr.rr[i][0], rz = pr.rr[i][1];
+    const double w = v[3 * l + 2];
+    double dvt = 0.0, dlamc = 0.0;
+    if constexpr (HQ) {
+      const double dth = SQ(3 * l + 2);
+      const double dJv0 = -dth * rx * w, dJv1 = -dth * rz * w;
+      dvt = (dn[i][1]) * pr.Jv[i][0] + (-dn[i][0]) * pr.Jv[i][1] + pr.t[i][0] * dJv0 + pr.t[i][1] * dJv1;
+      dlamc = dvt;
+    }
+    if constexpr (HV) {
+      const double dw = SV(3 * l + 2);
+      const double dJv0 = SV(3 * l) + (-rz) * dw, dJv1 = SV(3 * l + 1) + rx * dw;
+      dvt = pr.t[i][0] * dJv0 + pr.t[i][1] * dJv1;
+      dlamc = dvt;
+    }
+    if constexpr (HU) {
+      const double dft = SU(NA + 2 * i), dgam = SU(NA + 2 * NC + i);
+      const double q1 = ft * ft + 1.0;
+      const double dsg = dft / (q1 * sqrt(q1));
+      dlamc = dgam * pr.sg[i] + gam * dsg;
+    }
+    dy[5 * i + 0] = HU ? SU(NA + 2 * i + 1) : 0.0;
+    dy[5 * i + 1] = sabs_d(pr.lamc[i]) * dlamc;
+    dy[5 * i + 2] = HU ? SU(NA + 2 * NC + i) : 0.0;
+    if constexpr (HU) {
+      const double dft = SU(NA + 2 * i), dfn = SU(NA + 2 * i + 1);
+      dy[5 * i + 3] = sabs_d(P.mu[i] * fn) * P.mu[i] * dfn - pr.sg[i] * dft;
+    } else {
+      dy[5 * i + 3] = 0.0;
+    }
+    dy[5 * i + 4] = HQ ? srelu_d(pr.sd[i]) * dsd[i] : 0.0;
+  }
+  if constexpr (M::NGO > 0) {
+    constexpr int NG = Prim<M>::NG;
+    if constexpr (HQ) {
+      double dg[Pos<NG>::v];
+      int r = 0;
+#pragma unroll
+      for (int i = 0; i < NC; ++i) dg[r++] = -dsd[i];
+#pragma unroll
+      for (int k = 0; k < M::NJL; ++k) {
+        const int jj = M::jl_joint(k);
+        const int p = M::jparent(jj), c = M::jchild(jj);
+        const double drel = SQ(3 * c + 2) - (p >= 0 ? SQ(3 * p + 2) : 0.0);
+        dg[r++] = drel;
+        dg[r++] = -drel;
+      }
+#pragma unroll
+      for (int k = 0; k < M::NHB; ++k) {
+        const double dpz = SQ(3 * M::hb_link(k) + 1);
+        dg[r++] = -dpz;
+        dg[r++] = dpz;
+      }
+#pragma unroll
+      for (int jg = 0; jg < NG; ++jg) dg[jg] *= srelu_d(pr.gp[jg]);
+#pragma unroll
+      for (int o = 0; o < M::NGO; ++o) {
+        double acc = 0.0;
+#pragma unroll
+        for (int jg = 0; jg < NG; ++jg) acc += P.mix[o][jg] * dg[jg];
+        dy[5 * NC + o] = acc;
+      }
+    } else {
+#pragma unroll
+      for (int o = 0; o < M::NGO; ++o) dy[5 * NC + o] = 0.0;
+    }
+  }
+#undef SQ
+#undef SV
+#undef SU
+}
+
+// ---------------------------------------------------------------------------
+template <class M>
+struct Rec2 {
+  Prim<M> pr;
+  double xs[Dims<M>::NX];  // stage input (q, v)
+  double r[Dims<M>::NR];   // unscaled rate rows: vdot (NQ), Omega (NY)
+  double wq[3 * M::NL];    // sum_j h a_ij v_{s,j}: dS term of the q-row stage inputs
+};
+
+template <class M>
+struct K2Dims {
+  using D = Dims<M>;
+  static constexpr int NCW = (D::NCOL + 31) / 32;
+  static constexpr int NT = 32 * (5 + NCW);
+  static constexpr int NX = D::NX;
+  static constexpr int PER = (NX + 31) / 32;  // state coordinates per lane of warp 0
+  static constexpr int count_q() {
+    int n = 0;
+    for (int i = 0; i < M::NDIRX; ++i) n += M::dir(i) < 3 * M::NL ? 1 : 0;
+    return n;
+  }
+  static constexpr int NDIRQ = count_q();
+};
+
+template <class M>
+struct AuxScratch {
+  static constexpr int NG = Prim<M>::NG;
+  double sgv[Pos<NG>::v];
+};
+
+template <class M>
+struct Fused2Shared {
+  using D = Dims<M>;
+  Rec2<M> ring[4];
+  SParams<M> sp;
+  AuxScratch<M> ax;
+  double At[2][D::NDIR][D::NRP];
+  double KV[5][D::NH][D::NCOLP];
+  double PQ[Pos<M::NPUSH>::v][D::NCOLP];
+  double PV[Pos<M::NPUSH>::v][D::NCOLP];
+  double DY[Pos<D::NY>::v][D::NCOLP];
+  double x[D::NXT];
+  double vbs[2][D::NQ];
+  double U[2 * D::NU + 1];
+  double S;
+  int bad;
+};
+
+// Lane-0 critical chain of one rate evaluation: forces, Gram matrix, sparse
+// Cholesky (generated straight-line code, M::chol_solve), joint reactions,
+// vdot (cito/contact_dynamics.py:86-108, multibody.py:259-321).  Reads the
+// stage input, cos/sin and FOH control of the record; writes the factor, the
+// reactions and vdot (pr.vdot and the vdot rows of r).
+template <class M>
+__device__ __forceinline__ void crit_chain(const KParams& P, Rec2<M>& R) {
+  using D = Dims<M>;
+  constexpr int NL = M::NL, NJ = M::NJ, NC = M::NC, NA = M::NA, NQ = D::NQ;
+  Prim<M>& pr = R.pr;
+  const double* q = R.xs;
+  const double* v = R.xs + NQ;
+  double cl[NL], sl[NL];
+#pragma unroll
+  for (int l = 0; l < NL; ++l) {
+    cl[l] = pr.c[l];
+    sl[l] = pr.s[l];
+  }
+  double W[NQ];
+#pragma unroll
+  for (int k = 0; k < NQ; ++k) W[k] = 0.0;
+#pragma unroll
+  for (int l = 0; l < NL; ++l) W[3 * l + 1] += P.neg_mg[l];
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {
+    const int p = M::jparent(j), c = M::jchild(j), a = M::jact(j);
+    double mo = 0.0;
+    if (a >= 0) mo = mo + pr.u[a];
+    if (P.jspring[j]) {
+      const double th_p = p >= 0 ? q[3 * p + 2] : 0.0;
+      const double om_p = p >= 0 ? v[3 * p + 2] : 0.0;
+      const double rel = q[3 * c + 2] - th_p - P.jrest[j];
+      mo = mo - P.jk[j] * rel - P.jd[j] * (v[3 * c + 2] - om_p);
+    }
+    W[3 * c + 2] += mo;
+    if (p >= 0) W[3 * p + 2] += -mo;
+  }
+#pragma unroll
+  for (int i = 0; i < NC; ++i) {
+    const int l = M::clink(i);
+    const double rx = cl[l] * P.cr[i][0] - sl[l] * P.cr[i][1];
+    const double rz = sl[l] * P.cr[i][0] + cl[l] * P.cr[i][1];
+    double n0, n1;
+    if constexpr (M::IMPLICIT) {
+      const T2 t2 = surface_t2(P, q[3 * l] + rx, q[3 * l + 1] + rz);
+      const double gn = sqrt(t2.gx * t2.gx + t2.gz * t2.gz);
+      n0 = t2.gx / gn;
+      n1 = t2.gz / gn;
+    } else {
+      n0 = 0.0;
+      n1 = 1.0;
+    }
+    const double t0 = n1, t1 = -n0;
+    const double ft = pr.u[NA + 2 * i], fn = pr.u[NA + 2 * i + 1];
+    const double F0 = t0 * ft + n0 * fn, F1 = t1 * ft + n1 * fn;
+    W[3 * l] += F0;
+    W[3 * l + 1] += F1;
+    W[3 * l + 2] += (-rz) * F0 + rx * F1;
+  }
+  double* vdot = R.r;
+  if constexpr (NJ == 0) {
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+      vdot[3 * l] = P.minv_m[l] * W[3 * l];
+      vdot[3 * l + 1] = P.minv_m[l] * W[3 * l + 1];
+      const double vd2 = P.minv_I[l] * W[3 * l + 2];
+      vdot[3 * l + 2] = vd2;
+      pr.vdot[3 * l + 2] = vd2;
+    }
+  } else {
+    constexpr int NJ2 = 2 * NJ;
+    double Rj[NJ][2][2];
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      const int p = M::jparent(j), c = M::jchild(j);
+      if (p >= 0) {
+        Rj[j][0][0] = cl[p] * P.jrp[j][0] - sl[p] * P.jrp[j][1];
+        Rj[j][0][1] = sl[p] * P.jrp[j][0] + cl[p] * P.jrp[j][1];
+      } else {
+        Rj[j][0][0] = Rj[j][0][1] = 0.0;
+      }
+      Rj[j][1][0] = cl[c] * P.jrc[j][0] - sl[c] * P.jrc[j][1];
+      Rj[j][1][1] = sl[c] * P.jrc[j][0] + cl[c] * P.jrc[j][1];
+    }
+    double Lr[NJ2 * (NJ2 + 1) / 2];
+#pragma unroll
+    for (int a = 0; a < NJ; ++a)
+#pragma unroll
+      for (int bp = 0; bp <= a; ++bp) {
+        if (!M::lnzb(a, bp)) continue;
+        const int j = M::jperm(a), k = M::jperm(bp);
+        double g00 = 0.0, g01 = 0.0, g10 = 0.0, g11 = 0.0;
+#pragma unroll
+        for (int sa = 0; sa < 2; ++sa)
+#pragma unroll
+          for (int sb = 0; sb < 2; ++sb) {
+            const int la = sa == 0 ? M::jparent(j) : M::jchild(j);
+            const int lb = sb == 0 ? M::jparent(k) : M::jchild(k);
+            if (la < 0 || la != lb) continue;
+            const double sg = (sa == sb) ? 1.0 : -1.0;
+            const double dA0 = -Rj[j][sa][1], dA1 = Rj[j][sa][0], dB0 = -Rj[k][sb][1], dB1 = Rj[k][sb][0];
+            const double mI = P.minv_I[la], mm = P.minv_m[la];
+            g00 += sg * (dA0 * dB0 * mI + mm);
+            g01 += sg * (dA0 * dB1 * mI);
+            g10 += sg * (dA1 * dB0 * mI);
+            g11 += sg * (dA1 * dB1 * mI + mm);
+          }
+        Lr[LI(2 * a, 2 * bp)] = g00;
+        Lr[LI(2 * a + 1, 2 * bp)] = g10;
+        Lr[LI(2 * a + 1, 2 * bp + 1)] = g11;
+        if (a != bp) Lr[LI(2 * a, 2 * bp + 1)] = g01;
+      }
+    double y[NJ2];
+#pragma unroll
+    for (int a = 0; a < NJ; ++a) {
+      const int j = M::jperm(a);
+#pragma unroll
+      for (int al = 0; al < 2; ++al) {
+        double acc = 0.0;
+#pragma unroll
+        for (int sa = 0; sa < 2; ++sa) {
+          const int l = sa == 0 ? M::jparent(j) : M::jchild(j);
+          if (l < 0) continue;
+          const double sgn = sa == 0 ? 1.0 : -1.0;
+          const double dP = al == 0 ? -Rj[j][sa][1] : Rj[j][sa][0];
+          const double om = v[3 * l + 2];
+          acc += sgn * (P.minv_m[l] * W[3 * l + al] + dP * P.minv_I[l] * W[3 * l + 2] - Rj[j][sa][al] * om * om);
+        }
+        y[2 * a + al] = acc;
+      }
+    }
+    double Lir[NJ2];
+    M::chol_solve(Lr, y, Lir);
+#pragma unroll
+    for (int r = 0; r < NJ2; ++r) {
+      pr.Li[r] = Lir[r];
+#pragma unroll
+      for (int c = 0; c <= r; ++c)
+        if (M::lnzb(r / 2, c / 2)) pr.L[LI(r, c)] = Lr[LI(r, c)];
+    }
+#pragma unroll
+    for (int a = 0; a < NJ; ++a) {
+      const int j = M::jperm(a);
+      const double l0 = -y[2 * a], l1 = -y[2 * a + 1];
+      pr.lam[2 * j] = l0;
+      pr.lam[2 * j + 1] = l1;
+#pragma unroll
+      for (int sa = 0; sa < 2; ++sa) {
+        const int l = sa == 0 ? M::jparent(j) : M::jchild(j);
+        if (l < 0) continue;
+        const double sgn = sa == 0 ? 1.0 : -1.0;
+        W[3 * l] += sgn * l0;
+        W[3 * l + 1] += sgn * l1;
+        W[3 * l + 2] += sgn * ((-Rj[j][sa][1]) * l0 + Rj[j][sa][0] * l1);
+      }
+    }
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+      vdot[3 * l] = P.minv_m[l] * W[3 * l];
+      vdot[3 * l + 1] = P.minv_m[l] * W[3 * l + 1];
+      const double vd2 = P.minv_I[l] * W[3 * l + 2];
+      vdot[3 * l + 2] = vd2;
+      pr.vdot[3 * l + 2] = vd2;
+    }
+  }
+}
+
+// Warp 1: everything of stage `a` that is off the critical chain.
+template <class M>
+__device__ __forceinline__ void aux_stage(const KParams& P, Fused2Shared<M>& sh, int a, int lane, double (&VS)[6],
+                                          double& ky, double& yv) {
+  using D = Dims<M>;
+  constexpr int NL = M::NL, NJ = M::NJ, NC = M::NC, NA = M::NA, NQ = D::NQ, NY = D::NY;
+  const int s = a / 6, i = a % 6;
+  Rec2<M>& R = sh.ring[a & 3];
+  Prim<M>& pr = R.pr;
+  const SParams<M>& Q = sh.sp;
+  const double* q = R.xs;
+  const double* v = R.xs + NQ;
+  const double S = sh.S, h = P.h;
+  (void)NL;
+  // 1: rotated joint anchors (per joint side), contact frames / forces / Omega (per contact)
+  for (int e = lane; e < 2 * NJ + NC; e += 32) {
+    if (e < 2 * NJ) {
+      const int j = e >> 1, side = e & 1;
+      const int l = side ? Q.jc[j] : Q.jp[j];
+      if (l >= 0) {
+        const double ax = side ? Q.jrc[j][0] : Q.jrp[j][0], az = side ? Q.jrc[j][1] : Q.jrp[j][1];
+        const double c = pr.c[l], sn = pr.s[l];
+        double* Rj = side ? pr.rc[j] : pr.rp[j];
+        Rj[0] = c * ax - sn * az;
+        Rj[1] = sn * ax + c * az;
+      }
+    } else {
+      const int ci = e - 2 * NJ, l = Q.cl[ci];
+      const double c = pr.c[l], sn = pr.s[l];
+      const double rx = c * Q.cr[ci][0] - sn * Q.cr[ci][1];
+      const double rz = sn * Q.cr[ci][0] + c * Q.cr[ci][1];
+      pr.rr[ci][0] = rx;
+      pr.rr[ci][1] = rz;
+      const double Px = q[3 * l] + rx, Pz = q[3 * l + 1] + rz;
+      double n0, n1, sd;
+      if constexpr (M::IMPLICIT) {
+        T2 t2 = surface_t2(P, Px, Pz);
+        pr.hv[ci] = t2.v;
+        pr.g[ci][0] = t2.gx;
+        pr.g[ci][1] = t2.gz;
+        pr.H[ci][0] = t2.hxx;
+        pr.H[ci][1] = t2.hxz;
+        pr.H[ci][2] = t2.hzz;
+        const double gn = sqrt(t2.gx * t2.gx + t2.gz * t2.gz);
+        pr.gn[ci] = gn;
+        n0 = t2.gx / gn;
+        n1 = t2.gz / gn;
+        sd = t2.v / gn;
+      } else {
+        n0 = 0.0;
+        n1 = 1.0;
+        sd = Pz - P.height;
+      }
+      pr.sd[ci] = sd;
+      const double t0 = n1, t1 = -n0;
+      pr.n[ci][0] = n0;
+      pr.n[ci][1] = n1;
+      pr.t[ci][0] = t0;
+      pr.t[ci][1] = t1;
+      const double ft = pr.u[NA + 2 * ci], fn = pr.u[NA + 2 * ci + 1], gam = pr.u[NA + 2 * NC + ci];
+      pr.F[ci][0] = t0 * ft + n0 * fn;
+      pr.F[ci][1] = t1 * ft + n1 * fn;
+      const double om = v[3 * l + 2];
+      const double Jv0 = v[3 * l] + (-rz) * om, Jv1 = v[3 * l + 1] + rx * om;
+      pr.Jv[ci][0] = Jv0;
+      pr.Jv[ci][1] = Jv1;
+      const double sgt = ft / sqrt(ft * ft + 1.0);  // friction_stationarity (contact_dynamics.py:55-66)
+      pr.sg[ci] = sgt;
+      const double lamc = t0 * Jv0 + t1 * Jv1 + gam * sgt;
+      pr.lamc[ci] = lamc;
+      double* yo = R.r + NQ + 5 * ci;  // aux_rate rows (augmentation.py:134-153)
+      yo[0] = fn;
+      yo[1] = sabs(lamc);
+      yo[2] = gam;
+      yo[3] = sabs(Q.mu[ci] * fn) - sabs(ft);
+      yo[4] = srelu(sd);
+    }
+  }
+  __syncwarp();
+  if constexpr (M::NGO > 0) {  // path rows g(x, u) (augmentation.py:112-129) and their mixing
+    constexpr int NG = Prim<M>::NG;
+    if (lane == 0) {
+      double gpl[Pos<NG>::v];
+      int r = 0;
+#pragma unroll
+      for (int ci = 0; ci < NC; ++ci) gpl[r++] = -pr.sd[ci];
+#pragma unroll
+      for (int k = 0; k < M::NJL; ++k) {
+        const int jj = M::jl_joint(k);
+        const int p = M::jparent(jj), c = M::jchild(jj);
+        const double rel = q[3 * c + 2] - (p >= 0 ? q[3 * p + 2] : 0.0);
+        gpl[r++] = rel - P.jl_hi[k];
+        gpl[r++] = P.jl_lo[k] - rel;
+      }
+#pragma unroll
+      for (int k = 0; k < M::NHB; ++k) {
+        const double pz = q[3 * M::hb_link(k) + 1];
+        gpl[r++] = P.hb_lo[k] - pz;
+        gpl[r++] = pz - P.hb_hi[k];
+      }
+      double sgv[Pos<NG>::v];
+#pragma unroll
+      for (int jg = 0; jg < NG; ++jg) {
+        pr.gp[jg] = gpl[jg];
+        sgv[jg] = srelu(gpl[jg]);
+      }
+#pragma unroll
+      for (int o = 0; o < M::NGO; ++o) {
+        double acc = 0.0;
+#pragma unroll
+        for (int jg = 0; jg < NG; ++jg) acc += P.mix[o][jg] * sgv[jg];
+        R.r[NQ + 5 * NC + o] = acc;
+      }
+    }
+    __syncwarp();
+  }
+  // 2: y accumulators (augmentation.py:206-209), dS terms of the q-row stage inputs
+  if (lane < NY) {
+    ky = (i == 0 ? 0.0 : ky) + P.b[i] * (S * R.r[NQ + lane]);
+    if (i == 5) yv = yv + h * ky;
+  }
+  if (lane < NQ) {
+    const double vsk = v[lane];
+    double ws = 0.0;
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+      if (j == i) VS[j] = vsk;
+      if (j < i) ws += P.ha[i][j] * VS[j];
+    }
+    if (i == 5) VS[5] = vsk;
+    R.wq[lane] = ws;
+    if (i == 5) {
+      double w2 = 0.0;
+#pragma unroll
+      for (int j = 0; j < 6; ++j) w2 += P.b[j] * VS[j];
+      sh.vbs[s & 1][lane] = h * w2;
+    }
+  }
+}
+
+// One tangent column through RK stage I (record R, rate Jacobian At).
+template <class M>
+__device__ __forceinline__ void col_stage2(const KParams& P, Fused2Shared<M>& sh, const Rec2<M>& R,
+                                           const double (*At)[Dims<M>::NRP], int s, const int I, int col, double S,
+                                           double dS, bool isU, int um, bool uplus, double (&hq)[Pos<M::NHIST>::v],
+                                           double (&hv)[Pos<M::NHIST>::v]) {
+  using D = Dims<M>;
+  constexpr int NQ = D::NQ, NR = D::NR, NDIRX = M::NDIRX;
+  const double h = P.h;
+  const double tau = h * (double)s + P.ch[I];
+  const double hb = h * P.b[I];
+  if (I == 0) {
+#pragma unroll
+    for (int p = 0; p < M::NPUSH; ++p) sh.PQ[p][col] += P.he1 * S * sh.PV[p][col];
+  }
+  double vals[Pos<NDIRX>::v];
+#pragma unroll
+  for (int kd = 0; kd < NDIRX; ++kd) {
+    const int d = M::dir(kd);
+    double val;
+    if (d < NQ) {
+      const int hs = M::hslot(d);
+      val = hq[hs] + S * P.hc1[I] * hv[hs] + dS * R.wq[d];
+#pragma unroll
+      for (int l = 0; l < 5; ++l)
+        if (l < I) val += S * P.cq[I][l] * sh.KV[l][hs][col];
+    } else {
+      const int hs = M::hslot(d - NQ);
+      val = hv[hs];
+#pragma unroll
+      for (int l = 0; l < 5; ++l)
+        if (l < I) val += P.ha[I][l] * sh.KV[l][hs][col];
+    }
+    vals[kd] = val;
+  }
+  const double coef = uplus ? tau : (1.0 - tau);
+  double accs[NR];
+  if (isU) {
+    const double* Au = At[NDIRX + um];
+#pragma unroll
+    for (int rr = 0; rr < NR; ++rr) accs[rr] = Au[rr] * coef;
+  } else {
+#pragma unroll
+    for (int rr = 0; rr < NR; ++rr) accs[rr] = 0.0;
+  }
+#pragma unroll
+  for (int kd = 0; kd < NDIRX; ++kd) {
+    const double vk = vals[kd];
+#pragma unroll
+    for (int rr = 0; rr < NR; ++rr)
+      if (M::adep(rr, kd)) accs[rr] += At[kd][rr] * vk;
+  }
+#pragma unroll
+  for (int rr = 0; rr < NR; ++rr) {
+    const double dk = S * accs[rr] + dS * R.r[rr];
+    if (rr < NQ) {
+      const int hs = M::hslot(rr);
+      if (hs >= 0) {
+        if (I < 5) {
+          sh.KV[I][hs][col] = dk;
+        } else {
+          double incv = P.b[5] * dk, incq = 0.0;
+#pragma unroll
+          for (int l = 0; l < 5; ++l) {
+            const double kv = sh.KV[l][hs][col];
+            incv += P.b[l] * kv;
+            incq += P.e2[l] * kv;
+          }
+          hq[hs] = hq[hs] + P.he1 * S * hv[hs] + S * incq + dS * sh.vbs[s & 1][rr];
+          hv[hs] = hv[hs] + h * incv;
+        }
+      } else {
+        const int p = M::pslot(rr);
+        sh.PV[p][col] += hb * dk;
+        sh.PQ[p][col] += S * P.e2[I] * dk + dS * hb * R.xs[NQ + rr];
+      }
+    } else {
+      sh.DY[rr - NQ][col] += hb * dk;
+    }
+  }
+}
+
+template <class M, int MINB>
+__global__ void __launch_bounds__(K2Dims<M>::NT, MINB) k_linearize2(const KParams P, int64_t B,
+                                                                    const double* __restrict__ xt0s,
+                                                                    const double* __restrict__ Us,
+                                                                    const double* __restrict__ Ss,
+                                                                    double* __restrict__ ends, double* __restrict__ jx,
+                                                                    double* __restrict__ ju, double* __restrict__ js,
+                                                                    int32_t* __restrict__ bad, const ZSrc zs) {
+  using D = Dims<M>;
+  using K = K2Dims<M>;
+  constexpr int NQ = D::NQ, NX = D::NX, NU = D::NU, NY = D::NY, NXT = D::NXT, NCOL = D::NCOL;
+  constexpr int NDIRX = M::NDIRX, NDIR = D::NDIR, NHIST = M::NHIST, PER = K::PER, NDIRQ = K::NDIRQ;
+  static_assert(NQ <= 32 && NY <= 32, "aux warp owns one q coordinate and one y row per lane");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Fused2Shared<M>& sh = *reinterpret_cast<Fused2Shared<M>*>(smem_raw);
+  const int64_t b = blockIdx.x;
+  if (b >= B) return;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t zp = zs.z ? b / zs.n_int : 0, zk = zs.z ? b % zs.n_int : 0;
+  const double* zb = zs.z ? zs.z + zp * zs.zstride : nullptr;
+  const double* src_x = zs.z ? zb + (2 * zk + 1) * NXT : xt0s + b * NXT;
+  const double* src_U = zs.z ? zb + zs.base_u + zk * (2 * NU + 1) : Us + b * 2 * NU;
+  for (int k = tid; k < 2 * NU; k += blockDim.x) sh.U[k] = src_U[k];
+  if (tid == 0) {
+    sh.S = zs.z ? src_U[2 * NU] : Ss[b];
+    sh.bad = 0;
+  }
+  for (int j = tid; j < M::NJ; j += blockDim.x) {
+    sh.sp.jrp[j][0] = P.jrp[j][0];
+    sh.sp.jrp[j][1] = P.jrp[j][1];
+    sh.sp.jrc[j][0] = P.jrc[j][0];
+    sh.sp.jrc[j][1] = P.jrc[j][1];
+    sh.sp.jp[j] = M::jparent(j);
+    sh.sp.jc[j] = M::jchild(j);
+  }
+  for (int c = tid; c < M::NC; c += blockDim.x) {
+    sh.sp.cr[c][0] = P.cr[c][0];
+    sh.sp.cr[c][1] = P.cr[c][1];
+    sh.sp.mu[c] = P.mu[c];
+    sh.sp.cl[c] = M::clink(c);
+  }
+  // warp 0: state coordinates (lane + 32 p) and their stage slopes in registers
+  double xr[PER], Kr[6][PER];
+  if (warp == 0) {
+#pragma unroll
+    for (int p = 0; p < PER; ++p) {
+      const int k = lane + 32 * p;
+      xr[p] = k < NX ? src_x[k] : 0.0;
+    }
+  }
+  // warp 1: y row `lane` and the stage velocities of q coordinate `lane`
+  double yv = 0.0, ky = 0.0, VS[6];
+  if (warp == 1 && lane < NY) yv = src_x[NX + lane];
+  // column threads
+  const int col = tid - 32 * 5;
+  const bool colthr = warp >= 5 && col < NCOL;
+  const double dS = (col == NCOL - 1) ? 1.0 : 0.0;
+  const int sc = (col >= 0 && col < M::NHCOL) ? M::hcol(col) : -1;
+  const int uj = col - M::NHCOL;
+  const bool isU = (uj >= 0) && (uj < 2 * NU);
+  const int um = isU ? (uj % Pos<NU>::v) : 0;
+  const bool uplus = isU && (uj >= NU);
+  double hq[Pos<NHIST>::v], hv[Pos<NHIST>::v];
+  if (colthr) {
+#pragma unroll
+    for (int c = 0; c < NQ; ++c) {
+      const double e_q = (sc == c) ? 1.0 : 0.0, e_v = (sc == NQ + c) ? 1.0 : 0.0;
+      if (M::hslot(c) >= 0) {
+        hq[M::hslot(c)] = e_q;
+        hv[M::hslot(c)] = e_v;
+      } else {
+        sh.PQ[M::pslot(c)][col] = e_q;
+        sh.PV[M::pslot(c)][col] = e_v;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < NY; ++k) sh.DY[k][col] = 0.0;
+  }
+  __syncthreads();
+  const double S = sh.S, h = P.h;
+  const int NST = 6 * P.substeps;
+  for (int t = 0; t < NST + 3; ++t) {
+    CITO_MARK((t * 8 + (warp < 8 ? warp : 7)) * 2);
+    if (warp == 0) {
+      if (t < NST) {
+        const int s = t / 6, i = t % 6;
+        Rec2<M>& R = sh.ring[t & 3];
+        // stage input (augmentation.py:200-205), coordinates owned by this lane
+#pragma unroll
+        for (int p = 0; p < PER; ++p) {
+          const int k = lane + 32 * p;
+          double a = xr[p];
+#pragma unroll
+          for (int j = 0; j < 5; ++j)
+            if (j < i) a = a + P.ha[i][j] * Kr[j][p];
+          if (k < NX) R.xs[k] = a;
+        }
+        __syncwarp();
+        const double tau = h * (double)s + P.ch[i];
+        for (int e = lane; e < M::NL + NU; e += 32) {
+          if (e < M::NL) {
+            double sv, cv;
+            sincos(R.xs[3 * e + 2], &sv, &cv);
+            R.pr.s[e] = sv;
+            R.pr.c[e] = cv;
+          } else {
+            const int m = e - M::NL;
+            R.pr.u[m] = (1.0 - tau) * sh.U[m] + tau * sh.U[NU + m];  // foh_eval :166-169
+          }
+        }
+        __syncwarp();
+        if (lane == 0) crit_chain<M>(P, R);
+        __syncwarp();
+        // stage slopes k_i = S * f (q rows: stage-input velocity, v rows: vdot)
+#pragma unroll
+        for (int p = 0; p < PER; ++p) {
+          const int k = lane + 32 * p;
+          double f = 0.0;
+          if (k < NQ)
+            f = R.xs[NQ + k];
+          else if (k < NX)
+            f = R.r[k - NQ];
+          const double kk = S * f;
+#pragma unroll
+          for (int j = 0; j < 6; ++j)
+            if (j == i) Kr[j][p] = kk;
+          if (i == 5) {
+            double inc = 0.0;
+#pragma unroll
+            for (int j = 0; j < 6; ++j) inc += P.b[j] * Kr[j][p];
+            xr[p] = xr[p] + h * inc;
+          }
+        }
+      }
+    } else if (warp == 1) {
+      if (t >= 1 && t <= NST) aux_stage<M>(P, sh, t - 1, lane, VS, ky, yv);
+    } else if (warp < 5) {
+      if (t >= 2 && t <= NST + 1) {
+        const int st = t - 2;
+        const Rec2<M>& R = sh.ring[st & 3];
+        const double* v = R.xs + NQ;
+        if (warp == 2) {
+          for (int kd = lane; kd < NDIRQ; kd += 32)
+            tan_rate_k<M, 1>(P, R.pr, v, M::dir(kd), &sh.At[st & 1][kd][0]);
+        } else if (warp == 3) {
+          for (int kd = NDIRQ + lane; kd < NDIRX; kd += 32)
+            tan_rate_k<M, 2>(P, R.pr, v, M::dir(kd), &sh.At[st & 1][kd][0]);
+        } else {
+          for (int kd = NDIRX + lane; kd < NDIR; kd += 32)
+            tan_rate_k<M, 3>(P, R.pr, v, NX + (kd - NDIRX), &sh.At[st & 1][kd][0]);
+        }
+      }
+    } else if (colthr && t >= 3) {
+      const int st = t - 3;
+      col_stage2<M>(P, sh, sh.ring[st & 3], sh.At[st & 1], st / 6, st % 6, col, S, dS, isU, um, uplus, hq, hv);
+    }
+    CITO_MARK((t * 8 + (warp < 8 ? warp : 7)) * 2 + 1);
+    __syncthreads();
+  }
+  // ---- outputs
+  if (warp == 0) {
+#pragma unroll
+    for (int p = 0; p < PER; ++p) {
+      const int k = lane + 32 * p;
+      if (k < NX) sh.x[k] = xr[p];
+    }
+  } else if (warp == 1 && lane < NY) {
+    sh.x[NX + lane] = yv;
+  }
+  double* jxb = jx + b * NXT * NXT;
+  double* jub = ju + b * NXT * 2 * NU;
+  double* jsb = js + b * NXT;
+  if (colthr) {
+    double* dst;
+    int stride;
+    if (sc >= 0) {
+      dst = jxb + sc;
+      stride = NXT;
+    } else if (isU) {
+      dst = jub + uj;
+      stride = 2 * NU;
+    } else {
+      dst = jsb;
+      stride = 1;
+    }
+#pragma unroll
+    for (int c = 0; c < NQ; ++c) {
+      const int hs = M::hslot(c);
+      dst[c * stride] = hs >= 0 ? hq[hs] : sh.PQ[M::pslot(c)][col];
+      dst[(NQ + c) * stride] = hs >= 0 ? hv[hs] : sh.PV[M::pslot(c)][col];
+    }
+#pragma unroll
+    for (int k = 0; k < NY; ++k) dst[(NX + k) * stride] = sh.DY[k][col];
+  }
+  if constexpr (M::NLCOL > 0) {  // closed-form columns (state directions no rate reads)
+    double dqc = 0.0;
+    for (int ss = 0; ss < P.substeps; ++ss) {
+      double inc = 0.0;
+#pragma unroll
+      for (int ii = 0; ii < 6; ++ii) inc += P.b[ii] * S;
+      dqc = dqc + h * inc;
+    }
+    for (int e = tid; e < M::NLCOL * NXT; e += blockDim.x) {
+      const int lc = e / NXT, r = e % NXT;
+      const int c = M::lcol(lc);
+      double val = (r == c) ? 1.0 : 0.0;
+      if (c >= NQ && r == c - NQ) val = dqc;
+      jxb[r * NXT + c] = val;
+    }
+  }
+  for (int e = tid; e < NXT * NY; e += blockDim.x) {
+    const int r = e / Pos<NY>::v, c = NX + e % Pos<NY>::v;
+    jxb[r * NXT + c] = (r == c) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  for (int k = tid; k < NXT; k += blockDim.x) {
+    const double e = sh.x[k];
+    ends[b * NXT + k] = e;
+    if (zs.defects) zs.defects[b * NXT + k] = zb[(2 * zk + 2) * NXT + k] - e;
+    if (!isfinite(e)) sh.bad = 1;
+  }
+  __syncthreads();
+  if (tid == 0 && bad) bad[b] = sh.bad;
+}

@@ -799,6 +799,39 @@ __global__ void __launch_bounds__(64) k_primal(const KParams P, int64_t B, const
   if (bad) bad[b] = nb;
 }
 
+// K5: pointwise audit of sampled states (verifier.replay_check, SURVEY.md §8(f)
+// row 3; /root/reference/pkg/src/cito/verifier.py:257-272, 314-318): per sample
+// (one thread) the contact signed distances (multibody.py:384-392), the joint
+// anchor residuals joint_constraint_value (multibody.py:324-336) and the
+// auxiliary rates Omega(x, u) (augmentation.py:134-153).
+template <class M>
+__global__ void __launch_bounds__(64) k_audit(const KParams P, int64_t B, const double* __restrict__ xs, int64_t xstride,
+                                              const double* __restrict__ us, double* __restrict__ sds,
+                                              double* __restrict__ cj, double* __restrict__ omega) {
+  using D = Dims<M>;
+  constexpr int NX = D::NX, NU = D::NU, NY = D::NY, NXT = D::NXT, NC = M::NC, NJ = M::NJ;
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  double x[NX], u[Pos<NU>::v], r[NXT];
+  Prim<M> pr;
+  for (int k = 0; k < NX; ++k) x[k] = xs[b * xstride + k];
+  for (int m = 0; m < NU; ++m) u[m] = us[b * NU + m];
+  prim_rate<M>(P, x, u, pr, r);
+  for (int i = 0; i < NC; ++i) sds[b * NC + i] = pr.sd[i];
+  for (int k = 0; k < NY; ++k) omega[b * NY + k] = r[NX + k];
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {
+    const int p = M::jparent(j), c = M::jchild(j);
+    double px = P.jrp[j][0], pz = P.jrp[j][1];  // world parent: the anchor itself
+    if (p >= 0) {
+      px = x[3 * p] + pr.rp[j][0];
+      pz = x[3 * p + 1] + pr.rp[j][1];
+    }
+    cj[b * 2 * NJ + 2 * j] = px - (x[3 * c] + pr.rc[j][0]);
+    cj[b * 2 * NJ + 2 * j + 1] = pz - (x[3 * c + 1] + pr.rc[j][1]);
+  }
+}
+
 // ===========================================================================
 // K1 (fused, warp-specialized, software-pipelined) -- one CTA per interval.
 //   warp 0      : primal producer.  Tick t computes RK stage t of the primal
