@@ -368,44 +368,10 @@ __device__ void prim_rate(const KParams& P, const double* xs, const double* u, P
         y[2 * a + al] = acc;
       }
     }
-    // sparse Cholesky G = L L^T (no fill outside M::lnzb), reciprocal pivots
+    // sparse Cholesky G = L L^T (no fill outside M::lnzb), reciprocal pivots, both
+    // solves: generated straight-line code (gen_models.py), every value in a register
     double Lir[NJ2];
-#pragma unroll
-    for (int cc = 0; cc < NJ2; ++cc) {
-      double d = Lr[LI(cc, cc)];
-#pragma unroll
-      for (int k = 0; k < cc; ++k)
-        if (M::lnzb(cc / 2, k / 2)) d -= Lr[LI(cc, k)] * Lr[LI(cc, k)];
-      const double lcc = sqrt(d);
-      Lr[LI(cc, cc)] = lcc;
-      const double il = 1.0 / lcc;
-      Lir[cc] = il;
-#pragma unroll
-      for (int r = cc + 1; r < NJ2; ++r) {
-        if (!M::lnzb(r / 2, cc / 2)) continue;
-        double x = Lr[LI(r, cc)];
-#pragma unroll
-        for (int k = 0; k < cc; ++k)
-          if (M::lnzb(r / 2, k / 2) && M::lnzb(cc / 2, k / 2)) x -= Lr[LI(r, k)] * Lr[LI(cc, k)];
-        Lr[LI(r, cc)] = x * il;
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < NJ2; ++r) {
-      double x = y[r];
-#pragma unroll
-      for (int k = 0; k < r; ++k)
-        if (M::lnzb(r / 2, k / 2)) x -= Lr[LI(r, k)] * y[k];
-      y[r] = x * Lir[r];
-    }
-#pragma unroll
-    for (int r = NJ2 - 1; r >= 0; --r) {
-      double x = y[r];
-#pragma unroll
-      for (int k = r + 1; k < NJ2; ++k)
-        if (M::lnzb(k / 2, r / 2)) x -= Lr[LI(k, r)] * y[k];
-      y[r] = x * Lir[r];
-    }
+    M::chol_solve(Lr, y, Lir);
     // publish the factor (elimination order) for the tangent threads
 #pragma unroll
     for (int r = 0; r < NJ2; ++r) {
@@ -599,22 +565,7 @@ __device__ void tan_rate(const KParams& P, const Prim<M>& pr, const double* v, i
       zp[2 * a] = z[2 * M::jperm(a)];
       zp[2 * a + 1] = z[2 * M::jperm(a) + 1];
     }
-#pragma unroll
-    for (int r = 0; r < NJ2; ++r) {
-      double x = zp[r];
-#pragma unroll
-      for (int k = 0; k < r; ++k)
-        if (M::lnzb(r / 2, k / 2)) x -= pr.L[LI(r, k)] * zp[k];
-      zp[r] = x * pr.Li[r];
-    }
-#pragma unroll
-    for (int r = NJ2 - 1; r >= 0; --r) {
-      double x = zp[r];
-#pragma unroll
-      for (int k = r + 1; k < NJ2; ++k)
-        if (M::lnzb(k / 2, r / 2)) x -= pr.L[LI(k, r)] * zp[k];
-      zp[r] = x * pr.Li[r];
-    }
+    M::tri_solve(pr.L, pr.Li, zp);  // generated straight-line sparse solves (gen_models.py)
 #pragma unroll
     for (int a = 0; a < NJ; ++a) {
       z[2 * M::jperm(a)] = zp[2 * a];
@@ -1088,43 +1039,7 @@ __device__ __forceinline__ void fused_primal(const KParams& P, FusedShared<M>& s
 #pragma unroll
         for (int c = 0; c <= r; ++c) Lr[LI(r, c)] = M::lnzb(r / 2, c / 2) ? w.Lw[LI(r, c)] : 0.0;
       }
-      // fill-in positions (none for trees) start from zero
-#pragma unroll
-      for (int cc = 0; cc < NJ2; ++cc) {
-        double d = Lr[LI(cc, cc)];
-#pragma unroll
-        for (int k = 0; k < cc; ++k)
-          if (M::lnzb(cc / 2, k / 2)) d -= Lr[LI(cc, k)] * Lr[LI(cc, k)];
-        const double il = rsqrt(d);
-        const double lcc = d * il;
-        Lr[LI(cc, cc)] = lcc;
-        Lir[cc] = il;
-#pragma unroll
-        for (int r = cc + 1; r < NJ2; ++r) {
-          if (!M::lnzb(r / 2, cc / 2)) continue;
-          double x = Lr[LI(r, cc)];
-#pragma unroll
-          for (int k = 0; k < cc; ++k)
-            if (M::lnzb(r / 2, k / 2) && M::lnzb(cc / 2, k / 2)) x -= Lr[LI(r, k)] * Lr[LI(cc, k)];
-          Lr[LI(r, cc)] = x * il;
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < NJ2; ++r) {
-        double x = y[r];
-#pragma unroll
-        for (int k = 0; k < r; ++k)
-          if (M::lnzb(r / 2, k / 2)) x -= Lr[LI(r, k)] * y[k];
-        y[r] = x * Lir[r];
-      }
-#pragma unroll
-      for (int r = NJ2 - 1; r >= 0; --r) {
-        double x = y[r];
-#pragma unroll
-        for (int k = r + 1; k < NJ2; ++k)
-          if (M::lnzb(k / 2, r / 2)) x -= Lr[LI(k, r)] * y[k];
-        y[r] = x * Lir[r];
-      }
+      M::chol_solve(Lr, y, Lir);  // generated straight-line sparse Cholesky + solves (gen_models.py)
 #pragma unroll
       for (int r = 0; r < NJ2; ++r) {
         pr.Li[r] = Lir[r];
