@@ -434,7 +434,7 @@ def run_ours(args):
 
         e2e_step()
         h2d = z.nbytes
-        d2h = int(4 * (lay.N - 1) + sum(v.numel() * v.element_size() for v in scp_api.asm._pinned.values()))
+        d2h = int(scp_api._plan["pk"].nbytes)  # one packed D2H per step (CSC, b, h, flags)
     elif args.workload == "multistart":
         Z_pin = torch.as_tensor(Z).pin_memory()
         ms_host = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in ms_out.items()}

@@ -673,14 +673,40 @@ def build_subproblem(tr, lin, z_j, delta, config):
     return asm.to_program(out, z_j)
 
 
+class _Packed:
+    """One device buffer (and its pinned host mirror) holding every per-iteration
+    output of GpuSCPStep at fixed offsets, so the whole result comes back with a
+    single device->host copy and every kernel argument is a constant pointer."""
+
+    def __init__(self, fields, device):
+        import torch
+
+        off, self.layout = 0, {}
+        for name, dtype, n in fields:
+            isz = torch.empty((), dtype=dtype).element_size()
+            off = (off + 255) // 256 * 256
+            self.layout[name] = (off, dtype, int(n), isz)
+            off += max(1, int(n)) * isz
+        self.nbytes = (off + 255) // 256 * 256
+        self.dev = torch.empty(self.nbytes, dtype=torch.uint8, device=device)
+        self.host = torch.empty(self.nbytes, dtype=torch.uint8, pin_memory=True)
+        self.d, self.h = {}, {}
+        for name, (o, dtype, n, isz) in self.layout.items():
+            self.d[name] = self.dev[o: o + max(1, n) * isz].view(dtype)[:n]
+            self.h[name] = self.host[o: o + max(1, n) * isz].view(dtype)[:n].numpy()
+
+
 class GpuSCPStep:
     """One SCP iteration's pre-IPM work in a single device pass (public API).
 
     ``iterate(z, delta, z_j=None)`` = cito.scp.linearize_all + build_subproblem
     (scp.py:412-413) with host numpy in / host scipy out: one pinned H2D of z,
-    the interval + node kernels, the whole-subproblem assembly, one batched
-    pinned D2H and a single synchronization.  Raises FloatingPointError for
-    non-finite interval end states like the reference (augmentation.py:231-233).
+    the interval + node kernels, the whole-subproblem assembly (+ preconditioning,
+    scp.py:414), ONE pinned D2H of a packed result buffer and a single
+    synchronization.  All device buffers and kernel argument tables are built
+    once; the host work per call is the C-ABI launches and the scipy wrappers.
+    Raises FloatingPointError for non-finite interval end states like the
+    reference (augmentation.py:231-233).
     Returns (LinearizedProblem (lazy, device-backed), ConicProgram, meta)."""
 
     def __init__(self, tr_or_scenario, w_prox=2000.0, w_ep=50000.0, device=None):
@@ -694,27 +720,157 @@ class GpuSCPStep:
         gt = self.gt
         scale_v = build_scaling(gt.scenario, gt.lay)[0]
         self.asm = SubproblemAssembler(SubproblemPattern(gt.scenario, gt.lay, scale_v, w_prox, w_ep), gt.device)
-        self._z_pin = torch.empty(gt.lay.dim, dtype=torch.float64, pin_memory=True)
-        self._bad_pin = torch.empty(gt.lay.N - 1, dtype=torch.int32, pin_memory=True)
         self._Lazy = LazyLinearizedProblem
+        self._plan = None
+        self._last_lin = None
+
+    # -- one-time plan: buffers + constant ctypes argument tables
+    def _build_plan(self):
+        import ctypes
+        import weakref  # noqa: F401
+
+        import torch
+
+        gt, asm, pat = self.gt, self.asm, self.asm.pat
+        if getattr(asm, "_rhs", None) is None:
+            asm._prepare_batched()
+        lay, dev = gt.lay, gt.device
+        N, nxt, nu, nq, nc = lay.N, lay.n_xt, lay.n_u, lay.n_q, lay.n_c
+        n_psi = 3 * nc + lay.n_g_out
+        NI = N - 1
+        f64 = dict(dtype=torch.float64, device=dev)
+        # linearization outputs (device only; the lazy LinearizedProblem reads them on demand)
+        lin = dict(ends=torch.empty((NI, nxt), **f64), jx=torch.empty((NI, nxt, nxt), **f64),
+                   ju=torch.empty((NI, nxt, 2 * nu), **f64), js=torch.empty((NI, nxt), **f64),
+                   defects=torch.empty((NI, nxt), **f64),
+                   psi=torch.empty((NI, n_psi), **f64), psi_jac=torch.empty((NI, n_psi, 2 * lay.n_y), **f64),
+                   theta=torch.empty((N, 6 * nc), **f64), theta_jac=torch.empty((N, 6 * nc, 3 * nq + 3 * nc), **f64),
+                   imp_v=torch.empty((N, nq), **f64), imp_jac=torch.empty((N, nq, 3 * nq + 2 * nc), **f64))
+        dA, dG = asm._mats["A"], asm._mats["G"]
+        nA, nG = dA["nrows"], dG["nrows"]
+        i32, i64, fd = torch.int32, torch.int64, torch.float64
+        pk = _Packed([("bad", i32, NI), ("A_indptr", i32, pat.n + 1), ("G_indptr", i32, pat.n + 1),
+                      ("rhs", fd, nA + nG), ("row_scale_A", fd, nA), ("row_scale_G", fd, nG),
+                      ("A_data", fd, dA["nsup"]), ("G_data", fd, dG["nsup"]),
+                      ("A_indices", i32, dA["nsup"]), ("G_indices", i32, dG["nsup"])], dev)
+        lin["bad"] = pk.d["bad"]
+        z_dev = torch.empty(lay.dim, **f64)
+        z_pin = torch.empty(lay.dim, dtype=torch.float64, pin_memory=True)
+        rowmax = torch.empty(max(1, nA + nG), dtype=i64, device=dev)
+        arr = lambda xs: ctypes_ptr_array([x.data_ptr() for x in xs])  # noqa: E731
+        mats = [dA, dG]
+        r = asm._rhs
+        soc_start, soc_dim = soc_tables(pat.n_orthant, pat.soc_dims, dev)
+        L = _lib.lib()
+        keep = []  # ctypes arrays must outlive the plan
+
+        def k(a):
+            keep.append(a)
+            return a
+
+        lin_ptrs = k(arr([lin[kk] for kk in LIN_SOURCES]))
+        asm_args = (2, pat.n, k(arr([d["sp_ptr"] for d in mats])), k(arr([d["row"] for d in mats])),
+                    k(arr([d["src"] for d in mats])), k(arr([d["idx"] for d in mats])),
+                    k(arr([d["val"] for d in mats])), asm.sigma_dev.data_ptr(), lin_ptrs,
+                    k(arr([d["counts"] for d in mats])), k(arr([pk.d["A_indptr"], pk.d["G_indptr"]])),
+                    k(arr([pk.d["A_indices"], pk.d["G_indices"]])), k(arr([pk.d["A_data"], pk.d["G_data"]])))
+        rm_arr = k(arr([rowmax[:nA], rowmax[nA:]]))
+        # b and h: one contiguous vector (rows [0, nA) = b, [nA, nA + nG) = h) in the packed buffer
+        rhs_dev = pk.d["rhs"]
+        rhs_args = (r["n"], r["rows"].data_ptr(), r["form"].data_ptr(), r["vsrc"].data_ptr(), r["voff"].data_ptr(),
+                    r["seg_src"].data_ptr(), r["seg_off"].data_ptr(), r["seg_len"].data_ptr(), r["seg_cb"].data_ptr(),
+                    r["cols"].data_ptr(), z_dev.data_ptr(), lin_ptrs, rhs_dev.data_ptr())
+        pc_args = (pat.n, pk.d["A_indptr"].data_ptr(), pk.d["A_indices"].data_ptr(), pk.d["A_data"].data_ptr(), nA,
+                   rhs_dev.data_ptr(), pk.d["G_indptr"].data_ptr(), pk.d["G_indices"].data_ptr(),
+                   pk.d["G_data"].data_ptr(), nG, rhs_dev[nA:].data_ptr(), pat.n_orthant, len(pat.soc_dims),
+                   soc_start.data_ptr(), soc_dim.data_ptr(), rowmax[:nA].data_ptr(), rowmax[nA:].data_ptr(), 1,
+                   max(dA["nsup"], dG["nsup"]), pk.d["row_scale_A"].data_ptr(), pk.d["row_scale_G"].data_ptr())
+        o = lin
+        lin_args = (gt.disc._h.ptr, N, 1, int(lay.dim), int(gt.base_u), int(gt.base_p), z_dev.data_ptr())
+        lin_outs = tuple(o[kk].data_ptr() for kk in ("ends", "jx", "ju", "js", "defects", "bad", "psi", "psi_jac",
+                                                     "theta", "theta_jac", "imp_v", "imp_jac"))
+        dim = lay.dim
+        P_idx = np.arange(dim, dtype=np.int32)
+        P_ptr = np.concatenate([np.arange(dim + 1), np.full(pat.n - dim, dim)]).astype(np.int32)
+        self._plan = dict(lin=lin, pk=pk, z_dev=z_dev, z_pin=z_pin, rowmax=rowmax, rhs_dev=rhs_dev,
+                          rhs_const=r["const"], asm_args=asm_args, rm_arr=rm_arr, rhs_args=rhs_args,
+                          pc_args=pc_args, lin_args=lin_args, lin_outs=lin_outs, keep=keep, L=L, nA=nA, nG=nG,
+                          soc=(soc_start, soc_dim), P_idx=P_idx, P_ptr=P_ptr,
+                          P_plain=None, meta=_Meta(pat.z_idx, pat.sp_idx, pat.sm_idx, pat.t_idx))
 
     def iterate(self, z, delta, z_j=None, epsilon=None, precondition=False):
         """Returns (lin, prog, meta); with ``precondition`` the program comes back
         row-scaled on the device (= cito.conic.precondition, scp.py:414) and the
         result is (lin, scaled_prog, Preconditioner, meta)."""
+        import scipy.sparse as sp
         import torch
 
         z = np.asarray(z, dtype=float)
         if not np.all(np.isfinite(z)):
             raise FloatingPointError("non-finite reference point")
-        gt = self.gt
-        self._z_pin.numpy()[:] = z
-        z_dev = self._z_pin.to(gt.device, non_blocking=True)
-        r = gt.linearize_device(z_dev, delta, epsilon)
-        out = self.asm.assemble_device(r, z_dev, precondition=precondition)
-        self._bad_pin.copy_(r["bad"], non_blocking=True)
-        res = self.asm.to_program(out, z if z_j is None else z_j)  # the one synchronization
-        bad = self._bad_pin.numpy()
+        if self._plan is None:
+            self._build_plan()
+        pl = self._plan
+        gt, pat = self.gt, self.asm.pat
+        # a LinearizedProblem handed out by the previous call still points at the
+        # reused device buffers: give it its own host copy before overwriting them
+        prev = self._last_lin() if self._last_lin is not None else None
+        if prev is not None and prev._host is None:
+            prev.materialize()
+        if epsilon is None:
+            epsilon = gt.scenario.ctcs_epsilon
+        stream = torch.cuda.current_stream(gt.device)
+        s = stream.cuda_stream
+        L = pl["L"]
+        pl["z_pin"].numpy()[:] = z
+        pl["z_dev"].copy_(pl["z_pin"], non_blocking=True)
+        _lib.check(L.cito_linearize_all_dev(*pl["lin_args"], float(delta), float(epsilon), *pl["lin_outs"], s),
+                   "linearize_all")
+        if precondition:
+            pl["rowmax"].zero_()
+        _lib.check(L.cito_csc_assemble2_dev(*pl["asm_args"], pl["rm_arr"] if precondition else None, s),
+                   "csc_assemble")
+        rhs = pl["rhs_dev"]
+        rhs.copy_(pl["rhs_const"])
+        _lib.check(L.cito_rhs_dev(*pl["rhs_args"], s), "rhs")
+        pk = pl["pk"]
+        nA = pl["nA"]
+        if precondition:
+            _lib.check(L.cito_precondition_dev(*pl["pc_args"], s), "precondition")
+        pk.host.copy_(pk.dev, non_blocking=True)
+        stream.synchronize()  # the one synchronization
+        hh = pk.h
+        bad = hh["bad"]
         if bad.any():
             raise FloatingPointError(f"non-finite state in intervals {np.where(bad != 0)[0].tolist()}")
-        return (self._Lazy(r, z.copy()),) + tuple(res)
+        ConicProgram, ConeSpec = _conic_types()
+        mats = {}
+        for M, nrows in (("A", nA), ("G", pl["nG"])):
+            indptr = hh[f"{M}_indptr"].copy()
+            nnz = int(indptr[-1])
+            mats[M] = sp.csc_matrix((hh[f"{M}_data"][:nnz].copy(), hh[f"{M}_indices"][:nnz].copy(), indptr),
+                                    shape=(nrows, pat.n))
+        zj = z if z_j is None else z_j
+        c = pat.objective_c(zj)
+        P_data = pat.P_diag[: pat.lay.dim]
+        if precondition:  # cost normalization (conic.py:311-316)
+            omega = max(1.0, float(np.max(np.abs(c))) if c.size else 0.0)
+            if P_data.size:
+                omega = max(omega, float(np.max(np.abs(P_data))))
+            P = sp.csc_matrix((P_data * (1.0 / omega), pl["P_idx"], pl["P_ptr"]), shape=(pat.n, pat.n))
+            c = c / omega
+        else:
+            if pl["P_plain"] is None:
+                pl["P_plain"] = sp.csc_matrix((P_data, pl["P_idx"], pl["P_ptr"]), shape=(pat.n, pat.n))
+            P = pl["P_plain"].copy()
+        prog = ConicProgram(P=P, c=c, A=mats["A"], b=hh["rhs"][:nA].copy(), G=mats["G"], h=hh["rhs"][nA:].copy(),
+                            cones=ConeSpec(nonneg=pat.n_orthant, soc=pat.soc_dims))
+        lin = self._Lazy(pl["lin"], z.copy())
+        import weakref
+
+        self._last_lin = weakref.ref(lin)
+        if precondition:
+            prec = _preconditioner_type()(row_scale_A=hh["row_scale_A"].copy(), row_scale_G=hh["row_scale_G"].copy(),
+                                          var_scale=np.ones(pat.n), cost_scale=omega)
+            return lin, prog, prec, pl["meta"]
+        return lin, prog, pl["meta"]
