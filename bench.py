@@ -484,7 +484,8 @@ def run_ours(args):
     roofline = {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": (achieved / peak) if achieved else None,
                 "traffic": ncu_traffic(f"k_linearize_{'scp' if fine else args.workload}"),
-                "kernel": "k_linearize<Topo_halfcheetah_g2>", "kernel_ms": k1_ms, "intervals_per_launch": B_k1,
+                "kernel": ("k_linearize2<Topo_halfcheetah_g2,1>" if B_k1 <= 148 else "k_linearize<Topo_halfcheetah_g2,3>"),
+                "kernel_ms": k1_ms, "intervals_per_launch": B_k1,
                 "flops_per_interval": F, "flops_definition": fdef,
                 "peak_source": "measured in this run: FP64 DFMA probe kernel (cito_dfma_peak); MEASURED_PEAKS.json "
                                "has no fp64 entry"}

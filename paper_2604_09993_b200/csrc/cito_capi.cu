@@ -79,12 +79,15 @@ cito_status ensure_pool() {
   return CITO_OK;
 }
 
-// Kernel generation of K1: 1 = k_linearize (cito_kernels.cuh, default),
-// 2 = k_linearize2 (short-primal-chain variant, cito_k1v2.cuh; CITO_K1=2).
+// K1 selection.  Default (auto): k_linearize2 (cito_k1v2.cuh: short primal chain,
+// off-chain aux warp, q/v and u Jacobian warps) while the grid fits the SMs once
+// -- the latency case of one SCP iteration -- and k_linearize<M, 3> (cito_kernels.cuh,
+// 4 warps, 3 CTAs/SM) for batches, where its smaller footprint gives more
+// throughput.  CITO_K1=1 / CITO_K1=2 force one generation for A/B measurements.
 static int k1_version() {
   static int v = [] {
     const char* e = getenv("CITO_K1");
-    return (e && e[0] == '2') ? 2 : 1;
+    return (e && e[0] == '1') ? 1 : (e && e[0] == '2') ? 2 : 0;
   }();
   return v;
 }
@@ -109,7 +112,8 @@ cito_status launch_linearize(const KParams& P, int64_t B, const double* xt0s, co
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   count_launch();
-  if (k1_version() == 2) {
+  const int ver = k1_version();
+  if (ver == 2 || (ver == 0 && B <= sms)) {
     if (B <= sms)
       k_linearize2<M, 1><<<(unsigned)B, K2Dims<M>::NT, smem2, st>>>(P, B, xt0s, Us, Ss, ends, jx, ju, js, bad, zs);
     else

@@ -35,7 +35,7 @@
 template <class M, int KIND>
 __device__ __forceinline__ void tan_rate_k(const KParams& P, const Prim<M>& pr, const double* v, int dir, double* out) {
   constexpr int NL = M::NL, NJ = M::NJ, NC = M::NC, NA = M::NA, NQ = 3 * NL, NX = 2 * NQ;
-  constexpr bool HQ = KIND == 1, HV = KIND == 2, HU = KIND == 3;
+  constexpr bool HQ = (KIND & 1) != 0, HV = (KIND & 2) != 0, HU = (KIND & 4) != 0;
   (void)NL;
 #define SQ(k) ((dir) == (k) ? 1.0 : 0.0)
 #define SV(k) ((dir) == NQ + (k) ? 1.0 : 0.0)
@@ -195,24 +195,28 @@ __device__ __forceinline__ void tan_rate_k(const KParams& P, const Prim<M>& pr, 
     const double ft = pr.u[NA + 2 * i], fn = pr.u[NA + 2 * i + 1], gam = pr.u[NA + 2 * NC + i];
     const double rx = pr.rr[i][0], rz = pr.rr[i][1];
     const double w = v[3 * l + 2];
-    double dvt = 0.0, dlamc = 0.0;
-    if constexpr (HQ) {
-      const double dth = SQ(3 * l + 2);
-      const double dJv0 = -dth * rx * w, dJv1 = -dth * rz * w;
-      dvt = (dn[i][1]) * pr.Jv[i][0] + (-dn[i][0]) * pr.Jv[i][1] + pr.t[i][0] * dJv0 + pr.t[i][1] * dJv1;
-      dlamc = dvt;
-    }
-    if constexpr (HV) {
-      const double dw = SV(3 * l + 2);
-      const double dJv0 = SV(3 * l) + (-rz) * dw, dJv1 = SV(3 * l + 1) + rx * dw;
-      dvt = pr.t[i][0] * dJv0 + pr.t[i][1] * dJv1;
+    double dlamc = 0.0;
+    if constexpr (HQ || HV) {
+      double dJv0 = 0.0, dJv1 = 0.0, dvt = 0.0;
+      if constexpr (HQ) {
+        const double dth = SQ(3 * l + 2);
+        dJv0 = -dth * rx * w;
+        dJv1 = -dth * rz * w;
+        if constexpr (M::IMPLICIT) dvt = (dn[i][1]) * pr.Jv[i][0] + (-dn[i][0]) * pr.Jv[i][1];
+      }
+      if constexpr (HV) {
+        const double dw = SV(3 * l + 2);
+        dJv0 += SV(3 * l) + (-rz) * dw;
+        dJv1 += SV(3 * l + 1) + rx * dw;
+      }
+      dvt += pr.t[i][0] * dJv0 + pr.t[i][1] * dJv1;
       dlamc = dvt;
     }
     if constexpr (HU) {
       const double dft = SU(NA + 2 * i), dgam = SU(NA + 2 * NC + i);
       const double q1 = ft * ft + 1.0;
       const double dsg = dft / (q1 * sqrt(q1));
-      dlamc = dgam * pr.sg[i] + gam * dsg;
+      dlamc += dgam * pr.sg[i] + gam * dsg;
     }
     dy[5 * i + 0] = HU ? SU(NA + 2 * i + 1) : 0.0;
     dy[5 * i + 1] = sabs_d(pr.lamc[i]) * dlamc;
@@ -278,7 +282,12 @@ template <class M>
 struct K2Dims {
   using D = Dims<M>;
   static constexpr int NCW = (D::NCOL + 31) / 32;
-  static constexpr int NT = 32 * (5 + NCW);
+  // warp roles, ordered so the heavy roles (primal, columns, q/v Jacobian) sit on
+  // distinct SM sub-partitions (warp w -> SMSP w % 4) and only the light ones
+  // (off-chain aux, u Jacobian) share: 0 primal, 1..NCW columns, then q/v
+  // Jacobian, aux, u Jacobian
+  static constexpr int W_COL0 = 1, W_JQV = 1 + NCW, W_AUX = 2 + NCW, W_JU = 3 + NCW;
+  static constexpr int NT = 32 * (4 + NCW);
   static constexpr int NX = D::NX;
   static constexpr int PER = (NX + 31) / 32;  // state coordinates per lane of warp 0
   static constexpr int count_q() {
@@ -288,6 +297,25 @@ struct K2Dims {
   }
   static constexpr int NDIRQ = count_q();
 };
+
+// Per-thread state that lives across ticks, one union for all roles (each thread
+// has exactly one role, so the roles share the same registers): warp 0 = state
+// coordinates + stage slopes, aux = stage velocities + y accumulator/row,
+// columns = substep-start tangents of the history coordinates.
+template <class M>
+struct RegState {
+  static constexpr int PER = (Dims<M>::NX + 31) / 32;
+  static constexpr int NH = Pos<M::NHIST>::v;
+  static constexpr int a = 7 * PER, b = 8, c = 2 * NH;
+  static constexpr int N = a > b ? (a > c ? a : c) : (b > c ? b : c);
+};
+#define RS_XR(p) rs[(p)]
+#define RS_KR(j, p) rs[PER + (j) * PER + (p)]
+#define RS_VS(j) rs[(j)]
+#define RS_KY rs[6]
+#define RS_YV rs[7]
+#define RS_HQ(h) rs[(h)]
+#define RS_HV(h) rs[RegState<M>::NH + (h)]
 
 template <class M>
 struct AuxScratch {
@@ -482,8 +510,8 @@ __device__ __forceinline__ void crit_chain(const KParams& P, Rec2<M>& R) {
 
 // Warp 1: everything of stage `a` that is off the critical chain.
 template <class M>
-__device__ __forceinline__ void aux_stage(const KParams& P, Fused2Shared<M>& sh, int a, int lane, double (&VS)[6],
-                                          double& ky, double& yv) {
+__device__ __forceinline__ void aux_stage(const KParams& P, Fused2Shared<M>& sh, int a, int lane,
+                                          double (&rs)[RegState<M>::N]) {
   using D = Dims<M>;
   constexpr int NL = M::NL, NJ = M::NJ, NC = M::NC, NA = M::NA, NQ = D::NQ, NY = D::NY;
   const int s = a / 6, i = a % 6;
@@ -598,23 +626,23 @@ __device__ __forceinline__ void aux_stage(const KParams& P, Fused2Shared<M>& sh,
   }
   // 2: y accumulators (augmentation.py:206-209), dS terms of the q-row stage inputs
   if (lane < NY) {
-    ky = (i == 0 ? 0.0 : ky) + P.b[i] * (S * R.r[NQ + lane]);
-    if (i == 5) yv = yv + h * ky;
+    RS_KY = (i == 0 ? 0.0 : RS_KY) + P.b[i] * (S * R.r[NQ + lane]);
+    if (i == 5) RS_YV = RS_YV + h * RS_KY;
   }
   if (lane < NQ) {
     const double vsk = v[lane];
     double ws = 0.0;
 #pragma unroll
     for (int j = 0; j < 5; ++j) {
-      if (j == i) VS[j] = vsk;
-      if (j < i) ws += P.ha[i][j] * VS[j];
+      if (j == i) RS_VS(j) = vsk;
+      if (j < i) ws += P.ha[i][j] * RS_VS(j);
     }
-    if (i == 5) VS[5] = vsk;
+    if (i == 5) RS_VS(5) = vsk;
     R.wq[lane] = ws;
     if (i == 5) {
       double w2 = 0.0;
 #pragma unroll
-      for (int j = 0; j < 6; ++j) w2 += P.b[j] * VS[j];
+      for (int j = 0; j < 6; ++j) w2 += P.b[j] * RS_VS(j);
       sh.vbs[s & 1][lane] = h * w2;
     }
   }
@@ -624,8 +652,7 @@ __device__ __forceinline__ void aux_stage(const KParams& P, Fused2Shared<M>& sh,
 template <class M>
 __device__ __forceinline__ void col_stage2(const KParams& P, Fused2Shared<M>& sh, const Rec2<M>& R,
                                            const double (*At)[Dims<M>::NRP], int s, const int I, int col, double S,
-                                           double dS, bool isU, int um, bool uplus, double (&hq)[Pos<M::NHIST>::v],
-                                           double (&hv)[Pos<M::NHIST>::v]) {
+                                           double dS, bool isU, int um, bool uplus, double (&rs)[RegState<M>::N]) {
   using D = Dims<M>;
   constexpr int NQ = D::NQ, NR = D::NR, NDIRX = M::NDIRX;
   const double h = P.h;
@@ -635,6 +662,14 @@ __device__ __forceinline__ void col_stage2(const KParams& P, Fused2Shared<M>& sh
 #pragma unroll
     for (int p = 0; p < M::NPUSH; ++p) sh.PQ[p][col] += P.he1 * S * sh.PV[p][col];
   }
+  // stage coefficients, once per tick (warp-uniform): S h^2 sum a a (q rows), h a (v rows)
+  double cqs[5], has[5];
+#pragma unroll
+  for (int l = 0; l < 5; ++l) {
+    cqs[l] = S * P.cq[I][l];
+    has[l] = P.ha[I][l];
+  }
+  const double shc = S * P.hc1[I];
   double vals[Pos<NDIRX>::v];
 #pragma unroll
   for (int kd = 0; kd < NDIRX; ++kd) {
@@ -642,16 +677,16 @@ __device__ __forceinline__ void col_stage2(const KParams& P, Fused2Shared<M>& sh
     double val;
     if (d < NQ) {
       const int hs = M::hslot(d);
-      val = hq[hs] + S * P.hc1[I] * hv[hs] + dS * R.wq[d];
+      val = RS_HQ(hs) + shc * RS_HV(hs) + dS * R.wq[d];
 #pragma unroll
       for (int l = 0; l < 5; ++l)
-        if (l < I) val += S * P.cq[I][l] * sh.KV[l][hs][col];
+        if (l < I) val += cqs[l] * sh.KV[l][hs][col];
     } else {
       const int hs = M::hslot(d - NQ);
-      val = hv[hs];
+      val = RS_HV(hs);
 #pragma unroll
       for (int l = 0; l < 5; ++l)
-        if (l < I) val += P.ha[I][l] * sh.KV[l][hs][col];
+        if (l < I) val += has[l] * sh.KV[l][hs][col];
     }
     vals[kd] = val;
   }
@@ -674,7 +709,8 @@ __device__ __forceinline__ void col_stage2(const KParams& P, Fused2Shared<M>& sh
   }
 #pragma unroll
   for (int rr = 0; rr < NR; ++rr) {
-    const double dk = S * accs[rr] + dS * R.r[rr];
+    double dk = S * accs[rr];
+    if (dS != 0.0) dk = dk + dS * R.r[rr];  // the dilation column only
     if (rr < NQ) {
       const int hs = M::hslot(rr);
       if (hs >= 0) {
@@ -688,8 +724,8 @@ __device__ __forceinline__ void col_stage2(const KParams& P, Fused2Shared<M>& sh
             incv += P.b[l] * kv;
             incq += P.e2[l] * kv;
           }
-          hq[hs] = hq[hs] + P.he1 * S * hv[hs] + S * incq + dS * sh.vbs[s & 1][rr];
-          hv[hs] = hv[hs] + h * incv;
+          RS_HQ(hs) = RS_HQ(hs) + P.he1 * S * RS_HV(hs) + S * incq + dS * sh.vbs[s & 1][rr];
+          RS_HV(hs) = RS_HV(hs) + h * incv;
         }
       } else {
         const int p = M::pslot(rr);
@@ -713,7 +749,7 @@ __global__ void __launch_bounds__(K2Dims<M>::NT, MINB) k_linearize2(const KParam
   using D = Dims<M>;
   using K = K2Dims<M>;
   constexpr int NQ = D::NQ, NX = D::NX, NU = D::NU, NY = D::NY, NXT = D::NXT, NCOL = D::NCOL;
-  constexpr int NDIRX = M::NDIRX, NDIR = D::NDIR, NHIST = M::NHIST, PER = K::PER, NDIRQ = K::NDIRQ;
+  constexpr int NDIRX = M::NDIRX, NDIR = D::NDIR, NHIST = M::NHIST, PER = K::PER;
   static_assert(NQ <= 32 && NY <= 32, "aux warp owns one q coordinate and one y row per lane");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Fused2Shared<M>& sh = *reinterpret_cast<Fused2Shared<M>*>(smem_raw);
@@ -744,34 +780,34 @@ __global__ void __launch_bounds__(K2Dims<M>::NT, MINB) k_linearize2(const KParam
     sh.sp.cl[c] = M::clink(c);
   }
   // warp 0: state coordinates (lane + 32 p) and their stage slopes in registers
-  double xr[PER], Kr[6][PER];
+  double rs[RegState<M>::N];
+#pragma unroll
+  for (int k = 0; k < RegState<M>::N; ++k) rs[k] = 0.0;
   if (warp == 0) {
 #pragma unroll
     for (int p = 0; p < PER; ++p) {
       const int k = lane + 32 * p;
-      xr[p] = k < NX ? src_x[k] : 0.0;
+      RS_XR(p) = k < NX ? src_x[k] : 0.0;
     }
   }
   // warp 1: y row `lane` and the stage velocities of q coordinate `lane`
-  double yv = 0.0, ky = 0.0, VS[6];
-  if (warp == 1 && lane < NY) yv = src_x[NX + lane];
+  if (warp == K::W_AUX && lane < NY) RS_YV = src_x[NX + lane];
   // column threads
-  const int col = tid - 32 * 5;
-  const bool colthr = warp >= 5 && col < NCOL;
+  const int col = tid - 32 * K::W_COL0;
+  const bool colthr = warp >= K::W_COL0 && warp < K::W_COL0 + K::NCW && col < NCOL;
   const double dS = (col == NCOL - 1) ? 1.0 : 0.0;
   const int sc = (col >= 0 && col < M::NHCOL) ? M::hcol(col) : -1;
   const int uj = col - M::NHCOL;
   const bool isU = (uj >= 0) && (uj < 2 * NU);
   const int um = isU ? (uj % Pos<NU>::v) : 0;
   const bool uplus = isU && (uj >= NU);
-  double hq[Pos<NHIST>::v], hv[Pos<NHIST>::v];
   if (colthr) {
 #pragma unroll
     for (int c = 0; c < NQ; ++c) {
       const double e_q = (sc == c) ? 1.0 : 0.0, e_v = (sc == NQ + c) ? 1.0 : 0.0;
       if (M::hslot(c) >= 0) {
-        hq[M::hslot(c)] = e_q;
-        hv[M::hslot(c)] = e_v;
+        RS_HQ(M::hslot(c)) = e_q;
+        RS_HV(M::hslot(c)) = e_v;
       } else {
         sh.PQ[M::pslot(c)][col] = e_q;
         sh.PV[M::pslot(c)][col] = e_v;
@@ -793,10 +829,10 @@ __global__ void __launch_bounds__(K2Dims<M>::NT, MINB) k_linearize2(const KParam
 #pragma unroll
         for (int p = 0; p < PER; ++p) {
           const int k = lane + 32 * p;
-          double a = xr[p];
+          double a = RS_XR(p);
 #pragma unroll
           for (int j = 0; j < 5; ++j)
-            if (j < i) a = a + P.ha[i][j] * Kr[j][p];
+            if (j < i) a = a + P.ha[i][j] * RS_KR(j, p);
           if (k < NX) R.xs[k] = a;
         }
         __syncwarp();
@@ -827,36 +863,33 @@ __global__ void __launch_bounds__(K2Dims<M>::NT, MINB) k_linearize2(const KParam
           const double kk = S * f;
 #pragma unroll
           for (int j = 0; j < 6; ++j)
-            if (j == i) Kr[j][p] = kk;
+            if (j == i) RS_KR(j, p) = kk;
           if (i == 5) {
             double inc = 0.0;
 #pragma unroll
-            for (int j = 0; j < 6; ++j) inc += P.b[j] * Kr[j][p];
-            xr[p] = xr[p] + h * inc;
+            for (int j = 0; j < 6; ++j) inc += P.b[j] * RS_KR(j, p);
+            RS_XR(p) = RS_XR(p) + h * inc;
           }
         }
       }
-    } else if (warp == 1) {
-      if (t >= 1 && t <= NST) aux_stage<M>(P, sh, t - 1, lane, VS, ky, yv);
-    } else if (warp < 5) {
+    } else if (warp == K::W_AUX) {
+      if (t >= 1 && t <= NST) aux_stage<M>(P, sh, t - 1, lane, rs);
+    } else if (warp == K::W_JQV || warp == K::W_JU) {
       if (t >= 2 && t <= NST + 1) {
         const int st = t - 2;
         const Rec2<M>& R = sh.ring[st & 3];
         const double* v = R.xs + NQ;
-        if (warp == 2) {
-          for (int kd = lane; kd < NDIRQ; kd += 32)
-            tan_rate_k<M, 1>(P, R.pr, v, M::dir(kd), &sh.At[st & 1][kd][0]);
-        } else if (warp == 3) {
-          for (int kd = NDIRQ + lane; kd < NDIRX; kd += 32)
-            tan_rate_k<M, 2>(P, R.pr, v, M::dir(kd), &sh.At[st & 1][kd][0]);
-        } else {
+        if (warp == K::W_JQV) {  // q and v directions (kinds 1 | 2)
+          for (int kd = lane; kd < NDIRX; kd += 32)
+            tan_rate_k<M, 3>(P, R.pr, v, M::dir(kd), &sh.At[st & 1][kd][0]);
+        } else {  // control directions (kind 4)
           for (int kd = NDIRX + lane; kd < NDIR; kd += 32)
-            tan_rate_k<M, 3>(P, R.pr, v, NX + (kd - NDIRX), &sh.At[st & 1][kd][0]);
+            tan_rate_k<M, 4>(P, R.pr, v, NX + (kd - NDIRX), &sh.At[st & 1][kd][0]);
         }
       }
     } else if (colthr && t >= 3) {
       const int st = t - 3;
-      col_stage2<M>(P, sh, sh.ring[st & 3], sh.At[st & 1], st / 6, st % 6, col, S, dS, isU, um, uplus, hq, hv);
+      col_stage2<M>(P, sh, sh.ring[st & 3], sh.At[st & 1], st / 6, st % 6, col, S, dS, isU, um, uplus, rs);
     }
     CITO_MARK((t * 8 + (warp < 8 ? warp : 7)) * 2 + 1);
     __syncthreads();
@@ -866,10 +899,10 @@ __global__ void __launch_bounds__(K2Dims<M>::NT, MINB) k_linearize2(const KParam
 #pragma unroll
     for (int p = 0; p < PER; ++p) {
       const int k = lane + 32 * p;
-      if (k < NX) sh.x[k] = xr[p];
+      if (k < NX) sh.x[k] = RS_XR(p);
     }
-  } else if (warp == 1 && lane < NY) {
-    sh.x[NX + lane] = yv;
+  } else if (warp == K::W_AUX && lane < NY) {
+    sh.x[NX + lane] = RS_YV;
   }
   double* jxb = jx + b * NXT * NXT;
   double* jub = ju + b * NXT * 2 * NU;
@@ -890,8 +923,8 @@ __global__ void __launch_bounds__(K2Dims<M>::NT, MINB) k_linearize2(const KParam
 #pragma unroll
     for (int c = 0; c < NQ; ++c) {
       const int hs = M::hslot(c);
-      dst[c * stride] = hs >= 0 ? hq[hs] : sh.PQ[M::pslot(c)][col];
-      dst[(NQ + c) * stride] = hs >= 0 ? hv[hs] : sh.PV[M::pslot(c)][col];
+      dst[c * stride] = hs >= 0 ? RS_HQ(hs) : sh.PQ[M::pslot(c)][col];
+      dst[(NQ + c) * stride] = hs >= 0 ? RS_HV(hs) : sh.PV[M::pslot(c)][col];
     }
 #pragma unroll
     for (int k = 0; k < NY; ++k) dst[(NX + k) * stride] = sh.DY[k][col];
