@@ -377,19 +377,25 @@ def precondition(prog):
 
     A program produced by this package's build_subproblem is scaled where it
     already lives (device copy of the last assembly); any other program is
-    uploaded, scaled by the same kernels and copied back.  Returns
-    (scaled ConicProgram, Preconditioner) with the reference's types when
-    cito.conic is loaded; A/G values and row scales are bit-identical to the
-    reference's, b/h scale the GPU's own b/h by the same factors."""
+    uploaded, scaled by the same kernels and copied back.  The sparsity pattern
+    does not change, so only the scaled values, b, h and the row scales come
+    back (pinned, one synchronization).  Returns (scaled ConicProgram,
+    Preconditioner) with the reference's types when cito.conic is loaded; A/G
+    values and row scales are bit-identical to the reference's, b/h scale the
+    GPU's own b/h by the same factors."""
     import scipy.sparse as sp
     import torch
 
     ConicProgram, ConeSpec = _conic_types()
     dev = torch.device("cuda", torch.cuda.current_device())
-    stream = torch.cuda.current_stream(dev).cuda_stream
+    stream = torch.cuda.current_stream(dev)
     cones = prog.cones
     n = int(prog.A.shape[1])
     nA, nG = int(prog.A.shape[0]), int(prog.G.shape[0])
+    A = sp.csc_matrix(prog.A)
+    G = sp.csc_matrix(prog.G)
+    A.sort_indices()
+    G.sort_indices()
     own = None
     for asm in _assemblers.values():
         last = getattr(asm, "last", None)
@@ -397,39 +403,36 @@ def precondition(prog):
             own = last[1]
             break
     if own is not None:  # device copy of exactly these values (to_program copied it out unchanged)
-        out = {k: own[k].clone() for k in ("A_indptr", "A_indices", "A_data", "b", "G_indptr", "G_indices", "G_data",
-                                           "h")}
+        out = {k: own[k] for k in ("A_indptr", "A_indices", "G_indptr", "G_indices")}
+        out.update({k: own[k].clone() for k in ("A_data", "b", "G_data", "h")})
     else:
-        def up(M):
-            M = sp.csc_matrix(M)
-            M.sort_indices()
-            return (torch.as_tensor(M.indptr.astype(np.int32), device=dev),
-                    torch.as_tensor(M.indices.astype(np.int32) if M.nnz else np.zeros(1, np.int32), device=dev),
-                    torch.as_tensor(M.data.astype(np.float64) if M.nnz else np.zeros(1), device=dev))
-
-        out = {}
-        for M, mat in (("A", prog.A), ("G", prog.G)):
-            out[f"{M}_indptr"], out[f"{M}_indices"], out[f"{M}_data"] = up(mat)
-        out["b"] = torch.as_tensor(np.ascontiguousarray(prog.b, dtype=np.float64).reshape(-1), device=dev)
-        out["h"] = torch.as_tensor(np.ascontiguousarray(prog.h, dtype=np.float64).reshape(-1), device=dev)
+        i32 = lambda a: torch.as_tensor(np.ascontiguousarray(a, dtype=np.int32) if a.size else np.zeros(1, np.int32),  # noqa
+                                        device=dev)
+        f64 = lambda a: torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64).reshape(-1) if np.size(a)  # noqa
+                                        else np.zeros(1), device=dev)
+        out = {"A_indptr": i32(A.indptr), "A_indices": i32(A.indices), "A_data": f64(A.data),
+               "G_indptr": i32(G.indptr), "G_indices": i32(G.indices), "G_data": f64(G.data),
+               "b": f64(prog.b), "h": f64(prog.h)}
     start, dim = soc_tables(int(cones.nonneg), tuple(cones.soc), dev)
-    max_nnz = max(int(prog.A.nnz), int(prog.G.nnz))
-    sA, sG = precondition_device(n, out, nA, nG, int(cones.nonneg), len(cones.soc), start, dim, None, max_nnz, stream)
-    host = {k: v.cpu().numpy() for k, v in out.items()}
-    mats = {}
-    for M, mat in (("A", prog.A), ("G", prog.G)):
-        indptr = host[f"{M}_indptr"]
-        nnz = int(indptr[-1])
-        mats[M] = sp.csc_matrix((host[f"{M}_data"][:nnz], host[f"{M}_indices"][:nnz], indptr), shape=mat.shape)
+    sA, sG = precondition_device(n, out, nA, nG, int(cones.nonneg), len(cones.soc), start, dim, None,
+                                 max(A.nnz, G.nnz), stream.cuda_stream)
+    # values come back into fresh pinned buffers: nnz prefixes only (pattern unchanged)
+    back = {"A": out["A_data"][: A.nnz], "G": out["G_data"][: G.nnz], "b": out["b"][:nA], "h": out["h"][:nG],
+            "sA": sA, "sG": sG}
+    pin = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in back.items()}
+    for k, v in back.items():
+        pin[k].copy_(v, non_blocking=True)
+    stream.synchronize()
+    h = {k: v.numpy() for k, v in pin.items()}
+    mats = {"A": sp.csc_matrix((h["A"], A.indices.copy(), A.indptr.copy()), shape=A.shape),
+            "G": sp.csc_matrix((h["G"], G.indices.copy(), G.indptr.copy()), shape=G.shape)}
     omega = max(1.0, float(np.max(np.abs(prog.c))) if prog.c.size else 0.0)
     if prog.P.nnz:
         omega = max(omega, float(np.max(np.abs(prog.P.data))))
     P = sp.csc_matrix(prog.P / omega)
     P.sort_indices()
-    scaled = ConicProgram(P=P, c=prog.c / omega, A=mats["A"], b=host["b"][:nA].copy(), G=mats["G"],
-                          h=host["h"][:nG].copy(), cones=cones)
-    prec = _preconditioner_type()(row_scale_A=sA.cpu().numpy().copy(), row_scale_G=sG.cpu().numpy().copy(),
-                                  var_scale=np.ones(n), cost_scale=omega)
+    scaled = ConicProgram(P=P, c=prog.c / omega, A=mats["A"], b=h["b"], G=mats["G"], h=h["h"], cones=cones)
+    prec = _preconditioner_type()(row_scale_A=h["sA"], row_scale_G=h["sG"], var_scale=np.ones(n), cost_scale=omega)
     return scaled, prec
 
 

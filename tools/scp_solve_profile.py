@@ -1,0 +1,69 @@
+"""configs[1]: the reference's own CI-SCVX loop (cito.scp.solve: backtracking
+homotopy + host IPM, unchanged) on HalfCheetah N=30 with the GPU drop-ins
+installed; per-iteration wall time of each stage.  (GPU box; needs the
+reference installed in baseline/_ref -- it runs through the jax shim, test
+infrastructure.)  Writes one JSON object to stdout.
+
+  python tools/scp_solve_profile.py [max_iters] [N]
+"""
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+os.environ.setdefault("CITO_REF_SRC", os.path.join(ROOT, "baseline", "_ref"))
+
+import ref_runner  # noqa: E402
+
+ref_runner.import_cito()
+from dataclasses import replace  # noqa: E402
+
+import torch  # noqa: E402
+from cito import ocp, scp  # noqa: E402
+
+import paper_2604_09993_b200.linearize as G  # noqa: E402
+import paper_2604_09993_b200.subproblem as SP  # noqa: E402
+from paper_2604_09993_b200 import install  # noqa: E402
+
+iters = int(sys.argv[1]) if len(sys.argv) > 1 else 3
+N = int(sys.argv[2]) if len(sys.argv) > 2 else 30
+sc = ocp.load_scenario(os.path.join(ref_runner.assets_dir(), "halfcheetah_bound.json"))
+sc = replace(sc, N=N, s_bounds=None)
+tr = ocp.get_transcription(sc)
+install(tr)
+times = {"linearize_all": [], "build_subproblem": [], "precondition": [], "ipm_solve": []}
+
+
+def timed(name, fn):
+    def w(*a, **k):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = fn(*a, **k)
+        torch.cuda.synchronize()
+        times[name].append(time.perf_counter() - t0)
+        return r
+    return w
+
+
+scp.linearize_all = timed("linearize_all", G.linearize_all)
+scp.build_subproblem = timed("build_subproblem", SP.build_subproblem)
+scp.precondition = timed("precondition", SP.precondition)
+scp.ipm_solve = timed("ipm_solve", scp.ipm_solve)
+# warm the GPU path (build + first-call setup) outside the measured loop
+z0 = tr.initial_guess()
+lin = G.linearize_all(tr, z0, 1.0)
+SP.precondition(SP.build_subproblem(tr, lin, z0, 1.0, scp.SCPConfig())[0])
+t0 = time.perf_counter()
+z, hist, status = scp.solve(sc, scp.SCPConfig(max_iters=iters))
+wall = time.perf_counter() - t0
+out = {"scenario": f"halfcheetah_bound N={N} (substeps {sc.substeps})", "iterations": len(hist) - 1,
+       "status": status, "wall_s": wall,
+       "per_iteration_ms": {k: [1e3 * x for x in v] for k, v in times.items()},
+       "mean_ms": {k: (1e3 * sum(v) / len(v) if v else None) for k, v in times.items()},
+       "delta": [h.delta for h in hist], "j_px": [h.j_px for h in hist], "j_ep": [h.j_ep for h in hist],
+       "note": "GPU: linearize_all + build_subproblem + precondition (drop-ins); host: the reference's IPM "
+               "(cito/_ipm.py) and homotopy, unchanged"}
+print(json.dumps(out))
