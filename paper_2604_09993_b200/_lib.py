@@ -12,6 +12,9 @@ from .model import Dims, ModelDesc
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 SO_PATH = os.path.join(_HERE, "_lib", "libcito_b200.so")
+# A/B builds of the same library for kernel experiments (tools/ only); in-tree like the product library
+if os.environ.get("CITO_LIB_VARIANT"):
+    SO_PATH = os.path.join(_HERE, "_lib", f"libcito_b200_{os.environ['CITO_LIB_VARIANT']}.so")
 
 CITO_OK, CITO_ERR_ARG, CITO_ERR_NONFINITE, CITO_ERR_CUDA, CITO_ERR_UNSUPPORTED = range(5)
 

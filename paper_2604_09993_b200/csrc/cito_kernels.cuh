@@ -25,6 +25,10 @@
 
 #include "models_gen.cuh"
 
+#ifndef CITO_COL_RC
+#define CITO_COL_RC 18  // rate rows per accumulator chunk of the column stage (register budget)
+#endif
+
 #define KMAX_L 16
 #define KMAX_J 16
 #define KMAX_C 8
@@ -1198,48 +1202,51 @@ __device__ __forceinline__ void col_stage(const KParams& P, FusedShared<M>& sh, 
     vals[kd] = val;
   }
   const double coef = uplus ? tau : (1.0 - tau);
-  double accs[NR];
-  if (isU) {
-    const double* Au = At[NDIRX + um];
+  // rate rows in chunks of RC so the accumulators of one chunk, the stage-input
+  // tangents and the column state fit the register budget (3 CTAs/SM variant)
+  constexpr int RC = CITO_COL_RC, NCH = (NR + RC - 1) / RC;
 #pragma unroll
-    for (int rr = 0; rr < NR; ++rr) accs[rr] = Au[rr] * coef;
-  } else {
+  for (int ch = 0; ch < NCH; ++ch) {
+    const int r0 = ch * RC;
+    double accs[RC];
 #pragma unroll
-    for (int rr = 0; rr < NR; ++rr) accs[rr] = 0.0;
-  }
+    for (int j = 0; j < RC; ++j) accs[j] = (isU && r0 + j < NR) ? At[NDIRX + um][r0 + j] * coef : 0.0;
 #pragma unroll
-  for (int kd = 0; kd < NDIRX; ++kd) {
-    const double vk = vals[kd];
+    for (int kd = 0; kd < NDIRX; ++kd) {
+      const double vk = vals[kd];
 #pragma unroll
-    for (int rr = 0; rr < NR; ++rr)
-      if (M::adep(rr, kd)) accs[rr] += At[kd][rr] * vk;
-  }
+      for (int j = 0; j < RC; ++j)
+        if (r0 + j < NR && M::adep(r0 + j, kd)) accs[j] += At[kd][r0 + j] * vk;
+    }
 #pragma unroll
-  for (int rr = 0; rr < NR; ++rr) {
-    const double dk = S * accs[rr] + dS * R.r[rr];
-    if (rr < NQ) {
-      const int hs = M::hslot(rr);
-      if (hs >= 0) {
-        if (I < 5) {
-          sh.KV[I][hs][col] = dk;
-        } else {
-          double incv = P.b[5] * dk, incq = 0.0;
+    for (int j = 0; j < RC; ++j) {
+      const int rr = r0 + j;
+      if (rr >= NR) break;
+      const double dk = S * accs[j] + dS * R.r[rr];
+      if (rr < NQ) {
+        const int hs = M::hslot(rr);
+        if (hs >= 0) {
+          if (I < 5) {
+            sh.KV[I][hs][col] = dk;
+          } else {
+            double incv = P.b[5] * dk, incq = 0.0;
 #pragma unroll
-          for (int l = 0; l < 5; ++l) {
-            const double kv = sh.KV[l][hs][col];
-            incv += P.b[l] * kv;
-            incq += P.e2[l] * kv;
+            for (int l = 0; l < 5; ++l) {
+              const double kv = sh.KV[l][hs][col];
+              incv += P.b[l] * kv;
+              incq += P.e2[l] * kv;
+            }
+            hq[hs] = hq[hs] + P.he1 * S * hv[hs] + S * incq + dS * sh.vbs[s & 1][rr];
+            hv[hs] = hv[hs] + h * incv;
           }
-          hq[hs] = hq[hs] + P.he1 * S * hv[hs] + S * incq + dS * sh.vbs[s & 1][rr];
-          hv[hs] = hv[hs] + h * incv;
+        } else {
+          const int p = M::pslot(rr);
+          sh.PV[p][col] += hb * dk;
+          sh.PQ[p][col] += S * P.e2[I] * dk + dS * hb * R.vs[rr];
         }
       } else {
-        const int p = M::pslot(rr);
-        sh.PV[p][col] += hb * dk;
-        sh.PQ[p][col] += S * P.e2[I] * dk + dS * hb * R.vs[rr];
+        sh.DY[rr - NQ][col] += hb * dk;
       }
-    } else {
-      sh.DY[rr - NQ][col] += hb * dk;
     }
   }
 }
