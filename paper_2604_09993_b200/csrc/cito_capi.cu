@@ -127,13 +127,30 @@ cito_status launch_linearize(const KParams& P, int64_t B, const double* xt0s, co
   return CITO_OK;
 }
 
+// Propagate: a warp-pair CTA per interval (k_linearize2<M, 1, false>: critical
+// chain + off-chain warp, ~2x lower latency) while the grid fits the SMs once,
+// else one thread per interval (k_primal, throughput).
 template <class M>
 cito_status launch_propagate(const KParams& P, int64_t B, const double* xt0s, const double* Us, const double* Ss,
                              double* ends, int32_t* bad, cudaStream_t st) {
   if (B <= 0) return CITO_OK;
-  const int nt = 64;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   count_launch();
-  k_primal<M, false><<<(unsigned)((B + nt - 1) / nt), nt, 0, st>>>(P, B, xt0s, Us, Ss, ends, bad, nullptr, nullptr);
+  if (B <= sms && k1_version() != 1) {
+    static bool attr_done = false;
+    const size_t smem = sizeof(Fused2Shared<M>);
+    if (!attr_done) {
+      CUDA_TRY(cudaFuncSetAttribute(k_linearize2<M, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr_done = true;
+    }
+    k_linearize2<M, 1, false><<<(unsigned)B, 64, smem, st>>>(P, B, xt0s, Us, Ss, ends, nullptr, nullptr, nullptr, bad,
+                                                             ZSrc{});
+  } else {
+    const int nt = 64;
+    k_primal<M, false><<<(unsigned)((B + nt - 1) / nt), nt, 0, st>>>(P, B, xt0s, Us, Ss, ends, bad, nullptr, nullptr);
+  }
   CUDA_TRY(cudaGetLastError());
   return CITO_OK;
 }

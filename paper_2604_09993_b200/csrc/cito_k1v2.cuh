@@ -741,8 +741,10 @@ __device__ __forceinline__ void col_stage2(const KParams& P, Fused2Shared<M>& sh
   }
 }
 
-template <class M, int MINB>
-__global__ void __launch_bounds__(K2Dims<M>::NT, MINB) k_linearize2(const KParams P, int64_t B,
+// JAC = false: the primal flow only (propagate for small batches): warps 0 and 1
+// (critical chain + off-chain aux for the y rows), end states + finite flags.
+template <class M, int MINB, bool JAC = true>
+__global__ void __launch_bounds__(JAC ? K2Dims<M>::NT : 64, MINB) k_linearize2(const KParams P, int64_t B,
                                                                     const double* __restrict__ xt0s,
                                                                     const double* __restrict__ Us,
                                                                     const double* __restrict__ Ss,
@@ -794,10 +796,11 @@ __global__ void __launch_bounds__(K2Dims<M>::NT, MINB) k_linearize2(const KParam
     }
   }
   // warp 1: y row `lane` and the stage velocities of q coordinate `lane`
-  if (warp == K::W_AUX && lane < NY) RS_YV = src_x[NX + lane];
+  constexpr int W_AUX = JAC ? K::W_AUX : 1;
+  if (warp == W_AUX && lane < NY) RS_YV = src_x[NX + lane];
   // column threads
   const int col = tid - 32 * K::W_COL0;
-  const bool colthr = warp >= K::W_COL0 && warp < K::W_COL0 + K::NCW && col < NCOL;
+  const bool colthr = JAC && warp >= K::W_COL0 && warp < K::W_COL0 + K::NCW && col < NCOL;
   const double dS = (col == NCOL - 1) ? 1.0 : 0.0;
   const int sc = (col >= 0 && col < M::NHCOL) ? M::hcol(col) : -1;
   const int uj = col - M::NHCOL;
@@ -822,7 +825,7 @@ __global__ void __launch_bounds__(K2Dims<M>::NT, MINB) k_linearize2(const KParam
   __syncthreads();
   const double S = sh.S, h = P.h;
   const int NST = 6 * P.substeps;
-  for (int t = 0; t < NST + 3; ++t) {
+  for (int t = 0; t < NST + (JAC ? 3 : 1); ++t) {
     CITO_MARK((t * 8 + (warp < 8 ? warp : 7)) * 2);
     if (warp == 0) {
       if (t < NST) {
@@ -875,9 +878,9 @@ __global__ void __launch_bounds__(K2Dims<M>::NT, MINB) k_linearize2(const KParam
           }
         }
       }
-    } else if (warp == K::W_AUX) {
+    } else if (warp == W_AUX) {
       if (t >= 1 && t <= NST) aux_stage<M>(P, sh, t - 1, lane, rs);
-    } else if (warp == K::W_JQV || warp == K::W_JU) {
+    } else if (JAC && (warp == K::W_JQV || warp == K::W_JU)) {
       if (t >= 2 && t <= NST + 1) {
         const int st = t - 2;
         const Rec2<M>& R = sh.ring[st & 3];
@@ -890,7 +893,7 @@ __global__ void __launch_bounds__(K2Dims<M>::NT, MINB) k_linearize2(const KParam
             tan_rate_k<M, 4>(P, R.pr, v, NX + (kd - NDIRX), &sh.At[st & 1][kd][0]);
         }
       }
-    } else if (colthr && t >= 3) {
+    } else if (JAC && colthr && t >= 3) {
       const int st = t - 3;
       col_stage2<M>(P, sh, sh.ring[st & 3], sh.At[st & 1], st / 6, st % 6, col, S, dS, isU, um, uplus, rs);
     }
@@ -904,9 +907,10 @@ __global__ void __launch_bounds__(K2Dims<M>::NT, MINB) k_linearize2(const KParam
       const int k = lane + 32 * p;
       if (k < NX) sh.x[k] = RS_XR(p);
     }
-  } else if (warp == K::W_AUX && lane < NY) {
+  } else if (warp == W_AUX && lane < NY) {
     sh.x[NX + lane] = RS_YV;
   }
+  if constexpr (JAC) {
   double* jxb = jx + b * NXT * NXT;
   double* jub = ju + b * NXT * 2 * NU;
   double* jsb = js + b * NXT;
@@ -952,6 +956,7 @@ __global__ void __launch_bounds__(K2Dims<M>::NT, MINB) k_linearize2(const KParam
     const int r = e / Pos<NY>::v, c = NX + e % Pos<NY>::v;
     jxb[r * NXT + c] = (r == c) ? 1.0 : 0.0;
   }
+  }  // JAC
   __syncthreads();
   for (int k = tid; k < NXT; k += blockDim.x) {
     const double e = sh.x[k];
