@@ -565,7 +565,7 @@ def _lib_launches():
     """Kernels launched by libcito_b200 so far (global counter of the C ABI)."""
     from paper_2604_09993_b200 import _lib
 
-    return int(_lib.lib().cito_launch_count(None))
+    return _lib.launch_count()
 
 
 def _assembler_of(trs):

@@ -171,6 +171,15 @@ cito_status cito_linearize_all_dev(cito_handle* h, int32_t N, int32_t n_problems
                                    double* defects, int32_t* bad, double* psi, double* psi_jac, double* theta,
                                    double* theta_jac, double* imp, double* imp_jac, void* stream);
 
+/* Same as cito_linearize_all_dev with the relaxation parameters read from
+ * device memory (d_delta_eps = {delta, epsilon}), so one captured CUDA graph of
+ * an SCP iteration replays for every delta of the homotopy (scp.py:354-380). */
+cito_status cito_linearize_all_dev2(cito_handle* h, int32_t N, int32_t n_problems, int64_t zstride, int64_t base_u,
+                                    int64_t base_p, const double* z, const double* d_delta_eps, double* ends,
+                                    double* jx, double* ju, double* js, double* defects, int32_t* bad, double* psi,
+                                    double* psi_jac, double* theta, double* theta_jac, double* imp, double* imp_jac,
+                                    void* stream);
+
 /* Multiple-shooting rows of the SCP subproblem, written straight into CSC value
  * slots (cito/scp.py:226-236 + cito/conic.py:209-269).  The slot map is built
  * once per sparsity pattern by the host (paper_2604_09993_b200/scatter.py):

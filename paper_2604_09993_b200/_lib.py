@@ -71,6 +71,9 @@ def _load():
                                              + [_dp] * 13)
         L.cito_audit_dev.restype = ctypes.c_int
         L.cito_audit_dev.argtypes = [ctypes.c_void_p, ctypes.c_int64, _dp, ctypes.c_int64] + [_dp] * 5
+        L.cito_linearize_all_dev2.restype = ctypes.c_int
+        L.cito_linearize_all_dev2.argtypes = ([ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64,
+                                               ctypes.c_int64, ctypes.c_int64, _dp, _dp] + [_dp] * 13)
         L.cito_csc_assemble_dev.restype = ctypes.c_int
         L.cito_csc_assemble_dev.argtypes = [ctypes.c_int32] + [_dp] * 12
         L.cito_csc_assemble2_dev.restype = ctypes.c_int
@@ -89,6 +92,19 @@ def _load():
 
 def lib():
     return _load()
+
+
+_graph_launches = 0  # library kernels launched through CUDA-graph replays (not seen by the C counter)
+
+
+def add_graph_launches(n):
+    global _graph_launches
+    _graph_launches += int(n)
+
+
+def launch_count():
+    """Kernels of this library launched so far: direct launches (C counter) + graph replays."""
+    return int(lib().cito_launch_count(None)) + _graph_launches
 
 
 def check(status, what=""):

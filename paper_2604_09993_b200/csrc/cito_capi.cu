@@ -486,10 +486,11 @@ cito_status cito_propagate_host(cito_handle* h, int64_t B, const double* xt0s, c
   return count_bad(bad, B);
 }
 
-cito_status cito_linearize_all_dev(cito_handle* h, int32_t N, int32_t n_problems, int64_t zstride, int64_t base_u,
-                                   int64_t base_p, const double* z, double delta, double epsilon, double* ends, double* jx, double* ju, double* js,
-                                   double* defects, int32_t* bad, double* psi, double* psi_jac, double* theta,
-                                   double* theta_jac, double* imp, double* imp_jac, void* stream) {
+static cito_status linearize_all_impl(cito_handle* h, int32_t N, int32_t n_problems, int64_t zstride, int64_t base_u,
+                                      int64_t base_p, const double* z, double delta, double epsilon,
+                                      const double* d_delta_eps, double* ends, double* jx, double* ju, double* js,
+                                      double* defects, int32_t* bad, double* psi, double* psi_jac, double* theta,
+                                      double* theta_jac, double* imp, double* imp_jac, void* stream) {
   if (!h) return fail(CITO_ERR_ARG, "null handle");
   if (N < 2) return fail(CITO_ERR_ARG, "need at least two grid nodes");
   if (n_problems < 1) return fail(CITO_ERR_ARG, "n_problems must be >= 1");
@@ -501,7 +502,7 @@ cito_status cito_linearize_all_dev(cito_handle* h, int32_t N, int32_t n_problems
     CUDA_TRY(cudaEventCreateWithFlags(&h->ev_in, cudaEventDisableTiming));
     CUDA_TRY(cudaEventCreateWithFlags(&h->ev_out, cudaEventDisableTiming));
   }
-  const ZSrc zs{z, base_u, base_p, defects, zstride, N - 1, N};
+  const ZSrc zs{z, base_u, base_p, defects, zstride, N - 1, N, d_delta_eps};
   // node relations (K3) on the auxiliary stream, concurrently with the interval kernel (K1)
   CUDA_TRY(cudaEventRecord(h->ev_in, s));
   CUDA_TRY(cudaStreamWaitEvent(h->aux, h->ev_in, 0));
@@ -514,6 +515,24 @@ cito_status cito_linearize_all_dev(cito_handle* h, int32_t N, int32_t n_problems
   CUDA_TRY(cudaStreamWaitEvent(s, h->ev_out, 0));
   __atomic_add_fetch(&h->launches, 2, __ATOMIC_RELAXED);
   return CITO_OK;
+}
+
+cito_status cito_linearize_all_dev(cito_handle* h, int32_t N, int32_t n_problems, int64_t zstride, int64_t base_u,
+                                   int64_t base_p, const double* z, double delta, double epsilon, double* ends, double* jx, double* ju, double* js,
+                                   double* defects, int32_t* bad, double* psi, double* psi_jac, double* theta,
+                                   double* theta_jac, double* imp, double* imp_jac, void* stream) {
+  return linearize_all_impl(h, N, n_problems, zstride, base_u, base_p, z, delta, epsilon, nullptr, ends, jx, ju, js,
+                            defects, bad, psi, psi_jac, theta, theta_jac, imp, imp_jac, stream);
+}
+
+cito_status cito_linearize_all_dev2(cito_handle* h, int32_t N, int32_t n_problems, int64_t zstride, int64_t base_u,
+                                    int64_t base_p, const double* z, const double* d_delta_eps, double* ends,
+                                    double* jx, double* ju, double* js, double* defects, int32_t* bad, double* psi,
+                                    double* psi_jac, double* theta, double* theta_jac, double* imp, double* imp_jac,
+                                    void* stream) {
+  if (!d_delta_eps) return fail(CITO_ERR_ARG, "null delta/epsilon pointer");
+  return linearize_all_impl(h, N, n_problems, zstride, base_u, base_p, z, 0.0, 0.0, d_delta_eps, ends, jx, ju, js,
+                            defects, bad, psi, psi_jac, theta, theta_jac, imp, imp_jac, stream);
 }
 
 cito_status cito_scatter_dynamics_dev(cito_handle* h, int64_t n_int, const double* ends, const double* jx,

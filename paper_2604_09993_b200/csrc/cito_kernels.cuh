@@ -95,6 +95,7 @@ struct ZSrc {
   int64_t zstride;  // distance between the decision vectors of consecutive problems (multi-start batches)
   int32_t n_int;    // intervals per problem (N - 1)
   int32_t n_node;   // nodes per problem (N)
+  const double* de;  // optional device [delta, epsilon] (graph replays with changing delta)
 };
 
 template <int N>

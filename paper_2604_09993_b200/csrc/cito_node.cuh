@@ -303,6 +303,10 @@ __global__ void __launch_bounds__(64) k_node(const KParams P, int64_t Np, int64_
   constexpr int NL = M::NL, NC = M::NC, NQ = 3 * NL, NY = 5 * NC + M::NGO;
   constexpr int NPSI = 3 * NC + M::NGO, NV = 3 * NQ + 3 * NC, NI = 3 * NQ + 2 * NC;
   constexpr int NXT = 2 * NQ + NY;
+  if (zs.de) {  // relaxation parameters from device memory (CUDA-graph replays)
+    delta = zs.de[0];
+    eps = zs.de[1];
+  }
   // item space: [Np * 2NY psi columns][Nn * NV theta columns][Nn * NI impulse columns]
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n_psi = Np * (2 * NY), n_th = Nn * NV, n_imp = Nn * NI;

@@ -712,9 +712,7 @@ class GpuSCPStep:
     reference (augmentation.py:231-233).
     Returns (LinearizedProblem (lazy, device-backed), ConicProgram, meta)."""
 
-    def __init__(self, tr_or_scenario, w_prox=2000.0, w_ep=50000.0, device=None):
-        import torch
-
+    def __init__(self, tr_or_scenario, w_prox=2000.0, w_ep=50000.0, device=None, use_graph=True):
         from .linearize import GpuTranscription, LazyLinearizedProblem
         from .scenario import build_scaling
 
@@ -726,6 +724,7 @@ class GpuSCPStep:
         self._Lazy = LazyLinearizedProblem
         self._plan = None
         self._last_lin = None
+        self.use_graph = use_graph
 
     # -- one-time plan: buffers + constant ctypes argument tables
     def _build_plan(self):
@@ -757,8 +756,11 @@ class GpuSCPStep:
                       ("A_data", fd, dA["nsup"]), ("G_data", fd, dG["nsup"]),
                       ("A_indices", i32, dA["nsup"]), ("G_indices", i32, dG["nsup"])], dev)
         lin["bad"] = pk.d["bad"]
-        z_dev = torch.empty(lay.dim, **f64)
-        z_pin = torch.empty(lay.dim, dtype=torch.float64, pin_memory=True)
+        # z followed by [delta, epsilon]: one H2D per call, read by the kernels from device
+        # memory so a captured graph replays for any delta of the homotopy
+        zde_dev = torch.empty(lay.dim + 2, **f64)
+        zde_pin = torch.empty(lay.dim + 2, dtype=torch.float64, pin_memory=True)
+        z_dev = zde_dev[: lay.dim]
         rowmax = torch.empty(max(1, nA + nG), dtype=i64, device=dev)
         arr = lambda xs: ctypes_ptr_array([x.data_ptr() for x in xs])  # noqa: E731
         mats = [dA, dG]
@@ -789,17 +791,56 @@ class GpuSCPStep:
                    soc_start.data_ptr(), soc_dim.data_ptr(), rowmax[:nA].data_ptr(), rowmax[nA:].data_ptr(), 1,
                    max(dA["nsup"], dG["nsup"]), pk.d["row_scale_A"].data_ptr(), pk.d["row_scale_G"].data_ptr())
         o = lin
-        lin_args = (gt.disc._h.ptr, N, 1, int(lay.dim), int(gt.base_u), int(gt.base_p), z_dev.data_ptr())
+        lin_args = (gt.disc._h.ptr, N, 1, int(lay.dim), int(gt.base_u), int(gt.base_p), z_dev.data_ptr(),
+                    zde_dev[lay.dim:].data_ptr())
         lin_outs = tuple(o[kk].data_ptr() for kk in ("ends", "jx", "ju", "js", "defects", "bad", "psi", "psi_jac",
                                                      "theta", "theta_jac", "imp_v", "imp_jac"))
         dim = lay.dim
         P_idx = np.arange(dim, dtype=np.int32)
         P_ptr = np.concatenate([np.arange(dim + 1), np.full(pat.n - dim, dim)]).astype(np.int32)
-        self._plan = dict(lin=lin, pk=pk, z_dev=z_dev, z_pin=z_pin, rowmax=rowmax, rhs_dev=rhs_dev,
+        self._plan = dict(lin=lin, pk=pk, z_dev=z_dev, zde_dev=zde_dev, zde_pin=zde_pin, rowmax=rowmax, rhs_dev=rhs_dev,
+                          graphs={}, graph_kernels={},
                           rhs_const=r["const"], asm_args=asm_args, rm_arr=rm_arr, rhs_args=rhs_args,
                           pc_args=pc_args, lin_args=lin_args, lin_outs=lin_outs, keep=keep, L=L, nA=nA, nG=nG,
                           soc=(soc_start, soc_dim), P_idx=P_idx, P_ptr=P_ptr,
                           P_plain=None, meta=_Meta(pat.z_idx, pat.sp_idx, pat.sm_idx, pat.t_idx))
+
+    def _launch(self, precondition):
+        """The device work of one iteration on the current stream: H2D of
+        [z, delta, epsilon], K1 + K3, CSC assembly, rhs, optional row scaling,
+        D2H of the packed result."""
+        import torch
+
+        pl = self._plan
+        L = pl["L"]
+        s = torch.cuda.current_stream(self.gt.device).cuda_stream
+        pl["zde_dev"].copy_(pl["zde_pin"], non_blocking=True)
+        _lib.check(L.cito_linearize_all_dev2(*pl["lin_args"], *pl["lin_outs"], s), "linearize_all")
+        if precondition:
+            pl["rowmax"].zero_()
+        _lib.check(L.cito_csc_assemble2_dev(*pl["asm_args"], pl["rm_arr"] if precondition else None, s),
+                   "csc_assemble")
+        pl["rhs_dev"].copy_(pl["rhs_const"])
+        _lib.check(L.cito_rhs_dev(*pl["rhs_args"], s), "rhs")
+        if precondition:
+            _lib.check(L.cito_precondition_dev(*pl["pc_args"], s), "precondition")
+        pl["pk"].host.copy_(pl["pk"].dev, non_blocking=True)
+
+    def _capture(self, precondition):
+        """Capture _launch as a CUDA graph (after one eager run that performs the
+        library's first-call setup); one replay per iteration afterwards."""
+        import torch
+
+        pl = self._plan
+        self._launch(precondition)
+        torch.cuda.current_stream(self.gt.device).synchronize()
+        g = torch.cuda.CUDAGraph()
+        n0 = int(pl["L"].cito_launch_count(None))
+        with torch.cuda.graph(g):
+            self._launch(precondition)
+        pl["graph_kernels"][precondition] = int(pl["L"].cito_launch_count(None)) - n0
+        pl["graphs"][precondition] = g
+        return g
 
     def iterate(self, z, delta, z_j=None, epsilon=None, precondition=False):
         """Returns (lin, prog, meta); with ``precondition`` the program comes back
@@ -823,24 +864,21 @@ class GpuSCPStep:
         if epsilon is None:
             epsilon = gt.scenario.ctcs_epsilon
         stream = torch.cuda.current_stream(gt.device)
-        s = stream.cuda_stream
-        L = pl["L"]
-        pl["z_pin"].numpy()[:] = z
-        pl["z_dev"].copy_(pl["z_pin"], non_blocking=True)
-        _lib.check(L.cito_linearize_all_dev(*pl["lin_args"], float(delta), float(epsilon), *pl["lin_outs"], s),
-                   "linearize_all")
-        if precondition:
-            pl["rowmax"].zero_()
-        _lib.check(L.cito_csc_assemble2_dev(*pl["asm_args"], pl["rm_arr"] if precondition else None, s),
-                   "csc_assemble")
-        rhs = pl["rhs_dev"]
-        rhs.copy_(pl["rhs_const"])
-        _lib.check(L.cito_rhs_dev(*pl["rhs_args"], s), "rhs")
+        zp = pl["zde_pin"].numpy()
+        dim = pat.lay.dim
+        zp[:dim] = z
+        zp[dim] = float(delta)
+        zp[dim + 1] = float(epsilon)
+        if self.use_graph:
+            g = pl["graphs"].get(bool(precondition))
+            if g is None:
+                g = self._capture(bool(precondition))
+            g.replay()
+            _lib.add_graph_launches(pl["graph_kernels"][bool(precondition)])
+        else:
+            self._launch(bool(precondition))
         pk = pl["pk"]
         nA = pl["nA"]
-        if precondition:
-            _lib.check(L.cito_precondition_dev(*pl["pc_args"], s), "precondition")
-        pk.host.copy_(pk.dev, non_blocking=True)
         stream.synchronize()  # the one synchronization
         hh = pk.h
         bad = hh["bad"]

@@ -211,3 +211,27 @@ def test_gpu_precondition_reference_unit_cases():
         so, ss = prog.h - prog.G @ xv, scaled.h - scaled.G @ xv
         blk_o, blk_s = so[2:5], ss[2:5]
         assert (blk_o[0] >= np.linalg.norm(blk_o[1:])) == (blk_s[0] >= np.linalg.norm(blk_s[1:]))
+
+
+@pytest.mark.gpu
+def test_gpu_scp_step_graph_replay_equals_eager():
+    """GpuSCPStep replays one captured CUDA graph per iteration; delta/epsilon are
+    read from device memory, so every delta of the homotopy must give exactly the
+    eager result (same kernels, same order)."""
+    from paper_2604_09993_b200.subproblem import GpuSCPStep
+
+    name = "halfcheetah_n30"
+    g = load_golden(name)
+    sc = golden_scenario(name)
+    sg, se = GpuSCPStep(sc, use_graph=True), GpuSCPStep(sc, use_graph=False)
+    z = g["ig_z"]
+    for delta, pc in ((1.0, False), (0.3, False), (0.05, True), (0.7, True), (0.2, False)):
+        rg, re_ = sg.iterate(z, delta, precondition=pc), se.iterate(z, delta, precondition=pc)
+        pg, pe = rg[1], re_[1]
+        for M in ("A", "G"):
+            a, b = getattr(pg, M), getattr(pe, M)
+            assert np.array_equal(a.indptr, b.indptr) and np.array_equal(a.indices, b.indices)
+            assert np.array_equal(a.data, b.data)
+        assert np.array_equal(pg.b, pe.b) and np.array_equal(pg.h, pe.h) and np.array_equal(pg.c, pe.c)
+        assert np.array_equal(rg[0].psi, re_[0].psi) and np.array_equal(rg[0].theta_jac, re_[0].theta_jac)
+    assert sg._plan["graph_kernels"][False] >= 5 and len(sg._plan["graphs"]) == 2
