@@ -263,11 +263,16 @@ def run_ours(args):
 
     rank, world, local = env_rank()
     dist = None
+    # CITO_BENCH_BACKEND=gloo + CITO_BENCH_DEVICE=0 exercise the multi-rank code path
+    # with several ranks on one GPU (test only: no kernel waits on another rank)
+    backend = os.environ.get("CITO_BENCH_BACKEND", "nccl")
+    if os.environ.get("CITO_BENCH_DEVICE") is not None:
+        local = int(os.environ["CITO_BENCH_DEVICE"])
     if world > 1:
         import torch.distributed as dist
 
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        dist.init_process_group(backend)
     dev = torch.device("cuda", local if world > 1 else 0)
     torch.cuda.set_device(dev)
     from paper_2604_09993_b200 import synth
