@@ -26,6 +26,10 @@
 
 #include "cito_kernels.cuh"
 
+#ifndef CITO_V2_SPLIT
+#define CITO_V2_SPLIT 0  // 1: separate q and v rate-Jacobian warps (7 warps)
+#endif
+
 // ---------------------------------------------------------------------------
 // Rate-Jacobian column of one input direction, specialised on the direction
 // kind (1: q, 2: v, 3: u): the derivative of prim_rate restricted to the seed
@@ -286,8 +290,14 @@ struct K2Dims {
   // distinct SM sub-partitions (warp w -> SMSP w % 4) and only the light ones
   // (off-chain aux, u Jacobian) share: 0 primal, 1..NCW columns, then q/v
   // Jacobian, aux, u Jacobian
-  static constexpr int W_COL0 = 1, W_JQV = 1 + NCW, W_AUX = 2 + NCW, W_JU = 3 + NCW;
+#if CITO_V2_SPLIT
+  // 7 warps: separate q and v Jacobian warps (0 primal, cols, q, aux, v, u)
+  static constexpr int W_COL0 = 1, W_JQV = 1 + NCW, W_AUX = 2 + NCW, W_JV = 3 + NCW, W_JU = 4 + NCW;
+  static constexpr int NT = 32 * (5 + NCW);
+#else
+  static constexpr int W_COL0 = 1, W_JQV = 1 + NCW, W_AUX = 2 + NCW, W_JU = 3 + NCW, W_JV = -1;
   static constexpr int NT = 32 * (4 + NCW);
+#endif
   static constexpr int NX = D::NX;
   static constexpr int PER = (NX + 31) / 32;  // state coordinates per lane of warp 0
   static constexpr int count_q() {
@@ -880,12 +890,18 @@ __global__ void __launch_bounds__(JAC ? K2Dims<M>::NT : 64, MINB) k_linearize2(c
       }
     } else if (warp == W_AUX) {
       if (t >= 1 && t <= NST) aux_stage<M>(P, sh, t - 1, lane, rs);
-    } else if (JAC && (warp == K::W_JQV || warp == K::W_JU)) {
+    } else if (JAC && (warp == K::W_JQV || warp == K::W_JU || warp == K::W_JV)) {
       if (t >= 2 && t <= NST + 1) {
         const int st = t - 2;
         const Rec2<M>& R = sh.ring[st & 3];
         const double* v = R.xs + NQ;
-        if (warp == K::W_JQV) {  // q and v directions (kinds 1 | 2)
+        if (K::W_JV >= 0 && warp == K::W_JQV) {  // q directions (kind 1)
+          for (int kd = lane; kd < K::NDIRQ; kd += 32)
+            tan_rate_k<M, 1>(P, R.pr, v, M::dir(kd), &sh.At[st & 1][kd][0]);
+        } else if (K::W_JV >= 0 && warp == K::W_JV) {  // v directions (kind 2)
+          for (int kd = K::NDIRQ + lane; kd < NDIRX; kd += 32)
+            tan_rate_k<M, 2>(P, R.pr, v, M::dir(kd), &sh.At[st & 1][kd][0]);
+        } else if (warp == K::W_JQV) {  // q and v directions (kinds 1 | 2)
           for (int kd = lane; kd < NDIRX; kd += 32)
             tan_rate_k<M, 3>(P, R.pr, v, M::dir(kd), &sh.At[st & 1][kd][0]);
         } else {  // control directions (kind 4)
