@@ -673,32 +673,30 @@ __device__ __forceinline__ void col_stage2(const KParams& P, Fused2Shared<M>& sh
     for (int p = 0; p < M::NPUSH; ++p) sh.PQ[p][col] += P.he1 * S * sh.PV[p][col];
   }
   // stage coefficients, once per tick (warp-uniform): S h^2 sum a a (q rows), h a (v rows)
-  double cqs[5], has[5];
-#pragma unroll
-  for (int l = 0; l < 5; ++l) {
-    cqs[l] = S * P.cq[I][l];
-    has[l] = P.ha[I][l];
-  }
+  // stage-input tangents along the rate-Jacobian directions: base value, then the
+  // history terms in stage order (a runtime loop of I steps over all directions:
+  // no predicated dead terms, one small loop body)
   const double shc = S * P.hc1[I];
   double vals[Pos<NDIRX>::v];
 #pragma unroll
   for (int kd = 0; kd < NDIRX; ++kd) {
     const int d = M::dir(kd);
-    double val;
     if (d < NQ) {
       const int hs = M::hslot(d);
-      val = RS_HQ(hs) + shc * RS_HV(hs) + dS * R.wq[d];
-#pragma unroll
-      for (int l = 0; l < 5; ++l)
-        if (l < I) val += cqs[l] * sh.KV[l][hs][col];
+      vals[kd] = RS_HQ(hs) + shc * RS_HV(hs) + dS * R.wq[d];
     } else {
-      const int hs = M::hslot(d - NQ);
-      val = RS_HV(hs);
-#pragma unroll
-      for (int l = 0; l < 5; ++l)
-        if (l < I) val += has[l] * sh.KV[l][hs][col];
+      vals[kd] = RS_HV(M::hslot(d - NQ));
     }
-    vals[kd] = val;
+  }
+#pragma unroll 1
+  for (int l = 0; l < I; ++l) {
+    const double cq = S * P.cq[I][l], ca = P.ha[I][l];
+#pragma unroll
+    for (int kd = 0; kd < NDIRX; ++kd) {
+      const int d = M::dir(kd);
+      const int hs = M::hslot(d < NQ ? d : d - NQ);
+      vals[kd] += (d < NQ ? cq : ca) * sh.KV[l][hs][col];
+    }
   }
   const double coef = uplus ? tau : (1.0 - tau);
   // rate rows in chunks of RC so the accumulators of one chunk, the stage-input

@@ -1182,25 +1182,29 @@ __device__ __forceinline__ void col_stage(const KParams& P, FusedShared<M>& sh, 
 #pragma unroll
     for (int p = 0; p < M::NPUSH; ++p) sh.PQ[p][col] += P.he1 * S * sh.PV[p][col];
   }
+  // stage-input tangents along the rate-Jacobian directions: base value, then the
+  // history terms in stage order (a runtime loop of I steps over all directions:
+  // no predicated dead terms, one small loop body)
   double vals[Pos<NDIRX>::v];
 #pragma unroll
   for (int kd = 0; kd < NDIRX; ++kd) {
     const int d = M::dir(kd);
-    double val;
     if (d < NQ) {
       const int hs = M::hslot(d);
-      val = hq[hs] + S * P.hc1[I] * hv[hs] + dS * R.wq[d];
-#pragma unroll
-      for (int l = 0; l < 5; ++l)
-        if (l < I) val += S * P.cq[I][l] * sh.KV[l][hs][col];
+      vals[kd] = hq[hs] + S * P.hc1[I] * hv[hs] + dS * R.wq[d];
     } else {
-      const int hs = M::hslot(d - NQ);
-      val = hv[hs];
-#pragma unroll
-      for (int l = 0; l < 5; ++l)
-        if (l < I) val += P.ha[I][l] * sh.KV[l][hs][col];
+      vals[kd] = hv[M::hslot(d - NQ)];
     }
-    vals[kd] = val;
+  }
+#pragma unroll 1
+  for (int l = 0; l < I; ++l) {
+    const double cq = S * P.cq[I][l], ca = P.ha[I][l];
+#pragma unroll
+    for (int kd = 0; kd < NDIRX; ++kd) {
+      const int d = M::dir(kd);
+      const int hs = M::hslot(d < NQ ? d : d - NQ);
+      vals[kd] += (d < NQ ? cq : ca) * sh.KV[l][hs][col];
+    }
   }
   const double coef = uplus ? tau : (1.0 - tau);
   // rate rows in chunks of RC so the accumulators of one chunk, the stage-input
