@@ -677,9 +677,9 @@ def build_subproblem(tr, lin, z_j, delta, config):
 
 
 class _Packed:
-    """One device buffer (and its pinned host mirror) holding every per-iteration
-    output of GpuSCPStep at fixed offsets, so the whole result comes back with a
-    single device->host copy and every kernel argument is a constant pointer."""
+    """One device buffer holding every per-iteration output of GpuSCPStep at fixed
+    offsets, so the whole result comes back with a single device->host copy and
+    every kernel argument is a constant pointer."""
 
     def __init__(self, fields, device):
         import torch
@@ -692,11 +692,35 @@ class _Packed:
             off += max(1, int(n)) * isz
         self.nbytes = (off + 255) // 256 * 256
         self.dev = torch.empty(self.nbytes, dtype=torch.uint8, device=device)
-        self.host = torch.empty(self.nbytes, dtype=torch.uint8, pin_memory=True)
-        self.d, self.h = {}, {}
+        self.d = {}
         for name, (o, dtype, n, isz) in self.layout.items():
             self.d[name] = self.dev[o: o + max(1, n) * isz].view(dtype)[:n]
-            self.h[name] = self.host[o: o + max(1, n) * isz].view(dtype)[:n].numpy()
+
+
+class _HostBuf:
+    """A pinned host mirror of a _Packed buffer whose arrays are handed out
+    without copying.  It is free again once no array viewing it is alive: every
+    view's numpy base is `self.nb`, so its reference count tells."""
+
+    def __init__(self, pk):
+        import torch
+
+        self.host = torch.empty(pk.nbytes, dtype=torch.uint8, pin_memory=True)
+        self.nb = self.host.numpy()
+        self.h = {}
+        for name, (o, dtype, n, isz) in pk.layout.items():
+            npdt = torch.empty((), dtype=dtype).numpy().dtype
+            self.h[name] = self.nb[o: o + max(1, n) * isz].view(npdt)[:n]
+        self.graphs = {}
+        self._base = None
+
+    def free(self):
+        import sys as _sys
+
+        rc = _sys.getrefcount(self.nb)
+        if self._base is None:
+            self._base = rc
+        return rc <= self._base
 
 
 class GpuSCPStep:
@@ -799,16 +823,16 @@ class GpuSCPStep:
         P_idx = np.arange(dim, dtype=np.int32)
         P_ptr = np.concatenate([np.arange(dim + 1), np.full(pat.n - dim, dim)]).astype(np.int32)
         self._plan = dict(lin=lin, pk=pk, z_dev=z_dev, zde_dev=zde_dev, zde_pin=zde_pin, rowmax=rowmax, rhs_dev=rhs_dev,
-                          graphs={}, graph_kernels={},
+                          hosts=[], graph_kernels={},
                           rhs_const=r["const"], asm_args=asm_args, rm_arr=rm_arr, rhs_args=rhs_args,
                           pc_args=pc_args, lin_args=lin_args, lin_outs=lin_outs, keep=keep, L=L, nA=nA, nG=nG,
                           soc=(soc_start, soc_dim), P_idx=P_idx, P_ptr=P_ptr,
                           P_plain=None, meta=_Meta(pat.z_idx, pat.sp_idx, pat.sm_idx, pat.t_idx))
 
-    def _launch(self, precondition):
+    def _launch(self, precondition, hb):
         """The device work of one iteration on the current stream: H2D of
         [z, delta, epsilon], K1 + K3, CSC assembly, rhs, optional row scaling,
-        D2H of the packed result."""
+        D2H of the packed result into the pinned host buffer `hb`."""
         import torch
 
         pl = self._plan
@@ -824,22 +848,34 @@ class GpuSCPStep:
         _lib.check(L.cito_rhs_dev(*pl["rhs_args"], s), "rhs")
         if precondition:
             _lib.check(L.cito_precondition_dev(*pl["pc_args"], s), "precondition")
-        pl["pk"].host.copy_(pl["pk"].dev, non_blocking=True)
+        hb.host.copy_(pl["pk"].dev, non_blocking=True)
 
-    def _capture(self, precondition):
-        """Capture _launch as a CUDA graph (after one eager run that performs the
-        library's first-call setup); one replay per iteration afterwards."""
+    def _host_buffer(self):
+        """A pinned result buffer no live array points into (a new one when every
+        buffer is still referenced by programs the caller kept)."""
+        pl = self._plan
+        for hb in pl["hosts"]:
+            if hb.free():
+                return hb
+        hb = _HostBuf(pl["pk"])
+        hb.free()  # record the baseline reference count
+        pl["hosts"].append(hb)
+        return hb
+
+    def _capture(self, precondition, hb):
+        """Capture _launch (D2H into `hb`) as a CUDA graph, after one eager run
+        that performs the library's first-call setup; one replay per iteration."""
         import torch
 
         pl = self._plan
-        self._launch(precondition)
+        self._launch(precondition, hb)
         torch.cuda.current_stream(self.gt.device).synchronize()
         g = torch.cuda.CUDAGraph()
         n0 = int(pl["L"].cito_launch_count(None))
         with torch.cuda.graph(g):
-            self._launch(precondition)
+            self._launch(precondition, hb)
         pl["graph_kernels"][precondition] = int(pl["L"].cito_launch_count(None)) - n0
-        pl["graphs"][precondition] = g
+        hb.graphs[precondition] = g
         return g
 
     def iterate(self, z, delta, z_j=None, epsilon=None, precondition=False):
@@ -869,28 +905,28 @@ class GpuSCPStep:
         zp[:dim] = z
         zp[dim] = float(delta)
         zp[dim + 1] = float(epsilon)
+        hb = self._host_buffer()
         if self.use_graph:
-            g = pl["graphs"].get(bool(precondition))
+            g = hb.graphs.get(bool(precondition))
             if g is None:
-                g = self._capture(bool(precondition))
+                g = self._capture(bool(precondition), hb)
             g.replay()
             _lib.add_graph_launches(pl["graph_kernels"][bool(precondition)])
         else:
-            self._launch(bool(precondition))
-        pk = pl["pk"]
+            self._launch(bool(precondition), hb)
         nA = pl["nA"]
         stream.synchronize()  # the one synchronization
-        hh = pk.h
+        hh = hb.h
         bad = hh["bad"]
         if bad.any():
             raise FloatingPointError(f"non-finite state in intervals {np.where(bad != 0)[0].tolist()}")
         ConicProgram, ConeSpec = _conic_types()
         mats = {}
-        for M, nrows in (("A", nA), ("G", pl["nG"])):
-            indptr = hh[f"{M}_indptr"].copy()
+        for M, nrows in (("A", nA), ("G", pl["nG"])):  # views into the pinned buffer (no copy)
+            indptr = hh[f"{M}_indptr"]
             nnz = int(indptr[-1])
-            mats[M] = sp.csc_matrix((hh[f"{M}_data"][:nnz].copy(), hh[f"{M}_indices"][:nnz].copy(), indptr),
-                                    shape=(nrows, pat.n))
+            mats[M] = sp.csc_matrix((hh[f"{M}_data"][:nnz], hh[f"{M}_indices"][:nnz], indptr),
+                                    shape=(nrows, pat.n), copy=False)
         zj = z if z_j is None else z_j
         c = pat.objective_c(zj)
         P_data = pat.P_diag[: pat.lay.dim]
@@ -904,14 +940,14 @@ class GpuSCPStep:
             if pl["P_plain"] is None:
                 pl["P_plain"] = sp.csc_matrix((P_data, pl["P_idx"], pl["P_ptr"]), shape=(pat.n, pat.n))
             P = pl["P_plain"].copy()
-        prog = ConicProgram(P=P, c=c, A=mats["A"], b=hh["rhs"][:nA].copy(), G=mats["G"], h=hh["rhs"][nA:].copy(),
+        prog = ConicProgram(P=P, c=c, A=mats["A"], b=hh["rhs"][:nA], G=mats["G"], h=hh["rhs"][nA:],
                             cones=ConeSpec(nonneg=pat.n_orthant, soc=pat.soc_dims))
         lin = self._Lazy(pl["lin"], z.copy())
         import weakref
 
         self._last_lin = weakref.ref(lin)
         if precondition:
-            prec = _preconditioner_type()(row_scale_A=hh["row_scale_A"].copy(), row_scale_G=hh["row_scale_G"].copy(),
+            prec = _preconditioner_type()(row_scale_A=hh["row_scale_A"], row_scale_G=hh["row_scale_G"],
                                           var_scale=np.ones(pat.n), cost_scale=omega)
             return lin, prog, prec, pl["meta"]
         return lin, prog, pl["meta"]
