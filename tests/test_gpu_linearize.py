@@ -146,3 +146,31 @@ def test_device_path_matches_host_path():
     for a, b in zip(host, out[:4]):
         assert np.array_equal(a, b.cpu().numpy())
     assert disc.launch_count() >= 2
+
+
+@pytest.mark.parametrize("substeps,B", [(1, 40), (8, 199), (10, 64), (8, 600)])
+def test_linearize_substeps_vs_oracle(substeps, B):
+    """Other substep counts (configs[4]: 8 substeps, N=200 -> 199 intervals) on both K1
+    generations (B <= #SMs: the latency kernel; B > #SMs: the batch kernel)."""
+    from dataclasses import replace
+
+    from paper_2604_09993_b200 import synth
+
+    sc = replace(golden_scenario("halfcheetah_n30"), substeps=substeps)
+    desc = scenario_desc(sc)
+    xt0, U, S, _ = synth.random_intervals(sc, B, seed=substeps, finite_fn=lambda x, u, s: synth.well_posed(
+        pyoracle.propagate(desc, sc.substeps, x, u, s)[0]))
+    e0, jx0, ju0, js0, _ = pyoracle.linearize(desc, sc.substeps, xt0, U, S)
+    e, jx, ju, js = _disc(sc).linearize_batch(xt0, U, S)
+    worst = max(rel_err(a[b], r[b]) for b in range(B) for a, r in ((e, e0), (jx, jx0), (ju, ju0), (js, js0)))
+    assert worst <= TOL, worst
+    ends = _disc(sc).propagate_batch(xt0, U, S)
+    assert rel_err(ends, e0) <= TOL
+
+
+def test_linearize_empty_batch():
+    sc = golden_scenario("monoped_n20")
+    d = _disc(sc)
+    e, jx, ju, js = d.linearize_batch(np.zeros((0, d.n_xt)), np.zeros((0, 2 * d.n_u)), np.zeros(0))
+    assert e.shape == (0, d.n_xt) and jx.shape == (0, d.n_xt, d.n_xt) and ju.shape == (0, d.n_xt, 2 * d.n_u)
+    assert d.propagate_batch(np.zeros((0, d.n_xt)), np.zeros((0, 2 * d.n_u)), np.zeros(0)).shape == (0, d.n_xt)
