@@ -584,12 +584,26 @@ cito_status cito_csc_assemble2_dev(int32_t nmat, int32_t ncols, const int64_t* c
     sa.counts[m] = counts[m];
     sa.out_ptr[m] = out_ptr[m];
   }
-  count_launch(3);
-  k_csc_count<<<dim3(gx, nmat), 32 * wpb, 0, s>>>(ncols, ca, sigma, L);
+  // two launches: per-block nonzero totals (into the counts workspace), then
+  // prefix + per-column scan + compacted write (CITO_CSC3=1: the older three-launch
+  // count / scan / write sequence)
+  static const bool three = getenv("CITO_CSC3") != nullptr;
+  if (three) {
+    count_launch(3);
+    k_csc_count<<<dim3(gx, nmat), 32 * wpb, 0, s>>>(ncols, ca, sigma, L);
+    CUDA_TRY(cudaGetLastError());
+    k_scan<<<nmat, 1024, 0, s>>>(sa);
+    CUDA_TRY(cudaGetLastError());
+    k_csc_write<<<dim3(gx, nmat), 32 * wpb, 0, s>>>(ncols, ca, sigma, L);
+    CUDA_TRY(cudaGetLastError());
+    return CITO_OK;
+  }
+  (void)gx;
+  const unsigned nb = (unsigned)((ncols + CSC_CPB - 1) / CSC_CPB);
+  count_launch(2);
+  k_csc_blocksum<<<dim3(nb, nmat), 256, 0, s>>>(ncols, ca, sigma, L);
   CUDA_TRY(cudaGetLastError());
-  k_scan<<<nmat, 1024, 0, s>>>(sa);
-  CUDA_TRY(cudaGetLastError());
-  k_csc_write<<<dim3(gx, nmat), 32 * wpb, 0, s>>>(ncols, ca, sigma, L);
+  k_csc_write2<<<dim3(nb, nmat), 256, 0, s>>>(ncols, ca, sigma, L);
   CUDA_TRY(cudaGetLastError());
   return CITO_OK;
 }

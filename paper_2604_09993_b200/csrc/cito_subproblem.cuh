@@ -130,6 +130,113 @@ __global__ void __launch_bounds__(256) k_csc_write(int32_t ncols, const CscArgs 
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Two-launch compaction (replaces count + scan + write): columns are processed
+// in blocks of CSC_CPB columns (one CTA, 8 warps).
+//   k_csc_blocksum  number of exact nonzeros of every column block -> bsum[block]
+//   k_csc_write2    prefix = sum of bsum over the preceding blocks (CTA reduce),
+//                   per-column counts + warp scan -> indptr of the block's
+//                   columns, then the ballot-compacted write (+ row inf-norms)
+#define CSC_CPB 32
+
+__global__ void __launch_bounds__(256) k_csc_blocksum(int32_t ncols, const CscArgs a, const double* __restrict__ sigma,
+                                                      const LinTable L) {
+  const int m = blockIdx.y;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t* __restrict__ sp_ptr = a.sp_ptr[m];
+  __shared__ int32_t wsum[8];
+  int n = 0;
+  for (int k = warp; k < CSC_CPB; k += 8) {
+    const int64_t c = (int64_t)blockIdx.x * CSC_CPB + k;
+    if (c >= ncols) break;
+    const double sig = sigma[c];
+    for (int64_t e = sp_ptr[c] + lane; e < sp_ptr[c + 1]; e += 32)
+      n += sp_value(e, sig, a.src[m], a.idx[m], a.val[m], L) != 0.0;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+  if (lane == 0) wsum[warp] = n;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += wsum[w];
+    a.counts[m][blockIdx.x] = t;  // the counts workspace holds the block totals
+  }
+}
+
+__global__ void __launch_bounds__(256) k_csc_write2(int32_t ncols, const CscArgs a, const double* __restrict__ sigma,
+                                                    const LinTable L) {
+  const int m = blockIdx.y;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t* __restrict__ sp_ptr = a.sp_ptr[m];
+  const int64_t c0 = (int64_t)blockIdx.x * CSC_CPB;
+  __shared__ int32_t red[8];
+  __shared__ int32_t ccount[CSC_CPB];
+  __shared__ int32_t cbase[CSC_CPB];
+  // prefix over the preceding column blocks
+  int pre = 0;
+  for (int j = tid; j < (int)blockIdx.x; j += blockDim.x) pre += a.counts[m][j];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
+  if (lane == 0) red[warp] = pre;
+  // per-column nonzero counts of this block
+  for (int k = warp; k < CSC_CPB; k += 8) {
+    const int64_t c = c0 + k;
+    int n = 0;
+    if (c < ncols) {
+      const double sig = sigma[c];
+      for (int64_t e = sp_ptr[c] + lane; e < sp_ptr[c + 1]; e += 32)
+        n += sp_value(e, sig, a.src[m], a.idx[m], a.val[m], L) != 0.0;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+    if (lane == 0) ccount[k] = n;
+  }
+  __syncthreads();
+  if (warp == 0) {  // exclusive scan of the block's column counts (CSC_CPB == 32: one per lane)
+    int blockpre = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) blockpre += red[w];
+    const int v = ccount[lane];
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const int base = blockpre + incl - v;
+    cbase[lane] = base;
+    const int64_t c = c0 + lane;
+    if (c < ncols) a.out_ptr[m][c] = base;
+    if (c == ncols - 1) a.out_ptr[m][ncols] = base + v;
+  }
+  __syncthreads();
+  const unsigned lt = (1u << lane) - 1u;
+  for (int k = warp; k < CSC_CPB; k += 8) {
+    const int64_t c = c0 + k;
+    if (c >= ncols) break;
+    const double sig = sigma[c];
+    int32_t base = cbase[k];
+    for (int64_t e0 = sp_ptr[c]; e0 < sp_ptr[c + 1]; e0 += 32) {
+      const int64_t e = e0 + lane;
+      const bool in = e < sp_ptr[c + 1];
+      const double v = in ? sp_value(e, sig, a.src[m], a.idx[m], a.val[m], L) : 0.0;
+      const bool nz = in && v != 0.0;
+      const unsigned msk = __ballot_sync(0xffffffffu, nz);
+      if (nz) {
+        const int32_t pos = base + __popc(msk & lt);
+        const int32_t r = a.row[m][e];
+        a.out_rows[m][pos] = r;
+        a.out_vals[m][pos] = v;
+        if (a.rowmax[m]) atomicMax(&a.rowmax[m][r], (unsigned long long)__double_as_longlong(fabs(v)));
+      }
+      base += __popc(msk);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) k_rhs(int64_t nrows, const int32_t* __restrict__ rows,
                                              const int8_t* __restrict__ form, const int8_t* __restrict__ vsrc,
                                              const int64_t* __restrict__ voff, const int8_t* __restrict__ seg_src,
