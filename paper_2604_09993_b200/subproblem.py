@@ -553,18 +553,27 @@ class SubproblemAssembler:
             nA, nG = mats[0]["nrows"], mats[1]["nrows"]
             rm = torch.zeros(max(1, nA + nG), dtype=torch.int64, device=self.device)
             rowmax = (rm[:nA], rm[nA:])
+        # b/h of the linearized rows on a side stream, concurrently with the CSC compaction
+        r = self._rhs
+        cur = torch.cuda.current_stream(self.device) if stream is None else torch.cuda.ExternalStream(stream)
+        if getattr(self, "_side", None) is None:
+            self._side = torch.cuda.Stream(self.device)
+        side = self._side
+        side.wait_stream(cur)
+        with torch.cuda.stream(side):
+            rhs = r["const"].clone()
+            _lib.check(_lib.lib().cito_rhs_dev(
+                r["n"], r["rows"].data_ptr(), r["form"].data_ptr(), r["vsrc"].data_ptr(), r["voff"].data_ptr(),
+                r["seg_src"].data_ptr(), r["seg_off"].data_ptr(), r["seg_len"].data_ptr(), r["seg_cb"].data_ptr(),
+                r["cols"].data_ptr(), z_ref_dev.data_ptr(), ptrs, rhs.data_ptr(), side.cuda_stream), "rhs")
         _lib.check(_lib.lib().cito_csc_assemble2_dev(
             2, self.pat.n, arr([d["sp_ptr"] for d in mats]), arr([d["row"] for d in mats]),
             arr([d["src"] for d in mats]), arr([d["idx"] for d in mats]), arr([d["val"] for d in mats]),
             self.sigma_dev.data_ptr(), ptrs, arr([d["counts"] for d in mats]), arr([o[0] for o in outs]),
             arr([o[1] for o in outs]), arr([o[2] for o in outs]), arr(rowmax) if rowmax else None, s),
             "csc_assemble")
-        r = self._rhs
-        rhs = r["const"].clone()
-        _lib.check(_lib.lib().cito_rhs_dev(
-            r["n"], r["rows"].data_ptr(), r["form"].data_ptr(), r["vsrc"].data_ptr(), r["voff"].data_ptr(),
-            r["seg_src"].data_ptr(), r["seg_off"].data_ptr(), r["seg_len"].data_ptr(), r["seg_cb"].data_ptr(),
-            r["cols"].data_ptr(), z_ref_dev.data_ptr(), ptrs, rhs.data_ptr(), s), "rhs")
+        cur.wait_stream(side)
+        rhs.record_stream(cur)
         out["b"], out["h"] = rhs[: r["nA"]], rhs[r["nA"]:]
         if precondition:
             self._precondition(out, rowmax, s)
@@ -823,7 +832,7 @@ class GpuSCPStep:
         P_idx = np.arange(dim, dtype=np.int32)
         P_ptr = np.concatenate([np.arange(dim + 1), np.full(pat.n - dim, dim)]).astype(np.int32)
         self._plan = dict(lin=lin, pk=pk, z_dev=z_dev, zde_dev=zde_dev, zde_pin=zde_pin, rowmax=rowmax, rhs_dev=rhs_dev,
-                          hosts=[], graph_kernels={},
+                          hosts=[], graph_kernels={}, side=torch.cuda.Stream(dev),
                           rhs_const=r["const"], asm_args=asm_args, rm_arr=rm_arr, rhs_args=rhs_args,
                           pc_args=pc_args, lin_args=lin_args, lin_outs=lin_outs, keep=keep, L=L, nA=nA, nG=nG,
                           soc=(soc_start, soc_dim), P_idx=P_idx, P_ptr=P_ptr,
@@ -842,10 +851,16 @@ class GpuSCPStep:
         _lib.check(L.cito_linearize_all_dev2(*pl["lin_args"], *pl["lin_outs"], s), "linearize_all")
         if precondition:
             pl["rowmax"].zero_()
+        # b/h of the linearized rows on a side stream, concurrently with the CSC compaction
+        cur = torch.cuda.current_stream(self.gt.device)
+        side = pl["side"]
+        side.wait_stream(cur)
+        with torch.cuda.stream(side):
+            pl["rhs_dev"].copy_(pl["rhs_const"])
+            _lib.check(L.cito_rhs_dev(*pl["rhs_args"], side.cuda_stream), "rhs")
         _lib.check(L.cito_csc_assemble2_dev(*pl["asm_args"], pl["rm_arr"] if precondition else None, s),
                    "csc_assemble")
-        pl["rhs_dev"].copy_(pl["rhs_const"])
-        _lib.check(L.cito_rhs_dev(*pl["rhs_args"], s), "rhs")
+        cur.wait_stream(side)
         if precondition:
             _lib.check(L.cito_precondition_dev(*pl["pc_args"], s), "precondition")
         hb.host.copy_(pl["pk"].dev, non_blocking=True)
