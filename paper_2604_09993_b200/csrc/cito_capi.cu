@@ -102,6 +102,8 @@ cito_status launch_linearize(const KParams& P, int64_t B, const double* xt0s, co
   if (!attr_done) {
     CUDA_TRY(cudaFuncSetAttribute(k_linearize<M, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1));
     CUDA_TRY(cudaFuncSetAttribute(k_linearize<M, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1));
+    CUDA_TRY(cudaFuncSetAttribute(k_linearize<M, 1, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(3 * ((smem1 + 127) / 128 * 128))));
     CUDA_TRY(cudaFuncSetAttribute(k_linearize2<M, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
     CUDA_TRY(cudaFuncSetAttribute(k_linearize2<M, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
     attr_done = true;
@@ -121,7 +123,14 @@ cito_status launch_linearize(const KParams& P, int64_t B, const double* xt0s, co
   } else if (B <= sms) {
     k_linearize<M, 1><<<(unsigned)B, FusedDims<M>::NT, smem1, st>>>(P, B, xt0s, Us, Ss, ends, jx, ju, js, bad, zs);
   } else {
-    k_linearize<M, 3><<<(unsigned)B, FusedDims<M>::NT, smem1, st>>>(P, B, xt0s, Us, Ss, ends, jx, ju, js, bad, zs);
+    // three intervals per CTA in lockstep (same-role warps share an SM sub-partition and
+    // fetch the same instructions); CITO_K1_IPC1=1: one interval per CTA, 3 CTAs/SM
+    static const bool ipc3 = getenv("CITO_K1_IPC1") == nullptr;
+    if (ipc3)
+      k_linearize<M, 1, 3><<<(unsigned)((B + 2) / 3), 3 * FusedDims<M>::NT, 3 * ((smem1 + 127) / 128 * 128), st>>>(
+          P, B, xt0s, Us, Ss, ends, jx, ju, js, bad, zs);
+    else
+      k_linearize<M, 3><<<(unsigned)B, FusedDims<M>::NT, smem1, st>>>(P, B, xt0s, Us, Ss, ends, jx, ju, js, bad, zs);
   }
   CUDA_TRY(cudaGetLastError());
   return CITO_OK;

@@ -1256,8 +1256,11 @@ __device__ __forceinline__ void col_stage(const KParams& P, FusedShared<M>& sh, 
   }
 }
 
-template <class M, int MINB>
-__global__ void __launch_bounds__(FusedDims<M>::NT, MINB) k_linearize(const KParams P, int64_t B,
+// IPC > 1: IPC intervals per CTA, one 4-warp group each, ticking in lockstep (one
+// barrier per tick for all groups), so the groups' same-role warps share one SM
+// sub-partition and fetch the same instructions at the same time.
+template <class M, int MINB, int IPC = 1>
+__global__ void __launch_bounds__(FusedDims<M>::NT * IPC, MINB) k_linearize(const KParams P, int64_t B,
                                                                const double* __restrict__ xt0s,
                                                                const double* __restrict__ Us,
                                                                const double* __restrict__ Ss,
@@ -1267,29 +1270,34 @@ __global__ void __launch_bounds__(FusedDims<M>::NT, MINB) k_linearize(const KPar
   using D = Dims<M>;
   constexpr int NQ = D::NQ, NX = D::NX, NU = D::NU, NY = D::NY, NXT = D::NXT, NCOL = D::NCOL, NR = D::NR;
   constexpr int NDIRX = M::NDIRX, NDIR = D::NDIR, NHIST = M::NHIST;
+  constexpr int NT1 = FusedDims<M>::NT;
+  constexpr size_t SHB = (sizeof(FusedShared<M>) + 127) / 128 * 128;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  FusedShared<M>& sh = *reinterpret_cast<FusedShared<M>*>(smem_raw);
-  const int64_t b = blockIdx.x;
-  if (b >= B) return;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int grp = IPC == 1 ? 0 : (int)(threadIdx.x / NT1);
+  FusedShared<M>& sh = *reinterpret_cast<FusedShared<M>*>(smem_raw + grp * SHB);
+  const int64_t b_raw = (int64_t)blockIdx.x * IPC + grp;
+  if (IPC == 1 && b_raw >= B) return;
+  const bool active = b_raw < B;  // a spare group recomputes interval B-1 and writes nothing
+  const int64_t b = active ? b_raw : B - 1;
+  const int tid = IPC == 1 ? (int)threadIdx.x : (int)(threadIdx.x % NT1), warp = tid >> 5, lane = tid & 31;
   // inputs: either packed batches or gathered straight from the decision vector
   // z (cito/scp.py:98-100, layout cito/ocp.py:154-174)
   const int64_t zp = zs.z ? b / zs.n_int : 0, zk = zs.z ? b % zs.n_int : 0;  // problem, interval
   const double* zb = zs.z ? zs.z + zp * zs.zstride : nullptr;
   const double* src_x = zs.z ? zb + (2 * zk + 1) * NXT : xt0s + b * NXT;
   const double* src_U = zs.z ? zb + zs.base_u + zk * (2 * NU + 1) : Us + b * 2 * NU;
-  for (int k = tid; k < NXT; k += blockDim.x) sh.x[k] = src_x[k];
-  for (int k = tid; k < 2 * NU; k += blockDim.x) sh.U[k] = src_U[k];
+  for (int k = tid; k < NXT; k += NT1) sh.x[k] = src_x[k];
+  for (int k = tid; k < 2 * NU; k += NT1) sh.U[k] = src_U[k];
   if (tid == 0) {
     sh.S = zs.z ? src_U[2 * NU] : Ss[b];
     sh.bad = 0;
   }
-  for (int l = tid; l < M::NL; l += blockDim.x) {
+  for (int l = tid; l < M::NL; l += NT1) {
     sh.sp.minv_m[l] = P.minv_m[l];
     sh.sp.minv_I[l] = P.minv_I[l];
     sh.sp.neg_mg[l] = P.neg_mg[l];
   }
-  for (int j = tid; j < M::NJ; j += blockDim.x) {
+  for (int j = tid; j < M::NJ; j += NT1) {
     sh.sp.jrp[j][0] = P.jrp[j][0];
     sh.sp.jrp[j][1] = P.jrp[j][1];
     sh.sp.jrc[j][0] = P.jrc[j][0];
@@ -1317,7 +1325,7 @@ __global__ void __launch_bounds__(FusedDims<M>::NT, MINB) k_linearize(const KPar
 #pragma unroll
     for (int k = 0; k < M::NLCOL; ++k) sh.sp.lc[k] = M::lcol(k);
   }
-  for (int c = tid; c < M::NC; c += blockDim.x) {
+  for (int c = tid; c < M::NC; c += NT1) {
     sh.sp.cr[c][0] = P.cr[c][0];
     sh.sp.cr[c][1] = P.cr[c][1];
     sh.sp.mu[c] = P.mu[c];
@@ -1376,7 +1384,7 @@ __global__ void __launch_bounds__(FusedDims<M>::NT, MINB) k_linearize(const KPar
   double* jxb = jx + b * NXT * NXT;
   double* jub = ju + b * NXT * 2 * NU;
   double* jsb = js + b * NXT;
-  if (colthr) {
+  if (colthr && active) {
     double* dst;
     int stride;
     if (sc >= 0) {
@@ -1406,7 +1414,7 @@ __global__ void __launch_bounds__(FusedDims<M>::NT, MINB) k_linearize(const KPar
       for (int ii = 0; ii < 6; ++ii) inc += P.b[ii] * S;
       dqc = dqc + h * inc;
     }
-    for (int e = tid; e < M::NLCOL * NXT; e += blockDim.x) {
+    for (int e = active ? tid : M::NLCOL * NXT; e < M::NLCOL * NXT; e += NT1) {
       const int lc = e / NXT, r = e % NXT;
       const int c = sh.sp.lc[lc];
       double val = (r == c) ? 1.0 : 0.0;
@@ -1414,16 +1422,16 @@ __global__ void __launch_bounds__(FusedDims<M>::NT, MINB) k_linearize(const KPar
       jxb[r * NXT + c] = val;
     }
   }
-  for (int e = tid; e < NXT * NY; e += blockDim.x) {  // y0 columns of jx: identity (rates ignore y)
+  for (int e = active ? tid : NXT * NY; e < NXT * NY; e += NT1) {  // y0 columns of jx: identity (rates ignore y)
     const int r = e / Pos<NY>::v, c = NX + e % Pos<NY>::v;
     jxb[r * NXT + c] = (r == c) ? 1.0 : 0.0;
   }
-  for (int k = tid; k < NXT; k += blockDim.x) {
+  for (int k = active ? tid : NXT; k < NXT; k += NT1) {
     const double e = sh.x[k];
     ends[b * NXT + k] = e;
     if (zs.defects) zs.defects[b * NXT + k] = zb[(2 * zk + 2) * NXT + k] - e;  // scp.py:115
     if (!isfinite(e)) sh.bad = 1;
   }
   __syncthreads();
-  if (tid == 0 && bad) bad[b] = sh.bad;
+  if (tid == 0 && bad && active) bad[b] = sh.bad;
 }
