@@ -420,7 +420,7 @@ def run_ours(args):
             asmf.assemble_device(r, zf)
 
         nf = max(5, K // 5)
-        fms, fk1, _ = timed(fine_step, nf, 3)
+        fms, fk1, _ = timed(fine_step, nf, 5)
         extra["fine_extra"] = {"workload": "HalfCheetah N=200, 8 RKF substeps, one SCP iteration (configs[4]; "
                                            "the reference has no RK4)",
                                "value": (scf.N - 1) * nf / (fms * 1e-3), "unit": UNIT, "ms_per_step": fms / nf,
@@ -489,7 +489,8 @@ def run_ours(args):
     roofline = {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": (achieved / peak) if achieved else None,
                 "traffic": ncu_traffic(f"k_linearize_{'scp' if fine else args.workload}"),
-                "kernel": ("k_linearize2<Topo_halfcheetah_g2,1>" if B_k1 <= 148 else "k_linearize<Topo_halfcheetah_g2,3>"),
+                "kernel": ("k_linearize2<Topo_halfcheetah_g2,1> (1 interval/CTA)" if B_k1 <= 98
+                           else "k_linearize<Topo_halfcheetah_g2,1,3> (3 intervals/CTA in lockstep)"),
                 "kernel_ms": k1_ms, "intervals_per_launch": B_k1,
                 "flops_per_interval": F, "flops_definition": fdef,
                 "peak_source": "measured in this run: FP64 DFMA probe kernel (cito_dfma_peak); MEASURED_PEAKS.json "

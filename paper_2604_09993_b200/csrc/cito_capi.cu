@@ -115,12 +115,17 @@ cito_status launch_linearize(const KParams& P, int64_t B, const double* xt0s, co
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   count_launch();
   const int ver = k1_version();
-  if (ver == 2 || (ver == 0 && B <= sms)) {
+  // batches up to lat_max intervals use the latency kernel, one CTA per SM; above
+  // ~2/3 of the SMs the lockstep 3-interval batch kernel is faster (measured
+  // crossover 96..120 intervals on 148 SMs: instruction fetch)
+  static const int64_t lat_max = getenv("CITO_K1_LAT_MAX") ? atoll(getenv("CITO_K1_LAT_MAX")) : -1;
+  const int64_t lmax = lat_max >= 0 ? lat_max : (2 * (int64_t)sms) / 3;
+  if (ver == 2 || (ver == 0 && B <= lmax)) {
     if (B <= sms)
       k_linearize2<M, 1><<<(unsigned)B, K2Dims<M>::NT, smem2, st>>>(P, B, xt0s, Us, Ss, ends, jx, ju, js, bad, zs);
     else
       k_linearize2<M, 2><<<(unsigned)B, K2Dims<M>::NT, smem2, st>>>(P, B, xt0s, Us, Ss, ends, jx, ju, js, bad, zs);
-  } else if (B <= sms) {
+  } else if (ver == 1 && B <= sms) {
     k_linearize<M, 1><<<(unsigned)B, FusedDims<M>::NT, smem1, st>>>(P, B, xt0s, Us, Ss, ends, jx, ju, js, bad, zs);
   } else {
     // three intervals per CTA in lockstep (same-role warps share an SM sub-partition and
