@@ -5,7 +5,9 @@ sc = S.bundled("halfcheetah_bound", N=30)
 g, n_g = sc.path_constraints()
 disc = Discretizer(sc.model, sc.mixing_matrix(n_g), g, substeps=sc.substeps)
 dev = torch.device("cuda")
-for B in (29, 60, 74, 75, 96, 120, 140, 148, 149, 199):
+import os
+BS = [int(x) for x in os.environ.get('KNEE_B', '29,60,74,75,96,120,140,148,149,199').split(',')]
+for B in BS:
     x, U, Sv = synth.random_intervals(sc, B, seed=0)
     xd, Ud, Sd = (torch.as_tensor(a, device=dev) for a in (x, U, Sv))
     out = disc.linearize_batch_device(xd, Ud, Sd)

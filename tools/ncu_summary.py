@@ -29,6 +29,7 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio",
         "smsp__average_warps_issue_stalled_mio_throttle_per_issue_active.ratio",
         "smsp__average_warps_issue_stalled_lg_throttle_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_no_instruction_per_issue_active.ratio",
         "l1tex__t_sectors_pipe_lsu_mem_local_op_ld.sum", "l1tex__t_sectors_pipe_lsu_mem_local_op_st.sum",
         "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
         "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed"]
@@ -65,7 +66,9 @@ def full(rep, tag, key):
                  "dram_bytes_per_launch": k0.get("dram__bytes_read.sum", 0) + k0.get("dram__bytes_write.sum", 0),
                  "registers": k0.get("launch__registers_per_thread"),
                  "issue_active_pct": k0.get("smsp__issue_active.avg.pct_of_peak_sustained_active"),
-                 "fp64_pipe_pct": k0.get("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active")}
+                 "fp64_pipe_pct": k0.get("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"),
+                 "stall_no_instruction": k0.get("smsp__average_warps_issue_stalled_no_instruction_per_issue_active.ratio"),
+                 "stall_wait": k0.get("smsp__average_warps_issue_stalled_wait_per_issue_active.ratio")}
     with open(summ_path, "w") as f:
         json.dump(summ, f, indent=1)
     print(json.dumps(summ[key], indent=1))
