@@ -92,7 +92,7 @@ __device__ __forceinline__ void tan_rate_k(const KParams& P, const Prim<M>& pr, 
         const double Hd1 = pr.H[i][1] * dP[i][0] + pr.H[i][2] * dP[i][1];
         const double gn = pr.gn[i], g0 = pr.g[i][0], g1 = pr.g[i][1];
         const double gHd = g0 * Hd0 + g1 * Hd1;
-        const double ign3 = 1.0 / (gn * gn * gn);
+        const double ign3 = pr.ign3[i];
         dn[i][0] = Hd0 / gn - g0 * gHd * ign3;
         dn[i][1] = Hd1 / gn - g1 * gHd * ign3;
         dsd[i] = (g0 * dP[i][0] + g1 * dP[i][1]) / gn - pr.hv[i] * gHd * ign3;
@@ -218,20 +218,19 @@ __device__ __forceinline__ void tan_rate_k(const KParams& P, const Prim<M>& pr, 
     }
     if constexpr (HU) {
       const double dft = SU(NA + 2 * i), dgam = SU(NA + 2 * NC + i);
-      const double q1 = ft * ft + 1.0;
-      const double dsg = dft / (q1 * sqrt(q1));
+      const double dsg = dft * pr.dsgf[i];
       dlamc += dgam * pr.sg[i] + gam * dsg;
     }
     dy[5 * i + 0] = HU ? SU(NA + 2 * i + 1) : 0.0;
-    dy[5 * i + 1] = sabs_d(pr.lamc[i]) * dlamc;
+    dy[5 * i + 1] = pr.dlam[i] * dlamc;
     dy[5 * i + 2] = HU ? SU(NA + 2 * NC + i) : 0.0;
     if constexpr (HU) {
       const double dft = SU(NA + 2 * i), dfn = SU(NA + 2 * i + 1);
-      dy[5 * i + 3] = sabs_d(P.mu[i] * fn) * P.mu[i] * dfn - pr.sg[i] * dft;
+      dy[5 * i + 3] = pr.dmu[i] * dfn - pr.sg[i] * dft;
     } else {
       dy[5 * i + 3] = 0.0;
     }
-    dy[5 * i + 4] = HQ ? srelu_d(pr.sd[i]) * dsd[i] : 0.0;
+    dy[5 * i + 4] = HQ ? pr.dsrl[i] * dsd[i] : 0.0;
   }
   if constexpr (M::NGO > 0) {
     constexpr int NG = Prim<M>::NG;
@@ -255,7 +254,7 @@ __device__ __forceinline__ void tan_rate_k(const KParams& P, const Prim<M>& pr, 
         dg[r++] = dpz;
       }
 #pragma unroll
-      for (int jg = 0; jg < NG; ++jg) dg[jg] *= srelu_d(pr.gp[jg]);
+      for (int jg = 0; jg < NG; ++jg) dg[jg] *= pr.dgp[jg];
 #pragma unroll
       for (int o = 0; o < M::NGO; ++o) {
         double acc = 0.0;
@@ -563,6 +562,7 @@ __device__ __forceinline__ void aux_stage(const KParams& P, Fused2Shared<M>& sh,
         pr.H[ci][2] = t2.hzz;
         const double gn = sqrt(t2.gx * t2.gx + t2.gz * t2.gz);
         pr.gn[ci] = gn;
+        pr.ign3[ci] = 1.0 / (gn * gn * gn);
         n0 = t2.gx / gn;
         n1 = t2.gz / gn;
         sd = t2.v / gn;
@@ -584,10 +584,15 @@ __device__ __forceinline__ void aux_stage(const KParams& P, Fused2Shared<M>& sh,
       const double Jv0 = v[3 * l] + (-rz) * om, Jv1 = v[3 * l + 1] + rx * om;
       pr.Jv[ci][0] = Jv0;
       pr.Jv[ci][1] = Jv1;
-      const double sgt = ft / sqrt(ft * ft + 1.0);  // friction_stationarity (contact_dynamics.py:55-66)
+      const double q1 = ft * ft + 1.0, sq1 = sqrt(q1);
+      const double sgt = ft / sq1;  // friction_stationarity (contact_dynamics.py:55-66)
       pr.sg[ci] = sgt;
+      pr.dsgf[ci] = 1.0 / (q1 * sq1);
       const double lamc = t0 * Jv0 + t1 * Jv1 + gam * sgt;
       pr.lamc[ci] = lamc;
+      pr.dlam[ci] = sabs_d(lamc);
+      pr.dmu[ci] = sabs_d(Q.mu[ci] * fn) * Q.mu[ci];
+      pr.dsrl[ci] = srelu_d(sd);
       double* yo = R.r + NQ + 5 * ci;  // aux_rate rows (augmentation.py:134-153)
       yo[0] = fn;
       yo[1] = sabs(lamc);
@@ -622,6 +627,7 @@ __device__ __forceinline__ void aux_stage(const KParams& P, Fused2Shared<M>& sh,
 #pragma unroll
       for (int jg = 0; jg < NG; ++jg) {
         pr.gp[jg] = gpl[jg];
+        pr.dgp[jg] = srelu_d(gpl[jg]);
         sgv[jg] = srelu(gpl[jg]);
       }
 #pragma unroll

@@ -194,6 +194,12 @@ struct Prim {
   double hv[NC], g[NC][2], H[NC][3], gn[NC];  // implicit surface data
   double sd[NC], lamc[NC], sg[NC];
   double gp[Pos<NG>::v];
+  // derivative factors of the smooth primitives, once per stage for all tangent
+  // directions (filled by the off-chain warp of k_linearize2 only; tan_rate of
+  // k_linearize computes them per lane): sabs'(lamc), sabs'(mu fn) mu, srelu'(sd),
+  // 1 / (ft^2 + 1)^(3/2), 1 / |grad h|^3 (implicit terrain), srelu'(g)
+  double dlam[NC], dmu[NC], dsrl[NC], dsgf[NC], ign3[NC];
+  double dgp[Pos<NG>::v];
   double u[Pos<M::NA + 3 * M::NC>::v];
 };
 
