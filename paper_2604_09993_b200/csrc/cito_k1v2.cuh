@@ -356,7 +356,8 @@ struct Fused2Shared {
 // stage input, cos/sin and FOH control of the record; writes the factor, the
 // reactions and vdot (pr.vdot and the vdot rows of r).
 template <class M>
-__device__ __forceinline__ void crit_chain(const KParams& P, Rec2<M>& R) {
+__device__ __forceinline__ void crit_chain(const KParams& P, Rec2<M>& R, int t) {
+  (void)t;
   using D = Dims<M>;
   constexpr int NL = M::NL, NJ = M::NJ, NC = M::NC, NA = M::NA, NQ = D::NQ;
   Prim<M>& pr = R.pr;
@@ -434,6 +435,7 @@ __device__ __forceinline__ void crit_chain(const KParams& P, Rec2<M>& R) {
       Rj[j][1][0] = cl[c] * P.jrc[j][0] - sl[c] * P.jrc[j][1];
       Rj[j][1][1] = sl[c] * P.jrc[j][0] + cl[c] * P.jrc[j][1];
     }
+    CITO_MARK_P(t, 3);  // kinematics + forces done
     double Lr[NJ2 * (NJ2 + 1) / 2];
 #pragma unroll
     for (int a = 0; a < NJ; ++a)
@@ -482,7 +484,9 @@ __device__ __forceinline__ void crit_chain(const KParams& P, Rec2<M>& R) {
       }
     }
     double Lir[NJ2];
+    CITO_MARK_P(t, 4);  // Gram + rhs done
     M::chol_solve(Lr, y, Lir);
+    CITO_MARK_P(t, 5);  // factor + solves done
 #pragma unroll
     for (int r = 0; r < NJ2; ++r) {
       pr.Li[r] = Lir[r];
@@ -845,6 +849,7 @@ __global__ void __launch_bounds__(JAC ? K2Dims<M>::NT : 64, MINB) k_linearize2(c
       if (t < NST) {
         const int s = t / 6, i = t % 6;
         Rec2<M>& R = sh.ring[t & 3];
+        CITO_MARK_P(t, 0);
         // stage input (augmentation.py:200-205), coordinates owned by this lane
 #pragma unroll
         for (int p = 0; p < PER; ++p) {
@@ -856,6 +861,7 @@ __global__ void __launch_bounds__(JAC ? K2Dims<M>::NT : 64, MINB) k_linearize2(c
           if (k < NX) R.xs[k] = a;
         }
         __syncwarp();
+        CITO_MARK_P(t, 1);
         const double tau = h * (double)s + P.ch[i];
         for (int e = lane; e < M::NL + NU; e += 32) {
           if (e < M::NL) {
@@ -869,7 +875,9 @@ __global__ void __launch_bounds__(JAC ? K2Dims<M>::NT : 64, MINB) k_linearize2(c
           }
         }
         __syncwarp();
-        if (lane == 0) crit_chain<M>(P, R);
+        CITO_MARK_P(t, 2);
+        if (lane == 0) crit_chain<M>(P, R, t);
+        CITO_MARK_P(t, 6);
         __syncwarp();
         // stage slopes k_i = S * f (q rows: stage-input velocity, v rows: vdot)
 #pragma unroll
@@ -891,6 +899,7 @@ __global__ void __launch_bounds__(JAC ? K2Dims<M>::NT : 64, MINB) k_linearize2(c
             RS_XR(p) = RS_XR(p) + h * inc;
           }
         }
+        CITO_MARK_P(t, 7);
       }
     } else if (warp == W_AUX) {
       if (t >= 1 && t <= NST) aux_stage<M>(P, sh, t - 1, lane, rs);
