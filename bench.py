@@ -381,8 +381,29 @@ def run_ours(args):
 
     K, W = args.steps, max(3, args.warmup)
     clocks = Clocks(dev.index if world == 1 else local)
+    step_k1_ms = None
     if args.workload in ("scp", "fine"):
         ms_tot, k1_ms, launches = timed(lambda rec: scp_step(z_dev, rec), K, W)
+        # the interval kernel alone (the roofline kernel; in the step it overlaps K3 and
+        # includes the fork/join): same intervals, device-resident, events on its stream
+        zh = z_dev.cpu().numpy()
+        xs = torch.as_tensor(np.stack([zh[lay.xp(k)] for k in range(n_int)]), device=dev)
+        us = torch.as_tensor(np.stack([zh[lay.u(k)] for k in range(n_int)]), device=dev)
+        ss = torch.as_tensor(np.array([zh[lay.s(k)][0] for k in range(n_int)]), device=dev)
+        kout = gt.disc.linearize_batch_device(xs, us, ss)
+        for _ in range(W):
+            gt.disc.linearize_batch_device(xs, us, ss, out=kout)
+        kev = []
+        for _ in range(K):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            gt.disc.linearize_batch_device(xs, us, ss, out=kout)
+            e1.record(stream)
+            kev.append((e0, e1))
+        torch.cuda.synchronize()
+        step_k1_ms = k1_ms
+        k1_ms = float(np.mean([a.elapsed_time(b) for a, b in kev]))
         units_per_step, B_k1 = n_int, n_int
     elif args.workload == "multistart":
         gt.disc = gt50.disc  # launch counter of the handle actually used
@@ -438,7 +459,7 @@ def run_ours(args):
             return scp_api.iterate(z, delta)
 
         e2e_step()
-        h2d = z.nbytes
+        h2d = z.nbytes + 16  # z plus [delta, epsilon] (one pinned H2D per step)
         d2h = int(scp_api._plan["pk"].nbytes)  # one packed D2H per step (CSC, b, h, flags)
     elif args.workload == "multistart":
         Z_pin = torch.as_tensor(Z).pin_memory()
@@ -492,6 +513,7 @@ def run_ours(args):
                 "kernel": ("k_linearize2<Topo_halfcheetah_g2,1> (1 interval/CTA)" if B_k1 <= 98
                            else "k_linearize<Topo_halfcheetah_g2,1,3> (3 intervals/CTA in lockstep)"),
                 "kernel_ms": k1_ms, "intervals_per_launch": B_k1,
+                "step_linearize_all_ms": step_k1_ms,
                 "flops_per_interval": F, "flops_definition": fdef,
                 "peak_source": "measured in this run: FP64 DFMA probe kernel (cito_dfma_peak); MEASURED_PEAKS.json "
                                "has no fp64 entry"}
