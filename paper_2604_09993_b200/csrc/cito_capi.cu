@@ -163,7 +163,7 @@ cito_status launch_propagate(const KParams& P, int64_t B, const double* xt0s, co
                                                              ZSrc{});
   } else {
     const int nt = 64;
-    k_primal<M, false><<<(unsigned)((B + nt - 1) / nt), nt, 0, st>>>(P, B, xt0s, Us, Ss, ends, bad, nullptr, nullptr);
+    k_primal<M><<<(unsigned)((B + nt - 1) / nt), nt, 0, st>>>(P, B, xt0s, Us, Ss, ends, bad);
   }
   CUDA_TRY(cudaGetLastError());
   return CITO_OK;

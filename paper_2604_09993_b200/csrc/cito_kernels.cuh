@@ -676,9 +676,9 @@ struct Dims {
   static constexpr int NT = ((NCOL > NDIR ? NCOL : NDIR) + 31) / 32 * 32;
 };
 
-// Per-stage record of the primal trajectory: everything the tangent kernel needs
-// to form the rate Jacobian of that stage and the dS terms, so K1b never
-// recomputes (or waits on) the primal chain.
+// Per-stage record of the primal trajectory (a slot of K1's smem ring): everything
+// the Jacobian and column warps need for that stage's rate Jacobian and dS terms,
+// so they never recompute (or wait on) the primal chain.
 template <class M>
 struct Rec {
   Prim<M> pr;
@@ -688,25 +688,22 @@ struct Rec {
 };
 
 // ---------------------------------------------------------------------------
-// K1a / K2: primal RKF flow, one thread per interval (cito/augmentation.py:195-211).
-// REC=true also writes the per-stage records (rec) and the per-substep
-// h*sum_i b_i v_{s,i} (vb) consumed by K1b.
-template <class M, bool REC>
+// K2: primal RKF flow, one thread per interval (cito/augmentation.py:195-211);
+// the throughput variant of propagate for batches larger than the SMs.
+template <class M>
 __global__ void __launch_bounds__(64) k_primal(const KParams P, int64_t B, const double* __restrict__ xt0s,
                                                const double* __restrict__ Us, const double* __restrict__ Ss,
-                                               double* __restrict__ ends, int32_t* __restrict__ bad,
-                                               Rec<M>* __restrict__ rec, double* __restrict__ vb) {
+                                               double* __restrict__ ends, int32_t* __restrict__ bad) {
   using D = Dims<M>;
-  constexpr int NQ = D::NQ, NX = D::NX, NU = D::NU, NY = D::NY, NXT = D::NXT, NR = D::NR;
+  constexpr int NX = D::NX, NU = D::NU, NY = D::NY, NXT = D::NXT;
   const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
-  double x[NXT], xs[NX], r[NXT], K[6][NX], ky[Pos<NY>::v], U[2 * NU + 1], VS[6][NQ];
+  double x[NXT], xs[NX], r[NXT], K[6][NX], ky[Pos<NY>::v], U[2 * NU + 1];
   Prim<M> pr;
   for (int k = 0; k < NXT; ++k) x[k] = xt0s[b * NXT + k];
   for (int k = 0; k < 2 * NU; ++k) U[k] = Us[b * 2 * NU + k];
   const double S = Ss[b];
   const double h = P.h;
-  const int nst = 6 * P.substeps;
   for (int s = 0; s < P.substeps; ++s) {
     const double tau0 = h * (double)s;
 #pragma unroll
@@ -725,18 +722,6 @@ __global__ void __launch_bounds__(64) k_primal(const KParams P, int64_t B, const
       for (int k = 0; k < NX; ++k) K[i][k] = S * r[k];
 #pragma unroll
       for (int k = 0; k < NY; ++k) ky[k] += P.b[i] * (S * r[NX + k]);
-      if (REC) {
-        Rec<M>& R = rec[b * nst + s * 6 + i];
-        R.pr = pr;
-        for (int k = 0; k < NQ; ++k) {
-          VS[i][k] = xs[NQ + k];
-          R.vs[k] = xs[NQ + k];
-          double w = 0.0;
-          for (int j = 0; j < i; ++j) w += P.ha[i][j] * VS[j][k];
-          R.wq[k] = w;
-        }
-        for (int k = 0; k < NR; ++k) R.r[k] = r[NQ + k];
-      }
     }
     for (int k = 0; k < NX; ++k) {
       double inc = 0.0;
@@ -745,13 +730,6 @@ __global__ void __launch_bounds__(64) k_primal(const KParams P, int64_t B, const
     }
 #pragma unroll
     for (int k = 0; k < NY; ++k) x[NX + k] = x[NX + k] + h * ky[k];
-    if (REC) {
-      for (int k = 0; k < NQ; ++k) {
-        double w = 0.0;
-        for (int j = 0; j < 6; ++j) w += P.b[j] * VS[j][k];
-        vb[(b * P.substeps + s) * NQ + k] = h * w;
-      }
-    }
   }
   int nb = 0;
   for (int k = 0; k < NXT; ++k) {
