@@ -590,28 +590,10 @@ def run_reference(args):
 
 
 def _lib_launches():
-    """Kernels launched by libcito_b200 so far (global counter of the C ABI)."""
+    """Kernels launched by libcito_b200 so far (C ABI counter + CUDA-graph replays)."""
     from paper_2604_09993_b200 import _lib
 
     return _lib.launch_count()
-
-
-def _assembler_of(trs):
-    from paper_2604_09993_b200.subproblem import _assemblers
-
-    return [a for k, a in _assemblers.items() if k[0] == id(trs)][0]
-
-
-class _TrShim:
-    """Minimal Transcription-like view of a GpuTranscription for build_subproblem."""
-
-    def __init__(self, gt):
-        from paper_2604_09993_b200.linearize import _cache
-        from paper_2604_09993_b200.scenario import build_scaling
-
-        self.scenario, self.layout = gt.scenario, gt.lay
-        self.scaling = type("S", (), {"scale": build_scaling(gt.scenario, gt.lay)[0]})()
-        _cache[id(self)] = (self, gt)
 
 
 def main():

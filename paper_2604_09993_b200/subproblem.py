@@ -661,11 +661,12 @@ def build_subproblem(tr, lin, z_j, delta, config):
 
     key = (id(tr), float(config.w_prox), float(config.w_ep))
     asm = _assemblers.get(key)
-    if asm is None:
+    if asm is None or getattr(asm, "owner", None) is not tr:  # the strong ref keeps id(tr) from being reused
         dev = torch.device("cuda", torch.cuda.current_device())
         scale_v = tr.scaling.scale if hasattr(tr, "scaling") else build_scaling(tr.scenario, tr.layout)[0]
         pat = SubproblemPattern(tr.scenario, tr.layout, scale_v, config.w_prox, config.w_ep)
         asm = SubproblemAssembler(pat, dev)
+        asm.owner = tr
         _assemblers[key] = asm
     dev = asm.device
     from .linearize import _cache
