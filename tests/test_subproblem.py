@@ -151,3 +151,23 @@ def test_gpu_scp_step_iterate_matches_reference():
     assert rel_err(lin.jx, g["ig_jx"]) <= 1e-9 and rel_err(lin.defects, g["ig_defects"]) <= 1e-9
     with pytest.raises(FloatingPointError):
         step.iterate(np.full_like(g["ig_z"], np.nan), 1.0)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", CASES)
+def test_gpu_scp_step_all_models_match_reference(name):
+    """GpuSCPStep (captured graph, packed result) on every golden model: pattern
+    bit-exact and values rel <= 1e-9 against the reference's build_subproblem."""
+    from paper_2604_09993_b200.subproblem import GpuSCPStep
+
+    g = load_golden(name)
+    step = GpuSCPStep(golden_scenario(name))
+    for _ in range(2):  # first call captures the graph, second replays it
+        lin, prog, meta = step.iterate(g["ig_z"], 1.0, z_j=g["sp0_zj"])
+        for M in ("A", "G"):
+            mat = getattr(prog, M)
+            assert np.array_equal(mat.indptr, g[f"sp0_{M}_indptr"]) and np.array_equal(mat.indices,
+                                                                                      g[f"sp0_{M}_indices"])
+            assert rel_err(mat.data, g[f"sp0_{M}_data"]) <= 1e-9, M
+        assert rel_err(prog.b, g["sp0_b"]) <= 1e-9 and rel_err(prog.h, g["sp0_h"]) <= 1e-9
+        assert np.array_equal(prog.c, g["sp0_c"])
