@@ -460,7 +460,7 @@ def run_ours(args):
 
         e2e_step()
         h2d = z.nbytes + 16  # z plus [delta, epsilon] (one pinned H2D per step)
-        d2h = int(scp_api._plan["pk"].nbytes)  # one packed D2H per step (CSC, b, h, flags)
+        d2h = scp_api.d2h_bytes()  # packed D2H per step: fixed fields + the CSC arrays up to their caps
     elif args.workload == "multistart":
         Z_pin = torch.as_tensor(Z).pin_memory()
         ms_host = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in ms_out.items()}

@@ -722,6 +722,7 @@ class _HostBuf:
             npdt = torch.empty((), dtype=dtype).numpy().dtype
             self.h[name] = self.nb[o: o + max(1, n) * isz].view(npdt)[:n]
         self.graphs = {}
+        self.caps = {}
         self._base = None
 
     def free(self):
@@ -864,7 +865,38 @@ class GpuSCPStep:
         cur.wait_stream(side)
         if precondition:
             _lib.check(L.cito_precondition_dev(*pl["pc_args"], s), "precondition")
-        hb.host.copy_(pl["pk"].dev, non_blocking=True)
+        self._d2h(hb)
+
+    def _d2h(self, hb, tail=False):
+        """Device -> pinned copies of the packed result: the fixed fields in one
+        copy, the CSC values/indices only up to the buffer's caps (the nnz of
+        the previous result + 25 %, so about half of the superset-sized
+        arrays); `tail` copies what lies beyond the caps (the rare case of a
+        result with more nonzeros than the caps)."""
+        pk = self._plan["pk"]
+        lay = pk.layout
+        if not tail:
+            end = lay["A_data"][0]  # fixed fields precede the CSC arrays
+            hb.host[:end].copy_(pk.dev[:end], non_blocking=True)
+        for M in ("A", "G"):
+            cap = hb.caps.get(M, lay[f"{M}_data"][2])
+            for fld in (f"{M}_data", f"{M}_indices"):
+                o, _, n, isz = lay[fld]
+                lo, hi = (cap, n) if tail else (0, min(cap, n))
+                if hi > lo:
+                    hb.host[o + lo * isz: o + hi * isz].copy_(pk.dev[o + lo * isz: o + hi * isz], non_blocking=True)
+
+    def d2h_bytes(self):
+        """Bytes of the device->host copies one (graph-replayed) iteration makes."""
+        pk = self._plan["pk"]
+        lay = pk.layout
+        hb = self._plan["hosts"][-1] if self._plan["hosts"] else None
+        n = lay["A_data"][0]
+        for M in ("A", "G"):
+            cap = hb.caps.get(M, lay[f"{M}_data"][2]) if hb is not None else lay[f"{M}_data"][2]
+            for fld in (f"{M}_data", f"{M}_indices"):
+                n += min(cap, lay[fld][2]) * lay[fld][3]
+        return int(n)
 
     def _host_buffer(self):
         """A pinned result buffer no live array points into (a new one when every
@@ -884,8 +916,12 @@ class GpuSCPStep:
         import torch
 
         pl = self._plan
+        hb.caps = {}
         self._launch(precondition, hb)
         torch.cuda.current_stream(self.gt.device).synchronize()
+        for M in ("A", "G"):  # D2H caps of the captured copies: this result's nnz + 25 % (+4096)
+            nnz = int(hb.h[f"{M}_indptr"][-1])
+            hb.caps[M] = min(pl["pk"].layout[f"{M}_data"][2], nnz + nnz // 4 + 4096)
         g = torch.cuda.CUDAGraph()
         n0 = int(pl["L"].cito_launch_count(None))
         with torch.cuda.graph(g):
@@ -933,6 +969,10 @@ class GpuSCPStep:
         nA = pl["nA"]
         stream.synchronize()  # the one synchronization
         hh = hb.h
+        if any(int(hh[f"{M}_indptr"][-1]) > hb.caps.get(M, 1 << 62) for M in ("A", "G")):
+            self._d2h(hb, tail=True)  # more nonzeros than the captured copies cover
+            stream.synchronize()
+            hb.graphs.clear()  # recapture with caps from this result
         bad = hh["bad"]
         if bad.any():
             raise FloatingPointError(f"non-finite state in intervals {np.where(bad != 0)[0].tolist()}")

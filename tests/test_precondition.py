@@ -262,3 +262,28 @@ def test_gpu_scp_step_results_survive_later_iterations():
     for d in (0.5, 0.25):
         step.iterate(z2, d)
     assert len(step._plan["hosts"]) == n_before  # freed buffers are reused
+
+
+@pytest.mark.gpu
+def test_gpu_scp_step_d2h_caps_overflow():
+    """The captured D2H copies cover the CSC arrays only up to caps; a result with
+    more nonzeros than the caps must still come back complete (tail copy) and
+    trigger a recapture."""
+    from paper_2604_09993_b200.subproblem import GpuSCPStep
+
+    name = "halfcheetah_n30"
+    g = load_golden(name)
+    sc = golden_scenario(name)
+    sg, se = GpuSCPStep(sc, use_graph=True), GpuSCPStep(sc, use_graph=False)
+    z = g["ig_z"]
+    sg.iterate(z, 1.0)  # capture
+    for hb in sg._plan["hosts"]:
+        hb.caps = {"A": 100, "G": 10}  # pretend the captured copies were tiny
+    _, pg, _ = sg.iterate(z, 0.5)
+    _, pe, _ = se.iterate(z, 0.5)
+    for M in ("A", "G"):
+        a, b = getattr(pg, M), getattr(pe, M)
+        assert np.array_equal(a.indptr, b.indptr) and np.array_equal(a.indices, b.indices)
+        assert np.array_equal(a.data, b.data)
+    assert np.array_equal(pg.b, pe.b)
+    assert sg.d2h_bytes() < sg._plan["pk"].nbytes
