@@ -297,14 +297,16 @@ def run_ours(args):
 
     k1_ev = []
 
+    lin_out = gt.linearize_device(z_dev, delta)  # output buffers reused by every step
+
     def scp_step(zd, record=False):
         if record:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            r = gt.linearize_device(zd, delta, k1_events=(e0, e1))
+            r = gt.linearize_device(zd, delta, k1_events=(e0, e1), out=lin_out)
             k1_ev.append((e0, e1))
         else:
-            r = gt.linearize_device(zd, delta)
-        asm.assemble_device(r, zd)  # whole subproblem: CSC of A, G (+ zero compaction), b, h
+            r = gt.linearize_device(zd, delta, out=lin_out)
+        asm.assemble_device(r, zd, reuse=True)  # whole subproblem: CSC of A, G (+ zero compaction), b, h
         return r
 
     # --- batch workload state
@@ -431,14 +433,16 @@ def run_ours(args):
         zf = torch.as_tensor(initial_guess(scf, gtf.disc, gtf.lay), device=dev)
         asmf = SubproblemAssembler(SubproblemPattern(scf, gtf.lay, build_scaling(scf, gtf.lay)[0]), dev)
 
+        fine_out = gtf.linearize_device(zf, delta)
+
         def fine_step(record=False):
             if record:
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                r = gtf.linearize_device(zf, delta, k1_events=(e0, e1))
+                r = gtf.linearize_device(zf, delta, k1_events=(e0, e1), out=fine_out)
                 k1_ev.append((e0, e1))
             else:
-                r = gtf.linearize_device(zf, delta)
-            asmf.assemble_device(r, zf)
+                r = gtf.linearize_device(zf, delta, out=fine_out)
+            asmf.assemble_device(r, zf, reuse=True)
 
         nf = max(5, K // 5)
         fms, fk1, _ = timed(fine_step, nf, 5)

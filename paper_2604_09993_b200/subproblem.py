@@ -523,10 +523,12 @@ class SubproblemAssembler:
                          cols=torch.cat([dA["cols"], dG["cols"]]), const=torch.cat([dA["rhs_const"], dG["rhs_const"]]),
                          n=dA["nlin"] + dG["nlin"], nA=nA)
 
-    def assemble_device(self, lin, z_ref_dev, stream=None, precondition=False):
+    def assemble_device(self, lin, z_ref_dev, stream=None, precondition=False, reuse=False):
         """lin: dict of device tensors with the LIN_SOURCES fields.  Returns device
         tensors {A_indptr, A_indices, A_data, b, G_indptr, G_indices, G_data, h}
         (data/indices sized to the superset; valid prefix = indptr[-1]).
+        ``reuse``: write into buffers owned by the assembler (no allocation per
+        call; the previous call's result is overwritten) -- for iteration loops.
         Four kernel launches: count (A and G), scan, write, rhs.  With
         ``precondition`` the program is returned already row-scaled as
         cito.conic.precondition does (conic.py:290-338): the row inf-norms are
@@ -541,10 +543,18 @@ class SubproblemAssembler:
         out = {}
         mats = [self._mats["A"], self._mats["G"]]
         outs = []
+        owned = getattr(self, "_owned", None) if reuse else None
+        if reuse and owned is None:
+            owned = self._owned = {}
         for M, d in zip(("A", "G"), mats):
-            indptr = torch.empty(self.pat.n + 1, dtype=torch.int32, device=self.device)
-            rows = torch.empty(max(1, d["nsup"]), dtype=torch.int32, device=self.device)
-            vals = torch.empty(max(1, d["nsup"]), dtype=torch.float64, device=self.device)
+            if owned is not None and M in owned:
+                indptr, rows, vals = owned[M]
+            else:
+                indptr = torch.empty(self.pat.n + 1, dtype=torch.int32, device=self.device)
+                rows = torch.empty(max(1, d["nsup"]), dtype=torch.int32, device=self.device)
+                vals = torch.empty(max(1, d["nsup"]), dtype=torch.float64, device=self.device)
+                if owned is not None:
+                    owned[M] = (indptr, rows, vals)
             out[f"{M}_indptr"], out[f"{M}_indices"], out[f"{M}_data"] = indptr, rows, vals
             outs.append((indptr, rows, vals))
         arr = lambda xs: ctypes_ptr_array([x.data_ptr() for x in xs])  # noqa: E731
@@ -561,7 +571,13 @@ class SubproblemAssembler:
         side = self._side
         side.wait_stream(cur)
         with torch.cuda.stream(side):
-            rhs = r["const"].clone()
+            if owned is not None:
+                if "rhs" not in owned:
+                    owned["rhs"] = torch.empty_like(r["const"])
+                rhs = owned["rhs"]
+                rhs.copy_(r["const"])
+            else:
+                rhs = r["const"].clone()
             _lib.check(_lib.lib().cito_rhs_dev(
                 r["n"], r["rows"].data_ptr(), r["form"].data_ptr(), r["vsrc"].data_ptr(), r["voff"].data_ptr(),
                 r["seg_src"].data_ptr(), r["seg_off"].data_ptr(), r["seg_len"].data_ptr(), r["seg_cb"].data_ptr(),
@@ -573,7 +589,8 @@ class SubproblemAssembler:
             arr([o[1] for o in outs]), arr([o[2] for o in outs]), arr(rowmax) if rowmax else None, s),
             "csc_assemble")
         cur.wait_stream(side)
-        rhs.record_stream(cur)
+        if owned is None:
+            rhs.record_stream(cur)
         out["b"], out["h"] = rhs[: r["nA"]], rhs[r["nA"]:]
         if precondition:
             self._precondition(out, rowmax, s)
