@@ -350,6 +350,18 @@ struct Fused2Shared {
   int bad;
 };
 
+// Accumulate into `a`, the first contribution assigned rather than added to 0.0
+// (with every loop unrolled the `set` flags are compile-time constants, so the
+// chain carries no "0.0 + x" additions; only the sign of an exact zero differs).
+__device__ __forceinline__ void acc_add(double& a, bool& set, double x) {
+  if (set) {
+    a += x;
+  } else {
+    a = x;
+    set = true;
+  }
+}
+
 // Lane-0 critical chain of one rate evaluation: forces, Gram matrix, sparse
 // Cholesky (generated straight-line code, M::chol_solve), joint reactions,
 // vdot (cito/contact_dynamics.py:86-108, multibody.py:259-321).  Reads the
@@ -370,23 +382,26 @@ __device__ __forceinline__ void crit_chain(const KParams& P, Rec2<M>& R, int t) 
     sl[l] = pr.s[l];
   }
   double W[NQ];
+  bool Ws[NQ];
 #pragma unroll
-  for (int k = 0; k < NQ; ++k) W[k] = 0.0;
+  for (int k = 0; k < NQ; ++k) {
+    W[k] = 0.0;
+    Ws[k] = false;
+  }
 #pragma unroll
-  for (int l = 0; l < NL; ++l) W[3 * l + 1] += P.neg_mg[l];
+  for (int l = 0; l < NL; ++l) acc_add(W[3 * l + 1], Ws[3 * l + 1], P.neg_mg[l]);
 #pragma unroll
   for (int j = 0; j < NJ; ++j) {
     const int p = M::jparent(j), c = M::jchild(j), a = M::jact(j);
-    double mo = 0.0;
-    if (a >= 0) mo = mo + pr.u[a];
+    double mo = a >= 0 ? pr.u[a] : 0.0;
     if (P.jspring[j]) {
       const double th_p = p >= 0 ? q[3 * p + 2] : 0.0;
       const double om_p = p >= 0 ? v[3 * p + 2] : 0.0;
       const double rel = q[3 * c + 2] - th_p - P.jrest[j];
       mo = mo - P.jk[j] * rel - P.jd[j] * (v[3 * c + 2] - om_p);
     }
-    W[3 * c + 2] += mo;
-    if (p >= 0) W[3 * p + 2] += -mo;
+    acc_add(W[3 * c + 2], Ws[3 * c + 2], mo);
+    if (p >= 0) acc_add(W[3 * p + 2], Ws[3 * p + 2], -mo);
   }
 #pragma unroll
   for (int i = 0; i < NC; ++i) {
@@ -406,9 +421,9 @@ __device__ __forceinline__ void crit_chain(const KParams& P, Rec2<M>& R, int t) 
     const double t0 = n1, t1 = -n0;
     const double ft = pr.u[NA + 2 * i], fn = pr.u[NA + 2 * i + 1];
     const double F0 = t0 * ft + n0 * fn, F1 = t1 * ft + n1 * fn;
-    W[3 * l] += F0;
-    W[3 * l + 1] += F1;
-    W[3 * l + 2] += (-rz) * F0 + rx * F1;
+    acc_add(W[3 * l], Ws[3 * l], F0);
+    acc_add(W[3 * l + 1], Ws[3 * l + 1], F1);
+    acc_add(W[3 * l + 2], Ws[3 * l + 2], (-rz) * F0 + rx * F1);
   }
   double* vdot = R.r;
   if constexpr (NJ == 0) {
@@ -444,6 +459,7 @@ __device__ __forceinline__ void crit_chain(const KParams& P, Rec2<M>& R, int t) 
         if (!M::lnzb(a, bp)) continue;
         const int j = M::jperm(a), k = M::jperm(bp);
         double g00 = 0.0, g01 = 0.0, g10 = 0.0, g11 = 0.0;
+        bool gs = false, gs01 = false, gs10 = false, gs11 = false;
 #pragma unroll
         for (int sa = 0; sa < 2; ++sa)
 #pragma unroll
@@ -454,10 +470,10 @@ __device__ __forceinline__ void crit_chain(const KParams& P, Rec2<M>& R, int t) 
             const double sg = (sa == sb) ? 1.0 : -1.0;
             const double dA0 = -Rj[j][sa][1], dA1 = Rj[j][sa][0], dB0 = -Rj[k][sb][1], dB1 = Rj[k][sb][0];
             const double mI = P.minv_I[la], mm = P.minv_m[la];
-            g00 += sg * (dA0 * dB0 * mI + mm);
-            g01 += sg * (dA0 * dB1 * mI);
-            g10 += sg * (dA1 * dB0 * mI);
-            g11 += sg * (dA1 * dB1 * mI + mm);
+            acc_add(g00, gs, sg * (dA0 * dB0 * mI + mm));
+            acc_add(g01, gs01, sg * (dA0 * dB1 * mI));
+            acc_add(g10, gs10, sg * (dA1 * dB0 * mI));
+            acc_add(g11, gs11, sg * (dA1 * dB1 * mI + mm));
           }
         Lr[LI(2 * a, 2 * bp)] = g00;
         Lr[LI(2 * a + 1, 2 * bp)] = g10;
@@ -471,6 +487,7 @@ __device__ __forceinline__ void crit_chain(const KParams& P, Rec2<M>& R, int t) 
 #pragma unroll
       for (int al = 0; al < 2; ++al) {
         double acc = 0.0;
+        bool as = false;
 #pragma unroll
         for (int sa = 0; sa < 2; ++sa) {
           const int l = sa == 0 ? M::jparent(j) : M::jchild(j);
@@ -478,7 +495,8 @@ __device__ __forceinline__ void crit_chain(const KParams& P, Rec2<M>& R, int t) 
           const double sgn = sa == 0 ? 1.0 : -1.0;
           const double dP = al == 0 ? -Rj[j][sa][1] : Rj[j][sa][0];
           const double om = v[3 * l + 2];
-          acc += sgn * (P.minv_m[l] * W[3 * l + al] + dP * P.minv_I[l] * W[3 * l + 2] - Rj[j][sa][al] * om * om);
+          acc_add(acc, as,
+                  sgn * (P.minv_m[l] * W[3 * l + al] + dP * P.minv_I[l] * W[3 * l + 2] - Rj[j][sa][al] * om * om));
         }
         y[2 * a + al] = acc;
       }
