@@ -515,6 +515,7 @@ def run_ours(args):
                 "frac": (achieved / peak) if achieved else None,
                 "traffic": ncu_traffic(f"k_linearize_{'scp' if fine else args.workload}"),
                 "kernel": ("k_linearize2<Topo_halfcheetah_g2,1> (1 interval/CTA)" if B_k1 <= 98
+                           else "k_linearize<Topo_halfcheetah_g2,1,2> (2 intervals/CTA in lockstep)" if B_k1 <= 246
                            else "k_linearize<Topo_halfcheetah_g2,1,3> (3 intervals/CTA in lockstep)"),
                 "kernel_ms": k1_ms, "intervals_per_launch": B_k1,
                 "step_linearize_all_ms": step_k1_ms,

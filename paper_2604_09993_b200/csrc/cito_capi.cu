@@ -102,6 +102,8 @@ cito_status launch_linearize(const KParams& P, int64_t B, const double* xt0s, co
   if (!attr_done) {
     CUDA_TRY(cudaFuncSetAttribute(k_linearize<M, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1));
     CUDA_TRY(cudaFuncSetAttribute(k_linearize<M, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1));
+    CUDA_TRY(cudaFuncSetAttribute(k_linearize<M, 1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(2 * ((smem1 + 127) / 128 * 128))));
     CUDA_TRY(cudaFuncSetAttribute(k_linearize<M, 1, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(3 * ((smem1 + 127) / 128 * 128))));
     CUDA_TRY(cudaFuncSetAttribute(k_linearize2<M, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
@@ -131,7 +133,14 @@ cito_status launch_linearize(const KParams& P, int64_t B, const double* xt0s, co
     // three intervals per CTA in lockstep (same-role warps share an SM sub-partition and
     // fetch the same instructions); CITO_K1_IPC1=1: one interval per CTA, 3 CTAs/SM
     static const bool ipc3 = getenv("CITO_K1_IPC1") == nullptr;
-    if (ipc3)
+    // two lockstep intervals per CTA while that keeps at most ~1.65 waves of CTAs
+    // (measured crossover with three per CTA at 245..250 intervals on 148 SMs)
+    static const int64_t ipc2_env = getenv("CITO_K1_IPC2_MAX") ? atoll(getenv("CITO_K1_IPC2_MAX")) : -1;
+    const int64_t ipc2_max = ipc2_env >= 0 ? ipc2_env : (5 * (int64_t)sms) / 3;
+    if (ipc3 && B <= ipc2_max)
+      k_linearize<M, 1, 2><<<(unsigned)((B + 1) / 2), 2 * FusedDims<M>::NT, 2 * ((smem1 + 127) / 128 * 128), st>>>(
+          P, B, xt0s, Us, Ss, ends, jx, ju, js, bad, zs);
+    else if (ipc3)
       k_linearize<M, 1, 3><<<(unsigned)((B + 2) / 3), 3 * FusedDims<M>::NT, 3 * ((smem1 + 127) / 128 * 128), st>>>(
           P, B, xt0s, Us, Ss, ends, jx, ju, js, bad, zs);
     else
