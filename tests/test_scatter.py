@@ -160,3 +160,27 @@ def test_initial_guess_matches_reference_and_batch():
         Z = initial_guess_batch(sc, gt.disc, [sc.seed, 3, 11], gt.lay)
         assert np.array_equal(Z[0], z)
         assert np.array_equal(Z[2], initial_guess(sc, gt.disc, gt.lay, seed=11))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("P", [6, 12])
+def test_multistart_on_batch_kernels_equals_single_problems(P):
+    """Multi-start batches large enough for the lockstep batch kernels (6 x 29 = 174
+    intervals: 2 per CTA; 12 x 29 = 348: 3 per CTA) read z in-kernel exactly like
+    the single-problem latency kernel."""
+    import torch
+
+    from paper_2604_09993_b200.linearize import GpuTranscription, initial_guess_batch
+
+    sc = golden_scenario("halfcheetah_n30")
+    gt = GpuTranscription(sc)
+    Z = initial_guess_batch(sc, gt.disc, list(range(P)), gt.lay)
+    zd = torch.as_tensor(Z, device=gt.device)
+    allp = gt.linearize_device(zd, 0.3)
+    n_int, n_node = gt.lay.N - 1, gt.lay.N
+    for p in (0, P // 2, P - 1):
+        one = gt.linearize_device(zd[p].contiguous(), 0.3)
+        for k, v in one.items():
+            rows = n_node if k in ("theta", "theta_jac", "imp_v", "imp_jac") else n_int
+            got = allp[k][p * rows:(p + 1) * rows]
+            assert rel_err(got.cpu().numpy(), v.cpu().numpy()) <= 1e-11, (P, k)
