@@ -747,8 +747,7 @@ __device__ __forceinline__ void col_stage2(const KParams& P, Fused2Shared<M>& sh
     for (int j = 0; j < RC; ++j) {
       const int rr = r0 + j;
       if (rr >= NR) break;
-      double dk = S * accs[j];
-      if (dS != 0.0) dk = dk + dS * R.r[rr];  // the dilation column only
+      const double dk = S * accs[j] + dS * R.r[rr];  // dS = 1 for the dilation column only
       if (rr < NQ) {
         const int hs = M::hslot(rr);
         if (hs >= 0) {
