@@ -315,7 +315,8 @@ template <class M>
 struct RegState {
   static constexpr int PER = (Dims<M>::NX + 31) / 32;
   static constexpr int NH = Pos<M::NHIST>::v;
-  static constexpr int a = 7 * PER, b = 8, c = 2 * NH;
+  static constexpr int NPU = Pos<M::NPUSH>::v, NYR = Pos<5 * M::NC + M::NGO>::v;
+  static constexpr int a = 7 * PER, b = 8, c = 2 * NH + 2 * NPU + NYR;  // columns: history, push rows, y rows
   static constexpr int N = a > b ? (a > c ? a : c) : (b > c ? b : c);
 };
 #define RS_XR(p) rs[(p)]
@@ -325,6 +326,9 @@ struct RegState {
 #define RS_YV rs[7]
 #define RS_HQ(h) rs[(h)]
 #define RS_HV(h) rs[RegState<M>::NH + (h)]
+#define RS_PQ(p) rs[2 * RegState<M>::NH + (p)]
+#define RS_PV(p) rs[2 * RegState<M>::NH + RegState<M>::NPU + (p)]
+#define RS_DY(k) rs[2 * RegState<M>::NH + 2 * RegState<M>::NPU + (k)]
 
 template <class M>
 struct AuxScratch {
@@ -698,7 +702,7 @@ __device__ __forceinline__ void col_stage2(const KParams& P, Fused2Shared<M>& sh
   const double hb = h * P.b[I];
   if (I == 0) {
 #pragma unroll
-    for (int p = 0; p < M::NPUSH; ++p) sh.PQ[p][col] += P.he1 * S * sh.PV[p][col];
+    for (int p = 0; p < M::NPUSH; ++p) RS_PQ(p) += P.he1 * S * RS_PV(p);
   }
   // stage coefficients, once per tick (warp-uniform): S h^2 sum a a (q rows), h a (v rows)
   // stage-input tangents along the rate-Jacobian directions: base value, then the
@@ -766,11 +770,11 @@ __device__ __forceinline__ void col_stage2(const KParams& P, Fused2Shared<M>& sh
           }
         } else {
           const int p = M::pslot(rr);
-          sh.PV[p][col] += hb * dk;
-          sh.PQ[p][col] += S * P.e2[I] * dk + dS * hb * R.xs[NQ + rr];
+          RS_PV(p) += hb * dk;
+          RS_PQ(p) += S * P.e2[I] * dk + dS * hb * R.xs[NQ + rr];
         }
       } else {
-        sh.DY[rr - NQ][col] += hb * dk;
+        RS_DY(rr - NQ) += hb * dk;
       }
     }
   }
@@ -850,12 +854,12 @@ __global__ void __launch_bounds__(JAC ? K2Dims<M>::NT : 64, MINB) k_linearize2(c
         RS_HQ(M::hslot(c)) = e_q;
         RS_HV(M::hslot(c)) = e_v;
       } else {
-        sh.PQ[M::pslot(c)][col] = e_q;
-        sh.PV[M::pslot(c)][col] = e_v;
+        RS_PQ(M::pslot(c)) = e_q;
+        RS_PV(M::pslot(c)) = e_v;
       }
     }
 #pragma unroll
-    for (int k = 0; k < NY; ++k) sh.DY[k][col] = 0.0;
+    for (int k = 0; k < NY; ++k) RS_DY(k) = 0.0;
   }
   __syncthreads();
   const double S = sh.S, h = P.h;
@@ -976,11 +980,11 @@ __global__ void __launch_bounds__(JAC ? K2Dims<M>::NT : 64, MINB) k_linearize2(c
 #pragma unroll
     for (int c = 0; c < NQ; ++c) {
       const int hs = M::hslot(c);
-      dst[c * stride] = hs >= 0 ? RS_HQ(hs) : sh.PQ[M::pslot(c)][col];
-      dst[(NQ + c) * stride] = hs >= 0 ? RS_HV(hs) : sh.PV[M::pslot(c)][col];
+      dst[c * stride] = hs >= 0 ? RS_HQ(hs) : RS_PQ(M::pslot(c));
+      dst[(NQ + c) * stride] = hs >= 0 ? RS_HV(hs) : RS_PV(M::pslot(c));
     }
 #pragma unroll
-    for (int k = 0; k < NY; ++k) dst[(NX + k) * stride] = sh.DY[k][col];
+    for (int k = 0; k < NY; ++k) dst[(NX + k) * stride] = RS_DY(k);
   }
   if constexpr (M::NLCOL > 0) {  // closed-form columns (state directions no rate reads)
     double dqc = 0.0;
