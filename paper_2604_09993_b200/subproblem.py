@@ -724,31 +724,50 @@ class _Packed:
             self.d[name] = self.dev[o: o + max(1, n) * isz].view(dtype)[:n]
 
 
+class _Span:
+    """Owner object of one handed-out array over pinned memory (numpy
+    __array_interface__): the array's base, with `size` equal to the array's
+    length so scipy's _prune_array never copies it, and weakly referenceable so
+    the buffer knows when the caller has dropped the array."""
+
+    def __init__(self, ptr, n, dtype):
+        self.size = int(n)
+        self.__array_interface__ = {"data": (int(ptr), False), "shape": (int(n),), "typestr": dtype.str,
+                                    "version": 3}
+
+
 class _HostBuf:
     """A pinned host mirror of a _Packed buffer whose arrays are handed out
-    without copying.  It is free again once no array viewing it is alive: every
-    view's numpy base is `self.nb`, so its reference count tells."""
+    without copying.  It is free again once every array handed out from it has
+    been dropped (weak references to their _Span owners)."""
 
     def __init__(self, pk):
         import torch
 
         self.host = torch.empty(pk.nbytes, dtype=torch.uint8, pin_memory=True)
         self.nb = self.host.numpy()
-        self.h = {}
+        self.h, self.np_dtype, self.off = {}, {}, {}
         for name, (o, dtype, n, isz) in pk.layout.items():
             npdt = torch.empty((), dtype=dtype).numpy().dtype
             self.h[name] = self.nb[o: o + max(1, n) * isz].view(npdt)[:n]
+            self.np_dtype[name], self.off[name] = (npdt, isz), o
+        self.base_ptr = self.nb.ctypes.data
         self.graphs = {}
         self.caps = {}
-        self._base = None
+        self.live = []
+
+    def wrap(self, name, start, n):
+        """Array of n elements of field `name` from element `start`, owned by a _Span."""
+        import weakref
+
+        npdt, isz = self.np_dtype[name]
+        span = _Span(self.base_ptr + self.off[name] + start * isz, n, npdt)
+        self.live.append(weakref.ref(span))
+        return np.asarray(span)
 
     def free(self):
-        import sys as _sys
-
-        rc = _sys.getrefcount(self.nb)
-        if self._base is None:
-            self._base = rc
-        return rc <= self._base
+        self.live = [r for r in self.live if r() is not None]
+        return not self.live
 
 
 class GpuSCPStep:
@@ -923,7 +942,6 @@ class GpuSCPStep:
             if hb.free():
                 return hb
         hb = _HostBuf(pl["pk"])
-        hb.free()  # record the baseline reference count
         pl["hosts"].append(hb)
         return hb
 
@@ -995,11 +1013,10 @@ class GpuSCPStep:
             raise FloatingPointError(f"non-finite state in intervals {np.where(bad != 0)[0].tolist()}")
         ConicProgram, ConeSpec = _conic_types()
         mats = {}
-        for M, nrows in (("A", nA), ("G", pl["nG"])):  # views into the pinned buffer (no copy)
-            indptr = hh[f"{M}_indptr"]
-            nnz = int(indptr[-1])
-            mats[M] = sp.csc_matrix((hh[f"{M}_data"][:nnz], hh[f"{M}_indices"][:nnz], indptr),
-                                    shape=(nrows, pat.n), copy=False)
+        for M, nrows in (("A", nA), ("G", pl["nG"])):  # arrays over the pinned buffer (no copy)
+            nnz = int(hh[f"{M}_indptr"][-1])
+            mats[M] = sp.csc_matrix((hb.wrap(f"{M}_data", 0, nnz), hb.wrap(f"{M}_indices", 0, nnz),
+                                     hb.wrap(f"{M}_indptr", 0, pat.n + 1)), shape=(nrows, pat.n), copy=False)
         zj = z if z_j is None else z_j
         c = pat.objective_c(zj)
         P_data = pat.P_diag[: pat.lay.dim]
@@ -1013,14 +1030,15 @@ class GpuSCPStep:
             if pl["P_plain"] is None:
                 pl["P_plain"] = sp.csc_matrix((P_data, pl["P_idx"], pl["P_ptr"]), shape=(pat.n, pat.n))
             P = pl["P_plain"].copy()
-        prog = ConicProgram(P=P, c=c, A=mats["A"], b=hh["rhs"][:nA], G=mats["G"], h=hh["rhs"][nA:],
+        prog = ConicProgram(P=P, c=c, A=mats["A"], b=hb.wrap("rhs", 0, nA), G=mats["G"], h=hb.wrap("rhs", nA, pl["nG"]),
                             cones=ConeSpec(nonneg=pat.n_orthant, soc=pat.soc_dims))
         lin = self._Lazy(pl["lin"], z.copy())
         import weakref
 
         self._last_lin = weakref.ref(lin)
         if precondition:
-            prec = _preconditioner_type()(row_scale_A=hh["row_scale_A"], row_scale_G=hh["row_scale_G"],
+            prec = _preconditioner_type()(row_scale_A=hb.wrap("row_scale_A", 0, nA),
+                                          row_scale_G=hb.wrap("row_scale_G", 0, pl["nG"]),
                                           var_scale=np.ones(pat.n), cost_scale=omega)
             return lin, prog, prec, pl["meta"]
         return lin, prog, pl["meta"]
