@@ -1027,9 +1027,12 @@ class GpuSCPStep:
             P = sp.csc_matrix((P_data * (1.0 / omega), pl["P_idx"], pl["P_ptr"]), shape=(pat.n, pat.n))
             c = c / omega
         else:
-            if pl["P_plain"] is None:
-                pl["P_plain"] = sp.csc_matrix((P_data, pl["P_idx"], pl["P_ptr"]), shape=(pat.n, pat.n))
-            P = pl["P_plain"].copy()
+            if pl["P_plain"] is None:  # constant: one read-only matrix shared by every result
+                Pm = sp.csc_matrix((P_data.copy(), pl["P_idx"].copy(), pl["P_ptr"].copy()), shape=(pat.n, pat.n))
+                for arr in (Pm.data, Pm.indices, Pm.indptr):
+                    arr.flags.writeable = False
+                pl["P_plain"] = Pm
+            P = pl["P_plain"]
         prog = ConicProgram(P=P, c=c, A=mats["A"], b=hb.wrap("rhs", 0, nA), G=mats["G"], h=hb.wrap("rhs", nA, pl["nG"]),
                             cones=ConeSpec(nonneg=pat.n_orthant, soc=pat.soc_dims))
         lin = self._Lazy(pl["lin"], z.copy())
