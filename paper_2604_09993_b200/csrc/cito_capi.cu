@@ -60,25 +60,6 @@ struct TopoOps {
                        cudaStream_t);
 };
 
-// Stream-ordered workspace (records of the primal trajectory): allocated from
-// the device's default memory pool with a high release threshold, so repeated
-// calls reuse the same memory and concurrent calls on different streams never
-// share a buffer.
-cito_status ensure_pool() {
-  static std::once_flag once;
-  static cudaError_t err = cudaSuccess;
-  std::call_once(once, [] {
-    int dev = 0;
-    cudaMemPool_t pool;
-    err = cudaGetDevice(&dev);
-    if (err == cudaSuccess) err = cudaDeviceGetDefaultMemPool(&pool, dev);
-    uint64_t thr = ~0ull;
-    if (err == cudaSuccess) err = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-  });
-  if (err != cudaSuccess) return fail(CITO_ERR_CUDA, std::string("mempool: ") + cudaGetErrorString(err));
-  return CITO_OK;
-}
-
 // K1 selection.  Default (auto): k_linearize2 (cito_k1v2.cuh: short primal chain,
 // off-chain aux warp, q/v and u Jacobian warps) while the grid fits the SMs once
 // -- the latency case of one SCP iteration -- and k_linearize<M, 3> (cito_kernels.cuh,

@@ -793,7 +793,7 @@ __global__ void __launch_bounds__(JAC ? K2Dims<M>::NT : 64, MINB) k_linearize2(c
   using D = Dims<M>;
   using K = K2Dims<M>;
   constexpr int NQ = D::NQ, NX = D::NX, NU = D::NU, NY = D::NY, NXT = D::NXT, NCOL = D::NCOL;
-  constexpr int NDIRX = M::NDIRX, NDIR = D::NDIR, NHIST = M::NHIST, PER = K::PER;
+  constexpr int NDIRX = M::NDIRX, NDIR = D::NDIR, PER = K::PER;
   static_assert(NQ <= 32 && NY <= 32, "aux warp owns one q coordinate and one y row per lane");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Fused2Shared<M>& sh = *reinterpret_cast<Fused2Shared<M>*>(smem_raw);

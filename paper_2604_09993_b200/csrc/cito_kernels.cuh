@@ -1252,7 +1252,7 @@ __global__ void __launch_bounds__(FusedDims<M>::NT * IPC, MINB) k_linearize(cons
                                                                double* __restrict__ ju, double* __restrict__ js,
                                                                int32_t* __restrict__ bad, const ZSrc zs) {
   using D = Dims<M>;
-  constexpr int NQ = D::NQ, NX = D::NX, NU = D::NU, NY = D::NY, NXT = D::NXT, NCOL = D::NCOL, NR = D::NR;
+  constexpr int NQ = D::NQ, NX = D::NX, NU = D::NU, NY = D::NY, NXT = D::NXT, NCOL = D::NCOL;
   constexpr int NDIRX = M::NDIRX, NDIR = D::NDIR, NHIST = M::NHIST;
   constexpr int NT1 = FusedDims<M>::NT;
   constexpr size_t SHB = (sizeof(FusedShared<M>) + 127) / 128 * 128;
