@@ -539,7 +539,20 @@ class SubproblemAssembler:
         if getattr(self, "_rhs", None) is None:
             self._prepare_batched()
         s = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
-        ptrs = ctypes_ptr_array([lin[k].data_ptr() for k in LIN_SOURCES])
+        if reuse:  # stable pointers: memoize the ctypes pointer tables (host launch overhead)
+            memo = self.__dict__.setdefault("_ptr_memo", {})
+
+            def arr(xs):
+                key = tuple(x.data_ptr() for x in xs)
+                a = memo.get(key)
+                if a is None:
+                    if len(memo) > 64:
+                        memo.clear()
+                    a = memo[key] = ctypes_ptr_array(list(key))
+                return a
+        else:
+            arr = lambda xs: ctypes_ptr_array([x.data_ptr() for x in xs])  # noqa: E731
+        ptrs = arr([lin[k] for k in LIN_SOURCES])
         out = {}
         mats = [self._mats["A"], self._mats["G"]]
         outs = []
@@ -557,7 +570,6 @@ class SubproblemAssembler:
                     owned[M] = (indptr, rows, vals)
             out[f"{M}_indptr"], out[f"{M}_indices"], out[f"{M}_data"] = indptr, rows, vals
             outs.append((indptr, rows, vals))
-        arr = lambda xs: ctypes_ptr_array([x.data_ptr() for x in xs])  # noqa: E731
         rowmax = None
         if precondition:
             nA, nG = mats[0]["nrows"], mats[1]["nrows"]
