@@ -33,8 +33,23 @@ for name, kw in (("pointmass_rest", {}), ("monoped_hop", {"N": 20}), ("biped_wal
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
     ms = float(np.median(ts))
+    import time
+
+    from paper_2604_09993_b200.subproblem import GpuSCPStep
+
+    step = GpuSCPStep(gt)
+    zh = z.cpu().numpy()
+    for _ in range(5):
+        step.iterate(zh, 1.0)
+    t0 = time.perf_counter()
+    for _ in range(50):
+        step.iterate(zh, 1.0)
+    e2e = (time.perf_counter() - t0) / 50 * 1e3
     rows.append({"scenario": name, "N": sc.N, "substeps": sc.substeps, "intervals": sc.N - 1,
-                 "ms_per_iteration": ms, "us_per_interval": 1e3 * ms / (sc.N - 1)})
+                 "ms_per_iteration": ms, "us_per_interval": 1e3 * ms / (sc.N - 1),
+                 "e2e_ms_GpuSCPStep": e2e})
     print(rows[-1], flush=True)
-json.dump({"note": "device time of linearize_all (K1 || K3) + whole-subproblem assembly, initial guess, median of 30",
+json.dump({"note": "device time of linearize_all (K1 || K3) + whole-subproblem assembly (eager launches, device "
+                   "events; small models are host-issue bound here), initial guess, median of 30; e2e = wall time of "
+                   "GpuSCPStep.iterate (one CUDA graph, host numpy in / scipy program out)",
            "rows": rows}, open("gpurun_out/models_timing.json", "w"), indent=1)
