@@ -553,7 +553,7 @@ static void rate_unscaled(const cito_model_desc* m, const dual* x, const dual* u
   const dual* tau = u;
   const dual* phi = u + na;
   const dual* gam = u + na + 2 * nc;
-  dual w[3 * CITO_MAX_LINKS];
+  dual w[3 * CITO_MAX_LINKS] = {{0}};
   generalized_forces(m, q, v, tau, w);
   if (nc) contact_wrench(m, q, phi, w);
   for (int i = 0; i < nq; ++i) out[i] = v[i];
@@ -814,8 +814,7 @@ static void impulse_one(const cito_model_desc* m, const double* vec, double* imp
   const dual* vm = x + nq;
   const dual* vp = x + 2 * nq;
   const dual* Phi = x + 3 * nq;
-  dual w[3 * CITO_MAX_LINKS], vplus[3 * CITO_MAX_LINKS];
-  for (int i = 0; i < nq; ++i) w[i] = dc(0.0);
+  dual w[3 * CITO_MAX_LINKS] = {{0}}, vplus[3 * CITO_MAX_LINKS];
   if (nc) contact_wrench(m, q, Phi, w);
   eliminate(m, q, NULL, w, 1, vm, vplus);
   for (int a = 0; a < nq; ++a) {
