@@ -35,9 +35,27 @@ __device__ __forceinline__ Dn dfb(Dn a, Dn b, double delta) {  // smoothmath.py:
 }
 __device__ __forceinline__ Dn dsng(Dn x) { return x / dsqrt(x * x + dn(1.0)); }  // contact_dynamics.py:50-52
 
+// Node input [q-, v-, v+, Phi, Gamma] seeded on direction `dir`, read lazily from
+// its three source segments (z or a packed vector): a dual is formed at each use
+// instead of materialising all of them (their seeds alone would take 2 x NV
+// registers per thread).
+struct NodeIn {
+  const double *p0, *p1, *p2;  // [q-, v-] | [v+] | [Phi, Gamma]
+  int nq2, nq3, dir;
+  __device__ __forceinline__ Dn at(int k) const {
+    const double v = k < nq2 ? p0[k] : (k < nq3 ? p1[k - nq2] : p2[k - nq3]);
+    return {v, dir == k ? 1.0 : 0.0};
+  }
+};
+struct NodeView {  // NodeIn shifted by a segment offset
+  const NodeIn& in;
+  int off;
+  __device__ __forceinline__ Dn operator[](int k) const { return in.at(off + k); }
+};
+
 // contact point, frame and signed distance in dual arithmetic (multibody.py:264-269, 384-411)
-template <class M>
-__device__ void contact_geom(const KParams& P, const Dn* q, int i, Dn* dPdth, Dn* n, Dn* t, Dn& sd) {
+template <class M, class Q>
+__device__ __forceinline__ void contact_geom(const KParams& P, const Q& q, int i, Dn* dPdth, Dn* n, Dn* t, Dn& sd) {
   const int l = M::clink(i);
   double sv, cv;
   sincos(q[3 * l + 2].v, &sv, &cv);
@@ -66,10 +84,10 @@ __device__ void contact_geom(const KParams& P, const Dn* q, int i, Dn* dPdth, Dn
 }
 
 template <class M>
-__device__ void node_psi(const KParams& P, const double* yp, int dir, double delta, double eps, double* val,
-                         double* jcol, int jstride) {
+__device__ __forceinline__ void node_psi(const KParams& P, const double* ya, const double* yb, int dir, double delta,
+                                         double eps, double* val, double* jcol, int jstride) {
   constexpr int NC = M::NC, NY = 5 * NC + M::NGO;
-  auto Y = [&](int k) -> Dn { return {yp[k], dir == k ? 1.0 : 0.0}; };
+  auto Y = [&](int k) -> Dn { return {k < NY ? ya[k] : yb[k - NY], dir == k ? 1.0 : 0.0}; };  // [y+_k, y-_{k+1}]
   int r = 0;
 #pragma unroll
   for (int i = 0; i < NC; ++i) {
@@ -92,17 +110,10 @@ __device__ void node_psi(const KParams& P, const double* yp, int dir, double del
 }
 
 template <class M>
-__device__ void node_theta(const KParams& P, const double* vec, int dir, double delta, double* val, double* jcol,
-                           int jstride) {
-  constexpr int NL = M::NL, NC = M::NC, NQ = 3 * NL, NV = 3 * NQ + 3 * NC;
-  Dn x[NV];
-#pragma unroll
-  for (int k = 0; k < NV; ++k) x[k] = {vec[k], dir == k ? 1.0 : 0.0};
-  const Dn* q = x;
-  const Dn* vm = x + NQ;
-  const Dn* vp = x + 2 * NQ;
-  const Dn* Phi = x + 3 * NQ;
-  const Dn* Gam = x + 3 * NQ + 2 * NC;
+__device__ __forceinline__ void node_theta(const KParams& P, const NodeIn& x, double delta, double* val,
+                                           double* jcol, int jstride) {
+  constexpr int NL = M::NL, NC = M::NC, NQ = 3 * NL;
+  const NodeView q{x, 0}, vm{x, NQ}, vp{x, 2 * NQ}, Phi{x, 3 * NQ}, Gam{x, 3 * NQ + 2 * NC};
 #pragma unroll
   for (int i = 0; i < NC; ++i) {
     const int l = M::clink(i);
@@ -132,16 +143,56 @@ __device__ void node_theta(const KParams& P, const double* vec, int dir, double 
   }
 }
 
+// Block pattern of the joint Gram matrix (joints coupled iff they share a link) and
+// of its Cholesky factor in JOINT order, fill included (symbolic elimination at
+// compile time).  Skipping the structural zeros leaves every computed value
+// bit-identical to the dense factorisation (the skipped terms are exact zeros).
 template <class M>
-__device__ void node_impulse(const KParams& P, const double* vec, int dir, double* val, double* jcol, int jstride) {
-  constexpr int NL = M::NL, NJ = M::NJ, NC = M::NC, NQ = 3 * NL, NI = 3 * NQ + 2 * NC;
-  Dn x[NI];
+struct JointFill {
+  static constexpr int NB = M::NJ > 0 ? M::NJ : 1;
+  bool g[NB][NB], l[NB][NB];
+  constexpr JointFill() : g(), l() {
+    for (int j = 0; j < M::NJ; ++j)
+      for (int k = 0; k < M::NJ; ++k) {
+        const int pj = M::jparent(j), cj = M::jchild(j), pk = M::jparent(k), ck = M::jchild(k);
+        const bool share = j == k || (pj >= 0 && (pj == pk || pj == ck)) || cj == ck || (pk >= 0 && cj == pk);
+        g[j][k] = share;
+        l[j][k] = share;
+      }
+    for (int c = 0; c < M::NJ; ++c)
+      for (int r = c + 1; r < M::NJ; ++r)
+        if (l[r][c])
+          for (int r2 = c + 1; r2 <= r; ++r2)
+            if (l[r2][c]) l[r][r2] = l[r2][r] = true;
+  }
+};
+
+// Entry (2j+al, 2k+be) of the joint Gram matrix J M^-1 J^T in dual arithmetic
+// (contact_dynamics.py:91-92), from the rotated joint anchors R[joint][side][xz].
+template <class M, int NJP>
+__device__ __forceinline__ Dn gram_entry(const KParams& P, const Dn (&R)[NJP][2][2], int j, int k, int al, int be) {
+  Dn g = dn(0.0);
 #pragma unroll
-  for (int k = 0; k < NI; ++k) x[k] = {vec[k], dir == k ? 1.0 : 0.0};
-  const Dn* q = x;
-  const Dn* vm = x + NQ;
-  const Dn* vp = x + 2 * NQ;
-  const Dn* Phi = x + 3 * NQ;
+  for (int sa = 0; sa < 2; ++sa)
+#pragma unroll
+    for (int sb = 0; sb < 2; ++sb) {
+      const int la = sa == 0 ? M::jparent(j) : M::jchild(j);
+      const int lb = sb == 0 ? M::jparent(k) : M::jchild(k);
+      if (la < 0 || la != lb) continue;
+      const double sg = (sa == sb) ? 1.0 : -1.0;
+      const Dn dA = al == 0 ? -R[j][sa][1] : R[j][sa][0], dB = be == 0 ? -R[k][sb][1] : R[k][sb][0];
+      Dn v = P.minv_I[la] * (dA * dB);
+      if (al == be) v = v + dn(P.minv_m[la]);
+      g = g + sg * v;
+    }
+  return g;
+}
+
+template <class M>
+__device__ __forceinline__ void node_impulse(const KParams& P, const NodeIn& x, double* val, double* jcol,
+                                             int jstride) {
+  constexpr int NL = M::NL, NJ = M::NJ, NC = M::NC, NQ = 3 * NL;
+  const NodeView q{x, 0}, vm{x, NQ}, vp{x, 2 * NQ}, Phi{x, 3 * NQ};
   Dn w[NQ];
 #pragma unroll
   for (int k = 0; k < NQ; ++k) w[k] = dn(0.0);
@@ -185,32 +236,25 @@ __device__ void node_impulse(const KParams& P, const double* vec, int dir, doubl
         R[j][sa][0] = ax * cth[l] - az * sth[l];
         R[j][sa][1] = ax * sth[l] + az * cth[l];
       }
-    Dn G[NJ2][NJ2];
+    // Gram matrix G = J M^-1 J^T, packed lower triangle in joint order (values; the
+    // tangent along this thread's direction, nonzero for link angles only, is
+    // recomputed where the solve needs it)
+    constexpr int NPK = NJ2 * (NJ2 + 1) / 2;
+    constexpr JointFill<M> F{};
+    double Lv[NPK];
 #pragma unroll
-    for (int a = 0; a < NJ2; ++a)
-#pragma unroll
-      for (int bb = 0; bb < NJ2; ++bb) G[a][bb] = dn(0.0);
+    for (int e = 0; e < NPK; ++e) Lv[e] = 0.0;  // fill entries start at 0
+    auto gram = [&](int j, int k, int al, int be) -> Dn { return gram_entry<M>(P, R, j, k, al, be); };
 #pragma unroll
     for (int j = 0; j < NJ; ++j)
 #pragma unroll
       for (int k = 0; k <= j; ++k)
 #pragma unroll
-        for (int sa = 0; sa < 2; ++sa)
+        for (int al = 0; al < 2; ++al)
 #pragma unroll
-          for (int sb = 0; sb < 2; ++sb) {
-            const int la = sa == 0 ? M::jparent(j) : M::jchild(j);
-            const int lb = sb == 0 ? M::jparent(k) : M::jchild(k);
-            if (la < 0 || la != lb) continue;
-            const double sg = (sa == sb) ? 1.0 : -1.0;
-            const Dn dA[2] = {-R[j][sa][1], R[j][sa][0]}, dB[2] = {-R[k][sb][1], R[k][sb][0]};
-#pragma unroll
-            for (int al = 0; al < 2; ++al)
-#pragma unroll
-              for (int be = 0; be < 2; ++be) {
-                Dn v = P.minv_I[la] * (dA[al] * dB[be]);
-                if (al == be) v = v + dn(P.minv_m[la]);
-                G[2 * j + al][2 * k + be] = G[2 * j + al][2 * k + be] + sg * v;
-              }
+          for (int be = 0; be < 2; ++be) {
+            if ((j == k && be > al) || !F.g[j][k]) continue;
+            Lv[LI(2 * j + al, 2 * k + be)] = gram(j, k, al, be).v;
           }
     // rhs = J (v- + M^-1 w)
     Dn a[NQ];
@@ -220,7 +264,7 @@ __device__ void node_impulse(const KParams& P, const double* vec, int dir, doubl
       a[3 * l + 1] = vm[3 * l + 1] + P.minv_m[l] * w[3 * l + 1];
       a[3 * l + 2] = vm[3 * l + 2] + P.minv_I[l] * w[3 * l + 2];
     }
-    Dn z[NJ2];
+    double xv[NJ2], dx[NJ2];
 #pragma unroll
     for (int j = 0; j < NJ; ++j)
 #pragma unroll
@@ -234,38 +278,73 @@ __device__ void node_impulse(const KParams& P, const double* vec, int dir, doubl
           const Dn dPa = al == 0 ? -R[j][sa][1] : R[j][sa][0];
           acc = acc + sgn * (a[3 * l + al] + dPa * a[3 * l + 2]);
         }
-        z[2 * j + al] = acc;
+        xv[2 * j + al] = acc.v;
+        dx[2 * j + al] = acc.d;
       }
-    // Cholesky in dual arithmetic, solve, Phi_j = -x
-    Dn L[NJ2][NJ2];
+    // G x = rhs: dense Cholesky in joint order with the value arithmetic of the
+    // dual-number form it replaces (cito/contact_dynamics.py:117-121); the
+    // tangent reuses the factor, G dx = d(rhs) - dG x, with unfused products so
+    // directions that leave G unchanged round exactly like forward-mode duals
 #pragma unroll
     for (int cc = 0; cc < NJ2; ++cc) {
-      Dn d = G[cc][cc];
+      double d = Lv[LI(cc, cc)];
 #pragma unroll
-      for (int k = 0; k < cc; ++k) d = d - L[cc][k] * L[cc][k];
-      L[cc][cc] = dsqrt(d);
+      for (int k = 0; k < cc; ++k)
+        if (F.l[cc / 2][k / 2]) d = d - Lv[LI(cc, k)] * Lv[LI(cc, k)];
+      Lv[LI(cc, cc)] = sqrt(d);
 #pragma unroll
       for (int r = cc + 1; r < NJ2; ++r) {
-        Dn x2 = G[r][cc];
+        if (!F.l[r / 2][cc / 2]) continue;
+        double x2 = Lv[LI(r, cc)];
 #pragma unroll
-        for (int k = 0; k < cc; ++k) x2 = x2 - L[r][k] * L[cc][k];
-        L[r][cc] = x2 / L[cc][cc];
+        for (int k = 0; k < cc; ++k)
+          if (F.l[r / 2][k / 2] && F.l[cc / 2][k / 2]) x2 = x2 - Lv[LI(r, k)] * Lv[LI(cc, k)];
+        Lv[LI(r, cc)] = x2 / Lv[LI(cc, cc)];
       }
     }
 #pragma unroll
     for (int r = 0; r < NJ2; ++r) {
-      Dn x2 = z[r];
+      double x2 = xv[r];
 #pragma unroll
-      for (int k = 0; k < r; ++k) x2 = x2 - L[r][k] * z[k];
-      z[r] = x2 / L[r][r];
+      for (int k = 0; k < r; ++k)
+        if (F.l[r / 2][k / 2]) x2 = x2 - Lv[LI(r, k)] * xv[k];
+      xv[r] = x2 / Lv[LI(r, r)];
     }
 #pragma unroll
     for (int r = NJ2 - 1; r >= 0; --r) {
-      Dn x2 = z[r];
+      double x2 = xv[r];
 #pragma unroll
-      for (int k = r + 1; k < NJ2; ++k) x2 = x2 - L[k][r] * z[k];
-      z[r] = x2 / L[r][r];
+      for (int k = r + 1; k < NJ2; ++k)
+        if (F.l[k / 2][r / 2]) x2 = x2 - Lv[LI(k, r)] * xv[k];
+      xv[r] = x2 / Lv[LI(r, r)];
     }
+#pragma unroll
+    for (int r = 0; r < NJ2; ++r)
+#pragma unroll
+      for (int c = 0; c < NJ2; ++c)
+        if (F.g[r / 2][c / 2]) {
+          const Dn g = r >= c ? gram(r / 2, c / 2, r % 2, c % 2) : gram(c / 2, r / 2, c % 2, r % 2);
+          dx[r] = __dsub_rn(dx[r], __dmul_rn(g.d, xv[c]));
+        }
+#pragma unroll
+    for (int r = 0; r < NJ2; ++r) {
+      double x2 = dx[r];
+#pragma unroll
+      for (int k = 0; k < r; ++k)
+        if (F.l[r / 2][k / 2]) x2 = __dsub_rn(x2, __dmul_rn(Lv[LI(r, k)], dx[k]));
+      dx[r] = x2 / Lv[LI(r, r)];
+    }
+#pragma unroll
+    for (int r = NJ2 - 1; r >= 0; --r) {
+      double x2 = dx[r];
+#pragma unroll
+      for (int k = r + 1; k < NJ2; ++k)
+        if (F.l[k / 2][r / 2]) x2 = __dsub_rn(x2, __dmul_rn(Lv[LI(k, r)], dx[k]));
+      dx[r] = x2 / Lv[LI(r, r)];
+    }
+    Dn z[NJ2];
+#pragma unroll
+    for (int r = 0; r < NJ2; ++r) z[r] = {xv[r], dx[r]};
     // v+ = v- + M^-1 (w + J^T Phi_j)
 #pragma unroll
     for (int j = 0; j < NJ; ++j)
@@ -314,42 +393,33 @@ __global__ void __launch_bounds__(64) k_node(const KParams P, int64_t Np, int64_
     constexpr int NY2 = Pos<2 * NY>::v;
     const int64_t k = t / NY2;
     const int d = (int)(t % NY2);
-    double buf[NY2];
-    const double* yp = y_pairs + k * 2 * NY;
+    const double* ya = y_pairs + k * 2 * NY;
+    const double* yb = ya + NY;
     if (zs.z) {  // [y+_k, y-_{k+1}] straight from z (Transcription._node_inputs, ocp.py:316-318)
       const double* zb = zs.z + (k / zs.n_int) * zs.zstride;
       const int64_t kk = k % zs.n_int;
-#pragma unroll
-      for (int i = 0; i < NY; ++i) {
-        buf[i] = zb[(2 * kk + 1) * NXT + 2 * NQ + i];
-        buf[NY + i] = zb[(2 * kk + 2) * NXT + 2 * NQ + i];
-      }
-      yp = buf;
+      ya = zb + (2 * kk + 1) * NXT + 2 * NQ;
+      yb = zb + (2 * kk + 2) * NXT + 2 * NQ;
     }
-    node_psi<M>(P, yp, d, delta, eps, d == 0 ? psi + k * NPSI : nullptr, psi_jac + k * NPSI * 2 * NY + d, 2 * NY);
+    node_psi<M>(P, ya, yb, d, delta, eps, d == 0 ? psi + k * NPSI : nullptr, psi_jac + k * NPSI * 2 * NY + d, 2 * NY);
   } else if (t < n_psi + n_th + n_imp) {
     const bool is_th = t < n_psi + n_th;
     const int64_t e = is_th ? t - n_psi : t - n_psi - n_th;
     const int64_t k = is_th ? e / NV : e / NI;
     const int d = is_th ? (int)(e % NV) : (int)(e % NI);
-    double buf[NV];
-    const double* vec = theta_vecs + k * NV;
+    NodeIn x{theta_vecs + k * NV, theta_vecs + k * NV + 2 * NQ, theta_vecs + k * NV + 3 * NQ, 2 * NQ, 3 * NQ, d};
     if (zs.z) {  // [q-, v-, v+, Phi, Gamma] of node k straight from z (ocp.py:319-333)
       const double* zb = zs.z + (k / zs.n_node) * zs.zstride;
       const int64_t kk = k % zs.n_node;
-#pragma unroll
-      for (int i = 0; i < 2 * NQ; ++i) buf[i] = zb[2 * kk * NXT + i];
-#pragma unroll
-      for (int i = 0; i < NQ; ++i) buf[2 * NQ + i] = zb[(2 * kk + 1) * NXT + NQ + i];
-#pragma unroll
-      for (int i = 0; i < 3 * NC; ++i) buf[3 * NQ + i] = zb[zs.base_p + 3 * NC * kk + i];
-      vec = buf;
+      x.p0 = zb + 2 * kk * NXT;
+      x.p1 = zb + (2 * kk + 1) * NXT + NQ;
+      x.p2 = zb + zs.base_p + 3 * NC * kk;
     }
     if (is_th) {
       if (NC > 0)
-        node_theta<M>(P, vec, d, delta, d == 0 ? th + k * 6 * NC : nullptr, th_jac + k * 6 * NC * NV + d, NV);
+        node_theta<M>(P, x, delta, d == 0 ? th + k * 6 * NC : nullptr, th_jac + k * 6 * NC * NV + d, NV);
     } else {
-      node_impulse<M>(P, vec, d, d == 0 ? imp + k * NQ : nullptr, imp_jac + k * NQ * NI + d, NI);
+      node_impulse<M>(P, x, d == 0 ? imp + k * NQ : nullptr, imp_jac + k * NQ * NI + d, NI);
     }
   }
 }
