@@ -281,10 +281,11 @@ __device__ __forceinline__ void node_impulse(const KParams& P, const NodeIn& x, 
         xv[2 * j + al] = acc.v;
         dx[2 * j + al] = acc.d;
       }
-    // G x = rhs: dense Cholesky in joint order with the value arithmetic of the
-    // dual-number form it replaces (cito/contact_dynamics.py:117-121); the
-    // tangent reuses the factor, G dx = d(rhs) - dG x, with unfused products so
-    // directions that leave G unchanged round exactly like forward-mode duals
+    // G x = rhs: Cholesky in joint order (the elimination order decides which
+    // mathematically-zero Jacobian entries come out as exact zeros, and joint
+    // order reproduces the reference's pattern; cito/contact_dynamics.py:117-121),
+    // reciprocal pivots; the tangent reuses the factor: G dx = d(rhs) - dG x
+    double Li[NJ2];
 #pragma unroll
     for (int cc = 0; cc < NJ2; ++cc) {
       double d = Lv[LI(cc, cc)];
@@ -292,6 +293,7 @@ __device__ __forceinline__ void node_impulse(const KParams& P, const NodeIn& x, 
       for (int k = 0; k < cc; ++k)
         if (F.l[cc / 2][k / 2]) d = d - Lv[LI(cc, k)] * Lv[LI(cc, k)];
       Lv[LI(cc, cc)] = sqrt(d);
+      Li[cc] = 1.0 / Lv[LI(cc, cc)];
 #pragma unroll
       for (int r = cc + 1; r < NJ2; ++r) {
         if (!F.l[r / 2][cc / 2]) continue;
@@ -299,7 +301,7 @@ __device__ __forceinline__ void node_impulse(const KParams& P, const NodeIn& x, 
 #pragma unroll
         for (int k = 0; k < cc; ++k)
           if (F.l[r / 2][k / 2] && F.l[cc / 2][k / 2]) x2 = x2 - Lv[LI(r, k)] * Lv[LI(cc, k)];
-        Lv[LI(r, cc)] = x2 / Lv[LI(cc, cc)];
+        Lv[LI(r, cc)] = x2 * Li[cc];
       }
     }
 #pragma unroll
@@ -308,7 +310,7 @@ __device__ __forceinline__ void node_impulse(const KParams& P, const NodeIn& x, 
 #pragma unroll
       for (int k = 0; k < r; ++k)
         if (F.l[r / 2][k / 2]) x2 = x2 - Lv[LI(r, k)] * xv[k];
-      xv[r] = x2 / Lv[LI(r, r)];
+      xv[r] = x2 * Li[r];
     }
 #pragma unroll
     for (int r = NJ2 - 1; r >= 0; --r) {
@@ -316,8 +318,9 @@ __device__ __forceinline__ void node_impulse(const KParams& P, const NodeIn& x, 
 #pragma unroll
       for (int k = r + 1; k < NJ2; ++k)
         if (F.l[k / 2][r / 2]) x2 = x2 - Lv[LI(k, r)] * xv[k];
-      xv[r] = x2 / Lv[LI(r, r)];
+      xv[r] = x2 * Li[r];
     }
+    if (x.dir < NQ && x.dir % 3 == 2) {  // only link angles move G
 #pragma unroll
     for (int r = 0; r < NJ2; ++r)
 #pragma unroll
@@ -326,13 +329,14 @@ __device__ __forceinline__ void node_impulse(const KParams& P, const NodeIn& x, 
           const Dn g = r >= c ? gram(r / 2, c / 2, r % 2, c % 2) : gram(c / 2, r / 2, c % 2, r % 2);
           dx[r] = __dsub_rn(dx[r], __dmul_rn(g.d, xv[c]));
         }
+    }
 #pragma unroll
     for (int r = 0; r < NJ2; ++r) {
       double x2 = dx[r];
 #pragma unroll
       for (int k = 0; k < r; ++k)
         if (F.l[r / 2][k / 2]) x2 = __dsub_rn(x2, __dmul_rn(Lv[LI(r, k)], dx[k]));
-      dx[r] = x2 / Lv[LI(r, r)];
+      dx[r] = x2 * Li[r];
     }
 #pragma unroll
     for (int r = NJ2 - 1; r >= 0; --r) {
@@ -340,7 +344,7 @@ __device__ __forceinline__ void node_impulse(const KParams& P, const NodeIn& x, 
 #pragma unroll
       for (int k = r + 1; k < NJ2; ++k)
         if (F.l[k / 2][r / 2]) x2 = __dsub_rn(x2, __dmul_rn(Lv[LI(k, r)], dx[k]));
-      dx[r] = x2 / Lv[LI(r, r)];
+      dx[r] = x2 * Li[r];
     }
     Dn z[NJ2];
 #pragma unroll
