@@ -507,15 +507,25 @@ static cito_status linearize_all_impl(cito_handle* h, int32_t N, int32_t n_probl
     CUDA_TRY(cudaEventCreateWithFlags(&h->ev_out, cudaEventDisableTiming));
   }
   const ZSrc zs{z, base_u, base_p, defects, zstride, N - 1, N, d_delta_eps};
-  // node relations (K3) on the auxiliary stream, concurrently with the interval kernel (K1)
+  // node relations (K3) on the auxiliary stream, concurrently with the interval kernel (K1).
+  // K1 is enqueued first (CITO_K3_FIRST=1 restores the old order for A/B): its CTAs are
+  // dispatched first and K3's fill the SMs K1 leaves idle (its last partial wave)
+  static const bool k3_first = getenv("CITO_K3_FIRST") && atoi(getenv("CITO_K3_FIRST")) == 1;
   CUDA_TRY(cudaEventRecord(h->ev_in, s));
   CUDA_TRY(cudaStreamWaitEvent(h->aux, h->ev_in, 0));
-  cito_status st = h->ops->node(h->P, P * (N - 1), P * N, nullptr, nullptr, delta, epsilon, psi, psi_jac, theta,
-                                theta_jac, imp, imp_jac, h->aux, zs);
+  cito_status st;
+  if (!k3_first) {
+    st = h->ops->linearize(h->P, P * (N - 1), nullptr, nullptr, nullptr, ends, jx, ju, js, bad, s, zs);
+    if (st != CITO_OK) return st;
+  }
+  st = h->ops->node(h->P, P * (N - 1), P * N, nullptr, nullptr, delta, epsilon, psi, psi_jac, theta, theta_jac, imp,
+                    imp_jac, h->aux, zs);
   if (st != CITO_OK) return st;
   CUDA_TRY(cudaEventRecord(h->ev_out, h->aux));
-  st = h->ops->linearize(h->P, P * (N - 1), nullptr, nullptr, nullptr, ends, jx, ju, js, bad, s, zs);
-  if (st != CITO_OK) return st;
+  if (k3_first) {
+    st = h->ops->linearize(h->P, P * (N - 1), nullptr, nullptr, nullptr, ends, jx, ju, js, bad, s, zs);
+    if (st != CITO_OK) return st;
+  }
   CUDA_TRY(cudaStreamWaitEvent(s, h->ev_out, 0));
   __atomic_add_fetch(&h->launches, 2, __ATOMIC_RELAXED);
   return CITO_OK;
