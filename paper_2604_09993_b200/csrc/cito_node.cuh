@@ -377,8 +377,11 @@ __device__ __forceinline__ void node_impulse(const KParams& P, const NodeIn& x, 
   }
 }
 
+#ifndef CITO_K3_MINB
+#define CITO_K3_MINB 1
+#endif
 template <class M>
-__global__ void __launch_bounds__(64) k_node(const KParams P, int64_t Np, int64_t Nn, const double* __restrict__ y_pairs,
+__global__ void __launch_bounds__(64, CITO_K3_MINB) k_node(const KParams P, int64_t Np, int64_t Nn, const double* __restrict__ y_pairs,
                                              const double* __restrict__ theta_vecs, double delta, double eps,
                                              double* __restrict__ psi, double* __restrict__ psi_jac,
                                              double* __restrict__ th, double* __restrict__ th_jac,

@@ -109,6 +109,22 @@ def test_linearize_all_matches_reference_golden():
 
 
 @pytest.mark.gpu
+def test_linearize_all_exact_zero_pattern_equals_reference():
+    """The subproblem CSC drops exact zeros (conic.py:99-125), so every Jacobian entry
+    that is an exact zero in the reference must be one here and vice versa -- including
+    rounding residues of mathematically-zero entries (the node kernel's elimination order)."""
+    from paper_2604_09993_b200.linearize import GpuTranscription
+
+    for name in ["pointmass_rest", "monoped_n20", "halfcheetah_n30", "biped_walk"]:
+        g = load_golden(name)
+        gt = GpuTranscription(golden_scenario(name))
+        lin = gt.linearize_all(g["ig_z"], float(g["ig_delta"]))
+        for f, k in (("jx", "ig_jx"), ("ju", "ig_ju"), ("js", "ig_js"), ("psi_jac", "ig_psi_jac"),
+                     ("theta_jac", "ig_theta_jac"), ("imp_jac", "ig_imp_jac")):
+            assert np.array_equal(getattr(lin, f) == 0, g[k] == 0), (name, f)
+
+
+@pytest.mark.gpu
 def test_node_relations_random_z_vs_reference():
     import torch
 
