@@ -12,6 +12,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/cito_b200.h"
 #include "cito_kernels.cuh"
@@ -229,6 +230,8 @@ struct cito_handle {
   cudaStream_t stream = nullptr;
   cudaStream_t aux = nullptr;  // concurrent node-relation kernel of linearize_all
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  cudaStream_t cstream = nullptr;      // D2H stream of the chunked *_host pipeline
+  std::vector<cudaEvent_t> chunk_ev;  // one per in-flight chunk
   int64_t launches = 0;
 };
 
@@ -350,6 +353,8 @@ cito_status cito_destroy(cito_handle* h) {
   if (h->aux) cudaStreamDestroy(h->aux);
   if (h->ev_in) cudaEventDestroy(h->ev_in);
   if (h->ev_out) cudaEventDestroy(h->ev_out);
+  if (h->cstream) cudaStreamDestroy(h->cstream);
+  for (cudaEvent_t e : h->chunk_ev) cudaEventDestroy(e);
   delete h;
   return CITO_OK;
 }
@@ -449,15 +454,49 @@ cito_status cito_linearize_host(cito_handle* h, int64_t B, const double* xt0s, c
   CUDA_TRY(cudaMemcpyAsync(d_x, xt0s, B * D.n_xt * 8, cudaMemcpyHostToDevice, s));
   if (D.n_u) CUDA_TRY(cudaMemcpyAsync(d_U, Us, B * 2 * D.n_u * 8, cudaMemcpyHostToDevice, s));
   CUDA_TRY(cudaMemcpyAsync(d_S, Ss, B * 8, cudaMemcpyHostToDevice, s));
-  st = h->ops->linearize(h->P, B, d_x, d_U, d_S, d_e, d_jx, d_ju, d_js, d_bad, s, ZSrc{});
-  if (st != CITO_OK) return st;
-  h->launches++;
-  CUDA_TRY(cudaMemcpyAsync(ends, d_e, B * D.n_xt * 8, cudaMemcpyDeviceToHost, s));
-  CUDA_TRY(cudaMemcpyAsync(jx, d_jx, B * D.n_xt * D.n_xt * 8, cudaMemcpyDeviceToHost, s));
-  if (D.n_u) CUDA_TRY(cudaMemcpyAsync(ju, d_ju, B * D.n_xt * 2 * D.n_u * 8, cudaMemcpyDeviceToHost, s));
-  CUDA_TRY(cudaMemcpyAsync(js, d_js, B * D.n_xt * 8, cudaMemcpyDeviceToHost, s));
+  // Large batches run as a pipeline of one-wave chunks (3 intervals per CTA x #SMs, the
+  // last chunk takes the remainder): all chunk launches are queued on `s` first, then
+  // each chunk's results are copied back on `cstream` as soon as its kernel is done, so
+  // the D2H of chunk c overlaps the kernels of chunks c+1.. (with pageable destinations
+  // the copy calls block the host, which is why the launches are issued before them).
+  // CITO_HOST_CHUNKS=0 disables the pipeline (A/B).
+  static const bool chunked = !(getenv("CITO_HOST_CHUNKS") && atoi(getenv("CITO_HOST_CHUNKS")) == 0);
+  int dev = 0, sms = 148;
+  CUDA_TRY(cudaGetDevice(&dev));
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t wave = 3 * (int64_t)sms;
+  const int64_t chunk = (chunked && B >= 4 * wave) ? wave : B;
+  const int64_t nch = B / chunk;
+  const int64_t nx = D.n_xt, nu2 = 2 * D.n_u;
+  if (nch > 1) {
+    if (!h->cstream) CUDA_TRY(cudaStreamCreateWithFlags(&h->cstream, cudaStreamNonBlocking));
+    while ((int64_t)h->chunk_ev.size() < nch) {
+      cudaEvent_t e;
+      CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      h->chunk_ev.push_back(e);
+    }
+  }
+  for (int64_t c = 0; c < nch; ++c) {
+    const int64_t b0 = c * chunk, nb = (c == nch - 1) ? B - b0 : chunk;
+    st = h->ops->linearize(h->P, nb, d_x + b0 * nx, d_U + b0 * nu2, d_S + b0, d_e + b0 * nx, d_jx + b0 * nx * nx,
+                           d_ju + b0 * nx * nu2, d_js + b0 * nx, d_bad + b0, s, ZSrc{});
+    if (st != CITO_OK) return st;
+    h->launches++;
+    if (nch > 1) CUDA_TRY(cudaEventRecord(h->chunk_ev[c], s));
+  }
+  cudaStream_t cs = nch > 1 ? h->cstream : s;
   int32_t* hb = bad;
-  if (hb) CUDA_TRY(cudaMemcpyAsync(hb, d_bad, B * 4, cudaMemcpyDeviceToHost, s));
+  for (int64_t c = 0; c < nch; ++c) {
+    const int64_t b0 = c * chunk, nb = (c == nch - 1) ? B - b0 : chunk;
+    if (nch > 1) CUDA_TRY(cudaStreamWaitEvent(cs, h->chunk_ev[c], 0));
+    CUDA_TRY(cudaMemcpyAsync(ends + b0 * nx, d_e + b0 * nx, nb * nx * 8, cudaMemcpyDeviceToHost, cs));
+    CUDA_TRY(cudaMemcpyAsync(jx + b0 * nx * nx, d_jx + b0 * nx * nx, nb * nx * nx * 8, cudaMemcpyDeviceToHost, cs));
+    if (D.n_u)
+      CUDA_TRY(cudaMemcpyAsync(ju + b0 * nx * nu2, d_ju + b0 * nx * nu2, nb * nx * nu2 * 8, cudaMemcpyDeviceToHost, cs));
+    CUDA_TRY(cudaMemcpyAsync(js + b0 * nx, d_js + b0 * nx, nb * nx * 8, cudaMemcpyDeviceToHost, cs));
+    if (hb) CUDA_TRY(cudaMemcpyAsync(hb + b0, d_bad + b0, nb * 4, cudaMemcpyDeviceToHost, cs));
+  }
+  CUDA_TRY(cudaStreamSynchronize(cs));
   CUDA_TRY(cudaStreamSynchronize(s));
   return count_bad(hb, B);
 }

@@ -119,14 +119,26 @@ class Discretizer:
         _lib.check(st, "propagate_batch")
         return ends
 
-    def linearize_batch(self, xt0s, Us, Ss):
-        """End states and Jacobians (d/dstate, d/dU, d/dS) (augmentation.py:236-242)."""
+    def linearize_batch(self, xt0s, Us, Ss, out=None):
+        """End states and Jacobians (d/dstate, d/dU, d/dS) (augmentation.py:236-242).
+
+        ``out`` (extension, not in the reference signature): caller-owned
+        C-contiguous float64 arrays (ends (B, n_xt), jx (B, n_xt, n_xt),
+        ju (B, n_xt, 2 n_u), js (B, n_xt)) to write into -- e.g. page-locked
+        buffers reused across calls, which lets the chunked device->host
+        pipeline of ``cito_linearize_host`` run fully asynchronously."""
         xt0s, Us, Ss, B = self._batch(xt0s, Us, Ss)
         n, nu2 = self.n_xt, 2 * self.n_u
-        ends = np.empty((B, n))
-        jx = np.empty((B, n, n))
-        ju = np.empty((B, n, nu2))
-        js = np.empty((B, n))
+        if out is None:
+            ends = np.empty((B, n))
+            jx = np.empty((B, n, n))
+            ju = np.empty((B, n, nu2))
+            js = np.empty((B, n))
+        else:
+            ends, jx, ju, js = out
+            for a, shp in ((ends, (B, n)), (jx, (B, n, n)), (ju, (B, n, nu2)), (js, (B, n))):
+                if a.shape != shp or a.dtype != np.float64 or not a.flags.c_contiguous:
+                    raise ValueError(f"out array must be C-contiguous float64 of shape {shp}")
         bad = np.zeros(B, dtype=np.int32)
         if B == 0:
             return ends, jx, ju, js

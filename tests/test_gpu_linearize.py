@@ -148,6 +148,36 @@ def test_device_path_matches_host_path():
     assert disc.launch_count() >= 2
 
 
+def test_chunked_host_pipeline_matches_device_path():
+    """Batches of >= 4 waves go through the chunked D2H pipeline of cito_linearize_host
+    (one-wave chunks, the last one taking the remainder): same bits as one device launch,
+    into fresh arrays and into caller-owned (page-locked) out= buffers."""
+    import torch
+
+    from paper_2604_09993_b200 import synth
+
+    sc = golden_scenario("halfcheetah_n30")
+    disc = _disc(sc)
+    n_sm = torch.cuda.get_device_properties(0).multi_processor_count
+    B = 4 * 3 * n_sm + 37
+    xt0, U, S = synth.random_intervals(sc, B, seed=5)
+    n0 = disc.launch_count()
+    host = disc.linearize_batch(xt0, U, S)
+    assert disc.launch_count() - n0 == 4  # four chunks
+    dev = torch.device("cuda")
+    out = disc.linearize_batch_device(torch.as_tensor(xt0, device=dev), torch.as_tensor(U, device=dev),
+                                      torch.as_tensor(S, device=dev))
+    torch.cuda.synchronize()
+    for a, b in zip(host, out[:4]):
+        assert np.array_equal(a, b.cpu().numpy())
+    pinned = tuple(torch.empty(a.shape, dtype=torch.float64, pin_memory=True).numpy() for a in host)
+    res = disc.linearize_batch(xt0, U, S, out=pinned)
+    for a, b, r in zip(host, pinned, res):
+        assert r is b and np.array_equal(a, b)
+    with pytest.raises(ValueError):
+        disc.linearize_batch(xt0, U, S, out=(pinned[0], pinned[1], pinned[2], pinned[3][:-1]))
+
+
 @pytest.mark.parametrize("substeps,B", [(1, 40), (8, 199), (10, 64), (8, 600)])
 def test_linearize_substeps_vs_oracle(substeps, B):
     """Other substep counts (configs[4]: 8 substeps, N=200 -> 199 intervals) on both K1
