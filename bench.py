@@ -467,14 +467,12 @@ def run_ours(args):
         d2h = scp_api.d2h_bytes()  # packed D2H per step: fixed fields + the CSC arrays up to their caps
     elif args.workload == "multistart":
         Z_pin = torch.as_tensor(Z).pin_memory()
-        ms_host = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in ms_out.items()}
+        ms_host = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True).numpy() for k, v in ms_out.items()}
 
         def e2e_step():
-            zd = Z_pin.to(dev, non_blocking=True)
-            o = gt50.linearize_device(zd, 1.0, out=ms_out)
-            for k, v in o.items():
-                ms_host[k].copy_(v, non_blocking=True)
-            torch.cuda.current_stream(dev).synchronize()
+            # public multi-start API: host Z in, host arrays out (caller-owned page-locked
+            # buffers); chunks of ~one K1 wave, each copied back while the next computes
+            return gt50.linearize_to_host(Z_pin, 1.0, out=ms_host)
 
         e2e_step()
         h2d = Z.nbytes

@@ -172,6 +172,24 @@ class GpuTranscription:
         self._i_yp, self._i_th = t(idx_yp), t(idx_th)
         self.n_imp = 3 * n_q + 2 * lay.n_c
 
+    def _alloc_out(self, P):
+        """Device result buffers of linearize_device for P problems (problem-major)."""
+        import torch
+
+        lay = self.lay
+        N, nxt, nu, nq, nc = lay.N, lay.n_xt, lay.n_u, lay.n_q, lay.n_c
+        NI, NN = P * (N - 1), P * N
+        n_psi = 3 * nc + lay.n_g_out
+        f64 = dict(dtype=torch.float64, device=self.device)
+        out = dict(ends=torch.empty((NI, nxt), **f64), jx=torch.empty((NI, nxt, nxt), **f64),
+                   ju=torch.empty((NI, nxt, 2 * nu), **f64), js=torch.empty((NI, nxt), **f64),
+                   defects=torch.empty((NI, nxt), **f64),
+                   bad=torch.empty((NI,), dtype=torch.int32, device=self.device),
+                   psi=torch.empty((NI, n_psi), **f64), psi_jac=torch.empty((NI, n_psi, 2 * lay.n_y), **f64),
+                   theta=torch.empty((NN, 6 * nc), **f64), theta_jac=torch.empty((NN, 6 * nc, 3 * nq + 3 * nc), **f64),
+                   imp_v=torch.empty((NN, nq), **f64), imp_jac=torch.empty((NN, nq, 3 * nq + 2 * nc), **f64))
+        return out
+
     def linearize_device(self, z_dev, delta, epsilon=None, k1_events=None, out=None):
         """Everything on the device in one C-ABI call (cito_linearize_all_dev): the
         interval kernel and the node-relation kernel read z directly and run
@@ -187,18 +205,9 @@ class GpuTranscription:
         P = 1 if z_dev.dim() == 1 else z_dev.shape[0]
         if z_dev.shape[-1] != lay.dim or not z_dev.is_contiguous():
             raise ValueError(f"z must be contiguous with last dimension {lay.dim}")
-        N, nxt, nu, nq, nc = lay.N, lay.n_xt, lay.n_u, lay.n_q, lay.n_c
-        NI, NN = P * (N - 1), P * N
-        n_psi = 3 * nc + lay.n_g_out
+        N = lay.N
         if out is None:
-            f64 = dict(dtype=torch.float64, device=self.device)
-            out = dict(ends=torch.empty((NI, nxt), **f64), jx=torch.empty((NI, nxt, nxt), **f64),
-                       ju=torch.empty((NI, nxt, 2 * nu), **f64), js=torch.empty((NI, nxt), **f64),
-                       defects=torch.empty((NI, nxt), **f64),
-                       bad=torch.empty((NI,), dtype=torch.int32, device=self.device),
-                       psi=torch.empty((NI, n_psi), **f64), psi_jac=torch.empty((NI, n_psi, 2 * lay.n_y), **f64),
-                       theta=torch.empty((NN, 6 * nc), **f64), theta_jac=torch.empty((NN, 6 * nc, 3 * nq + 3 * nc), **f64),
-                       imp_v=torch.empty((NN, nq), **f64), imp_jac=torch.empty((NN, nq, 3 * nq + 2 * nc), **f64))
+            out = self._alloc_out(P)
         stream = torch.cuda.current_stream(self.device)
         if k1_events is not None:
             k1_events[0].record(stream)
@@ -211,6 +220,59 @@ class GpuTranscription:
             stream.cuda_stream), "linearize_all")
         if k1_events is not None:
             k1_events[1].record(stream)
+        return out
+
+    def linearize_to_host(self, Z, delta, epsilon=None, out=None):
+        """Multi-start linearization with host arrays in and out (the configs[3] path):
+        ``Z`` (P, dim) decision vectors, one per start; returns a dict of numpy arrays
+        stacked problem-major like ``linearize_device`` (written into ``out``, a dict of
+        caller-owned -- e.g. page-locked -- arrays, when given).  The problems run as
+        chunks of about one wave of the interval kernel (3 intervals per CTA x #SMs;
+        the last chunk takes the remainder), each chunk's results copied back on a
+        side stream while the next chunks compute.  Raises FloatingPointError like
+        linearize_all (scp.py:116-118) for non-finite end states."""
+        import torch
+
+        Zt = Z if torch.is_tensor(Z) else torch.from_numpy(np.ascontiguousarray(np.asarray(Z, dtype=np.float64)))
+        if Zt.dim() == 1:
+            Zt = Zt[None]
+        P, N = Zt.shape[0], self.lay.N
+        dev = self.device
+        z_dev = Zt.to(dev, non_blocking=True)
+        if getattr(self, "_host_plan", (None,))[0] != P:
+            self._host_plan = (P, self._alloc_out(P))  # device result buffers
+        dbuf = self._host_plan[1]
+        if out is None:
+            out = {k: np.empty(tuple(v.shape), dtype=np.int32 if v.dtype == torch.int32 else np.float64)
+                   for k, v in dbuf.items()}
+        hout = {k: torch.from_numpy(v) for k, v in out.items()}
+        n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+        per = max(1, (3 * n_sm) // (N - 1))
+        nch = max(1, P // per)
+        stream = torch.cuda.current_stream(dev)
+        if not hasattr(self, "_copy_stream"):
+            self._copy_stream = torch.cuda.Stream(dev)
+        cs = self._copy_stream
+
+        def rows(v, p0, p1):  # interval arrays have N-1 rows per problem, node arrays N
+            per_p = N - 1 if v.shape[0] == P * (N - 1) else N
+            return slice(p0 * per_p, p1 * per_p)
+
+        chunks = []
+        for c in range(nch):  # all launches first: pageable destinations make the copies block the host
+            p0, p1 = c * per, (P if c == nch - 1 else (c + 1) * per)
+            self.linearize_device(z_dev[p0:p1], delta, epsilon, out={k: v[rows(v, p0, p1)] for k, v in dbuf.items()})
+            ev = torch.cuda.Event()
+            ev.record(stream)
+            chunks.append((p0, p1, ev))
+        for p0, p1, ev in chunks:
+            cs.wait_event(ev)
+            with torch.cuda.stream(cs):
+                for k, v in dbuf.items():
+                    hout[k][rows(v, p0, p1)].copy_(v[rows(v, p0, p1)], non_blocking=True)
+        cs.synchronize()
+        if out["bad"].any():
+            raise FloatingPointError(f"non-finite state in intervals {np.where(out['bad'] != 0)[0].tolist()}")
         return out
 
     def linearize_all(self, z, delta, epsilon=None, jobs=1):

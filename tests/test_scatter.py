@@ -162,6 +162,32 @@ def test_multistart_batch_equals_single_problems():
 
 
 @pytest.mark.gpu
+def test_linearize_to_host_chunked_equals_device():
+    """GpuTranscription.linearize_to_host (multi-start, host arrays, chunked D2H pipeline)
+    == one linearize_device call over all problems; fresh and caller-owned outputs."""
+    import torch
+
+    from paper_2604_09993_b200.linearize import GpuTranscription, initial_guess_batch
+
+    sc = golden_scenario("halfcheetah_n30")
+    gt = GpuTranscription(sc)
+    per = (3 * torch.cuda.get_device_properties(0).multi_processor_count) // (gt.lay.N - 1)
+    P = 2 * per + 3  # two chunks, the last one taking the remainder
+    Z = initial_guess_batch(sc, gt.disc, list(range(P)), gt.lay)
+    ref = {k: v.cpu().numpy() for k, v in gt.linearize_device(torch.as_tensor(Z, device=gt.device), 0.5).items()}
+    got = gt.linearize_to_host(Z, 0.5)
+    pinned = {k: torch.empty(v.shape, dtype=torch.int32 if v.dtype == np.int32 else torch.float64,
+                             pin_memory=True).numpy() for k, v in ref.items()}
+    got2 = gt.linearize_to_host(torch.as_tensor(Z).pin_memory(), 0.5, out=pinned)
+    assert got2 is pinned
+    for k, v in ref.items():
+        assert np.array_equal(got[k], v) and np.array_equal(pinned[k], v), k
+    Z[P - 1, :] = np.nan
+    with pytest.raises(FloatingPointError):
+        gt.linearize_to_host(Z, 0.5)
+
+
+@pytest.mark.gpu
 def test_initial_guess_matches_reference_and_batch():
     """GPU initial guess == the reference's initial_guess (golden ig_z); the
     multi-start batched version == one call per seed."""
