@@ -204,7 +204,9 @@ cito_status cito_scatter_dynamics_dev(cito_handle* h, int64_t n_int, const doubl
  * (sp_val * lin[sp_src][sp_idx]) * sigma[col].  Exact zeros are dropped and the
  * rest compacted: out_ptr[ncols+1] (int32), out_rows/out_vals[<= superset nnz].
  * lin: HOST array of 10 device pointers {jx, ju, js, imp_jac, theta_jac,
- * psi_jac, ends, imp_v, theta, psi}; counts: device workspace [ncols]. */
+ * psi_jac, ends, imp_v, theta, psi}; counts: device int32 workspace
+ * [ncols + 64], ZEROED before the first call and kept between calls (the one-pass
+ * compaction stores its per-block totals and launch epoch there). */
 cito_status cito_csc_assemble_dev(int32_t ncols, const int64_t* sp_ptr, const int32_t* sp_row, const int8_t* sp_src,
                                   const int64_t* sp_idx, const double* sp_val, const double* sigma,
                                   const double* const* lin, int32_t* counts, int32_t* out_ptr, int32_t* out_rows,

@@ -653,10 +653,17 @@ cito_status cito_csc_assemble2_dev(int32_t nmat, int32_t ncols, const int64_t* c
   }
   (void)gx;
   const unsigned nb = (unsigned)((ncols + CSC_CPB - 1) / CSC_CPB);
-  count_launch(2);
-  k_csc_blocksum<<<dim3(nb, nmat), 256, 0, s>>>(ncols, ca, sigma, L);
-  CUDA_TRY(cudaGetLastError());
-  k_csc_write2<<<dim3(nb, nmat), 256, 0, s>>>(ncols, ca, sigma, L);
+  static const bool two = getenv("CITO_CSC2") != nullptr;  // A/B: block totals + write (two launches)
+  if (two) {
+    count_launch(2);
+    k_csc_blocksum<<<dim3(nb, nmat), 256, 0, s>>>(ncols, ca, sigma, L);
+    CUDA_TRY(cudaGetLastError());
+    k_csc_write2<<<dim3(nb, nmat), 256, 0, s>>>(ncols, ca, sigma, L);
+    CUDA_TRY(cudaGetLastError());
+    return CITO_OK;
+  }
+  count_launch(1);
+  k_csc_onepass<<<dim3(nb, nmat), 256, 0, s>>>(ncols, ca, sigma, L);
   CUDA_TRY(cudaGetLastError());
   return CITO_OK;
 }

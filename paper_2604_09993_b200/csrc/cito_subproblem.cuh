@@ -237,6 +237,114 @@ __global__ void __launch_bounds__(256) k_csc_write2(int32_t ncols, const CscArgs
   }
 }
 
+// One-pass CSC compaction (default): each column block counts its exact nonzeros,
+// publishes the total tagged with this launch's epoch, then sums the totals of
+// the preceding blocks (decoupled look-back: a block only waits on lower-index
+// blocks, which are dispatched before it), scans its columns and writes.  The
+// counts workspace of matrix m holds the tagged totals as uint64 per block; the
+// launch epoch and a finished-block counter live after them in counts[0] (the
+// last block to finish advances the epoch, so the next launch -- e.g. the next
+// CUDA-graph replay -- uses a fresh tag without any reset).
+__global__ void __launch_bounds__(256) k_csc_onepass(int32_t ncols, const CscArgs a, const double* __restrict__ sigma,
+                                                     const LinTable L) {
+  const int m = blockIdx.y;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t* __restrict__ sp_ptr = a.sp_ptr[m];
+  const int nb = gridDim.x;
+  const int64_t c0 = (int64_t)blockIdx.x * CSC_CPB;
+  unsigned long long* flags = reinterpret_cast<unsigned long long*>(a.counts[m]);
+  unsigned* sync = reinterpret_cast<unsigned*>(a.counts[0]) + 2 * nb;  // [epoch, finished blocks]
+  __shared__ int32_t red[8];
+  __shared__ int32_t ccount[CSC_CPB];
+  __shared__ int32_t cbase[CSC_CPB];
+  __shared__ unsigned tag_s;
+  if (tid == 0) tag_s = *((volatile unsigned*)sync) + 1u;
+  // per-column nonzero counts of this block
+  for (int k = warp; k < CSC_CPB; k += 8) {
+    const int64_t c = c0 + k;
+    int n = 0;
+    if (c < ncols) {
+      const double sig = sigma[c];
+      for (int64_t e = sp_ptr[c] + lane; e < sp_ptr[c + 1]; e += 32)
+        n += sp_value(e, sig, a.src[m], a.idx[m], a.val[m], L) != 0.0;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+    if (lane == 0) ccount[k] = n;
+  }
+  __syncthreads();
+  const unsigned tag = tag_s;
+  if (warp == 0) {  // publish this block's total
+    int t = ccount[lane];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane == 0) atomicExch(&flags[blockIdx.x], ((unsigned long long)tag << 32) | (unsigned)t);
+  }
+  // prefix over the preceding column blocks (spin until each is published with this tag)
+  int pre = 0;
+  for (int j = tid; j < (int)blockIdx.x; j += blockDim.x) {
+    unsigned long long f;
+    do {
+      f = *((volatile unsigned long long*)&flags[j]);
+    } while ((unsigned)(f >> 32) != tag);
+    pre += (int)(unsigned)(f & 0xffffffffull);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
+  if (lane == 0) red[warp] = pre;
+  __syncthreads();
+  if (warp == 0) {  // exclusive scan of the block's column counts (CSC_CPB == 32: one per lane)
+    int blockpre = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) blockpre += red[w];
+    const int v = ccount[lane];
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const int base = blockpre + incl - v;
+    cbase[lane] = base;
+    const int64_t c = c0 + lane;
+    if (c < ncols) a.out_ptr[m][c] = base;
+    if (c == ncols - 1) a.out_ptr[m][ncols] = base + v;
+  }
+  __syncthreads();
+  const unsigned lt = (1u << lane) - 1u;
+  for (int k = warp; k < CSC_CPB; k += 8) {
+    const int64_t c = c0 + k;
+    if (c >= ncols) break;
+    const double sig = sigma[c];
+    int32_t base = cbase[k];
+    for (int64_t e0 = sp_ptr[c]; e0 < sp_ptr[c + 1]; e0 += 32) {
+      const int64_t e = e0 + lane;
+      const bool in = e < sp_ptr[c + 1];
+      const double v = in ? sp_value(e, sig, a.src[m], a.idx[m], a.val[m], L) : 0.0;
+      const bool nz = in && v != 0.0;
+      const unsigned msk = __ballot_sync(0xffffffffu, nz);
+      if (nz) {
+        const int32_t pos = base + __popc(msk & lt);
+        const int32_t r = a.row[m][e];
+        a.out_rows[m][pos] = r;
+        a.out_vals[m][pos] = v;
+        if (a.rowmax[m]) atomicMax(&a.rowmax[m][r], (unsigned long long)__double_as_longlong(fabs(v)));
+      }
+      base += __popc(msk);
+    }
+  }
+  // the last block of the launch advances the epoch (every block has read it by then)
+  if (tid == 0) {
+    __threadfence();
+    const unsigned done = atomicAdd(&sync[1], 1u);
+    if (done == (unsigned)(nb * gridDim.y) - 1u) {
+      sync[1] = 0u;
+      __threadfence();
+      atomicAdd(&sync[0], 1u);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) k_rhs(int64_t nrows, const int32_t* __restrict__ rows,
                                              const int8_t* __restrict__ form, const int8_t* __restrict__ vsrc,
                                              const int64_t* __restrict__ voff, const int8_t* __restrict__ seg_src,

@@ -482,7 +482,9 @@ class SubproblemAssembler:
             d = dict(sp_ptr=t(csc["indptr"], np.int64), row=t(csc["row"], np.int32), src=t(csc["src"], np.int8),
                      idx=t(csc["idx"], np.int64), val=t(csc["val"], np.float64), nrows=csc["nrows"],
                      nsup=int(csc["row"].size), rhs_const=t(np.nan_to_num(csc["rhs"]), np.float64))
-            d["counts"] = torch.empty(pattern.n, dtype=torch.int32, device=device)
+            # block totals / per-column counts; the one-pass compaction keeps tagged block
+            # totals and its launch epoch here across calls, so it starts zeroed
+            d["counts"] = torch.zeros(pattern.n + 64, dtype=torch.int32, device=device)
             # rhs descriptors of the linearized rows
             nr = len(rows)
             r_row = np.array([r[0] for r in rows], dtype=np.int32)

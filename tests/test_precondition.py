@@ -234,7 +234,7 @@ def test_gpu_scp_step_graph_replay_equals_eager():
             assert np.array_equal(a.data, b.data)
         assert np.array_equal(pg.b, pe.b) and np.array_equal(pg.h, pe.h) and np.array_equal(pg.c, pe.c)
         assert np.array_equal(rg[0].psi, re_[0].psi) and np.array_equal(rg[0].theta_jac, re_[0].theta_jac)
-    assert sg._plan["graph_kernels"][False] >= 5
+    assert sg._plan["graph_kernels"][False] >= 4  # K1, K3, one-pass CSC compaction, rhs
     assert {k for hb in sg._plan["hosts"] for k in hb.graphs} == {False, True}
 
 
