@@ -171,3 +171,22 @@ def test_gpu_scp_step_all_models_match_reference(name):
             assert rel_err(mat.data, g[f"sp0_{M}_data"]) <= 1e-9, M
         assert rel_err(prog.b, g["sp0_b"]) <= 1e-9 and rel_err(prog.h, g["sp0_h"]) <= 1e-9
         assert np.array_equal(prog.c, g["sp0_c"])
+
+
+def test_csc_direct_equals_scipy_constructor():
+    """GpuSCPStep's direct csc_matrix construction (no per-call constructor checks)
+    gives the same matrix object state as scipy's constructor and a valid format."""
+    from paper_2604_09993_b200.subproblem import _csc_direct
+
+    A = sp.random(40, 70, density=0.15, format="csc", random_state=3)
+    A.sort_indices()
+    d, i, p = A.data.copy(), A.indices.astype(np.int32), A.indptr.astype(np.int32)
+    first = _csc_direct(d, i, p, A.shape)  # the probe (regular constructor)
+    fast = _csc_direct(d, i, p, A.shape)
+    assert set(vars(fast)) == set(vars(first))  # before any lazily cached attribute
+    assert fast.data is d and fast.indices is i and fast.indptr is p  # no copies
+    for m in (first, fast):
+        assert isinstance(m, sp.csc_matrix) and m.shape == A.shape
+        m.check_format(full_check=True)
+        assert (m != A).nnz == 0 and m.has_sorted_indices
+        assert np.array_equal(m.toarray(), A.toarray()) and np.allclose(m.T @ np.ones(40), A.T @ np.ones(40))
