@@ -4,31 +4,56 @@
 Metric (BASELINE.json): interval linearizations/sec (fp64), HalfCheetah N=30;
 SCP-iteration linearize ms (= ms_per_step).
 
-Workload ``scp`` (default, configs[1]): one SCP iteration's linearization of
-HalfCheetah (halfcheetah_bound.json, N=30, 5 substeps -> 29 intervals) at an
-SCP-realistic point (the scenario's initial guess; rank r uses seed r):
-gather from z -> K1 interval linearize (ends, Phi, B-, B+, dS) -> defects ->
-K3 node relations + Jacobians -> K4 scatter of the dynamics rows into CSC
-values + b.  ``batch``: configs[2], 4096 independent synthetic intervals per
-GPU (one K1 launch per step).
+Workloads (``--workload``):
+  scp (default, configs[1])  one SCP iteration's pre-IPM work for HalfCheetah
+        (halfcheetah_bound.json, N=30, 5 RKF substeps -> 29 intervals) at the
+        scenario's initial guess (rank r: seed r): K1 interval linearization +
+        defects and K3 node relations (one linearize_all call, cito/scp.py:87-135),
+        then the whole-subproblem CSC assembly with exact-zero compaction + b/h
+        (cito/scp.py:160-351 + cito/conic.py:209-269).  At N > 1 GPUs: replicas
+        (one independent problem per rank, no collective).
+  batch (configs[2])   B (default 4096) independent synthetic HalfCheetah
+        intervals, split in contiguous ranges over the ranks (strong scaling),
+        the full results gathered to rank 0's GPU with one grouped NCCL
+        send/recv inside the timed step (paper_2604_09993_b200.parallel).
+  multistart (configs[3] analogue)  P (default 1024) HalfCheetah N=50 initial
+        guesses (no quadruped exists in the reference), whole problems per rank,
+        linearize_all of each rank's problems in one call + NCCL gather of all
+        LinearizedProblem arrays to rank 0.
+  fine (configs[4])    as scp with N=200, 8 RKF substeps.
 
-  value  device-resident throughput (inputs already in HBM), CUDA events per
-         step on the launching stream, L2 flushed (256 MiB write) between steps,
+Line fields:
+  value  whole-job throughput, inputs resident in HBM: CUDA events on the
+         launching stream per step, L2 flushed (256 MiB write) between steps,
          max over ranks.
-  e2e    same step through the public API with host buffers: H2D of z (pinned)
-         + device work + D2H of every output (LinearizedProblem arrays, CSC
-         values, b) inside the timed region.
-  --impl reference   the reference algorithm on the host cores: the C oracle
-         port (oracle/cito_oracle.c; JAX, the reference's runtime, is not
-         installable here), all threads, same workload/metric.
+  e2e    the same metric through the public API with host buffers:
+         scp/fine: GpuSCPStep.iterate -- pinned H2D of [z, delta, epsilon], the
+           device step, ONE packed D2H of the assembled program (CSC arrays, b,
+           h, flags); the returned LinearizedProblem stays device-backed (lazy:
+           cito.scp.solve only hands it to build_subproblem), so its Jacobians
+           are not copied (h2d/d2h bytes per step are reported).
+         batch: Discretizer.linearize_batch (N=1) / ShardedBatch.linearize(...,
+           collect="host") (N>1): host arrays in, every Jacobian back on the host.
+         multistart: GpuTranscription.linearize_to_host / ShardedMultiStart(...,
+           collect="host"): host arrays of every LinearizedProblem field.
+  roofline  the dominant kernel (K1) timed alone with CUDA events: counted
+         algorithmic fp64 flops / time / the DFMA peak measured in this run
+         (frac), and the ncu-executed fp64 instruction flops (frac_executed).
+  cpu_baseline  the reference arm's line (``--impl reference``) run in a
+         subprocess on rank 0: the reference algorithm on the host cores
+         (oracle port for the linearization, the reference's own Python for the
+         subproblem assembly) -- "iteration" leg and "linearize_only" leg.
 
-Multi-GPU: one process per GPU (torchrun); each rank linearizes its own
-independent problem(s) (weak scaling), no data-path collective.
+``--impl reference``: the reference's CPU implementation of the same workload
+(the C oracle port, oracle/cito_oracle.c, all host threads; JAX, the reference's
+runtime, is not installable here), same config/metric/unit; N>1: rank 0 only.
+``--gpus N`` without torchrun re-launches itself under torch.distributed.run.
 """
 
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import tempfile
@@ -41,6 +66,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "interval linearizations/sec (fp64) HalfCheetah N=30; SCP-iteration linearize ms"
 UNIT = "intervals/s"
+FINE = dict(N=200, substeps=8)  # configs[4]: the reference has no RK4; its RKF at 8 substeps
 
 
 def parse():
@@ -51,12 +77,12 @@ def parse():
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--workload", choices=["scp", "fine", "batch", "multistart"], default="scp")
     p.add_argument("--no-fine-extra", action="store_true")
-    p.add_argument("--problems", type=int, default=128, help="multistart: problems per GPU (configs[3]: 1024 / 8)")
-    p.add_argument("--batch", type=int, default=4096)
+    p.add_argument("--no-batch-extra", action="store_true")
+    p.add_argument("--problems", type=int, default=1024, help="multistart: problems in total (configs[3]: 1024)")
+    p.add_argument("--batch", type=int, default=4096, help="batch: intervals in total (configs[2]: 4096)")
     p.add_argument("--cpu-seconds", type=float, default=10.0)
     p.add_argument("--sample-seconds", type=float, default=None, help="reference arm: time-bounded sample")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--no-batch-extra", action="store_true")
     return p.parse_args()
 
 
@@ -64,10 +90,40 @@ def env_rank():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
+def relaunch_under_torchrun(args):
+    """``bench.py --gpus N`` started without torchrun: run N ranks (one per GPU) the
+    way the driver does, with the same arguments."""
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd, cwd=ROOT))
+
+
+def config_for(args, world):
+    """The `config` dict of both arms (identical for the same arguments)."""
+    wl = args.workload
+    desc = {
+        "scp": "scp: one SCP-iteration linearize of HalfCheetah N=30 (halfcheetah_bound.json, 5 RKF substeps, "
+               "29 intervals; K1+K3 + whole-subproblem assembly) at the scenario's initial guess",
+        "fine": "fine: one SCP-iteration linearize of HalfCheetah N=200, 8 RKF substeps (configs[4]; 199 intervals; "
+                "K1+K3 + whole-subproblem assembly) at the scenario's initial guess",
+        "batch": f"batch: {args.batch} independent synthetic HalfCheetah intervals in total (configs[2]), "
+                 "split over the GPUs, results gathered to rank 0",
+        "multistart": f"multistart: {args.problems} HalfCheetah N=50 initial guesses in total (configs[3] "
+                      "analogue), linearize_all (K1+K3) split over the GPUs, results gathered to rank 0",
+    }[wl]
+    per = {"scp": 29, "fine": 199, "batch": args.batch, "multistart": args.problems * 49}[wl]
+    par = (f"replicas x{world} (an independent problem per rank, no collective)" if wl in ("scp", "fine")
+           else f"shards x{world} (contiguous ranges per rank; one grouped NCCL send/recv to rank 0 for result "
+                "collection)" if world > 1 else "single GPU")
+    return {"workload": desc, "intervals_per_step": per * (world if wl in ("scp", "fine") else 1),
+            "l2": "flushed (256 MiB write) between timed steps", "parallelism": par}
+
+
 # --------------------------------------------------------------------------- shared problem setup
-FINE = dict(N=200, substeps=8)  # configs[4]: HalfCheetah fine grid (the reference has no RK4: its RKF at 8 substeps)
-
-
 def scp_problem(seed, fine=False):
     from paper_2604_09993_b200 import scenario as S
 
@@ -114,76 +170,57 @@ def _reference_scp():
         return None
 
 
-def cpu_step_fn(sc, seed):
+class CpuIteration:
     """One SCP iteration's pre-IPM work on the host: the reference's linearization
     algorithm via the oracle port (intervals + node relations) and, when the
     reference is installed, its own build_subproblem + canonicalize."""
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import pyoracle
 
-    from paper_2604_09993_b200.linearize import node_inputs
-    from paper_2604_09993_b200.model import pack_model
-    from paper_2604_09993_b200.scenario import Layout
+    def __init__(self, sc):
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import pyoracle
 
-    lay = Layout(sc)
-    g, n_g = sc.path_constraints()
-    desc = pack_model(sc.model, sc.mixing_matrix(n_g), g)
-    from paper_2604_09993_b200.linearize import initial_guess
+        from paper_2604_09993_b200.linearize import initial_guess, node_inputs
+        from paper_2604_09993_b200.model import pack_model
+        from paper_2604_09993_b200.scenario import Layout
 
-    z = initial_guess(sc, _OracleDisc(sc), lay)
-    starts = np.stack([z[lay.xp(k)] for k in range(lay.N - 1)])
-    Us = np.stack([z[lay.u(k)] for k in range(lay.N - 1)])
-    Ss = np.array([z[lay.s(k)][0] for k in range(lay.N - 1)])
-    yp, tv = node_inputs(lay, z)
-    ref = _reference_scp()
-    tr = None
-    if ref is not None:
-        from dataclasses import replace
+        self.po, self.sc = pyoracle, sc
+        lay = self.lay = Layout(sc)
+        g, n_g = sc.path_constraints()
+        self.desc = pack_model(sc.model, sc.mixing_matrix(n_g), g)
+        z = self.z = initial_guess(sc, _OracleDisc(sc), lay)
+        n = lay.N - 1
+        self.starts = np.stack([z[lay.xp(k)] for k in range(n)])
+        self.Us = np.stack([z[lay.u(k)] for k in range(n)])
+        self.Ss = np.array([z[lay.s(k)][0] for k in range(n)])
+        self.yp, self.tv = node_inputs(lay, z)
+        ref = _reference_scp()
+        self.tr = None
+        if ref is not None:
+            from dataclasses import replace
 
-        ocp, scp = ref
-        rsc = ocp.load_scenario(os.path.join(ROOT, "tests", "golden", "assets", "halfcheetah_bound.json"))
-        tr = ocp.Transcription(replace(rsc, N=sc.N, s_bounds=None, substeps=sc.substeps))
-    step_fn.with_assembly = tr is not None
+            ocp, self.scp = ref
+            rsc = ocp.load_scenario(os.path.join(ROOT, "tests", "golden", "assets", "halfcheetah_bound.json"))
+            self.tr = ocp.Transcription(replace(rsc, N=sc.N, s_bounds=None, substeps=sc.substeps))
 
-    def step():
-        e, jx, ju, js, _ = pyoracle.linearize(desc, sc.substeps, starts, Us, Ss)
-        psi, pj, th, tj, imp, ij = pyoracle.node_linearize(desc, yp, tv, 1.0, sc.ctcs_epsilon)
-        if tr is not None:
+    def linearize(self):
+        e, jx, ju, js, _ = self.po.linearize(self.desc, self.sc.substeps, self.starts, self.Us, self.Ss)
+        node = self.po.node_linearize(self.desc, self.yp, self.tv, 1.0, self.sc.ctcs_epsilon)
+        return e, jx, ju, js, node
+
+    def iteration(self):
+        e, jx, ju, js, (psi, pj, th, tj, imp, ij) = self.linearize()
+        if self.tr is not None:
+            lay, z, scp = self.lay, self.z, self.scp
             defects = np.stack([z[lay.xm(k + 1)] for k in range(lay.N - 1)]) - e
             lin = scp.LinearizedProblem(z_ref=z, ends=e, jx=jx, ju=ju, js=js, defects=defects, psi=psi, psi_jac=pj,
                                         theta=th, theta_jac=tj, imp_v=imp, imp_jac=ij)
-            scp.build_subproblem(tr, lin, z, 1.0, scp.SCPConfig())
-        return lay.N - 1
-
-    return step, pyoracle
+            scp.build_subproblem(self.tr, lin, z, 1.0, scp.SCPConfig())
+        return self.lay.N - 1
 
 
-def step_fn():
-    pass
-
-
-def cpu_batch_fn(sc, B):
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import pyoracle
-
-    from paper_2604_09993_b200 import synth
-    from paper_2604_09993_b200.model import pack_model
-
-    g, n_g = sc.path_constraints()
-    desc = pack_model(sc.model, sc.mixing_matrix(n_g), g)
-    x, U, S = synth.random_intervals(sc, B, seed=0)
-
-    def step():
-        pyoracle.linearize(desc, sc.substeps, x, U, S)
-        return B
-
-    return step, pyoracle
-
-
-def time_cpu(step, seconds, min_steps=1):
-    n, t0 = 0, time.perf_counter()
-    units = 0
-    while n < min_steps or time.perf_counter() - t0 < seconds:
+def time_cpu(step, seconds=None, steps=None):
+    n, units, t0 = 0, 0, time.perf_counter()
+    while (n < steps) if seconds is None else (n < 1 or time.perf_counter() - t0 < seconds):
         units += step()
         n += 1
     dt = time.perf_counter() - t0
@@ -199,7 +236,6 @@ class Clocks:
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index):
-        self.index = index
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
@@ -219,11 +255,11 @@ class Clocks:
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         sm = [float(r[1]) for r in rows]
-        mx = float(rows[0][2])
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if "Active" in v and "Not" not in v})
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": reasons, "samples": len(rows),
-                "power_w_max": max(float(r[3]) for r in rows if r[3].strip() not in ("", "[N/A]"))}
+        pw = [float(r[3]) for r in rows if r[3].strip() not in ("", "[N/A]")]
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(rows[0][2]), "reasons": reasons,
+                "samples": len(rows), "power_w_max": max(pw) if pw else None}
 
 
 def fp64_peak_tflops(torch, dev):
@@ -242,20 +278,41 @@ def fp64_peak_tflops(torch, dev):
     return best
 
 
+def _profile_json(name):
+    path = os.path.join(ROOT, "profiles", name)
+    return json.load(open(path)) if os.path.exists(path) else {}
+
+
 def flops_per_interval(key):
-    path = os.path.join(ROOT, "profiles", "flops_per_interval.json")
-    if not os.path.exists(path):
-        return None, None
-    d = json.load(open(path))
+    d = _profile_json("flops_per_interval.json")
     e = d.get(key)
     return (e["flops"], d.get("definition")) if e else (None, None)
 
 
+def executed_flops_per_interval(B):
+    """ncu-executed fp64 flops per interval (DFMA = 2) of the K1 generation that serves
+    a batch of B intervals (profiles/fp64_instruction_counts.json)."""
+    d = _profile_json("fp64_instruction_counts.json")
+    key = "latency" if B <= 98 else "batch"
+    e = d.get(key)
+    return (e["executed_fp64_flops_per_interval"], e.get("source")) if e else (None, None)
+
+
 def ncu_traffic(key):
-    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
-    if not os.path.exists(path):
-        return None
-    return json.load(open(path)).get(key, {}).get("dram_bytes_per_launch")
+    return _profile_json("ncu_summary.json").get(key, {}).get("dram_bytes_per_launch")
+
+
+def _lib_launches():
+    """Kernels launched by libcito_b200 so far (C ABI counter + CUDA-graph replays)."""
+    from paper_2604_09993_b200 import _lib
+
+    return _lib.launch_count()
+
+
+def k1_kernel_name(B):
+    return ("k_linearize2<Topo_halfcheetah_g2,1> (1 interval/CTA)" if B <= 98
+            else "k_linearize<Topo_halfcheetah_g2,1,2> (2 intervals/CTA in lockstep)" if B <= 246
+            else "k_linearize<Topo_halfcheetah_g2,1,3> (3 intervals/CTA in lockstep)")
 
 
 def run_ours(args):
@@ -277,83 +334,21 @@ def run_ours(args):
     torch.cuda.set_device(dev)
     from paper_2604_09993_b200 import synth
     from paper_2604_09993_b200.linearize import GpuTranscription, initial_guess
+    from paper_2604_09993_b200.parallel import HostResult, ShardedBatch, ShardedMultiStart, gather_slices, shard_range
     from paper_2604_09993_b200.scenario import build_scaling
-    from paper_2604_09993_b200.subproblem import SubproblemAssembler, SubproblemPattern, build_subproblem
+    from paper_2604_09993_b200.subproblem import GpuSCPStep, SubproblemAssembler, SubproblemPattern
 
-    fine = args.workload == "fine"
-    sc = scp_problem(seed=rank, fine=fine)
-    gt = GpuTranscription(sc, device=dev.index)
-    lay = gt.lay
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
-
-    # --- SCP-iteration workload state
-    z = initial_guess(sc, gt.disc, lay)
-    z_dev = torch.as_tensor(z, device=dev)
-    delta = 1.0
-    scale_v, state_scale, u_scale = build_scaling(sc, lay)
-    asm = SubproblemAssembler(SubproblemPattern(sc, lay, scale_v), dev)
-    n_int = lay.N - 1
-
     k1_ev = []
+    K, W = args.steps, max(3, args.warmup)
 
-    lin_out = gt.linearize_device(z_dev, delta)  # output buffers reused by every step
-
-    def scp_step(zd, record=False):
-        if record:
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            r = gt.linearize_device(zd, delta, k1_events=(e0, e1), out=lin_out)
-            k1_ev.append((e0, e1))
-        else:
-            r = gt.linearize_device(zd, delta, out=lin_out)
-        asm.assemble_device(r, zd, reuse=True)  # whole subproblem: CSC of A, G (+ zero compaction), b, h
-        return r
-
-    # --- batch workload state
-    if args.workload == "batch" or (args.workload == "scp" and not args.no_batch_extra):
-        B = args.batch
-        ok = lambda x, u, s: synth.well_posed(gt.disc.propagate_batch_device(
-            *(torch.as_tensor(a, device=dev) for a in (x, u, s)))[0].cpu().numpy())
-        xb, Ub, Sb, redrawn = synth.random_intervals(sc, B, seed=100 + rank, finite_fn=ok)
-        xb_d, Ub_d, Sb_d = (torch.as_tensor(a, device=dev) for a in (xb, Ub, Sb))
-        bout = gt.disc.linearize_batch_device(xb_d, Ub_d, Sb_d)
-
-    def batch_step(record=False):
-        if record:
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-        gt.disc.linearize_batch_device(xb_d, Ub_d, Sb_d, out=bout)
-        if record:
-            e1.record(stream)
-            k1_ev.append((e0, e1))
-
-    if args.workload == "multistart":
-        # configs[3] analogue: HalfCheetah N=50 multi-start initial guesses (no quadruped
-        # exists in the reference); each rank owns `problems` starts
-        from paper_2604_09993_b200 import scenario as S2
-        from paper_2604_09993_b200.parallel import gather_rows
-
-        sc50 = S2.bundled("halfcheetah_bound", N=50)
-        gt50 = GpuTranscription(sc50, device=dev.index)
-        from paper_2604_09993_b200.linearize import initial_guess_batch
-
-        seeds = [rank * args.problems + i for i in range(args.problems)]
-        Z = initial_guess_batch(sc50, gt50.disc, seeds, gt50.lay)  # batched multi-start generation (§8(f) 4)
-        Z_dev = torch.as_tensor(Z, device=dev)
-        ms_out = gt50.linearize_device(Z_dev, 1.0)
-
-        def ms_step(record=False):
-            if record:
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                gt50.linearize_device(Z_dev, 1.0, k1_events=(e0, e1), out=ms_out)
-                k1_ev.append((e0, e1))
-            else:
-                gt50.linearize_device(Z_dev, 1.0, out=ms_out)
-            # result collection: per-problem max |defect| to every rank (NCCL all_gather at N > 1)
-            metric = ms_out["defects"].view(args.problems, -1).abs().amax(dim=1)
-            return gather_rows(metric) if dist else metric
+    def ev_pair():
+        return torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
     def timed(step_fn, K, W):
+        """W warm-up steps, then K steps bracketed by barrier + synchronize; per-step
+        CUDA events on the launching stream (L2 flush outside them); max over ranks."""
         for _ in range(W):
             step_fn(False)
         torch.cuda.synchronize()
@@ -364,137 +359,210 @@ def run_ours(args):
         evs = []
         launches0 = _lib_launches()
         for _ in range(K):
-            flush.zero_()  # L2 flush outside the timed events
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            flush.zero_()
+            e0, e1 = ev_pair()
             e0.record(stream)
             step_fn(True)
             e1.record(stream)
             evs.append((e0, e1))
         torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
         launches = _lib_launches() - launches0
         ms = float(np.sum([a.elapsed_time(b) for a, b in evs]))
-        k1_ms = float(np.mean([a.elapsed_time(b) for a, b in k1_ev]))
+        k1_ms = float(np.mean([a.elapsed_time(b) for a, b in k1_ev])) if k1_ev else None
         if dist:
             t = torch.tensor([ms], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
-            dist.barrier()
         return ms, k1_ms, launches
 
-    K, W = args.steps, max(3, args.warmup)
-    clocks = Clocks(dev.index if world == 1 else local)
-    step_k1_ms = None
-    if args.workload in ("scp", "fine"):
-        ms_tot, k1_ms, launches = timed(lambda rec: scp_step(z_dev, rec), K, W)
-        # the interval kernel alone (the roofline kernel; in the step it overlaps K3 and
-        # includes the fork/join): same intervals, device-resident, events on its stream
-        zh = z_dev.cpu().numpy()
-        xs = torch.as_tensor(np.stack([zh[lay.xp(k)] for k in range(n_int)]), device=dev)
-        us = torch.as_tensor(np.stack([zh[lay.u(k)] for k in range(n_int)]), device=dev)
-        ss = torch.as_tensor(np.array([zh[lay.s(k)][0] for k in range(n_int)]), device=dev)
-        kout = gt.disc.linearize_batch_device(xs, us, ss)
-        for _ in range(W):
-            gt.disc.linearize_batch_device(xs, us, ss, out=kout)
+    def kernel_alone(disc, xs, us, ss, reps):
+        """K1 alone (the roofline kernel), device-resident, events on its stream."""
+        kout = disc.linearize_batch_device(xs, us, ss)
+        for _ in range(3):
+            disc.linearize_batch_device(xs, us, ss, out=kout)
         kev = []
-        for _ in range(K):
+        for _ in range(reps):
             flush.zero_()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0, e1 = ev_pair()
             e0.record(stream)
-            gt.disc.linearize_batch_device(xs, us, ss, out=kout)
+            disc.linearize_batch_device(xs, us, ss, out=kout)
             e1.record(stream)
             kev.append((e0, e1))
         torch.cuda.synchronize()
-        step_k1_ms = k1_ms
-        k1_ms = float(np.mean([a.elapsed_time(b) for a, b in kev]))
-        units_per_step, B_k1 = n_int, n_int
-    elif args.workload == "multistart":
-        gt.disc = gt50.disc  # launch counter of the handle actually used
-        ms_tot, k1_ms, launches = timed(ms_step, K, W)
-        units_per_step = B_k1 = args.problems * (sc50.N - 1)
-    else:
-        ms_tot, k1_ms, launches = timed(batch_step, K, W)
-        units_per_step, B_k1 = args.batch, args.batch
-    clk = clocks.stop()
-    ms_per_step = ms_tot / K
-    value = world * units_per_step * K / (ms_tot * 1e-3)
+        return float(np.mean([a.elapsed_time(b) for a, b in kev]))
 
-    extra = {}
-    if args.workload == "scp" and not args.no_batch_extra:
-        bms, bk1, _ = timed(batch_step, max(5, K // 5), 3)
-        nb = max(5, K // 5)
-        extra["batch_extra"] = {"workload": f"HalfCheetah synthetic batch of {args.batch} intervals (configs[2])",
-                                "value": args.batch * nb / (bms * 1e-3), "unit": UNIT, "ms_per_step": bms / nb,
-                                "k1_ms": bk1}
+    def scp_setup(fine, seed):
+        sc = scp_problem(seed=seed, fine=fine)
+        gt = GpuTranscription(sc, device=dev.index)
+        z = initial_guess(sc, gt.disc, gt.lay)
+        z_dev = torch.as_tensor(z, device=dev)
+        asm = SubproblemAssembler(SubproblemPattern(sc, gt.lay, build_scaling(sc, gt.lay)[0]), dev)
+        out = gt.linearize_device(z_dev, 1.0)  # output buffers reused by every step
 
-    if args.workload == "scp" and not args.no_fine_extra:
-        # configs[4]: HalfCheetah N=200, 8 substeps, one SCP iteration (K1 + K3 + assembly)
-        scf = scp_problem(seed=rank, fine=True)
-        gtf = GpuTranscription(scf, device=dev.index)
-        zf = torch.as_tensor(initial_guess(scf, gtf.disc, gtf.lay), device=dev)
-        asmf = SubproblemAssembler(SubproblemPattern(scf, gtf.lay, build_scaling(scf, gtf.lay)[0]), dev)
-
-        fine_out = gtf.linearize_device(zf, delta)
-
-        def fine_step(record=False):
+        def step(record=False):
             if record:
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                r = gtf.linearize_device(zf, delta, k1_events=(e0, e1), out=fine_out)
+                e0, e1 = ev_pair()
+                r = gt.linearize_device(z_dev, 1.0, k1_events=(e0, e1), out=out)
                 k1_ev.append((e0, e1))
             else:
-                r = gtf.linearize_device(zf, delta, out=fine_out)
-            asmf.assemble_device(r, zf, reuse=True)
+                r = gt.linearize_device(z_dev, 1.0, out=out)
+            asm.assemble_device(r, z_dev, reuse=True)  # whole subproblem: CSC of A, G (+ zero compaction), b, h
+        return sc, gt, z, z_dev, step
 
-        nf = max(5, K // 5)
-        fms, fk1, _ = timed(fine_step, nf, 5)
-        extra["fine_extra"] = {"workload": "HalfCheetah N=200, 8 RKF substeps, one SCP iteration (configs[4]; "
-                                           "the reference has no RK4)",
-                               "value": (scf.N - 1) * nf / (fms * 1e-3), "unit": UNIT, "ms_per_step": fms / nf,
-                               "k1_ms": fk1}
+    def batch_setup(B):
+        """configs[2]: B intervals in total, rank r linearizes its contiguous range into
+        rank 0's full arrays (NCCL gather)."""
+        sc = scp_problem(seed=0)
+        gt = GpuTranscription(sc, device=dev.index)
+        ok = lambda x, u, s: synth.well_posed(gt.disc.propagate_batch_device(  # noqa: E731
+            *(torch.as_tensor(a, device=dev) for a in (x, u, s)))[0].cpu().numpy())
+        xb, Ub, Sb, _ = synth.random_intervals(sc, B, seed=100, finite_fn=ok)
+        lo, hi = shard_range(B, rank, world)
+        sb = ShardedBatch(gt.disc, device=dev)
+        x_d, U_d, S_d = (torch.as_tensor(a, device=dev) for a in (xb, Ub, Sb))
+        sb.compute(x_d, U_d, S_d)  # allocate
 
-    # --- e2e through the public API with host (pinned) buffers
-    if args.workload in ("scp", "fine"):
-        # public API of one SCP iteration's pre-IPM work (= cito.scp.linearize_all +
-        # build_subproblem, scp.py:412-413): host numpy z in, host scipy ConicProgram out
-        from paper_2604_09993_b200.subproblem import GpuSCPStep
+        def step(record=False):
+            out, _, _ = sb.compute(x_d, U_d, S_d)
+            if dist is not None and world > 1:
+                if record:
+                    c0, c1 = ev_pair()
+                    c0.record(stream)
+                sb._collect(out, B, lo, "device", None)
+                if record:
+                    c1.record(stream)
+                    k1_ev.append((c0, c1))
+        return gt, sb, xb, Ub, Sb, (lo, hi), step
 
+    clocks = Clocks(dev.index)
+    extra = {}
+    wl = args.workload
+    if wl in ("scp", "fine"):
+        fine = wl == "fine"
+        sc, gt, z, z_dev, step = scp_setup(fine, rank)
+        lay = gt.lay
+        n_int = lay.N - 1
+        ms_tot, step_k1_ms, launches = timed(step, K, W)
+        units_per_step = n_int * world
+        zh = z
+        xs = torch.as_tensor(np.stack([zh[lay.xp(k)] for k in range(n_int)]), device=dev)
+        us = torch.as_tensor(np.stack([zh[lay.u(k)] for k in range(n_int)]), device=dev)
+        ss = torch.as_tensor(np.array([zh[lay.s(k)][0] for k in range(n_int)]), device=dev)
+        k1_ms = kernel_alone(gt.disc, xs, us, ss, K)
+        B_k1 = n_int
+        extra["linearize_only"] = {"value": n_int * world / (step_k1_ms * 1e-3), "unit": UNIT,
+                                   "ms_per_step": step_k1_ms,
+                                   "what": "linearize_all alone (K1 + K3 + defects, one C call) inside the step"}
         scp_api = GpuSCPStep(gt)
 
         def e2e_step():
-            return scp_api.iterate(z, delta)
+            return scp_api.iterate(z, 1.0)
 
         e2e_step()
         h2d = z.nbytes + 16  # z plus [delta, epsilon] (one pinned H2D per step)
         d2h = scp_api.d2h_bytes()  # packed D2H per step: fixed fields + the CSC arrays up to their caps
-    elif args.workload == "multistart":
-        Z_pin = torch.as_tensor(Z).pin_memory()
-        ms_host = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True).numpy() for k, v in ms_out.items()}
+        e2e_note = "GpuSCPStep.iterate: host z in, host scipy program out; LinearizedProblem device-backed (lazy)"
+    elif wl == "batch":
+        B = args.batch
+        gt, sb, xb, Ub, Sb, (lo, hi), step = batch_setup(B)
+        ms_tot, collect_ms, launches = timed(step, K, W)
+        units_per_step = B
+        xs, us, ss = (torch.as_tensor(a[lo:hi], device=dev) for a in (xb, Ub, Sb))
+        k1_ms = kernel_alone(gt.disc, xs, us, ss, K)
+        B_k1 = hi - lo
+        if collect_ms is not None:
+            extra["collect"] = {"nccl_gather_ms": collect_ms, "what": "grouped NCCL send/recv of every rank's "
+                                "ends/jx/ju/js/flags into rank 0's full device arrays (device time on rank 0's stream)"}
+        host = HostResult(sb.shapes(B)) if world > 1 else None
+        bout = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True).numpy() for t in sb._alloc(B).values()][:4]
 
         def e2e_step():
-            # public multi-start API: host Z in, host arrays out (caller-owned page-locked
-            # buffers); chunks of ~one K1 wave, each copied back while the next computes
-            return gt50.linearize_to_host(Z_pin, 1.0, out=ms_host)
+            if world > 1:
+                return sb.linearize(xb, Ub, Sb, collect="host", host=host)
+            return gt.disc.linearize_batch(xb, Ub, Sb, out=tuple(bout))
 
         e2e_step()
-        h2d = Z.nbytes
-        d2h = int(sum(v.numel() * v.element_size() for v in ms_out.values()))
-    else:
-        xb_p, Ub_p, Sb_p = (torch.as_tensor(a).pin_memory() for a in (xb, Ub, Sb))
-        bouts = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in bout]
+        h2d = (xb.nbytes + Ub.nbytes + Sb.nbytes) // world
+        n, nu2 = gt.disc.n_xt, 2 * gt.disc.n_u
+        d2h = (B * 8 * (2 * n + n * n + n * nu2) + 4 * B) // world
+        e2e_note = ("Discretizer.linearize_batch: host arrays in, all four result arrays back on the host"
+                    if world == 1 else "ShardedBatch.linearize(collect='host'): every rank H2D its rows, "
+                    "linearizes, D2H into one shared page-locked host result (the N-parallel-D2H collection)")
+    else:  # multistart
+        from paper_2604_09993_b200 import scenario as S2
 
-        xb_n, Ub_n, Sb_n = (t.numpy() for t in (xb_p, Ub_p, Sb_p))
-        outs_n = tuple(t.numpy() for t in bouts[:4])
+        sc50 = S2.bundled("halfcheetah_bound", N=50)
+        ms = ShardedMultiStart(sc50, list(range(args.problems)), device=dev)
+        gt = ms.gt
+        B_loc = (ms.hi - ms.lo) * (sc50.N - 1)
+
+        def step(record=False):
+            if record:
+                e0, e1 = ev_pair()
+                e0.record(stream)
+            ms.compute(1.0)
+            if record:
+                e1.record(stream)
+            if dist is not None and world > 1:
+                gather_slices(ms.out, ms.full, ms.rows, ms.all_bounds)
+            if record:
+                k1_ev.append((e0, e1))
+
+        ms_tot, lin_ms, launches = timed(step, K, W)
+        units_per_step = args.problems * (sc50.N - 1)
+        lay = gt.lay
+        xs = torch.as_tensor(np.concatenate([np.stack([z[lay.xp(k)] for k in range(lay.N - 1)]) for z in ms.Z]),
+                             device=dev)
+        us = torch.as_tensor(np.concatenate([np.stack([z[lay.u(k)] for k in range(lay.N - 1)]) for z in ms.Z]),
+                             device=dev)
+        ss = torch.as_tensor(np.concatenate([np.array([z[lay.s(k)][0] for k in range(lay.N - 1)]) for z in ms.Z]),
+                             device=dev)
+        k1_ms = kernel_alone(gt.disc, xs, us, ss, K)
+        B_k1 = B_loc
+        host = HostResult(ms.shapes()) if world > 1 else None
+        ms_host = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True).numpy() for k, v in ms.out.items()}
+        Z_pin = torch.as_tensor(ms.Z).pin_memory()
 
         def e2e_step():
-            # public drop-in Discretizer.linearize_batch (augmentation.py:236-242): host
-            # arrays in, host arrays out (caller-owned page-locked buffers); the C entry
-            # copies the inputs up and pipelines the results back chunk by chunk
-            return gt.disc.linearize_batch(xb_n, Ub_n, Sb_n, out=outs_n)
+            if world > 1:
+                return ms.linearize(1.0, collect="host", host=host)
+            return gt.linearize_to_host(Z_pin, 1.0, out=ms_host)
 
         e2e_step()
-        h2d = xb.nbytes + Ub.nbytes + Sb.nbytes
-        d2h = int(sum(t.numel() * t.element_size() for t in bout[:4])) + 4 * args.batch  # + per-interval flags
+        h2d = ms.Z.nbytes
+        d2h = int(sum(v.numel() * v.element_size() for v in ms.out.values()))
+        e2e_note = ("GpuTranscription.linearize_to_host: host Z in, every LinearizedProblem array back on the host"
+                    if world == 1 else "ShardedMultiStart.linearize(collect='host'): per-rank D2H into one shared "
+                    "page-locked host result")
+    clk = clocks.stop()
+    ms_per_step = ms_tot / K
+    value = units_per_step * K / (ms_tot * 1e-3)
+
+    # --- extras: configs[2] batch beside the scp headline; configs[4] fine grid
+    if wl == "scp" and not args.no_batch_extra:
+        B = args.batch
+        _, _, _, _, _, (blo, bhi), bstep = batch_setup(B)
+        nb = max(5, K // 5)
+        bms, bcoll, _ = timed(bstep, nb, 3)
+        extra["batch_extra"] = {"workload": f"HalfCheetah synthetic batch of {B} intervals (configs[2])"
+                                + (f", split over {world} GPUs + NCCL gather to rank 0" if world > 1 else ""),
+                                "value": B * nb / (bms * 1e-3), "unit": UNIT, "ms_per_step": bms / nb,
+                                "nccl_gather_ms": bcoll}
+    if wl == "scp" and not args.no_fine_extra:
+        _, gtf, _, _, fstep = scp_setup(True, rank)
+        nf = max(5, K // 5)
+        fms, fk1, _ = timed(fstep, nf, 5)
+        extra["fine_extra"] = {"workload": "HalfCheetah N=200, 8 RKF substeps, one SCP iteration (configs[4]; "
+                                           "the reference has no RK4)",
+                               "value": (gtf.lay.N - 1) * world * nf / (fms * 1e-3), "unit": UNIT,
+                               "ms_per_step": fms / nf, "linearize_all_ms": fk1}
+
+    # --- e2e through the public API with host buffers
     for _ in range(W):
         e2e_step()
+    torch.cuda.synchronize()
     if dist:
         dist.barrier()
     t0 = time.perf_counter()
@@ -505,28 +573,27 @@ def run_ours(args):
         t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    e2e_value = world * units_per_step * K / e2e_s
+    e2e_value = units_per_step * K / e2e_s
 
     peak = fp64_peak_tflops(torch, dev)
-    key = "halfcheetah_s8" if fine else "halfcheetah_s5"
-    F, fdef = flops_per_interval(key)
+    F, fdef = flops_per_interval("halfcheetah_s8" if wl == "fine" else "halfcheetah_s5")
+    Fx, fxsrc = executed_flops_per_interval(B_k1) if wl != "fine" else (None, None)
     achieved = F * B_k1 / (k1_ms * 1e-3) / 1e12 if F else None
+    achieved_x = Fx * B_k1 / (k1_ms * 1e-3) / 1e12 if Fx else None
     roofline = {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": (achieved / peak) if achieved else None,
-                "traffic": ncu_traffic(f"k_linearize_{'scp' if fine else args.workload}"),
-                "kernel": ("k_linearize2<Topo_halfcheetah_g2,1> (1 interval/CTA)" if B_k1 <= 98
-                           else "k_linearize<Topo_halfcheetah_g2,1,2> (2 intervals/CTA in lockstep)" if B_k1 <= 246
-                           else "k_linearize<Topo_halfcheetah_g2,1,3> (3 intervals/CTA in lockstep)"),
-                "kernel_ms": k1_ms, "intervals_per_launch": B_k1,
-                "step_linearize_all_ms": step_k1_ms,
+                "traffic": ncu_traffic(f"k_linearize_{'scp' if wl == 'fine' else wl}"),
+                "kernel": k1_kernel_name(B_k1), "kernel_ms": k1_ms, "intervals_per_launch": B_k1,
                 "flops_per_interval": F, "flops_definition": fdef,
+                "achieved_executed": achieved_x, "frac_executed": (achieved_x / peak) if achieved_x else None,
+                "executed_flops_per_interval": Fx, "executed_source": fxsrc,
                 "peak_source": "measured in this run: FP64 DFMA probe kernel (cito_dfma_peak); MEASURED_PEAKS.json "
                                "has no fp64 entry"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         # the reference arm itself, in a subprocess (isolates the jax shim), time-bounded sample
-        p = subprocess.run([sys.executable, os.path.abspath(__file__), "--impl", "reference", "--workload", args.workload,
+        p = subprocess.run([sys.executable, os.path.abspath(__file__), "--impl", "reference", "--workload", wl,
                             "--sample-seconds", str(args.cpu_seconds), "--warmup", "1", "--problems",
                             str(args.problems), "--batch", str(args.batch)], capture_output=True, text=True,
                            cwd=ROOT, env={k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE")})
@@ -535,28 +602,20 @@ def run_ours(args):
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
-        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic" if args.workload == "batch" else "synthetic (scenario initial guess, seed=rank)",
-        "config": {"workload": {"scp": "scp: one SCP-iteration linearize of HalfCheetah N=30 (halfcheetah_bound.json, "
-                                       "5 RKF substeps, 29 intervals; K1+K3 + whole-subproblem assembly)",
-                                "fine": "fine: one SCP-iteration linearize of HalfCheetah N=200, 8 RKF substeps "
-                                        "(configs[4]; 199 intervals; K1+K3 + whole-subproblem assembly)",
-                                "batch": f"batch: {args.batch} independent synthetic HalfCheetah intervals per GPU "
-                                         "(configs[2])",
-                                "multistart": f"multistart: {args.problems} HalfCheetah N=50 initial guesses per GPU "
-                                              "(configs[3] analogue), linearize_all (K1+K3) + NCCL all_gather of "
-                                              "per-problem defect norms"}[args.workload],
-                   "intervals_per_step_per_gpu": units_per_step, "l2": "flushed (256 MiB write) between timed steps",
-                   "parallelism": f"replicas x{world} (independent problems per rank, no collective)"},
+        "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak" if wl in ("scp", "fine") else "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic" if wl == "batch" else "synthetic (scenario initial guess; scp: seed = rank)",
+        "config": config_for(args, world),
         "roofline": roofline, "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                "ms_per_step": e2e_s / K * 1e3},
+                "ms_per_step": e2e_s / K * 1e3, "api": e2e_note},
         "gpu_launches": int(launches), "clocks": clk,
     }
     line.update(extra)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:
+        dist.barrier()
         dist.destroy_process_group()
 
 
@@ -564,45 +623,100 @@ def run_reference(args):
     rank, world, local = env_rank()
     if rank != 0:
         return
-    sc = scp_problem(seed=0, fine=args.workload == "fine")
-    if args.workload in ("scp", "fine", "multistart"):
-        step, po = cpu_step_fn(sc, 0)
-        sample = (f"HalfCheetah N={sc.N} ({sc.substeps} substeps) initial-guess SCP iteration per step: oracle-port "
-                  f"linearization ({sc.N - 1} intervals + node relations)" + (" + the reference's own build_subproblem/canonicalize (baseline/_ref)"
-                                         if step_fn.with_assembly else " (reference not installed: no assembly)"))
-    else:
-        B = max(8, min(args.batch, 256))
-        step, po = cpu_batch_fn(sc, B)
-        sample = f"{B} synthetic HalfCheetah intervals per step (bounded sample of the {args.batch}-interval batch)"
-    for _ in range(max(1, args.warmup)):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle
+
+    wl = args.workload
+    legs = {}
+    if wl in ("scp", "fine"):
+        it = CpuIteration(scp_problem(seed=0, fine=wl == "fine"))
+        n_int = it.lay.N - 1
+        it.iteration()
+        what = (f"HalfCheetah N={it.sc.N} ({it.sc.substeps} substeps) initial-guess SCP iteration per step: oracle-port "
+                f"linearization ({n_int} intervals + node relations)")
+        what += (" + the reference's own build_subproblem/canonicalize (baseline/_ref)" if it.tr is not None
+                 else " (reference not installed: no assembly)")
+        secs = args.sample_seconds
+        v, n, dt = time_cpu(it.iteration, secs, None if secs else args.steps)
+        lv, ln, ldt = time_cpu(lambda: (it.linearize(), n_int)[1], secs / 2 if secs else None,
+                               None if secs else args.steps)
+        legs["iteration"] = {"value": v, "ms_per_step": dt / n * 1e3, "steps": n}
+        legs["linearize_only"] = {"value": lv, "ms_per_step": ldt / ln * 1e3, "steps": ln,
+                                  "what": "oracle-port linearize_batch + node relations only (no assembly)"}
+        sample = f"{what}; {n} steps in {dt:.1f} s"
+    elif wl == "batch":
+        sc = scp_problem(seed=0)
+        from paper_2604_09993_b200 import synth
+        from paper_2604_09993_b200.model import pack_model
+
+        g, n_g = sc.path_constraints()
+        desc = pack_model(sc.model, sc.mixing_matrix(n_g), g)
+        Bs = max(8, min(args.batch, 256))
+        x, U, S = synth.random_intervals(sc, Bs, seed=100)
+
+        def step():
+            pyoracle.linearize(desc, sc.substeps, x, U, S)
+            return Bs
+
         step()
-    t0 = time.perf_counter()
-    units, n = 0, 0
-    while (n < args.steps) if args.sample_seconds is None else (n < 1 or time.perf_counter() - t0 < args.sample_seconds):
-        units += step()
-        n += 1
-    dt = time.perf_counter() - t0
-    v = units / dt
-    sample += f"; {n} steps in {dt:.1f} s on {os.cpu_count()} host cores"
-    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": n, "warmup": args.warmup,
-            "ms_per_step": dt / n * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": args.workload, "note": "reference algorithm on host cores via the C oracle port; "
-                       "the reference's JAX runtime is not installable (no jax wheel, no network)"},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": po.get_threads(), "kind": "port", "sample": sample},
+        v, n, dt = time_cpu(step, args.sample_seconds, None if args.sample_seconds else args.steps)
+        legs["linearize_only"] = {"value": v, "ms_per_step": dt / n * 1e3, "steps": n}
+        sample = f"{Bs} synthetic HalfCheetah intervals per step (bounded sample of the {args.batch}-interval batch); " \
+                 f"{n} steps in {dt:.1f} s"
+    else:
+        from paper_2604_09993_b200 import scenario as S2
+        from paper_2604_09993_b200.linearize import initial_guess_batch, node_inputs
+        from paper_2604_09993_b200.model import pack_model
+        from paper_2604_09993_b200.scenario import Layout
+
+        sc = S2.bundled("halfcheetah_bound", N=50)
+        lay = Layout(sc)
+        g, n_g = sc.path_constraints()
+        desc = pack_model(sc.model, sc.mixing_matrix(n_g), g)
+        P = max(1, min(args.problems, 4))
+        Z = initial_guess_batch(sc, _OracleBatchDisc(sc), list(range(P)), lay)
+        n = lay.N - 1
+
+        def step():
+            for z in Z:
+                pyoracle.linearize(desc, sc.substeps, np.stack([z[lay.xp(k)] for k in range(n)]),
+                                   np.stack([z[lay.u(k)] for k in range(n)]),
+                                   np.array([z[lay.s(k)][0] for k in range(n)]))
+                yp, tv = node_inputs(lay, z)
+                pyoracle.node_linearize(desc, yp, tv, 1.0, sc.ctcs_epsilon)
+            return P * n
+
+        step()
+        v, n_s, dt = time_cpu(step, args.sample_seconds, None if args.sample_seconds else args.steps)
+        legs["linearize_only"] = {"value": v, "ms_per_step": dt / n_s * 1e3, "steps": n_s}
+        sample = f"{P} of the {args.problems} HalfCheetah N=50 starts per step (bounded sample): oracle-port " \
+                 f"linearize_all; {n_s} steps in {dt:.1f} s"
+    head = legs.get("iteration", legs["linearize_only"])
+    v = head["value"]
+    sample += f" on {pyoracle.get_threads()} of {os.cpu_count()} host cores"
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": head["steps"],
+            "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True,
+            "scaling": "weak" if wl in ("scp", "fine") else "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic" if wl == "batch" else "synthetic (scenario initial guess; scp: seed = rank)",
+            "impl": "reference", "config": config_for(args, world),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": pyoracle.get_threads(), "kind": "port",
+                             "sample": sample, "legs": legs,
+                             "note": "reference algorithm on host cores via the C oracle port (dense forward-mode "
+                                     "duals like jacfwd, LU like jnp.linalg.solve); the reference's JAX runtime is "
+                                     "not installable (no jax wheel, no network)"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def _lib_launches():
-    """Kernels launched by libcito_b200 so far (C ABI counter + CUDA-graph replays)."""
-    from paper_2604_09993_b200 import _lib
-
-    return _lib.launch_count()
+class _OracleBatchDisc(_OracleDisc):
+    def propagate_batch(self, xt0s, Us, Ss):
+        return self.po.propagate(self.desc, self.substeps, np.asarray(xt0s), np.asarray(Us), np.asarray(Ss))[0]
 
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_under_torchrun(args)
     if args.impl == "reference":
         run_reference(args)
     else:
@@ -611,4 +725,3 @@ def main():
 
 if __name__ == "__main__":
     main()
-

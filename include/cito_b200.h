@@ -205,8 +205,14 @@ cito_status cito_scatter_dynamics_dev(cito_handle* h, int64_t n_int, const doubl
  * rest compacted: out_ptr[ncols+1] (int32), out_rows/out_vals[<= superset nnz].
  * lin: HOST array of 10 device pointers {jx, ju, js, imp_jac, theta_jac,
  * psi_jac, ends, imp_v, theta, psi}; counts: device int32 workspace
- * [ncols + 64], ZEROED before the first call and kept between calls (the one-pass
- * compaction stores its per-block totals and launch epoch there). */
+ * [ncols + 64] per matrix.  The one-pass compaction keeps a fixed header
+ * [ticket, finished CTAs, pad, pad] at the start of counts[0] followed by one
+ * uint64 flag per column block; it returns them to zero at the end of every
+ * launch, so the rules are: ZERO the workspace before its first use, keep it
+ * between calls (any ncols up to the size it was allocated for), and zero it
+ * again after a call that returned CITO_ERR_CUDA (a launch that did not
+ * complete leaves its tickets behind).  One workspace per stream: two
+ * concurrent launches must not share it. */
 cito_status cito_csc_assemble_dev(int32_t ncols, const int64_t* sp_ptr, const int32_t* sp_row, const int8_t* sp_src,
                                   const int64_t* sp_idx, const double* sp_val, const double* sigma,
                                   const double* const* lin, int32_t* counts, int32_t* out_ptr, int32_t* out_rows,

@@ -238,27 +238,38 @@ __global__ void __launch_bounds__(256) k_csc_write2(int32_t ncols, const CscArgs
 }
 
 // One-pass CSC compaction (default): each column block counts its exact nonzeros,
-// publishes the total tagged with this launch's epoch, then sums the totals of
-// the preceding blocks (decoupled look-back: a block only waits on lower-index
-// blocks, which are dispatched before it), scans its columns and writes.  The
-// counts workspace of matrix m holds the tagged totals as uint64 per block; the
-// launch epoch and a finished-block counter live after them in counts[0] (the
-// last block to finish advances the epoch, so the next launch -- e.g. the next
-// CUDA-graph replay -- uses a fresh tag without any reset).
+// publishes its total, then sums the totals of the preceding blocks (decoupled
+// look-back), scans its columns and writes.  Deadlock freedom does not rely on
+// the hardware dispatching CTAs in blockIdx order: every CTA takes its tile from
+// an atomic ticket, so a tile only ever waits on tiles whose CTAs started before
+// it (already resident or finished), whatever else shares the SMs (the rhs kernel
+// on the side stream, a CUDA graph's neighbours).  Tiles are numbered over both
+// matrices (A's blocks first), gridDim = (column blocks, nmat).
+// Workspace (the caller's counts[0], int32[ncols + 64]): a fixed header
+//   [0] ticket  [1] finished CTAs  [2..3] padding
+// then one uint64 flag per tile: (1 << 32) | block total once published.  The
+// last CTA of a launch returns header and flags to zero, so every launch --
+// e.g. every replay of a captured CUDA graph -- starts from a clean workspace;
+// the workspace must be zero before the first launch (and again after a launch
+// that did not complete, see include/cito_b200.h).
+#define CSC_HDR_WORDS 4
+
 __global__ void __launch_bounds__(256) k_csc_onepass(int32_t ncols, const CscArgs a, const double* __restrict__ sigma,
                                                      const LinTable L) {
-  const int m = blockIdx.y;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t* __restrict__ sp_ptr = a.sp_ptr[m];
-  const int nb = gridDim.x;
-  const int64_t c0 = (int64_t)blockIdx.x * CSC_CPB;
-  unsigned long long* flags = reinterpret_cast<unsigned long long*>(a.counts[m]);
-  unsigned* sync = reinterpret_cast<unsigned*>(a.counts[0]) + 2 * nb;  // [epoch, finished blocks]
+  const int nb = gridDim.x, ntiles = gridDim.x * gridDim.y;
+  unsigned* hdr = reinterpret_cast<unsigned*>(a.counts[0]);
+  unsigned long long* flags = reinterpret_cast<unsigned long long*>(a.counts[0] + CSC_HDR_WORDS);
   __shared__ int32_t red[8];
   __shared__ int32_t ccount[CSC_CPB];
   __shared__ int32_t cbase[CSC_CPB];
-  __shared__ unsigned tag_s;
-  if (tid == 0) tag_s = *((volatile unsigned*)sync) + 1u;
+  __shared__ int tile_s, last_s;
+  if (tid == 0) tile_s = (int)atomicAdd(&hdr[0], 1u);
+  __syncthreads();
+  const int tile = tile_s;
+  const int m = tile / nb, bx = tile - m * nb;
+  const int64_t* __restrict__ sp_ptr = a.sp_ptr[m];
+  const int64_t c0 = (int64_t)bx * CSC_CPB;
   // per-column nonzero counts of this block
   for (int k = warp; k < CSC_CPB; k += 8) {
     const int64_t c = c0 + k;
@@ -273,20 +284,20 @@ __global__ void __launch_bounds__(256) k_csc_onepass(int32_t ncols, const CscArg
     if (lane == 0) ccount[k] = n;
   }
   __syncthreads();
-  const unsigned tag = tag_s;
   if (warp == 0) {  // publish this block's total
     int t = ccount[lane];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-    if (lane == 0) atomicExch(&flags[blockIdx.x], ((unsigned long long)tag << 32) | (unsigned)t);
+    if (lane == 0) atomicExch(&flags[tile], (1ull << 32) | (unsigned)t);
   }
-  // prefix over the preceding column blocks (spin until each is published with this tag)
+  // prefix over the preceding column blocks of the same matrix (tiles m*nb .. tile-1,
+  // all taken by CTAs that started before this one)
   int pre = 0;
-  for (int j = tid; j < (int)blockIdx.x; j += blockDim.x) {
+  for (int j = m * nb + tid; j < tile; j += blockDim.x) {
     unsigned long long f;
     do {
       f = *((volatile unsigned long long*)&flags[j]);
-    } while ((unsigned)(f >> 32) != tag);
+    } while ((f >> 32) == 0ull);
     pre += (int)(unsigned)(f & 0xffffffffull);
   }
 #pragma unroll
@@ -310,7 +321,20 @@ __global__ void __launch_bounds__(256) k_csc_onepass(int32_t ncols, const CscArg
     if (c < ncols) a.out_ptr[m][c] = base;
     if (c == ncols - 1) a.out_ptr[m][ncols] = base + v;
   }
+  // every read of the flags by this CTA is done: count it as finished
+  if (tid == 0) {
+    __threadfence();
+    last_s = atomicAdd(&hdr[1], 1u) == (unsigned)ntiles - 1u;
+  }
   __syncthreads();
+  if (last_s) {  // all other CTAs are past their look-back: clean the workspace for the next launch
+    for (int j = tid; j < ntiles; j += blockDim.x) flags[j] = 0ull;
+    if (tid == 0) {
+      hdr[0] = 0u;
+      hdr[1] = 0u;
+    }
+    __threadfence();
+  }
   const unsigned lt = (1u << lane) - 1u;
   for (int k = warp; k < CSC_CPB; k += 8) {
     const int64_t c = c0 + k;
@@ -331,16 +355,6 @@ __global__ void __launch_bounds__(256) k_csc_onepass(int32_t ncols, const CscArg
         if (a.rowmax[m]) atomicMax(&a.rowmax[m][r], (unsigned long long)__double_as_longlong(fabs(v)));
       }
       base += __popc(msk);
-    }
-  }
-  // the last block of the launch advances the epoch (every block has read it by then)
-  if (tid == 0) {
-    __threadfence();
-    const unsigned done = atomicAdd(&sync[1], 1u);
-    if (done == (unsigned)(nb * gridDim.y) - 1u) {
-      sync[1] = 0u;
-      __threadfence();
-      atomicAdd(&sync[0], 1u);
     }
   }
 }

@@ -83,7 +83,9 @@ class Discretizer:
         self._h = _lib.Handle(self._desc, substeps)
         d = self._h.dims
         self.n_u = d.n_u
-        assert d.n_xt == self.n_xt and d.n_y == self.n_y
+        if d.n_xt != self.n_xt or d.n_y != self.n_y:
+            raise RuntimeError(f"library dims (n_xt={d.n_xt}, n_y={d.n_y}) disagree with the model "
+                               f"(n_xt={self.n_xt}, n_y={self.n_y})")
 
     # -- input normalisation (mirrors jnp.asarray(...).reshape(len(Ss), -1))
     def _batch(self, xt0s, Us, Ss):

@@ -83,7 +83,15 @@ class LazyLinearizedProblem:
         raise AttributeError(name)
 
     def device_arrays(self):
+        """The device tensors behind this result, or None once the producer has
+        reclaimed them for a later iteration (the host copy is then authoritative)."""
         return self._dev
+
+    def release_device(self):
+        """Take a host copy and drop the device references: called by the producer
+        right before it overwrites the buffers with the next iteration."""
+        self.materialize()
+        self._dev = None
 
 
 def _lp_type():
@@ -165,8 +173,9 @@ class GpuTranscription:
         # layout bases as used by the fused kernels (identical to ocp.Layout's formulas, ocp.py:154-174)
         self.base_u = 2 * N * lay.n_xt
         self.base_p = self.base_u + (N - 1) * (2 * lay.n_u + 1)
-        assert int(lay.u(0)[0]) == self.base_u and int(lay.phi(0)[0]) == self.base_p
-        assert int(lay.xp(N - 1)[0]) == (2 * (N - 1) + 1) * lay.n_xt
+        if not (int(lay.u(0)[0]) == self.base_u and int(lay.phi(0)[0]) == self.base_p
+                and int(lay.xp(N - 1)[0]) == (2 * (N - 1) + 1) * lay.n_xt):
+            raise ValueError("decision-vector layout differs from cito.ocp.Layout (ocp.py:154-174)")
         t = lambda a: torch.as_tensor(np.ascontiguousarray(a, dtype=np.int64), device=self.device)
         self._i_start, self._i_end, self._i_u, self._i_s = t(idx_start), t(idx_end), t(idx_u), t(idx_s)
         self._i_yp, self._i_th = t(idx_yp), t(idx_th)
@@ -301,39 +310,9 @@ def initial_guess(scenario, disc, lay=None, seed=None):
     auxiliary channels come from the N-1 sequential K2 propagations."""
     from .scenario import Layout
 
-    sc = scenario
-    lay = lay or Layout(sc)
-    model = sc.model
-    rng = np.random.default_rng(sc.seed if seed is None else seed)
+    lay = lay or Layout(scenario)
     n_q = lay.n_q
-    z = np.zeros(lay.dim)
-    q_i, q_f = sc.x_init[:n_q], sc.x_final[:n_q]
-    for k in range(lay.N):
-        frac = k / (lay.N - 1)
-        pose = (1.0 - frac) * q_i + frac * q_f
-        z[lay.xm(k)[:n_q]] = pose
-        z[lay.xp(k)[:n_q]] = pose
-    for k in range(lay.N - 1):
-        u = np.zeros(2 * lay.n_u)
-        for side in range(2):
-            base = side * lay.n_u + lay.n_a
-            for i in range(lay.n_c):
-                mu = model.contacts[i].friction_mu
-                fn = rng.uniform(0.0, sc.guess_force_scale)
-                ft = rng.uniform(-mu * fn, mu * fn) if fn > 0 else 0.0
-                u[base + 2 * i] = ft
-                u[base + 2 * i + 1] = fn
-        z[lay.u(k)] = u
-        z[lay.s(k)] = sc.s_nominal
-    for k in range(lay.N):
-        blk = np.zeros(2 * lay.n_c)
-        for i in range(lay.n_c):
-            mu = model.contacts[i].friction_mu
-            pn = rng.uniform(0.0, sc.guess_impulse_scale) if sc.guess_impulse_scale else 0.0
-            pt = rng.uniform(-mu * pn, mu * pn) if pn > 0 else 0.0
-            blk[2 * i] = pt
-            blk[2 * i + 1] = pn
-        z[lay.phi(k)] = blk
+    z = _initial_guess_no_y(scenario, lay, seed)
     z[lay.y_of_xm(0)] = np.zeros(lay.n_y)
     for k in range(lay.N):
         z[lay.y_of_xp(k)] = z[lay.y_of_xm(k)]

@@ -21,6 +21,7 @@ boxes per (k, side), dilation boxes, slack nonnegativity, then SOC blocks in
 add_soc order (node impulse cones inside the node loop, control cones).
 """
 
+import os
 import sys
 from dataclasses import dataclass
 
@@ -207,7 +208,8 @@ class SubproblemPattern:
         for idx_set in (self.sp_idx, self.sm_idx, self.t_idx):
             for i in idx_set:
                 G.add([i], -1, 0, [-1.0], 0.0)
-        assert eq_s == n_eq and in_s == n_in
+        if eq_s != n_eq or in_s != n_in:
+            raise RuntimeError(f"row count mismatch: eq {eq_s} vs {n_eq}, ineq {in_s} vs {n_in}")
         self.n_orthant = G.n
         # SOC rows follow the orthant rows (conic.py:250-258)
         g_rows = G.arrays()
@@ -254,7 +256,8 @@ class SubproblemPattern:
         row, col, src, idx, val, rhs = arrs
         order = np.lexsort((row, col))
         key = col[order] * (nrows + 1) + row[order]
-        assert np.all(np.diff(key) > 0), "duplicate (row, col) in the superset"
+        if not np.all(np.diff(key) > 0):
+            raise RuntimeError("duplicate (row, col) in the superset pattern")
         counts = np.bincount(col, minlength=ncols)
         return dict(indptr=np.concatenate([[0], np.cumsum(counts)]).astype(np.int64), row=row[order].astype(np.int32),
                     col=col[order], src=src[order], idx=idx[order], val=val[order], rhs=rhs, nrows=nrows)
@@ -458,6 +461,7 @@ class ConicProgram:
 
 
 _CSC_FAST = None  # None: not probed yet; else (maxprint,) when the direct construction is valid
+_CSC_CHECK = os.environ.get("CITO_CHECK_CSC", "0") == "1"
 
 
 def _csc_direct(data, indices, indptr, shape):
@@ -465,10 +469,22 @@ def _csc_direct(data, indices, indptr, shape):
     float64 data, len == nnz; sorted, no duplicates -- the device compaction's
     output), without the constructor's per-call dtype/format checks (~20 us per
     matrix).  Probed once against the regular constructor: if this scipy's matrix
-    carries attributes the direct form does not set, the regular one is used."""
+    carries attributes the direct form does not set, the regular one is used.
+    Every call keeps the O(1) invariants (int32/float64 dtypes, indptr[0] == 0,
+    indptr[-1] == nnz, len(indptr) == ncols + 1); CITO_CHECK_CSC=1 adds scipy's
+    full format check (sorted, in-range indices) for debugging."""
     global _CSC_FAST
     import scipy.sparse as sp
 
+    if (indices.dtype != np.int32 or indptr.dtype != np.int32 or data.dtype != np.float64
+            or len(indptr) != shape[1] + 1 or indptr[0] != 0 or indptr[-1] != len(indices)
+            or len(data) != len(indices)):
+        raise RuntimeError("device CSC compaction returned an inconsistent matrix "
+                           f"(indptr[0]={indptr[0]}, indptr[-1]={indptr[-1]}, nnz={len(indices)})")
+    if _CSC_CHECK:
+        m = sp.csc_matrix((data, indices, indptr), shape=shape, copy=False)
+        m.check_format(full_check=True)
+        return m
     if _CSC_FAST is None:
         ref = sp.csc_matrix((data, indices, indptr), shape=shape, copy=False)
         keys = set(vars(ref))
@@ -732,7 +748,7 @@ def build_subproblem(tr, lin, z_j, delta, config):
 
     cached = _cache.get(id(tr))
     last = getattr(cached[1], "last", None) if cached and cached[0] is tr else None
-    if hasattr(lin, "device_arrays"):  # produced by our linearize_all: already on the device
+    if hasattr(lin, "device_arrays") and lin.device_arrays() is not None:  # ours, buffers still current
         lin_dev = lin.device_arrays()
         z_ref = torch.as_tensor(np.ascontiguousarray(lin.z_ref, dtype=np.float64), device=dev)
     elif last is not None and last[0] is lin:
@@ -1024,8 +1040,8 @@ class GpuSCPStep:
         # a LinearizedProblem handed out by the previous call still points at the
         # reused device buffers: give it its own host copy before overwriting them
         prev = self._last_lin() if self._last_lin is not None else None
-        if prev is not None and prev._host is None:
-            prev.materialize()
+        if prev is not None and prev.device_arrays() is not None:
+            prev.release_device()
         if epsilon is None:
             epsilon = gt.scenario.ctcs_epsilon
         stream = torch.cuda.current_stream(gt.device)

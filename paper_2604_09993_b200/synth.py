@@ -60,7 +60,6 @@ def _draw(scenario, B, rng):
     v = rng.normal(0.0, 0.5, size=(B, n_q))
     y = rng.uniform(0.0, 0.1, size=(B, n_y))
     xt0 = np.concatenate([q, v, y], axis=1)
-    assert xt0.shape == (B, n_xt)
     U = np.zeros((B, 2, n_u))
     act = [model.joints[j] for j in model.actuated_joints]
     for side in range(2):

@@ -10,8 +10,9 @@ sys.path.insert(0, os.path.join(ROOT, "oracle"))  # test infrastructure: the CPU
 
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 GOLDEN_CASES = ["pointmass_rest", "monoped_n20", "halfcheetah_n30", "biped_walk"]
-SCEN_OF = {"pointmass_rest": ("pointmass_rest", None), "monoped_n20": ("monoped_hop", 20),
-           "halfcheetah_n30": ("halfcheetah_bound", 30), "biped_walk": ("biped_walk", None)}
+SCEN_OF = {"pointmass_rest": ("pointmass_rest", {}), "monoped_n20": ("monoped_hop", {"N": 20}),
+           "halfcheetah_n30": ("halfcheetah_bound", {"N": 30}), "biped_walk": ("biped_walk", {}),
+           "halfcheetah_n200s8": ("halfcheetah_bound", {"N": 200, "substeps": 8})}
 
 
 def pytest_configure(config):
@@ -33,8 +34,8 @@ def load_golden(name):
 def golden_scenario(name):
     from paper_2604_09993_b200 import scenario as S
 
-    scen, N = SCEN_OF[name]
-    return S.bundled(scen, **({"N": N} if N else {}))
+    scen, overrides = SCEN_OF[name]
+    return S.bundled(scen, **overrides)
 
 
 def scenario_desc(sc):

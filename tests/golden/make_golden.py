@@ -38,7 +38,7 @@ CASES = {
     "pointmass_rest": ("pointmass_rest", None, 4, True),
     "monoped_n20": ("monoped_hop", 20, 4, True),
     "halfcheetah_n30": ("halfcheetah_bound", 30, 4, True),
-    "biped_walk": ("biped_walk", None, 3, False),
+    "biped_walk": ("biped_walk", None, 3, True),
 }
 
 

@@ -21,7 +21,7 @@ sys.path.insert(0, os.path.join(ROOT, "oracle"))
 
 import ref_runner  # noqa: E402
 
-CASES = ["pointmass_rest", "monoped_n20", "halfcheetah_n30"]
+CASES = ["pointmass_rest", "monoped_n20", "halfcheetah_n30", "biped_walk"]
 TAGS = ["sp0", "sp1", "sp2"]
 
 

@@ -19,7 +19,7 @@ sys.path.insert(0, os.path.join(ROOT, "oracle"))
 import ref_runner  # noqa: E402
 
 CASES = {"pointmass_rest": ("pointmass_rest", None), "monoped_n20": ("monoped_hop", 20),
-         "halfcheetah_n30": ("halfcheetah_bound", 30)}
+         "halfcheetah_n30": ("halfcheetah_bound", 30), "biped_walk": ("biped_walk", None)}
 
 
 def main(names):

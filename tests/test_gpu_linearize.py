@@ -204,3 +204,31 @@ def test_linearize_empty_batch():
     e, jx, ju, js = d.linearize_batch(np.zeros((0, d.n_xt)), np.zeros((0, 2 * d.n_u)), np.zeros(0))
     assert e.shape == (0, d.n_xt) and jx.shape == (0, d.n_xt, d.n_xt) and ju.shape == (0, d.n_xt, 2 * d.n_u)
     assert d.propagate_batch(np.zeros((0, d.n_xt)), np.zeros((0, 2 * d.n_u)), np.zeros(0)).shape == (0, d.n_xt)
+
+
+def test_linearize_configs2_batch_4096_vs_oracle():
+    """configs[2] at its bench size: 4096 synthetic HalfCheetah intervals in one device
+    launch (the 3-interval lockstep batch kernel) and through the chunked host pipeline,
+    every interval against the oracle (rel <= 1e-9) with the oracle's exact-zero pattern."""
+    import torch
+
+    from paper_2604_09993_b200 import synth
+
+    sc = golden_scenario("halfcheetah_n30")
+    desc = scenario_desc(sc)
+    B = 4096
+    xt0, U, S, _ = synth.random_intervals(sc, B, seed=100, finite_fn=lambda x, u, s: synth.well_posed(
+        pyoracle.propagate(desc, sc.substeps, x, u, s)[0]))
+    ref = pyoracle.linearize(desc, sc.substeps, xt0, U, S)[:4]
+    disc = _disc(sc)
+    dev = torch.device("cuda")
+    out = disc.linearize_batch_device(*(torch.as_tensor(a, device=dev) for a in (xt0, U, S)))
+    torch.cuda.synchronize()
+    dev_out = [t.cpu().numpy() for t in out[:4]]
+    host_out = disc.linearize_batch(xt0, U, S)
+    for a, h, r in zip(dev_out, host_out, ref):
+        assert np.array_equal(a, h)
+        d = np.abs(a - r).reshape(B, -1).max(axis=1) / (1.0 + np.abs(r).reshape(B, -1).max(axis=1))
+        assert d.max() <= TOL, (int(d.argmax()), float(d.max()))
+    for a, r in zip(dev_out[1:3], ref[1:3]):  # jx, ju: structural zeros stay exact
+        assert np.array_equal(a == 0.0, r == 0.0)

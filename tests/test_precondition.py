@@ -15,7 +15,7 @@ import scipy.sparse as sp
 
 from conftest import golden_scenario, load_golden, rel_err
 
-CASES = ["pointmass_rest", "monoped_n20", "halfcheetah_n30"]
+CASES = ["pointmass_rest", "monoped_n20", "halfcheetah_n30", "biped_walk"]
 TAGS = ["sp0", "sp1", "sp2"]
 
 

@@ -41,15 +41,66 @@ import paper_2604_09993_b200.linearize as G
 import paper_2604_09993_b200.subproblem as SPB
 from paper_2604_09993_b200 import install
 
-name, iters, compare = sys.argv[1], int(sys.argv[2]), sys.argv[3] == "1"
+name, iters, compare, N, ref_lin = sys.argv[1], int(sys.argv[2]), sys.argv[3] == "1", int(sys.argv[4]), sys.argv[5]
 sc = ocp.load_scenario(os.path.join(REF, "cito", "assets", name + ".json"))
+if N:
+    sc = replace(sc, N=N, s_bounds=None)
 cfg = scp.SCPConfig(max_iters=iters)
 out = {}
+
+
+def oracle_linearize_all(tr, z, delta, jobs=1):
+    """cito.scp.linearize_all (scp.py:87-135) with the interval + node linearization of
+    the pinned C oracle (test infrastructure): the reference's own path for models
+    whose shim linearization (jacfwd under torch.func, ~5 s per interval) is too slow."""
+    import pyoracle
+    from paper_2604_09993_b200.model import pack_model
+    lay = tr.layout
+    desc = pack_model(tr.model, tr.mixing, tr.path_fn)
+    n = lay.N - 1
+    xs = np.stack([z[lay.xp(k)] for k in range(n)])
+    us = np.stack([z[lay.u(k)] for k in range(n)])
+    ss = np.array([z[lay.s(k)][0] for k in range(n)])
+    e, jx, ju, js, bad = pyoracle.linearize(desc, tr.scenario.substeps, xs, us, ss)
+    if bad.any():
+        raise FloatingPointError("non-finite state during interval integration")
+    yp, tv, _ = tr._node_inputs(z)
+    psi, pj, th, tj, imp, ij = pyoracle.node_linearize(desc, yp, tv, delta, tr.scenario.ctcs_epsilon)
+    defects = np.stack([z[lay.xm(k + 1)] for k in range(n)]) - e
+    return scp.LinearizedProblem(z_ref=z, ends=e, jx=jx, ju=ju, js=js, defects=defects, psi=psi, psi_jac=pj,
+                                 theta=th, theta_jac=tj, imp_v=imp, imp_jac=ij)
+
+
+class OracleDisc:
+    """propagate() of the pinned oracle for the reference arm's initial_guess."""
+    def __init__(self, tr):
+        import pyoracle
+        from paper_2604_09993_b200.model import pack_model
+        self.po, self.desc, self.m = pyoracle, pack_model(tr.model, tr.mixing, tr.path_fn), tr.scenario.substeps
+
+    def propagate(self, xt0, U, S):
+        e, bad = self.po.propagate(self.desc, self.m, np.asarray(xt0)[None], np.asarray(U).reshape(1, -1),
+                                   np.array([float(S)]))
+        if bad.any():
+            raise FloatingPointError("non-finite state during interval integration")
+        return e[0]
+
+
 if compare:
     ocp._transcriptions.clear()
-    z_ref, hist_ref, st_ref = scp.solve(sc, cfg)
+    orig = scp.linearize_all
+    if ref_lin == "oracle":
+        trr = ocp.get_transcription(sc)
+        trr.discretizer = OracleDisc(trr)
+        scp.linearize_all = oracle_linearize_all
+    try:
+        z_ref, hist_ref, st_ref = scp.solve(sc, cfg)
+    finally:
+        scp.linearize_all = orig
     out["ref"] = [h.z.tolist() for h in hist_ref]
     out["ref_delta"] = [h.delta for h in hist_ref]
+    out["ref_jpx"] = [h.j_px for h in hist_ref]
+    out["ref_jep"] = [h.j_ep for h in hist_ref]
 ocp._transcriptions.clear()
 tr = ocp.get_transcription(sc)
 install(tr)                       # tr.discretizer -> GPU (initial_guess uses it)
@@ -63,18 +114,20 @@ finally:
     scp.linearize_all, scp.build_subproblem, scp.precondition = orig
 out["gpu"] = [h.z.tolist() for h in hist]
 out["gpu_delta"] = [h.delta for h in hist]
+out["gpu_jpx"] = [h.j_px for h in hist]
+out["gpu_jep"] = [h.j_ep for h in hist]
 out["status"] = st
 out["launches"] = tr.discretizer.launch_count() + G._cache[id(tr)][1].disc.launch_count()
 print("RESULT " + json.dumps(out))
 '''
 
 
-def _run(name, iters, compare, timeout=1500):
+def _run(name, iters, compare, N=0, ref_lin="shim", timeout=1500):
     ref = _ref_src()
     if ref is None:
         pytest.skip("reference package not available (baseline/_ref or /root/reference)")
     code = f"ROOT = {ROOT!r}\nREF = {ref!r}\n" + SCRIPT
-    p = subprocess.run([sys.executable, "-c", code, name, str(iters), "1" if compare else "0"], capture_output=True,
+    p = subprocess.run([sys.executable, "-c", code, name, str(iters), "1" if compare else "0", str(N), ref_lin], capture_output=True,
                        text=True, timeout=timeout, cwd=ROOT)
     line = [l for l in p.stdout.splitlines() if l.startswith("RESULT ")]
     assert p.returncode == 0 and line, p.stderr[-3000:]
@@ -95,9 +148,20 @@ def test_scp_solve_pointmass_matches_reference_path():
 
 
 @pytest.mark.gpu
-def test_scp_solve_halfcheetah_runs_with_gpu_linearization():
+def test_scp_solve_halfcheetah_n30_matches_reference_path():
+    """configs[1]: HalfCheetah N=30, the reference's cito.scp.solve (backtracking
+    homotopy + host IPM, scp.py:383-467) for 3 iterations, once on its own path
+    (reference build_subproblem/precondition, linearization by the pinned oracle
+    port, which matches the reference's jacfwd to <= 1e-11) and once with the
+    three GPU drop-ins installed: every iterate, delta and progress measure agree."""
     import numpy as np
 
-    r = _run("halfcheetah_bound", 2, False)
-    assert len(r["gpu"]) == 3
-    assert all(np.all(np.isfinite(np.asarray(z))) for z in r["gpu"])
+    r = _run("halfcheetah_bound", 3, True, N=30, ref_lin="oracle")
+    assert len(r["gpu"]) == len(r["ref"]) == 4
+    for zg, zr in zip(r["gpu"], r["ref"]):
+        zg, zr = np.asarray(zg), np.asarray(zr)
+        assert np.all(np.isfinite(zg))
+        assert np.max(np.abs(zg - zr)) <= 1e-6 * (1.0 + np.max(np.abs(zr)))
+    assert np.allclose(r["gpu_delta"], r["ref_delta"], rtol=1e-9)
+    assert np.allclose(r["gpu_jpx"], r["ref_jpx"], rtol=1e-5, atol=1e-9)
+    assert np.allclose(r["gpu_jep"], r["ref_jep"], rtol=1e-5, atol=1e-9)

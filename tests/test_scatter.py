@@ -8,12 +8,15 @@ import scipy.sparse as sp
 
 from conftest import golden_scenario, load_golden, rel_err
 
-CASES = ["pointmass_rest", "monoped_n20", "halfcheetah_n30"]
+CASES = ["pointmass_rest", "monoped_n20", "halfcheetah_n30", "biped_walk"]
 
 
 def _ref_dyn(g, lay):
-    A = sp.csc_matrix((g["csc_A_data"], g["csc_A_indices"], g["csc_A_indptr"]), shape=tuple(g["csc_A_shape"]))
-    n_dyn = int(g["csc_n_dyn_rows"])
+    # csc_* (make_golden.py) and sp0_* (make_golden_subproblem.py) are the same reference
+    # build_subproblem call (initial guess, delta = 1); biped_walk carries only sp0_*
+    t = "csc" if "csc_A_data" in g else "sp0"
+    A = sp.csc_matrix((g[f"{t}_A_data"], g[f"{t}_A_indices"], g[f"{t}_A_indptr"]), shape=tuple(g[f"{t}_A_shape"]))
+    n_dyn = (lay.N - 1) * lay.n_xt
     Ad = A[:n_dyn, :].tocsc()
     Ad.sort_indices()
     return A, Ad, n_dyn
@@ -74,7 +77,7 @@ def test_gpu_scatter_values_match_reference(name):
     torch.cuda.synchronize()
     assert int(mm.item()) == 0
     assert rel_err(data.cpu().numpy(), Ad.data) <= 1e-9
-    assert rel_err(b.cpu().numpy(), g["csc_b"][:n_dyn]) <= 1e-9
+    assert rel_err(b.cpu().numpy(), g["csc_b" if "csc_b" in g else "sp0_b"][:n_dyn]) <= 1e-9
     # and straight into the reference's full A.data (other rows untouched)
     sx, su, ss = DynamicsCSC.slots_into(A.indptr, A.indices, lay)
     scat.set_slots(sx, su, ss)

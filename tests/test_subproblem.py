@@ -10,7 +10,7 @@ import scipy.sparse as sp
 
 from conftest import golden_scenario, load_golden, rel_err
 
-CASES = ["pointmass_rest", "monoped_n20", "halfcheetah_n30"]
+CASES = ["pointmass_rest", "monoped_n20", "halfcheetah_n30", "biped_walk"]
 TAGS = ["sp0", "sp1", "sp2"]
 
 
@@ -176,8 +176,10 @@ def test_gpu_scp_step_all_models_match_reference(name):
 def test_csc_direct_equals_scipy_constructor():
     """GpuSCPStep's direct csc_matrix construction (no per-call constructor checks)
     gives the same matrix object state as scipy's constructor and a valid format."""
+    import paper_2604_09993_b200.subproblem as SPB
     from paper_2604_09993_b200.subproblem import _csc_direct
 
+    SPB._CSC_FAST = None  # probe again: this test must see the probe call first
     A = sp.random(40, 70, density=0.15, format="csc", random_state=3)
     A.sort_indices()
     d, i, p = A.data.copy(), A.indices.astype(np.int32), A.indptr.astype(np.int32)
@@ -190,3 +192,15 @@ def test_csc_direct_equals_scipy_constructor():
         m.check_format(full_check=True)
         assert (m != A).nnz == 0 and m.has_sorted_indices
         assert np.array_equal(m.toarray(), A.toarray()) and np.allclose(m.T @ np.ones(40), A.T @ np.ones(40))
+
+
+def test_csc_direct_rejects_inconsistent_arrays():
+    from paper_2604_09993_b200.subproblem import _csc_direct
+
+    d, i = np.ones(3), np.array([0, 1, 2], dtype=np.int32)
+    with pytest.raises(RuntimeError):
+        _csc_direct(d, i, np.array([0, 1, 4], dtype=np.int32), (3, 2))  # indptr[-1] != nnz
+    with pytest.raises(RuntimeError):
+        _csc_direct(d, i, np.array([1, 2, 3], dtype=np.int32), (3, 2))  # indptr[0] != 0
+    with pytest.raises(RuntimeError):
+        _csc_direct(d, i.astype(np.int64), np.array([0, 1, 3], dtype=np.int32), (3, 2))
