@@ -39,7 +39,8 @@ extern "C" {
 #define CITO_SURFACE_IMPLICIT 1
 
 /* postfix byte-code of an implicit surface h(px, pz) (cito/multibody.py:144-172);
- * the grammar of the reference: constants, +, *, ** (constant exponent), sin, cos */
+ * the grammar of the reference: constants, +, *, **, sin, cos.  a**b with a
+ * non-constant exponent b is emitted as  b a LOG MUL EXP  (= exp(b log a)). */
 #define CITO_OP_CONST 0 /* push arg */
 #define CITO_OP_PX 1
 #define CITO_OP_PZ 2
@@ -49,6 +50,8 @@ extern "C" {
 #define CITO_OP_SIN 6
 #define CITO_OP_COS 7
 #define CITO_OP_NEG 8
+#define CITO_OP_LOG 9 /* natural log (variable-exponent powers) */
+#define CITO_OP_EXP 10
 
 typedef enum {
   CITO_OK = 0,

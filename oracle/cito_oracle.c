@@ -269,13 +269,21 @@ static taylor2 t2_eval(const cito_model_desc* m, double px, double pz) {
       r.hxz = f1 * a.hxz + f2 * a.gx * a.gz;
       r.hzz = f1 * a.hzz + f2 * a.gz * a.gz;
       st[sp++] = r;
-    } else if (op == CITO_OP_SIN || op == CITO_OP_COS) {
+    } else if (op == CITO_OP_SIN || op == CITO_OP_COS || op == CITO_OP_LOG || op == CITO_OP_EXP) {
       taylor2 a = st[--sp];
       double f0, f1, f2;
       if (op == CITO_OP_SIN) {
         f0 = sin(a.v);
         f1 = cos(a.v);
         f2 = -f0;
+      } else if (op == CITO_OP_LOG) { /* a**b with symbolic b: exp(b log a) */
+        f0 = log(a.v);
+        f1 = 1.0 / a.v;
+        f2 = -f1 * f1;
+      } else if (op == CITO_OP_EXP) {
+        f0 = exp(a.v);
+        f1 = f0;
+        f2 = f0;
       } else {
         f0 = cos(a.v);
         f1 = -sin(a.v);

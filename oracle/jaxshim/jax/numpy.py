@@ -118,8 +118,12 @@ def exp(x):
     return torch.exp(asarray(x))
 
 
+def log(x):
+    return torch.log(asarray(x))
+
+
 def power(a, b):
-    return torch.pow(asarray(a), b)
+    return torch.pow(asarray(a), b if isinstance(b, (int, float)) else asarray(b))
 
 
 class linalg:  # noqa: N801

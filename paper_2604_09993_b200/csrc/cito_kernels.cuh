@@ -23,7 +23,13 @@
 
 #include <cstdint>
 
+// CITO_MODELS_GEN: a single-topology table generated at run time (the JIT build of
+// paper_2604_09993_b200/build.py::build_topology); default: the bundled set
+#ifdef CITO_MODELS_GEN
+#include CITO_MODELS_GEN
+#else
 #include "models_gen.cuh"
+#endif
 
 #ifndef CITO_COL_RC
 #define CITO_COL_RC 18  // rate rows per accumulator chunk of the column stage (register budget)
@@ -156,6 +162,14 @@ __device__ inline T2 surface_t2(const KParams& P, double px, double pz) {
         sincos(a.v, &s, &f0);
         f1 = -s;
         f2 = -f0;
+      } else if (op == 9) {  // log (variable exponent: a**b = exp(b log a))
+        f0 = log(a.v);
+        f1 = 1.0 / a.v;
+        f2 = -f1 * f1;
+      } else if (op == 10) {  // exp
+        f0 = exp(a.v);
+        f1 = f0;
+        f2 = f0;
       } else {
         f0 = -a.v;
         f1 = -1.0;

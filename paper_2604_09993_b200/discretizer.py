@@ -100,11 +100,11 @@ class Discretizer:
         xt0s, Us, Ss, B = self._batch(np.asarray(xt0).reshape(1, -1), np.asarray(U).reshape(1, -1), [float(S)])
         ends = np.empty((1, self.n_xt))
         bad = np.zeros(1, dtype=np.int32)
-        st = _lib.lib().cito_propagate_host(self._h.ptr, 1, xt0s.ctypes.data, Us.ctypes.data, Ss.ctypes.data,
+        st = self._h.L.cito_propagate_host(self._h.ptr, 1, xt0s.ctypes.data, Us.ctypes.data, Ss.ctypes.data,
                                             ends.ctypes.data, bad.ctypes.data)
         if st == _lib.CITO_ERR_NONFINITE:
             raise FloatingPointError("non-finite state during interval integration")
-        _lib.check(st, "propagate")
+        self._h.check(st, "propagate")
         return ends[0]
 
     def propagate_batch(self, xt0s, Us, Ss):
@@ -114,11 +114,11 @@ class Discretizer:
         bad = np.zeros(B, dtype=np.int32)
         if B == 0:
             return ends
-        st = _lib.lib().cito_propagate_host(self._h.ptr, B, xt0s.ctypes.data, Us.ctypes.data, Ss.ctypes.data,
+        st = self._h.L.cito_propagate_host(self._h.ptr, B, xt0s.ctypes.data, Us.ctypes.data, Ss.ctypes.data,
                                             ends.ctypes.data, bad.ctypes.data)
         if st == _lib.CITO_ERR_NONFINITE:
             raise FloatingPointError(f"non-finite state in intervals {np.where(bad != 0)[0].tolist()}")
-        _lib.check(st, "propagate_batch")
+        self._h.check(st, "propagate_batch")
         return ends
 
     def linearize_batch(self, xt0s, Us, Ss, out=None):
@@ -144,13 +144,13 @@ class Discretizer:
         bad = np.zeros(B, dtype=np.int32)
         if B == 0:
             return ends, jx, ju, js
-        st = _lib.lib().cito_linearize_host(self._h.ptr, B, xt0s.ctypes.data, Us.ctypes.data, Ss.ctypes.data,
+        st = self._h.L.cito_linearize_host(self._h.ptr, B, xt0s.ctypes.data, Us.ctypes.data, Ss.ctypes.data,
                                             ends.ctypes.data, jx.ctypes.data, ju.ctypes.data, js.ctypes.data,
                                             bad.ctypes.data)
         if st == _lib.CITO_ERR_NONFINITE:
             # the reference raises from its propagate_batch pass (augmentation.py:238 -> :231-233)
             raise FloatingPointError(f"non-finite state in intervals {np.where(bad != 0)[0].tolist()}")
-        _lib.check(st, "linearize_batch")
+        self._h.check(st, "linearize_batch")
         return ends, jx, ju, js
 
     def integrate(self, start, param):
@@ -177,7 +177,7 @@ class Discretizer:
                    torch.empty((B,), dtype=torch.int32, device=dev))
         ends, jx, ju, js, bad = out
         s = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
-        _lib.check(_lib.lib().cito_linearize_dev(self._h.ptr, B, xt0s.data_ptr(), Us.data_ptr(), Ss.data_ptr(),
+        self._h.check(self._h.L.cito_linearize_dev(self._h.ptr, B, xt0s.data_ptr(), Us.data_ptr(), Ss.data_ptr(),
                                                  ends.data_ptr(), jx.data_ptr(), ju.data_ptr(), js.data_ptr(),
                                                  bad.data_ptr(), s), "linearize_dev")
         return out
@@ -192,7 +192,7 @@ class Discretizer:
                    torch.empty((B,), dtype=torch.int32, device=dev))
         ends, bad = out
         s = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
-        _lib.check(_lib.lib().cito_propagate_dev(self._h.ptr, B, xt0s.data_ptr(), Us.data_ptr(), Ss.data_ptr(),
+        self._h.check(self._h.L.cito_propagate_dev(self._h.ptr, B, xt0s.data_ptr(), Us.data_ptr(), Ss.data_ptr(),
                                                  ends.data_ptr(), bad.data_ptr(), s), "propagate_dev")
         return out
 

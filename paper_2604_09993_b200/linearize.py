@@ -124,7 +124,7 @@ class NodeLinearizer:
                    torch.empty((Nn, n_q), **f64), torch.empty((Nn, n_q, 3 * n_q + 2 * n_c), **f64))
         s = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
         yp = y_pairs if Np else theta_vecs
-        _lib.check(_lib.lib().cito_node_linearize_dev(h.ptr, Np, Nn, yp.data_ptr(), theta_vecs.data_ptr(),
+        h.check(h.L.cito_node_linearize_dev(h.ptr, Np, Nn, yp.data_ptr(), theta_vecs.data_ptr(),
                                                       float(delta), float(epsilon),
                                                       *[o.data_ptr() for o in out], s), "node_linearize")
         return out
@@ -221,7 +221,7 @@ class GpuTranscription:
         if k1_events is not None:
             k1_events[0].record(stream)
         o = out
-        _lib.check(_lib.lib().cito_linearize_all_dev(
+        self.disc._h.check(self.disc._h.L.cito_linearize_all_dev(
             self.disc._h.ptr, N, P, int(lay.dim), int(self.base_u), int(self.base_p), z_dev.data_ptr(), float(delta),
             float(epsilon), o["ends"].data_ptr(), o["jx"].data_ptr(), o["ju"].data_ptr(), o["js"].data_ptr(),
             o["defects"].data_ptr(), o["bad"].data_ptr(), o["psi"].data_ptr(), o["psi_jac"].data_ptr(),

@@ -24,7 +24,7 @@ MAX_EXPR = 256
 SURFACE_FLAT = 0
 SURFACE_IMPLICIT = 1
 
-OP_CONST, OP_PX, OP_PZ, OP_ADD, OP_MUL, OP_POW, OP_SIN, OP_COS, OP_NEG = range(9)
+OP_CONST, OP_PX, OP_PZ, OP_ADD, OP_MUL, OP_POW, OP_SIN, OP_COS, OP_NEG, OP_LOG, OP_EXP = range(11)
 
 _d2 = ctypes.c_double * 2
 
@@ -216,10 +216,15 @@ def compile_surface_expression(expression):
                 emit(OP_MUL)
         elif isinstance(e, sympy.Pow):
             base, ex = e.args
-            if not ex.is_Number:
-                raise ValueError(f"surface expression: non-constant exponent in {e}")
-            walk(base)
-            emit(OP_POW, float(ex))
+            if ex.is_Number:
+                walk(base)
+                emit(OP_POW, float(ex))
+            else:  # base**ex = exp(ex * log(base)) (jnp.power for a symbolic exponent)
+                walk(ex)
+                walk(base)
+                emit(OP_LOG)
+                emit(OP_MUL)
+                emit(OP_EXP)
         elif isinstance(e, sympy.sin):
             walk(e.args[0])
             emit(OP_SIN)

@@ -301,6 +301,8 @@ class ShardedMultiStart:
 
         self.group = group
         self.rank, self.world = _world(group)
+        if device is not None and not isinstance(device, int):
+            device = torch.device(device).index
         self.gt = GpuTranscription(scenario, device=device)
         self.device = self.gt.device
         self.P = len(seeds)

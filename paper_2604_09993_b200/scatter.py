@@ -161,7 +161,7 @@ class DynamicsScatter:
 
         self._mismatch.zero_()
         s = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
-        _lib.check(_lib.lib().cito_scatter_dynamics_dev(
+        self.disc._h.check(self.disc._h.L.cito_scatter_dynamics_dev(
             self.disc._h.ptr, self.lay.N - 1, ends.data_ptr(), jx.data_ptr(), ju.data_ptr(), js.data_ptr(),
             z_dev.data_ptr(), self._xp.data_ptr(), self._u.data_ptr(), self._s.data_ptr(), self._sig_x.data_ptr(),
             self._sig_u.data_ptr(), self.sig_s, self._sx.data_ptr(), self._su.data_ptr(), self._ss.data_ptr(),

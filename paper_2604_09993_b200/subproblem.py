@@ -944,7 +944,8 @@ class GpuSCPStep:
         L = pl["L"]
         s = torch.cuda.current_stream(self.gt.device).cuda_stream
         pl["zde_dev"].copy_(pl["zde_pin"], non_blocking=True)
-        _lib.check(L.cito_linearize_all_dev2(*pl["lin_args"], *pl["lin_outs"], s), "linearize_all")
+        h = self.gt.disc._h  # the handle's own library (a run-time compiled topology has its own)
+        h.check(h.L.cito_linearize_all_dev2(*pl["lin_args"], *pl["lin_outs"], s), "linearize_all")
         if precondition:
             pl["rowmax"].zero_()
         # b/h of the linearized rows on a side stream, concurrently with the CSC compaction
@@ -1016,10 +1017,10 @@ class GpuSCPStep:
             nnz = int(hb.h[f"{M}_indptr"][-1])
             hb.caps[M] = min(pl["pk"].layout[f"{M}_data"][2], nnz + nnz // 4 + 4096)
         g = torch.cuda.CUDAGraph()
-        n0 = int(pl["L"].cito_launch_count(None))
+        n0 = _lib.launch_count()
         with torch.cuda.graph(g):
             self._launch(precondition, hb)
-        pl["graph_kernels"][precondition] = int(pl["L"].cito_launch_count(None)) - n0
+        pl["graph_kernels"][precondition] = _lib.launch_count() - n0
         hb.graphs[precondition] = g
         return g
 

@@ -53,3 +53,20 @@ def key_from_desc(desc):
 
 def compiled_keys():
     return {key_from_parts(*e[1:]): e[0] for e in COMPILED}
+
+
+def entry_from_desc(desc, name=None):
+    """A COMPILED-style entry for the topology of a packed model (any RobotModel
+    within the kernel limits): what the JIT build (build.build_topology) compiles
+    when the bundled library does not carry it."""
+    import hashlib
+
+    joints = tuple((int(desc.joint_parent[j]), int(desc.joint_child[j]), int(desc.joint_actuated[j]))
+                   for j in range(desc.n_joints))
+    contacts = tuple(int(desc.contact_link[i]) for i in range(desc.n_contacts))
+    jl = tuple(int(desc.jl_joint[k]) for k in range(desc.n_joint_limits))
+    hb = tuple(int(desc.hb_link[k]) for k in range(desc.n_height_bounds))
+    key = key_from_desc(desc)
+    if name is None:
+        name = "jit_" + hashlib.sha1(key.encode()).hexdigest()[:12]
+    return (name, int(desc.n_links), joints, contacts, desc.surface_kind == 1, int(desc.n_g_out), jl, hb), key

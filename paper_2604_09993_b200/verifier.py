@@ -75,7 +75,7 @@ class ReplayAuditor:
         cj = torch.empty((B, max(1, 2 * n_j)), **f64)
         om = torch.empty((B, max(1, lay.n_y)), **f64)
         s = torch.cuda.current_stream(self.device).cuda_stream
-        _lib.check(_lib.lib().cito_audit_dev(self.nominal._h.ptr, B, xs.data_ptr(), int(xs.stride(0)), us.data_ptr(),
+        self.nominal._h.check(self.nominal._h.L.cito_audit_dev(self.nominal._h.ptr, B, xs.data_ptr(), int(xs.stride(0)), us.data_ptr(),
                                              sds.data_ptr(), cj.data_ptr(), om.data_ptr(), s), "audit")
         return sds[:, : lay.n_c], cj[:, : 2 * n_j], om[:, : lay.n_y]
 

@@ -72,8 +72,10 @@ def test_recipes_reproduce_reference_csc_n200():
 
 
 @pytest.mark.gpu
-def test_gpu_linearize_all_n200_vs_oracle():
-    """K1 (199 intervals, 8 substeps) + K3 at the reference's initial guess, per interval."""
+def test_gpu_linearize_all_n200_vs_golden():
+    """K1 (199 intervals, 8 substeps; golden: oracle) + K3 (golden: the reference's own
+    node Jacobians, whose rounding residues the exact-zero pattern must reproduce) at
+    the reference's initial guess, per interval / node."""
     import torch
 
     from paper_2604_09993_b200.linearize import GpuTranscription

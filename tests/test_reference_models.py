@@ -239,9 +239,13 @@ def test_ind_directional_fd_pointmass_rest():
         assert rel_err((fp - fm) / (2 * h), pred) <= 1e-5
 
 
-def test_unsupported_topology_fails_loudly():
+def test_unsupported_topology_fails_loudly(monkeypatch):
+    """With the run-time topology build switched off (CITO_JIT=0) a topology outside
+    the bundled library raises instead of silently falling back."""
     from paper_2604_09993_b200 import Discretizer
     from paper_2604_09993_b200._lib import UnsupportedModelError
+
+    monkeypatch.setenv("CITO_JIT", "0")
 
     link = LinkSpec(mass=1.0, inertia=0.1)
     m = RobotModel(links=(link, link, link), joints=(JointSpec(-1, 0, (0, 0), (0, 0)), JointSpec(0, 1, (0, 0), (0, 0)),
