@@ -233,6 +233,25 @@ cito_status cito_csc_assemble2_dev(int32_t nmat, int32_t ncols, const int64_t* c
                                    int32_t* const* out_rows, double* const* out_vals,
                                    unsigned long long* const* rowmax, void* stream);
 
+/* Packed form of cito_csc_assemble2_dev (the default of the Python layer): one
+ * 16-byte record per superset entry, {double w; uint32 key; int32 row}, sorted by
+ * (column, row): key = (src + 1) << 27 | idx (idx < 2^27); src < 0 -> constant
+ * value w, else value = lin[src][idx] * w with w = sign * sigma[col] (sign = +-1,
+ * which makes it bit-identical to (sign * lin) * sigma).  Entries are processed in
+ * flat tiles of 2048 (one CTA each): ntile[m] >= max(1, ceil(nsup[m] / 2048))
+ * tiles, tcol[m] (device int32[ntile + 1]) = first column whose first superset
+ * entry lies in tile t (searchsorted(sp_ptr, 2048 t)), ncols + 1 at the end.
+ * ws: device uint32 workspace of ws_words >= 4 + 2 * (sum of ntile) words,
+ * zero before the first call; the kernel leaves it zero (zero it again after a
+ * call that returned CITO_ERR_CUDA).  Pointer arguments except ws, lin (host
+ * array of 10 device pointers) and the host arrays nsup/ntile are host arrays of
+ * nmat device pointers. */
+cito_status cito_csc_assemble_packed_dev(int32_t nmat, int32_t ncols, const void* const* ent, const int64_t* nsup,
+                                        const int64_t* const* sp_ptr, const int32_t* const* tcol, const int32_t* ntile,
+                                        const double* const* lin, uint32_t* ws, int64_t ws_words,
+                                        int32_t* const* out_ptr, int32_t* const* out_rows, double* const* out_vals,
+                                        unsigned long long* const* rowmax, void* stream);
+
 /* b / h of the linearized rows: out[rows[i]] = form ? J.z[cols] - v : v - J.z[cols]
  * with J split in up to 3 segments (seg_src < 0 = unused), v = lin[vsrc[i]][voff[i]]. */
 cito_status cito_rhs_dev(int64_t nrows, const int32_t* rows, const int8_t* form, const int8_t* vsrc,

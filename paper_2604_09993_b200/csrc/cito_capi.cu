@@ -74,24 +74,33 @@ static int k1_version() {
   return v;
 }
 
+// Opt a kernel into `bytes` of dynamic shared memory once; false if the device
+// cannot give a CTA that much (large topologies: the multi-interval batch
+// variants are then skipped).
+template <class K>
+static bool smem_ok(K kernel, size_t bytes) {
+  static int optin = -1;
+  if (optin < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  }
+  if (bytes > (size_t)optin) return false;
+  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) == cudaSuccess;
+}
+
 template <class M>
 cito_status launch_linearize(const KParams& P, int64_t B, const double* xt0s, const double* Us, const double* Ss,
                              double* ends, double* jx, double* ju, double* js, int32_t* bad, cudaStream_t st,
                              ZSrc zs) {
   if (B <= 0) return CITO_OK;
-  static bool attr_done = false;
   const size_t smem1 = sizeof(FusedShared<M>), smem2 = sizeof(Fused2Shared<M>);
-  if (!attr_done) {
-    CUDA_TRY(cudaFuncSetAttribute(k_linearize<M, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1));
-    CUDA_TRY(cudaFuncSetAttribute(k_linearize<M, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1));
-    CUDA_TRY(cudaFuncSetAttribute(k_linearize<M, 1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(2 * ((smem1 + 127) / 128 * 128))));
-    CUDA_TRY(cudaFuncSetAttribute(k_linearize<M, 1, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(3 * ((smem1 + 127) / 128 * 128))));
-    CUDA_TRY(cudaFuncSetAttribute(k_linearize2<M, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
-    CUDA_TRY(cudaFuncSetAttribute(k_linearize2<M, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
-    attr_done = true;
-  }
+  const size_t sm1r = (smem1 + 127) / 128 * 128;
+  // which variants fit this topology's shared-memory footprint (decided once per topology)
+  static const bool ok_b1 = smem_ok(k_linearize<M, 1>, smem1), ok_b3 = smem_ok(k_linearize<M, 3>, smem1);
+  static const bool ok_l2 = smem_ok(k_linearize<M, 1, 2>, 2 * sm1r), ok_l3 = smem_ok(k_linearize<M, 1, 3>, 3 * sm1r);
+  static const bool ok_v2 = smem_ok(k_linearize2<M, 1>, smem2), ok_v22 = smem_ok(k_linearize2<M, 2>, smem2);
+  if (!ok_b1 && !ok_v2) return fail(CITO_ERR_UNSUPPORTED, "topology needs more shared memory than a CTA can have");
   // latency variant (full register budget) while the grid fits the SMs once,
   // occupancy variant for large batches
   int dev = 0, sms = 148;
@@ -104,8 +113,8 @@ cito_status launch_linearize(const KParams& P, int64_t B, const double* xt0s, co
   // crossover 96..120 intervals on 148 SMs: instruction fetch)
   static const int64_t lat_max = getenv("CITO_K1_LAT_MAX") ? atoll(getenv("CITO_K1_LAT_MAX")) : -1;
   const int64_t lmax = lat_max >= 0 ? lat_max : (2 * (int64_t)sms) / 3;
-  if (ver == 2 || (ver == 0 && B <= lmax)) {
-    if (B <= sms)
+  if (ok_v2 && (ver == 2 || (ver == 0 && B <= lmax) || !ok_b1)) {
+    if (B <= sms || !ok_v22)
       k_linearize2<M, 1><<<(unsigned)B, K2Dims<M>::NT, smem2, st>>>(P, B, xt0s, Us, Ss, ends, jx, ju, js, bad, zs);
     else
       k_linearize2<M, 2><<<(unsigned)B, K2Dims<M>::NT, smem2, st>>>(P, B, xt0s, Us, Ss, ends, jx, ju, js, bad, zs);
@@ -119,11 +128,11 @@ cito_status launch_linearize(const KParams& P, int64_t B, const double* xt0s, co
     // (measured crossover with three per CTA at 245..250 intervals on 148 SMs)
     static const int64_t ipc2_env = getenv("CITO_K1_IPC2_MAX") ? atoll(getenv("CITO_K1_IPC2_MAX")) : -1;
     const int64_t ipc2_max = ipc2_env >= 0 ? ipc2_env : (5 * (int64_t)sms) / 3;
-    if (ipc3 && B <= ipc2_max)
-      k_linearize<M, 1, 2><<<(unsigned)((B + 1) / 2), 2 * FusedDims<M>::NT, 2 * ((smem1 + 127) / 128 * 128), st>>>(
+    if (ipc3 && ok_l2 && (B <= ipc2_max || !ok_l3))
+      k_linearize<M, 1, 2><<<(unsigned)((B + 1) / 2), 2 * FusedDims<M>::NT, 2 * sm1r, st>>>(
           P, B, xt0s, Us, Ss, ends, jx, ju, js, bad, zs);
-    else if (ipc3)
-      k_linearize<M, 1, 3><<<(unsigned)((B + 2) / 3), 3 * FusedDims<M>::NT, 3 * ((smem1 + 127) / 128 * 128), st>>>(
+    else if (ipc3 && ok_l3)
+      k_linearize<M, 1, 3><<<(unsigned)((B + 2) / 3), 3 * FusedDims<M>::NT, 3 * sm1r, st>>>(
           P, B, xt0s, Us, Ss, ends, jx, ju, js, bad, zs);
     else
       k_linearize<M, 3><<<(unsigned)B, FusedDims<M>::NT, smem1, st>>>(P, B, xt0s, Us, Ss, ends, jx, ju, js, bad, zs);
@@ -143,13 +152,9 @@ cito_status launch_propagate(const KParams& P, int64_t B, const double* xt0s, co
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   count_launch();
-  if (B <= sms && k1_version() != 1) {
-    static bool attr_done = false;
-    const size_t smem = sizeof(Fused2Shared<M>);
-    if (!attr_done) {
-      CUDA_TRY(cudaFuncSetAttribute(k_linearize2<M, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr_done = true;
-    }
+  const size_t smem = sizeof(Fused2Shared<M>);
+  static const bool ok_pair = smem_ok(k_linearize2<M, 1, false>, smem);
+  if (B <= sms && k1_version() != 1 && ok_pair) {
     k_linearize2<M, 1, false><<<(unsigned)B, 64, smem, st>>>(P, B, xt0s, Us, Ss, ends, nullptr, nullptr, nullptr, bad,
                                                              ZSrc{});
   } else {
@@ -664,6 +669,39 @@ cito_status cito_csc_assemble2_dev(int32_t nmat, int32_t ncols, const int64_t* c
   }
   count_launch(1);
   k_csc_onepass<<<dim3(nb, nmat), 256, 0, s>>>(ncols, ca, sigma, L);
+  CUDA_TRY(cudaGetLastError());
+  return CITO_OK;
+}
+
+cito_status cito_csc_assemble_packed_dev(int32_t nmat, int32_t ncols, const void* const* ent, const int64_t* nsup,
+                                        const int64_t* const* sp_ptr, const int32_t* const* tcol, const int32_t* ntile,
+                                        const double* const* lin, uint32_t* ws, int64_t ws_words,
+                                        int32_t* const* out_ptr, int32_t* const* out_rows, double* const* out_vals,
+                                        unsigned long long* const* rowmax, void* stream) {
+  if (nmat < 1 || nmat > 2 || ncols < 0 || !ent || !nsup || !sp_ptr || !tcol || !ntile || !ws)
+    return fail(CITO_ERR_ARG, "csc_assemble_packed: bad arguments");
+  CscPackedArgs a;
+  int64_t tiles = 0;
+  for (int m = 0; m < 2; ++m) {
+    const bool on = m < nmat;
+    a.ent[m] = on ? (const CscEnt*)ent[m] : nullptr;
+    a.nsup[m] = on ? nsup[m] : 0;
+    a.sp_ptr[m] = on ? sp_ptr[m] : nullptr;
+    a.tcol[m] = on ? tcol[m] : nullptr;
+    a.ntile[m] = on ? ntile[m] : 0;
+    a.out_ptr[m] = on ? out_ptr[m] : nullptr;
+    a.out_rows[m] = on ? out_rows[m] : nullptr;
+    a.out_vals[m] = on ? out_vals[m] : nullptr;
+    a.rowmax[m] = (on && rowmax) ? rowmax[m] : nullptr;
+    if (on && (ntile[m] < 1 || (int64_t)ntile[m] * CSC_TILE < nsup[m] || nsup[m] >= (1ll << 27)))
+      return fail(CITO_ERR_ARG, "csc_assemble_packed: tile count does not cover the entries");
+    tiles += on ? ntile[m] : 0;
+  }
+  if (ws_words < CSC_HDR_WORDS + 2 * tiles) return fail(CITO_ERR_ARG, "csc_assemble_packed: workspace too small");
+  LinTable L;
+  for (int k = 0; k < 10; ++k) L.p[k] = lin ? lin[k] : nullptr;
+  count_launch(1);
+  k_csc_flat<<<(unsigned)tiles, 256, 0, (cudaStream_t)stream>>>(ncols, a, L, ws);
   CUDA_TRY(cudaGetLastError());
   return CITO_OK;
 }

@@ -19,6 +19,16 @@ struct LinTable {
   const double* p[10];  // jx, ju, js, imp_jac, theta_jac, psi_jac, ends, imp_v, theta, psi
 };
 
+// L.p[s] without indexing the parameter array dynamically (which would copy the
+// table to local memory): selects between the 10 kernel-parameter pointers
+__device__ __forceinline__ const double* lin_ptr(const LinTable& L, int s) {
+  const double* p = L.p[0];
+#pragma unroll
+  for (int k = 1; k < 10; ++k)
+    if (s == k) p = L.p[k];
+  return p;
+}
+
 __device__ __forceinline__ double sp_value(int64_t e, double sig, const int8_t* __restrict__ src,
                                            const int64_t* __restrict__ idx, const double* __restrict__ val,
                                            const LinTable& L) {
@@ -356,6 +366,168 @@ __global__ void __launch_bounds__(256) k_csc_onepass(int32_t ncols, const CscArg
       }
       base += __popc(msk);
     }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Entry-parallel compaction (default since round 2): the superset entries of A and
+// G are processed as flat tiles of CSC_TILE = 256 x CSC_TJ entries, one CTA per tile,
+// instead of a warp per column (A has ~20 superset entries per column, G ~3, so a
+// warp per column idles most lanes and serialises dependent loads).
+//   record  CscEnt {w, key, row} (16 B, one vector load): key = (src + 1) << 27 | idx;
+//           src < 0: constant value w; else value = lin[src][idx] * w with
+//           w = val * sigma[col] folded on the host (val = +-1 for every linearized
+//           entry, so lin * (val sigma) == (val lin) sigma bit for bit)
+//   flags   one ballot per (stage j, warp) -> 64 masks in smem; one warp scans the
+//           64 popcounts: offsets of every entry inside the tile; the tile total is
+//           published and summed by the following tiles (decoupled look-back over
+//           ticket-ordered tiles, as in k_csc_onepass)
+//   indptr  the columns whose first superset entry lies in the tile (tcol[t] ..
+//           tcol[t+1]) read their offset from the masks: no per-column pass at all
+// Workspace ws: [ticket, finished CTAs, pad, pad] + one uint64 flag per tile, zero
+// before the first launch; the last CTA returns it to zero.
+#define CSC_TJ 8
+#define CSC_TILE (256 * CSC_TJ)
+
+struct __align__(16) CscEnt {
+  double w;
+  uint32_t key;
+  int32_t row;
+};
+
+struct CscPackedArgs {
+  const CscEnt* ent[2];
+  int64_t nsup[2];
+  const int64_t* sp_ptr[2];
+  const int32_t* tcol[2];  // ntile + 1 entries: first column owned by each tile, ncols + 1 at the end
+  int32_t ntile[2];
+  int32_t* out_ptr[2];
+  int32_t* out_rows[2];
+  double* out_vals[2];
+  unsigned long long* rowmax[2];
+};
+
+__global__ void __launch_bounds__(256) k_csc_flat(int32_t ncols, const CscPackedArgs a, const LinTable L,
+                                                  unsigned* __restrict__ ws) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int ntiles = a.ntile[0] + a.ntile[1];
+  unsigned long long* flags = reinterpret_cast<unsigned long long*>(ws + CSC_HDR_WORDS);
+  __shared__ int tile_s, last_s, tbase_s, ttot_s;
+  __shared__ unsigned masks[CSC_TJ][8];
+  __shared__ int base[CSC_TJ][8];
+  __shared__ int red[8];
+  if (tid == 0) tile_s = (int)atomicAdd(&ws[0], 1u);
+  __syncthreads();
+  const int tile = tile_s;
+  const int m = tile < a.ntile[0] ? 0 : 1;
+  const int t0 = m ? a.ntile[0] : 0, lt = tile - t0;
+  const int64_t e0 = (int64_t)lt * CSC_TILE, nsup = a.nsup[m];
+  const CscEnt* __restrict__ ent = a.ent[m];
+  // evaluate the tile's entries: record loads first (all in flight), then the lin loads
+  uint32_t key[CSC_TJ];
+  int32_t row[CSC_TJ];
+  double v[CSC_TJ];
+#pragma unroll
+  for (int j = 0; j < CSC_TJ; ++j) {
+    const int64_t e = e0 + j * 256 + tid;
+    if (e < nsup) {
+      const CscEnt r = ent[e];
+      v[j] = r.w;
+      key[j] = r.key;
+      row[j] = r.row;
+    } else {
+      v[j] = 0.0;
+      key[j] = 0u;
+      row[j] = 0;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < CSC_TJ; ++j) {
+    const int s = (int)(key[j] >> 27) - 1;
+    if (s >= 0) v[j] = lin_ptr(L, s)[key[j] & 0x7ffffffu] * v[j];
+  }
+#pragma unroll
+  for (int j = 0; j < CSC_TJ; ++j) {
+    const unsigned mk = __ballot_sync(0xffffffffu, v[j] != 0.0);
+    if (lane == 0) masks[j][warp] = mk;
+  }
+  __syncthreads();
+  if (warp == 0) {  // exclusive scan of the 64 (j, warp) popcounts in entry order
+    const int i0 = 2 * lane, i1 = 2 * lane + 1;
+    const int c0 = __popc(masks[i0 >> 3][i0 & 7]), c1 = __popc(masks[i1 >> 3][i1 & 7]);
+    int incl = c0 + c1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const int ex = incl - c0 - c1;
+    base[i0 >> 3][i0 & 7] = ex;
+    base[i1 >> 3][i1 & 7] = ex + c0;
+    if (lane == 31) {
+      ttot_s = incl;
+      atomicExch(&flags[tile], (1ull << 32) | (unsigned)incl);  // publish the tile total
+    }
+  }
+  // look-back: totals of the preceding tiles of this matrix (ticket order: all started earlier)
+  int pre = 0;
+  for (int j = t0 + tid; j < tile; j += blockDim.x) {
+    unsigned long long f;
+    do {
+      f = *((volatile unsigned long long*)&flags[j]);
+    } while ((f >> 32) == 0ull);
+    pre += (int)(unsigned)(f & 0xffffffffull);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
+  if (lane == 0) red[warp] = pre;
+  __syncthreads();
+  if (tid == 0) {
+    int t = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += red[w];
+    tbase_s = t;
+    __threadfence();
+    last_s = atomicAdd(&ws[1], 1u) == (unsigned)ntiles - 1u;
+  }
+  __syncthreads();
+  if (last_s) {  // every CTA is past its look-back: clean the workspace for the next launch
+    for (int j = tid; j < ntiles; j += blockDim.x) flags[j] = 0ull;
+    if (tid == 0) {
+      ws[0] = 0u;
+      ws[1] = 0u;
+    }
+    __threadfence();
+  }
+  const int tb = tbase_s;
+  const unsigned ltm = (1u << lane) - 1u;
+  int32_t* __restrict__ orow = a.out_rows[m];
+  double* __restrict__ oval = a.out_vals[m];
+  unsigned long long* rmax = a.rowmax[m];
+#pragma unroll
+  for (int j = 0; j < CSC_TJ; ++j) {
+    if (v[j] != 0.0) {
+      const int pos = tb + base[j][warp] + __popc(masks[j][warp] & ltm);
+      orow[pos] = row[j];
+      oval[pos] = v[j];
+      // fused row inf-norm (cito/conic.py:281-287): non-negative doubles order like their bits
+      if (rmax) atomicMax(&rmax[row[j]], (unsigned long long)__double_as_longlong(fabs(v[j])));
+    }
+  }
+  // indptr of the columns whose first superset entry lies in this tile
+  const int64_t* __restrict__ sp = a.sp_ptr[m];
+  const int c_lo = a.tcol[m][lt], c_hi = a.tcol[m][lt + 1];
+  const int64_t nin = nsup - e0 < CSC_TILE ? nsup - e0 : CSC_TILE;
+  for (int c = c_lo + tid; c < c_hi && c <= ncols; c += blockDim.x) {
+    const int64_t l = sp[c] - e0;
+    int cnt;
+    if (l >= nin) {
+      cnt = ttot_s;
+    } else {
+      const int j = (int)(l >> 8), r = (int)(l & 255), w = r >> 5, ln = r & 31;
+      cnt = base[j][w] + __popc(masks[j][w] & ((1u << ln) - 1u));
+    }
+    a.out_ptr[m][c] = tb + cnt;
   }
 }
 

@@ -462,6 +462,28 @@ class ConicProgram:
 
 _CSC_FAST = None  # None: not probed yet; else (maxprint,) when the direct construction is valid
 _CSC_CHECK = os.environ.get("CITO_CHECK_CSC", "0") == "1"
+_CSC_RECIPES = os.environ.get("CITO_CSC_RECIPES", "0") == "1"  # A/B switch: warp-per-column compaction
+
+
+def packed_entries(csc, sigma):
+    """16-byte records {w, key, row} of a superset CSC for k_csc_flat (include/cito_b200.h,
+    cito_csc_assemble_packed_dev) and the first column owned by each 2048-entry tile."""
+    src = csc["src"].astype(np.int64)
+    idx = np.asarray(csc["idx"], dtype=np.int64)
+    val = np.asarray(csc["val"], dtype=np.float64)
+    col = np.asarray(csc["col"], dtype=np.int64)
+    lin = src >= 0
+    if np.any(np.abs(val[lin]) != 1.0):
+        raise RuntimeError("packed CSC records need sign-only recipes for the linearized entries")
+    if idx.size and (idx.max() >= (1 << 27) or idx.min() < 0):
+        raise RuntimeError("lin index outside the 27-bit key range")
+    rec = np.zeros(src.size, dtype=np.dtype([("w", "<f8"), ("key", "<u4"), ("row", "<i4")]))
+    rec["w"] = np.where(lin, val * sigma[col], val)
+    rec["key"] = (((src + 1) << 27) | np.where(lin, idx, 0)).astype(np.uint32)
+    rec["row"] = csc["row"]
+    ntile = max(1, -(-src.size // 2048))
+    tcol = np.searchsorted(csc["indptr"], np.arange(ntile, dtype=np.int64) * 2048, side="left")
+    return rec, np.concatenate([tcol, [len(csc["indptr"])]]).astype(np.int32)
 
 
 def _csc_direct(data, indices, indptr, shape):
@@ -529,6 +551,9 @@ class SubproblemAssembler:
             # block totals / per-column counts; the one-pass compaction keeps tagged block
             # totals and its launch epoch here across calls, so it starts zeroed
             d["counts"] = torch.zeros(pattern.n + 64, dtype=torch.int32, device=device)
+            # packed 16-byte records of the entry-parallel compaction (k_csc_flat)
+            rec, tcol = packed_entries(csc, pattern.sigma_full())
+            d.update(ent=t(rec.view(np.uint8), np.uint8), tcol=t(tcol, np.int32), ntile=len(tcol) - 1)
             # rhs descriptors of the linearized rows
             nr = len(rows)
             r_row = np.array([r[0] for r in rows], dtype=np.int32)
@@ -554,6 +579,26 @@ class SubproblemAssembler:
                      seg_len=t(seg_len, np.int32), seg_cb=t(seg_cb, np.int64),
                      cols=t(np.concatenate(cols) if cols else np.zeros(1), np.int64))
             self._mats[M] = d
+
+    def packed_args(self, lin_ptrs, outs, rowmax, arr):
+        """Argument tuple of cito_csc_assemble_packed_dev for A and G (without the
+        stream); `outs` = [(indptr, indices, data)] per matrix, `arr` builds a
+        ctypes pointer table from tensors."""
+        import ctypes
+
+        import torch
+
+        mats = [self._mats["A"], self._mats["G"]]
+        if getattr(self, "_ws", None) is None:
+            tiles = sum(d["ntile"] for d in mats)
+            self._ws = torch.zeros(4 + 2 * tiles, dtype=torch.int32, device=self.device)
+            self._nsup = (ctypes.c_int64 * 2)(*[d["nsup"] for d in mats])
+            self._ntile = (ctypes.c_int32 * 2)(*[d["ntile"] for d in mats])
+        return (2, self.pat.n, arr([d["ent"] for d in mats]), ctypes.cast(self._nsup, ctypes.c_void_p),
+                arr([d["sp_ptr"] for d in mats]), arr([d["tcol"] for d in mats]),
+                ctypes.cast(self._ntile, ctypes.c_void_p), lin_ptrs, self._ws.data_ptr(), self._ws.numel(),
+                arr([o[0] for o in outs]), arr([o[1] for o in outs]), arr([o[2] for o in outs]),
+                arr(rowmax) if rowmax else None)
 
     def _prepare_batched(self):
         """Concatenate the rhs descriptors of A and G (one launch) and allocate
@@ -640,12 +685,16 @@ class SubproblemAssembler:
                 r["n"], r["rows"].data_ptr(), r["form"].data_ptr(), r["vsrc"].data_ptr(), r["voff"].data_ptr(),
                 r["seg_src"].data_ptr(), r["seg_off"].data_ptr(), r["seg_len"].data_ptr(), r["seg_cb"].data_ptr(),
                 r["cols"].data_ptr(), z_ref_dev.data_ptr(), ptrs, rhs.data_ptr(), side.cuda_stream), "rhs")
-        _lib.check(_lib.lib().cito_csc_assemble2_dev(
-            2, self.pat.n, arr([d["sp_ptr"] for d in mats]), arr([d["row"] for d in mats]),
-            arr([d["src"] for d in mats]), arr([d["idx"] for d in mats]), arr([d["val"] for d in mats]),
-            self.sigma_dev.data_ptr(), ptrs, arr([d["counts"] for d in mats]), arr([o[0] for o in outs]),
-            arr([o[1] for o in outs]), arr([o[2] for o in outs]), arr(rowmax) if rowmax else None, s),
-            "csc_assemble")
+        if _CSC_RECIPES:  # A/B: the warp-per-column recipe-table form
+            _lib.check(_lib.lib().cito_csc_assemble2_dev(
+                2, self.pat.n, arr([d["sp_ptr"] for d in mats]), arr([d["row"] for d in mats]),
+                arr([d["src"] for d in mats]), arr([d["idx"] for d in mats]), arr([d["val"] for d in mats]),
+                self.sigma_dev.data_ptr(), ptrs, arr([d["counts"] for d in mats]), arr([o[0] for o in outs]),
+                arr([o[1] for o in outs]), arr([o[2] for o in outs]), arr(rowmax) if rowmax else None, s),
+                "csc_assemble")
+        else:
+            _lib.check(_lib.lib().cito_csc_assemble_packed_dev(*self.packed_args(ptrs, outs, rowmax, arr), s),
+                       "csc_assemble")
         cur.wait_stream(side)
         if owned is None:
             rhs.record_stream(cur)
@@ -909,6 +958,12 @@ class GpuSCPStep:
                     k(arr([d["counts"] for d in mats])), k(arr([pk.d["A_indptr"], pk.d["G_indptr"]])),
                     k(arr([pk.d["A_indices"], pk.d["G_indices"]])), k(arr([pk.d["A_data"], pk.d["G_data"]])))
         rm_arr = k(arr([rowmax[:nA], rowmax[nA:]]))
+        outs = [(pk.d["A_indptr"], pk.d["A_indices"], pk.d["A_data"]), (pk.d["G_indptr"], pk.d["G_indices"],
+                                                                       pk.d["G_data"])]
+        packed = tuple(k(a) if a is not None and not isinstance(a, int) else a
+                       for a in asm.packed_args(lin_ptrs, outs, None, arr))
+        packed_pc = tuple(k(a) if a is not None and not isinstance(a, int) else a
+                          for a in asm.packed_args(lin_ptrs, outs, [rowmax[:nA], rowmax[nA:]], arr))
         # b and h: one contiguous vector (rows [0, nA) = b, [nA, nA + nG) = h) in the packed buffer
         rhs_dev = pk.d["rhs"]
         rhs_args = (r["n"], r["rows"].data_ptr(), r["form"].data_ptr(), r["vsrc"].data_ptr(), r["voff"].data_ptr(),
@@ -930,6 +985,7 @@ class GpuSCPStep:
         self._plan = dict(lin=lin, pk=pk, z_dev=z_dev, zde_dev=zde_dev, zde_pin=zde_pin, rowmax=rowmax, rhs_dev=rhs_dev,
                           hosts=[], graph_kernels={}, side=torch.cuda.Stream(dev),
                           rhs_const=r["const"], asm_args=asm_args, rm_arr=rm_arr, rhs_args=rhs_args,
+                          packed=packed, packed_pc=packed_pc,
                           pc_args=pc_args, lin_args=lin_args, lin_outs=lin_outs, keep=keep, L=L, nA=nA, nG=nG,
                           soc=(soc_start, soc_dim), P_idx=P_idx, P_ptr=P_ptr,
                           P_plain=None, meta=_Meta(pat.z_idx, pat.sp_idx, pat.sm_idx, pat.t_idx))
@@ -955,8 +1011,12 @@ class GpuSCPStep:
         with torch.cuda.stream(side):
             pl["rhs_dev"].copy_(pl["rhs_const"])
             _lib.check(L.cito_rhs_dev(*pl["rhs_args"], side.cuda_stream), "rhs")
-        _lib.check(L.cito_csc_assemble2_dev(*pl["asm_args"], pl["rm_arr"] if precondition else None, s),
-                   "csc_assemble")
+        if not _CSC_RECIPES:
+            _lib.check(L.cito_csc_assemble_packed_dev(*(pl["packed_pc"] if precondition else pl["packed"]), s),
+                       "csc_assemble")
+        else:
+            _lib.check(L.cito_csc_assemble2_dev(*pl["asm_args"], pl["rm_arr"] if precondition else None, s),
+                       "csc_assemble")
         cur.wait_stream(side)
         if precondition:
             _lib.check(L.cito_precondition_dev(*pl["pc_args"], s), "precondition")

@@ -12,14 +12,10 @@ sys.path.insert(0, ROOT)
 PROF_SO = os.path.join(ROOT, "paper_2604_09993_b200", "_lib", "libcito_b200_prof.so")
 
 
-def build():
-    from paper_2604_09993_b200 import build as b
-
-    b.build()  # regenerates models_gen.cuh
-    cmd = [b.NVCC, "-std=c++17", "-O3", "-lineinfo", "-gencode", "arch=compute_100a,code=sm_100a", "-DCITO_PROF",
-           "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"),
-           "-o", PROF_SO, os.path.join(b.CSRC, "cito_capi.cu"), "-lcudart"]
-    subprocess.check_call(cmd)
+def build(extra=()):
+    # HalfCheetah-only variant library (tools/variant.py) with the cycle marks compiled in
+    subprocess.check_call([sys.executable, os.path.join(ROOT, "tools", "variant.py"), "prof", "-DCITO_PROF",
+                           *extra])
 
 
 def run(B):
@@ -72,6 +68,6 @@ def run(B):
 
 if __name__ == "__main__":
     if sys.argv[1] == "build":
-        build()
+        build(sys.argv[2:])
     else:
         run(int(sys.argv[2]) if len(sys.argv) > 2 else 29)
