@@ -766,6 +766,59 @@ class SubproblemAssembler:
         return prog, meta
 
 
+_LAZY_TYPES = {}
+
+
+def _lazy_program_type(base):
+    """A subclass of the (reference's) ConicProgram dataclass whose A, b, G, h are
+    read from GpuSCPStep's device copy of the unscaled values on first access."""
+    t = _LAZY_TYPES.get(base)
+    if t is not None:
+        return t
+
+    def _field(name):
+        def get(self):
+            self._materialize()
+            return self._host[name]
+
+        def set_(self, v):
+            self._materialize()
+            self._host[name] = v
+
+        return property(get, set_)
+
+    class LazyProgram(base):
+        @classmethod
+        def _new(cls, step, mats, nA, nG, P, c, cones):
+            o = object.__new__(cls)
+            o.__dict__.update(P=P, c=c, cones=cones, _step=step, _mats=mats, _nA=nA, _nG=nG, _host=None)
+            return o
+
+        def _materialize(self):
+            if self._host is not None:
+                return
+            import scipy.sparse as sp
+            import torch
+
+            u = self._step._plan["unscaled"]
+            h = {}
+            for M in ("A", "G"):
+                ref = self._mats[M]
+                nnz = ref.indices.size
+                vals = u[f"{M}_data"][:nnz].cpu().numpy()
+                h[M] = sp.csc_matrix((vals, ref.indices.copy(), ref.indptr.copy()), shape=ref.shape)
+            rhs = u["rhs"][: self._nA + self._nG].cpu().numpy()
+            torch.cuda.current_stream(self._step.gt.device).synchronize()
+            h["b"], h["h"] = rhs[: self._nA].copy(), rhs[self._nA:].copy()
+            self._host = h
+
+    for name in ("A", "b", "G", "h"):
+        setattr(LazyProgram, name, _field(name))
+    LazyProgram.__name__ = base.__name__
+    _LAZY_TYPES[base] = LazyProgram
+    return LazyProgram
+
+
 def ctypes_ptr_array(ptrs):
     import ctypes
 
@@ -934,6 +987,12 @@ class GpuSCPStep:
                       ("A_data", fd, dA["nsup"]), ("G_data", fd, dG["nsup"]),
                       ("A_indices", i32, dA["nsup"]), ("G_indices", i32, dG["nsup"])], dev)
         lin["bad"] = pk.d["bad"]
+        # the unscaled values of a preconditioned iteration stay on the device (D2D copy
+        # before the row scaling): build_subproblem's program in the install_scp drop-ins
+        # reads them only if a caller looks at it (cito.scp.solve does not)
+        unscaled = dict(A_data=torch.empty(max(1, dA["nsup"]), dtype=fd, device=dev),
+                        G_data=torch.empty(max(1, dG["nsup"]), dtype=fd, device=dev),
+                        rhs=torch.empty(max(1, nA + nG), dtype=fd, device=dev))
         # z followed by [delta, epsilon]: one H2D per call, read by the kernels from device
         # memory so a captured graph replays for any delta of the homotopy
         zde_dev = torch.empty(lay.dim + 2, **f64)
@@ -985,7 +1044,7 @@ class GpuSCPStep:
         self._plan = dict(lin=lin, pk=pk, z_dev=z_dev, zde_dev=zde_dev, zde_pin=zde_pin, rowmax=rowmax, rhs_dev=rhs_dev,
                           hosts=[], graph_kernels={}, side=torch.cuda.Stream(dev),
                           rhs_const=r["const"], asm_args=asm_args, rm_arr=rm_arr, rhs_args=rhs_args,
-                          packed=packed, packed_pc=packed_pc,
+                          packed=packed, packed_pc=packed_pc, unscaled=unscaled,
                           pc_args=pc_args, lin_args=lin_args, lin_outs=lin_outs, keep=keep, L=L, nA=nA, nG=nG,
                           soc=(soc_start, soc_dim), P_idx=P_idx, P_ptr=P_ptr,
                           P_plain=None, meta=_Meta(pat.z_idx, pat.sp_idx, pat.sm_idx, pat.t_idx))
@@ -1019,6 +1078,9 @@ class GpuSCPStep:
                        "csc_assemble")
         cur.wait_stream(side)
         if precondition:
+            u, d = pl["unscaled"], pl["pk"].d
+            for kk in ("A_data", "G_data", "rhs"):
+                u[kk][: d[kk].numel()].copy_(d[kk])
             _lib.check(L.cito_precondition_dev(*pl["pc_args"], s), "precondition")
         self._d2h(hb)
 
@@ -1103,6 +1165,10 @@ class GpuSCPStep:
         prev = self._last_lin() if self._last_lin is not None else None
         if prev is not None and prev.device_arrays() is not None:
             prev.release_device()
+        prev = self._last_unscaled() if getattr(self, "_last_unscaled", None) is not None else None
+        if prev is not None:
+            prev._materialize()  # the device copy of its values is about to be overwritten
+        self._last_unscaled = None
         if epsilon is None:
             epsilon = gt.scenario.ctcs_epsilon
         stream = torch.cuda.current_stream(gt.device)
@@ -1162,5 +1228,34 @@ class GpuSCPStep:
             prec = _preconditioner_type()(row_scale_A=hb.wrap("row_scale_A", 0, nA),
                                           row_scale_G=hb.wrap("row_scale_G", 0, pl["nG"]),
                                           var_scale=np.ones(pat.n), cost_scale=omega)
+            self._pc_parts = (mats, nA, pl["nG"])
             return lin, prog, prec, pl["meta"]
+        self._pc_parts = None
         return lin, prog, pl["meta"]
+
+    def unscaled_program(self, z_j):
+        """The program of the last preconditioned iterate BEFORE row scaling
+        (= cito.scp.build_subproblem's output), lazily: its A/G values and b/h come
+        back from the device copy only when first read (valid until the next
+        iterate, which materializes it first).  P and c (host) are exact."""
+        import weakref
+
+        import scipy.sparse as sp
+
+        if self._pc_parts is None:
+            raise RuntimeError("unscaled_program needs a preceding iterate(..., precondition=True)")
+        mats, nA, nG = self._pc_parts
+        pat = self.asm.pat
+        pl = self._plan
+        if pl["P_plain"] is None:
+            P_data = pat.P_diag[: pat.lay.dim]
+            Pm = sp.csc_matrix((P_data.copy(), pl["P_idx"].copy(), pl["P_ptr"].copy()), shape=(pat.n, pat.n))
+            for arr in (Pm.data, Pm.indices, Pm.indptr):
+                arr.flags.writeable = False
+            pl["P_plain"] = Pm
+        ConicProgram, ConeSpec = _conic_types()
+        prog = _lazy_program_type(ConicProgram)._new(
+            self, mats, nA, nG, P=pl["P_plain"], c=pat.objective_c(z_j),
+            cones=ConeSpec(nonneg=pat.n_orthant, soc=pat.soc_dims))
+        self._last_unscaled = weakref.ref(prog)
+        return prog

@@ -41,7 +41,8 @@ import paper_2604_09993_b200.linearize as G
 import paper_2604_09993_b200.subproblem as SPB
 from paper_2604_09993_b200 import install
 
-name, iters, compare, N, ref_lin = sys.argv[1], int(sys.argv[2]), sys.argv[3] == "1", int(sys.argv[4]), sys.argv[5]
+name, iters, compare, N, ref_lin, mode = (sys.argv[1], int(sys.argv[2]), sys.argv[3] == "1", int(sys.argv[4]),
+                                          sys.argv[5], sys.argv[6])
 sc = ocp.load_scenario(os.path.join(REF, "cito", "assets", name + ".json"))
 if N:
     sc = replace(sc, N=N, s_bounds=None)
@@ -104,30 +105,51 @@ if compare:
 ocp._transcriptions.clear()
 tr = ocp.get_transcription(sc)
 install(tr)                       # tr.discretizer -> GPU (initial_guess uses it)
+import time
 orig = scp.linearize_all, scp.build_subproblem, scp.precondition
-scp.linearize_all = G.linearize_all         # GPU linearize_all (intervals + node relations)
-scp.build_subproblem = SPB.build_subproblem  # GPU subproblem assembly (CSC values, b, h)
-scp.precondition = SPB.precondition          # GPU row scaling of the assembled program
+if mode == "scp":  # one device pass per iteration (paper_2604_09993_b200.scp_dropin)
+    from paper_2604_09993_b200.scp_dropin import install_scp
+    drop = install_scp(scp)
+    fns = (scp.linearize_all, scp.build_subproblem, scp.precondition)
+else:
+    fns = (G.linearize_all,           # GPU linearize_all (intervals + node relations)
+           SPB.build_subproblem,       # GPU subproblem assembly (CSC values, b, h)
+           SPB.precondition)           # GPU row scaling of the assembled program
+pre_ipm = []
+
+
+def timed(f):
+    def w(*a, **k):
+        t0 = time.perf_counter()
+        r = f(*a, **k)
+        pre_ipm.append(time.perf_counter() - t0)
+        return r
+    return w
+
+
+scp.linearize_all, scp.build_subproblem, scp.precondition = (timed(f) for f in fns)
 try:
     z, hist, st = scp.solve(sc, cfg)
 finally:
     scp.linearize_all, scp.build_subproblem, scp.precondition = orig
+out["pre_ipm_ms"] = [1e3 * (pre_ipm[3 * i] + pre_ipm[3 * i + 1] + pre_ipm[3 * i + 2]) for i in range(len(pre_ipm) // 3)]
 out["gpu"] = [h.z.tolist() for h in hist]
 out["gpu_delta"] = [h.delta for h in hist]
 out["gpu_jpx"] = [h.j_px for h in hist]
 out["gpu_jep"] = [h.j_ep for h in hist]
 out["status"] = st
-out["launches"] = tr.discretizer.launch_count() + G._cache[id(tr)][1].disc.launch_count()
+out["launches"] = tr.discretizer.launch_count() + (G._cache[id(tr)][1].disc.launch_count() if mode != "scp"
+                                                   else drop._step(tr).gt.disc.launch_count())
 print("RESULT " + json.dumps(out))
 '''
 
 
-def _run(name, iters, compare, N=0, ref_lin="shim", timeout=1500):
+def _run(name, iters, compare, N=0, ref_lin="shim", mode="three", timeout=1500):
     ref = _ref_src()
     if ref is None:
         pytest.skip("reference package not available (baseline/_ref or /root/reference)")
     code = f"ROOT = {ROOT!r}\nREF = {ref!r}\n" + SCRIPT
-    p = subprocess.run([sys.executable, "-c", code, name, str(iters), "1" if compare else "0", str(N), ref_lin], capture_output=True,
+    p = subprocess.run([sys.executable, "-c", code, name, str(iters), "1" if compare else "0", str(N), ref_lin, mode], capture_output=True,
                        text=True, timeout=timeout, cwd=ROOT)
     line = [l for l in p.stdout.splitlines() if l.startswith("RESULT ")]
     assert p.returncode == 0 and line, p.stderr[-3000:]
@@ -157,6 +179,23 @@ def test_scp_solve_halfcheetah_n30_matches_reference_path():
     import numpy as np
 
     r = _run("halfcheetah_bound", 3, True, N=30, ref_lin="oracle")
+    _check_halfcheetah(r)
+
+
+@pytest.mark.gpu
+def test_scp_solve_halfcheetah_n30_one_pass_dropins():
+    """Same, with install_scp: linearize_all + build_subproblem + precondition of every
+    iteration served by one CUDA-graph replay and one D2H (scp_dropin.py).  Records
+    the pre-IPM wall time per iteration."""
+    r = _run("halfcheetah_bound", 3, True, N=30, ref_lin="oracle", mode="scp")
+    _check_halfcheetah(r)
+    assert len(r["pre_ipm_ms"]) == 3 and r["launches"] > 0
+    print("pre-IPM ms per iteration (install_scp):", r["pre_ipm_ms"])
+
+
+def _check_halfcheetah(r):
+    import numpy as np
+
     assert len(r["gpu"]) == len(r["ref"]) == 4
     for zg, zr in zip(r["gpu"], r["ref"]):
         zg, zr = np.asarray(zg), np.asarray(zr)

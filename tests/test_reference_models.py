@@ -253,3 +253,133 @@ def test_unsupported_topology_fails_loudly(monkeypatch):
                    contacts=(), surface=FlatSurface(), gravity=9.81)
     with pytest.raises(UnsupportedModelError):
         Discretizer(m)
+
+
+# --------------------------------------------------------------------------- rate-level reference tests
+def _rate(disc, xt, u):
+    """The augmented rate [q'; v'; Omega](x, u) from the GPU path itself: at S = 0 every
+    stage input equals the start state, so d(end)/dS = sum_substeps h sum_i b_i f = f
+    (augmentation.py:195-211 with constant control)."""
+    n_u = disc.n_u
+    U = np.concatenate([u, u]).reshape(1, 2 * n_u)
+    _, _, _, js = disc.linearize_batch(np.asarray(xt)[None], U, [0.0])
+    return js[0]
+
+
+@pytest.mark.gpu
+def test_dilation_consistency():
+    """tests/test_augmentation.py:158-185: integrating with dilation S equals integrating
+    the undilated system over [0, S] with the same number of steps (manual RKF
+    comparator with the same stage recursion, FOH control evaluated at t / S)."""
+    from paper_2604_09993_b200 import Discretizer
+
+    m = point_mass_model()
+    g, n_g = build_path_constraints(m)
+    disc = Discretizer(m, np.eye(n_g), g, substeps=8)
+    xt0 = np.concatenate([[0.0, 1.0, 0.2], [0.3, 0.0, 0.0], np.zeros(6)])
+    U = np.array([[0.1, 0.5, 0.1], [0.2, 0.3, 0.0]])
+    S = 0.7
+    end_dilated = disc.propagate(xt0, U, S)
+    A = [[], [1 / 4], [3 / 32, 9 / 32], [1932 / 2197, -7200 / 2197, 7296 / 2197],
+         [439 / 216, -8.0, 3680 / 513, -845 / 4104], [-8 / 27, 2.0, -3544 / 2565, 1859 / 4104, -11 / 40]]
+    Bw = [16 / 135, 0.0, 6656 / 12825, 28561 / 56430, -9 / 50, 2 / 55]
+    C = [0.0, 1 / 4, 3 / 8, 12 / 13, 1.0, 1 / 2]  # the RKF tableau (cito/augmentation.py:46-56)
+    h = S / 8
+    xt = xt0.copy()
+    for step in range(8):
+        ks = []
+        for stage in range(6):
+            xs = xt.copy()
+            for j, a in enumerate(A[stage]):
+                xs = xs + h * a * ks[j]
+            tau = (step * h + C[stage] * h) / S
+            ks.append(_rate(disc, xs, (1.0 - tau) * U[0] + tau * U[1]))
+        xt = xt + h * sum(b * k for b, k in zip(Bw, ks))
+    assert np.allclose(end_dilated, xt, atol=1e-9)
+
+
+@pytest.mark.gpu
+def test_pendulum_closed_form():
+    """tests/test_acceptance.py:490-503: theta'' = -1.5 g / L cos(theta) at 20 random
+    consistent states of the pinned pendulum (rate from the GPU kernel)."""
+    from paper_2604_09993_b200 import Discretizer
+
+    m = pendulum_model()
+    disc = Discretizer(m, substeps=5)
+    rng = np.random.default_rng(8)
+    L = 1.0
+    for _ in range(20):
+        th = rng.uniform(-np.pi, np.pi)
+        w = rng.normal()
+        q = np.array([0.5 * L * np.cos(th), 0.5 * L * np.sin(th), th])
+        v = np.array([-0.5 * L * np.sin(th) * w, 0.5 * L * np.cos(th) * w, w])
+        f = _rate(disc, np.concatenate([q, v]), np.zeros(0))
+        assert abs(f[5] - (-1.5 * m.gravity / L * np.cos(th))) <= 1e-9
+
+
+@pytest.mark.gpu
+def test_aux_rate_channels():
+    """tests/test_augmentation.py:30-58: Omega channel values.  Inactive contact at
+    height 0.3: Omega = [0, 0, 0, 0, srelu(0.3)], path channel srelu(-0.3); unit
+    normal force -> channel 0 = 1; a structured path row with value 0.5 (a link
+    height bound lo - p_z = 0.5; the reference's lambda g(x, u) = [0.5] has no
+    device form) passes srelu(0.5) = 0.30902 straight through identity mixing."""
+    from paper_2604_09993_b200 import Discretizer
+
+    srelu = lambda x: 0.5 * (x + np.sqrt(x * x + 1.0) - 1.0)  # noqa: E731  (smoothmath.py:60-63)
+    m = point_mass_model()
+    g, n_g = build_path_constraints(m)
+    disc = Discretizer(m, np.eye(n_g), g, substeps=5)
+    f = _rate(disc, np.concatenate([[0.0, 0.3, 0.0, 0.0, 0.0, 0.0], np.zeros(6)]), np.zeros(3))
+    yd = f[6:]
+    assert np.allclose(yd[:4], 0.0, atol=1e-14)
+    assert yd[4] == pytest.approx(srelu(0.3), abs=1e-14)
+    assert yd[5] == pytest.approx(srelu(-0.3), abs=1e-14)
+    f = _rate(disc, np.zeros(12), np.array([0.0, 1.0, 0.0]))
+    assert f[6] == pytest.approx(1.0)
+    g2, n_g2 = build_path_constraints(m, body_height_bounds=((0, 0.5, 10.0),))
+    disc2 = Discretizer(m, np.eye(n_g2), g2, substeps=5)
+    f = _rate(disc2, np.zeros(6 + 5 + n_g2), np.zeros(3))
+    assert f[6 + 5 + 1] == pytest.approx(srelu(0.5), abs=1e-12)
+    assert f[6 + 5 + 1] == pytest.approx(0.30902, abs=1e-5)
+
+
+@pytest.mark.gpu
+def test_node_constraint_jacobians_directional_fd():
+    """tests/test_acceptance.py:266-304: the K3 node Jacobians against central
+    differences of the K3 node values, pointmass_rest, 50 random points (seed 5),
+    h = 1e-6, delta = 0.05, the reference's _rel_err <= 1e-5."""
+    import torch
+
+    from conftest import golden_scenario
+
+    from paper_2604_09993_b200.linearize import GpuTranscription
+
+    sc = golden_scenario("pointmass_rest")
+    gt = GpuTranscription(sc)
+    lay = gt.lay
+    rng = np.random.default_rng(5)
+    h, delta = 1e-6, 0.05
+    n_q = lay.n_q
+
+    def nodes(z):
+        r = gt.linearize_device(torch.as_tensor(z, device=gt.device), delta)
+        torch.cuda.synchronize()
+        return {k: r[k].cpu().numpy() for k in ("psi", "theta", "imp_v", "psi_jac", "theta_jac", "imp_jac")}
+
+    for _ in range(50):
+        z = 0.5 * rng.normal(size=lay.dim)
+        d = rng.normal(size=lay.dim)
+        J, p, mn = nodes(z), nodes(z + h * d), nodes(z - h * d)
+        fd_psi = (p["psi"] - mn["psi"]) / (2 * h)
+        for k in range(lay.N - 1):
+            dy = np.concatenate([d[lay.y_of_xp(k)], d[lay.y_of_xm(k + 1)]])
+            assert rel_err(fd_psi[k], J["psi_jac"][k] @ dy) <= 1e-5
+        fd_th = (p["theta"] - mn["theta"]) / (2 * h)
+        fd_imp = (p["imp_v"] - mn["imp_v"]) / (2 * h)
+        for k in range(lay.N):
+            dvec = np.concatenate([d[lay.xm(k)][:n_q], d[lay.xm(k)][n_q: 2 * n_q], d[lay.xp(k)][n_q: 2 * n_q],
+                                   d[lay.phi(k)], d[lay.gam(k)]])
+            assert rel_err(fd_th[k], J["theta_jac"][k] @ dvec) <= 1e-5
+            # imp_v = v+ - impact_map(...): the reference's impulse_defect velocity rows
+            assert rel_err(fd_imp[k], J["imp_jac"][k] @ dvec[: J["imp_jac"].shape[2]]) <= 1e-5
