@@ -49,7 +49,10 @@ class SCPDropIns:
 
     def linearize_all(self, tr, z, delta, epsilon=None, jobs=1):
         step = self._step(tr)
+        first = step._plan is None
         lin, scaled, prec, meta = step.iterate(z, delta, epsilon=epsilon, precondition=True)
+        if first:  # solve keeps iteration k's results alive during k+1: two slots, both captured now
+            step.reserve(2, precondition=True)
         self._last = (lin, step, scaled, prec, meta)
         self._served = None
         self.iterations += 1
@@ -75,8 +78,9 @@ class SCPDropIns:
         if served is None or served[0] is not prog:
             return subproblem.precondition(prog)
         _, scaled, prec = served
-        # cost normalization of this program's own c and P (conic.py:311-316); the
-        # iterate scaled them for z_j = z, which is what scp.solve passes
+        if prog.c is self._last[1]._c_last[1]:  # the objective the iterate scaled (z_j = z, as scp.solve passes)
+            return scaled, prec
+        # cost normalization of this program's own c and P (conic.py:311-316)
         c = prog.c
         omega = max(1.0, float(np.max(np.abs(c))) if c.size else 0.0)
         if prog.P.nnz:

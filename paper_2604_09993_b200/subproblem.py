@@ -789,9 +789,9 @@ def _lazy_program_type(base):
 
     class LazyProgram(base):
         @classmethod
-        def _new(cls, step, mats, nA, nG, P, c, cones):
+        def _new(cls, step, hb, mats, nA, nG, P, c, cones):
             o = object.__new__(cls)
-            o.__dict__.update(P=P, c=c, cones=cones, _step=step, _mats=mats, _nA=nA, _nG=nG, _host=None)
+            o.__dict__.update(P=P, c=c, cones=cones, _step=step, _hb=hb, _mats=mats, _nA=nA, _nG=nG, _host=None)
             return o
 
         def _materialize(self):
@@ -800,7 +800,7 @@ def _lazy_program_type(base):
             import scipy.sparse as sp
             import torch
 
-            u = self._step._plan["unscaled"]
+            u = self._hb.slot["unscaled"]
             h = {}
             for M in ("A", "G"):
                 ref = self._mats[M]
@@ -959,26 +959,14 @@ class GpuSCPStep:
 
     # -- one-time plan: buffers + constant ctypes argument tables
     def _build_plan(self):
-        import ctypes
-        import weakref  # noqa: F401
-
         import torch
 
         gt, asm, pat = self.gt, self.asm, self.asm.pat
         if getattr(asm, "_rhs", None) is None:
             asm._prepare_batched()
         lay, dev = gt.lay, gt.device
-        N, nxt, nu, nq, nc = lay.N, lay.n_xt, lay.n_u, lay.n_q, lay.n_c
-        n_psi = 3 * nc + lay.n_g_out
-        NI = N - 1
+        NI = lay.N - 1
         f64 = dict(dtype=torch.float64, device=dev)
-        # linearization outputs (device only; the lazy LinearizedProblem reads them on demand)
-        lin = dict(ends=torch.empty((NI, nxt), **f64), jx=torch.empty((NI, nxt, nxt), **f64),
-                   ju=torch.empty((NI, nxt, 2 * nu), **f64), js=torch.empty((NI, nxt), **f64),
-                   defects=torch.empty((NI, nxt), **f64),
-                   psi=torch.empty((NI, n_psi), **f64), psi_jac=torch.empty((NI, n_psi, 2 * lay.n_y), **f64),
-                   theta=torch.empty((N, 6 * nc), **f64), theta_jac=torch.empty((N, 6 * nc, 3 * nq + 3 * nc), **f64),
-                   imp_v=torch.empty((N, nq), **f64), imp_jac=torch.empty((N, nq, 3 * nq + 2 * nc), **f64))
         dA, dG = asm._mats["A"], asm._mats["G"]
         nA, nG = dA["nrows"], dG["nrows"]
         i32, i64, fd = torch.int32, torch.int64, torch.float64
@@ -986,13 +974,6 @@ class GpuSCPStep:
                       ("rhs", fd, nA + nG), ("row_scale_A", fd, nA), ("row_scale_G", fd, nG),
                       ("A_data", fd, dA["nsup"]), ("G_data", fd, dG["nsup"]),
                       ("A_indices", i32, dA["nsup"]), ("G_indices", i32, dG["nsup"])], dev)
-        lin["bad"] = pk.d["bad"]
-        # the unscaled values of a preconditioned iteration stay on the device (D2D copy
-        # before the row scaling): build_subproblem's program in the install_scp drop-ins
-        # reads them only if a caller looks at it (cito.scp.solve does not)
-        unscaled = dict(A_data=torch.empty(max(1, dA["nsup"]), dtype=fd, device=dev),
-                        G_data=torch.empty(max(1, dG["nsup"]), dtype=fd, device=dev),
-                        rhs=torch.empty(max(1, nA + nG), dtype=fd, device=dev))
         # z followed by [delta, epsilon]: one H2D per call, read by the kernels from device
         # memory so a captured graph replays for any delta of the homotopy
         zde_dev = torch.empty(lay.dim + 2, **f64)
@@ -1000,67 +981,97 @@ class GpuSCPStep:
         z_dev = zde_dev[: lay.dim]
         rowmax = torch.empty(max(1, nA + nG), dtype=i64, device=dev)
         arr = lambda xs: ctypes_ptr_array([x.data_ptr() for x in xs])  # noqa: E731
-        mats = [dA, dG]
-        r = asm._rhs
         soc_start, soc_dim = soc_tables(pat.n_orthant, pat.soc_dims, dev)
-        L = _lib.lib()
         keep = []  # ctypes arrays must outlive the plan
-
-        def k(a):
-            keep.append(a)
-            return a
-
-        lin_ptrs = k(arr([lin[kk] for kk in LIN_SOURCES]))
-        asm_args = (2, pat.n, k(arr([d["sp_ptr"] for d in mats])), k(arr([d["row"] for d in mats])),
-                    k(arr([d["src"] for d in mats])), k(arr([d["idx"] for d in mats])),
-                    k(arr([d["val"] for d in mats])), asm.sigma_dev.data_ptr(), lin_ptrs,
-                    k(arr([d["counts"] for d in mats])), k(arr([pk.d["A_indptr"], pk.d["G_indptr"]])),
-                    k(arr([pk.d["A_indices"], pk.d["G_indices"]])), k(arr([pk.d["A_data"], pk.d["G_data"]])))
-        rm_arr = k(arr([rowmax[:nA], rowmax[nA:]]))
-        outs = [(pk.d["A_indptr"], pk.d["A_indices"], pk.d["A_data"]), (pk.d["G_indptr"], pk.d["G_indices"],
-                                                                       pk.d["G_data"])]
-        packed = tuple(k(a) if a is not None and not isinstance(a, int) else a
-                       for a in asm.packed_args(lin_ptrs, outs, None, arr))
-        packed_pc = tuple(k(a) if a is not None and not isinstance(a, int) else a
-                          for a in asm.packed_args(lin_ptrs, outs, [rowmax[:nA], rowmax[nA:]], arr))
-        # b and h: one contiguous vector (rows [0, nA) = b, [nA, nA + nG) = h) in the packed buffer
-        rhs_dev = pk.d["rhs"]
-        rhs_args = (r["n"], r["rows"].data_ptr(), r["form"].data_ptr(), r["vsrc"].data_ptr(), r["voff"].data_ptr(),
-                    r["seg_src"].data_ptr(), r["seg_off"].data_ptr(), r["seg_len"].data_ptr(), r["seg_cb"].data_ptr(),
-                    r["cols"].data_ptr(), z_dev.data_ptr(), lin_ptrs, rhs_dev.data_ptr())
+        rhs_dev = pk.d["rhs"]  # b and h: rows [0, nA) = b, [nA, nA + nG) = h
         pc_args = (pat.n, pk.d["A_indptr"].data_ptr(), pk.d["A_indices"].data_ptr(), pk.d["A_data"].data_ptr(), nA,
                    rhs_dev.data_ptr(), pk.d["G_indptr"].data_ptr(), pk.d["G_indices"].data_ptr(),
                    pk.d["G_data"].data_ptr(), nG, rhs_dev[nA:].data_ptr(), pat.n_orthant, len(pat.soc_dims),
                    soc_start.data_ptr(), soc_dim.data_ptr(), rowmax[:nA].data_ptr(), rowmax[nA:].data_ptr(), 1,
                    max(dA["nsup"], dG["nsup"]), pk.d["row_scale_A"].data_ptr(), pk.d["row_scale_G"].data_ptr())
-        o = lin
-        lin_args = (gt.disc._h.ptr, N, 1, int(lay.dim), int(gt.base_u), int(gt.base_p), z_dev.data_ptr(),
-                    zde_dev[lay.dim:].data_ptr())
-        lin_outs = tuple(o[kk].data_ptr() for kk in ("ends", "jx", "ju", "js", "defects", "bad", "psi", "psi_jac",
-                                                     "theta", "theta_jac", "imp_v", "imp_jac"))
+        rm_arr = arr([rowmax[:nA], rowmax[nA:]])
+        keep.append(rm_arr)
         dim = lay.dim
         P_idx = np.arange(dim, dtype=np.int32)
         P_ptr = np.concatenate([np.arange(dim + 1), np.full(pat.n - dim, dim)]).astype(np.int32)
-        self._plan = dict(lin=lin, pk=pk, z_dev=z_dev, zde_dev=zde_dev, zde_pin=zde_pin, rowmax=rowmax, rhs_dev=rhs_dev,
-                          hosts=[], graph_kernels={}, side=torch.cuda.Stream(dev),
-                          rhs_const=r["const"], asm_args=asm_args, rm_arr=rm_arr, rhs_args=rhs_args,
-                          packed=packed, packed_pc=packed_pc, unscaled=unscaled,
-                          pc_args=pc_args, lin_args=lin_args, lin_outs=lin_outs, keep=keep, L=L, nA=nA, nG=nG,
-                          soc=(soc_start, soc_dim), P_idx=P_idx, P_ptr=P_ptr,
+        self._plan = dict(pk=pk, z_dev=z_dev, zde_dev=zde_dev, zde_pin=zde_pin, rowmax=rowmax, rhs_dev=rhs_dev,
+                          hosts=[], graph_kernels={}, side=torch.cuda.Stream(dev), rhs_const=asm._rhs["const"],
+                          rm_arr=rm_arr, pc_args=pc_args, keep=keep, L=_lib.lib(), nA=nA, nG=nG,
+                          soc=(soc_start, soc_dim), P_idx=P_idx, P_ptr=P_ptr, arr=arr,
                           P_plain=None, meta=_Meta(pat.z_idx, pat.sp_idx, pat.sm_idx, pat.t_idx))
+
+    def _make_slot(self):
+        """Device buffers of one in-flight iteration, paired with a pinned host buffer:
+        the linearization outputs (read lazily by the LinearizedProblem handed out)
+        and the unscaled program values (read lazily by unscaled_program), plus the
+        kernel argument tables that point at them.  A slot is reused only when every
+        result handed out from it has been dropped, so nothing is ever overwritten
+        under a live result and no copy-out is needed before the next iteration."""
+        import torch
+
+        gt, asm, pat, pl = self.gt, self.asm, self.asm.pat, self._plan
+        lay, dev = gt.lay, gt.device
+        N, nxt, nu, nq, nc = lay.N, lay.n_xt, lay.n_u, lay.n_q, lay.n_c
+        n_psi = 3 * nc + lay.n_g_out
+        NI = N - 1
+        f64 = dict(dtype=torch.float64, device=dev)
+        pk, arr = pl["pk"], pl["arr"]
+        lin = dict(ends=torch.empty((NI, nxt), **f64), jx=torch.empty((NI, nxt, nxt), **f64),
+                   ju=torch.empty((NI, nxt, 2 * nu), **f64), js=torch.empty((NI, nxt), **f64),
+                   defects=torch.empty((NI, nxt), **f64),
+                   psi=torch.empty((NI, n_psi), **f64), psi_jac=torch.empty((NI, n_psi, 2 * lay.n_y), **f64),
+                   theta=torch.empty((N, 6 * nc), **f64), theta_jac=torch.empty((N, 6 * nc, 3 * nq + 3 * nc), **f64),
+                   imp_v=torch.empty((N, nq), **f64), imp_jac=torch.empty((N, nq, 3 * nq + 2 * nc), **f64))
+        lin["bad"] = pk.d["bad"]
+        dA, dG = asm._mats["A"], asm._mats["G"]
+        unscaled = dict(A_data=torch.empty(max(1, dA["nsup"]), **f64), G_data=torch.empty(max(1, dG["nsup"]), **f64),
+                        rhs=torch.empty(max(1, pl["nA"] + pl["nG"]), **f64))
+        keep = []
+
+        def k(a):
+            if a is not None and not isinstance(a, int):
+                keep.append(a)
+            return a
+
+        mats = [dA, dG]
+        lin_ptrs = k(arr([lin[kk] for kk in LIN_SOURCES]))
+        outs = [(pk.d["A_indptr"], pk.d["A_indices"], pk.d["A_data"]),
+                (pk.d["G_indptr"], pk.d["G_indices"], pk.d["G_data"])]
+        rowmax = pl["rowmax"]
+        nA = pl["nA"]
+        r = asm._rhs
+        slot = dict(
+            lin=lin, unscaled=unscaled, keep=keep,
+            packed=tuple(k(a) for a in asm.packed_args(lin_ptrs, outs, None, arr)),
+            packed_pc=tuple(k(a) for a in asm.packed_args(lin_ptrs, outs, [rowmax[:nA], rowmax[nA:]], arr)),
+            asm_args=(2, pat.n, k(arr([d["sp_ptr"] for d in mats])), k(arr([d["row"] for d in mats])),
+                      k(arr([d["src"] for d in mats])), k(arr([d["idx"] for d in mats])),
+                      k(arr([d["val"] for d in mats])), asm.sigma_dev.data_ptr(), lin_ptrs,
+                      k(arr([d["counts"] for d in mats])), k(arr([o[0] for o in outs])), k(arr([o[1] for o in outs])),
+                      k(arr([o[2] for o in outs]))),
+            rhs_args=(r["n"], r["rows"].data_ptr(), r["form"].data_ptr(), r["vsrc"].data_ptr(),
+                      r["voff"].data_ptr(), r["seg_src"].data_ptr(), r["seg_off"].data_ptr(),
+                      r["seg_len"].data_ptr(), r["seg_cb"].data_ptr(), r["cols"].data_ptr(), pl["z_dev"].data_ptr(),
+                      lin_ptrs, pl["rhs_dev"].data_ptr()),
+            lin_args=(gt.disc._h.ptr, N, 1, int(lay.dim), int(gt.base_u), int(gt.base_p), pl["z_dev"].data_ptr(),
+                      pl["zde_dev"][lay.dim:].data_ptr()),
+            lin_outs=tuple(lin[kk].data_ptr() for kk in ("ends", "jx", "ju", "js", "defects", "bad", "psi",
+                                                         "psi_jac", "theta", "theta_jac", "imp_v", "imp_jac")))
+        return slot
 
     def _launch(self, precondition, hb):
         """The device work of one iteration on the current stream: H2D of
-        [z, delta, epsilon], K1 + K3, CSC assembly, rhs, optional row scaling,
-        D2H of the packed result into the pinned host buffer `hb`."""
+        [z, delta, epsilon], K1 + K3, CSC assembly, rhs, optional row scaling (the
+        unscaled values kept in the slot), D2H of the packed result into the
+        pinned host buffer `hb` (outputs in hb's device slot)."""
         import torch
 
-        pl = self._plan
+        pl, sl = self._plan, hb.slot
         L = pl["L"]
         s = torch.cuda.current_stream(self.gt.device).cuda_stream
         pl["zde_dev"].copy_(pl["zde_pin"], non_blocking=True)
         h = self.gt.disc._h  # the handle's own library (a run-time compiled topology has its own)
-        h.check(h.L.cito_linearize_all_dev2(*pl["lin_args"], *pl["lin_outs"], s), "linearize_all")
+        h.check(h.L.cito_linearize_all_dev2(*sl["lin_args"], *sl["lin_outs"], s), "linearize_all")
         if precondition:
             pl["rowmax"].zero_()
         # b/h of the linearized rows on a side stream, concurrently with the CSC compaction
@@ -1069,16 +1080,16 @@ class GpuSCPStep:
         side.wait_stream(cur)
         with torch.cuda.stream(side):
             pl["rhs_dev"].copy_(pl["rhs_const"])
-            _lib.check(L.cito_rhs_dev(*pl["rhs_args"], side.cuda_stream), "rhs")
+            _lib.check(L.cito_rhs_dev(*sl["rhs_args"], side.cuda_stream), "rhs")
         if not _CSC_RECIPES:
-            _lib.check(L.cito_csc_assemble_packed_dev(*(pl["packed_pc"] if precondition else pl["packed"]), s),
+            _lib.check(L.cito_csc_assemble_packed_dev(*(sl["packed_pc"] if precondition else sl["packed"]), s),
                        "csc_assemble")
         else:
-            _lib.check(L.cito_csc_assemble2_dev(*pl["asm_args"], pl["rm_arr"] if precondition else None, s),
+            _lib.check(L.cito_csc_assemble2_dev(*sl["asm_args"], pl["rm_arr"] if precondition else None, s),
                        "csc_assemble")
         cur.wait_stream(side)
         if precondition:
-            u, d = pl["unscaled"], pl["pk"].d
+            u, d = sl["unscaled"], pl["pk"].d
             for kk in ("A_data", "G_data", "rhs"):
                 u[kk][: d[kk].numel()].copy_(d[kk])
             _lib.check(L.cito_precondition_dev(*pl["pc_args"], s), "precondition")
@@ -1123,6 +1134,7 @@ class GpuSCPStep:
             if hb.free():
                 return hb
         hb = _HostBuf(pl["pk"])
+        hb.slot = self._make_slot()
         pl["hosts"].append(hb)
         return hb
 
@@ -1132,6 +1144,7 @@ class GpuSCPStep:
         import torch
 
         pl = self._plan
+        pl["captures"] = pl.get("captures", 0) + 1
         hb.caps = {}
         self._launch(precondition, hb)
         torch.cuda.current_stream(self.gt.device).synchronize()
@@ -1160,15 +1173,6 @@ class GpuSCPStep:
             self._build_plan()
         pl = self._plan
         gt, pat = self.gt, self.asm.pat
-        # a LinearizedProblem handed out by the previous call still points at the
-        # reused device buffers: give it its own host copy before overwriting them
-        prev = self._last_lin() if self._last_lin is not None else None
-        if prev is not None and prev.device_arrays() is not None:
-            prev.release_device()
-        prev = self._last_unscaled() if getattr(self, "_last_unscaled", None) is not None else None
-        if prev is not None:
-            prev._materialize()  # the device copy of its values is about to be overwritten
-        self._last_unscaled = None
         if epsilon is None:
             epsilon = gt.scenario.ctcs_epsilon
         stream = torch.cuda.current_stream(gt.device)
@@ -1204,6 +1208,7 @@ class GpuSCPStep:
                                   hb.wrap(f"{M}_indptr", 0, pat.n + 1), (nrows, pat.n))
         zj = z if z_j is None else z_j
         c = pat.objective_c(zj)
+        self._c_last = (zj, c)  # the unscaled objective, for unscaled_program(z_j) of the same point
         P_data = pat.P_diag[: pat.lay.dim]
         if precondition:  # cost normalization (conic.py:311-316)
             omega = max(1.0, float(np.max(np.abs(c))) if c.size else 0.0)
@@ -1220,31 +1225,51 @@ class GpuSCPStep:
             P = pl["P_plain"]
         prog = ConicProgram(P=P, c=c, A=mats["A"], b=hb.wrap("rhs", 0, nA), G=mats["G"], h=hb.wrap("rhs", nA, pl["nG"]),
                             cones=ConeSpec(nonneg=pat.n_orthant, soc=pat.soc_dims))
-        lin = self._Lazy(pl["lin"], z.copy())
+        lin = self._Lazy(hb.slot["lin"], z.copy())
         import weakref
 
+        hb.live.append(weakref.ref(lin))  # the slot's device outputs stay untouched while lin lives
         self._last_lin = weakref.ref(lin)
         if precondition:
             prec = _preconditioner_type()(row_scale_A=hb.wrap("row_scale_A", 0, nA),
                                           row_scale_G=hb.wrap("row_scale_G", 0, pl["nG"]),
                                           var_scale=np.ones(pat.n), cost_scale=omega)
-            self._pc_parts = (mats, nA, pl["nG"])
+            self._pc_parts = (mats, nA, pl["nG"], hb)
             return lin, prog, prec, pl["meta"]
         self._pc_parts = None
         return lin, prog, pl["meta"]
 
+    def reserve(self, n, precondition=False):
+        """Make sure n result slots exist with their CUDA graphs captured for this
+        mode, so a loop that keeps the previous result alive while computing the
+        next (cito.scp.solve holds lin/prog of iteration k during k+1) never
+        captures in the middle of the loop.  Uses the last [z, delta, epsilon]."""
+        import torch
+
+        if self._plan is None or not self.use_graph:
+            return
+        pl = self._plan
+        while len(pl["hosts"]) < n:
+            hb = _HostBuf(pl["pk"])
+            hb.slot = self._make_slot()
+            pl["hosts"].append(hb)
+        for hb in pl["hosts"][:n]:
+            if bool(precondition) not in hb.graphs:
+                self._capture(bool(precondition), hb)
+        torch.cuda.current_stream(self.gt.device).synchronize()
+
     def unscaled_program(self, z_j):
         """The program of the last preconditioned iterate BEFORE row scaling
         (= cito.scp.build_subproblem's output), lazily: its A/G values and b/h come
-        back from the device copy only when first read (valid until the next
-        iterate, which materializes it first).  P and c (host) are exact."""
+        back from the slot's device copy only when first read (the program keeps
+        its slot busy, so the copy stays valid).  P and c (host) are exact."""
         import weakref
 
         import scipy.sparse as sp
 
         if self._pc_parts is None:
             raise RuntimeError("unscaled_program needs a preceding iterate(..., precondition=True)")
-        mats, nA, nG = self._pc_parts
+        mats, nA, nG, hb = self._pc_parts
         pat = self.asm.pat
         pl = self._plan
         if pl["P_plain"] is None:
@@ -1254,8 +1279,10 @@ class GpuSCPStep:
                 arr.flags.writeable = False
             pl["P_plain"] = Pm
         ConicProgram, ConeSpec = _conic_types()
+        zl, cl = self._c_last
+        c = cl if (z_j is zl or np.array_equal(z_j, zl)) else pat.objective_c(z_j)
         prog = _lazy_program_type(ConicProgram)._new(
-            self, mats, nA, nG, P=pl["P_plain"], c=pat.objective_c(z_j),
+            self, hb, mats, nA, nG, P=pl["P_plain"], c=c,
             cones=ConeSpec(nonneg=pat.n_orthant, soc=pat.soc_dims))
-        self._last_unscaled = weakref.ref(prog)
+        hb.live.append(weakref.ref(prog))
         return prog

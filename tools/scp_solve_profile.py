@@ -53,9 +53,21 @@ def timed(name, fn):
     return w
 
 
+dev_ms = []
 if one_pass:
     from paper_2604_09993_b200.scp_dropin import install_scp
+    from paper_2604_09993_b200.subproblem import GpuSCPStep
 
+    _orig_replay = torch.cuda.CUDAGraph.replay
+
+    def _timed_replay(g):  # device time of each iteration's graph (CUDA events on the replay stream)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _orig_replay(g)
+        e1.record()
+        dev_ms.append((e0, e1))
+
+    torch.cuda.CUDAGraph.replay = _timed_replay
     d = install_scp(scp)
     fns = (scp.linearize_all, scp.build_subproblem, scp.precondition)
 else:
@@ -65,6 +77,7 @@ z0 = tr.initial_guess()
 for _ in range(2):
     lin = fns[0](tr, z0, 1.0)
     fns[2](fns[1](tr, lin, z0, 1.0, scp.SCPConfig())[0])
+del lin  # a result kept alive here would hold one of the step's result slots for the whole run
 scp.linearize_all = timed("linearize_all", fns[0])
 scp.build_subproblem = timed("build_subproblem", fns[1])
 scp.precondition = timed("precondition", fns[2])
@@ -77,6 +90,9 @@ out = {"scenario": f"halfcheetah_bound N={N} (substeps {sc.substeps})", "iterati
        "per_iteration_ms": {k: [1e3 * x for x in v] for k, v in times.items()},
        "mean_ms": {k: (1e3 * sum(v) / len(v) if v else None) for k, v in times.items()},
        "delta": [h.delta for h in hist], "j_px": [h.j_px for h in hist], "j_ep": [h.j_ep for h in hist],
+       "slots": ({id(t): (len(st._plan["hosts"]), st._plan.get("captures")) for t, st in d._steps.values()}
+                 if one_pass else None),
+       "graph_device_ms": [a.elapsed_time(b) for a, b in dev_ms[-(len(hist) - 1):]] if dev_ms else None,
        "pre_ipm_ms": [1e3 * (a + b + c) for a, b, c in zip(times["linearize_all"], times["build_subproblem"],
                                                            times["precondition"])],
        "mode": "install_scp (one device pass per iteration)" if one_pass else "three separate drop-ins",
