@@ -48,7 +48,80 @@ def chol_order(joints):
 
 
 def chol_code(nj, lnz):
-    """Straight-line sparse Cholesky + both triangular solves of the 2 nj x 2 nj
+    """Straight-line block LDL^T factorisation + solves of the 2 nj x 2 nj joint Gram
+    matrix in elimination order, 2x2 blocks (one joint = one block; only structurally
+    nonzero blocks, constant indices only, so every value lives in a register).
+    G = L D L^T with unit block-lower L:
+        D_b  = G_bb - sum_k W_bk L_bk^T          W_rb = G_rb - sum_k W_rk L_bk^T
+        L_rb = W_rb D_b^-1                      (D_b^-1 by the 2x2 adjugate / det)
+    one reciprocal per joint on the dependency chain instead of two square roots
+    (the chain of the tree's deepest path sets the latency of the primal stage).
+    Packed storage LI(r, c) = r (r + 1) / 2 + c: the off-diagonal blocks hold L_rb,
+    the diagonal block slots hold D_b^-1 (symmetric: (2b,2b), (2b+1,2b), (2b+1,2b+1));
+    Li is not used by the block form (written as 0)."""
+    LI = lambda r, c: r * (r + 1) // 2 + c  # noqa: E731
+    blk = lambda a, b: (a, b) in lnz  # noqa: E731
+    f = ["  __device__ __forceinline__ static void chol_solve(double* L, double* y, double* Li) {\n"]
+    for r in range(2 * nj):
+        f.append(f"    Li[{r}] = 0.0;\n")
+    for b in range(nj):
+        ks = [k for k in range(b) if blk(b, k)]
+        f.append(f"    double D{b}_00 = L[{LI(2 * b, 2 * b)}], D{b}_10 = L[{LI(2 * b + 1, 2 * b)}], "
+                 f"D{b}_11 = L[{LI(2 * b + 1, 2 * b + 1)}];\n")
+        for k in ks:  # D -= W_bk L_bk^T (symmetric: lower triangle)
+            f.append(f"    D{b}_00 -= W{b}_{k}_00 * L{b}_{k}_00 + W{b}_{k}_01 * L{b}_{k}_01;"
+                     f" D{b}_10 -= W{b}_{k}_10 * L{b}_{k}_00 + W{b}_{k}_11 * L{b}_{k}_01;"
+                     f" D{b}_11 -= W{b}_{k}_10 * L{b}_{k}_10 + W{b}_{k}_11 * L{b}_{k}_11;\n")
+        f.append(f"    const double id{b} = 1.0 / (D{b}_00 * D{b}_11 - D{b}_10 * D{b}_10);\n")
+        f.append(f"    const double I{b}_00 = D{b}_11 * id{b}, I{b}_10 = -D{b}_10 * id{b}, I{b}_11 = D{b}_00 * id{b};\n")
+        f.append(f"    L[{LI(2 * b, 2 * b)}] = I{b}_00; L[{LI(2 * b + 1, 2 * b)}] = I{b}_10; "
+                 f"L[{LI(2 * b + 1, 2 * b + 1)}] = I{b}_11;\n")
+        for r in range(b + 1, nj):
+            if not blk(r, b):
+                continue
+            f.append(f"    double W{r}_{b}_00 = L[{LI(2 * r, 2 * b)}], W{r}_{b}_01 = L[{LI(2 * r, 2 * b + 1)}], "
+                     f"W{r}_{b}_10 = L[{LI(2 * r + 1, 2 * b)}], W{r}_{b}_11 = L[{LI(2 * r + 1, 2 * b + 1)}];\n")
+            for k in ks:
+                if not blk(r, k):
+                    continue
+                for i in range(2):
+                    for j in range(2):  # (W_rk L_bk^T)_ij = sum_m W_rk[i][m] L_bk[j][m]
+                        f.append(f"    W{r}_{b}_{i}{j} -= W{r}_{k}_{i}0 * L{b}_{k}_{j}0 + W{r}_{k}_{i}1 * L{b}_{k}_{j}1;\n")
+            for i in range(2):
+                for j in range(2):  # L_rb = W_rb D_b^-1 (D^-1 symmetric: [[I00, I10], [I10, I11]])
+                    d0 = f"I{b}_00" if j == 0 else f"I{b}_10"
+                    d1 = f"I{b}_10" if j == 0 else f"I{b}_11"
+                    f.append(f"    const double L{r}_{b}_{i}{j} = W{r}_{b}_{i}0 * {d0} + W{r}_{b}_{i}1 * {d1};"
+                             f" L[{LI(2 * r + i, 2 * b + j)}] = L{r}_{b}_{i}{j};\n")
+    solve = []
+    for b in range(nj):  # forward: z_b = y_b - sum_k L_bk z_k
+        for i in range(2):
+            terms = "".join(f" - L[{LI(2 * b + i, 2 * k)}] * y[{2 * k}] - L[{LI(2 * b + i, 2 * k + 1)}] * y[{2 * k + 1}]"
+                            for k in range(b) if blk(b, k))
+            if terms:
+                solve.append(f"    y[{2 * b + i}] = y[{2 * b + i}]{terms};\n")
+    for b in range(nj):  # diagonal: w_b = D_b^-1 z_b
+        solve.append(f"    {{ const double z0 = y[{2 * b}], z1 = y[{2 * b + 1}];"
+                     f" y[{2 * b}] = L[{LI(2 * b, 2 * b)}] * z0 + L[{LI(2 * b + 1, 2 * b)}] * z1;"
+                     f" y[{2 * b + 1}] = L[{LI(2 * b + 1, 2 * b)}] * z0 + L[{LI(2 * b + 1, 2 * b + 1)}] * z1; }}\n")
+    for b in range(nj - 1, -1, -1):  # backward: x_b = w_b - sum_r L_rb^T x_r
+        for i in range(2):
+            terms = "".join(f" - L[{LI(2 * r, 2 * b + i)}] * y[{2 * r}] - L[{LI(2 * r + 1, 2 * b + i)}] * y[{2 * r + 1}]"
+                            for r in range(b + 1, nj) if blk(r, b))
+            if terms:
+                solve.append(f"    y[{2 * b + i}] = y[{2 * b + i}]{terms};\n")
+    f += solve
+    f.append("  }\n")
+    # both triangular solves with a given factor (rate-Jacobian tangents reuse the primal factor)
+    f.append("  __device__ __forceinline__ static void tri_solve(const double* L, const double* Li, double* y) {\n")
+    f.append("    (void)Li;\n")
+    f += solve
+    f.append("  }\n")
+    return "".join(f)
+
+
+def chol_code_llt(nj, lnz):
+    """(A/B only, CITO_CHOL=llt) Straight-line scalar sparse Cholesky + both triangular solves of the 2 nj x 2 nj
     joint Gram matrix in elimination order (only structurally nonzero entries,
     constant indices only, so every value lives in a register).  Same operation
     order as the loop form it replaces (left-looking columns, reciprocal pivots
@@ -169,7 +242,7 @@ def main(out_path, entries=None):
         s += ("  __host__ __device__ static constexpr bool lnzb(int a, int b) { return (("
               + "".join(f"a == {i} ? {v}u : " for i, v in enumerate(lbits)) + "0u) >> b) & 1u; }\n")
         if joints:
-            s += chol_code(len(joints), lnz)
+            s += (chol_code_llt if os.environ.get("CITO_CHOL") == "llt" else chol_code)(len(joints), lnz)
         s += f"  static constexpr int NHCOL = {len(heavy)}, NLCOL = {len(light)};\n"
         s += chain("hcol", heavy)
         s += chain("lcol", light)

@@ -18,10 +18,13 @@ for B in [int(a) for a in (sys.argv[1:] or ["29", "4096"])]:
                      ("propagate", lambda: disc.propagate_batch_device(xd, Ud, Sd))):
         for _ in range(3): fn()
         torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        n = 10
-        e0.record()
-        for _ in range(n): fn()
-        e1.record(); torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1) / n
+        flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
+        ts = []
+        for _ in range(10):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(); fn(); e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        ms = float(np.median(ts))
         print(f"B={B} {name}: {ms:.3f} ms  -> {B/ms*1e3:.3e} intervals/s", flush=True)
