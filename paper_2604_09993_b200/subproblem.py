@@ -1093,35 +1093,39 @@ class GpuSCPStep:
             for kk in ("A_data", "G_data", "rhs"):
                 u[kk][: d[kk].numel()].copy_(d[kk])
             _lib.check(L.cito_precondition_dev(*pl["pc_args"], s), "precondition")
-        self._d2h(hb)
+        self._d2h(hb, precondition=precondition)
 
-    def _d2h(self, hb, tail=False):
+    def _d2h(self, hb, tail=False, precondition=True):
         """Device -> pinned copies of the packed result: the fixed fields in one
-        copy, the CSC values/indices only up to the buffer's caps (the nnz of
-        the previous result + 25 %, so about half of the superset-sized
-        arrays); `tail` copies what lies beyond the caps (the rare case of a
-        result with more nonzeros than the caps)."""
+        copy (the row scales only for a preconditioned iteration), the CSC
+        values/indices only up to the buffer's caps (the nnz of the captured
+        result + 1/32 + 256, about 45 % of the superset-sized arrays); `tail`
+        copies what lies beyond the caps (a result with more nonzeros than
+        the captured one: one extra copy + synchronization, then recapture)."""
         pk = self._plan["pk"]
         lay = pk.layout
         if not tail:
-            end = lay["A_data"][0]  # fixed fields precede the CSC arrays
+            # fixed fields precede the CSC arrays: bad, indptrs, rhs, then the row scales
+            end = lay["A_data"][0] if precondition else lay["row_scale_A"][0]
             hb.host[:end].copy_(pk.dev[:end], non_blocking=True)
+        caps = hb.caps.get(bool(precondition), {})  # per captured graph (plain / preconditioned)
         for M in ("A", "G"):
-            cap = hb.caps.get(M, lay[f"{M}_data"][2])
+            cap = caps.get(M, lay[f"{M}_data"][2])
             for fld in (f"{M}_data", f"{M}_indices"):
                 o, _, n, isz = lay[fld]
                 lo, hi = (cap, n) if tail else (0, min(cap, n))
                 if hi > lo:
                     hb.host[o + lo * isz: o + hi * isz].copy_(pk.dev[o + lo * isz: o + hi * isz], non_blocking=True)
 
-    def d2h_bytes(self):
+    def d2h_bytes(self, precondition=False):
         """Bytes of the device->host copies one (graph-replayed) iteration makes."""
         pk = self._plan["pk"]
         lay = pk.layout
         hb = self._plan["hosts"][-1] if self._plan["hosts"] else None
-        n = lay["A_data"][0]
+        n = lay["A_data"][0] if precondition else lay["row_scale_A"][0]
+        caps = hb.caps.get(bool(precondition), {}) if hb is not None else {}
         for M in ("A", "G"):
-            cap = hb.caps.get(M, lay[f"{M}_data"][2]) if hb is not None else lay[f"{M}_data"][2]
+            cap = caps.get(M, lay[f"{M}_data"][2])
             for fld in (f"{M}_data", f"{M}_indices"):
                 n += min(cap, lay[fld][2]) * lay[fld][3]
         return int(n)
@@ -1145,12 +1149,14 @@ class GpuSCPStep:
 
         pl = self._plan
         pl["captures"] = pl.get("captures", 0) + 1
-        hb.caps = {}
+        hb.caps[bool(precondition)] = {}  # the eager run copies the full arrays
         self._launch(precondition, hb)
         torch.cuda.current_stream(self.gt.device).synchronize()
-        for M in ("A", "G"):  # D2H caps of the captured copies: this result's nnz + 25 % (+4096)
+        caps = {}
+        for M in ("A", "G"):  # D2H caps of the captured copies: this result's nnz + 1/32 + 256
             nnz = int(hb.h[f"{M}_indptr"][-1])
-            hb.caps[M] = min(pl["pk"].layout[f"{M}_data"][2], nnz + nnz // 4 + 4096)
+            caps[M] = min(pl["pk"].layout[f"{M}_data"][2], nnz + nnz // 32 + 256)
+        hb.caps[bool(precondition)] = caps
         g = torch.cuda.CUDAGraph()
         n0 = _lib.launch_count()
         with torch.cuda.graph(g):
@@ -1193,10 +1199,11 @@ class GpuSCPStep:
         nA = pl["nA"]
         stream.synchronize()  # the one synchronization
         hh = hb.h
-        if any(int(hh[f"{M}_indptr"][-1]) > hb.caps.get(M, 1 << 62) for M in ("A", "G")):
-            self._d2h(hb, tail=True)  # more nonzeros than the captured copies cover
+        caps = hb.caps.get(bool(precondition), {})
+        if any(int(hh[f"{M}_indptr"][-1]) > caps.get(M, 1 << 62) for M in ("A", "G")):
+            self._d2h(hb, tail=True, precondition=precondition)  # more nonzeros than the captured copies cover
             stream.synchronize()
-            hb.graphs.clear()  # recapture with caps from this result
+            hb.graphs.pop(bool(precondition), None)  # recapture with caps from this result
         bad = hh["bad"]
         if bad.any():
             raise FloatingPointError(f"non-finite state in intervals {np.where(bad != 0)[0].tolist()}")

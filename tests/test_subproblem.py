@@ -204,3 +204,39 @@ def test_csc_direct_rejects_inconsistent_arrays():
         _csc_direct(d, i, np.array([1, 2, 3], dtype=np.int32), (3, 2))  # indptr[0] != 0
     with pytest.raises(RuntimeError):
         _csc_direct(d, i.astype(np.int64), np.array([0, 1, 3], dtype=np.int32), (3, 2))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["pointmass_rest", "halfcheetah_n30"])
+@pytest.mark.parametrize("precondition", [False, True])
+def test_gpu_scp_step_graph_replay_pattern_change(name, precondition):
+    """A captured iteration replayed at a point whose pattern differs (nonzero
+    impulses) must equal a fresh step at that point bit for bit: the D2H caps of
+    the captured copies are per graph, and a result with more nonzeros takes the
+    tail copy + recapture path."""
+    from paper_2604_09993_b200.subproblem import GpuSCPStep
+
+    g = load_golden(name)
+    sc = golden_scenario(name)
+    lay_dim = g["ig_z"].size
+    rng = np.random.default_rng(3)
+    z2 = g["ig_z"].copy()
+    from paper_2604_09993_b200.scenario import Layout
+
+    lay = Layout(sc)
+    for k in range(lay.N):  # impulses on: more nonzeros in the node rows
+        z2[lay.phi(k)] = rng.uniform(0.1, 0.5, size=2 * lay.n_c)
+    assert z2.size == lay_dim
+    a = GpuSCPStep(sc)
+    for _ in range(2):
+        a.iterate(g["ig_z"], 1.0, precondition=precondition)
+    ra = a.iterate(z2, 0.5, precondition=precondition)
+    rb = GpuSCPStep(sc, use_graph=False).iterate(z2, 0.5, precondition=precondition)
+    for M in ("A", "G"):
+        ma, mb = getattr(ra[1], M), getattr(rb[1], M)
+        assert np.array_equal(ma.indptr, mb.indptr) and np.array_equal(ma.indices, mb.indices)
+        assert np.array_equal(ma.data, mb.data)
+    assert np.array_equal(ra[1].b, rb[1].b) and np.array_equal(ra[1].h, rb[1].h)
+    ra2 = a.iterate(g["ig_z"], 1.0, precondition=precondition)  # and back
+    rc = GpuSCPStep(sc, use_graph=False).iterate(g["ig_z"], 1.0, precondition=precondition)
+    assert np.array_equal(ra2[1].A.data, rc[1].A.data) and np.array_equal(ra2[1].A.indices, rc[1].A.indices)

@@ -23,7 +23,12 @@ for _ in range(rounds):
         env = dict(os.environ)
         if v != "main":
             env["CITO_LIB_VARIANT"] = v
-        out = subprocess.run([sys.executable, "tools/quick_time.py"] + qargs, capture_output=True, text=True, env=env)
+        script = os.environ.get("AB_SCRIPT", "tools/quick_time.py")
+        if "=" in v:  # name=ENV=VALUE: the main library with an environment switch
+            name, k, val = v.split("=", 2)
+            env.pop("CITO_LIB_VARIANT", None)
+            env[k] = val
+        out = subprocess.run([sys.executable, script] + qargs, capture_output=True, text=True, env=env)
         for line in out.stdout.splitlines():
             m = re.match(r"B=(\d+) (\w+): ([0-9.]+) ms", line)
             if m:
