@@ -172,10 +172,20 @@ cito_status launch_node(const KParams& P, int64_t Np, int64_t Nn, const double* 
   constexpr int NQ = 3 * M::NL, NC = M::NC, NY = 5 * NC + M::NGO;
   const int64_t total = Np * (2 * NY) + Nn * (3 * NQ + 3 * NC) + Nn * (3 * NQ + 2 * NC);
   if (total <= 0) return CITO_OK;
-  const int nt = 64;
   count_launch();
-  k_node<M><<<(unsigned)((total + nt - 1) / nt), nt, 0, st>>>(P, Np, Nn, y_pairs, theta_vecs, delta, eps, psi,
-                                                               psi_jac, th, th_jac, imp, imp_jac, zs);
+  // warp per item (k_node_w) by default; CITO_K3=1: thread per (item, direction) (k_node)
+  static const bool thread_per_dir = getenv("CITO_K3") && getenv("CITO_K3")[0] == '1';
+  const size_t tsm = (size_t)K3W_WARPS * NodeTile<M>::N * sizeof(double);
+  static const bool ok_w = smem_ok(k_node_w<M>, tsm);
+  if (!thread_per_dir && ok_w) {
+    const int64_t warps = Np + 2 * Nn;
+    k_node_w<M><<<(unsigned)((warps + K3W_WARPS - 1) / K3W_WARPS), 32 * K3W_WARPS, tsm, st>>>(
+        P, Np, Nn, y_pairs, theta_vecs, delta, eps, psi, psi_jac, th, th_jac, imp, imp_jac, zs);
+  } else {
+    const int nt = 64;
+    k_node<M><<<(unsigned)((total + nt - 1) / nt), nt, 0, st>>>(P, Np, Nn, y_pairs, theta_vecs, delta, eps, psi,
+                                                                 psi_jac, th, th_jac, imp, imp_jac, zs);
+  }
   CUDA_TRY(cudaGetLastError());
   return CITO_OK;
 }

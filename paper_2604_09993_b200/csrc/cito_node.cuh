@@ -430,3 +430,140 @@ __global__ void __launch_bounds__(64, CITO_K3_MINB) k_node(const KParams P, int6
     }
   }
 }
+
+// ---------------------------------------------------------------------------
+// K3, warp per node item (default): the same dual-number code as k_node, but a warp
+// owns one item (an interval's psi block, a node's theta or impulse block) and its
+// lanes evaluate only the input directions whose column can be nonzero for the
+// topology (NodeDirs below: e.g. HalfCheetah impulse map 32 of 67, theta 24 of 69).
+// The other columns are structural: zero, or the identity of v+ in the impulse
+// defect v+ - impact_map(...).  Columns are assembled in a shared-memory tile and
+// the warp writes the item's whole Jacobian block row by row (contiguous,
+// coalesced, every sector written once) instead of 67 scattered column writes.
+// Every computed entry is bit-identical to k_node's (same operations per direction).
+template <class M>
+struct NodeDirs {
+  static constexpr int NL = M::NL, NC = M::NC, NQ = 3 * NL;
+  static constexpr int NV = 3 * NQ + 3 * NC, NI = 3 * NQ + 2 * NC;
+  static constexpr bool contact_link(int l) {
+    for (int i = 0; i < NC; ++i)
+      if (M::clink(i) == l) return true;
+    return false;
+  }
+  // impulse map (contact_dynamics.py:111-124): link angles move the anchors, the Gram
+  // matrix and the contact lever arms; contact-link positions move the contact frame
+  // (implicit terrain only); v- and the impulses enter the solve; v+ only as identity
+  static constexpr bool imp_live(int d) {
+    if (d < NQ) return d % 3 == 2 || (M::IMPLICIT && contact_link(d / 3));
+    if (d < 2 * NQ) return true;
+    if (d < 3 * NQ) return false;
+    return true;
+  }
+  // impact residuals (contact_dynamics.py:134-172): only the contact links' q, v-, v+
+  // and the contact impulses / Gamma
+  static constexpr bool th_live(int d) {
+    if (d < 3 * NQ) return contact_link((d % NQ) / 3);
+    return true;
+  }
+  int imp[NI > 0 ? NI : 1], th[NV > 0 ? NV : 1];
+  int n_imp, n_th;
+  constexpr NodeDirs() : imp(), th(), n_imp(0), n_th(0) {
+    for (int d = 0; d < NI; ++d)
+      if (imp_live(d)) imp[n_imp++] = d;
+    for (int d = 0; d < NV; ++d)
+      if (th_live(d)) th[n_th++] = d;
+  }
+};
+
+// the live-direction tables in constant memory (indexed by lane at run time)
+template <class M>
+__constant__ const NodeDirs<M> kNodeDirs = NodeDirs<M>();
+
+template <class M>
+struct NodeTile {
+  static constexpr int NL = M::NL, NC = M::NC, NQ = 3 * NL, NY = 5 * NC + M::NGO;
+  static constexpr int NPSI = 3 * NC + M::NGO, NV = 3 * NQ + 3 * NC, NI = 3 * NQ + 2 * NC;
+  static constexpr int A = NPSI * 2 * NY, B = 6 * NC * NV, C = NQ * NI;
+  static constexpr int N = A > B ? (A > C ? A : C) : (B > C ? B : C);  // doubles per warp
+};
+
+#define K3W_WARPS 4
+template <class M>
+__global__ void __launch_bounds__(32 * K3W_WARPS) k_node_w(const KParams P, int64_t Np, int64_t Nn,
+                                                          const double* __restrict__ y_pairs,
+                                                          const double* __restrict__ theta_vecs, double delta, double eps,
+                                                          double* __restrict__ psi, double* __restrict__ psi_jac,
+                                                          double* __restrict__ th, double* __restrict__ th_jac,
+                                                          double* __restrict__ imp, double* __restrict__ imp_jac,
+                                                          const ZSrc zs) {
+  using T = NodeTile<M>;
+  constexpr int NC = M::NC, NQ = T::NQ, NY = T::NY, NPSI = T::NPSI, NV = T::NV, NI = T::NI;
+  constexpr int NXT = 2 * NQ + NY;
+  constexpr NodeDirs<M> DIRC{};  // compile-time counts
+  const NodeDirs<M>& DIRS = kNodeDirs<M>;
+  extern __shared__ __align__(16) double k3_tile[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  double* tile = k3_tile + (size_t)wib * T::N;
+  if (zs.de) {  // relaxation parameters from device memory (CUDA-graph replays)
+    delta = zs.de[0];
+    eps = zs.de[1];
+  }
+  const int64_t w = (int64_t)blockIdx.x * K3W_WARPS + wib;
+  if (w < Np) {  // psi of interval k: 2 NY directions, all live (ocp.py:277-287)
+    const int64_t k = w;
+    const double* ya = y_pairs + k * 2 * NY;
+    const double* yb = ya + NY;
+    if (zs.z) {
+      const double* zb = zs.z + (k / zs.n_int) * zs.zstride;
+      const int64_t kk = k % zs.n_int;
+      ya = zb + (2 * kk + 1) * NXT + 2 * NQ;
+      yb = zb + (2 * kk + 2) * NXT + 2 * NQ;
+    }
+    for (int d = lane; d < 2 * NY; d += 32)
+      node_psi<M>(P, ya, yb, d, delta, eps, d == 0 ? psi + k * NPSI : nullptr, tile + d, 2 * NY);
+    __syncwarp();
+    double* dst = psi_jac + k * T::A;
+    for (int e = lane; e < T::A; e += 32) dst[e] = tile[e];
+    return;
+  }
+  const int64_t wn = w - Np;
+  if (wn >= 2 * Nn) return;
+  const bool is_th = wn < Nn;
+  const int64_t k = is_th ? wn : wn - Nn;
+  NodeIn x{theta_vecs + k * NV, theta_vecs + k * NV + 2 * NQ, theta_vecs + k * NV + 3 * NQ, 2 * NQ, 3 * NQ, 0};
+  if (zs.z) {
+    const double* zb = zs.z + (k / zs.n_node) * zs.zstride;
+    const int64_t kk = k % zs.n_node;
+    x.p0 = zb + 2 * kk * NXT;
+    x.p1 = zb + (2 * kk + 1) * NXT + NQ;
+    x.p2 = zb + zs.base_p + 3 * NC * kk;
+  }
+  if (is_th) {
+    if constexpr (NC > 0) {
+      constexpr int NCOL = NV, NROW = 6 * NC;
+      for (int e = lane; e < NROW * NCOL; e += 32) tile[e] = 0.0;  // structural zeros
+      __syncwarp();
+      for (int i = lane; i < DIRC.n_th; i += 32) {
+        x.dir = DIRS.th[i];
+        node_theta<M>(P, x, delta, i == 0 ? th + k * NROW : nullptr, tile + x.dir, NCOL);
+      }
+      __syncwarp();
+      double* dst = th_jac + k * T::B;
+      for (int e = lane; e < T::B; e += 32) dst[e] = tile[e];
+    }
+  } else {
+    constexpr int NCOL = NI, NROW = NQ;
+    for (int e = lane; e < NROW * NCOL; e += 32) {
+      const int r = e / NCOL, c = e % NCOL;
+      tile[e] = (c == 2 * NQ + r) ? 1.0 : 0.0;  // d(v+ - impact_map)/dv+ = I; other dead columns 0
+    }
+    __syncwarp();
+    for (int i = lane; i < DIRC.n_imp; i += 32) {
+      x.dir = DIRS.imp[i];
+      node_impulse<M>(P, x, i == 0 ? imp + k * NQ : nullptr, tile + x.dir, NCOL);
+    }
+    __syncwarp();
+    double* dst = imp_jac + k * T::C;
+    for (int e = lane; e < T::C; e += 32) dst[e] = tile[e];
+  }
+}
