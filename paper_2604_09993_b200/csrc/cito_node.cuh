@@ -508,9 +508,12 @@ __global__ void __launch_bounds__(32 * K3W_WARPS) k_node_w(const KParams P, int6
     delta = zs.de[0];
     eps = zs.de[1];
   }
+  // warp order: impulse items, theta items, psi items -- the heaviest first, so the
+  // light ones fill the tail of the launch
   const int64_t w = (int64_t)blockIdx.x * K3W_WARPS + wib;
-  if (w < Np) {  // psi of interval k: 2 NY directions, all live (ocp.py:277-287)
-    const int64_t k = w;
+  if (w >= 2 * Nn) {  // psi of interval k: 2 NY directions, all live (ocp.py:277-287)
+    const int64_t k = w - 2 * Nn;
+    if (k >= Np) return;
     const double* ya = y_pairs + k * 2 * NY;
     const double* yb = ya + NY;
     if (zs.z) {
@@ -526,10 +529,8 @@ __global__ void __launch_bounds__(32 * K3W_WARPS) k_node_w(const KParams P, int6
     for (int e = lane; e < T::A; e += 32) dst[e] = tile[e];
     return;
   }
-  const int64_t wn = w - Np;
-  if (wn >= 2 * Nn) return;
-  const bool is_th = wn < Nn;
-  const int64_t k = is_th ? wn : wn - Nn;
+  const bool is_th = w >= Nn;
+  const int64_t k = is_th ? w - Nn : w;
   NodeIn x{theta_vecs + k * NV, theta_vecs + k * NV + 2 * NQ, theta_vecs + k * NV + 3 * NQ, 2 * NQ, 3 * NQ, 0};
   if (zs.z) {
     const double* zb = zs.z + (k / zs.n_node) * zs.zstride;
