@@ -143,30 +143,12 @@ __device__ __forceinline__ void node_theta(const KParams& P, const NodeIn& x, do
   }
 }
 
-// Block pattern of the joint Gram matrix (joints coupled iff they share a link) and
-// of its Cholesky factor in JOINT order, fill included (symbolic elimination at
-// compile time).  Skipping the structural zeros leaves every computed value
-// bit-identical to the dense factorisation (the skipped terms are exact zeros).
-template <class M>
-struct JointFill {
-  static constexpr int NB = M::NJ > 0 ? M::NJ : 1;
-  bool g[NB][NB], l[NB][NB];
-  constexpr JointFill() : g(), l() {
-    for (int j = 0; j < M::NJ; ++j)
-      for (int k = 0; k < M::NJ; ++k) {
-        const int pj = M::jparent(j), cj = M::jchild(j), pk = M::jparent(k), ck = M::jchild(k);
-        const bool share = j == k || (pj >= 0 && (pj == pk || pj == ck)) || cj == ck || (pk >= 0 && cj == pk);
-        g[j][k] = share;
-        l[j][k] = share;
-      }
-    for (int c = 0; c < M::NJ; ++c)
-      for (int r = c + 1; r < M::NJ; ++r)
-        if (l[r][c])
-          for (int r2 = c + 1; r2 <= r; ++r2)
-            if (l[r2][c]) l[r][r2] = l[r2][r] = true;
-  }
-};
-
+// The block pattern of the joint Gram matrix in joint order (joints coupled iff they
+// share a link) and of its Cholesky factor with fill come from the generated
+// topology (M::jfill_g / M::jfill_l, gen_models.py::joint_fill): constexpr bit tests
+// that fold away in the unrolled loops, so the factor lives in registers.  Skipping
+// the structural zeros leaves every computed value bit-identical to the dense
+// factorisation (the skipped terms are exact zeros).
 // Entry (2j+al, 2k+be) of the joint Gram matrix J M^-1 J^T in dual arithmetic
 // (contact_dynamics.py:91-92), from the rotated joint anchors R[joint][side][xz].
 template <class M, int NJP>
@@ -240,7 +222,6 @@ __device__ __forceinline__ void node_impulse(const KParams& P, const NodeIn& x, 
     // tangent along this thread's direction, nonzero for link angles only, is
     // recomputed where the solve needs it)
     constexpr int NPK = NJ2 * (NJ2 + 1) / 2;
-    constexpr JointFill<M> F{};
     double Lv[NPK];
 #pragma unroll
     for (int e = 0; e < NPK; ++e) Lv[e] = 0.0;  // fill entries start at 0
@@ -253,7 +234,7 @@ __device__ __forceinline__ void node_impulse(const KParams& P, const NodeIn& x, 
         for (int al = 0; al < 2; ++al)
 #pragma unroll
           for (int be = 0; be < 2; ++be) {
-            if ((j == k && be > al) || !F.g[j][k]) continue;
+            if ((j == k && be > al) || !M::jfill_g(j, k)) continue;
             Lv[LI(2 * j + al, 2 * k + be)] = gram(j, k, al, be).v;
           }
     // rhs = J (v- + M^-1 w)
@@ -291,16 +272,16 @@ __device__ __forceinline__ void node_impulse(const KParams& P, const NodeIn& x, 
       double d = Lv[LI(cc, cc)];
 #pragma unroll
       for (int k = 0; k < cc; ++k)
-        if (F.l[cc / 2][k / 2]) d = d - Lv[LI(cc, k)] * Lv[LI(cc, k)];
+        if (M::jfill_l(cc / 2, k / 2)) d = d - Lv[LI(cc, k)] * Lv[LI(cc, k)];
       Lv[LI(cc, cc)] = sqrt(d);
       Li[cc] = 1.0 / Lv[LI(cc, cc)];
 #pragma unroll
       for (int r = cc + 1; r < NJ2; ++r) {
-        if (!F.l[r / 2][cc / 2]) continue;
+        if (!M::jfill_l(r / 2, cc / 2)) continue;
         double x2 = Lv[LI(r, cc)];
 #pragma unroll
         for (int k = 0; k < cc; ++k)
-          if (F.l[r / 2][k / 2] && F.l[cc / 2][k / 2]) x2 = x2 - Lv[LI(r, k)] * Lv[LI(cc, k)];
+          if (M::jfill_l(r / 2, k / 2) && M::jfill_l(cc / 2, k / 2)) x2 = x2 - Lv[LI(r, k)] * Lv[LI(cc, k)];
         Lv[LI(r, cc)] = x2 * Li[cc];
       }
     }
@@ -309,7 +290,7 @@ __device__ __forceinline__ void node_impulse(const KParams& P, const NodeIn& x, 
       double x2 = xv[r];
 #pragma unroll
       for (int k = 0; k < r; ++k)
-        if (F.l[r / 2][k / 2]) x2 = x2 - Lv[LI(r, k)] * xv[k];
+        if (M::jfill_l(r / 2, k / 2)) x2 = x2 - Lv[LI(r, k)] * xv[k];
       xv[r] = x2 * Li[r];
     }
 #pragma unroll
@@ -317,7 +298,7 @@ __device__ __forceinline__ void node_impulse(const KParams& P, const NodeIn& x, 
       double x2 = xv[r];
 #pragma unroll
       for (int k = r + 1; k < NJ2; ++k)
-        if (F.l[k / 2][r / 2]) x2 = x2 - Lv[LI(k, r)] * xv[k];
+        if (M::jfill_l(k / 2, r / 2)) x2 = x2 - Lv[LI(k, r)] * xv[k];
       xv[r] = x2 * Li[r];
     }
     if (x.dir < NQ && x.dir % 3 == 2) {  // only link angles move G
@@ -325,7 +306,7 @@ __device__ __forceinline__ void node_impulse(const KParams& P, const NodeIn& x, 
     for (int r = 0; r < NJ2; ++r)
 #pragma unroll
       for (int c = 0; c < NJ2; ++c)
-        if (F.g[r / 2][c / 2]) {
+        if (M::jfill_g(r / 2, c / 2)) {
           const Dn g = r >= c ? gram(r / 2, c / 2, r % 2, c % 2) : gram(c / 2, r / 2, c % 2, r % 2);
           dx[r] = __dsub_rn(dx[r], __dmul_rn(g.d, xv[c]));
         }
@@ -335,7 +316,7 @@ __device__ __forceinline__ void node_impulse(const KParams& P, const NodeIn& x, 
       double x2 = dx[r];
 #pragma unroll
       for (int k = 0; k < r; ++k)
-        if (F.l[r / 2][k / 2]) x2 = __dsub_rn(x2, __dmul_rn(Lv[LI(r, k)], dx[k]));
+        if (M::jfill_l(r / 2, k / 2)) x2 = __dsub_rn(x2, __dmul_rn(Lv[LI(r, k)], dx[k]));
       dx[r] = x2 * Li[r];
     }
 #pragma unroll
@@ -343,7 +324,7 @@ __device__ __forceinline__ void node_impulse(const KParams& P, const NodeIn& x, 
       double x2 = dx[r];
 #pragma unroll
       for (int k = r + 1; k < NJ2; ++k)
-        if (F.l[k / 2][r / 2]) x2 = __dsub_rn(x2, __dmul_rn(Lv[LI(k, r)], dx[k]));
+        if (M::jfill_l(k / 2, r / 2)) x2 = __dsub_rn(x2, __dmul_rn(Lv[LI(k, r)], dx[k]));
       dx[r] = x2 * Li[r];
     }
     Dn z[NJ2];

@@ -120,6 +120,26 @@ def chol_code(nj, lnz):
     return "".join(f)
 
 
+def joint_fill(joints):
+    """Block pattern of the joint Gram matrix in JOINT order (joints coupled iff they
+    share a link) and of its Cholesky factor with fill (symbolic elimination in joint
+    order) -- K3's factorisation order (csrc/cito_node.cuh)."""
+    nj = len(joints)
+    g = [[False] * nj for _ in range(nj)]
+    for j in range(nj):
+        for k in range(nj):
+            pj, cj, pk, ck = joints[j][0], joints[j][1], joints[k][0], joints[k][1]
+            g[j][k] = j == k or (pj >= 0 and (pj == pk or pj == ck)) or cj == ck or (pk >= 0 and cj == pk)
+    lm = [row[:] for row in g]
+    for c in range(nj):
+        for r in range(c + 1, nj):
+            if lm[r][c]:
+                for r2 in range(c + 1, r + 1):
+                    if lm[r2][c]:
+                        lm[r][r2] = lm[r2][r] = True
+    return g, lm
+
+
 def chol_code_llt(nj, lnz):
     """(A/B only, CITO_CHOL=llt) Straight-line scalar sparse Cholesky + both triangular solves of the 2 nj x 2 nj
     joint Gram matrix in elimination order (only structurally nonzero entries,
@@ -243,6 +263,11 @@ def main(out_path, entries=None):
               + "".join(f"a == {i} ? {v}u : " for i, v in enumerate(lbits)) + "0u) >> b) & 1u; }\n")
         if joints:
             s += (chol_code_llt if os.environ.get("CITO_CHOL") == "llt" else chol_code)(len(joints), lnz)
+        jg, jl_ = joint_fill(joints)
+        for nm, mat in (("jfill_g", jg), ("jfill_l", jl_)):
+            bits = [sum(1 << b for b in range(len(joints)) if mat[a][b]) for a in range(len(joints))]
+            s += (f"  __host__ __device__ static constexpr bool {nm}(int a, int b) {{ return (("
+                  + "".join(f"a == {i} ? {v}u : " for i, v in enumerate(bits)) + "0u) >> b) & 1u; }\n")
         s += f"  static constexpr int NHCOL = {len(heavy)}, NLCOL = {len(light)};\n"
         s += chain("hcol", heavy)
         s += chain("lcol", light)

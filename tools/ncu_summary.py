@@ -1,6 +1,6 @@
 """Summarise ncu captures into profiles/ (committed evidence).
 
-  python tools/ncu_summary.py full <report.ncu-rep> <tag> <key>   -> profiles/ncu_<tag>.json (+ ncu_summary.json[key])
+  python tools/ncu_summary.py full <report.ncu-rep | raw.csv> <tag> <key>   -> profiles/ncu_<tag>.json (+ ncu_summary.json[key])
   python tools/ncu_summary.py launches <launches.csv> <tag>       -> profiles/launches_<tag>.json
 """
 
@@ -39,7 +39,9 @@ UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "M
 
 
 def full(rep, tag, key):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    # a report (.ncu-rep) or its `--page raw --csv` export (made on the GPU box)
+    out = open(rep).read() if rep.endswith(".csv") else subprocess.run(
+        ["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     h, units = rows[0], rows[1]
     kernels = []
