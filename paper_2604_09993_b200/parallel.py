@@ -144,6 +144,12 @@ class HostResult:
             dist.broadcast_object_list(name, src=_global_rank(group, 0), group=group)
         if self.rank != 0:
             self.shm = shared_memory.SharedMemory(name=name[0])
+            try:  # the segment belongs to rank 0: keep this process's tracker from unlinking it at exit
+                from multiprocessing import resource_tracker
+
+                resource_tracker.unregister(self.shm._name, "shared_memory")
+            except Exception:
+                pass
         self.buf = np.ndarray((self.nbytes,), dtype=np.uint8, buffer=self.shm.buf)
         self.arrays = {k: self.buf[o: o + int(np.prod(s)) * np.dtype(d).itemsize].view(d).reshape(s)
                        for k, (o, s, d) in self.layout.items()}
