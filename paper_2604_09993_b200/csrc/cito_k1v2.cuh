@@ -326,9 +326,21 @@ struct RegState {
 #define RS_YV rs[7]
 #define RS_HQ(h) rs[(h)]
 #define RS_HV(h) rs[RegState<M>::NH + (h)]
+#ifndef CITO_COL_SMEM
+#define CITO_COL_SMEM 0  // A/B: 1 = y-row accumulators in shared memory, 2 = + push rows
+#endif
+#if CITO_COL_SMEM >= 2
+#define RS_PQ(p) sh.PQ[(p)][col]
+#define RS_PV(p) sh.PV[(p)][col]
+#else
 #define RS_PQ(p) rs[2 * RegState<M>::NH + (p)]
 #define RS_PV(p) rs[2 * RegState<M>::NH + RegState<M>::NPU + (p)]
+#endif
+#if CITO_COL_SMEM >= 1
+#define RS_DY(k) sh.DY[(k)][col]
+#else
 #define RS_DY(k) rs[2 * RegState<M>::NH + 2 * RegState<M>::NPU + (k)]
+#endif
 
 template <class M>
 struct AuxScratch {
