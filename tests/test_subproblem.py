@@ -240,3 +240,40 @@ def test_gpu_scp_step_graph_replay_pattern_change(name, precondition):
     ra2 = a.iterate(g["ig_z"], 1.0, precondition=precondition)  # and back
     rc = GpuSCPStep(sc, use_graph=False).iterate(g["ig_z"], 1.0, precondition=precondition)
     assert np.array_equal(ra2[1].A.data, rc[1].A.data) and np.array_equal(ra2[1].A.indices, rc[1].A.indices)
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_packed_records_reproduce_reference_csc(name):
+    """The 16-byte records of k_csc_flat (subproblem.packed_entries), evaluated on the
+    host exactly as the kernel does (lin * w with w = sign * sigma folded), give the
+    reference CSC bit for bit; the tile column table covers every column once."""
+    from paper_2604_09993_b200.scenario import Layout, build_scaling
+    from paper_2604_09993_b200.subproblem import LIN_SOURCES, SubproblemPattern, packed_entries
+
+    g = load_golden(name)
+    sc = golden_scenario(name)
+    lay = Layout(sc)
+    pat = SubproblemPattern(sc, lay, build_scaling(sc, lay)[0])
+    lin = _lin(g, "sp0")
+    flat = [np.asarray(lin[k], dtype=float).reshape(-1) for k in LIN_SOURCES]
+    for M in ("A", "G"):
+        csc = getattr(pat, M)
+        rec, tcol = packed_entries(csc, pat.sigma_full())
+        src = (rec["key"] >> 27).astype(np.int64) - 1
+        idx = (rec["key"] & ((1 << 27) - 1)).astype(np.int64)
+        v = rec["w"].copy()
+        for s in np.unique(src[src >= 0]):
+            sel = src == s
+            v[sel] = flat[s][idx[sel]] * rec["w"][sel]
+        keep = v != 0.0
+        indptr = np.concatenate([[0], np.cumsum(np.bincount(csc["col"][keep], minlength=pat.n))])
+        assert np.array_equal(indptr, g[f"sp0_{M}_indptr"]) and np.array_equal(rec["row"][keep], g[f"sp0_{M}_indices"])
+        assert np.array_equal(v[keep], g[f"sp0_{M}_data"]), M
+        ntile = len(tcol) - 1
+        assert ntile == max(1, -(-rec.size // 2048)) and tcol[0] == 0 and tcol[-1] == pat.n + 1
+        sp = csc["indptr"]
+        for t in range(ntile):  # columns owned by tile t start inside it (the last tile takes the tail)
+            cols = np.arange(tcol[t], min(tcol[t + 1], pat.n + 1))
+            assert np.all(sp[cols] >= 2048 * t)
+            if t < ntile - 1:
+                assert np.all(sp[cols] < 2048 * (t + 1))
