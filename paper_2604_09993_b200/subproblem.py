@@ -240,11 +240,14 @@ class SubproblemPattern:
         return np.concatenate([self.sigma, np.ones(self.n - self.lay.dim)])
 
     def objective_c(self, z_j):
-        """c of the subproblem at iterate z_j (scp.py:341-346, conic.py:227-229)."""
+        """c of the subproblem at iterate z_j (scp.py:341-346, conic.py:227-229).
+        Same floating-point operations as ``c[:dim] + (-2 w) * ((z - 0) / sigma)``
+        (z - 0.0 is z for every z, -0.0 included), with fewer temporaries."""
         dim = self.lay.dim
         c = self.c_fixed.copy()
-        add = -2.0 * self.w_prox * ((np.asarray(z_j, dtype=float) - 0.0) / self.sigma[:dim])
-        c[:dim] = c[:dim] + add
+        add = np.divide(np.asarray(z_j, dtype=float), self.sigma[:dim])
+        add *= -2.0 * self.w_prox
+        c[:dim] += add
         return c
 
     @staticmethod
@@ -1200,6 +1203,27 @@ class GpuSCPStep:
         else:
             self._launch(bool(precondition), hb)
         nA = pl["nA"]
+        # host work that does not depend on the device results runs while the GPU works:
+        # the objective, the (scaled) P, the lazy LinearizedProblem
+        zj = z if z_j is None else z_j
+        c = pat.objective_c(zj)
+        c_unscaled = c
+        P_data = pat.P_diag[: pat.lay.dim]
+        if precondition:  # cost normalization (conic.py:311-316)
+            omega = max(1.0, float(np.max(np.abs(c))) if c.size else 0.0)
+            if P_data.size:
+                omega = max(omega, float(np.max(np.abs(P_data))))
+            P = sp.csc_matrix((P_data * (1.0 / omega), pl["P_idx"], pl["P_ptr"]), shape=(pat.n, pat.n))
+            c = c / omega
+        else:
+            if pl["P_plain"] is None:  # constant: one read-only matrix shared by every result
+                Pm = sp.csc_matrix((P_data.copy(), pl["P_idx"].copy(), pl["P_ptr"].copy()), shape=(pat.n, pat.n))
+                for arr in (Pm.data, Pm.indices, Pm.indptr):
+                    arr.flags.writeable = False
+                pl["P_plain"] = Pm
+            P = pl["P_plain"]
+        lin = self._Lazy(hb.slot["lin"], z.copy())
+        ConicProgram, ConeSpec = _conic_types()
         stream.synchronize()  # the one synchronization
         hh = hb.h
         caps = hb.caps.get(bool(precondition), {})
@@ -1217,32 +1241,14 @@ class GpuSCPStep:
         bad = hh["bad"]
         if bad.any():
             raise FloatingPointError(f"non-finite state in intervals {np.where(bad != 0)[0].tolist()}")
-        ConicProgram, ConeSpec = _conic_types()
+        self._c_last = (zj, c_unscaled)  # the unscaled objective, for unscaled_program(z_j) of the same point
         mats = {}
         for M, nrows in (("A", nA), ("G", pl["nG"])):  # arrays over the pinned buffer (no copy)
             nnz = int(hh[f"{M}_indptr"][-1])
             mats[M] = _csc_direct(hb.wrap(f"{M}_data", 0, nnz), hb.wrap(f"{M}_indices", 0, nnz),
                                   hb.wrap(f"{M}_indptr", 0, pat.n + 1), (nrows, pat.n))
-        zj = z if z_j is None else z_j
-        c = pat.objective_c(zj)
-        self._c_last = (zj, c)  # the unscaled objective, for unscaled_program(z_j) of the same point
-        P_data = pat.P_diag[: pat.lay.dim]
-        if precondition:  # cost normalization (conic.py:311-316)
-            omega = max(1.0, float(np.max(np.abs(c))) if c.size else 0.0)
-            if P_data.size:
-                omega = max(omega, float(np.max(np.abs(P_data))))
-            P = sp.csc_matrix((P_data * (1.0 / omega), pl["P_idx"], pl["P_ptr"]), shape=(pat.n, pat.n))
-            c = c / omega
-        else:
-            if pl["P_plain"] is None:  # constant: one read-only matrix shared by every result
-                Pm = sp.csc_matrix((P_data.copy(), pl["P_idx"].copy(), pl["P_ptr"].copy()), shape=(pat.n, pat.n))
-                for arr in (Pm.data, Pm.indices, Pm.indptr):
-                    arr.flags.writeable = False
-                pl["P_plain"] = Pm
-            P = pl["P_plain"]
         prog = ConicProgram(P=P, c=c, A=mats["A"], b=hb.wrap("rhs", 0, nA), G=mats["G"], h=hb.wrap("rhs", nA, pl["nG"]),
                             cones=ConeSpec(nonneg=pat.n_orthant, soc=pat.soc_dims))
-        lin = self._Lazy(hb.slot["lin"], z.copy())
         import weakref
 
         hb.live.append(weakref.ref(lin))  # the slot's device outputs stay untouched while lin lives
