@@ -6,19 +6,20 @@
 // the per-stage work is split so that only the dependent chain of the RK stage
 // recursion sits on the critical path:
 //
-//   warp 0        stage t   critical chain only: stage input (lanes own state
-//                           coordinates, stage slopes in registers), sin/cos and
-//                           FOH control (lane per link / control), then ONE lane
-//                           runs kinematics -> forces -> Gram -> straight-line
-//                           sparse Cholesky (generated per topology) -> joint
-//                           reactions -> vdot, all in registers.
-//   warp 1        stage t-1 everything off the chain: contact frames, signed
-//                           distances, Omega and path rows, the y accumulators,
-//                           the dS terms of the q-row stage inputs.
-//   warps 2,3,4   stage t-2 rate Jacobian, one warp per direction kind (q, v, u),
-//                           forward-mode tangents specialised per kind so the
-//                           structurally zero seed terms are never evaluated.
-//   warps 5..     stage t-3 tangent columns (one thread per column).
+//   warp 0          stage t   critical chain only: stage input (lanes own state
+//                             coordinates, stage slopes in registers), sin/cos and
+//                             FOH control (lane per link / control), then ONE lane
+//                             runs kinematics -> forces -> Gram -> straight-line
+//                             block LDL^T (generated per topology) -> joint
+//                             reactions -> vdot, all in registers.
+//   warps 1..NCW    stage t-3 tangent columns (one thread per column).
+//   warp NCW+1      stage t-2 rate Jacobian: one lane per input direction (q, v and
+//                             u; generic forward-mode tangent code, one code path).
+//   warp NCW+2      stage t-1 everything off the chain: contact frames, signed
+//                             distances, Omega and path rows, the y accumulators,
+//                             the dS terms of the q-row stage inputs.
+// (CITO_JAC_ONE_WARP=0 restores round 1's layout: separate q/v and u Jacobian warps
+// with direction-kind-specialised code.)
 //
 // A 4-slot ring of per-stage records in shared memory carries the stage from
 // role to role; one __syncthreads per tick.
@@ -289,7 +290,11 @@ struct K2Dims {
   // distinct SM sub-partitions (warp w -> SMSP w % 4) and only the light ones
   // (off-chain aux, u Jacobian) share: 0 primal, 1..NCW columns, then q/v
   // Jacobian, aux, u Jacobian
-#if CITO_V2_SPLIT
+#if CITO_JAC_ONE_WARP == 2
+  // 5 warps: 0 primal, columns, all rate-Jacobian directions on one warp, aux
+  static constexpr int W_COL0 = 1, W_JQV = 1 + NCW, W_AUX = 2 + NCW, W_JU = -1, W_JV = -1;
+  static constexpr int NT = 32 * (3 + NCW);
+#elif CITO_V2_SPLIT
   // 7 warps: separate q and v Jacobian warps (0 primal, cols, q, aux, v, u)
   static constexpr int W_COL0 = 1, W_JQV = 1 + NCW, W_AUX = 2 + NCW, W_JV = 3 + NCW, W_JU = 4 + NCW;
   static constexpr int NT = 32 * (5 + NCW);
@@ -326,6 +331,14 @@ struct RegState {
 #define RS_YV rs[7]
 #define RS_HQ(h) rs[(h)]
 #define RS_HV(h) rs[RegState<M>::NH + (h)]
+#ifndef CITO_JAC_ONE_WARP
+// 2 (default): every rate-Jacobian direction (q, v and u: 32 for HalfCheetah) on ONE
+// warp with the generic tangent code (kind 7), 5 warps per CTA -- one hot code path
+// less per tick (measured 0.108 vs 0.114 ms for 29 intervals, same box); 1: the same
+// with the u-Jacobian warp kept idle; 0: q/v and u directions on two warps
+// (specialised kinds 3 and 4)
+#define CITO_JAC_ONE_WARP 2
+#endif
 #ifndef CITO_COL_SMEM
 #define CITO_COL_SMEM 0  // A/B: 1 = y-row accumulators in shared memory, 2 = + push rows
 #endif
@@ -941,6 +954,12 @@ __global__ void __launch_bounds__(JAC ? K2Dims<M>::NT : 64, MINB) k_linearize2(c
         const int st = t - 2;
         const Rec2<M>& R = sh.ring[st & 3];
         const double* v = R.xs + NQ;
+#if CITO_JAC_ONE_WARP  // every rate-Jacobian direction on one warp (generic kind 7)
+        if (warp == K::W_JQV) {
+          for (int kd = lane; kd < NDIR; kd += 32)
+            tan_rate_k<M, 7>(P, R.pr, v, kd < NDIRX ? M::dir(kd) : NX + (kd - NDIRX), &sh.At[st & 1][kd][0]);
+        }
+#else
         if (K::W_JV >= 0 && warp == K::W_JQV) {  // q directions (kind 1)
           for (int kd = lane; kd < K::NDIRQ; kd += 32)
             tan_rate_k<M, 1>(P, R.pr, v, M::dir(kd), &sh.At[st & 1][kd][0]);
@@ -954,6 +973,7 @@ __global__ void __launch_bounds__(JAC ? K2Dims<M>::NT : 64, MINB) k_linearize2(c
           for (int kd = NDIRX + lane; kd < NDIR; kd += 32)
             tan_rate_k<M, 4>(P, R.pr, v, NX + (kd - NDIRX), &sh.At[st & 1][kd][0]);
         }
+#endif
       }
     } else if (JAC && colthr && t >= 3) {
       const int st = t - 3;
