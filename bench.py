@@ -576,6 +576,7 @@ def run_ours(args):
     e2e_value = units_per_step * K / e2e_s
 
     peak = fp64_peak_tflops(torch, dev)
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
     F, fdef = flops_per_interval("halfcheetah_s8" if wl == "fine" else "halfcheetah_s5")
     Fx, fxsrc = executed_flops_per_interval(B_k1) if wl != "fine" else (None, None)
     achieved = F * B_k1 / (k1_ms * 1e-3) / 1e12 if F else None
@@ -586,6 +587,9 @@ def run_ours(args):
                 "kernel": k1_kernel_name(B_k1), "kernel_ms": k1_ms, "intervals_per_launch": B_k1,
                 "flops_per_interval": F, "flops_definition": fdef,
                 "achieved_executed": achieved_x, "frac_executed": (achieved_x / peak) if achieved_x else None,
+                # the latency kernel runs one CTA per interval: with fewer intervals than SMs only
+                # B_k1 of the SMs carry work, so the same time against their share of the peak
+                "frac_of_busy_sms": ((achieved / (peak * min(1.0, B_k1 / n_sm))) if achieved and B_k1 <= 98 else None),
                 "executed_flops_per_interval": Fx, "executed_source": fxsrc,
                 "peak_source": "measured in this run: FP64 DFMA probe kernel (cito_dfma_peak); MEASURED_PEAKS.json "
                                "has no fp64 entry"}
