@@ -647,6 +647,20 @@ def run_reference(args):
         legs["iteration"] = {"value": v, "ms_per_step": dt / n * 1e3, "steps": n}
         legs["linearize_only"] = {"value": lv, "ms_per_step": ldt / ln * 1e3, "steps": ln,
                                   "what": "oracle-port linearize_batch + node relations only (no assembly)"}
+        if it.tr is not None and wl == "scp":
+            # the reference's own linearize_batch (unmodified source) through the jax -> torch.func
+            # shim, a tiny sample: eager per-element AD, far slower than JAX/XLA would be -- context
+            # only, never the headline
+            import torch
+
+            torch.set_num_threads(os.cpu_count() or 1)
+            xs, us, ss = it.starts[:1], it.Us[:1], it.Ss[:1]
+            it.tr.discretizer.linearize_batch(xs, us, ss)
+            sv, sn, sdt = time_cpu(lambda: (it.tr.discretizer.linearize_batch(xs, us, ss), 1)[1], None, 1)
+            legs["reference_source_shim"] = {"value": sv, "ms_per_step": sdt / sn * 1e3, "steps": sn,
+                                             "what": "cito.augmentation.Discretizer.linearize_batch of 1 interval, "
+                                                     "unmodified reference source under the jax->torch.func shim "
+                                                     f"({torch.get_num_threads()} torch threads)"}
         sample = f"{what}; {n} steps in {dt:.1f} s"
     elif wl == "batch":
         sc = scp_problem(seed=0)
@@ -698,13 +712,19 @@ def run_reference(args):
     head = legs.get("iteration", legs["linearize_only"])
     v = head["value"]
     sample += f" on {pyoracle.get_threads()} of {os.cpu_count()} host cores"
+    cpu_model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            cpu_model = next((l.split(":", 1)[1].strip() for l in f if l.startswith("model name")), None)
+    except OSError:
+        pass
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": head["steps"],
             "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True,
             "scaling": "weak" if wl in ("scp", "fine") else "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic" if wl == "batch" else "synthetic (scenario initial guess; scp: seed = rank)",
             "impl": "reference", "config": config_for(args, world),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": pyoracle.get_threads(), "kind": "port",
-                             "sample": sample, "legs": legs,
+                             "cpu_model": cpu_model, "sample": sample, "legs": legs,
                              "note": "reference algorithm on host cores via the C oracle port (dense forward-mode "
                                      "duals like jacfwd, LU like jnp.linalg.solve); the reference's JAX runtime is "
                                      "not installable (no jax wheel, no network)"},
