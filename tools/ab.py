@@ -24,7 +24,12 @@ for _ in range(rounds):
         if v != "main":
             env["CITO_LIB_VARIANT"] = v
         script = os.environ.get("AB_SCRIPT", "tools/quick_time.py")
-        if "=" in v:  # name=ENV=VALUE: the main library with an environment switch
+        if ":" in v:  # variant:ENV=VALUE: a variant library with an environment switch
+            lib, spec = v.split(":", 1)
+            k, val = spec.split("=", 1)
+            env["CITO_LIB_VARIANT"] = lib
+            env[k] = val
+        elif "=" in v:  # name=ENV=VALUE: the main library with an environment switch
             name, k, val = v.split("=", 2)
             env.pop("CITO_LIB_VARIANT", None)
             env[k] = val
