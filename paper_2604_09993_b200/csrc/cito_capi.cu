@@ -711,7 +711,20 @@ cito_status cito_csc_assemble_packed_dev(int32_t nmat, int32_t ncols, const void
   LinTable L;
   for (int k = 0; k < 10; ++k) L.p[k] = lin ? lin[k] : nullptr;
   count_launch(1);
-  k_csc_flat<<<(unsigned)tiles, 256, 0, (cudaStream_t)stream>>>(ncols, a, L, ws);
+  // programmatic dependent launch (CITO_PDL=0 turns it off): the tiles take their tickets
+  // and load their records while the producing kernel (K1) finishes
+  static const bool pdl = !(getenv("CITO_PDL") && getenv("CITO_PDL")[0] == '0');
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)tiles);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, k_csc_flat, ncols, a, L, ws));
   CUDA_TRY(cudaGetLastError());
   return CITO_OK;
 }

@@ -824,6 +824,10 @@ __global__ void __launch_bounds__(JAC ? K2Dims<M>::NT : 64, MINB) k_linearize2(c
   Fused2Shared<M>& sh = *reinterpret_cast<Fused2Shared<M>*>(smem_raw);
   const int64_t b = blockIdx.x;
   if (b >= B) return;
+  // programmatic dependent launch: a kernel enqueued after this one with the PDL attribute
+  // (the CSC compaction) may start its independent prologue now; it waits for this grid's
+  // completion and memory before reading any result (griddepcontrol.wait)
+  asm volatile("griddepcontrol.launch_dependents;");
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t zp = zs.z ? b / zs.n_int : 0, zk = zs.z ? b % zs.n_int : 0;
   const double* zb = zs.z ? zs.z + zp * zs.zstride : nullptr;

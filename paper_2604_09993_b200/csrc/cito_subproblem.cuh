@@ -441,6 +441,10 @@ __global__ void __launch_bounds__(256) k_csc_flat(int32_t ncols, const CscPacked
       row[j] = 0;
     }
   }
+  // launched with programmatic dependent launch behind the linearization: everything
+  // above (ticket, record loads) overlapped the producer's tail; its results are read
+  // only after this point (a no-op for a normal launch)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 #pragma unroll
   for (int j = 0; j < CSC_TJ; ++j) {
     const int s = (int)(key[j] >> 27) - 1;

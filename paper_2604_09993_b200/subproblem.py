@@ -1073,10 +1073,10 @@ class GpuSCPStep:
         L = pl["L"]
         s = torch.cuda.current_stream(self.gt.device).cuda_stream
         pl["zde_dev"].copy_(pl["zde_pin"], non_blocking=True)
+        if precondition:  # before the linearization: nothing sits between K1 and the compaction
+            pl["rowmax"].zero_()
         h = self.gt.disc._h  # the handle's own library (a run-time compiled topology has its own)
         h.check(h.L.cito_linearize_all_dev2(*sl["lin_args"], *sl["lin_outs"], s), "linearize_all")
-        if precondition:
-            pl["rowmax"].zero_()
         # b/h of the linearized rows on a side stream, concurrently with the CSC compaction
         cur = torch.cuda.current_stream(self.gt.device)
         side = pl["side"]

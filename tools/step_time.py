@@ -24,11 +24,30 @@ for N in [int(a) for a in (sys.argv[1:] or ["30"])]:
     def lin():
         gt.linearize_device(z, 1.0, out=out)
 
+    lay = gt.lay
+    zh = z.cpu().numpy()
+    xs = torch.as_tensor(np.stack([zh[lay.xp(k)] for k in range(N - 1)]), device=dev)
+    us = torch.as_tensor(np.stack([zh[lay.u(k)] for k in range(N - 1)]), device=dev)
+    ss = torch.as_tensor(np.array([zh[lay.s(k)][0] for k in range(N - 1)]), device=dev)
+    kout = gt.disc.linearize_batch_device(xs, us, ss)
+    yp_i = gt._i_yp
+    th_i = gt._i_th
+
+    def k1():
+        gt.disc.linearize_batch_device(xs, us, ss, out=kout)
+
+    yp = z[yp_i].contiguous()
+    tv = z[th_i].contiguous()
+    nout = gt.nodes.device(yp, tv, 1.0, sc.ctcs_epsilon)
+
+    def k3():
+        gt.nodes.device(yp, tv, 1.0, sc.ctcs_epsilon, out=nout)
+
     def step():
         r = gt.linearize_device(z, 1.0, out=out)
         asm.assemble_device(r, z, reuse=True)
 
-    for name, fn in (("linearize_all", lin), ("step", step)):
+    for name, fn in (("k1_alone", k1), ("k3_alone", k3), ("linearize_all", lin), ("step", step)):
         for _ in range(5):
             fn()
         torch.cuda.synchronize()
