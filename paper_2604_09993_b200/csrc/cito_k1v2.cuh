@@ -27,9 +27,6 @@
 
 #include "cito_kernels.cuh"
 
-#ifndef CITO_V2_SPLIT
-#define CITO_V2_SPLIT 0  // 1: separate q and v rate-Jacobian warps (7 warps)
-#endif
 
 // ---------------------------------------------------------------------------
 // Rate-Jacobian column of one input direction, specialised on the direction
@@ -286,30 +283,19 @@ template <class M>
 struct K2Dims {
   using D = Dims<M>;
   static constexpr int NCW = (D::NCOL + 31) / 32;
-  // warp roles, ordered so the heavy roles (primal, columns, q/v Jacobian) sit on
-  // distinct SM sub-partitions (warp w -> SMSP w % 4) and only the light ones
-  // (off-chain aux, u Jacobian) share: 0 primal, 1..NCW columns, then q/v
-  // Jacobian, aux, u Jacobian
+  // warp roles, ordered so the heavy roles (primal, columns, rate Jacobian) sit on
+  // distinct SM sub-partitions (warp w -> SMSP w % 4): 0 primal, 1..NCW columns, then
+  // the rate Jacobian and the off-chain aux warp (+ the u-Jacobian warp in the
+  // CITO_JAC_ONE_WARP=0/1 layouts)
 #if CITO_JAC_ONE_WARP == 2
-  // 5 warps: 0 primal, columns, all rate-Jacobian directions on one warp, aux
-  static constexpr int W_COL0 = 1, W_JQV = 1 + NCW, W_AUX = 2 + NCW, W_JU = -1, W_JV = -1;
+  static constexpr int W_COL0 = 1, W_JQV = 1 + NCW, W_AUX = 2 + NCW, W_JU = -1;
   static constexpr int NT = 32 * (3 + NCW);
-#elif CITO_V2_SPLIT
-  // 7 warps: separate q and v Jacobian warps (0 primal, cols, q, aux, v, u)
-  static constexpr int W_COL0 = 1, W_JQV = 1 + NCW, W_AUX = 2 + NCW, W_JV = 3 + NCW, W_JU = 4 + NCW;
-  static constexpr int NT = 32 * (5 + NCW);
 #else
-  static constexpr int W_COL0 = 1, W_JQV = 1 + NCW, W_AUX = 2 + NCW, W_JU = 3 + NCW, W_JV = -1;
+  static constexpr int W_COL0 = 1, W_JQV = 1 + NCW, W_AUX = 2 + NCW, W_JU = 3 + NCW;
   static constexpr int NT = 32 * (4 + NCW);
 #endif
   static constexpr int NX = D::NX;
   static constexpr int PER = (NX + 31) / 32;  // state coordinates per lane of warp 0
-  static constexpr int count_q() {
-    int n = 0;
-    for (int i = 0; i < M::NDIRX; ++i) n += M::dir(i) < 3 * M::NL ? 1 : 0;
-    return n;
-  }
-  static constexpr int NDIRQ = count_q();
 };
 
 // Per-thread state that lives across ticks, one union for all roles (each thread
@@ -953,7 +939,7 @@ __global__ void __launch_bounds__(JAC ? K2Dims<M>::NT : 64, MINB) k_linearize2(c
       }
     } else if (warp == W_AUX) {
       if (t >= 1 && t <= NST) aux_stage<M>(P, sh, t - 1, lane, rs);
-    } else if (JAC && (warp == K::W_JQV || warp == K::W_JU || warp == K::W_JV)) {
+    } else if (JAC && (warp == K::W_JQV || warp == K::W_JU)) {
       if (t >= 2 && t <= NST + 1) {
         const int st = t - 2;
         const Rec2<M>& R = sh.ring[st & 3];
@@ -964,13 +950,7 @@ __global__ void __launch_bounds__(JAC ? K2Dims<M>::NT : 64, MINB) k_linearize2(c
             tan_rate_k<M, 7>(P, R.pr, v, kd < NDIRX ? M::dir(kd) : NX + (kd - NDIRX), &sh.At[st & 1][kd][0]);
         }
 #else
-        if (K::W_JV >= 0 && warp == K::W_JQV) {  // q directions (kind 1)
-          for (int kd = lane; kd < K::NDIRQ; kd += 32)
-            tan_rate_k<M, 1>(P, R.pr, v, M::dir(kd), &sh.At[st & 1][kd][0]);
-        } else if (K::W_JV >= 0 && warp == K::W_JV) {  // v directions (kind 2)
-          for (int kd = K::NDIRQ + lane; kd < NDIRX; kd += 32)
-            tan_rate_k<M, 2>(P, R.pr, v, M::dir(kd), &sh.At[st & 1][kd][0]);
-        } else if (warp == K::W_JQV) {  // q and v directions (kinds 1 | 2)
+        if (warp == K::W_JQV) {  // q and v directions (kinds 1 | 2)
           for (int kd = lane; kd < NDIRX; kd += 32)
             tan_rate_k<M, 3>(P, R.pr, v, M::dir(kd), &sh.At[st & 1][kd][0]);
         } else {  // control directions (kind 4)
