@@ -28,8 +28,11 @@ Line fields:
          max over ranks.
   e2e    the same metric through the public API with host buffers:
          scp/fine: GpuSCPStep.iterate -- pinned H2D of [z, delta, epsilon], the
-           device step, ONE packed D2H of the assembled program (CSC arrays, b,
-           h, flags); the returned LinearizedProblem stays device-backed (lazy:
+           device step whose last kernels write the assembled program into a
+           pinned host buffer (CSC values and column pointers, b, h, flags; the
+           CSC row indices only when that buffer does not hold the current
+           sparsity pattern -- the compaction flags a moved pattern); the
+           returned LinearizedProblem stays device-backed (lazy:
            cito.scp.solve only hands it to build_subproblem), so its Jacobians
            are not copied (h2d/d2h bytes per step are reported).
          batch: Discretizer.linearize_batch (N=1) / ShardedBatch.linearize(...,
@@ -462,7 +465,8 @@ def run_ours(args):
 
         e2e_step()
         h2d = z.nbytes + 16  # z plus [delta, epsilon] (one pinned H2D per step)
-        d2h = scp_api.d2h_bytes()  # packed D2H per step: fixed fields + the CSC arrays up to their caps
+        d2h = None  # counted over the timed steps (GpuSCPStep.d2h_copied): fixed fields + CSC values, + the
+        # CSC row indices in a step whose result buffer does not hold the current pattern
         e2e_note = "GpuSCPStep.iterate: host z in, host scipy program out; LinearizedProblem device-backed (lazy)"
     elif wl == "batch":
         B = args.batch
@@ -565,10 +569,13 @@ def run_ours(args):
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
+    c0 = scp_api.d2h_copied if wl in ("scp", "fine") else 0
     t0 = time.perf_counter()
     for _ in range(K):
         e2e_step()
     e2e_s = time.perf_counter() - t0
+    if d2h is None:
+        d2h = (scp_api.d2h_copied - c0) / K
     if dist:
         t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

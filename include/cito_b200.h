@@ -245,12 +245,24 @@ cito_status cito_csc_assemble2_dev(int32_t nmat, int32_t ncols, const int64_t* c
  * zero before the first call; the kernel leaves it zero (zero it again after a
  * call that returned CITO_ERR_CUDA).  Pointer arguments except ws, lin (host
  * array of 10 device pointers) and the host arrays nsup/ntile are host arrays of
- * nmat device pointers. */
+ * nmat device pointers.  stamp_in / changed_at (device doubles, both null or both
+ * set): when any row index or column pointer written differs from what out_rows /
+ * out_ptr held before the call, *changed_at = *stamp_in -- the caller learns that
+ * the sparsity pattern moved since the previous call over the same outputs.
+ * nmat = 2 with out_rows[1] = out_vals[1] = NULL: concatenated output -- the second
+ * matrix's entries follow the first's nonzeros in out_rows[0] / out_vals[0], its
+ * column pointers (out_ptr[1]) relative to its own first entry.
+ * host_vals / host_rows (0 = off): byte offsets from the device outputs to a
+ * page-locked host mirror laid out the same way; the kernel also stores every
+ * value (host_vals) and, while *rows_wanted (device double) != 0, every row index
+ * (host_rows) there, so the result crosses the bus during the compaction. */
 cito_status cito_csc_assemble_packed_dev(int32_t nmat, int32_t ncols, const void* const* ent, const int64_t* nsup,
                                         const int64_t* const* sp_ptr, const int32_t* const* tcol, const int32_t* ntile,
                                         const double* const* lin, uint32_t* ws, int64_t ws_words,
                                         int32_t* const* out_ptr, int32_t* const* out_rows, double* const* out_vals,
-                                        unsigned long long* const* rowmax, void* stream);
+                                        unsigned long long* const* rowmax, const double* stamp_in,
+                                        double* changed_at, int64_t host_vals, int64_t host_rows,
+                                        const double* rows_wanted, void* stream);
 
 /* b / h of the linearized rows: out[rows[i]] = form ? J.z[cols] - v : v - J.z[cols]
  * with J split in up to 3 segments (seg_src < 0 = unused), v = lin[vsrc[i]][voff[i]]. */
@@ -268,15 +280,29 @@ cito_status cito_rhs_dev(int64_t nrows, const int32_t* rows, const int8_t* form,
  *   A.data, b, G.data, h multiplied by their row's scale (values bit-identical
  *   to scipy's Da @ A).
  * rowmax_A/G: device uint64 workspaces [nA]/[nG]; rowmax_ready != 0 means they
- * already hold the norms (fused into cito_csc_assemble2_dev), else this call
- * computes them.  max_nnz: upper bound of the stored entries of A and G.
+ * already hold the norms (fused into the compaction), else this call computes
+ * them; the call leaves them zero (ready for the next fused compaction).
+ * max_nnz: upper bound of the stored entries of A and G.
+ * keep_A/keep_b/keep_G/keep_h (optional, NULL = off): device arrays that receive
+ * the values before scaling.  G_rows = G_data = keep_G = NULL selects the
+ * concatenated layout of cito_csc_assemble_packed_dev: G's entries follow A's
+ * A_ptr[ncols] nonzeros in A_rows / A_data / keep_A, G_ptr relative to them.
+ * host_vals (0 = off): byte offset from A_data/G_data to a page-locked host
+ * mirror that also receives the scaled values.
  * The cost scaling (c / omega, P / omega) is a host-side scalar (Python layer). */
 cito_status cito_precondition_dev(int32_t ncols, const int32_t* A_ptr, const int32_t* A_rows, double* A_data,
                                   int32_t nA, double* b, const int32_t* G_ptr, const int32_t* G_rows, double* G_data,
                                   int32_t nG, double* h, int32_t n_nonneg, int32_t n_soc, const int32_t* soc_start,
                                   const int32_t* soc_dim, unsigned long long* rowmax_A, unsigned long long* rowmax_G,
                                   int32_t rowmax_ready, int32_t max_nnz, double* row_scale_A, double* row_scale_G,
+                                  double* keep_A, double* keep_b, double* keep_G, double* keep_h, int64_t host_vals,
                                   void* stream);
+
+/* Copy nbytes from device memory to page-locked host memory with a kernel (SM
+ * stores over the bus instead of a copy-engine transfer; both pointers 16-byte
+ * aligned, dst_host from cudaHostAlloc / a pinned allocation).  Used for the one
+ * device->host copy of an SCP iteration's packed result at the end of its graph. */
+cito_status cito_copy_to_host(void* dst_host, const void* src_dev, int64_t nbytes, void* stream);
 
 /* FP64 DFMA throughput probe (roofline denominator; not part of the reference
  * interface).  Launches one kernel on `stream`; returns the flops it issues

@@ -687,10 +687,19 @@ cito_status cito_csc_assemble_packed_dev(int32_t nmat, int32_t ncols, const void
                                         const int64_t* const* sp_ptr, const int32_t* const* tcol, const int32_t* ntile,
                                         const double* const* lin, uint32_t* ws, int64_t ws_words,
                                         int32_t* const* out_ptr, int32_t* const* out_rows, double* const* out_vals,
-                                        unsigned long long* const* rowmax, void* stream) {
-  if (nmat < 1 || nmat > 2 || ncols < 0 || !ent || !nsup || !sp_ptr || !tcol || !ntile || !ws)
+                                        unsigned long long* const* rowmax, const double* stamp_in,
+                                        double* changed_at, int64_t host_vals, int64_t host_rows,
+                                        const double* rows_wanted, void* stream) {
+  if (nmat < 1 || nmat > 2 || ncols < 0 || !ent || !nsup || !sp_ptr || !tcol || !ntile || !ws ||
+      (stamp_in == nullptr) != (changed_at == nullptr))
     return fail(CITO_ERR_ARG, "csc_assemble_packed: bad arguments");
   CscPackedArgs a;
+  a.stamp_in = stamp_in;
+  a.changed_at = changed_at;
+  if (host_rows && !rows_wanted) return fail(CITO_ERR_ARG, "csc_assemble_packed: host_rows needs rows_wanted");
+  a.host_vals = host_vals;
+  a.host_rows = host_rows;
+  a.rows_wanted = rows_wanted;
   int64_t tiles = 0;
   for (int m = 0; m < 2; ++m) {
     const bool on = m < nmat;
@@ -757,9 +766,12 @@ cito_status cito_precondition_dev(int32_t ncols, const int32_t* A_ptr, const int
                                   int32_t nG, double* h, int32_t n_nonneg, int32_t n_soc, const int32_t* soc_start,
                                   const int32_t* soc_dim, unsigned long long* rowmax_A, unsigned long long* rowmax_G,
                                   int32_t rowmax_ready, int32_t max_nnz, double* row_scale_A, double* row_scale_G,
+                                  double* keep_A, double* keep_b, double* keep_G, double* keep_h, int64_t host_vals,
                                   void* stream) {
   if (ncols < 0 || nA < 0 || nG < 0 || n_nonneg < 0 || n_nonneg > nG || n_soc < 0 || max_nnz < 0)
     return fail(CITO_ERR_ARG, "precondition: bad sizes");
+  if ((G_data == nullptr) != (G_rows == nullptr) || (G_data == nullptr && keep_G != nullptr))
+    return fail(CITO_ERR_ARG, "precondition: concatenated layout takes G_rows = G_data = keep_G = null");
   cudaStream_t s = (cudaStream_t)stream;
   PcArgs a;
   a.ptr[0] = A_ptr;
@@ -776,6 +788,12 @@ cito_status cito_precondition_dev(int32_t ncols, const int32_t* A_ptr, const int
   a.rowmax[1] = rowmax_G;
   a.scale[0] = row_scale_A;
   a.scale[1] = row_scale_G;
+  a.keep[0] = keep_A;
+  a.keep[1] = keep_G;
+  a.keep_rhs[0] = keep_b;
+  a.keep_rhs[1] = keep_h;
+  a.concat = G_data == nullptr;
+  a.host_vals = host_vals;
   if (!rowmax_ready) {
     if (nA) CUDA_TRY(cudaMemsetAsync(rowmax_A, 0, sizeof(unsigned long long) * (size_t)nA, s));
     if (nG) CUDA_TRY(cudaMemsetAsync(rowmax_G, 0, sizeof(unsigned long long) * (size_t)nG, s));
@@ -803,6 +821,37 @@ cito_status cito_precondition_dev(int32_t ncols, const int32_t* A_ptr, const int
     k_row_apply<<<dim3(gx, 2), 256, 0, s>>>(ncols, a);
     CUDA_TRY(cudaGetLastError());
   }
+  return CITO_OK;
+}
+
+// SM-driven copy into page-locked host memory (mapped under unified addressing):
+// 16-byte stores straight over the bus, issued by the kernel that follows the
+// producers in the same graph -- no copy-engine hand-off between the last kernel
+// and the transfer.
+__global__ void __launch_bounds__(256) k_copy_out(uint4* __restrict__ dst, const uint4* __restrict__ src, int64_t n16,
+                                                  unsigned char* __restrict__ dtail,
+                                                  const unsigned char* __restrict__ stail, int ntail) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += stride) dst[i] = src[i];
+  if (blockIdx.x == 0 && (int)threadIdx.x < ntail) dtail[threadIdx.x] = stail[threadIdx.x];
+}
+
+cito_status cito_copy_to_host(void* dst_host, const void* src_dev, int64_t nbytes, void* stream) {
+  if (nbytes < 0 || ((uintptr_t)dst_host & 15) || ((uintptr_t)src_dev & 15))
+    return fail(CITO_ERR_ARG, "copy_to_host: negative size or pointers not 16-byte aligned");
+  if (nbytes == 0) return CITO_OK;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t n16 = nbytes / 16;
+  const int ntail = (int)(nbytes - 16 * n16);
+  const int64_t want = (n16 + 255) / 256;
+  const unsigned grid = (unsigned)(want < 1 ? 1 : (want < 2 * sms ? want : 2 * sms));
+  count_launch();
+  k_copy_out<<<grid, 256, 0, (cudaStream_t)stream>>>((uint4*)dst_host, (const uint4*)src_dev, n16,
+                                                     (unsigned char*)dst_host + 16 * n16,
+                                                     (const unsigned char*)src_dev + 16 * n16, ntail);
+  CUDA_TRY(cudaGetLastError());
   return CITO_OK;
 }
 

@@ -386,6 +386,10 @@ __global__ void __launch_bounds__(256) k_csc_onepass(int32_t ncols, const CscArg
 //           tcol[t+1]) read their offset from the masks: no per-column pass at all
 // Workspace ws: [ticket, finished CTAs, pad, pad] + one uint64 flag per tile, zero
 // before the first launch; the last CTA returns it to zero.
+// Concatenated output (out_rows[1] = out_vals[1] = null): matrix 1's entries follow
+// matrix 0's nonzeros in out_rows[0] / out_vals[0] (its tiles look back over matrix
+// 0's tiles too), its column pointers stay relative to its own first entry -- both
+// matrices' values then sit in one array that comes back in one copy.
 #define CSC_TJ 8
 #define CSC_TILE (256 * CSC_TJ)
 
@@ -405,22 +409,40 @@ struct CscPackedArgs {
   int32_t* out_rows[2];
   double* out_vals[2];
   unsigned long long* rowmax[2];
+  // pattern-change stamp (both null = off): a CTA that writes a row index or a
+  // column pointer different from what the output held before stores *stamp_in
+  // into *changed_at, so the host learns whether the CSC pattern moved since the
+  // previous launch over the same outputs (and skips re-copying the indices)
+  const double* stamp_in;
+  double* changed_at;
+  // host mirror (0 = off): the values (host_vals) / the row indices (host_rows, only
+  // while *rows_wanted != 0) are also stored at byte offset host_* from their device
+  // address -- into page-locked host memory laid out like the device outputs, so the
+  // result crosses the bus while the compaction runs instead of in a copy after it
+  int64_t host_vals, host_rows;
+  const double* rows_wanted;
 };
+
+template <class T>
+__device__ __forceinline__ void mirror_store(T* dev_addr, int64_t delta, T v) {
+  *reinterpret_cast<T*>(reinterpret_cast<char*>(dev_addr) + delta) = v;
+}
 
 __global__ void __launch_bounds__(256) k_csc_flat(int32_t ncols, const CscPackedArgs a, const LinTable L,
                                                   unsigned* __restrict__ ws) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int ntiles = a.ntile[0] + a.ntile[1];
   unsigned long long* flags = reinterpret_cast<unsigned long long*>(ws + CSC_HDR_WORDS);
-  __shared__ int tile_s, last_s, tbase_s, ttot_s;
+  __shared__ int tile_s, last_s, tbase_s, ttot_s, obase_s;
   __shared__ unsigned masks[CSC_TJ][8];
   __shared__ int base[CSC_TJ][8];
-  __shared__ int red[8];
+  __shared__ int red[8], red_b[8];
   if (tid == 0) tile_s = (int)atomicAdd(&ws[0], 1u);
   __syncthreads();
   const int tile = tile_s;
   const int m = tile < a.ntile[0] ? 0 : 1;
   const int t0 = m ? a.ntile[0] : 0, lt = tile - t0;
+  const bool concat = a.out_vals[1] == nullptr;
   const int64_t e0 = (int64_t)lt * CSC_TILE, nsup = a.nsup[m];
   const CscEnt* __restrict__ ent = a.ent[m];
   // evaluate the tile's entries: record loads first (all in flight), then the lin loads
@@ -473,24 +495,39 @@ __global__ void __launch_bounds__(256) k_csc_flat(int32_t ncols, const CscPacked
       atomicExch(&flags[tile], (1ull << 32) | (unsigned)incl);  // publish the tile total
     }
   }
-  // look-back: totals of the preceding tiles of this matrix (ticket order: all started earlier)
-  int pre = 0;
-  for (int j = t0 + tid; j < tile; j += blockDim.x) {
+  // look-back: totals of the preceding tiles of this matrix (ticket order: all started
+  // earlier); concatenated output: of matrix 0's tiles too (`before`: its nonzeros)
+  int pre = 0, before = 0;
+  for (int j = (concat ? 0 : t0) + tid; j < tile; j += blockDim.x) {
     unsigned long long f;
     do {
       f = *((volatile unsigned long long*)&flags[j]);
     } while ((f >> 32) == 0ull);
-    pre += (int)(unsigned)(f & 0xffffffffull);
+    const int cnt = (int)(unsigned)(f & 0xffffffffull);
+    if (j >= t0)
+      pre += cnt;
+    else
+      before += cnt;
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
-  if (lane == 0) red[warp] = pre;
+  for (int o = 16; o > 0; o >>= 1) {
+    pre += __shfl_xor_sync(0xffffffffu, pre, o);
+    before += __shfl_xor_sync(0xffffffffu, before, o);
+  }
+  if (lane == 0) {
+    red[warp] = pre;
+    red_b[warp] = before;
+  }
   __syncthreads();
   if (tid == 0) {
-    int t = 0;
+    int t = 0, tb0 = 0;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) t += red[w];
+    for (int w = 0; w < 8; ++w) {
+      t += red[w];
+      tb0 += red_b[w];
+    }
     tbase_s = t;
+    obase_s = tb0;
     __threadfence();
     last_s = atomicAdd(&ws[1], 1u) == (unsigned)ntiles - 1u;
   }
@@ -505,15 +542,21 @@ __global__ void __launch_bounds__(256) k_csc_flat(int32_t ncols, const CscPacked
   }
   const int tb = tbase_s;
   const unsigned ltm = (1u << lane) - 1u;
-  int32_t* __restrict__ orow = a.out_rows[m];
-  double* __restrict__ oval = a.out_vals[m];
+  int32_t* __restrict__ orow = concat ? a.out_rows[0] + obase_s : a.out_rows[m];
+  double* __restrict__ oval = concat ? a.out_vals[0] + obase_s : a.out_vals[m];
   unsigned long long* rmax = a.rowmax[m];
+  const bool stamp = a.changed_at != nullptr;
+  const int64_t hv = a.host_vals, hr = (a.host_rows && *a.rows_wanted != 0.0) ? a.host_rows : 0;
+  bool moved = false;
 #pragma unroll
   for (int j = 0; j < CSC_TJ; ++j) {
     if (v[j] != 0.0) {
       const int pos = tb + base[j][warp] + __popc(masks[j][warp] & ltm);
+      if (stamp) moved |= orow[pos] != row[j];
       orow[pos] = row[j];
       oval[pos] = v[j];
+      if (hv) mirror_store(oval + pos, hv, v[j]);
+      if (hr) mirror_store(orow + pos, hr, row[j]);
       // fused row inf-norm (cito/conic.py:281-287): non-negative doubles order like their bits
       if (rmax) atomicMax(&rmax[row[j]], (unsigned long long)__double_as_longlong(fabs(v[j])));
     }
@@ -531,8 +574,10 @@ __global__ void __launch_bounds__(256) k_csc_flat(int32_t ncols, const CscPacked
       const int j = (int)(l >> 8), r = (int)(l & 255), w = r >> 5, ln = r & 31;
       cnt = base[j][w] + __popc(masks[j][w] & ((1u << ln) - 1u));
     }
+    if (stamp) moved |= a.out_ptr[m][c] != tb + cnt;
     a.out_ptr[m][c] = tb + cnt;
   }
+  if (stamp && __syncthreads_or(moved) && tid == 0) *a.changed_at = *a.stamp_in;
 }
 
 __global__ void __launch_bounds__(256) k_rhs(int64_t nrows, const int32_t* __restrict__ rows,
@@ -582,20 +627,33 @@ struct PcArgs {
   int32_t nrows[2];
   unsigned long long* rowmax[2];
   double* scale[2];
+  double* keep[2];      // optional: the unscaled values are stored here before scaling
+  double* keep_rhs[2];  // optional: the unscaled b / h
+  int32_t concat;       // G's entries follow A's nonzeros in rows[0] / data[0] / keep[0]
+  int64_t host_vals;    // host mirror of the scaled values (byte offset from data; 0 = off)
 };
+
+// entry arrays of matrix m (concatenated layout: G starts after A's nonzeros)
+__device__ __forceinline__ int32_t pc_off(const PcArgs& a, int m, int32_t ncols) {
+  return (a.concat && m == 1) ? a.ptr[0][ncols] : 0;
+}
 
 __global__ void __launch_bounds__(256) k_row_absmax(int32_t ncols, const PcArgs a) {
   const int m = blockIdx.y;
   const int lane = threadIdx.x & 31;
   const int64_t c = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (c >= ncols) return;
+  const int mm = a.concat ? 0 : m;
+  const int32_t off = pc_off(a, m, ncols);
   for (int32_t e = a.ptr[m][c] + lane; e < a.ptr[m][c + 1]; e += 32) {
-    const double v = a.data[m][e];
-    if (v != 0.0) atomicMax(&a.rowmax[m][a.rows[m][e]], (unsigned long long)__double_as_longlong(fabs(v)));
+    const double v = a.data[mm][off + e];
+    if (v != 0.0) atomicMax(&a.rowmax[m][a.rows[mm][off + e]], (unsigned long long)__double_as_longlong(fabs(v)));
   }
 }
 
-// one thread per A row, per orthant row of G, and per SOC block of G
+// one thread per A row, per orthant row of G, and per SOC block of G; every row
+// max is read by exactly one thread, which returns it to zero for the next call
+// (the fused norms of the next compaction accumulate into a zeroed workspace)
 __global__ void __launch_bounds__(256) k_row_scale(const PcArgs a, int32_t n_nonneg, int32_t n_soc,
                                                    const int32_t* __restrict__ soc_start,
                                                    const int32_t* __restrict__ soc_dim) {
@@ -603,12 +661,14 @@ __global__ void __launch_bounds__(256) k_row_scale(const PcArgs a, int32_t n_non
   const int64_t nA = a.nrows[0];
   if (i < nA) {
     const double r = __longlong_as_double((long long)a.rowmax[0][i]);
+    a.rowmax[0][i] = 0ull;
     a.scale[0][i] = 1.0 / (r == 0.0 ? 1.0 : r);  // ra[ra == 0] = 1; da = 1 / ra
     return;
   }
   const int64_t j = i - nA;
   if (j < n_nonneg) {
     const double r = __longlong_as_double((long long)a.rowmax[1][j]);
+    a.rowmax[1][j] = 0ull;
     a.scale[1][j] = r != 0.0 ? 1.0 / r : 1.0;
     return;
   }
@@ -616,24 +676,38 @@ __global__ void __launch_bounds__(256) k_row_scale(const PcArgs a, int32_t n_non
   if (k < n_soc) {
     const int32_t s0 = soc_start[k], d = soc_dim[k];
     double mx = 0.0;
-    for (int32_t r = 0; r < d; ++r) mx = fmax(mx, __longlong_as_double((long long)a.rowmax[1][s0 + r]));
+    for (int32_t r = 0; r < d; ++r) {
+      mx = fmax(mx, __longlong_as_double((long long)a.rowmax[1][s0 + r]));
+      a.rowmax[1][s0 + r] = 0ull;
+    }
     const double sc = mx > 0.0 ? 1.0 / mx : 1.0;
     for (int32_t r = 0; r < d; ++r) a.scale[1][s0 + r] = sc;
   }
 }
 
-// grid-stride over the stored entries (valid prefix = ptr[ncols]) and the rhs rows
+// grid-stride over the stored entries (valid prefix = ptr[ncols]) and the rhs rows;
+// the unscaled values go to keep / keep_rhs first when given
 __global__ void __launch_bounds__(256) k_row_apply(int32_t ncols, const PcArgs a) {
-  const int m = blockIdx.y;
-  const int32_t nnz = a.ptr[m][ncols];
+  const int m = blockIdx.y, mm = a.concat ? 0 : m;
+  const int32_t nnz = a.ptr[m][ncols], off = pc_off(a, m, ncols);
   const int64_t total = (int64_t)nnz + a.nrows[m];
   const double* __restrict__ sc = a.scale[m];
+  double* __restrict__ data = a.data[mm] + off;
+  const int32_t* __restrict__ rows = a.rows[mm] + off;
+  double* __restrict__ keep = a.keep[mm] ? a.keep[mm] + off : nullptr;
+  double* __restrict__ keep_rhs = a.keep_rhs[m];
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     if (i < nnz) {
-      a.data[m][i] = sc[a.rows[m][i]] * a.data[m][i];
+      const double v = data[i];
+      if (keep) keep[i] = v;
+      const double w = sc[rows[i]] * v;
+      data[i] = w;
+      if (a.host_vals) mirror_store(data + i, a.host_vals, w);
     } else {
       const int64_t r = i - nnz;
-      a.rhs[m][r] = sc[r] * a.rhs[m][r];
+      const double v = a.rhs[m][r];
+      if (keep_rhs) keep_rhs[r] = v;
+      a.rhs[m][r] = sc[r] * v;
     }
   }
 }

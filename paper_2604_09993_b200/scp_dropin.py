@@ -10,8 +10,9 @@ cito.scp.solve (/root/reference/pkg/src/cito/scp.py:383-467) calls, per attempt,
 
   linearize_all     runs the whole iteration on the GPU -- GpuSCPStep.iterate with
                     preconditioning: one pinned H2D of [z, delta, epsilon], one CUDA
-                    graph replay (K1 + K3, CSC assembly, rhs, row scaling), ONE packed
-                    D2H -- and returns the device-backed LinearizedProblem
+                    graph replay (K1 + K3, CSC assembly, rhs, row scaling; the result
+                    written into a pinned host buffer) -- and returns the device-backed
+                    LinearizedProblem
   build_subproblem  for that lin: the program before row scaling, whose A/G/b/h
                     stay on the device until read (scp.solve never reads them)
   precondition      for that program: the scaled program + Preconditioner already

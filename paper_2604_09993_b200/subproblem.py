@@ -373,7 +373,8 @@ def precondition_device(ncols, out, nA, nG, n_nonneg, n_soc, soc_start, soc_dim,
         int(ncols), out["A_indptr"].data_ptr(), out["A_indices"].data_ptr(), out["A_data"].data_ptr(), int(nA),
         out["b"].data_ptr(), out["G_indptr"].data_ptr(), out["G_indices"].data_ptr(), out["G_data"].data_ptr(),
         int(nG), out["h"].data_ptr(), int(n_nonneg), int(n_soc), soc_start.data_ptr(), soc_dim.data_ptr(),
-        rowmax[0].data_ptr(), rowmax[1].data_ptr(), int(ready), int(max_nnz), sA.data_ptr(), sG.data_ptr(), stream),
+        rowmax[0].data_ptr(), rowmax[1].data_ptr(), int(ready), int(max_nnz), sA.data_ptr(), sG.data_ptr(),
+        None, None, None, None, 0, stream),
         "precondition")
     return sA[:nA], sG[:nG]
 
@@ -583,10 +584,12 @@ class SubproblemAssembler:
                      cols=t(np.concatenate(cols) if cols else np.zeros(1), np.int64))
             self._mats[M] = d
 
-    def packed_args(self, lin_ptrs, outs, rowmax, arr):
+    def packed_args(self, lin_ptrs, outs, rowmax, arr, stamp=None, mirror=None):
         """Argument tuple of cito_csc_assemble_packed_dev for A and G (without the
         stream); `outs` = [(indptr, indices, data)] per matrix, `arr` builds a
-        ctypes pointer table from tensors."""
+        ctypes pointer table from tensors, `stamp` = optional (stamp_in, changed_at)
+        device pointers of the pattern-change stamp, `mirror` = optional
+        (host_vals, host_rows, rows_wanted) of the host mirror."""
         import ctypes
 
         import torch
@@ -601,7 +604,7 @@ class SubproblemAssembler:
                 arr([d["sp_ptr"] for d in mats]), arr([d["tcol"] for d in mats]),
                 ctypes.cast(self._ntile, ctypes.c_void_p), lin_ptrs, self._ws.data_ptr(), self._ws.numel(),
                 arr([o[0] for o in outs]), arr([o[1] for o in outs]), arr([o[2] for o in outs]),
-                arr(rowmax) if rowmax else None)
+                arr(rowmax) if rowmax else None, *(stamp or (None, None)), *(mirror or (0, 0, None)))
 
     def _prepare_batched(self):
         """Concatenate the rhs descriptors of A and G (one launch) and allocate
@@ -645,7 +648,7 @@ class SubproblemAssembler:
                     a = memo[key] = ctypes_ptr_array(list(key))
                 return a
         else:
-            arr = lambda xs: ctypes_ptr_array([x.data_ptr() for x in xs])  # noqa: E731
+            arr = lambda xs: ctypes_ptr_array([x.data_ptr() if x is not None else None for x in xs])  # noqa: E731
         ptrs = arr([lin[k] for k in LIN_SOURCES])
         out = {}
         mats = [self._mats["A"], self._mats["G"]]
@@ -805,10 +808,12 @@ def _lazy_program_type(base):
 
             u = self._hb.slot["unscaled"]
             h = {}
-            for M in ("A", "G"):
+            o = 0
+            for M in ("A", "G"):  # concatenated values: G's follow A's nonzeros
                 ref = self._mats[M]
                 nnz = ref.indices.size
-                vals = u[f"{M}_data"][:nnz].cpu().numpy()
+                vals = u["vals"][o: o + nnz].cpu().numpy()
+                o += nnz
                 h[M] = sp.csc_matrix((vals, ref.indices.copy(), ref.indptr.copy()), shape=ref.shape)
             rhs = u["rhs"][: self._nA + self._nG].cpu().numpy()
             torch.cuda.current_stream(self._step.gt.device).synchronize()
@@ -891,9 +896,11 @@ class _Span:
     """Owner object of one handed-out array over pinned memory (numpy
     __array_interface__): the array's base, with `size` equal to the array's
     length so scipy's _prune_array never copies it, and weakly referenceable so
-    the buffer knows when the caller has dropped the array."""
+    the buffer knows when the caller has dropped the array.  It holds the pinned
+    allocation itself, so an array outlives the GpuSCPStep that produced it."""
 
-    def __init__(self, ptr, n, dtype):
+    def __init__(self, ptr, n, dtype, owner):
+        self.owner = owner
         self.size = int(n)
         self.__array_interface__ = {"data": (int(ptr), False), "shape": (int(n),), "typestr": dtype.str,
                                     "version": 3}
@@ -916,15 +923,15 @@ class _HostBuf:
             self.np_dtype[name], self.off[name] = (npdt, isz), o
         self.base_ptr = self.nb.ctypes.data
         self.graphs = {}
-        self.caps = {}
         self.live = []
+        self.pat_gen = -1  # pattern generation of the CSC indices last copied into this buffer
 
     def wrap(self, name, start, n):
         """Array of n elements of field `name` from element `start`, owned by a _Span."""
         import weakref
 
         npdt, isz = self.np_dtype[name]
-        span = _Span(self.base_ptr + self.off[name] + start * isz, n, npdt)
+        span = _Span(self.base_ptr + self.off[name] + start * isz, n, npdt, self.host)
         self.live.append(weakref.ref(span))
         return np.asarray(span)
 
@@ -939,7 +946,8 @@ class GpuSCPStep:
     ``iterate(z, delta, z_j=None)`` = cito.scp.linearize_all + build_subproblem
     (scp.py:412-413) with host numpy in / host scipy out: one pinned H2D of z,
     the interval + node kernels, the whole-subproblem assembly (+ preconditioning,
-    scp.py:414), ONE pinned D2H of a packed result buffer and a single
+    scp.py:414) whose last kernel stores the CSC values straight into a pinned
+    host buffer (the fixed fields follow in one copy kernel), and a single
     synchronization.  All device buffers and kernel argument tables are built
     once; the host work per call is the C-ABI launches and the scipy wrappers.
     Raises FloatingPointError for non-finite interval end states like the
@@ -959,6 +967,8 @@ class GpuSCPStep:
         self._plan = None
         self._last_lin = None
         self.use_graph = use_graph
+        self.pattern_refetches = 0  # calls whose pattern moved after a values-only copy
+        self.d2h_copied = 0  # bytes of every device->host copy the calls made
 
     # -- one-time plan: buffers + constant ctypes argument tables
     def _build_plan(self):
@@ -973,38 +983,46 @@ class GpuSCPStep:
         dA, dG = asm._mats["A"], asm._mats["G"]
         nA, nG = dA["nrows"], dG["nrows"]
         i32, i64, fd = torch.int32, torch.int64, torch.float64
-        pk = _Packed([("bad", i32, NI), ("A_indptr", i32, pat.n + 1), ("G_indptr", i32, pat.n + 1),
+        # one result buffer, mirrored by each slot's pinned host buffer at the same offsets:
+        # the fixed fields, then the CSC values of A and G concatenated (the compaction
+        # writes G's entries right after A's nonzeros), then the row indices the same way.
+        # The kernel that finalises the values (the compaction, or the row scaling) also
+        # stores them into the host mirror; the fixed fields follow in one copy kernel.
+        nsup = dA["nsup"] + dG["nsup"]
+        pk = _Packed([("bad", i32, NI), ("changed_at", fd, 1), ("A_indptr", i32, pat.n + 1), ("G_indptr", i32, pat.n + 1),
                       ("rhs", fd, nA + nG), ("row_scale_A", fd, nA), ("row_scale_G", fd, nG),
-                      ("A_data", fd, dA["nsup"]), ("G_data", fd, dG["nsup"]),
-                      ("A_indices", i32, dA["nsup"]), ("G_indices", i32, dG["nsup"])], dev)
-        # z followed by [delta, epsilon]: one H2D per call, read by the kernels from device
-        # memory so a captured graph replays for any delta of the homotopy
-        zde_dev = torch.empty(lay.dim + 2, **f64)
-        zde_pin = torch.empty(lay.dim + 2, dtype=torch.float64, pin_memory=True)
+                      ("vals", fd, nsup), ("indices", i32, nsup)], dev)
+        # z followed by [delta, epsilon, stamp, rows wanted]: one H2D per call, read by the
+        # kernels from device memory so a captured graph replays for any delta of the
+        # homotopy; the stamp (call counter) is what the CSC compaction writes into
+        # changed_at when the sparsity pattern moves; rows wanted != 0 makes it mirror the
+        # row indices too (a host buffer that does not hold the current pattern)
+        zde_dev = torch.empty(lay.dim + 4, **f64)
+        zde_pin = torch.zeros(lay.dim + 4, dtype=torch.float64, pin_memory=True)
         z_dev = zde_dev[: lay.dim]
-        rowmax = torch.empty(max(1, nA + nG), dtype=i64, device=dev)
-        arr = lambda xs: ctypes_ptr_array([x.data_ptr() for x in xs])  # noqa: E731
+        rowmax = torch.zeros(max(1, nA + nG), dtype=i64, device=dev)  # zero between calls (k_row_scale resets it)
+        arr = lambda xs: ctypes_ptr_array([x.data_ptr() if x is not None else None for x in xs])  # noqa: E731
         soc_start, soc_dim = soc_tables(pat.n_orthant, pat.soc_dims, dev)
         keep = []  # ctypes arrays must outlive the plan
         rhs_dev = pk.d["rhs"]  # b and h: rows [0, nA) = b, [nA, nA + nG) = h
-        pc_args = (pat.n, pk.d["A_indptr"].data_ptr(), pk.d["A_indices"].data_ptr(), pk.d["A_data"].data_ptr(), nA,
-                   rhs_dev.data_ptr(), pk.d["G_indptr"].data_ptr(), pk.d["G_indices"].data_ptr(),
-                   pk.d["G_data"].data_ptr(), nG, rhs_dev[nA:].data_ptr(), pat.n_orthant, len(pat.soc_dims),
-                   soc_start.data_ptr(), soc_dim.data_ptr(), rowmax[:nA].data_ptr(), rowmax[nA:].data_ptr(), 1,
-                   max(dA["nsup"], dG["nsup"]), pk.d["row_scale_A"].data_ptr(), pk.d["row_scale_G"].data_ptr())
-        rm_arr = arr([rowmax[:nA], rowmax[nA:]])
-        keep.append(rm_arr)
+        pc_args = (pat.n, pk.d["A_indptr"].data_ptr(), pk.d["indices"].data_ptr(), pk.d["vals"].data_ptr(), nA,
+                   rhs_dev.data_ptr(), pk.d["G_indptr"].data_ptr(), None, None, nG, rhs_dev[nA:].data_ptr(),
+                   pat.n_orthant, len(pat.soc_dims), soc_start.data_ptr(), soc_dim.data_ptr(),
+                   rowmax[:nA].data_ptr(), rowmax[nA:].data_ptr(), 1, max(dA["nsup"], dG["nsup"]),
+                   pk.d["row_scale_A"].data_ptr(), pk.d["row_scale_G"].data_ptr())
         dim = lay.dim
         P_idx = np.arange(dim, dtype=np.int32)
         P_ptr = np.concatenate([np.arange(dim + 1), np.full(pat.n - dim, dim)]).astype(np.int32)
         self._plan = dict(pk=pk, z_dev=z_dev, zde_dev=zde_dev, zde_pin=zde_pin, rowmax=rowmax, rhs_dev=rhs_dev,
                           hosts=[], graph_kernels={}, side=torch.cuda.Stream(dev), rhs_const=asm._rhs["const"],
-                          rm_arr=rm_arr, pc_args=pc_args, keep=keep, L=_lib.lib(), nA=nA, nG=nG,
+                          pc_args=pc_args, keep=keep, L=_lib.lib(), nA=nA, nG=nG,
                           soc=(soc_start, soc_dim), P_idx=P_idx, P_ptr=P_ptr, arr=arr,
-                          P_plain=None, meta=_Meta(pat.z_idx, pat.sp_idx, pat.sm_idx, pat.t_idx))
+                          P_plain=None, meta=_Meta(pat.z_idx, pat.sp_idx, pat.sm_idx, pat.t_idx),
+                          stamp=(zde_dev[lay.dim + 2:].data_ptr(), pk.d["changed_at"].data_ptr()), calls=0,
+                          pat_gen=0, want_rows=zde_dev[lay.dim + 3:].data_ptr())
 
-    def _make_slot(self):
-        """Device buffers of one in-flight iteration, paired with a pinned host buffer:
+    def _make_slot(self, hb):
+        """Device buffers of one in-flight iteration, paired with the pinned host buffer hb:
         the linearization outputs (read lazily by the LinearizedProblem handed out)
         and the unscaled program values (read lazily by unscaled_program), plus the
         kernel argument tables that point at them.  A slot is reused only when every
@@ -1027,7 +1045,7 @@ class GpuSCPStep:
                    imp_v=torch.empty((N, nq), **f64), imp_jac=torch.empty((N, nq, 3 * nq + 2 * nc), **f64))
         lin["bad"] = pk.d["bad"]
         dA, dG = asm._mats["A"], asm._mats["G"]
-        unscaled = dict(A_data=torch.empty(max(1, dA["nsup"]), **f64), G_data=torch.empty(max(1, dG["nsup"]), **f64),
+        unscaled = dict(vals=torch.empty(max(1, dA["nsup"] + dG["nsup"]), **f64),
                         rhs=torch.empty(max(1, pl["nA"] + pl["nG"]), **f64))
         keep = []
 
@@ -1036,22 +1054,20 @@ class GpuSCPStep:
                 keep.append(a)
             return a
 
-        mats = [dA, dG]
         lin_ptrs = k(arr([lin[kk] for kk in LIN_SOURCES]))
-        outs = [(pk.d["A_indptr"], pk.d["A_indices"], pk.d["A_data"]),
-                (pk.d["G_indptr"], pk.d["G_indices"], pk.d["G_data"])]
+        outs = [(pk.d["A_indptr"], pk.d["indices"], pk.d["vals"]), (pk.d["G_indptr"], None, None)]  # concatenated
         rowmax = pl["rowmax"]
         nA = pl["nA"]
         r = asm._rhs
+        delta = hb.host.data_ptr() - pk.dev.data_ptr()  # device output -> its host mirror (bytes)
         slot = dict(
-            lin=lin, unscaled=unscaled, keep=keep,
-            packed=tuple(k(a) for a in asm.packed_args(lin_ptrs, outs, None, arr)),
-            packed_pc=tuple(k(a) for a in asm.packed_args(lin_ptrs, outs, [rowmax[:nA], rowmax[nA:]], arr)),
-            asm_args=(2, pat.n, k(arr([d["sp_ptr"] for d in mats])), k(arr([d["row"] for d in mats])),
-                      k(arr([d["src"] for d in mats])), k(arr([d["idx"] for d in mats])),
-                      k(arr([d["val"] for d in mats])), asm.sigma_dev.data_ptr(), lin_ptrs,
-                      k(arr([d["counts"] for d in mats])), k(arr([o[0] for o in outs])), k(arr([o[1] for o in outs])),
-                      k(arr([o[2] for o in outs]))),
+            lin=lin, unscaled=unscaled, keep=keep, delta=delta,
+            # plain: the compaction mirrors the values (final) and, when wanted, the rows;
+            # preconditioned: only the rows (the row scaling mirrors the scaled values)
+            packed=tuple(k(a) for a in asm.packed_args(lin_ptrs, outs, None, arr, pl["stamp"],
+                                                       (delta, delta, pl["want_rows"]))),
+            packed_pc=tuple(k(a) for a in asm.packed_args(lin_ptrs, outs, [rowmax[:nA], rowmax[nA:]], arr,
+                                                          pl["stamp"], (0, delta, pl["want_rows"]))),
             rhs_args=(r["n"], r["rows"].data_ptr(), r["form"].data_ptr(), r["vsrc"].data_ptr(),
                       r["voff"].data_ptr(), r["seg_src"].data_ptr(), r["seg_off"].data_ptr(),
                       r["seg_len"].data_ptr(), r["seg_cb"].data_ptr(), r["cols"].data_ptr(), pl["z_dev"].data_ptr(),
@@ -1073,8 +1089,6 @@ class GpuSCPStep:
         L = pl["L"]
         s = torch.cuda.current_stream(self.gt.device).cuda_stream
         pl["zde_dev"].copy_(pl["zde_pin"], non_blocking=True)
-        if precondition:  # before the linearization: nothing sits between K1 and the compaction
-            pl["rowmax"].zero_()
         h = self.gt.disc._h  # the handle's own library (a run-time compiled topology has its own)
         h.check(h.L.cito_linearize_all_dev2(*sl["lin_args"], *sl["lin_outs"], s), "linearize_all")
         # b/h of the linearized rows on a side stream, concurrently with the CSC compaction
@@ -1084,55 +1098,35 @@ class GpuSCPStep:
         with torch.cuda.stream(side):
             pl["rhs_dev"].copy_(pl["rhs_const"])
             _lib.check(L.cito_rhs_dev(*sl["rhs_args"], side.cuda_stream), "rhs")
-        if not _CSC_RECIPES:
-            _lib.check(L.cito_csc_assemble_packed_dev(*(sl["packed_pc"] if precondition else sl["packed"]), s),
-                       "csc_assemble")
-        else:
-            _lib.check(L.cito_csc_assemble2_dev(*sl["asm_args"], pl["rm_arr"] if precondition else None, s),
-                       "csc_assemble")
+        # the compaction (A and G concatenated; the fused row norms accumulate into the
+        # rowmax workspace, which the preconditioning leaves zero again)
+        _lib.check(L.cito_csc_assemble_packed_dev(*(sl["packed_pc"] if precondition else sl["packed"]), s),
+                   "csc_assemble")
         cur.wait_stream(side)
-        if precondition:
-            u, d = sl["unscaled"], pl["pk"].d
-            for kk in ("A_data", "G_data", "rhs"):
-                u[kk][: d[kk].numel()].copy_(d[kk])
-            _lib.check(L.cito_precondition_dev(*pl["pc_args"], s), "precondition")
-        self._d2h(hb, precondition=precondition)
+        if precondition:  # row scaling in place, the unscaled values kept in the slot by the same kernel
+            u = sl["unscaled"]
+            _lib.check(L.cito_precondition_dev(*pl["pc_args"], u["vals"].data_ptr(), u["rhs"].data_ptr(), None,
+                                               u["rhs"][pl["nA"]:].data_ptr(), sl["delta"], s), "precondition")
+        # the fixed fields (flags, column pointers, b/h, row scales) in one copy kernel; the
+        # values (and wanted rows) are in the host buffer already
+        end = pl["pk"].layout["vals" if precondition else "row_scale_A"][0]
+        _lib.check(L.cito_copy_to_host(hb.host.data_ptr(), pl["pk"].dev.data_ptr(), end, s), "copy_to_host")
 
-    def _d2h(self, hb, tail=False, precondition=True):
-        """Device -> pinned copies of the packed result: the fixed fields in one
-        copy (the row scales only for a preconditioned iteration), the CSC
-        values/indices only up to the buffer's caps (the nnz of the captured
-        result + 1/8 + 1024, about 55 % of the superset-sized arrays); `tail`
-        copies what lies beyond the caps (a result with more nonzeros than
-        the captured one: one extra copy + synchronization; a recapture after
-        the second such call in a row)."""
-        pk = self._plan["pk"]
-        lay = pk.layout
-        if not tail:
-            # fixed fields precede the CSC arrays: bad, indptrs, rhs, then the row scales
-            end = lay["A_data"][0] if precondition else lay["row_scale_A"][0]
-            hb.host[:end].copy_(pk.dev[:end], non_blocking=True)
-        caps = hb.caps.get(bool(precondition), {})  # per captured graph (plain / preconditioned)
-        for M in ("A", "G"):
-            cap = caps.get(M, lay[f"{M}_data"][2])
-            for fld in (f"{M}_data", f"{M}_indices"):
-                o, _, n, isz = lay[fld]
-                lo, hi = (cap, n) if tail else (0, min(cap, n))
-                if hi > lo:
-                    hb.host[o + lo * isz: o + hi * isz].copy_(pk.dev[o + lo * isz: o + hi * isz], non_blocking=True)
+    def _copy_rows(self, hb, nnz):
+        """Copy-engine transfer of the CSC row indices [0, nnz) into hb (a call whose
+        pattern moved although hb held the previous one)."""
+        o = self._plan["pk"].layout["indices"][0]
+        hb.host[o: o + 4 * nnz].copy_(self._plan["pk"].dev[o: o + 4 * nnz], non_blocking=True)
+        self.d2h_copied += 4 * nnz
 
-    def d2h_bytes(self, precondition=False):
-        """Bytes of the device->host copies one (graph-replayed) iteration makes."""
-        pk = self._plan["pk"]
-        lay = pk.layout
-        hb = self._plan["hosts"][-1] if self._plan["hosts"] else None
-        n = lay["A_data"][0] if precondition else lay["row_scale_A"][0]
-        caps = hb.caps.get(bool(precondition), {}) if hb is not None else {}
-        for M in ("A", "G"):
-            cap = caps.get(M, lay[f"{M}_data"][2])
-            for fld in (f"{M}_data", f"{M}_indices"):
-                n += min(cap, lay[fld][2]) * lay[fld][3]
-        return int(n)
+    def d2h_bytes(self, precondition=False, indices=False):
+        """Bytes one iteration moves device -> host at the last call's nonzero count:
+        the fixed fields + the values (+ the row indices with ``indices``, as in a
+        call whose buffer does not hold the current pattern).  ``self.d2h_copied``
+        counts the bytes every call actually moved."""
+        lay = self._plan["pk"].layout
+        nnz = self._plan.get("last_nnz", lay["vals"][2])
+        return int(lay["vals" if precondition else "row_scale_A"][0] + 8 * nnz + (4 * nnz if indices else 0))
 
     def _host_buffer(self):
         """A pinned result buffer no live array points into (a new one when every
@@ -1142,7 +1136,7 @@ class GpuSCPStep:
             if hb.free():
                 return hb
         hb = _HostBuf(pl["pk"])
-        hb.slot = self._make_slot()
+        hb.slot = self._make_slot(hb)
         pl["hosts"].append(hb)
         return hb
 
@@ -1153,16 +1147,8 @@ class GpuSCPStep:
 
         pl = self._plan
         pl["captures"] = pl.get("captures", 0) + 1
-        hb.caps[bool(precondition)] = {}  # the eager run copies the full arrays
         self._launch(precondition, hb)
         torch.cuda.current_stream(self.gt.device).synchronize()
-        caps = {}
-        # D2H caps of the captured copies: this result's nnz + 1/8 + 1024 (the SCP loop's
-        # pattern grows ~7 % when the impulses become nonzero)
-        for M in ("A", "G"):
-            nnz = int(hb.h[f"{M}_indptr"][-1])
-            caps[M] = min(pl["pk"].layout[f"{M}_data"][2], nnz + nnz // 8 + 1024)
-        hb.caps[bool(precondition)] = caps
         g = torch.cuda.CUDAGraph()
         n0 = _lib.launch_count()
         with torch.cuda.graph(g):
@@ -1193,7 +1179,14 @@ class GpuSCPStep:
         zp[:dim] = z
         zp[dim] = float(delta)
         zp[dim + 1] = float(epsilon)
+        pl["calls"] += 1
+        zp[dim + 2] = float(pl["calls"])  # the stamp of this call (changed_at)
         hb = self._host_buffer()
+        # the CSC row indices come back only into a buffer that does not hold the current
+        # pattern (the compaction mirrors them when asked; it stamps changed_at when the
+        # pattern moves, and then they are fetched after the synchronization)
+        idx_now = hb.pat_gen != pl["pat_gen"]
+        zp[dim + 3] = 1.0 if idx_now else 0.0
         if self.use_graph:
             g = hb.graphs.get(bool(precondition))
             if g is None:
@@ -1226,26 +1219,23 @@ class GpuSCPStep:
         ConicProgram, ConeSpec = _conic_types()
         stream.synchronize()  # the one synchronization
         hh = hb.h
-        caps = hb.caps.get(bool(precondition), {})
-        if any(int(hh[f"{M}_indptr"][-1]) > caps.get(M, 1 << 62) for M in ("A", "G")):
-            self._d2h(hb, tail=True, precondition=precondition)  # more nonzeros than the captured copies cover
-            stream.synchronize()
-            # one extra copy per call while the pattern is above the caps; recapture (caps
-            # from this result) only when it stays there, not on a one-off excursion
-            ov = hb.overflows = getattr(hb, "overflows", 0) + 1
-            if ov >= 2:
-                hb.graphs.pop(bool(precondition), None)
-                hb.overflows = 0
-        else:
-            hb.overflows = 0
+        nnz_A, nnz_G = int(hh["A_indptr"][-1]), int(hh["G_indptr"][-1])
+        nnz = pl["last_nnz"] = nnz_A + nnz_G
+        self.d2h_copied += self.d2h_bytes(precondition, idx_now)  # what the graph moved
+        if hh["changed_at"][0] == zp[dim + 2]:  # the pattern moved in this call
+            pl["pat_gen"] += 1
+            if not idx_now:
+                self._copy_rows(hb, nnz)
+                stream.synchronize()
+                self.pattern_refetches += 1
+        hb.pat_gen = pl["pat_gen"]
         bad = hh["bad"]
         if bad.any():
             raise FloatingPointError(f"non-finite state in intervals {np.where(bad != 0)[0].tolist()}")
         self._c_last = (zj, c_unscaled)  # the unscaled objective, for unscaled_program(z_j) of the same point
         mats = {}
-        for M, nrows in (("A", nA), ("G", pl["nG"])):  # arrays over the pinned buffer (no copy)
-            nnz = int(hh[f"{M}_indptr"][-1])
-            mats[M] = _csc_direct(hb.wrap(f"{M}_data", 0, nnz), hb.wrap(f"{M}_indices", 0, nnz),
+        for M, nrows, o, nnz in (("A", nA, 0, nnz_A), ("G", pl["nG"], nnz_A, nnz_G)):  # over the pinned buffer
+            mats[M] = _csc_direct(hb.wrap("vals", o, nnz), hb.wrap("indices", o, nnz),
                                   hb.wrap(f"{M}_indptr", 0, pat.n + 1), (nrows, pat.n))
         prog = ConicProgram(P=P, c=c, A=mats["A"], b=hb.wrap("rhs", 0, nA), G=mats["G"], h=hb.wrap("rhs", nA, pl["nG"]),
                             cones=ConeSpec(nonneg=pat.n_orthant, soc=pat.soc_dims))
@@ -1274,7 +1264,7 @@ class GpuSCPStep:
         pl = self._plan
         while len(pl["hosts"]) < n:
             hb = _HostBuf(pl["pk"])
-            hb.slot = self._make_slot()
+            hb.slot = self._make_slot(hb)
             pl["hosts"].append(hb)
         for hb in pl["hosts"][:n]:
             if bool(precondition) not in hb.graphs:

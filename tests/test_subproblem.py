@@ -242,6 +242,74 @@ def test_gpu_scp_step_graph_replay_pattern_change(name, precondition):
     assert np.array_equal(ra2[1].A.data, rc[1].A.data) and np.array_equal(ra2[1].A.indices, rc[1].A.indices)
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("precondition", [False, True])
+def test_gpu_scp_step_pattern_stamp_sequence(precondition):
+    """The CSC row indices come back only into a result buffer that does not hold
+    the current pattern (the compaction stamps a moved pattern): a sequence of
+    points whose patterns alternate, with the previous result kept alive like
+    cito.scp.solve and sometimes dropped, must give every program bit-equal to a
+    fresh eager step at the same point."""
+    from paper_2604_09993_b200.scenario import Layout
+    from paper_2604_09993_b200.subproblem import GpuSCPStep
+
+    name = "halfcheetah_n30"
+    g = load_golden(name)
+    sc = golden_scenario(name)
+    lay = Layout(sc)
+    rng = np.random.default_rng(5)
+    z1 = g["ig_z"]
+    z2 = z1.copy()
+    for k in range(lay.N):  # impulses on: a different pattern
+        z2[lay.phi(k)] = rng.uniform(0.1, 0.5, size=2 * lay.n_c)
+    pts = {"1": (z1, 0.7), "2": (z2, 0.7), "3": (z2, 0.4)}
+    ref = {k: GpuSCPStep(sc, use_graph=False).iterate(z, d, precondition=precondition)[1] for k, (z, d) in pts.items()}
+    pat = lambda p: [getattr(p, M).indptr for M in ("A", "G")] + [getattr(p, M).indices for M in ("A", "G")]  # noqa
+    assert not all(np.array_equal(u, v) for u, v in zip(pat(ref["1"]), pat(ref["2"])))
+    step = GpuSCPStep(sc)
+    keep = None
+    seq = ["1", "2", "2", "1", "1", "3", "2", "1", "1", "1", "3", "3"]
+    for i, key in enumerate(seq):
+        r = step.iterate(*pts[key], precondition=precondition)
+        prog = r[1]
+        for M in ("A", "G"):
+            ma, mb = getattr(prog, M), getattr(ref[key], M)
+            assert np.array_equal(ma.indptr, mb.indptr) and np.array_equal(ma.indices, mb.indices), (i, key, M)
+            assert np.array_equal(ma.data, mb.data), (i, key, M)
+        assert np.array_equal(prog.b, ref[key].b) and np.array_equal(prog.h, ref[key].h)
+        keep = r if i % 4 != 3 else None  # hold the previous result (two buffers in use) most of the time
+        del r, prog
+    assert len(step._plan["hosts"]) >= 2
+    # steady state (same pattern, buffer up to date): values only
+    b0 = step.d2h_copied
+    r = step.iterate(*pts["3"], precondition=precondition)
+    r = step.iterate(*pts["3"], precondition=precondition)
+    b1 = step.d2h_copied
+    r = step.iterate(*pts["3"], precondition=precondition)
+    assert step.d2h_copied - b1 == step.d2h_bytes(precondition) and b1 > b0
+    assert step.d2h_bytes(precondition) < step.d2h_bytes(precondition, indices=True)
+
+
+@pytest.mark.gpu
+def test_gpu_scp_step_results_outlive_the_step():
+    """The program's arrays live in the step's pinned result buffer; they keep that
+    allocation alive after the GpuSCPStep itself is dropped."""
+    import gc
+
+    from paper_2604_09993_b200.subproblem import GpuSCPStep
+
+    name = "halfcheetah_n30"
+    g = load_golden(name)
+    sc = golden_scenario(name)
+    prog = GpuSCPStep(sc).iterate(g["ig_z"], 1.0)[1]
+    saved = [a.copy() for a in (prog.A.data, prog.A.indices, prog.G.data, prog.b)]
+    gc.collect()
+    for _ in range(3):  # other steps allocate (and fill) pinned buffers of the same size
+        GpuSCPStep(sc).iterate(g["ig_z"] * 0.5, 0.3)
+    for a, b in zip((prog.A.data, prog.A.indices, prog.G.data, prog.b), saved):
+        assert np.array_equal(a, b)
+
+
 @pytest.mark.parametrize("name", CASES)
 def test_packed_records_reproduce_reference_csc(name):
     """The 16-byte records of k_csc_flat (subproblem.packed_entries), evaluated on the

@@ -43,7 +43,8 @@ for _ in range(200):
     tot["wait"].append(t2 - t1)
     tot["post"].append(t3 - t2)
 print({k: round(float(np.median(v)) * 1e3, 4) for k, v in tot.items()}, "ms (median)")
-print("packed D2H bytes", step._plan["pk"].nbytes)
+print("packed D2H bytes", step._plan["pk"].nbytes, "copied per call", step.d2h_bytes(pc), "refetches",
+      step.pattern_refetches)
 
 if "--profile" in sys.argv:
     import cProfile

@@ -14,6 +14,8 @@ import os
 import sys
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "oracle"))
@@ -95,7 +97,35 @@ out = {"scenario": f"halfcheetah_bound N={N} (substeps {sc.substeps})", "iterati
        "graph_device_ms": [a.elapsed_time(b) for a, b in dev_ms[-(len(hist) - 1):]] if dev_ms else None,
        "pre_ipm_ms": [1e3 * (a + b + c) for a, b, c in zip(times["linearize_all"], times["build_subproblem"],
                                                            times["precondition"])],
+       "pattern": ({"refetches": sum(st.pattern_refetches for _, st in d._steps.values()),
+                    "d2h_bytes": sum(st.d2h_copied for _, st in d._steps.values()),
+                    "what": "calls whose CSC pattern moved after a values-only copy (one extra index copy each); "
+                            "all device->host bytes of the run incl. warm-up"} if one_pass else None),
        "mode": "install_scp (one device pass per iteration)" if one_pass else "three separate drop-ins",
        "note": "GPU: linearize_all + build_subproblem + precondition (drop-ins); host: the reference's IPM "
                "(cito/_ipm.py) and homotopy, unchanged"}
+if one_pass and "--idle-probe" in sys.argv:
+    # the same pre-IPM call back to back, after 2.5 s of idling, and after 2.5 s of host
+    # numpy work (what the IPM does between two calls): separates GPU idle wake-up from
+    # cold host caches in the per-iteration numbers above
+    cfg = scp.SCPConfig()
+
+    def one():
+        t = time.perf_counter()
+        lin = scp.linearize_all(tr, z, 0.5)
+        prog, _ = scp.build_subproblem(tr, lin, z, 0.5, cfg)
+        scp.precondition(prog)
+        return 1e3 * (time.perf_counter() - t)
+
+    probe = {"back_to_back": [], "after_idle_2p5s": [], "after_host_work_2p5s": []}
+    for _ in range(5):
+        probe["back_to_back"].append(min(one() for _ in range(20)))
+        time.sleep(2.5)
+        probe["after_idle_2p5s"].append(one())
+        t_end = time.perf_counter() + 2.5
+        M = np.random.default_rng(0).standard_normal((600, 600))
+        while time.perf_counter() < t_end:
+            M = np.linalg.solve(M + 600 * np.eye(600), M)
+        probe["after_host_work_2p5s"].append(one())
+    out["idle_probe_ms"] = probe
 print(json.dumps(out))
