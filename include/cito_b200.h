@@ -252,24 +252,26 @@ cito_status cito_csc_assemble2_dev(int32_t nmat, int32_t ncols, const int64_t* c
  * nmat = 2 with out_rows[1] = out_vals[1] = NULL: concatenated output -- the second
  * matrix's entries follow the first's nonzeros in out_rows[0] / out_vals[0], its
  * column pointers (out_ptr[1]) relative to its own first entry.
- * host_vals / host_rows (0 = off): byte offsets from the device outputs to a
+ * host_vals / host_pattern (0 = off): byte offsets from the device outputs to a
  * page-locked host mirror laid out the same way; the kernel also stores every
- * value (host_vals) and, while *rows_wanted (device double) != 0, every row index
- * (host_rows) there, so the result crosses the bus during the compaction. */
+ * value (host_vals) and every column pointer, the stamp and, while *rows_wanted
+ * (device double) != 0, every row index (host_pattern) there, so the result
+ * crosses the bus during the compaction. */
 cito_status cito_csc_assemble_packed_dev(int32_t nmat, int32_t ncols, const void* const* ent, const int64_t* nsup,
                                         const int64_t* const* sp_ptr, const int32_t* const* tcol, const int32_t* ntile,
                                         const double* const* lin, uint32_t* ws, int64_t ws_words,
                                         int32_t* const* out_ptr, int32_t* const* out_rows, double* const* out_vals,
                                         unsigned long long* const* rowmax, const double* stamp_in,
-                                        double* changed_at, int64_t host_vals, int64_t host_rows,
+                                        double* changed_at, int64_t host_vals, int64_t host_pattern,
                                         const double* rows_wanted, void* stream);
 
 /* b / h of the linearized rows: out[rows[i]] = form ? J.z[cols] - v : v - J.z[cols]
- * with J split in up to 3 segments (seg_src < 0 = unused), v = lin[vsrc[i]][voff[i]]. */
+ * with J split in up to 3 segments (seg_src < 0 = unused), v = lin[vsrc[i]][voff[i]];
+ * host != 0: each row also stored at out + host bytes (a page-locked host mirror). */
 cito_status cito_rhs_dev(int64_t nrows, const int32_t* rows, const int8_t* form, const int8_t* vsrc,
                          const int64_t* voff, const int8_t* seg_src, const int64_t* seg_off, const int32_t* seg_len,
                          const int64_t* seg_cb, const int64_t* cols, const double* z, const double* const* lin,
-                         double* out, void* stream);
+                         double* out, int64_t host, void* stream);
 
 /* cito.conic.precondition (cito/conic.py:290-338) of a device-resident program
  * (CSC A: nA rows, G: nG rows, int32 indptr/indices, ncols columns), in place:
@@ -287,22 +289,22 @@ cito_status cito_rhs_dev(int64_t nrows, const int32_t* rows, const int8_t* form,
  * the values before scaling.  G_rows = G_data = keep_G = NULL selects the
  * concatenated layout of cito_csc_assemble_packed_dev: G's entries follow A's
  * A_ptr[ncols] nonzeros in A_rows / A_data / keep_A, G_ptr relative to them.
- * host_vals (0 = off): byte offset from A_data/G_data to a page-locked host
- * mirror that also receives the scaled values.
+ * host (0 = off): byte offset from every output (data, b/h, row scales) to a
+ * page-locked host mirror that also receives it.
  * The cost scaling (c / omega, P / omega) is a host-side scalar (Python layer). */
 cito_status cito_precondition_dev(int32_t ncols, const int32_t* A_ptr, const int32_t* A_rows, double* A_data,
                                   int32_t nA, double* b, const int32_t* G_ptr, const int32_t* G_rows, double* G_data,
                                   int32_t nG, double* h, int32_t n_nonneg, int32_t n_soc, const int32_t* soc_start,
                                   const int32_t* soc_dim, unsigned long long* rowmax_A, unsigned long long* rowmax_G,
                                   int32_t rowmax_ready, int32_t max_nnz, double* row_scale_A, double* row_scale_G,
-                                  double* keep_A, double* keep_b, double* keep_G, double* keep_h, int64_t host_vals,
+                                  double* keep_A, double* keep_b, double* keep_G, double* keep_h, int64_t host,
                                   void* stream);
 
-/* Copy nbytes from device memory to page-locked host memory with a kernel (SM
- * stores over the bus instead of a copy-engine transfer; both pointers 16-byte
- * aligned, dst_host from cudaHostAlloc / a pinned allocation).  Used for the one
- * device->host copy of an SCP iteration's packed result at the end of its graph. */
-cito_status cito_copy_to_host(void* dst_host, const void* src_dev, int64_t nbytes, void* stream);
+/* Copy nbytes src -> dst with a kernel (device or page-locked host memory; SM stores,
+ * no copy-engine transfer); mirror != 0: also to dst + mirror bytes (a page-locked
+ * host mirror of dst).  dst, src and mirror 16-byte aligned.  Used inside an SCP
+ * iteration's graph for the small result fields (flags, constant rhs rows). */
+cito_status cito_copy_mirror(void* dst, const void* src, int64_t nbytes, int64_t mirror, void* stream);
 
 /* FP64 DFMA throughput probe (roofline denominator; not part of the reference
  * interface).  Launches one kernel on `stream`; returns the flops it issues

@@ -89,10 +89,10 @@ def _configure(L):
     L.cito_csc_assemble_packed_dev.restype = ctypes.c_int
     L.cito_csc_assemble_packed_dev.argtypes = ([ctypes.c_int32, ctypes.c_int32] + [_dp] * 7 + [ctypes.c_int64] +
                                                [_dp] * 6 + [ctypes.c_int64, ctypes.c_int64, _dp, _dp])
-    L.cito_copy_to_host.restype = ctypes.c_int
-    L.cito_copy_to_host.argtypes = [_dp, _dp, ctypes.c_int64, _dp]
+    L.cito_copy_mirror.restype = ctypes.c_int
+    L.cito_copy_mirror.argtypes = [_dp, _dp, ctypes.c_int64, ctypes.c_int64, _dp]
     L.cito_rhs_dev.restype = ctypes.c_int
-    L.cito_rhs_dev.argtypes = [ctypes.c_int64] + [_dp] * 13
+    L.cito_rhs_dev.argtypes = [ctypes.c_int64] + [_dp] * 12 + [ctypes.c_int64, _dp]
     L.cito_dfma_peak.restype = ctypes.c_double
     L.cito_dfma_peak.argtypes = [ctypes.c_int32, _dp, _dp]
     return L

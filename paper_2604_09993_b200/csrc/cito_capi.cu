@@ -688,7 +688,7 @@ cito_status cito_csc_assemble_packed_dev(int32_t nmat, int32_t ncols, const void
                                         const double* const* lin, uint32_t* ws, int64_t ws_words,
                                         int32_t* const* out_ptr, int32_t* const* out_rows, double* const* out_vals,
                                         unsigned long long* const* rowmax, const double* stamp_in,
-                                        double* changed_at, int64_t host_vals, int64_t host_rows,
+                                        double* changed_at, int64_t host_vals, int64_t host_pattern,
                                         const double* rows_wanted, void* stream) {
   if (nmat < 1 || nmat > 2 || ncols < 0 || !ent || !nsup || !sp_ptr || !tcol || !ntile || !ws ||
       (stamp_in == nullptr) != (changed_at == nullptr))
@@ -696,9 +696,10 @@ cito_status cito_csc_assemble_packed_dev(int32_t nmat, int32_t ncols, const void
   CscPackedArgs a;
   a.stamp_in = stamp_in;
   a.changed_at = changed_at;
-  if (host_rows && !rows_wanted) return fail(CITO_ERR_ARG, "csc_assemble_packed: host_rows needs rows_wanted");
+  if (host_pattern && !rows_wanted)
+    return fail(CITO_ERR_ARG, "csc_assemble_packed: host_pattern needs rows_wanted");
   a.host_vals = host_vals;
-  a.host_rows = host_rows;
+  a.host_pattern = host_pattern;
   a.rows_wanted = rows_wanted;
   int64_t tiles = 0;
   for (int m = 0; m < 2; ++m) {
@@ -749,14 +750,14 @@ cito_status cito_csc_assemble_dev(int32_t ncols, const int64_t* sp_ptr, const in
 cito_status cito_rhs_dev(int64_t nrows, const int32_t* rows, const int8_t* form, const int8_t* vsrc,
                          const int64_t* voff, const int8_t* seg_src, const int64_t* seg_off, const int32_t* seg_len,
                          const int64_t* seg_cb, const int64_t* cols, const double* z, const double* const* lin,
-                         double* out, void* stream) {
+                         double* out, int64_t host, void* stream) {
   if (nrows <= 0) return CITO_OK;
   LinTable L;
   for (int k = 0; k < 10; ++k) L.p[k] = lin ? lin[k] : nullptr;
   const int wpb = 8;
   count_launch();
   k_rhs<<<(unsigned)((nrows + wpb - 1) / wpb), 32 * wpb, 0, (cudaStream_t)stream>>>(
-      nrows, rows, form, vsrc, voff, seg_src, seg_off, seg_len, seg_cb, cols, z, L, out);
+      nrows, rows, form, vsrc, voff, seg_src, seg_off, seg_len, seg_cb, cols, z, L, out, host);
   CUDA_TRY(cudaGetLastError());
   return CITO_OK;
 }
@@ -766,7 +767,7 @@ cito_status cito_precondition_dev(int32_t ncols, const int32_t* A_ptr, const int
                                   int32_t nG, double* h, int32_t n_nonneg, int32_t n_soc, const int32_t* soc_start,
                                   const int32_t* soc_dim, unsigned long long* rowmax_A, unsigned long long* rowmax_G,
                                   int32_t rowmax_ready, int32_t max_nnz, double* row_scale_A, double* row_scale_G,
-                                  double* keep_A, double* keep_b, double* keep_G, double* keep_h, int64_t host_vals,
+                                  double* keep_A, double* keep_b, double* keep_G, double* keep_h, int64_t host,
                                   void* stream) {
   if (ncols < 0 || nA < 0 || nG < 0 || n_nonneg < 0 || n_nonneg > nG || n_soc < 0 || max_nnz < 0)
     return fail(CITO_ERR_ARG, "precondition: bad sizes");
@@ -793,7 +794,7 @@ cito_status cito_precondition_dev(int32_t ncols, const int32_t* A_ptr, const int
   a.keep_rhs[0] = keep_b;
   a.keep_rhs[1] = keep_h;
   a.concat = G_data == nullptr;
-  a.host_vals = host_vals;
+  a.host = host;
   if (!rowmax_ready) {
     if (nA) CUDA_TRY(cudaMemsetAsync(rowmax_A, 0, sizeof(unsigned long long) * (size_t)nA, s));
     if (nG) CUDA_TRY(cudaMemsetAsync(rowmax_G, 0, sizeof(unsigned long long) * (size_t)nG, s));
@@ -824,21 +825,28 @@ cito_status cito_precondition_dev(int32_t ncols, const int32_t* A_ptr, const int
   return CITO_OK;
 }
 
-// SM-driven copy into page-locked host memory (mapped under unified addressing):
-// 16-byte stores straight over the bus, issued by the kernel that follows the
-// producers in the same graph -- no copy-engine hand-off between the last kernel
-// and the transfer.
+// Copy kernel, optionally mirrored into page-locked host memory (mapped under
+// unified addressing): 16-byte stores straight over the bus from the SMs, so a
+// small result field travels inside the graph's kernel stream -- no copy-engine
+// hand-off.
 __global__ void __launch_bounds__(256) k_copy_out(uint4* __restrict__ dst, const uint4* __restrict__ src, int64_t n16,
                                                   unsigned char* __restrict__ dtail,
-                                                  const unsigned char* __restrict__ stail, int ntail) {
+                                                  const unsigned char* __restrict__ stail, int ntail, int64_t mirror) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += stride) dst[i] = src[i];
-  if (blockIdx.x == 0 && (int)threadIdx.x < ntail) dtail[threadIdx.x] = stail[threadIdx.x];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += stride) {
+    const uint4 v = src[i];
+    dst[i] = v;
+    if (mirror) mirror_store(dst + i, mirror, v);
+  }
+  if (blockIdx.x == 0 && (int)threadIdx.x < ntail) {
+    dtail[threadIdx.x] = stail[threadIdx.x];
+    if (mirror) mirror_store(dtail + threadIdx.x, mirror, stail[threadIdx.x]);
+  }
 }
 
-cito_status cito_copy_to_host(void* dst_host, const void* src_dev, int64_t nbytes, void* stream) {
-  if (nbytes < 0 || ((uintptr_t)dst_host & 15) || ((uintptr_t)src_dev & 15))
-    return fail(CITO_ERR_ARG, "copy_to_host: negative size or pointers not 16-byte aligned");
+cito_status cito_copy_mirror(void* dst, const void* src, int64_t nbytes, int64_t mirror, void* stream) {
+  if (nbytes < 0 || ((uintptr_t)dst & 15) || ((uintptr_t)src & 15) || (mirror & 15))
+    return fail(CITO_ERR_ARG, "copy: negative size or pointers not 16-byte aligned");
   if (nbytes == 0) return CITO_OK;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -848,9 +856,9 @@ cito_status cito_copy_to_host(void* dst_host, const void* src_dev, int64_t nbyte
   const int64_t want = (n16 + 255) / 256;
   const unsigned grid = (unsigned)(want < 1 ? 1 : (want < 2 * sms ? want : 2 * sms));
   count_launch();
-  k_copy_out<<<grid, 256, 0, (cudaStream_t)stream>>>((uint4*)dst_host, (const uint4*)src_dev, n16,
-                                                     (unsigned char*)dst_host + 16 * n16,
-                                                     (const unsigned char*)src_dev + 16 * n16, ntail);
+  k_copy_out<<<grid, 256, 0, (cudaStream_t)stream>>>((uint4*)dst, (const uint4*)src, n16,
+                                                     (unsigned char*)dst + 16 * n16,
+                                                     (const unsigned char*)src + 16 * n16, ntail, mirror);
   CUDA_TRY(cudaGetLastError());
   return CITO_OK;
 }

@@ -415,11 +415,12 @@ struct CscPackedArgs {
   // previous launch over the same outputs (and skips re-copying the indices)
   const double* stamp_in;
   double* changed_at;
-  // host mirror (0 = off): the values (host_vals) / the row indices (host_rows, only
-  // while *rows_wanted != 0) are also stored at byte offset host_* from their device
-  // address -- into page-locked host memory laid out like the device outputs, so the
-  // result crosses the bus while the compaction runs instead of in a copy after it
-  int64_t host_vals, host_rows;
+  // host mirror (0 = off): the values (host_vals) / the pattern (host_pattern: column
+  // pointers, the stamp, and the row indices while *rows_wanted != 0) are also stored
+  // at that byte offset from their device address -- into page-locked host memory
+  // laid out like the device outputs, so the result crosses the bus while the
+  // compaction runs instead of in a copy after it
+  int64_t host_vals, host_pattern;
   const double* rows_wanted;
 };
 
@@ -437,6 +438,10 @@ __global__ void __launch_bounds__(256) k_csc_flat(int32_t ncols, const CscPacked
   __shared__ unsigned masks[CSC_TJ][8];
   __shared__ int base[CSC_TJ][8];
   __shared__ int red[8], red_b[8];
+  // the tile's output staged for the host mirror: written back as whole 16-byte
+  // chunks of its contiguous output range (full bus lines instead of scattered words)
+  __shared__ __align__(16) double stage_v[CSC_TILE];
+  __shared__ __align__(16) int32_t stage_r[CSC_TILE];
   if (tid == 0) tile_s = (int)atomicAdd(&ws[0], 1u);
   __syncthreads();
   const int tile = tile_s;
@@ -546,7 +551,7 @@ __global__ void __launch_bounds__(256) k_csc_flat(int32_t ncols, const CscPacked
   double* __restrict__ oval = concat ? a.out_vals[0] + obase_s : a.out_vals[m];
   unsigned long long* rmax = a.rowmax[m];
   const bool stamp = a.changed_at != nullptr;
-  const int64_t hv = a.host_vals, hr = (a.host_rows && *a.rows_wanted != 0.0) ? a.host_rows : 0;
+  const int64_t hv = a.host_vals, hp = a.host_pattern, hr = (hp && *a.rows_wanted != 0.0) ? hp : 0;
   bool moved = false;
 #pragma unroll
   for (int j = 0; j < CSC_TJ; ++j) {
@@ -555,8 +560,8 @@ __global__ void __launch_bounds__(256) k_csc_flat(int32_t ncols, const CscPacked
       if (stamp) moved |= orow[pos] != row[j];
       orow[pos] = row[j];
       oval[pos] = v[j];
-      if (hv) mirror_store(oval + pos, hv, v[j]);
-      if (hr) mirror_store(orow + pos, hr, row[j]);
+      if (hv) stage_v[pos - tb] = v[j];
+      if (hr) stage_r[pos - tb] = row[j];
       // fused row inf-norm (cito/conic.py:281-287): non-negative doubles order like their bits
       if (rmax) atomicMax(&rmax[row[j]], (unsigned long long)__double_as_longlong(fabs(v[j])));
     }
@@ -576,8 +581,39 @@ __global__ void __launch_bounds__(256) k_csc_flat(int32_t ncols, const CscPacked
     }
     if (stamp) moved |= a.out_ptr[m][c] != tb + cnt;
     a.out_ptr[m][c] = tb + cnt;
+    if (hp) mirror_store(a.out_ptr[m] + c, hp, tb + cnt);
   }
-  if (stamp && __syncthreads_or(moved) && tid == 0) *a.changed_at = *a.stamp_in;
+  if (stamp && __syncthreads_or(moved) && tid == 0) {
+    *a.changed_at = *a.stamp_in;
+    if (hp) mirror_store(a.changed_at, hp, *a.stamp_in);
+  }
+  if (hv || hr) {  // the staged range [tb, tb + ttot) -> host, 16-byte stores
+    __syncthreads();
+    const int n = ttot_s;
+    if (hv) {
+      double* hd = reinterpret_cast<double*>(reinterpret_cast<char*>(oval + tb) + hv);
+      const int head = (reinterpret_cast<uintptr_t>(hd) & 15) ? 1 : 0;
+      const int np = (n - head) >> 1;
+      double2* d2 = reinterpret_cast<double2*>(hd + head);
+      for (int k = tid; k < np; k += blockDim.x) d2[k] = make_double2(stage_v[head + 2 * k], stage_v[head + 2 * k + 1]);
+      if (tid == 0 && head && n > 0) hd[0] = stage_v[0];
+      if (tid == 1 && n > head && ((n - head) & 1)) hd[n - 1] = stage_v[n - 1];
+    }
+    if (hr) {
+      int32_t* hd = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(orow + tb) + hr);
+      const int head = (int)((16 - (reinterpret_cast<uintptr_t>(hd) & 15)) & 15) / 4;
+      const int h0 = head < n ? head : n;
+      const int nq = (n - h0) >> 2;
+      int4* d4 = reinterpret_cast<int4*>(hd + h0);
+      for (int k = tid; k < nq; k += blockDim.x) {
+        const int e = h0 + 4 * k;
+        d4[k] = make_int4(stage_r[e], stage_r[e + 1], stage_r[e + 2], stage_r[e + 3]);
+      }
+      if (tid < h0) hd[tid] = stage_r[tid];
+      const int t0e = h0 + 4 * nq;
+      if (tid < n - t0e) hd[t0e + tid] = stage_r[t0e + tid];
+    }
+  }
 }
 
 __global__ void __launch_bounds__(256) k_rhs(int64_t nrows, const int32_t* __restrict__ rows,
@@ -586,7 +622,7 @@ __global__ void __launch_bounds__(256) k_rhs(int64_t nrows, const int32_t* __res
                                              const int64_t* __restrict__ seg_off, const int32_t* __restrict__ seg_len,
                                              const int64_t* __restrict__ seg_cb, const int64_t* __restrict__ cols,
                                              const double* __restrict__ z, const LinTable L,
-                                             double* __restrict__ out) {
+                                             double* __restrict__ out, int64_t host) {
   const int lane = threadIdx.x & 31;
   const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (i >= nrows) return;
@@ -604,7 +640,9 @@ __global__ void __launch_bounds__(256) k_rhs(int64_t nrows, const int32_t* __res
   for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
   if (lane == 0) {
     const double v = L.p[vsrc[i]][voff[i]];
-    out[rows[i]] = form[i] == 0 ? v - dot : dot - v;  // dynamics: ends - J.ref ; others: J.ref - value
+    const double r = form[i] == 0 ? v - dot : dot - v;  // dynamics: ends - J.ref ; others: J.ref - value
+    out[rows[i]] = r;
+    if (host) mirror_store(out + rows[i], host, r);  // page-locked host mirror (0 = off)
   }
 }
 
@@ -630,7 +668,7 @@ struct PcArgs {
   double* keep[2];      // optional: the unscaled values are stored here before scaling
   double* keep_rhs[2];  // optional: the unscaled b / h
   int32_t concat;       // G's entries follow A's nonzeros in rows[0] / data[0] / keep[0]
-  int64_t host_vals;    // host mirror of the scaled values (byte offset from data; 0 = off)
+  int64_t host;         // host mirror of every output (byte offset from the device address; 0 = off)
 };
 
 // entry arrays of matrix m (concatenated layout: G starts after A's nonzeros)
@@ -663,6 +701,7 @@ __global__ void __launch_bounds__(256) k_row_scale(const PcArgs a, int32_t n_non
     const double r = __longlong_as_double((long long)a.rowmax[0][i]);
     a.rowmax[0][i] = 0ull;
     a.scale[0][i] = 1.0 / (r == 0.0 ? 1.0 : r);  // ra[ra == 0] = 1; da = 1 / ra
+    if (a.host) mirror_store(a.scale[0] + i, a.host, a.scale[0][i]);
     return;
   }
   const int64_t j = i - nA;
@@ -670,6 +709,7 @@ __global__ void __launch_bounds__(256) k_row_scale(const PcArgs a, int32_t n_non
     const double r = __longlong_as_double((long long)a.rowmax[1][j]);
     a.rowmax[1][j] = 0ull;
     a.scale[1][j] = r != 0.0 ? 1.0 / r : 1.0;
+    if (a.host) mirror_store(a.scale[1] + j, a.host, a.scale[1][j]);
     return;
   }
   const int64_t k = j - n_nonneg;
@@ -681,7 +721,10 @@ __global__ void __launch_bounds__(256) k_row_scale(const PcArgs a, int32_t n_non
       a.rowmax[1][s0 + r] = 0ull;
     }
     const double sc = mx > 0.0 ? 1.0 / mx : 1.0;
-    for (int32_t r = 0; r < d; ++r) a.scale[1][s0 + r] = sc;
+    for (int32_t r = 0; r < d; ++r) {
+      a.scale[1][s0 + r] = sc;
+      if (a.host) mirror_store(a.scale[1] + s0 + r, a.host, sc);
+    }
   }
 }
 
@@ -702,12 +745,13 @@ __global__ void __launch_bounds__(256) k_row_apply(int32_t ncols, const PcArgs a
       if (keep) keep[i] = v;
       const double w = sc[rows[i]] * v;
       data[i] = w;
-      if (a.host_vals) mirror_store(data + i, a.host_vals, w);
+      if (a.host) mirror_store(data + i, a.host, w);
     } else {
       const int64_t r = i - nnz;
       const double v = a.rhs[m][r];
       if (keep_rhs) keep_rhs[r] = v;
       a.rhs[m][r] = sc[r] * v;
+      if (a.host) mirror_store(a.rhs[m] + r, a.host, sc[r] * v);
     }
   }
 }

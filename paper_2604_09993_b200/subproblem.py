@@ -690,7 +690,7 @@ class SubproblemAssembler:
             _lib.check(_lib.lib().cito_rhs_dev(
                 r["n"], r["rows"].data_ptr(), r["form"].data_ptr(), r["vsrc"].data_ptr(), r["voff"].data_ptr(),
                 r["seg_src"].data_ptr(), r["seg_off"].data_ptr(), r["seg_len"].data_ptr(), r["seg_cb"].data_ptr(),
-                r["cols"].data_ptr(), z_ref_dev.data_ptr(), ptrs, rhs.data_ptr(), side.cuda_stream), "rhs")
+                r["cols"].data_ptr(), z_ref_dev.data_ptr(), ptrs, rhs.data_ptr(), 0, side.cuda_stream), "rhs")
         if _CSC_RECIPES:  # A/B: the warp-per-column recipe-table form
             _lib.check(_lib.lib().cito_csc_assemble2_dev(
                 2, self.pat.n, arr([d["sp_ptr"] for d in mats]), arr([d["row"] for d in mats]),
@@ -914,7 +914,7 @@ class _HostBuf:
     def __init__(self, pk):
         import torch
 
-        self.host = torch.empty(pk.nbytes, dtype=torch.uint8, pin_memory=True)
+        self.host = torch.zeros(pk.nbytes, dtype=torch.uint8, pin_memory=True)
         self.nb = self.host.numpy()
         self.h, self.np_dtype, self.off = {}, {}, {}
         for name, (o, dtype, n, isz) in pk.layout.items():
@@ -1071,7 +1071,7 @@ class GpuSCPStep:
             rhs_args=(r["n"], r["rows"].data_ptr(), r["form"].data_ptr(), r["vsrc"].data_ptr(),
                       r["voff"].data_ptr(), r["seg_src"].data_ptr(), r["seg_off"].data_ptr(),
                       r["seg_len"].data_ptr(), r["seg_cb"].data_ptr(), r["cols"].data_ptr(), pl["z_dev"].data_ptr(),
-                      lin_ptrs, pl["rhs_dev"].data_ptr()),
+                      lin_ptrs, pl["rhs_dev"].data_ptr(), delta),
             lin_args=(gt.disc._h.ptr, N, 1, int(lay.dim), int(gt.base_u), int(gt.base_p), pl["z_dev"].data_ptr(),
                       pl["zde_dev"][lay.dim:].data_ptr()),
             lin_outs=tuple(lin[kk].data_ptr() for kk in ("ends", "jx", "ju", "js", "defects", "bad", "psi",
@@ -1095,9 +1095,15 @@ class GpuSCPStep:
         cur = torch.cuda.current_stream(self.gt.device)
         side = pl["side"]
         side.wait_stream(cur)
-        with torch.cuda.stream(side):
-            pl["rhs_dev"].copy_(pl["rhs_const"])
+        pk = pl["pk"]
+        with torch.cuda.stream(side):  # every store also into hb's host mirror
+            rc = pl["rhs_const"]
+            _lib.check(L.cito_copy_mirror(pl["rhs_dev"].data_ptr(), rc.data_ptr(), rc.numel() * 8, sl["delta"],
+                                          side.cuda_stream), "rhs constants")
             _lib.check(L.cito_rhs_dev(*sl["rhs_args"], side.cuda_stream), "rhs")
+            # K1's non-finite flags (final once the side stream starts)
+            _lib.check(L.cito_copy_mirror(hb.host.data_ptr(), pk.dev.data_ptr(), pk.layout["changed_at"][0], 0,
+                                          side.cuda_stream), "flags")
         # the compaction (A and G concatenated; the fused row norms accumulate into the
         # rowmax workspace, which the preconditioning leaves zero again)
         _lib.check(L.cito_csc_assemble_packed_dev(*(sl["packed_pc"] if precondition else sl["packed"]), s),
@@ -1107,10 +1113,9 @@ class GpuSCPStep:
             u = sl["unscaled"]
             _lib.check(L.cito_precondition_dev(*pl["pc_args"], u["vals"].data_ptr(), u["rhs"].data_ptr(), None,
                                                u["rhs"][pl["nA"]:].data_ptr(), sl["delta"], s), "precondition")
-        # the fixed fields (flags, column pointers, b/h, row scales) in one copy kernel; the
-        # values (and wanted rows) are in the host buffer already
-        end = pl["pk"].layout["vals" if precondition else "row_scale_A"][0]
-        _lib.check(L.cito_copy_to_host(hb.host.data_ptr(), pl["pk"].dev.data_ptr(), end, s), "copy_to_host")
+        # no copy at the end: every result field reached hb's host mirror from the kernel
+        # that wrote it (flags, rhs rows, column pointers, stamp, values, wanted row
+        # indices; row scales and scaled values/rhs from the preconditioning)
 
     def _copy_rows(self, hb, nnz):
         """Copy-engine transfer of the CSC row indices [0, nnz) into hb (a call whose
@@ -1124,9 +1129,15 @@ class GpuSCPStep:
         the fixed fields + the values (+ the row indices with ``indices``, as in a
         call whose buffer does not hold the current pattern).  ``self.d2h_copied``
         counts the bytes every call actually moved."""
-        lay = self._plan["pk"].layout
-        nnz = self._plan.get("last_nnz", lay["vals"][2])
-        return int(lay["vals" if precondition else "row_scale_A"][0] + 8 * nnz + (4 * nnz if indices else 0))
+        pl = self._plan
+        lay = pl["pk"].layout
+        nnz = pl.get("last_nnz", lay["vals"][2])
+        nrhs = pl["nA"] + pl["nG"]
+        n = (4 * lay["bad"][2] + 8 + 4 * (lay["A_indptr"][2] + lay["G_indptr"][2]) + 8 * nrhs + 8 * nnz
+             + (4 * nnz if indices else 0))
+        if precondition:  # the row scales, and b/h once more (scaled)
+            n += 16 * nrhs
+        return int(n)
 
     def _host_buffer(self):
         """A pinned result buffer no live array points into (a new one when every
