@@ -110,16 +110,25 @@ if one_pass and "--idle-probe" in sys.argv:
     # cold host caches in the per-iteration numbers above
     cfg = scp.SCPConfig()
 
+    split = []
+
     def one():
         t = time.perf_counter()
         lin = scp.linearize_all(tr, z, 0.5)
+        t1 = time.perf_counter()
         prog, _ = scp.build_subproblem(tr, lin, z, 0.5, cfg)
+        t2 = time.perf_counter()
         scp.precondition(prog)
-        return 1e3 * (time.perf_counter() - t)
+        t3 = time.perf_counter()
+        split.append((t1 - t, t2 - t1, t3 - t2))
+        return 1e3 * (t3 - t)
 
     probe = {"back_to_back": [], "after_idle_2p5s": [], "after_host_work_2p5s": []}
     for _ in range(5):
+        split.clear()
         probe["back_to_back"].append(min(one() for _ in range(20)))
+        probe.setdefault("back_to_back_split_ms", []).append(
+            [round(1e3 * float(np.median([x[i] for x in split])), 4) for i in range(3)])
         time.sleep(2.5)
         probe["after_idle_2p5s"].append(one())
         t_end = time.perf_counter() + 2.5
