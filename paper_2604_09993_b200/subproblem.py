@@ -925,6 +925,7 @@ class _HostBuf:
         self.graphs = {}
         self.live = []
         self.pat_gen = -1  # pattern generation of the CSC indices last copied into this buffer
+        self.rhs_scaled = False  # b/h here were row-scaled by a preconditioned call (constant rows too)
 
     def wrap(self, name, start, n):
         """Array of n elements of field `name` from element `start`, owned by a _Span."""
@@ -1015,6 +1016,7 @@ class GpuSCPStep:
         P_ptr = np.concatenate([np.arange(dim + 1), np.full(pat.n - dim, dim)]).astype(np.int32)
         self._plan = dict(pk=pk, z_dev=z_dev, zde_dev=zde_dev, zde_pin=zde_pin, rowmax=rowmax, rhs_dev=rhs_dev,
                           hosts=[], graph_kernels={}, side=torch.cuda.Stream(dev), rhs_const=asm._rhs["const"],
+                          rhs_const_host=asm._rhs["const"].cpu().numpy(),
                           pc_args=pc_args, keep=keep, L=_lib.lib(), nA=nA, nG=nG,
                           soc=(soc_start, soc_dim), P_idx=P_idx, P_ptr=P_ptr, arr=arr,
                           P_plain=None, meta=_Meta(pat.z_idx, pat.sp_idx, pat.sm_idx, pat.t_idx),
@@ -1097,8 +1099,10 @@ class GpuSCPStep:
         side.wait_stream(cur)
         pk = pl["pk"]
         with torch.cuda.stream(side):  # every store also into hb's host mirror
+            # the constant rows of b/h: device only -- the host buffer holds them since its
+            # creation (restored after a preconditioned call scaled them there)
             rc = pl["rhs_const"]
-            _lib.check(L.cito_copy_mirror(pl["rhs_dev"].data_ptr(), rc.data_ptr(), rc.numel() * 8, sl["delta"],
+            _lib.check(L.cito_copy_mirror(pl["rhs_dev"].data_ptr(), rc.data_ptr(), rc.numel() * 8, 0,
                                           side.cuda_stream), "rhs constants")
             _lib.check(L.cito_rhs_dev(*sl["rhs_args"], side.cuda_stream), "rhs")
             # K1's non-finite flags (final once the side stream starts)
@@ -1132,10 +1136,12 @@ class GpuSCPStep:
         pl = self._plan
         lay = pl["pk"].layout
         nnz = pl.get("last_nnz", lay["vals"][2])
-        nrhs = pl["nA"] + pl["nG"]
-        n = (4 * lay["bad"][2] + 8 + 4 * (lay["A_indptr"][2] + lay["G_indptr"][2]) + 8 * nrhs + 8 * nnz
+        nrhs, nlin = pl["nA"] + pl["nG"], int(self.asm._rhs["n"])
+        # flags, stamp, column pointers, the linearized b/h rows (the constant ones stay in
+        # the host buffer), values, wanted row indices
+        n = (4 * lay["bad"][2] + 8 + 4 * (lay["A_indptr"][2] + lay["G_indptr"][2]) + 8 * nlin + 8 * nnz
              + (4 * nnz if indices else 0))
-        if precondition:  # the row scales, and b/h once more (scaled)
+        if precondition:  # the row scales and every b/h row once more (scaled)
             n += 16 * nrhs
         return int(n)
 
@@ -1148,6 +1154,7 @@ class GpuSCPStep:
                 return hb
         hb = _HostBuf(pl["pk"])
         hb.slot = self._make_slot(hb)
+        hb.h["rhs"][:] = pl["rhs_const_host"]
         pl["hosts"].append(hb)
         return hb
 
@@ -1160,6 +1167,7 @@ class GpuSCPStep:
         pl["captures"] = pl.get("captures", 0) + 1
         self._launch(precondition, hb)
         torch.cuda.current_stream(self.gt.device).synchronize()
+        hb.rhs_scaled |= bool(precondition)
         g = torch.cuda.CUDAGraph()
         n0 = _lib.launch_count()
         with torch.cuda.graph(g):
@@ -1198,6 +1206,9 @@ class GpuSCPStep:
         # pattern moves, and then they are fetched after the synchronization)
         idx_now = hb.pat_gen != pl["pat_gen"]
         zp[dim + 3] = 1.0 if idx_now else 0.0
+        if hb.rhs_scaled and not precondition:  # the constant b/h rows, scaled there by a preconditioned call
+            hb.h["rhs"][:] = pl["rhs_const_host"]
+            hb.rhs_scaled = False
         if self.use_graph:
             g = hb.graphs.get(bool(precondition))
             if g is None:
@@ -1206,6 +1217,7 @@ class GpuSCPStep:
             _lib.add_graph_launches(pl["graph_kernels"][bool(precondition)])
         else:
             self._launch(bool(precondition), hb)
+        hb.rhs_scaled |= bool(precondition)
         nA = pl["nA"]
         # host work that does not depend on the device results runs while the GPU works:
         # the objective, the (scaled) P, the lazy LinearizedProblem
@@ -1276,6 +1288,7 @@ class GpuSCPStep:
         while len(pl["hosts"]) < n:
             hb = _HostBuf(pl["pk"])
             hb.slot = self._make_slot(hb)
+            hb.h["rhs"][:] = pl["rhs_const_host"]
             pl["hosts"].append(hb)
         for hb in pl["hosts"][:n]:
             if bool(precondition) not in hb.graphs:

@@ -291,6 +291,28 @@ def test_gpu_scp_step_pattern_stamp_sequence(precondition):
 
 
 @pytest.mark.gpu
+def test_gpu_scp_step_mixed_modes_same_buffer():
+    """Plain and preconditioned calls alternating on the same result buffer: the
+    constant b/h rows live in the host buffer (scaled there by a preconditioned
+    call and restored before a plain one), so every program must equal a fresh
+    step of its own mode."""
+    from paper_2604_09993_b200.subproblem import GpuSCPStep
+
+    name = "halfcheetah_n30"
+    g = load_golden(name)
+    sc = golden_scenario(name)
+    z = g["ig_z"]
+    ref = {pc: GpuSCPStep(sc, use_graph=False).iterate(z, 0.8, precondition=pc)[1] for pc in (False, True)}
+    step = GpuSCPStep(sc)
+    for pc in (False, True, False, False, True, True, False):
+        prog = step.iterate(z, 0.8, precondition=pc)[1]
+        assert np.array_equal(prog.b, ref[pc].b) and np.array_equal(prog.h, ref[pc].h), pc
+        assert np.array_equal(prog.A.data, ref[pc].A.data) and np.array_equal(prog.G.data, ref[pc].G.data), pc
+        del prog  # the next call reuses a buffer (the last preconditioned one stays held for unscaled_program)
+    assert len(step._plan["hosts"]) <= 2
+
+
+@pytest.mark.gpu
 def test_gpu_scp_step_results_outlive_the_step():
     """The program's arrays live in the step's pinned result buffer; they keep that
     allocation alive after the GpuSCPStep itself is dropped."""
