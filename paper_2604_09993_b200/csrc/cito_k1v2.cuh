@@ -319,7 +319,7 @@ struct RegState {
 #define RS_HV(h) rs[RegState<M>::NH + (h)]
 #ifndef CITO_JAC_ONE_WARP
 // 2 (default): every rate-Jacobian direction (q, v and u: 32 for HalfCheetah) on ONE
-// warp with the generic tangent code (kind 7), 5 warps per CTA -- one hot code path
+// warp with the generic tangent code (kind 7), one warp fewer per CTA -- one hot code path
 // less per tick (measured 0.108 vs 0.114 ms for 29 intervals, same box); 1: the same
 // with the u-Jacobian warp kept idle; 0: q/v and u directions on two warps
 // (specialised kinds 3 and 4)
