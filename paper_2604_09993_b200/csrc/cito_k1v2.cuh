@@ -814,6 +814,9 @@ __global__ void __launch_bounds__(JAC ? K2Dims<M>::NT : 64, MINB) k_linearize2(c
   // (the CSC compaction) may start its independent prologue now; it waits for this grid's
   // completion and memory before reading any result (griddepcontrol.wait)
   asm volatile("griddepcontrol.launch_dependents;");
+#ifdef CITO_PROF
+  if (g_cito_prof && blockIdx.x == 0 && threadIdx.x == 0) g_cito_prof[1664] = clock64();
+#endif
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t zp = zs.z ? b / zs.n_int : 0, zk = zs.z ? b % zs.n_int : 0;
   const double* zb = zs.z ? zs.z + zp * zs.zstride : nullptr;
@@ -1032,4 +1035,7 @@ __global__ void __launch_bounds__(JAC ? K2Dims<M>::NT : 64, MINB) k_linearize2(c
   }
   __syncthreads();
   if (tid == 0 && bad) bad[b] = sh.bad;
+#ifdef CITO_PROF
+  if (g_cito_prof && blockIdx.x == 0 && threadIdx.x == 0) g_cito_prof[1665] = clock64();
+#endif
 }

@@ -37,7 +37,7 @@ def run(B):
     x, U, Sv = synth.random_intervals(sc, B, seed=0)
     dev = torch.device("cuda")
     xd, Ud, Sd = (torch.as_tensor(a, device=dev) for a in (x, U, Sv))
-    buf = torch.zeros(1024 + 40 * 16, dtype=torch.int64, device=dev)
+    buf = torch.zeros(1024 + 40 * 16 + 16, dtype=torch.int64, device=dev)
     for _ in range(3):
         disc.linearize_batch_device(xd, Ud, Sd)
     torch.cuda.synchronize()
@@ -47,7 +47,7 @@ def run(B):
     L.cito_prof_set(None)
     full = buf.cpu().numpy().astype(np.int64)
     a = full[:640].reshape(40, 8, 2)
-    pp = full[1024:].reshape(40, 16)
+    pp = full[1024:1024 + 640].reshape(40, 16)
     for t in (3, 10, 17):
         row = pp[t][pp[t] > 0]
         print("primal tick", t, "sub-step cycles", np.diff(row).tolist())
@@ -64,6 +64,10 @@ def run(B):
         tot.append(nxt - st.min())
         print(f"{t:4d}  " + "  ".join(f"{int(e - s):8d}" for s, e in zip(st, en)) + f"   {int(nxt - st.min()):8d}")
     print("total cycles", int(a[nt - 1, :nw, 1].max() - t0), "mean tick", float(np.mean(tot)))
+    k0, k1 = int(full[1664]), int(full[1665])
+    if k0 and k1:
+        print("kernel (CTA 0) cycles", k1 - k0, "prologue", int(t0 - k0),
+              "after tick", nt - 1, int(k1 - a[nt - 1, :nw, 1].max()), "(the remaining ticks + outputs)")
 
 
 if __name__ == "__main__":
