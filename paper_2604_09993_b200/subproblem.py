@@ -490,21 +490,23 @@ def packed_entries(csc, sigma):
     return rec, np.concatenate([tcol, [len(csc["indptr"])]]).astype(np.int32)
 
 
-def _csc_direct(data, indices, indptr, shape):
+def _csc_direct(data, indices, indptr, shape, check=True):
     """scipy.sparse.csc_matrix over arrays already in canonical form (int32 indices,
     float64 data, len == nnz; sorted, no duplicates -- the device compaction's
     output), without the constructor's per-call dtype/format checks (~20 us per
     matrix).  Probed once against the regular constructor: if this scipy's matrix
     carries attributes the direct form does not set, the regular one is used.
     Every call keeps the O(1) invariants (int32/float64 dtypes, indptr[0] == 0,
-    indptr[-1] == nnz, len(indptr) == ncols + 1); CITO_CHECK_CSC=1 adds scipy's
-    full format check (sorted, in-range indices) for debugging."""
+    indptr[-1] == nnz, len(indptr) == ncols + 1; check=False leaves the two that
+    read indptr's contents to the caller, for a matrix built before the device
+    result arrived); CITO_CHECK_CSC=1 adds scipy's full format check (sorted,
+    in-range indices) for debugging."""
     global _CSC_FAST
     import scipy.sparse as sp
 
     if (indices.dtype != np.int32 or indptr.dtype != np.int32 or data.dtype != np.float64
-            or len(indptr) != shape[1] + 1 or indptr[0] != 0 or indptr[-1] != len(indices)
-            or len(data) != len(indices)):
+            or len(indptr) != shape[1] + 1 or len(data) != len(indices)
+            or (check and (indptr[0] != 0 or indptr[-1] != len(indices)))):
         raise RuntimeError("device CSC compaction returned an inconsistent matrix "
                            f"(indptr[0]={indptr[0]}, indptr[-1]={indptr[-1]}, nnz={len(indices)})")
     if _CSC_CHECK:
@@ -1239,11 +1241,17 @@ class GpuSCPStep:
                 pl["P_plain"] = Pm
             P = pl["P_plain"]
         lin = self._Lazy(hb.slot["lin"], z.copy())
-        ConicProgram, ConeSpec = _conic_types()
+        # the scipy/program objects over the pinned buffer, built while the GPU works with
+        # the nonzero counts of the previous call (the pattern rarely moves between SCP
+        # iterations); checked after the synchronisation and rebuilt if they differ
+        pred = pl.get("last_nnz_ag")
+        early = pred is not None and bool(_CSC_FAST) and not _CSC_CHECK  # direct construction probed and on
+        built = self._program(hb, pred, P, c, precondition, omega if precondition else None) if early else None
         stream.synchronize()  # the one synchronization
         hh = hb.h
         nnz_A, nnz_G = int(hh["A_indptr"][-1]), int(hh["G_indptr"][-1])
         nnz = pl["last_nnz"] = nnz_A + nnz_G
+        pl["last_nnz_ag"] = (nnz_A, nnz_G)
         self.d2h_copied += self.d2h_bytes(precondition, idx_now)  # what the graph moved
         if hh["changed_at"][0] == zp[dim + 2]:  # the pattern moved in this call
             pl["pat_gen"] += 1
@@ -1256,24 +1264,46 @@ class GpuSCPStep:
         if bad.any():
             raise FloatingPointError(f"non-finite state in intervals {np.where(bad != 0)[0].tolist()}")
         self._c_last = (zj, c_unscaled)  # the unscaled objective, for unscaled_program(z_j) of the same point
-        mats = {}
-        for M, nrows, o, nnz in (("A", nA, 0, nnz_A), ("G", pl["nG"], nnz_A, nnz_G)):  # over the pinned buffer
-            mats[M] = _csc_direct(hb.wrap("vals", o, nnz), hb.wrap("indices", o, nnz),
-                                  hb.wrap(f"{M}_indptr", 0, pat.n + 1), (nrows, pat.n))
-        prog = ConicProgram(P=P, c=c, A=mats["A"], b=hb.wrap("rhs", 0, nA), G=mats["G"], h=hb.wrap("rhs", nA, pl["nG"]),
-                            cones=ConeSpec(nonneg=pat.n_orthant, soc=pat.soc_dims))
+        if (built is None or pred != (nnz_A, nnz_G) or hh["A_indptr"][0] != 0 or hh["G_indptr"][0] != 0
+                or _CSC_CHECK):
+            built = self._program(hb, (nnz_A, nnz_G), P, c, precondition, omega if precondition else None,
+                                  check=True)
+        mats, prog, prec = built
         import weakref
 
         hb.live.append(weakref.ref(lin))  # the slot's device outputs stay untouched while lin lives
         self._last_lin = weakref.ref(lin)
         if precondition:
-            prec = _preconditioner_type()(row_scale_A=hb.wrap("row_scale_A", 0, nA),
-                                          row_scale_G=hb.wrap("row_scale_G", 0, pl["nG"]),
-                                          var_scale=np.ones(pat.n), cost_scale=omega)
             self._pc_parts = (mats, nA, pl["nG"], hb)
             return lin, prog, prec, pl["meta"]
         self._pc_parts = None
         return lin, prog, pl["meta"]
+
+    def _program(self, hb, nnz_ag, P, c, precondition, omega, check=False):
+        """(mats, ConicProgram, Preconditioner or None) over hb's pinned arrays for the
+        given nonzero counts of A and G (no copy).  check=False skips the O(1) CSC
+        invariants that need the device result (the caller compares the counts)."""
+        pl, pat = self._plan, self.asm.pat
+        nA, nG = pl["nA"], pl["nG"]
+        ConicProgram, ConeSpec = _conic_types()
+        if pl.get("cones") is None or type(pl["cones"]) is not ConeSpec:
+            pl["cones"] = ConeSpec(nonneg=pat.n_orthant, soc=pat.soc_dims)
+        nnz_A, nnz_G = nnz_ag
+        mats = {}
+        for M, nrows, o, nnz in (("A", nA, 0, nnz_A), ("G", nG, nnz_A, nnz_G)):
+            mats[M] = _csc_direct(hb.wrap("vals", o, nnz), hb.wrap("indices", o, nnz),
+                                  hb.wrap(f"{M}_indptr", 0, pat.n + 1), (nrows, pat.n), check=check)
+        prog = ConicProgram(P=P, c=c, A=mats["A"], b=hb.wrap("rhs", 0, nA), G=mats["G"], h=hb.wrap("rhs", nA, nG),
+                            cones=pl["cones"])
+        prec = None
+        if precondition:
+            if pl.get("ones") is None:
+                pl["ones"] = np.ones(pat.n)
+                pl["ones"].flags.writeable = False
+            prec = _preconditioner_type()(row_scale_A=hb.wrap("row_scale_A", 0, nA),
+                                          row_scale_G=hb.wrap("row_scale_G", 0, nG), var_scale=pl["ones"],
+                                          cost_scale=omega)
+        return mats, prog, prec
 
     def reserve(self, n, precondition=False):
         """Make sure n result slots exist with their CUDA graphs captured for this
