@@ -5,7 +5,8 @@ import torch
 sys.path.insert(0, ".")
 from paper_2604_09993_b200 import scenario as S, synth, Discretizer
 
-sc = S.bundled("halfcheetah_bound", N=30)
+import os
+sc = S.bundled(os.environ.get("QT_SCENARIO", "halfcheetah_bound"), N=int(os.environ.get("QT_N", "30")))
 g, n_g = sc.path_constraints()
 disc = Discretizer(sc.model, sc.mixing_matrix(n_g), g, substeps=sc.substeps)
 for B in [int(a) for a in (sys.argv[1:] or ["29", "4096"])]:
