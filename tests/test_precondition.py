@@ -265,10 +265,12 @@ def test_gpu_scp_step_results_survive_later_iterations():
 
 
 @pytest.mark.gpu
-def test_gpu_scp_step_d2h_caps_overflow():
-    """The captured D2H copies cover the CSC arrays only up to caps; a result with
-    more nonzeros than the caps must still come back complete (tail copy) and
-    trigger a recapture."""
+@pytest.mark.parametrize("precondition", [False, True])
+def test_gpu_scp_step_prebuilt_program_rebuilt(precondition):
+    """iterate builds the scipy matrices / program over the pinned buffer before the
+    synchronisation with the previous call's nonzero counts; a call whose counts
+    differ must come back rebuilt and complete (here the prediction is forced
+    wrong), and the bytes moved stay below the packed buffer's size."""
     from paper_2604_09993_b200.subproblem import GpuSCPStep
 
     name = "halfcheetah_n30"
@@ -276,14 +278,16 @@ def test_gpu_scp_step_d2h_caps_overflow():
     sc = golden_scenario(name)
     sg, se = GpuSCPStep(sc, use_graph=True), GpuSCPStep(sc, use_graph=False)
     z = g["ig_z"]
-    sg.iterate(z, 1.0)  # capture
-    for hb in sg._plan["hosts"]:
-        hb.caps = {"A": 100, "G": 10}  # pretend the captured copies were tiny
-    _, pg, _ = sg.iterate(z, 0.5)
-    _, pe, _ = se.iterate(z, 0.5)
+    sg.iterate(z, 1.0, precondition=precondition)  # capture
+    sg._plan["last_nnz_ag"] = (100, 10)  # pretend the previous call had tiny matrices
+    rg = sg.iterate(z, 0.5, precondition=precondition)
+    re_ = se.iterate(z, 0.5, precondition=precondition)
     for M in ("A", "G"):
-        a, b = getattr(pg, M), getattr(pe, M)
-        assert np.array_equal(a.indptr, b.indptr) and np.array_equal(a.indices, b.indices)
+        a, b = getattr(rg[1], M), getattr(re_[1], M)
+        assert a.nnz > 100 and np.array_equal(a.indptr, b.indptr) and np.array_equal(a.indices, b.indices)
         assert np.array_equal(a.data, b.data)
-    assert np.array_equal(pg.b, pe.b)
-    assert sg.d2h_bytes() < sg._plan["pk"].nbytes
+    assert np.array_equal(rg[1].b, re_[1].b) and np.array_equal(rg[1].h, re_[1].h)
+    if precondition:
+        assert np.array_equal(rg[2].row_scale_A, re_[2].row_scale_A)
+    assert sg._plan["last_nnz_ag"] == (rg[1].A.nnz, rg[1].G.nnz)
+    assert sg.d2h_bytes(precondition) < sg._plan["pk"].nbytes

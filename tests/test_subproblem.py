@@ -211,9 +211,9 @@ def test_csc_direct_rejects_inconsistent_arrays():
 @pytest.mark.parametrize("precondition", [False, True])
 def test_gpu_scp_step_graph_replay_pattern_change(name, precondition):
     """A captured iteration replayed at a point whose pattern differs (nonzero
-    impulses) must equal a fresh step at that point bit for bit: the D2H caps of
-    the captured copies are per graph, and a result with more nonzeros takes the
-    tail copy + recapture path."""
+    impulses) must equal a fresh step at that point bit for bit: more nonzeros
+    than the captured call, the pattern stamp, the row indices fetched after the
+    synchronisation, the program objects rebuilt for the new counts."""
     from paper_2604_09993_b200.subproblem import GpuSCPStep
 
     g = load_golden(name)
