@@ -279,6 +279,15 @@ struct Rec2 {
   double wq[3 * M::NL];    // sum_j h a_ij v_{s,j}: dS term of the q-row stage inputs
 };
 
+#ifndef CITO_JAC_ONE_WARP
+// 2 (default): every rate-Jacobian direction (q, v and u: 32 for HalfCheetah) on ONE
+// warp with the generic tangent code (kind 7), one warp fewer per CTA; 1: the same
+// with the u-Jacobian warp kept idle (what was measured as "2" while this default
+// stood after K2Dims: 0.108 vs 0.114 ms for 29 intervals against 0; the real 5-warp
+// CTA: 0.087 vs 0.089 ms, same box); 0: q/v and u directions on two warps
+// (specialised kinds 3 and 4).  Defined before K2Dims, which sizes the CTA from it.
+#define CITO_JAC_ONE_WARP 2
+#endif
 template <class M>
 struct K2Dims {
   using D = Dims<M>;
@@ -317,14 +326,6 @@ struct RegState {
 #define RS_YV rs[7]
 #define RS_HQ(h) rs[(h)]
 #define RS_HV(h) rs[RegState<M>::NH + (h)]
-#ifndef CITO_JAC_ONE_WARP
-// 2 (default): every rate-Jacobian direction (q, v and u: 32 for HalfCheetah) on ONE
-// warp with the generic tangent code (kind 7), one warp fewer per CTA -- one hot code path
-// less per tick (measured 0.108 vs 0.114 ms for 29 intervals, same box); 1: the same
-// with the u-Jacobian warp kept idle; 0: q/v and u directions on two warps
-// (specialised kinds 3 and 4)
-#define CITO_JAC_ONE_WARP 2
-#endif
 #ifndef CITO_COL_SMEM
 #define CITO_COL_SMEM 0  // A/B: 1 = y-row accumulators in shared memory, 2 = + push rows
 #endif
