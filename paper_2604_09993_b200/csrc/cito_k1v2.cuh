@@ -360,6 +360,7 @@ struct Fused2Shared {
   double PV[Pos<M::NPUSH>::v][D::NCOLP];
   double DY[Pos<D::NY>::v][D::NCOLP];
   double x[D::NXT];
+  double xn[D::NXT];  // the next interval's start state (defects), loaded with the inputs
   double vbs[2][D::NQ];
   double U[2 * D::NU + 1];
   double S;
@@ -824,6 +825,9 @@ __global__ void __launch_bounds__(JAC ? K2Dims<M>::NT : 64, MINB) k_linearize2(c
   const double* src_x = zs.z ? zb + (2 * zk + 1) * NXT : xt0s + b * NXT;
   const double* src_U = zs.z ? zb + zs.base_u + zk * (2 * NU + 1) : Us + b * 2 * NU;
   for (int k = tid; k < 2 * NU; k += blockDim.x) sh.U[k] = src_U[k];
+  // z may live in page-locked host memory: every read of it is issued here, at once
+  if (zs.defects)
+    for (int k = tid; k < NXT; k += blockDim.x) sh.xn[k] = zb[(2 * zk + 2) * NXT + k];
   if (tid == 0) {
     sh.S = zs.z ? src_U[2 * NU] : Ss[b];
     sh.bad = 0;
@@ -1031,7 +1035,7 @@ __global__ void __launch_bounds__(JAC ? K2Dims<M>::NT : 64, MINB) k_linearize2(c
   for (int k = tid; k < NXT; k += blockDim.x) {
     const double e = sh.x[k];
     ends[b * NXT + k] = e;
-    if (zs.defects) zs.defects[b * NXT + k] = zb[(2 * zk + 2) * NXT + k] - e;
+    if (zs.defects) zs.defects[b * NXT + k] = sh.xn[k] - e;
     if (!isfinite(e)) sh.bad = 1;
   }
   __syncthreads();

@@ -846,6 +846,7 @@ struct FusedShared {
   double ky[Pos<D::NY>::v];
   double vbs[2][D::NQ];
   double U[2 * D::NU + 1];
+  double xn[D::NXT];  // the next interval's start state (defects), loaded with the inputs
   double S;
   int bad;
 };
@@ -1295,6 +1296,9 @@ __global__ void __launch_bounds__(FusedDims<M>::NT * IPC, MINB) k_linearize(cons
   const double* src_U = zs.z ? zb + zs.base_u + zk * (2 * NU + 1) : Us + b * 2 * NU;
   for (int k = tid; k < NXT; k += NT1) sh.x[k] = src_x[k];
   for (int k = tid; k < 2 * NU; k += NT1) sh.U[k] = src_U[k];
+  // z may live in page-locked host memory: every read of it is issued here, at once
+  if (zs.defects)
+    for (int k = tid; k < NXT; k += NT1) sh.xn[k] = zb[(2 * zk + 2) * NXT + k];
   if (tid == 0) {
     sh.S = zs.z ? src_U[2 * NU] : Ss[b];
     sh.bad = 0;
@@ -1436,7 +1440,7 @@ __global__ void __launch_bounds__(FusedDims<M>::NT * IPC, MINB) k_linearize(cons
   for (int k = active ? tid : NXT; k < NXT; k += NT1) {
     const double e = sh.x[k];
     ends[b * NXT + k] = e;
-    if (zs.defects) zs.defects[b * NXT + k] = zb[(2 * zk + 2) * NXT + k] - e;  // scp.py:115
+    if (zs.defects) zs.defects[b * NXT + k] = sh.xn[k] - e;  // scp.py:115
     if (!isfinite(e)) sh.bad = 1;
   }
   __syncthreads();

@@ -467,6 +467,10 @@ class ConicProgram:
 _CSC_FAST = None  # None: not probed yet; else (maxprint,) when the direct construction is valid
 _CSC_CHECK = os.environ.get("CITO_CHECK_CSC", "0") == "1"
 _CSC_RECIPES = os.environ.get("CITO_CSC_RECIPES", "0") == "1"  # A/B switch: warp-per-column compaction
+# A/B switch CITO_Z_HOST=1: z read straight from the pinned buffer by K1 / K3 / the
+# compaction (no H2D node before K1): -6 us on one box of the pool, +17 us on another
+# (host-memory read latency differs between boxes), so the default copies z first
+_Z_HOST = os.environ.get("CITO_Z_HOST", "0") == "1"
 
 
 def packed_entries(csc, sigma):
@@ -1022,8 +1026,14 @@ class GpuSCPStep:
                           pc_args=pc_args, keep=keep, L=_lib.lib(), nA=nA, nG=nG,
                           soc=(soc_start, soc_dim), P_idx=P_idx, P_ptr=P_ptr, arr=arr,
                           P_plain=None, meta=_Meta(pat.z_idx, pat.sp_idx, pat.sm_idx, pat.t_idx),
-                          stamp=(zde_dev[lay.dim + 2:].data_ptr(), pk.d["changed_at"].data_ptr()), calls=0,
-                          pat_gen=0, want_rows=zde_dev[lay.dim + 3:].data_ptr())
+                          # with _Z_HOST the interval / node kernels and the compaction read z,
+                          # delta, epsilon, stamp and the rows flag straight from the pinned
+                          # buffer (no H2D before K1); k_rhs reads the device copy made on its
+                          # own stream while K1 runs
+                          zsrc=zde_pin if _Z_HOST else zde_dev,
+                          stamp=((zde_pin if _Z_HOST else zde_dev)[lay.dim + 2:].data_ptr(),
+                                 pk.d["changed_at"].data_ptr()), calls=0,
+                          pat_gen=0, want_rows=(zde_pin if _Z_HOST else zde_dev)[lay.dim + 3:].data_ptr())
 
     def _make_slot(self, hb):
         """Device buffers of one in-flight iteration, paired with the pinned host buffer hb:
@@ -1076,8 +1086,8 @@ class GpuSCPStep:
                       r["voff"].data_ptr(), r["seg_src"].data_ptr(), r["seg_off"].data_ptr(),
                       r["seg_len"].data_ptr(), r["seg_cb"].data_ptr(), r["cols"].data_ptr(), pl["z_dev"].data_ptr(),
                       lin_ptrs, pl["rhs_dev"].data_ptr(), delta),
-            lin_args=(gt.disc._h.ptr, N, 1, int(lay.dim), int(gt.base_u), int(gt.base_p), pl["z_dev"].data_ptr(),
-                      pl["zde_dev"][lay.dim:].data_ptr()),
+            lin_args=(gt.disc._h.ptr, N, 1, int(lay.dim), int(gt.base_u), int(gt.base_p), pl["zsrc"].data_ptr(),
+                      pl["zsrc"][lay.dim:].data_ptr()),
             lin_outs=tuple(lin[kk].data_ptr() for kk in ("ends", "jx", "ju", "js", "defects", "bad", "psi",
                                                          "psi_jac", "theta", "theta_jac", "imp_v", "imp_jac")))
         return slot
@@ -1092,12 +1102,17 @@ class GpuSCPStep:
         pl, sl = self._plan, hb.slot
         L = pl["L"]
         s = torch.cuda.current_stream(self.gt.device).cuda_stream
-        pl["zde_dev"].copy_(pl["zde_pin"], non_blocking=True)
+        cur = torch.cuda.current_stream(self.gt.device)
+        side = pl["side"]
+        if _Z_HOST:  # the device copy of z for k_rhs, on the side stream while K1 runs
+            side.wait_stream(cur)
+            with torch.cuda.stream(side):
+                pl["zde_dev"].copy_(pl["zde_pin"], non_blocking=True)
+        else:
+            pl["zde_dev"].copy_(pl["zde_pin"], non_blocking=True)
         h = self.gt.disc._h  # the handle's own library (a run-time compiled topology has its own)
         h.check(h.L.cito_linearize_all_dev2(*sl["lin_args"], *sl["lin_outs"], s), "linearize_all")
         # b/h of the linearized rows on a side stream, concurrently with the CSC compaction
-        cur = torch.cuda.current_stream(self.gt.device)
-        side = pl["side"]
         side.wait_stream(cur)
         pk = pl["pk"]
         with torch.cuda.stream(side):  # every store also into hb's host mirror
