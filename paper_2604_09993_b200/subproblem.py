@@ -1201,7 +1201,8 @@ class GpuSCPStep:
         import torch
 
         z = np.asarray(z, dtype=float)
-        if not np.all(np.isfinite(z)):
+        # z . z finite <=> every entry finite (barring overflow, which the exact test then clears)
+        if not np.isfinite(z @ z) and not np.all(np.isfinite(z)):
             raise FloatingPointError("non-finite reference point")
         if self._plan is None:
             self._build_plan()
