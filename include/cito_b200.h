@@ -254,8 +254,8 @@ cito_status cito_csc_assemble2_dev(int32_t nmat, int32_t ncols, const int64_t* c
  * column pointers (out_ptr[1]) relative to its own first entry.
  * host_vals / host_pattern (0 = off): byte offsets from the device outputs to a
  * page-locked host mirror laid out the same way; the kernel also stores every
- * value (host_vals) and every column pointer, the stamp and, while *rows_wanted
- * (device double) != 0, every row index (host_pattern) there, so the result
+ * value (host_vals), the stamp and, while *rows_wanted (device double) != 0,
+ * every column pointer and row index (host_pattern) there, so the result
  * crosses the bus during the compaction. */
 cito_status cito_csc_assemble_packed_dev(int32_t nmat, int32_t ncols, const void* const* ent, const int64_t* nsup,
                                         const int64_t* const* sp_ptr, const int32_t* const* tcol, const int32_t* ntile,

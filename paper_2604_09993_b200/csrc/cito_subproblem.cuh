@@ -415,8 +415,8 @@ struct CscPackedArgs {
   // previous launch over the same outputs (and skips re-copying the indices)
   const double* stamp_in;
   double* changed_at;
-  // host mirror (0 = off): the values (host_vals) / the pattern (host_pattern: column
-  // pointers, the stamp, and the row indices while *rows_wanted != 0) are also stored
+  // host mirror (0 = off): the values (host_vals) / the pattern (host_pattern: the stamp,
+  // and the column pointers and row indices while *rows_wanted != 0) are also stored
   // at that byte offset from their device address -- into page-locked host memory
   // laid out like the device outputs, so the result crosses the bus while the
   // compaction runs instead of in a copy after it
@@ -581,7 +581,7 @@ __global__ void __launch_bounds__(256) k_csc_flat(int32_t ncols, const CscPacked
     }
     if (stamp) moved |= a.out_ptr[m][c] != tb + cnt;
     a.out_ptr[m][c] = tb + cnt;
-    if (hp) mirror_store(a.out_ptr[m] + c, hp, tb + cnt);
+    if (hr) mirror_store(a.out_ptr[m] + c, hr, tb + cnt);  // the pattern: only into a buffer that wants it
   }
   if (stamp && __syncthreads_or(moved) && tid == 0) {
     *a.changed_at = *a.stamp_in;

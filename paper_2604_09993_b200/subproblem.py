@@ -1138,12 +1138,20 @@ class GpuSCPStep:
         # that wrote it (flags, rhs rows, column pointers, stamp, values, wanted row
         # indices; row scales and scaled values/rhs from the preconditioning)
 
-    def _copy_rows(self, hb, nnz):
-        """Copy-engine transfer of the CSC row indices [0, nnz) into hb (a call whose
-        pattern moved although hb held the previous one)."""
-        o = self._plan["pk"].layout["indices"][0]
-        hb.host[o: o + 4 * nnz].copy_(self._plan["pk"].dev[o: o + 4 * nnz], non_blocking=True)
-        self.d2h_copied += 4 * nnz
+    def _copy_pattern(self, hb, stream):
+        """Copy-engine transfer of the CSC pattern (column pointers, then the row
+        indices [0, nnz)) into hb: a call whose pattern moved although hb held the
+        previous one, so the compaction did not store it there."""
+        pk = self._plan["pk"]
+        lay = pk.layout
+        o0, o1 = lay["A_indptr"][0], lay["G_indptr"][0] + 4 * lay["G_indptr"][2]
+        hb.host[o0:o1].copy_(pk.dev[o0:o1], non_blocking=True)
+        stream.synchronize()
+        nnz = int(hb.h["A_indptr"][-1]) + int(hb.h["G_indptr"][-1])
+        o = lay["indices"][0]
+        hb.host[o: o + 4 * nnz].copy_(pk.dev[o: o + 4 * nnz], non_blocking=True)
+        stream.synchronize()
+        self.d2h_copied += (o1 - o0) + 4 * nnz
 
     def d2h_bytes(self, precondition=False, indices=False):
         """Bytes one iteration moves device -> host at the last call's nonzero count:
@@ -1154,10 +1162,10 @@ class GpuSCPStep:
         lay = pl["pk"].layout
         nnz = pl.get("last_nnz", lay["vals"][2])
         nrhs, nlin = pl["nA"] + pl["nG"], int(self.asm._rhs["n"])
-        # flags, stamp, column pointers, the linearized b/h rows (the constant ones stay in
-        # the host buffer), values, wanted row indices
-        n = (4 * lay["bad"][2] + 8 + 4 * (lay["A_indptr"][2] + lay["G_indptr"][2]) + 8 * nlin + 8 * nnz
-             + (4 * nnz if indices else 0))
+        # flags, stamp, the linearized b/h rows (the constant ones stay in the host buffer),
+        # values; the pattern (column pointers, row indices) only when wanted
+        n = (4 * lay["bad"][2] + 8 + 8 * nlin + 8 * nnz
+             + (4 * (lay["A_indptr"][2] + lay["G_indptr"][2] + nnz) if indices else 0))
         if precondition:  # the row scales and every b/h row once more (scaled)
             n += 16 * nrhs
         return int(n)
@@ -1265,17 +1273,16 @@ class GpuSCPStep:
         built = self._program(hb, pred, P, c, precondition, omega if precondition else None) if early else None
         stream.synchronize()  # the one synchronization
         hh = hb.h
+        if hh["changed_at"][0] == zp[dim + 2]:  # the pattern moved in this call
+            pl["pat_gen"] += 1
+            if not idx_now:
+                self._copy_pattern(hb, stream)
+                self.pattern_refetches += 1
+        hb.pat_gen = pl["pat_gen"]
         nnz_A, nnz_G = int(hh["A_indptr"][-1]), int(hh["G_indptr"][-1])
         nnz = pl["last_nnz"] = nnz_A + nnz_G
         pl["last_nnz_ag"] = (nnz_A, nnz_G)
         self.d2h_copied += self.d2h_bytes(precondition, idx_now)  # what the graph moved
-        if hh["changed_at"][0] == zp[dim + 2]:  # the pattern moved in this call
-            pl["pat_gen"] += 1
-            if not idx_now:
-                self._copy_rows(hb, nnz)
-                stream.synchronize()
-                self.pattern_refetches += 1
-        hb.pat_gen = pl["pat_gen"]
         bad = hh["bad"]
         if bad.any():
             raise FloatingPointError(f"non-finite state in intervals {np.where(bad != 0)[0].tolist()}")
