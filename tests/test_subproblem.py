@@ -280,6 +280,7 @@ def test_gpu_scp_step_pattern_stamp_sequence(precondition):
         keep = r if i % 4 != 3 else None  # hold the previous result (two buffers in use) most of the time
         del r, prog
     assert len(step._plan["hosts"]) >= 2
+    assert step.pattern_refetches > 0  # a pattern moved under a buffer that held the previous one
     # steady state (same pattern, buffer up to date): values only
     b0 = step.d2h_copied
     r = step.iterate(*pts["3"], precondition=precondition)
