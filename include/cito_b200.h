@@ -256,14 +256,16 @@ cito_status cito_csc_assemble2_dev(int32_t nmat, int32_t ncols, const int64_t* c
  * page-locked host mirror laid out the same way; the kernel also stores every
  * value (host_vals), the stamp and, while *rows_wanted (device double) != 0,
  * every column pointer and row index (host_pattern) there, so the result
- * crosses the bus during the compaction. */
+ * crosses the bus during the compaction.  consts_wanted (device double, NULL =
+ * always): while it is 0 the mirror already holds this pattern's constant
+ * entries and 16-byte chunks of constants only are not stored again. */
 cito_status cito_csc_assemble_packed_dev(int32_t nmat, int32_t ncols, const void* const* ent, const int64_t* nsup,
                                         const int64_t* const* sp_ptr, const int32_t* const* tcol, const int32_t* ntile,
                                         const double* const* lin, uint32_t* ws, int64_t ws_words,
                                         int32_t* const* out_ptr, int32_t* const* out_rows, double* const* out_vals,
                                         unsigned long long* const* rowmax, const double* stamp_in,
                                         double* changed_at, int64_t host_vals, int64_t host_pattern,
-                                        const double* rows_wanted, void* stream);
+                                        const double* rows_wanted, const double* consts_wanted, void* stream);
 
 /* b / h of the linearized rows: out[rows[i]] = form ? J.z[cols] - v : v - J.z[cols]
  * with J split in up to 3 segments (seg_src < 0 = unused), v = lin[vsrc[i]][voff[i]];

@@ -88,7 +88,7 @@ def _configure(L):
                                         [ctypes.c_int32, ctypes.c_int32] + [_dp] * 6 + [ctypes.c_int64, _dp])
     L.cito_csc_assemble_packed_dev.restype = ctypes.c_int
     L.cito_csc_assemble_packed_dev.argtypes = ([ctypes.c_int32, ctypes.c_int32] + [_dp] * 7 + [ctypes.c_int64] +
-                                               [_dp] * 6 + [ctypes.c_int64, ctypes.c_int64, _dp, _dp])
+                                               [_dp] * 6 + [ctypes.c_int64, ctypes.c_int64, _dp, _dp, _dp])
     L.cito_copy_mirror.restype = ctypes.c_int
     L.cito_copy_mirror.argtypes = [_dp, _dp, ctypes.c_int64, ctypes.c_int64, _dp]
     L.cito_rhs_dev.restype = ctypes.c_int

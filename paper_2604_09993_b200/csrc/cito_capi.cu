@@ -689,7 +689,7 @@ cito_status cito_csc_assemble_packed_dev(int32_t nmat, int32_t ncols, const void
                                         int32_t* const* out_ptr, int32_t* const* out_rows, double* const* out_vals,
                                         unsigned long long* const* rowmax, const double* stamp_in,
                                         double* changed_at, int64_t host_vals, int64_t host_pattern,
-                                        const double* rows_wanted, void* stream) {
+                                        const double* rows_wanted, const double* consts_wanted, void* stream) {
   if (nmat < 1 || nmat > 2 || ncols < 0 || !ent || !nsup || !sp_ptr || !tcol || !ntile || !ws ||
       (stamp_in == nullptr) != (changed_at == nullptr))
     return fail(CITO_ERR_ARG, "csc_assemble_packed: bad arguments");
@@ -701,6 +701,7 @@ cito_status cito_csc_assemble_packed_dev(int32_t nmat, int32_t ncols, const void
   a.host_vals = host_vals;
   a.host_pattern = host_pattern;
   a.rows_wanted = rows_wanted;
+  a.consts_wanted = consts_wanted;
   int64_t tiles = 0;
   for (int m = 0; m < 2; ++m) {
     const bool on = m < nmat;

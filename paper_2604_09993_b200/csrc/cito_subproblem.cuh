@@ -422,6 +422,10 @@ struct CscPackedArgs {
   // compaction runs instead of in a copy after it
   int64_t host_vals, host_pattern;
   const double* rows_wanted;
+  // optional (null = always): while *consts_wanted == 0 the host mirror already holds
+  // this pattern's constant entries (src < 0: value w, the same every call), so 16-byte
+  // chunks of constants only are not stored again
+  const double* consts_wanted;
 };
 
 template <class T>
@@ -442,6 +446,7 @@ __global__ void __launch_bounds__(256) k_csc_flat(int32_t ncols, const CscPacked
   // chunks of its contiguous output range (full bus lines instead of scattered words)
   __shared__ __align__(16) double stage_v[CSC_TILE];
   __shared__ __align__(16) int32_t stage_r[CSC_TILE];
+  __shared__ uint8_t stage_c[CSC_TILE];
   if (tid == 0) tile_s = (int)atomicAdd(&ws[0], 1u);
   __syncthreads();
   const int tile = tile_s;
@@ -560,7 +565,10 @@ __global__ void __launch_bounds__(256) k_csc_flat(int32_t ncols, const CscPacked
       if (stamp) moved |= orow[pos] != row[j];
       orow[pos] = row[j];
       oval[pos] = v[j];
-      if (hv) stage_v[pos - tb] = v[j];
+      if (hv) {
+        stage_v[pos - tb] = v[j];
+        stage_c[pos - tb] = (key[j] >> 27) == 0u;  // a constant entry
+      }
       if (hr) stage_r[pos - tb] = row[j];
       // fused row inf-norm (cito/conic.py:281-287): non-negative doubles order like their bits
       if (rmax) atomicMax(&rmax[row[j]], (unsigned long long)__double_as_longlong(fabs(v[j])));
@@ -595,9 +603,13 @@ __global__ void __launch_bounds__(256) k_csc_flat(int32_t ncols, const CscPacked
       const int head = (reinterpret_cast<uintptr_t>(hd) & 15) ? 1 : 0;
       const int np = (n - head) >> 1;
       double2* d2 = reinterpret_cast<double2*>(hd + head);
-      for (int k = tid; k < np; k += blockDim.x) d2[k] = make_double2(stage_v[head + 2 * k], stage_v[head + 2 * k + 1]);
-      if (tid == 0 && head && n > 0) hd[0] = stage_v[0];
-      if (tid == 1 && n > head && ((n - head) & 1)) hd[n - 1] = stage_v[n - 1];
+      const bool cw = a.consts_wanted == nullptr || *a.consts_wanted != 0.0;
+      for (int k = tid; k < np; k += blockDim.x) {
+        const int e = head + 2 * k;
+        if (cw || !(stage_c[e] && stage_c[e + 1])) d2[k] = make_double2(stage_v[e], stage_v[e + 1]);
+      }
+      if (tid == 0 && head && n > 0 && (cw || !stage_c[0])) hd[0] = stage_v[0];
+      if (tid == 1 && n > head && ((n - head) & 1) && (cw || !stage_c[n - 1])) hd[n - 1] = stage_v[n - 1];
     }
     if (hr) {
       int32_t* hd = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(orow + tb) + hr);

@@ -471,6 +471,7 @@ _CSC_RECIPES = os.environ.get("CITO_CSC_RECIPES", "0") == "1"  # A/B switch: war
 # compaction (no H2D node before K1): -6 us on one box of the pool, +17 us on another
 # (host-memory read latency differs between boxes), so the default copies z first
 _Z_HOST = os.environ.get("CITO_Z_HOST", "0") == "1"
+_SKIP_CONSTS = os.environ.get("CITO_SKIP_CONSTS", "1") == "1"  # A/B: constant CSC entries not re-sent
 
 
 def packed_entries(csc, sigma):
@@ -595,7 +596,7 @@ class SubproblemAssembler:
         stream); `outs` = [(indptr, indices, data)] per matrix, `arr` builds a
         ctypes pointer table from tensors, `stamp` = optional (stamp_in, changed_at)
         device pointers of the pattern-change stamp, `mirror` = optional
-        (host_vals, host_rows, rows_wanted) of the host mirror."""
+        (host_vals, host_rows, rows_wanted, consts_wanted) of the host mirror."""
         import ctypes
 
         import torch
@@ -610,7 +611,7 @@ class SubproblemAssembler:
                 arr([d["sp_ptr"] for d in mats]), arr([d["tcol"] for d in mats]),
                 ctypes.cast(self._ntile, ctypes.c_void_p), lin_ptrs, self._ws.data_ptr(), self._ws.numel(),
                 arr([o[0] for o in outs]), arr([o[1] for o in outs]), arr([o[2] for o in outs]),
-                arr(rowmax) if rowmax else None, *(stamp or (None, None)), *(mirror or (0, 0, None)))
+                arr(rowmax) if rowmax else None, *(stamp or (None, None)), *(mirror or (0, 0, None, None)))
 
     def _prepare_batched(self):
         """Concatenate the rhs descriptors of A and G (one launch) and allocate
@@ -932,6 +933,7 @@ class _HostBuf:
         self.live = []
         self.pat_gen = -1  # pattern generation of the CSC indices last copied into this buffer
         self.rhs_scaled = False  # b/h here were row-scaled by a preconditioned call (constant rows too)
+        self.consts_ok = False  # the constant CSC entries here are current (unscaled, hb's pattern)
 
     def wrap(self, name, start, n):
         """Array of n elements of field `name` from element `start`, owned by a _Span."""
@@ -1004,8 +1006,8 @@ class GpuSCPStep:
         # homotopy; the stamp (call counter) is what the CSC compaction writes into
         # changed_at when the sparsity pattern moves; rows wanted != 0 makes it mirror the
         # row indices too (a host buffer that does not hold the current pattern)
-        zde_dev = torch.empty(lay.dim + 4, **f64)
-        zde_pin = torch.zeros(lay.dim + 4, dtype=torch.float64, pin_memory=True)
+        zde_dev = torch.empty(lay.dim + 5, **f64)
+        zde_pin = torch.zeros(lay.dim + 5, dtype=torch.float64, pin_memory=True)
         z_dev = zde_dev[: lay.dim]
         rowmax = torch.zeros(max(1, nA + nG), dtype=i64, device=dev)  # zero between calls (k_row_scale resets it)
         arr = lambda xs: ctypes_ptr_array([x.data_ptr() if x is not None else None for x in xs])  # noqa: E731
@@ -1033,7 +1035,8 @@ class GpuSCPStep:
                           zsrc=zde_pin if _Z_HOST else zde_dev,
                           stamp=((zde_pin if _Z_HOST else zde_dev)[lay.dim + 2:].data_ptr(),
                                  pk.d["changed_at"].data_ptr()), calls=0,
-                          pat_gen=0, want_rows=(zde_pin if _Z_HOST else zde_dev)[lay.dim + 3:].data_ptr())
+                          pat_gen=0, want_rows=(zde_pin if _Z_HOST else zde_dev)[lay.dim + 3:].data_ptr(),
+                          want_consts=(zde_pin if _Z_HOST else zde_dev)[lay.dim + 4:].data_ptr())
 
     def _make_slot(self, hb):
         """Device buffers of one in-flight iteration, paired with the pinned host buffer hb:
@@ -1079,9 +1082,9 @@ class GpuSCPStep:
             # plain: the compaction mirrors the values (final) and, when wanted, the rows;
             # preconditioned: only the rows (the row scaling mirrors the scaled values)
             packed=tuple(k(a) for a in asm.packed_args(lin_ptrs, outs, None, arr, pl["stamp"],
-                                                       (delta, delta, pl["want_rows"]))),
+                                                       (delta, delta, pl["want_rows"], pl["want_consts"]))),
             packed_pc=tuple(k(a) for a in asm.packed_args(lin_ptrs, outs, [rowmax[:nA], rowmax[nA:]], arr,
-                                                          pl["stamp"], (0, delta, pl["want_rows"]))),
+                                                          pl["stamp"], (0, delta, pl["want_rows"], None))),
             rhs_args=(r["n"], r["rows"].data_ptr(), r["form"].data_ptr(), r["vsrc"].data_ptr(),
                       r["voff"].data_ptr(), r["seg_src"].data_ptr(), r["seg_off"].data_ptr(),
                       r["seg_len"].data_ptr(), r["seg_cb"].data_ptr(), r["cols"].data_ptr(), pl["z_dev"].data_ptr(),
@@ -1150,14 +1153,18 @@ class GpuSCPStep:
         nnz = int(hb.h["A_indptr"][-1]) + int(hb.h["G_indptr"][-1])
         o = lay["indices"][0]
         hb.host[o: o + 4 * nnz].copy_(pk.dev[o: o + 4 * nnz], non_blocking=True)
+        ov = lay["vals"][0]  # the values too: the compaction skipped the constants at the old positions
+        hb.host[ov: ov + 8 * nnz].copy_(pk.dev[ov: ov + 8 * nnz], non_blocking=True)
         stream.synchronize()
-        self.d2h_copied += (o1 - o0) + 4 * nnz
+        self.d2h_copied += (o1 - o0) + 12 * nnz
 
     def d2h_bytes(self, precondition=False, indices=False):
         """Bytes one iteration moves device -> host at the last call's nonzero count:
-        the fixed fields + the values (+ the row indices with ``indices``, as in a
-        call whose buffer does not hold the current pattern).  ``self.d2h_copied``
-        counts the bytes every call actually moved."""
+        the fixed fields + the values (+ the pattern with ``indices``, as in a call
+        whose buffer does not hold the current pattern).  An upper bound when the
+        buffer already holds the constant entries (16-byte chunks of constants are
+        then not sent, ~15 % of the values).  ``self.d2h_copied`` accumulates it per
+        call (+ the copies of a pattern fetched after the synchronisation)."""
         pl = self._plan
         lay = pl["pk"].layout
         nnz = pl.get("last_nnz", lay["vals"][2])
@@ -1193,6 +1200,7 @@ class GpuSCPStep:
         self._launch(precondition, hb)
         torch.cuda.current_stream(self.gt.device).synchronize()
         hb.rhs_scaled |= bool(precondition)
+        hb.consts_ok &= not precondition
         g = torch.cuda.CUDAGraph()
         n0 = _lib.launch_count()
         with torch.cuda.graph(g):
@@ -1232,6 +1240,7 @@ class GpuSCPStep:
         # pattern moves, and then they are fetched after the synchronization)
         idx_now = hb.pat_gen != pl["pat_gen"]
         zp[dim + 3] = 1.0 if idx_now else 0.0
+        zp[dim + 4] = 0.0 if (_SKIP_CONSTS and hb.consts_ok and not idx_now) else 1.0  # constants already there
         if hb.rhs_scaled and not precondition:  # the constant b/h rows, scaled there by a preconditioned call
             hb.h["rhs"][:] = pl["rhs_const_host"]
             hb.rhs_scaled = False
@@ -1244,6 +1253,7 @@ class GpuSCPStep:
         else:
             self._launch(bool(precondition), hb)
         hb.rhs_scaled |= bool(precondition)
+        hb.consts_ok = not precondition  # (a moved pattern brings every value back below)
         nA = pl["nA"]
         # host work that does not depend on the device results runs while the GPU works:
         # the objective, the (scaled) P, the lazy LinearizedProblem
