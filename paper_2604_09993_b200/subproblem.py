@@ -1097,9 +1097,10 @@ class GpuSCPStep:
 
     def _launch(self, precondition, hb):
         """The device work of one iteration on the current stream: H2D of
-        [z, delta, epsilon], K1 + K3, CSC assembly, rhs, optional row scaling (the
-        unscaled values kept in the slot), D2H of the packed result into the
-        pinned host buffer `hb` (outputs in hb's device slot)."""
+        [z, delta, epsilon, stamp, flags], K1 + K3, CSC assembly, rhs, optional row
+        scaling (the unscaled values kept in the slot); the kernels that finalise
+        each result field also store it into the pinned host buffer `hb` (outputs
+        in hb's device slot)."""
         import torch
 
         pl, sl = self._plan, hb.slot
