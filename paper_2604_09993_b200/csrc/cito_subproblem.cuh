@@ -558,11 +558,19 @@ __global__ void __launch_bounds__(256) k_csc_flat(int32_t ncols, const CscPacked
   const bool stamp = a.changed_at != nullptr;
   const int64_t hv = a.host_vals, hp = a.host_pattern, hr = (hp && *a.rows_wanted != 0.0) ? hp : 0;
   bool moved = false;
+  // the previous launch's row indices at this tile's positions, all loads in flight
+  // before the first store (one memory round trip for the stamp, not one per entry)
+  int32_t old_row[CSC_TJ];
+  if (stamp) {
+#pragma unroll
+    for (int j = 0; j < CSC_TJ; ++j)
+      old_row[j] = v[j] != 0.0 ? orow[tb + base[j][warp] + __popc(masks[j][warp] & ltm)] : 0;
+  }
 #pragma unroll
   for (int j = 0; j < CSC_TJ; ++j) {
     if (v[j] != 0.0) {
       const int pos = tb + base[j][warp] + __popc(masks[j][warp] & ltm);
-      if (stamp) moved |= orow[pos] != row[j];
+      if (stamp) moved |= old_row[j] != row[j];
       orow[pos] = row[j];
       oval[pos] = v[j];
       if (hv) {
