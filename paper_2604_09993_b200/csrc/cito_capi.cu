@@ -114,10 +114,25 @@ cito_status launch_linearize(const KParams& P, int64_t B, const double* xt0s, co
   static const int64_t lat_max = getenv("CITO_K1_LAT_MAX") ? atoll(getenv("CITO_K1_LAT_MAX")) : -1;
   const int64_t lmax = lat_max >= 0 ? lat_max : (2 * (int64_t)sms) / 3;
   if (ok_v2 && (ver == 2 || (ver == 0 && B <= lmax) || !ok_b1)) {
-    if (B <= sms || !ok_v22)
-      k_linearize2<M, 1><<<(unsigned)B, K2Dims<M>::NT, smem2, st>>>(P, B, xt0s, Us, Ss, ends, jx, ju, js, bad, zs);
-    else
+    if (B <= sms || !ok_v22) {
+      // programmatic dependent launch (CITO_PDL=0 turns it off): behind a kernel that
+      // produces the inputs (the SCP graph's z upload) the CTAs start and load the model
+      // constants early; they wait for the producer before reading any input
+      static const bool pdl = !(getenv("CITO_PDL") && getenv("CITO_PDL")[0] == '0');
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)B);
+      cfg.blockDim = dim3(K2Dims<M>::NT);
+      cfg.dynamicSmemBytes = smem2;
+      cfg.stream = st;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = pdl ? 1 : 0;
+      CUDA_TRY(cudaLaunchKernelEx(&cfg, k_linearize2<M, 1>, P, B, xt0s, Us, Ss, ends, jx, ju, js, bad, zs));
+    } else {
       k_linearize2<M, 2><<<(unsigned)B, K2Dims<M>::NT, smem2, st>>>(P, B, xt0s, Us, Ss, ends, jx, ju, js, bad, zs);
+    }
   } else if (ver == 1 && B <= sms) {
     k_linearize<M, 1><<<(unsigned)B, FusedDims<M>::NT, smem1, st>>>(P, B, xt0s, Us, Ss, ends, jx, ju, js, bad, zs);
   } else {
@@ -833,6 +848,9 @@ cito_status cito_precondition_dev(int32_t ncols, const int32_t* A_ptr, const int
 __global__ void __launch_bounds__(256) k_copy_out(uint4* __restrict__ dst, const uint4* __restrict__ src, int64_t n16,
                                                   unsigned char* __restrict__ dtail,
                                                   const unsigned char* __restrict__ stail, int ntail, int64_t mirror) {
+  // a dependent kernel (PDL) may start its independent prologue right away; it waits for
+  // this grid's completion before reading what it copies
+  asm volatile("griddepcontrol.launch_dependents;");
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += stride) {
     const uint4 v = src[i];
