@@ -27,7 +27,7 @@ Line fields:
          launching stream per step, L2 flushed (256 MiB write) between steps,
          max over ranks.
   e2e    the same metric through the public API with host buffers:
-         scp/fine: GpuSCPStep.iterate -- pinned H2D of [z, delta, epsilon], the
+         scp/fine: GpuSCPStep.iterate -- upload of [z, delta, epsilon, ...] from pinned memory, the
            device step whose last kernels write the assembled program into a
            pinned host buffer (CSC values and column pointers, b, h, flags; the
            CSC row indices only when that buffer does not hold the current
@@ -464,7 +464,7 @@ def run_ours(args):
             return scp_api.iterate(z, 1.0)
 
         e2e_step()
-        h2d = z.nbytes + 16  # z plus [delta, epsilon] (one pinned H2D per step)
+        h2d = z.nbytes + 40  # z plus [delta, epsilon, stamp, two flags], uploaded from pinned memory per step
         d2h = None  # counted over the timed steps (GpuSCPStep.d2h_copied): fixed fields + CSC values, + the
         # CSC row indices in a step whose result buffer does not hold the current pattern
         e2e_note = "GpuSCPStep.iterate: host z in, host scipy program out; LinearizedProblem device-backed (lazy)"

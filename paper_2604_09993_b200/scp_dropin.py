@@ -9,7 +9,7 @@ cito.scp.solve (/root/reference/pkg/src/cito/scp.py:383-467) calls, per attempt,
 ``install_scp()`` replaces those three module globals of ``cito.scp``:
 
   linearize_all     runs the whole iteration on the GPU -- GpuSCPStep.iterate with
-                    preconditioning: one pinned H2D of [z, delta, epsilon], one CUDA
+                    preconditioning: one upload of [z, delta, epsilon, ...] from pinned memory, one CUDA
                     graph replay (K1 + K3, CSC assembly, rhs, row scaling; the result
                     written into a pinned host buffer) -- and returns the device-backed
                     LinearizedProblem

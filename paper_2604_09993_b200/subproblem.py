@@ -954,7 +954,7 @@ class GpuSCPStep:
     """One SCP iteration's pre-IPM work in a single device pass (public API).
 
     ``iterate(z, delta, z_j=None)`` = cito.scp.linearize_all + build_subproblem
-    (scp.py:412-413) with host numpy in / host scipy out: one pinned H2D of z,
+    (scp.py:412-413) with host numpy in / host scipy out: one upload of z from pinned memory,
     the interval + node kernels, the whole-subproblem assembly (+ preconditioning,
     scp.py:414) whose last kernel stores the CSC values straight into a pinned
     host buffer (the fixed fields follow in one copy kernel), and a single
