@@ -1349,20 +1349,29 @@ class GpuSCPStep:
         """Make sure n result slots exist with their CUDA graphs captured for this
         mode, so a loop that keeps the previous result alive while computing the
         next (cito.scp.solve holds lin/prog of iteration k during k+1) never
-        captures in the middle of the loop.  Uses the last [z, delta, epsilon]."""
+        captures in the middle of the loop.  Uses the last [z, delta, epsilon].  A
+        buffer that a live result still points into is never written (its capture
+        runs the iteration once): new buffers are made instead."""
         import torch
 
         if self._plan is None or not self.use_graph:
             return
         pl = self._plan
-        while len(pl["hosts"]) < n:
+        pc = bool(precondition)
+        ready = sum(1 for hb in pl["hosts"] if pc in hb.graphs)
+        for hb in list(pl["hosts"]):
+            if ready >= n:
+                break
+            if pc not in hb.graphs and hb.free():
+                self._capture(pc, hb)
+                ready += 1
+        while ready < n:
             hb = _HostBuf(pl["pk"])
             hb.slot = self._make_slot(hb)
             hb.h["rhs"][:] = pl["rhs_const_host"]
             pl["hosts"].append(hb)
-        for hb in pl["hosts"][:n]:
-            if bool(precondition) not in hb.graphs:
-                self._capture(bool(precondition), hb)
+            self._capture(pc, hb)
+            ready += 1
         torch.cuda.current_stream(self.gt.device).synchronize()
 
     def unscaled_program(self, z_j):

@@ -314,6 +314,24 @@ def test_gpu_scp_step_mixed_modes_same_buffer():
 
 
 @pytest.mark.gpu
+def test_gpu_scp_step_reserve_keeps_live_results():
+    """reserve() captures graphs by running an iteration into result buffers: it must
+    not write into a buffer a live result points into."""
+    from paper_2604_09993_b200.subproblem import GpuSCPStep
+
+    name = "halfcheetah_n30"
+    g = load_golden(name)
+    sc = golden_scenario(name)
+    step = GpuSCPStep(sc)
+    live = step.iterate(g["ig_z"], 1.0)[1]  # plain result, held
+    saved = [live.A.data.copy(), live.b.copy(), live.G.data.copy()]
+    step.reserve(2, precondition=True)  # preconditioned graphs: would scale a live buffer
+    assert np.array_equal(live.A.data, saved[0]) and np.array_equal(live.b, saved[1])
+    assert np.array_equal(live.G.data, saved[2])
+    assert sum(1 for hb in step._plan["hosts"] if True in hb.graphs) >= 2
+
+
+@pytest.mark.gpu
 def test_gpu_scp_step_results_outlive_the_step():
     """The program's arrays live in the step's pinned result buffer; they keep that
     allocation alive after the GpuSCPStep itself is dropped."""
